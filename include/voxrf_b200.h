@@ -1,0 +1,275 @@
+/* voxrf_b200 — C-ABI of the B200-native per-ray hot path.
+ *
+ * This is the drop-in boundary for the reference library's batch entry points
+ * (/root/reference/proj/include/voxrf/*.hpp). Every function below names the
+ * reference interface it replaces. The reference API is exception-based and
+ * Eigen-typed; this boundary is plain C: POD structs, raw pointers, sizes and
+ * an int status. The C++ binding that re-exposes the reference signatures on
+ * top of it (integration/voxrf_gpu_backend.cpp) maps the status back to the
+ * same exception types and messages.
+ *
+ * Status codes map to the reference's exception classes:
+ *   VRF_ERR_INVALID_ARGUMENT -> std::invalid_argument
+ *   VRF_ERR_OUT_OF_RANGE     -> std::out_of_range
+ *   VRF_ERR_RUNTIME          -> std::runtime_error (same message text)
+ *   VRF_ERR_CUDA             -> std::runtime_error ("cuda: ...")
+ * vrf_last_error(ctx) returns the message of the last failing call.
+ *
+ * Device state lives in a vrf_context (one per GPU): the fp32 vertex payload
+ * [V][28] (sigma_raw, r0..r8, g0..g8, b0..b8 — the .vxgf payload order,
+ * voxel_grid.cpp:230-233), a 1-bit-per-cell occupancy mask, the fp32
+ * gradient accumulator and RMSProp state, and the keyframe set. All calls are
+ * synchronous at return unless stated otherwise; no call ever falls back to a
+ * CPU implementation — without a usable CUDA device vrf_context_create fails.
+ */
+#ifndef VOXRF_B200_H
+#define VOXRF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VRF_ABI_VERSION 1
+
+enum {
+  VRF_OK = 0,
+  VRF_ERR_INVALID_ARGUMENT = 1,
+  VRF_ERR_OUT_OF_RANGE = 2,
+  VRF_ERR_RUNTIME = 3,
+  VRF_ERR_CUDA = 4
+};
+
+typedef struct vrf_context vrf_context;
+
+/* GridGeometry — voxel_grid.hpp:20-63 (res counts vertices per axis). */
+typedef struct {
+  int32_t res[3];
+  double origin[3];
+  double voxel_size;
+} vrf_grid_geometry;
+
+/* CameraIntrinsics — camera.hpp:11-24. */
+typedef struct {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double depth_scale;
+} vrf_intrinsics;
+
+/* Pose — pose.hpp:11-24; q = (w, x, y, z), x_world = q * x_cam + t. */
+typedef struct {
+  double q[4];
+  double t[3];
+} vrf_pose;
+
+/* RenderParams — renderer.hpp:12-24 (<= 0 selects the reference defaults). */
+typedef struct {
+  double step, t_near, t_far, termination_eps;
+} vrf_render_params;
+
+/* The MappingConfig fields mapping_step reads — mapping.hpp:19-41. */
+typedef struct {
+  double lambda_d, lr_sigma, lr_sh, rmsprop_decay, rmsprop_eps;
+  int32_t deterministic; /* 1: sorted/segmented fp64 gradient reduce (bit-reproducible) */
+  int32_t reserved;
+  vrf_render_params render;
+} vrf_mapping_config;
+
+/* MapStepStats — mapping.hpp:68-75, plus the composited-sample count. */
+typedef struct {
+  double loss_photometric, loss_geometric, loss_total;
+  int32_t rays_color, rays_depth;
+  double psnr_estimate;
+  int64_t samples;     /* sum over hit rays of RayWorkspace::count */
+  int32_t bad_ray;     /* -1, or the first batch index with a non-finite loss */
+  int32_t reserved;
+} vrf_map_step_stats;
+
+/* Loss weights + render params of TrackingConfig — tracking.hpp:29-51. */
+typedef struct {
+  double lambda_p, lambda_d;
+  vrf_render_params render;
+} vrf_tracking_loss;
+
+/* PoseGradient — tracking.hpp:60-65. */
+typedef struct {
+  double d_omega[3], d_tau[3];
+  double loss;
+  int32_t rays_used;
+  int32_t reserved;
+  int64_t samples;
+} vrf_pose_gradient_result;
+
+/* Gauss-Newton normal equations over residuals r = [sqrt(lp) (C-C*); sqrt(ld) (D-D*)]
+ * per hit ray, parameters [omega; tau] (the PosePerturbation chart,
+ * tracking.hpp:15-26). jtj: upper triangle, row-major (21). loss is the
+ * un-normalised sum; pose_gradient == (2/m) * jtr. */
+typedef struct {
+  double jtj[21];
+  double jtr[6];
+  double loss;
+  int32_t rays_used;
+  int32_t reserved;
+  int64_t samples;
+} vrf_normal_equations;
+
+/* TrackingConfig — tracking.hpp:29-51 (init policy handled by the caller). */
+typedef struct {
+  int32_t rays_per_iteration, iterations;
+  double lr_omega, lr_tau, beta1, beta2, adam_eps, lambda_p, lambda_d;
+  double convergence_step, divergence_factor;
+  int32_t divergence_patience, max_redraws;
+  uint64_t seed;
+  vrf_render_params render;
+} vrf_tracking_config;
+
+/* TrackFrameResult — tracking.hpp:75-80 (loss_trace returned separately). */
+typedef struct {
+  vrf_pose pose;
+  int32_t failed, iterations_run;
+  double final_loss;
+} vrf_track_frame_result;
+
+/* Gauss-Newton / Levenberg-Marquardt tracker (new; the reference only has Adam). */
+typedef struct {
+  int32_t rays_per_iteration, iterations;
+  double lambda_p, lambda_d;
+  double damping;        /* LM: (JtJ + damping*diag(JtJ) + 1e-12 I) delta = -Jtr */
+  int32_t max_redraws;
+  int32_t reserved;
+  uint64_t seed;         /* device Philox stream for the valid-depth pixel draws */
+  vrf_render_params render;
+} vrf_gn_config;
+
+/* Device buffers owned by a context (for NCCL collectives issued by the caller). */
+typedef struct {
+  float* payload;        /* [num_vertices][28] */
+  float* grad;           /* [padded_vertices][28] */
+  float* rms_v;          /* [padded_vertices][28] */
+  int64_t num_vertices;
+  int64_t padded_vertices;
+  void* stream;          /* cudaStream_t every call of this context runs on */
+} vrf_device_buffers;
+
+/* Per-rank partial results of the mapping forward pass. */
+typedef struct {
+  int32_t rays_color, rays_depth;
+  double sum_photometric, sum_geometric;
+  int64_t samples;
+  int32_t bad_ray;
+  int32_t reserved;
+} vrf_map_partials;
+
+/* ---- context */
+int vrf_context_create(int device, vrf_context** out);
+void vrf_context_destroy(vrf_context* ctx);
+const char* vrf_last_error(const vrf_context* ctx);
+int vrf_abi_version(void);
+/* Pads the gradient/RMSProp buffers to a multiple of world_size vertices so
+ * NCCL reduce-scatter shards are equal; call before vrf_grid_*. */
+int vrf_set_shard_multiple(vrf_context* ctx, int world_size);
+/* Run on an external stream (e.g. torch.cuda.current_stream()); NULL = own stream. */
+int vrf_set_stream(vrf_context* ctx, void* stream);
+int vrf_get_device_buffers(vrf_context* ctx, vrf_device_buffers* out);
+/* Number of kernels this context launched since creation (bench evidence). */
+int64_t vrf_kernel_launch_count(const vrf_context* ctx);
+
+/* ---- grid: VoxelGrid (voxel_grid.hpp:112-175) */
+/* VoxelGrid(geom, sigma_init) — voxel_grid.cpp:74-81 (all cells active). */
+int vrf_grid_init(vrf_context* ctx, const vrf_grid_geometry* geom, double sigma_init);
+/* Upload VoxelGrid::data() (double [V][28]) and occupancy() (uint8 per cell). */
+int vrf_grid_upload(vrf_context* ctx, const vrf_grid_geometry* geom, const double* payload,
+                    const uint8_t* occupancy);
+/* Upload a .vxgf-style fp32 payload and LSB-first occupancy bitmask
+ * (voxel_grid.cpp:222-239). */
+int vrf_grid_upload_f32(vrf_context* ctx, const vrf_grid_geometry* geom, const float* payload,
+                        const uint8_t* occupancy_bits);
+int vrf_grid_download(vrf_context* ctx, double* payload, uint8_t* occupancy);
+int vrf_grid_download_f32(vrf_context* ctx, float* payload);
+int vrf_grid_get_geometry(const vrf_context* ctx, vrf_grid_geometry* out);
+/* VoxelGrid::prune(tau) — voxel_grid.cpp:169-188. */
+int vrf_grid_prune(vrf_context* ctx, double tau, int64_t* deactivated);
+
+/* ---- frames: Frame (frame.hpp:10-19); colour H*W*3, depth H*W along-ray metres */
+int vrf_frames_upload(vrf_context* ctx, const vrf_intrinsics* intr, int n,
+                      const double* const* colors, const double* const* depths,
+                      const vrf_pose* poses);
+int vrf_frames_count(const vrf_context* ctx);
+
+/* ---- renderer: render_image — renderer.hpp:83-84 (renderer.cpp:149-174).
+ * color: ceil(H/stride)*ceil(W/stride)*3, depth: ceil(H/stride)*ceil(W/stride). */
+int vrf_render_image(vrf_context* ctx, const vrf_intrinsics* intr, const vrf_pose* pose,
+                     const vrf_render_params* params, int stride, double* color,
+                     double* depth);
+
+/* ---- mapping: mapping_step — mapping.hpp:80-82 (mapping.cpp:114-233) with the
+ * batch drawn by the caller (the reference draws it from its Rng,
+ * mapping.cpp:121-128): batch = n_rays (frame, px, py) int32 triples, host memory.
+ * Mutates the device grid and RMSProp state in place, like the reference. */
+int vrf_mapping_step(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* batch,
+                     int n_rays, vrf_map_step_stats* out);
+/* Same, batch already in device memory. */
+int vrf_mapping_step_device(vrf_context* ctx, const vrf_mapping_config* cfg,
+                            const int32_t* batch_dev, int n_rays, vrf_map_step_stats* out);
+/* The merged grid gradient of one batch (no update): double [V][28] host. */
+int vrf_mapping_gradient(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* batch,
+                         int n_rays, double* grad_out, vrf_map_step_stats* out);
+/* RmspropState — mapping.hpp:48-52. */
+int vrf_rmsprop_reset(vrf_context* ctx);
+int vrf_rmsprop_download(vrf_context* ctx, double* v);
+int vrf_rmsprop_upload(vrf_context* ctx, const double* v);
+/* Multi-GPU phases (ray-sharded data parallel):
+ *   forward (local partials) -> caller all-reduces partials ->
+ *   backward with the GLOBAL hit counts -> caller reduce-scatters grad ->
+ *   apply (RMSProp on the owned vertex shard, clears grad) -> caller all-gathers payload. */
+int vrf_map_forward(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* batch_dev,
+                    int n_rays, vrf_map_partials* out);
+int vrf_map_backward(vrf_context* ctx, const vrf_mapping_config* cfg, int32_t rays_color,
+                     int32_t rays_depth);
+int vrf_map_apply(vrf_context* ctx, const vrf_mapping_config* cfg, int64_t vertex_begin,
+                  int64_t vertex_end);
+
+/* ---- tracking */
+/* pose_gradient — tracking.hpp:70-73 (tracking.cpp:76-143); pixels: n (px, py). */
+int vrf_pose_gradient(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
+                      const vrf_pose* pose, const int32_t* pixels, int n,
+                      const vrf_tracking_loss* cfg, vrf_pose_gradient_result* out);
+int vrf_pose_normal_equations(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
+                              const vrf_pose* pose, const int32_t* pixels, int n,
+                              const vrf_tracking_loss* cfg, vrf_normal_equations* out);
+/* track_frame — tracking.hpp:82-84 (tracking.cpp:170-252): Adam, pixel draws from
+ * the reference Rng stream (xoshiro256**, seed cfg->seed). loss_trace: iterations. */
+int vrf_track_frame(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
+                    const vrf_pose* init, const vrf_tracking_config* cfg,
+                    vrf_track_frame_result* out, double* loss_trace);
+/* Gauss-Newton/LM tracking with the whole iteration loop on the device (one CUDA
+ * graph: draw -> render+Jacobian -> reduce -> 6x6 solve -> pose update). */
+int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
+                       const vrf_pose* init, const vrf_gn_config* cfg,
+                       vrf_track_frame_result* out);
+
+/* ---- host helpers: the reference's Rng stream (rng.hpp:13-81, xoshiro256**) */
+void vrf_rng_seed(uint64_t seed, uint64_t state[4]);
+uint64_t vrf_rng_next(uint64_t state[4]);
+/* mapping.cpp:121-128: per ray frame = U[n_frames), px = U[width), py = U[height) */
+void vrf_rng_draw_batch(uint64_t state[4], int n_frames, int width, int height, int n,
+                        int32_t* batch);
+/* tracking.cpp:147-166; returns the number of pixels written (<= count) */
+int vrf_rng_draw_valid_pixels(uint64_t state[4], const double* depth, int width, int height,
+                              int count, int max_redraws, int32_t* pixels);
+
+/* ---- inspection (parity tests): sample_ray / render_ray per explicit ray.
+ * rays: n * (ox, oy, oz, dx, dy, dz). */
+int vrf_debug_sample_rays(vrf_context* ctx, const double* rays, int n,
+                          const vrf_render_params* params, int cap, int32_t* counts,
+                          double* t, double* delta, uint32_t* cells);
+/* out: n * 8 doubles (r, g, b, depth, T_terminal, count, hit, terminated_early). */
+int vrf_debug_render_rays(vrf_context* ctx, const double* rays, int n,
+                          const vrf_render_params* params, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXRF_B200_H */

@@ -1,0 +1,400 @@
+"""ctypes binding of the CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+* ``Oracle``  -> oracle/liboracle_voxrf.so  (plain-C FP64 restatement, voxrf_oracle.c)
+* ``RefLib``  -> oracle/_ref/libvoxrf_ref.so (the reference's own sources compiled
+                 unchanged against oracle/shim; built by `make -C oracle ref`)
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline / reference arm
+may import this module. The product (paper_2307_03404_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle_voxrf.so"
+REF_SO = HERE / "_ref" / "libvoxrf_ref.so"
+REF_SRC = Path("/root/reference/proj")
+
+
+class Geometry(C.Structure):
+    _fields_ = [("res", C.c_int32 * 3), ("origin", C.c_double * 3), ("voxel_size", C.c_double)]
+
+
+class Grid(C.Structure):
+    _fields_ = [("geom", Geometry), ("data", C.c_void_p), ("active", C.c_void_p)]
+
+
+class Intr(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32), ("depth_scale", C.c_double)]
+
+
+class PoseS(C.Structure):
+    _fields_ = [("q", C.c_double * 4), ("t", C.c_double * 3)]
+
+
+class Params(C.Structure):
+    _fields_ = [("step", C.c_double), ("t_near", C.c_double), ("t_far", C.c_double),
+                ("termination_eps", C.c_double)]
+
+
+class FrameS(C.Structure):
+    _fields_ = [("color", C.c_void_p), ("depth", C.c_void_p), ("pose", PoseS)]
+
+
+class RayResult(C.Structure):
+    _fields_ = [("color", C.c_double * 3), ("depth", C.c_double),
+                ("transmittance_terminal", C.c_double), ("count", C.c_int32), ("hit", C.c_int32),
+                ("terminated_early", C.c_int32)]
+
+
+class MapCfg(C.Structure):
+    _fields_ = [("lambda_d", C.c_double), ("lr_sigma", C.c_double), ("lr_sh", C.c_double),
+                ("rmsprop_decay", C.c_double), ("rmsprop_eps", C.c_double), ("render", Params)]
+
+
+class MapStats(C.Structure):
+    _fields_ = [("loss_photometric", C.c_double), ("loss_geometric", C.c_double),
+                ("loss_total", C.c_double), ("rays_color", C.c_int32), ("rays_depth", C.c_int32),
+                ("psnr_estimate", C.c_double), ("samples", C.c_int64), ("bad_ray", C.c_int32)]
+
+
+class TrackLoss(C.Structure):
+    _fields_ = [("lambda_p", C.c_double), ("lambda_d", C.c_double), ("render", Params)]
+
+
+class PoseGrad(C.Structure):
+    _fields_ = [("d_omega", C.c_double * 3), ("d_tau", C.c_double * 3), ("loss", C.c_double),
+                ("rays_used", C.c_int32)]
+
+
+class NormalEqs(C.Structure):
+    _fields_ = [("jtj", C.c_double * 21), ("jtr", C.c_double * 6), ("loss", C.c_double),
+                ("rays_used", C.c_int32)]
+
+
+class TrackCfg(C.Structure):
+    _fields_ = [("rays_per_iteration", C.c_int32), ("iterations", C.c_int32),
+                ("lr_omega", C.c_double), ("lr_tau", C.c_double), ("beta1", C.c_double),
+                ("beta2", C.c_double), ("adam_eps", C.c_double), ("lambda_p", C.c_double),
+                ("lambda_d", C.c_double), ("convergence_step", C.c_double),
+                ("divergence_factor", C.c_double), ("divergence_patience", C.c_int32),
+                ("max_redraws", C.c_int32), ("seed", C.c_uint64), ("render", Params)]
+
+
+class TrackResult(C.Structure):
+    _fields_ = [("pose", PoseS), ("failed", C.c_int32), ("iterations_run", C.c_int32),
+                ("final_loss", C.c_double)]
+
+
+def build(ref: bool = True) -> None:
+    """make -C oracle (and the reference build when /root/reference is present)."""
+    subprocess.run(["make", "-s", "-C", str(HERE), "all"], check=True)
+    if ref and REF_SRC.exists():
+        subprocess.run(["make", "-s", "-j8", "-C", str(HERE), "ref"], check=True)
+
+
+def _ptr(a):
+    return C.c_void_p(a.ctypes.data)
+
+
+def geometry(geom) -> Geometry:
+    return Geometry((C.c_int32 * 3)(*map(int, geom.res)), (C.c_double * 3)(*map(float, geom.origin)),
+                    float(geom.voxel_size))
+
+
+def intr_s(i) -> Intr:
+    return Intr(i.fx, i.fy, i.cx, i.cy, int(i.width), int(i.height), i.depth_scale)
+
+
+def pose_s(p) -> PoseS:
+    return PoseS((C.c_double * 4)(*map(float, p.q)), (C.c_double * 3)(*map(float, p.t)))
+
+
+def params_s(p) -> Params:
+    return Params(p.step, p.t_near, p.t_far, p.termination_eps)
+
+
+class _GridHold:
+    """Keeps numpy buffers alive while a C struct points at them."""
+
+    def __init__(self, grid):
+        self.data = np.ascontiguousarray(grid.data, dtype=np.float64)
+        self.active = np.ascontiguousarray(grid.active, dtype=np.uint8)
+        self.s = Grid(geometry(grid.geom), self.data.ctypes.data, self.active.ctypes.data)
+
+
+class _FramesHold:
+    def __init__(self, frames):
+        self.colors = [np.ascontiguousarray(f.color, np.float64) for f in frames]
+        self.depths = [np.ascontiguousarray(f.depth, np.float64) for f in frames]
+        self.arr = (FrameS * max(1, len(frames)))(*[
+            FrameS(c.ctypes.data, d.ctypes.data, pose_s(f.gt_pose))
+            for c, d, f in zip(self.colors, self.depths, frames)])
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _check(rc, what):
+    if rc == 1:
+        raise ValueError(what)
+    if rc == 2:
+        raise IndexError(what)
+    if rc != 0:
+        raise OracleError(what)
+
+
+class Oracle:
+    """The plain-C restatement (voxrf_oracle.c)."""
+
+    def __init__(self):
+        if not ORACLE_SO.exists():
+            build(ref=False)
+        self.lib = C.CDLL(str(ORACLE_SO))
+
+    def generate_ray(self, intr, pose, u, v):
+        o = np.zeros(3)
+        d = np.zeros(3)
+        _check(self.lib.or_generate_ray(C.byref(intr_s(intr)), C.byref(pose_s(pose)),
+                                        C.c_double(u), C.c_double(v), _ptr(o), _ptr(d)),
+               "generate_ray: pixel outside image")
+        return o, d
+
+    def sample_ray(self, grid, o, d, params, cap=4096):
+        h = _GridHold(grid)
+        t = np.zeros(cap)
+        delta = np.zeros(cap)
+        cells = np.zeros(cap, np.uint32)
+        o = np.ascontiguousarray(o, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        n = self.lib.or_sample_ray(C.byref(h.s), _ptr(o), _ptr(d), C.byref(params_s(params)), cap,
+                                   _ptr(t), _ptr(delta), _ptr(cells))
+        if n < 0:
+            _check(-n, "sample_ray")
+        return t[:n], delta[:n], cells[:n]
+
+    def render_ray(self, grid, o, d, params):
+        h = _GridHold(grid)
+        r = RayResult()
+        o = np.ascontiguousarray(o, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        _check(self.lib.or_render_ray(C.byref(h.s), _ptr(o), _ptr(d), C.byref(params_s(params)),
+                                      C.byref(r)), "render_ray")
+        return r
+
+    def render_image(self, grid, intr, pose, params, stride=1):
+        h = _GridHold(grid)
+        ow = (intr.width + stride - 1) // stride
+        oh = (intr.height + stride - 1) // stride
+        color = np.zeros((oh, ow, 3))
+        depth = np.zeros((oh, ow))
+        _check(self.lib.or_render_image(C.byref(h.s), C.byref(intr_s(intr)), C.byref(pose_s(pose)),
+                                        C.byref(params_s(params)), stride, _ptr(color), _ptr(depth)),
+               "render_image")
+        return color, depth
+
+    def mapping_step(self, grid, frames, intr, cfg, batch, rms_v=None, apply=True, want_grad=False):
+        """Returns (new_data, new_rms_v, grad or None, stats). grid is not modified."""
+        data = np.ascontiguousarray(grid.data, np.float64).copy()
+        active = np.ascontiguousarray(grid.active, np.uint8)
+        gs = Grid(geometry(grid.geom), data.ctypes.data, active.ctypes.data)
+        fh = _FramesHold(frames)
+        v = np.zeros_like(data) if rms_v is None else np.ascontiguousarray(rms_v, np.float64).reshape(data.shape).copy()
+        grad = np.zeros_like(data) if want_grad else None
+        b = np.ascontiguousarray(batch, np.int32)
+        st = MapStats()
+        mc = MapCfg(cfg.lambda_d, cfg.lr_sigma, cfg.lr_sh, cfg.rmsprop_decay, cfg.rmsprop_eps,
+                    params_s(cfg.render))
+        rc = self.lib.or_mapping_step(C.byref(gs), fh.arr, len(frames), C.byref(intr_s(intr)),
+                                      C.byref(mc), _ptr(b), b.shape[0], _ptr(v),
+                                      _ptr(grad) if want_grad else None, 1 if apply else 0,
+                                      C.byref(st))
+        _check(rc, f"mapping_step (bad_ray={st.bad_ray}, rays_color={st.rays_color})")
+        return data, v, grad, st
+
+    def pose_gradient(self, grid, frame, intr, pose, pixels, lambda_p, lambda_d, params):
+        h = _GridHold(grid)
+        fh = _FramesHold([frame])
+        px = np.ascontiguousarray(pixels, np.int32)
+        out = PoseGrad()
+        _check(self.lib.or_pose_gradient(C.byref(h.s), fh.arr, C.byref(intr_s(intr)),
+                                         C.byref(pose_s(pose)), _ptr(px), px.shape[0],
+                                         C.byref(TrackLoss(lambda_p, lambda_d, params_s(params))),
+                                         C.byref(out)), "pose_gradient")
+        return out
+
+    def normal_eqs(self, grid, frame, intr, pose, pixels, lambda_p, lambda_d, params):
+        h = _GridHold(grid)
+        fh = _FramesHold([frame])
+        px = np.ascontiguousarray(pixels, np.int32)
+        out = NormalEqs()
+        _check(self.lib.or_pose_normal_eqs(C.byref(h.s), fh.arr, C.byref(intr_s(intr)),
+                                           C.byref(pose_s(pose)), _ptr(px), px.shape[0],
+                                           C.byref(TrackLoss(lambda_p, lambda_d, params_s(params))),
+                                           C.byref(out)), "normal_eqs")
+        return out
+
+    def track_frame(self, grid, frame, intr, init, tcfg):
+        h = _GridHold(grid)
+        fh = _FramesHold([frame])
+        out = TrackResult()
+        trace = np.zeros(max(tcfg.iterations, 1))
+        _check(self.lib.or_track_frame(C.byref(h.s), fh.arr, C.byref(intr_s(intr)),
+                                       C.byref(pose_s(init)), C.byref(track_cfg(tcfg)),
+                                       C.byref(out), _ptr(trace)), "track_frame")
+        return out, trace[:out.iterations_run]
+
+    def draw_batch(self, seed, n_frames, w, h, n):
+        st = (C.c_uint64 * 4)()
+        self.lib.or_rng_seed(C.c_uint64(seed), st)
+        out = np.zeros((n, 3), np.int32)
+        self.lib.or_draw_batch(st, n_frames, w, h, n, _ptr(out))
+        return out
+
+
+def track_cfg(c) -> TrackCfg:
+    return TrackCfg(c.rays_per_iteration, c.iterations, c.lr_omega, c.lr_tau, c.beta1, c.beta2,
+                    c.adam_eps, c.lambda_p, c.lambda_d, c.convergence_step, c.divergence_factor,
+                    c.divergence_patience, c.max_redraws, c.seed & (2**64 - 1), params_s(c.render))
+
+
+class RefLib:
+    """The reference's own functions (oracle/_ref/libvoxrf_ref.so)."""
+
+    def __init__(self):
+        if not REF_SO.exists():
+            if not REF_SRC.exists():
+                raise FileNotFoundError("oracle/_ref not built and /root/reference absent")
+            build(ref=True)
+        lib = C.CDLL(str(REF_SO))
+        lib.ref_grid_create.restype = C.c_void_p
+        lib.ref_grid_create.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.ref_frames_create.restype = C.c_void_p
+        lib.ref_frames_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+        lib.ref_mapper_create.restype = C.c_void_p
+        lib.ref_mapper_create.argtypes = [C.c_uint64]
+        lib.ref_last_error.restype = C.c_char_p
+        for n in ["ref_grid_destroy", "ref_frames_destroy", "ref_mapper_destroy"]:
+            getattr(lib, n).argtypes = [C.c_void_p]
+        lib.ref_grid_read.argtypes = [C.c_void_p, C.c_void_p]
+        lib.ref_mapper_rms.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+        lib.ref_mapping_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                         C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        lib.ref_mapping_grad.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        lib.ref_render_image.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                         C.c_int, C.c_void_p, C.c_void_p]
+        lib.ref_render_ray.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.ref_sample_ray.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.ref_pose_gradient.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
+        lib.ref_pose_normal_eqs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        lib.ref_track_frame.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        self.lib = lib
+
+    def _err(self, rc, what):
+        if rc != 0:
+            msg = self.lib.ref_last_error().decode()
+            _check(rc, f"{what}: {msg}")
+
+    def grid(self, grid):
+        g = geometry(grid.geom)
+        data = np.ascontiguousarray(grid.data, np.float64)
+        act = np.ascontiguousarray(grid.active, np.uint8)
+        return self.lib.ref_grid_create(C.byref(g), _ptr(data), _ptr(act))
+
+    def frames(self, frames, intr):
+        fh = _FramesHold(frames)
+        return self.lib.ref_frames_create(fh.arr, len(frames), intr.width, intr.height)
+
+    def read_grid(self, handle, nv):
+        out = np.zeros((nv, 28))
+        self.lib.ref_grid_read(handle, _ptr(out))
+        return out
+
+    def render_image(self, grid_h, intr, pose, params, stride=1, threads=1):
+        ow = (intr.width + stride - 1) // stride
+        oh = (intr.height + stride - 1) // stride
+        color = np.zeros((oh, ow, 3))
+        depth = np.zeros((oh, ow))
+        self._err(self.lib.ref_render_image(grid_h, C.byref(intr_s(intr)), C.byref(pose_s(pose)),
+                                            C.byref(params_s(params)), stride, threads,
+                                            _ptr(color), _ptr(depth)), "render_image")
+        return color, depth
+
+    def render_ray(self, grid_h, o, d, params):
+        r = RayResult()
+        o = np.ascontiguousarray(o, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        self._err(self.lib.ref_render_ray(grid_h, _ptr(o), _ptr(d), C.byref(params_s(params)),
+                                          C.byref(r)), "render_ray")
+        return r
+
+    def sample_ray(self, grid_h, o, d, params, cap=4096):
+        t = np.zeros(cap)
+        delta = np.zeros(cap)
+        n = C.c_int()
+        o = np.ascontiguousarray(o, np.float64)
+        d = np.ascontiguousarray(d, np.float64)
+        self._err(self.lib.ref_sample_ray(grid_h, _ptr(o), _ptr(d), C.byref(params_s(params)), cap,
+                                          _ptr(t), _ptr(delta), C.byref(n)), "sample_ray")
+        return t[:n.value], delta[:n.value]
+
+    def mapping_step(self, grid_h, frames_h, intr, cfg, n_rays, threads, deterministic, mapper):
+        st = MapStats()
+        mc = MapCfg(cfg.lambda_d, cfg.lr_sigma, cfg.lr_sh, cfg.rmsprop_decay, cfg.rmsprop_eps,
+                    params_s(cfg.render))
+        self._err(self.lib.ref_mapping_step(grid_h, frames_h, C.byref(intr_s(intr)), C.byref(mc),
+                                            n_rays, threads, 1 if deterministic else 0, mapper,
+                                            C.byref(st)), "mapping_step")
+        return st
+
+    def mapping_grad(self, grid_h, frames_h, intr, cfg, batch, nv):
+        b = np.ascontiguousarray(batch, np.int32)
+        out = np.zeros((nv, 28))
+        samples = C.c_int64()
+        mc = MapCfg(cfg.lambda_d, cfg.lr_sigma, cfg.lr_sh, cfg.rmsprop_decay, cfg.rmsprop_eps,
+                    params_s(cfg.render))
+        self._err(self.lib.ref_mapping_grad(grid_h, frames_h, C.byref(intr_s(intr)), C.byref(mc),
+                                            _ptr(b), b.shape[0], _ptr(out), C.byref(samples)),
+                  "mapping_grad")
+        return out, samples.value
+
+    def pose_gradient(self, grid_h, frames_h, intr, pose, pixels, lambda_p, lambda_d, params,
+                      threads=1):
+        px = np.ascontiguousarray(pixels, np.int32)
+        out = PoseGrad()
+        self._err(self.lib.ref_pose_gradient(grid_h, frames_h, C.byref(intr_s(intr)),
+                                             C.byref(pose_s(pose)), _ptr(px), px.shape[0],
+                                             C.byref(TrackLoss(lambda_p, lambda_d, params_s(params))),
+                                             threads, C.byref(out)), "pose_gradient")
+        return out
+
+    def normal_eqs(self, grid_h, frames_h, intr, pose, pixels, lambda_p, lambda_d, params):
+        px = np.ascontiguousarray(pixels, np.int32)
+        out = NormalEqs()
+        self._err(self.lib.ref_pose_normal_eqs(grid_h, frames_h, C.byref(intr_s(intr)),
+                                               C.byref(pose_s(pose)), _ptr(px), px.shape[0],
+                                               C.byref(TrackLoss(lambda_p, lambda_d,
+                                                                 params_s(params))),
+                                               C.byref(out)), "normal_eqs")
+        return out
+
+    def track_frame(self, grid_h, frames_h, intr, init, tcfg, threads=1):
+        out = TrackResult()
+        trace = np.zeros(max(tcfg.iterations, 1))
+        self._err(self.lib.ref_track_frame(grid_h, frames_h, C.byref(intr_s(intr)),
+                                           C.byref(pose_s(init)), C.byref(track_cfg(tcfg)), threads,
+                                           C.byref(out), _ptr(trace)), "track_frame")
+        return out, trace[:out.iterations_run]

@@ -1,0 +1,342 @@
+// C-ABI of libvoxrf_b200 (include/voxrf_b200.h): device context, memory,
+// orchestration of the kernels and the reference's error contract.
+#include "vrf_context.h"
+
+using namespace vrf;
+using namespace vrf_host;
+
+// =================================================================== C-ABI
+extern "C" {
+
+int vrf_abi_version(void) { return VRF_ABI_VERSION; }
+
+int vrf_context_create(int device, vrf_context** out) {
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) return VRF_ERR_CUDA;
+  if (device < 0 || device >= count) return VRF_ERR_INVALID_ARGUMENT;
+  if (cudaSetDevice(device) != cudaSuccess) return VRF_ERR_CUDA;
+  auto* ctx = new vrf_context;
+  ctx->device = device;
+  if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&ctx->d_err, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_stats, sizeof(MapStats)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_counts, sizeof(int) * 2) != cudaSuccess ||
+      cudaMalloc(&ctx->d_pcount, sizeof(PoseCount)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_pose_out, sizeof(PosePartial)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_pose, sizeof(DevPose)) != cudaSuccess) {
+    delete ctx;
+    return VRF_ERR_CUDA;
+  }
+  ctx->stream = ctx->own_stream;
+  *out = ctx;
+  return VRF_OK;
+}
+
+void vrf_context_destroy(vrf_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  free_grid(ctx);
+  cudaFree(ctx->rgbd);
+  cudaFree(ctx->poses);
+  cudaFree(ctx->d_err);
+  cudaFree(ctx->d_stats);
+  cudaFree(ctx->d_counts);
+  cudaFree(ctx->d_pcount);
+  cudaFree(ctx->d_pose_out);
+  cudaFree(ctx->d_pose);
+  for (DeviceScratch* s : {&ctx->s_batch, &ctx->s_raycd, &ctx->s_flags, &ctx->s_partials,
+                           &ctx->s_count, &ctx->s_offsets, &ctx->s_keys, &ctx->s_keys2,
+                           &ctx->s_ids, &ctx->s_ids2, &ctx->s_values, &ctx->s_grad64, &ctx->s_cub,
+                           &ctx->s_stage, &ctx->s_out})
+    cudaFree(s->ptr);
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* vrf_last_error(const vrf_context* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int vrf_set_shard_multiple(vrf_context* ctx, int world_size) {
+  if (world_size < 1) return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "world_size must be >= 1");
+  ctx->shard_multiple = world_size;
+  return VRF_OK;
+}
+
+int vrf_set_stream(vrf_context* ctx, void* stream) {
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  return VRF_OK;
+}
+
+int vrf_get_device_buffers(vrf_context* ctx, vrf_device_buffers* out) {
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  out->payload = ctx->payload;
+  out->grad = ctx->grad;
+  out->rms_v = ctx->rms;
+  out->num_vertices = ctx->V;
+  out->padded_vertices = ctx->Vpad;
+  out->stream = ctx->stream;
+  return VRF_OK;
+}
+
+int64_t vrf_kernel_launch_count(const vrf_context* ctx) { return ctx->launches; }
+
+// ----------------------------------------------------------------- grid
+int vrf_grid_init(vrf_context* ctx, const vrf_grid_geometry* geom, double sigma_init) {
+  cudaSetDevice(ctx->device);
+  int rc = alloc_grid(ctx, geom);
+  if (rc) return rc;
+  launch_fill_payload(ctx->payload, ctx->V, (float)sigma_init, ctx->stream);
+  LAUNCHED(1);
+  CU(cudaMemsetAsync(ctx->occ, 0xFF, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1), ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+static int upload_occupancy_u8(vrf_context* ctx, const uint8_t* occupancy) {
+  if (!occupancy) {
+    CU(cudaMemsetAsync(ctx->occ, 0xFF, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1), ctx->stream));
+    return VRF_OK;
+  }
+  int rc = ensure(ctx, ctx->s_stage, (size_t)ctx->C);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(ctx->s_stage.ptr, occupancy, (size_t)ctx->C, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  launch_pack_occupancy((const uint8_t*)ctx->s_stage.ptr, ctx->occ, ctx->C, ctx->stream);
+  LAUNCHED(1);
+  return VRF_OK;
+}
+
+int vrf_grid_upload(vrf_context* ctx, const vrf_grid_geometry* geom, const double* payload,
+                    const uint8_t* occupancy) {
+  cudaSetDevice(ctx->device);
+  int rc = alloc_grid(ctx, geom);
+  if (rc) return rc;
+  // fp64 -> fp32 in 32 MB chunks through a device staging buffer.
+  const long long total = ctx->V * 28;
+  const long long chunk = 4LL << 20;
+  if ((rc = ensure(ctx, ctx->s_out, sizeof(double) * chunk))) return rc;
+  for (long long off = 0; off < total; off += chunk) {
+    const long long n = std::min(chunk, total - off);
+    CU(cudaMemcpyAsync(ctx->s_out.ptr, payload + off, sizeof(double) * n, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    launch_f64_to_f32((const double*)ctx->s_out.ptr, ctx->payload + off, n, ctx->stream);
+    LAUNCHED(1);
+  }
+  if ((rc = upload_occupancy_u8(ctx, occupancy))) return rc;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_grid_upload_f32(vrf_context* ctx, const vrf_grid_geometry* geom, const float* payload,
+                        const uint8_t* occupancy_bits) {
+  cudaSetDevice(ctx->device);
+  int rc = alloc_grid(ctx, geom);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(ctx->payload, payload, sizeof(float) * 28 * ctx->V, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  if (occupancy_bits) {
+    // LSB-first byte mask (voxel_grid.cpp:234-236) == little-endian uint32 words.
+    CU(cudaMemsetAsync(ctx->occ, 0, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1), ctx->stream));
+    CU(cudaMemcpyAsync(ctx->occ, occupancy_bits, (size_t)((ctx->C + 7) / 8),
+                       cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    CU(cudaMemsetAsync(ctx->occ, 0xFF, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1), ctx->stream));
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_grid_download(vrf_context* ctx, double* payload, uint8_t* occupancy) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if (payload) {
+    const long long total = ctx->V * 28;
+    const long long chunk = 4LL << 20;
+    if ((rc = ensure(ctx, ctx->s_out, sizeof(double) * chunk))) return rc;
+    for (long long off = 0; off < total; off += chunk) {
+      const long long n = std::min(chunk, total - off);
+      launch_f32_to_f64(ctx->payload + off, (double*)ctx->s_out.ptr, n, ctx->stream);
+      LAUNCHED(1);
+      CU(cudaMemcpyAsync(payload + off, ctx->s_out.ptr, sizeof(double) * n,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  if (occupancy) {
+    if ((rc = ensure(ctx, ctx->s_stage, (size_t)ctx->C))) return rc;
+    launch_unpack_occupancy(ctx->occ, (uint8_t*)ctx->s_stage.ptr, ctx->C, ctx->stream);
+    LAUNCHED(1);
+    CU(cudaMemcpyAsync(occupancy, ctx->s_stage.ptr, (size_t)ctx->C, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_grid_download_f32(vrf_context* ctx, float* payload) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(payload, ctx->payload, sizeof(float) * 28 * ctx->V, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_grid_get_geometry(const vrf_context* ctx, vrf_grid_geometry* out) {
+  if (!ctx->has_grid) return VRF_ERR_RUNTIME;
+  *out = ctx->geom;
+  return VRF_OK;
+}
+
+int vrf_grid_prune(vrf_context* ctx, double tau, int64_t* deactivated) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if ((rc = ensure(ctx, ctx->s_out, sizeof(unsigned long long)))) return rc;
+  CU(cudaMemsetAsync(ctx->s_out.ptr, 0, sizeof(unsigned long long), ctx->stream));
+  launch_prune(dev_grid(ctx), ctx->occ, tau, (unsigned long long*)ctx->s_out.ptr, ctx->stream);
+  LAUNCHED(1);
+  unsigned long long n = 0;
+  CU(cudaMemcpyAsync(&n, ctx->s_out.ptr, sizeof(n), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (deactivated) *deactivated = (int64_t)n;
+  return VRF_OK;
+}
+
+// ----------------------------------------------------------------- frames
+int vrf_frames_upload(vrf_context* ctx, const vrf_intrinsics* intr, int n,
+                      const double* const* colors, const double* const* depths,
+                      const vrf_pose* poses) {
+  cudaSetDevice(ctx->device);
+  if (n < 0 || !intr || intr->width <= 0 || intr->height <= 0)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "intrinsics: empty image size");
+  cudaFree(ctx->rgbd);
+  cudaFree(ctx->poses);
+  ctx->rgbd = nullptr;
+  ctx->poses = nullptr;
+  ctx->n_frames = 0;
+  ctx->host_depth.clear();
+  const long long npix = (long long)intr->width * intr->height;
+  if (n > 0) {
+    CU(cudaMalloc(&ctx->rgbd, sizeof(double4) * npix * n));
+    CU(cudaMalloc(&ctx->poses, sizeof(DevPose) * n));
+    int rc = ensure(ctx, ctx->s_stage, sizeof(double) * npix * 4);
+    if (rc) return rc;
+    std::vector<DevPose> hp(n);
+    for (int f = 0; f < n; ++f) {
+      double* st = (double*)ctx->s_stage.ptr;
+      CU(cudaMemcpyAsync(st, colors[f], sizeof(double) * npix * 3, cudaMemcpyHostToDevice,
+                         ctx->stream));
+      CU(cudaMemcpyAsync(st + npix * 3, depths[f], sizeof(double) * npix, cudaMemcpyHostToDevice,
+                         ctx->stream));
+      launch_pack_frames(st, st + npix * 3, ctx->rgbd + npix * f, npix, ctx->stream);
+      LAUNCHED(1);
+      CU(cudaStreamSynchronize(ctx->stream));
+      hp[f] = dev_pose(&poses[f]);
+      ctx->host_depth.emplace_back(depths[f], depths[f] + npix);
+    }
+    CU(cudaMemcpyAsync(ctx->poses, hp.data(), sizeof(DevPose) * n, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  ctx->fintr = *intr;
+  ctx->n_frames = n;
+  return VRF_OK;
+}
+
+int vrf_frames_count(const vrf_context* ctx) { return ctx->n_frames; }
+
+// ----------------------------------------------------------------- render_image
+int vrf_render_image(vrf_context* ctx, const vrf_intrinsics* intr, const vrf_pose* pose,
+                     const vrf_render_params* params, int stride, double* color, double* depth) {
+  cudaSetDevice(ctx->device);
+  if (stride < 1)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "render_image: stride must be >= 1");
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  DevParams p;
+  if ((rc = resolve_params(ctx, params, &p))) return rc;
+  const int out_w = (intr->width + stride - 1) / stride;
+  const int out_h = (intr->height + stride - 1) / stride;
+  const long long n = (long long)out_w * out_h;
+  if (n <= 0) return VRF_OK;
+  if ((rc = ensure(ctx, ctx->s_out, sizeof(double) * 4 * n))) return rc;
+  double* dc = (double*)ctx->s_out.ptr;
+  CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+  launch_render_image(dev_grid(ctx), p, dev_cam(intr), dev_pose(pose), stride, out_w, out_h, dc,
+                      dc + 3 * n, ctx->d_err, ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  if ((rc = check_err_flag(ctx))) return rc;
+  CU(cudaMemcpyAsync(color, dc, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(depth, dc + 3 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+// ----------------------------------------------------------------- inspection
+int vrf_debug_sample_rays(vrf_context* ctx, const double* rays, int n,
+                          const vrf_render_params* params, int cap, int32_t* counts, double* t,
+                          double* delta, uint32_t* cells) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  DevParams p;
+  if ((rc = resolve_params(ctx, params, &p))) return rc;
+  if (n <= 0) return VRF_OK;
+  const size_t need = sizeof(double) * 6 * n + sizeof(int) * n + (size_t)n * cap * 20 + 64;
+  if ((rc = ensure(ctx, ctx->s_out, need))) return rc;
+  char* base = (char*)ctx->s_out.ptr;
+  double* d_rays = (double*)base;
+  double* d_t = d_rays + 6 * n;
+  double* d_delta = d_t + (size_t)n * cap;
+  uint32_t* d_cells = (uint32_t*)(d_delta + (size_t)n * cap);
+  int* d_counts = (int*)(d_cells + (size_t)n * cap);
+  CU(cudaMemcpyAsync(d_rays, rays, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+  launch_debug_rays(dev_grid(ctx), p, d_rays, n, cap, d_counts, d_t, d_delta, d_cells, nullptr,
+                    ctx->d_err, ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(counts, d_counts, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (cap > 0) {
+    CU(cudaMemcpyAsync(t, d_t, sizeof(double) * n * cap, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(delta, d_delta, sizeof(double) * n * cap, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(cells, d_cells, sizeof(uint32_t) * n * cap, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_debug_render_rays(vrf_context* ctx, const double* rays, int n,
+                          const vrf_render_params* params, double* out) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  DevParams p;
+  if ((rc = resolve_params(ctx, params, &p))) return rc;
+  if (n <= 0) return VRF_OK;
+  if ((rc = ensure(ctx, ctx->s_out, sizeof(double) * 14 * n))) return rc;
+  double* d_rays = (double*)ctx->s_out.ptr;
+  double* d_out = d_rays + 6 * n;
+  CU(cudaMemcpyAsync(d_rays, rays, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+  launch_debug_rays(dev_grid(ctx), p, d_rays, n, 0, nullptr, nullptr, nullptr, nullptr, d_out,
+                    ctx->d_err, ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  if ((rc = check_err_flag(ctx))) return rc;
+  CU(cudaMemcpyAsync(out, d_out, sizeof(double) * 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,273 @@
+// Internal: the vrf_context definition and host helpers shared by the C-ABI
+// translation units (vrf_capi.cu, vrf_map.cu, vrf_pose.cu).
+#pragma once
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/voxrf_b200.h"
+#include "vrf_internal.h"
+
+namespace vrf_host {
+
+struct DeviceScratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace vrf_host
+
+using vrf::DevPose;
+using vrf::MapStats;
+using vrf::PoseCount;
+using vrf::PosePartial;
+
+struct vrf_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  std::string err;
+  int shard_multiple = 1;
+  long long launches = 0;
+
+  // grid
+  bool has_grid = false;
+  vrf_grid_geometry geom{};
+  long long V = 0, Vpad = 0, C = 0;
+  float* payload = nullptr;
+  float* grad = nullptr;
+  float* rms = nullptr;
+  uint32_t* occ = nullptr;
+
+  // frames
+  int n_frames = 0;
+  vrf_intrinsics fintr{};
+  double4* rgbd = nullptr;
+  DevPose* poses = nullptr;
+  std::vector<std::vector<double>> host_depth;
+
+  // persistent small device state
+  int* d_err = nullptr;
+  MapStats* d_stats = nullptr;
+  int* d_counts = nullptr;
+  PoseCount* d_pcount = nullptr;
+  PosePartial* d_pose_out = nullptr;
+  DevPose* d_pose = nullptr;
+  // pinned host staging
+  void* h_pinned = nullptr;
+  size_t h_pinned_bytes = 0;
+
+  // grow-only scratch
+  vrf_host::DeviceScratch s_batch, s_raycd, s_flags, s_partials, s_count, s_offsets, s_keys, s_keys2,
+      s_ids, s_ids2, s_values, s_grad64, s_cub, s_stage, s_out;
+
+  // multi-GPU phase state
+  const int* last_batch = nullptr;
+  int last_n = 0;
+};
+
+namespace vrf_host {
+using namespace vrf;
+
+inline int set_err(vrf_context* c, int code, const std::string& m) {
+  c->err = m;
+  return code;
+}
+
+#define CU(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(ctx, VRF_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e_) + \
+                                            " (" #x ")");                               \
+  } while (0)
+
+#define LAUNCHED(n) (ctx->launches += (n))
+
+inline int ensure(vrf_context* ctx, DeviceScratch& s, size_t bytes) {
+  if (s.bytes >= bytes) return VRF_OK;
+  if (s.ptr) CU(cudaFree(s.ptr));
+  s.ptr = nullptr;
+  s.bytes = 0;
+  const size_t want = bytes < 256 ? 256 : bytes + bytes / 4;
+  CU(cudaMalloc(&s.ptr, want));
+  s.bytes = want;
+  return VRF_OK;
+}
+
+inline int ensure_pinned(vrf_context* ctx, size_t bytes) {
+  if (ctx->h_pinned_bytes >= bytes) return VRF_OK;
+  if (ctx->h_pinned) CU(cudaFreeHost(ctx->h_pinned));
+  ctx->h_pinned = nullptr;
+  const size_t want = bytes < 4096 ? 4096 : bytes + bytes / 4;
+  CU(cudaMallocHost(&ctx->h_pinned, want));
+  ctx->h_pinned_bytes = want;
+  return VRF_OK;
+}
+
+inline void free_grid(vrf_context* ctx) {
+  cudaFree(ctx->payload);
+  cudaFree(ctx->grad);
+  cudaFree(ctx->rms);
+  cudaFree(ctx->occ);
+  ctx->payload = ctx->grad = ctx->rms = nullptr;
+  ctx->occ = nullptr;
+  ctx->has_grid = false;
+}
+
+inline int validate_geometry(vrf_context* ctx, const vrf_grid_geometry* g) {
+  // GridGeometry::validate — voxel_grid.hpp:25-28
+  if (!g) return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "grid: null geometry");
+  if (std::min(g->res[0], std::min(g->res[1], g->res[2])) < 2)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "grid: resolution must be >= 2 per axis");
+  if (!(g->voxel_size > 0.0))
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "grid: voxel_size must be > 0");
+  const long long V = (long long)g->res[0] * g->res[1] * g->res[2];
+  if (V > 0xFFFFFFFFLL)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "grid: more than 2^32 vertices");
+  return VRF_OK;
+}
+
+inline int alloc_grid(vrf_context* ctx, const vrf_grid_geometry* g) {
+  int rc = validate_geometry(ctx, g);
+  if (rc) return rc;
+  free_grid(ctx);
+  ctx->geom = *g;
+  ctx->V = (long long)g->res[0] * g->res[1] * g->res[2];
+  ctx->C = (long long)(g->res[0] - 1) * (g->res[1] - 1) * (g->res[2] - 1);
+  const long long m = ctx->shard_multiple;
+  ctx->Vpad = (ctx->V + m - 1) / m * m;
+  CU(cudaMalloc(&ctx->payload, sizeof(float) * 28 * ctx->Vpad));
+  CU(cudaMalloc(&ctx->grad, sizeof(float) * 28 * ctx->Vpad));
+  CU(cudaMalloc(&ctx->rms, sizeof(float) * 28 * ctx->Vpad));
+  CU(cudaMalloc(&ctx->occ, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1)));
+  CU(cudaMemsetAsync(ctx->payload, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
+  CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
+  CU(cudaMemsetAsync(ctx->rms, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
+  ctx->has_grid = true;
+  return VRF_OK;
+}
+
+inline int need_grid(vrf_context* ctx) {
+  if (!ctx->has_grid) return set_err(ctx, VRF_ERR_RUNTIME, "voxrf_b200: no grid loaded");
+  return VRF_OK;
+}
+
+inline DevGrid dev_grid(const vrf_context* ctx) {
+  DevGrid g;
+  const vrf_grid_geometry& q = ctx->geom;
+  g.rx = q.res[0];
+  g.ry = q.res[1];
+  g.rz = q.res[2];
+  g.rxy = (uint32_t)q.res[0] * (uint32_t)q.res[1];
+  g.ox = q.origin[0];
+  g.oy = q.origin[1];
+  g.oz = q.origin[2];
+  g.hx = q.origin[0] + ((double)q.res[0] - 1.0) * q.voxel_size;
+  g.hy = q.origin[1] + ((double)q.res[1] - 1.0) * q.voxel_size;
+  g.hz = q.origin[2] + ((double)q.res[2] - 1.0) * q.voxel_size;
+  g.voxel = q.voxel_size;
+  g.inv_voxel = 1.0 / q.voxel_size;
+  g.payload = reinterpret_cast<const float4*>(ctx->payload);
+  g.occ = ctx->occ;
+  return g;
+}
+
+// RenderParams::effective_step/effective_t_far (renderer.hpp:18-24) and the
+// sample_ray argument checks (renderer.cpp:56-58).
+inline int resolve_params(vrf_context* ctx, const vrf_render_params* rp, DevParams* out) {
+  const vrf_grid_geometry& q = ctx->geom;
+  const double step = rp->step > 0.0 ? rp->step : 0.5 * q.voxel_size;
+  double e[3];
+  for (int a = 0; a < 3; ++a)
+    e[a] = (q.origin[a] + ((double)q.res[a] - 1.0) * q.voxel_size) - q.origin[a];
+  const double diag = std::sqrt((e[0] * e[0] + e[1] * e[1]) + e[2] * e[2]);
+  const double t_far = rp->t_far > 0.0 ? rp->t_far : diag;
+  if (!(step > 0.0)) return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "sample_ray: step must be > 0");
+  if (!(rp->t_near >= 0.0) || t_far <= rp->t_near)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "sample_ray: need 0 <= t_near < t_far");
+  out->step = step;
+  out->t_near = rp->t_near;
+  out->t_far = t_far;
+  out->eps = rp->termination_eps;
+  return VRF_OK;
+}
+
+inline DevCam dev_cam(const vrf_intrinsics* in) {
+  DevCam c;
+  c.fx = in->fx;
+  c.fy = in->fy;
+  c.cx = in->cx;
+  c.cy = in->cy;
+  c.width = in->width;
+  c.height = in->height;
+  return c;
+}
+
+inline DevPose dev_pose(const vrf_pose* p) {
+  DevPose d;
+  for (int i = 0; i < 4; ++i) d.q[i] = p->q[i];
+  for (int i = 0; i < 3; ++i) d.t[i] = p->t[i];
+  d.pad = 0.0;
+  return d;
+}
+
+// Device error flags -> the reference's exception classes.
+inline int check_err_flag(vrf_context* ctx) {
+  int flag = 0;
+  CU(cudaMemcpyAsync(&flag, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (flag & 2) return set_err(ctx, VRF_ERR_OUT_OF_RANGE, "generate_ray: pixel outside image");
+  if (flag & 1)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "sh_eval: direction must be unit length");
+  return VRF_OK;
+}
+
+inline int check_frames(vrf_context* ctx, const vrf_intrinsics* intr) {
+  if (ctx->n_frames == 0) return VRF_OK;
+  if (intr->width != ctx->fintr.width || intr->height != ctx->fintr.height)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT,
+                   "voxrf_b200: intrinsics size differs from the uploaded frames");
+  return VRF_OK;
+}
+
+inline double psnr_from_lp(double lp) {  // mapping.cpp:107-110
+  if (lp <= 0.0) return 99.0;
+  return std::min(99.0, 10.0 * std::log10(3.0 / lp));
+}
+
+// ----------------------------------------------------------------- mapping internals
+// Forward + fixed-order reduce for a device batch; leaves ray_cd/flags/stats on device.
+inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev,
+                           int n, bool fast, int* ray_count = nullptr) {
+  const DevGrid g = dev_grid(ctx);
+  DevParams p;
+  int rc = resolve_params(ctx, &cfg->render, &p);
+  if (rc) return rc;
+  const int nb = map_forward_blocks(n > 0 ? n : 1);
+  if ((rc = ensure(ctx, ctx->s_raycd, sizeof(double4) * (n > 0 ? n : 1)))) return rc;
+  if ((rc = ensure(ctx, ctx->s_flags, n > 0 ? n : 1))) return rc;
+  if ((rc = ensure(ctx, ctx->s_partials, sizeof(MapPartial) * nb))) return rc;
+  CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+  if (n > 0) {
+    launch_map_forward(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
+                       batch_dev, n, (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
+                       (MapPartial*)ctx->s_partials.ptr, ray_count, ctx->d_err, fast,
+                       ctx->stream);
+    LAUNCHED(1);
+  } else {
+    CU(cudaMemsetAsync(ctx->s_partials.ptr, 0, sizeof(MapPartial), ctx->stream));
+  }
+  launch_map_reduce((const MapPartial*)ctx->s_partials.ptr, n > 0 ? nb : 0, ctx->d_stats,
+                    ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  return VRF_OK;
+}
+
+}  // namespace vrf_host
+

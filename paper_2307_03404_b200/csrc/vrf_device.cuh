@@ -1,0 +1,306 @@
+// Device building blocks of the per-ray hot path (sm_100a).
+//
+// Numerics contract:
+//  * Everything that decides WHICH samples exist and WHERE they land — ray
+//    generation, slab clip, the uniform schedule, cell location, occupancy —
+//    is FP64 with the reference's exact operation order and no contraction
+//    (__dadd_rn/__dmul_rn/__ddiv_rn), so sample counts, cell ids and corner
+//    indices are bit-identical to the CPU reference.
+//  * sigma_raw (and with it alpha, T and the T < eps termination test) is also
+//    an FP64 replay of trilerp (voxel_grid.cpp:113-122) over the fp32 payload,
+//    so early termination cannot flip against the oracle.
+//  * The 27 SH channels use the ShT accumulator: double (parity/deterministic
+//    mode) or float (fast mode; colour error ~1e-7, far inside the 1e-4 bar).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vrf {
+
+constexpr int kPayload = 28;      // sigma + 27 SH (voxel_grid.hpp:13-16)
+constexpr int kVec4PerVertex = 7; // 112 B per vertex
+
+// voxel_grid.cpp:11-17
+constexpr double kC0 = 0.28209479177387814;
+constexpr double kC1 = 0.4886025119029199;
+constexpr double kC2_xy = 1.0925484305920792;
+constexpr double kC2_yz = -1.0925484305920792;
+constexpr double kC2_zz = 0.31539156525252005;
+constexpr double kC2_xz = -1.0925484305920792;
+constexpr double kC2_xxyy = 0.5462742152960396;
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+struct DevGrid {
+  int rx, ry, rz;
+  uint32_t rxy;           // rx * ry (vertex z stride)
+  double ox, oy, oz;      // world_min
+  double hx, hy, hz;      // world_max (voxel_grid.hpp:44-46)
+  double voxel;
+  double inv_voxel;       // 1 / voxel (spatial gradient scale, voxel_grid.cpp:136)
+  const float4* __restrict__ payload;  // [V][7]
+  const uint32_t* __restrict__ occ;    // 1 bit per cell, cell_index order
+};
+
+// RenderParams after effective_step / effective_t_far (renderer.hpp:18-24).
+struct DevParams {
+  double step, t_near, t_far, eps;
+};
+
+struct DevCam {
+  double fx, fy, cx, cy;
+  int width, height;
+};
+
+struct DevPose {
+  double q[4];  // w x y z
+  double t[3];
+  double pad;
+};
+
+// ---------------------------------------------------------------- geometry
+// Eigen (a.x*b.x + a.y*b.y) + a.z*b.z
+__device__ __forceinline__ double dot3(const double a[3], const double b[3]) {
+  return dadd(dadd(dmul(a[0], b[0]), dmul(a[1], b[1])), dmul(a[2], b[2]));
+}
+__device__ __forceinline__ void cross3(const double a[3], const double b[3], double o[3]) {
+  const double r0 = dsub(dmul(a[1], b[2]), dmul(a[2], b[1]));
+  const double r1 = dsub(dmul(a[2], b[0]), dmul(a[0], b[2]));
+  const double r2 = dsub(dmul(a[0], b[1]), dmul(a[1], b[0]));
+  o[0] = r0;
+  o[1] = r1;
+  o[2] = r2;
+}
+
+// pixel_direction_cam + Pose::rotate (camera.hpp:33-41, pose.hpp:16):
+// normalized() = v / sqrt(squaredNorm); q*v = v + w*uv + qv x uv, uv = 2 (qv x v).
+__device__ __forceinline__ void generate_dir(const DevCam& c, const DevPose& pose, double u,
+                                             double v, double d[3]) {
+  double cam[3] = {ddiv(dsub(u, c.cx), c.fx), ddiv(dsub(v, c.cy), c.fy), 1.0};
+  const double z = dot3(cam, cam);
+  if (z > 0.0) {
+    const double s = __dsqrt_rn(z);
+    cam[0] = ddiv(cam[0], s);
+    cam[1] = ddiv(cam[1], s);
+    cam[2] = ddiv(cam[2], s);
+  }
+  const double qv[3] = {pose.q[1], pose.q[2], pose.q[3]};
+  double uv[3], c2[3];
+  cross3(qv, cam, uv);
+  uv[0] = dadd(uv[0], uv[0]);
+  uv[1] = dadd(uv[1], uv[1]);
+  uv[2] = dadd(uv[2], uv[2]);
+  cross3(qv, uv, c2);
+  for (int i = 0; i < 3; ++i) d[i] = dadd(dadd(cam[i], dmul(pose.q[0], uv[i])), c2[i]);
+}
+
+// sh_eval — voxel_grid.cpp:34-47. Returns false if |d| is not unit (the
+// reference throws std::invalid_argument).
+__device__ __forceinline__ bool sh_basis(const double d[3], double b[9]) {
+  const double n = __dsqrt_rn(dot3(d, d));
+  if (fabs(dsub(n, 1.0)) > 1e-9) return false;
+  const double x = d[0], y = d[1], z = d[2];
+  b[0] = kC0;
+  b[1] = dmul(-kC1, y);
+  b[2] = dmul(kC1, z);
+  b[3] = dmul(-kC1, x);
+  b[4] = dmul(dmul(kC2_xy, x), y);
+  b[5] = dmul(dmul(kC2_yz, y), z);
+  b[6] = dmul(kC2_zz, dsub(dsub(dmul(dmul(2.0, z), z), dmul(x, x)), dmul(y, y)));
+  b[7] = dmul(dmul(kC2_xz, x), z);
+  b[8] = dmul(kC2_xxyy, dsub(dmul(x, x), dmul(y, y)));
+  return true;
+}
+
+// ---------------------------------------------------------------- march
+struct March {
+  double o[3], d[3];
+  double lo, hi, step;
+  long long nseg, k;
+};
+
+// Slab clip + range clamp + segment count — renderer.cpp:12-29, 51-73.
+__device__ __forceinline__ bool march_begin(const DevGrid& g, const DevParams& p, March& m) {
+  const double wmin[3] = {g.ox, g.oy, g.oz};
+  const double wmax[3] = {g.hx, g.hy, g.hz};
+  double t_enter = 0.0, t_exit = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+  for (int a = 0; a < 3; ++a) {
+    if (fabs(m.d[a]) < 1e-15) {
+      if (m.o[a] < wmin[a] || m.o[a] > wmax[a]) return false;
+      continue;
+    }
+    double t0 = ddiv(dsub(wmin[a], m.o[a]), m.d[a]);
+    double t1 = ddiv(dsub(wmax[a], m.o[a]), m.d[a]);
+    if (t0 > t1) {
+      const double tmp = t0;
+      t0 = t1;
+      t1 = tmp;
+    }
+    t_enter = (t_enter < t0) ? t0 : t_enter;
+    t_exit = (t1 < t_exit) ? t1 : t_exit;
+  }
+  if (!(t_enter < t_exit)) return false;
+  m.lo = (p.t_near < t_enter) ? t_enter : p.t_near;
+  m.hi = (t_exit < p.t_far) ? t_exit : p.t_far;
+  if (m.hi <= m.lo) return false;
+  m.step = p.step;
+  m.nseg = (long long)ceil(dsub(ddiv(dsub(m.hi, m.lo), p.step), 1e-12));
+  m.k = 0;
+  return true;
+}
+
+// One located sample: cell, fractional coordinates, base vertex.
+struct Sample {
+  double t, delta;
+  double fx, fy, fz;
+  uint32_t base;   // vertex_index(cell)
+  uint32_t cell;   // cell_index(cell)
+};
+
+// try_locate — voxel_grid.cpp:83-105 — for the segment midpoint, plus the
+// occupancy test (renderer.cpp:69-70). Returns false for a dropped sample.
+__device__ __forceinline__ bool locate(const DevGrid& g, const double p[3], Sample& s) {
+  const double gx = ddiv(dsub(p[0], g.ox), g.voxel);
+  const double gy = ddiv(dsub(p[1], g.oy), g.voxel);
+  const double gz = ddiv(dsub(p[2], g.oz), g.voxel);
+  if (!(gx >= 0.0 && gx <= (double)g.rx - 1.0)) return false;
+  if (!(gy >= 0.0 && gy <= (double)g.ry - 1.0)) return false;
+  if (!(gz >= 0.0 && gz <= (double)g.rz - 1.0)) return false;
+  int cx = (int)ceil(gx) - 1, cy = (int)ceil(gy) - 1, cz = (int)ceil(gz) - 1;
+  cx = cx < 0 ? 0 : (cx > g.rx - 2 ? g.rx - 2 : cx);
+  cy = cy < 0 ? 0 : (cy > g.ry - 2 ? g.ry - 2 : cy);
+  cz = cz < 0 ? 0 : (cz > g.rz - 2 ? g.rz - 2 : cz);
+  s.fx = dsub(gx, (double)cx);
+  s.fy = dsub(gy, (double)cy);
+  s.fz = dsub(gz, (double)cz);
+  s.base = (uint32_t)(cx + g.rx * (cy + (long long)g.ry * cz));
+  s.cell = (uint32_t)(cx + (g.rx - 1) * (cy + (long long)(g.ry - 1) * cz));
+  return true;
+}
+
+__device__ __forceinline__ bool cell_active(const DevGrid& g, uint32_t cell) {
+  return (__ldg(g.occ + (cell >> 5)) >> (cell & 31)) & 1u;
+}
+
+// Next scheduled, in-bounds, active sample — renderer.cpp:62-79 evaluated lazily.
+__device__ __forceinline__ bool march_next(const DevGrid& g, March& m, Sample& s) {
+  while (m.k < m.nseg) {
+    const double s0 = dadd(m.lo, dmul((double)m.k, m.step));
+    ++m.k;
+    const double s0s = dadd(s0, m.step);
+    const double s1 = (m.hi < s0s) ? m.hi : s0s;
+    const double len = dsub(s1, s0);
+    if (len < 1e-12) continue;
+    const double tm = dmul(0.5, dadd(s0, s1));
+    const double p[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
+                         dadd(m.o[2], dmul(tm, m.d[2]))};
+    if (!locate(g, p, s)) continue;
+    if (!cell_active(g, s.cell)) continue;
+    s.t = tm;
+    s.delta = len;
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ uint32_t corner_index(const DevGrid& g, uint32_t base, int k) {
+  return base + (uint32_t)(k & 1) + ((k >> 1) & 1) * (uint32_t)g.rx + ((k >> 2) & 1) * g.rxy;
+}
+
+// Trilinear weights in the reference order wx[dx]*wy[dy]*wz[dz].
+__device__ __forceinline__ void corner_weights(const Sample& s, double w[8]) {
+  const double wx[2] = {dsub(1.0, s.fx), s.fx};
+  const double wy[2] = {dsub(1.0, s.fy), s.fy};
+  const double wz[2] = {dsub(1.0, s.fz), s.fz};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w[k] = dmul(dmul(wx[k & 1], wy[(k >> 1) & 1]), wz[(k >> 2) & 1]);
+}
+
+// ---------------------------------------------------------------- shading
+// trilerp (voxel_grid.cpp:113-122) + per-channel SH colour with +0.5, clamp
+// and clamp flag (renderer.cpp:104-112).
+struct Shade {
+  double sigma_raw;
+  double c[3];
+  bool clamped[3];
+};
+
+template <typename ShT>
+__device__ __forceinline__ void shade(const DevGrid& g, const Sample& s, const double w[8],
+                                      const double basis[9], Shade& out) {
+  double sraw = 0.0;
+  ShT sh[27];
+#pragma unroll
+  for (int m = 0; m < 27; ++m) sh[m] = ShT(0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4* vp = g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
+    const double wk = w[k];
+    const ShT wks = ShT(wk);
+#pragma unroll
+    for (int j = 0; j < kVec4PerVertex; ++j) {
+      const float4 a = __ldg(vp + j);
+      const float vals[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int slot = 4 * j + e;
+        if (slot == 0) {
+          sraw = dadd(sraw, dmul(wk, (double)vals[e]));
+        } else {
+          if constexpr (sizeof(ShT) == 8)
+            sh[slot - 1] = dadd(sh[slot - 1], dmul(wk, (double)vals[e]));
+          else
+            sh[slot - 1] = fmaf(wks, vals[e], sh[slot - 1]);
+        }
+      }
+    }
+  }
+  out.sigma_raw = sraw;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    double v = 0.5;
+#pragma unroll
+    for (int m = 0; m < 9; ++m) v = dadd(v, dmul((double)sh[ch * 9 + m], basis[m]));
+    out.clamped[ch] = (v <= 0.0 || v >= 1.0);
+    out.c[ch] = (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);
+  }
+}
+
+// Compositing state of one ray — renderer.cpp:89-139.
+struct Composite {
+  double T;
+  double C[3];
+  double D;
+  int count;
+  bool terminated;
+};
+
+// One front-to-back step. Returns the weight; advances T; decay out for T_{i+1}.
+__device__ __forceinline__ double composite_step(Composite& st, const Shade& sh, double t,
+                                                 double delta, double eps, double& decay) {
+  const double sigma = (sh.sigma_raw < 0.0) ? 0.0 : sh.sigma_raw;
+  decay = exp(dmul(-sigma, delta));
+  const double alpha = dsub(1.0, decay);
+  const double w = dmul(st.T, alpha);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) st.C[ch] = dadd(st.C[ch], dmul(w, sh.c[ch]));
+  st.D = dadd(st.D, dmul(w, t));
+  st.T = dmul(st.T, decay);
+  ++st.count;
+  if (st.T < eps) st.terminated = true;
+  return w;
+}
+
+// ---------------------------------------------------------------- reductions
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+}  // namespace vrf

@@ -1,0 +1,94 @@
+// Internal host<->kernel interface of libvoxrf_b200 (not part of the C-ABI).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vrf_device.cuh"
+
+namespace vrf {
+
+// Per-block partial and reduced statistics of a mapping forward pass.
+struct MapPartial {
+  double lp, lg;
+  long long samples;
+  int m_c, m_d, bad;
+  int pad;
+};
+using MapStats = MapPartial;  // reduced: bad = first bad ray (INT_MAX if none)
+
+// Per-block partial / reduced normal equations of a pose pass.
+struct PosePartial {
+  double jtj[21];
+  double jtr[6];
+  double loss;
+  long long samples;
+  int m;
+  int bad;
+};
+
+struct PoseCount {
+  int m;
+  int pad;
+  long long samples;
+};
+
+enum FlagBits : uint8_t { kHit = 1, kDepthValid = 2 };
+
+// Launchers (vrf_kernels.cu). All take the context stream.
+void launch_render_image(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                         const DevPose& pose, int stride, int out_w, int out_h, double* color,
+                         double* depth, int* err_flag, cudaStream_t s);
+void launch_debug_rays(const DevGrid& g, const DevParams& p, const double* rays, int n, int cap,
+                       int* counts, double* t, double* delta, uint32_t* cells, double* out,
+                       int* err_flag, cudaStream_t s);
+void launch_map_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                        const double4* rgbd, const DevPose* poses, int n_frames,
+                        const int* batch, int n, double4* ray_cd, uint8_t* flags,
+                        MapPartial* partials, int* ray_count, int* err_flag, bool fast,
+                        cudaStream_t s);
+int map_forward_blocks(int n);
+void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s);
+void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                         const double4* rgbd, const DevPose* poses, const int* batch, int n,
+                         const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
+                         const int* global_counts, float4* grad, double lambda_d, bool fast,
+                         cudaStream_t s);
+void launch_map_backward_records(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                                 const double4* rgbd, const DevPose* poses, const int* batch,
+                                 int n, const double4* ray_cd, const uint8_t* flags,
+                                 const MapStats* stats, double lambda_d,
+                                 const long long* ray_offsets, uint32_t* keys, uint32_t* ids,
+                                 double* values, cudaStream_t s);
+void launch_segmented_reduce(const uint32_t* sorted_keys, const uint32_t* perm,
+                             const double* values, long long nrec, double* grad_out_f64,
+                             cudaStream_t s);
+void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, long long v_end,
+                    double rho, double lr_sigma, double lr_sh, double eps,
+                    const MapStats* stats, cudaStream_t s);
+void launch_pose_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                         const double4* rgbd, const DevPose* pose, const int* pixels, int n,
+                         double4* ray_cd, uint8_t* flags, PoseCount* counts, int* err_flag,
+                         cudaStream_t s);
+void launch_pose_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                          const double4* rgbd, const DevPose* pose, const int* pixels, int n,
+                          const double4* ray_cd, const uint8_t* flags, double lambda_p,
+                          double lambda_d, PosePartial* partials, cudaStream_t s);
+int pose_backward_blocks(int n);
+void launch_pose_reduce(const PosePartial* partials, int nparts, PosePartial* out,
+                        cudaStream_t s);
+
+// Utilities.
+void launch_fill_payload(float* payload, long long n_vertices, float sigma, cudaStream_t s);
+void launch_f64_to_f32(const double* in, float* out, long long n, cudaStream_t s);
+void launch_f32_to_f64(const float* in, double* out, long long n, cudaStream_t s);
+void launch_pack_occupancy(const uint8_t* occ_u8, uint32_t* bits, long long n_cells,
+                           cudaStream_t s);
+void launch_unpack_occupancy(const uint32_t* bits, uint8_t* occ_u8, long long n_cells,
+                             cudaStream_t s);
+void launch_pack_frames(const double* color, const double* depth, double4* rgbd, long long npix,
+                        cudaStream_t s);
+void launch_prune(const DevGrid& g, uint32_t* occ_bits, double tau, unsigned long long* count,
+                  cudaStream_t s);
+
+}  // namespace vrf

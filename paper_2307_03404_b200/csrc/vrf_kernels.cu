@@ -1,0 +1,857 @@
+// sm_100a kernels of the per-ray hot path.
+//
+//   K1 k_render_image      render_image          renderer.cpp:149-174 (+51-140)
+//   K0+fwd k_map_forward   mapping_step pass 1+2 forward, hit counts M_c/M_d,
+//                          loss partials        mapping.cpp:130-200
+//   K2 k_map_backward      recompute-march + prefix-form dL/dsigma, dL/dc +
+//                          trilinear adjoint scatter (red.global.add.v4.f32)
+//                                                gradients.cpp:69-114, mapping.cpp:172-195
+//   K3 k_map_records +     deterministic mode: per-sample fp64 records, stable
+//      k_segmented_reduce  radix sort by vertex, in-order fp64 segment sums
+//                                                gradients.cpp:28-57 (sorted merge)
+//   K4 k_rmsprop           sparse RMSProp (skip g == 0), clears g   mapping.cpp:218-231
+//   K5 k_pose_forward/     per-ray 4x6 Jacobian of [C; D] w.r.t. [omega; tau] ->
+//      k_pose_backward     J^T J (21) + J^T r (6) + loss      gradients.cpp:116-143,
+//                                                tracking.cpp:104-130
+#include <climits>
+
+#include "vrf_internal.h"
+
+namespace vrf {
+
+namespace {
+
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ void ray_from_pixel(const DevCam& cam, const DevPose& pose, double u,
+                                               double v, March& m) {
+  generate_dir(cam, pose, u, v, m.d);
+  m.o[0] = pose.t[0];
+  m.o[1] = pose.t[1];
+  m.o[2] = pose.t[2];
+}
+
+// Forward render of one ray: composite until termination. Returns false if the
+// SH basis precondition fails (sh_eval throws, voxel_grid.cpp:35-36).
+template <typename ShT>
+__device__ __forceinline__ bool render_forward(const DevGrid& g, const DevParams& p, March& m,
+                                               Composite& st, double basis[9]) {
+  st.T = 1.0;
+  st.C[0] = st.C[1] = st.C[2] = 0.0;
+  st.D = 0.0;
+  st.count = 0;
+  st.terminated = false;
+  if (!sh_basis(m.d, basis)) return false;
+  if (!march_begin(g, p, m)) return true;
+  Sample s;
+  while (march_next(g, m, s)) {
+    double w[8];
+    corner_weights(s, w);
+    Shade sh;
+    shade<ShT>(g, s, w, basis, sh);
+    double decay;
+    composite_step(st, sh, s.t, s.delta, p.eps, decay);
+    if (st.terminated) break;
+  }
+  if (st.count == 0) {
+    st.C[0] = st.C[1] = st.C[2] = 0.0;
+    st.D = 0.0;
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------ K1
+template <typename ShT>
+__global__ void __launch_bounds__(kThreads) k_render_image(DevGrid g, DevParams p, DevCam cam,
+                                                           DevPose pose, int stride, int out_w,
+                                                           int out_h, double* __restrict__ color,
+                                                           double* __restrict__ depth,
+                                                           int* err) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)out_w * out_h) return;
+  const int px = (int)(idx % out_w), py = (int)(idx / out_w);
+  March m;
+  ray_from_pixel(cam, pose, (double)px * stride, (double)py * stride, m);
+  Composite st;
+  double basis[9];
+  if (!render_forward<ShT>(g, p, m, st, basis)) {
+    atomicOr(err, 1);
+    return;
+  }
+  color[idx * 3 + 0] = st.C[0];
+  color[idx * 3 + 1] = st.C[1];
+  color[idx * 3 + 2] = st.C[2];
+  depth[idx] = st.count > 0 ? st.D : 0.0;
+}
+
+// ------------------------------------------------------------------ inspection
+__global__ void __launch_bounds__(kThreads) k_debug_rays(DevGrid g, DevParams p,
+                                                         const double* __restrict__ rays, int n,
+                                                         int cap, int* counts, double* t,
+                                                         double* delta, uint32_t* cells,
+                                                         double* out, int* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  March m;
+  for (int a = 0; a < 3; ++a) {
+    m.o[a] = rays[6 * i + a];
+    m.d[a] = rays[6 * i + 3 + a];
+  }
+  if (counts) {  // sample_ray: the full schedule (no termination)
+    int c = 0;
+    if (march_begin(g, p, m)) {
+      Sample s;
+      while (march_next(g, m, s)) {
+        if (c < cap) {
+          t[(long long)i * cap + c] = s.t;
+          delta[(long long)i * cap + c] = s.delta;
+          cells[(long long)i * cap + c] = s.cell;
+        }
+        ++c;
+      }
+    }
+    counts[i] = c;
+  }
+  if (out) {  // render_ray
+    Composite st;
+    double basis[9];
+    if (!render_forward<double>(g, p, m, st, basis)) {
+      atomicOr(err, 1);
+      return;
+    }
+    double* o = out + 8 * (long long)i;
+    o[0] = st.C[0];
+    o[1] = st.C[1];
+    o[2] = st.C[2];
+    o[3] = st.D;
+    o[4] = st.T;
+    o[5] = st.count;
+    o[6] = st.count > 0;
+    o[7] = st.terminated;
+  }
+}
+
+// ------------------------------------------------------------------ block reductions
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  T r = T(0);
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += smem[w];  // fixed order
+  return r;  // valid in thread 0
+}
+
+__device__ __forceinline__ int block_min(int v, int* smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, off));
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  int r = INT_MAX;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = min(r, smem[w]);
+  return r;
+}
+
+// ------------------------------------------------------------------ K0 + mapping forward
+template <typename ShT>
+__global__ void __launch_bounds__(kThreads) k_map_forward(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
+    double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials,
+    int* __restrict__ ray_count, int* err) {
+  __shared__ double s_d[32];
+  __shared__ long long s_l[32];
+  __shared__ int s_i[32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double lp = 0.0, lg = 0.0;
+  long long samples = 0;
+  int mc = 0, md = 0, bad = INT_MAX;
+  if (i < n) {
+    const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
+    uint8_t fl = 0;
+    if (f < 0 || f >= n_frames || px < 0 || px >= cam.width || py < 0 || py >= cam.height) {
+      atomicOr(err, 2);  // generate_ray: pixel outside image
+    } else {
+      March m;
+      ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+      Composite st;
+      double basis[9];
+      if (!render_forward<ShT>(g, p, m, st, basis)) atomicOr(err, 1);
+      const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+      if (st.count > 0) {
+        fl |= kHit;
+        mc = 1;
+        samples = st.count;
+        const double r0 = dsub(st.C[0], tg.x), r1 = dsub(st.C[1], tg.y), r2 = dsub(st.C[2], tg.z);
+        const double sq = dadd(dadd(dmul(r0, r0), dmul(r1, r1)), dmul(r2, r2));
+        if (!isfinite(sq) || !isfinite(st.D)) {
+          bad = i;
+        } else {
+          lp = sq;
+          if (tg.w > 0.0) {
+            fl |= kDepthValid;
+            md = 1;
+            const double dr = dsub(st.D, tg.w);
+            lg = dmul(dr, dr);
+          }
+        }
+      }
+      ray_cd[i] = make_double4(st.C[0], st.C[1], st.C[2], st.D);
+    }
+    flags[i] = fl;
+    if (ray_count) ray_count[i] = (fl & kHit) ? (int)samples : 0;
+  }
+  const double blp = block_sum(lp, s_d);
+  const double blg = block_sum(lg, s_d);
+  const long long bs = block_sum(samples, s_l);
+  const int bmc = block_sum(mc, s_i);
+  const int bmd = block_sum(md, s_i);
+  const int bbad = block_min(bad, s_i);
+  if (threadIdx.x == 0) {
+    MapPartial q;
+    q.lp = blp;
+    q.lg = blg;
+    q.samples = bs;
+    q.m_c = bmc;
+    q.m_d = bmd;
+    q.bad = bbad;
+    q.pad = 0;
+    partials[blockIdx.x] = q;
+  }
+}
+
+// Fixed-order reduction of the per-block partials (deterministic).
+__global__ void __launch_bounds__(1024) k_map_reduce(const MapPartial* __restrict__ parts,
+                                                     int nparts, MapStats* out) {
+  __shared__ double s_d[32];
+  __shared__ long long s_l[32];
+  __shared__ int s_i[32];
+  double lp = 0.0, lg = 0.0;
+  long long samples = 0;
+  int mc = 0, md = 0, bad = INT_MAX;
+  for (int k = threadIdx.x; k < nparts; k += blockDim.x) {
+    const MapPartial q = parts[k];
+    lp += q.lp;
+    lg += q.lg;
+    samples += q.samples;
+    mc += q.m_c;
+    md += q.m_d;
+    bad = min(bad, q.bad);
+  }
+  const double blp = block_sum(lp, s_d);
+  const double blg = block_sum(lg, s_d);
+  const long long bs = block_sum(samples, s_l);
+  const int bmc = block_sum(mc, s_i);
+  const int bmd = block_sum(md, s_i);
+  const int bbad = block_min(bad, s_i);
+  if (threadIdx.x == 0) {
+    MapStats r;
+    r.lp = blp;
+    r.lg = blg;
+    r.samples = bs;
+    r.m_c = bmc;
+    r.m_d = bmd;
+    r.bad = bbad;
+    r.pad = 0;
+    *out = r;
+  }
+}
+
+// ------------------------------------------------------------------ K2 mapping backward
+// Per-sample upstream of the map-parameter gradient (gradients.cpp:69-114):
+// prefix-form dL/dsigma_i and dL/dc_i, gated by sigma_raw > 0 and the clamp flags.
+struct MapUp {
+  double upc[3];
+  double upd;
+  bool use_depth;
+  double C[3], D;
+};
+
+__device__ __forceinline__ bool map_upstream(const MapStats& st, const int* global_counts,
+                                             const double4 cd, const double4 tg, uint8_t fl,
+                                             double lambda_d, MapUp& u) {
+  const int mc = global_counts ? global_counts[0] : st.m_c;
+  const int md = global_counts ? global_counts[1] : st.m_d;
+  if (mc == 0) return false;
+  u.C[0] = cd.x;
+  u.C[1] = cd.y;
+  u.C[2] = cd.z;
+  u.D = cd.w;
+  const double tgc[3] = {tg.x, tg.y, tg.z};
+  for (int ch = 0; ch < 3; ++ch) u.upc[ch] = ddiv(dmul(2.0, dsub(u.C[ch], tgc[ch])), (double)mc);
+  const bool depth_ok = (fl & kDepthValid) && md > 0;
+  u.upd = depth_ok ? ddiv(dmul(dmul(lambda_d, 2.0), dsub(u.D, tg.w)), (double)md) : 0.0;
+  u.use_depth = depth_ok && u.upd != 0.0;
+  return true;
+}
+
+// Walks the samples of one ray again and hands each sample's 28-slot upstream
+// and corner weights to `emit`.
+template <typename ShT, typename Emit>
+__device__ __forceinline__ void map_backward_ray(const DevGrid& g, const DevParams& p, March& m,
+                                                 const MapUp& u, Emit&& emit) {
+  double basis[9];
+  if (!sh_basis(m.d, basis)) return;
+  if (!march_begin(g, p, m)) return;
+  double T = 1.0, prefix[3] = {0.0, 0.0, 0.0}, prefix_d = 0.0;
+  Sample s;
+  int idx = 0;
+  while (march_next(g, m, s)) {
+    double w[8];
+    corner_weights(s, w);
+    Shade sh;
+    shade<ShT>(g, s, w, basis, sh);
+    const double sigma = (sh.sigma_raw < 0.0) ? 0.0 : sh.sigma_raw;
+    const double decay = exp(dmul(-sigma, s.delta));
+    const double wgt = dmul(T, dsub(1.0, decay));
+    const double T_next = dmul(T, decay);
+    double ds = 0.0, dcol[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      prefix[ch] = dadd(prefix[ch], dmul(sh.c[ch], wgt));
+      dcol[ch] = dmul(u.upc[ch], wgt);
+      ds = dadd(ds, dmul(dmul(u.upc[ch], s.delta),
+                         dadd(dsub(dmul(sh.c[ch], T_next), u.C[ch]), prefix[ch])));
+    }
+    if (u.use_depth) {
+      prefix_d = dadd(prefix_d, dmul(s.t, wgt));
+      ds = dadd(ds, dmul(dmul(u.upd, s.delta), dadd(dsub(dmul(s.t, T_next), u.D), prefix_d)));
+    }
+    const double up0 = sh.sigma_raw > 0.0 ? ds : 0.0;
+    emit(idx, s, w, up0, dcol, sh.clamped, basis);
+    ++idx;
+    T = T_next;
+    if (T < p.eps) break;
+  }
+}
+
+template <typename ShT>
+__global__ void __launch_bounds__(kThreads) k_map_backward(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
+    const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
+    const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
+    float4* __restrict__ grad, double lambda_d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const MapStats st = *stats;
+  if (st.bad != INT_MAX) return;  // non-finite loss: the reference throws before updating
+  const uint8_t fl = flags[i];
+  if (!(fl & kHit)) return;
+  const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
+  const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+  MapUp u;
+  if (!map_upstream(st, global_counts, ray_cd[i], tg, fl, lambda_d, u)) return;
+  March m;
+  ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+  map_backward_ray<ShT>(g, p, m, u,
+                        [&](int, const Sample& s, const double w[8], double up0,
+                            const double dcol[3], const bool clamped[3], const double basis[9]) {
+                          float up[28];
+                          up[0] = (float)up0;
+                          bool any = up0 != 0.0;
+#pragma unroll
+                          for (int ch = 0; ch < 3; ++ch) {
+                            const bool live = !clamped[ch] && dcol[ch] != 0.0;
+                            any |= live;
+#pragma unroll
+                            for (int mm = 0; mm < 9; ++mm)
+                              up[1 + ch * 9 + mm] = live ? (float)dmul(dcol[ch], basis[mm]) : 0.f;
+                          }
+                          if (!any) return;
+#pragma unroll
+                          for (int k = 0; k < 8; ++k) {
+                            const float wk = (float)w[k];
+                            float4* dst = grad + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
+#pragma unroll
+                            for (int j = 0; j < kVec4PerVertex; ++j) {
+                              const float4 v = make_float4(wk * up[4 * j], wk * up[4 * j + 1],
+                                                           wk * up[4 * j + 2], wk * up[4 * j + 3]);
+                              atomicAdd(dst + j, v);  // red.global.add.v4.f32
+                            }
+                          }
+                        });
+}
+
+// ------------------------------------------------------------------ K3 deterministic records
+// One record per (sample, corner), in the reference's accumulation order
+// (ray, sample, corner). values: per sample 8 weights + 28 upstream slots (fp64).
+__global__ void __launch_bounds__(kThreads) k_map_records(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
+    const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
+    const MapStats* __restrict__ stats, double lambda_d, const long long* __restrict__ offsets,
+    uint32_t* __restrict__ keys, uint32_t* __restrict__ ids, double* __restrict__ values) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const MapStats st = *stats;
+  if (st.bad != INT_MAX) return;
+  const uint8_t fl = flags[i];
+  if (!(fl & kHit)) return;
+  const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
+  const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+  MapUp u;
+  if (!map_upstream(st, nullptr, ray_cd[i], tg, fl, lambda_d, u)) return;
+  March m;
+  ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+  const long long base = offsets[i];
+  map_backward_ray<double>(
+      g, p, m, u,
+      [&](int idx, const Sample& s, const double w[8], double up0, const double dcol[3],
+          const bool clamped[3], const double basis[9]) {
+        const long long sid = base + idx;
+        double* v = values + sid * 36;
+        for (int k = 0; k < 8; ++k) {
+          v[k] = w[k];
+          keys[sid * 8 + k] = corner_index(g, s.base, k);
+          ids[sid * 8 + k] = (uint32_t)(sid * 8 + k);
+        }
+        v[8] = up0;
+        for (int ch = 0; ch < 3; ++ch)
+          for (int mm = 0; mm < 9; ++mm)
+            v[9 + ch * 9 + mm] = clamped[ch] ? 0.0 : dmul(dcol[ch], basis[mm]);
+      });
+}
+
+// In-order fp64 sums over runs of equal vertex keys (GradientBuffer::add order).
+__global__ void __launch_bounds__(kThreads) k_segmented_reduce(
+    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rec, const double* __restrict__ values,
+    long long nrec, double* __restrict__ grad) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrec) return;
+  const uint32_t key = keys[r];
+  if (r > 0 && keys[r - 1] == key) return;  // not a segment head
+  double acc[28];
+#pragma unroll
+  for (int c = 0; c < 28; ++c) acc[c] = 0.0;
+  for (long long q = r; q < nrec && keys[q] == key; ++q) {
+    const uint32_t id = rec[q];
+    const double* v = values + (long long)(id >> 3) * 36;
+    const double wk = v[id & 7];
+#pragma unroll
+    for (int c = 0; c < 28; ++c) acc[c] = dadd(acc[c], dmul(wk, v[8 + c]));
+  }
+  double* dst = grad + (size_t)key * 28;
+#pragma unroll
+  for (int c = 0; c < 28; ++c) dst[c] = acc[c];
+}
+
+// ------------------------------------------------------------------ K4 RMSProp
+__global__ void __launch_bounds__(256) k_rmsprop(float4* __restrict__ theta,
+                                                 float4* __restrict__ grad,
+                                                 float4* __restrict__ vstate, long long f_begin,
+                                                 long long f_end, double rho, double lr_sigma,
+                                                 double lr_sh, double eps,
+                                                 const MapStats* __restrict__ stats) {
+  if (stats) {
+    const MapStats st = *stats;
+    if (st.bad != INT_MAX || st.m_c == 0) return;
+  }
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long f = f_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; f < f_end;
+       f += (long long)gridDim.x * blockDim.x) {
+    const float4 g4 = grad[f];
+    if (g4.x == 0.f && g4.y == 0.f && g4.z == 0.f && g4.w == 0.f) continue;
+    float4 th = theta[f], v4 = vstate[f];
+    const int j = (int)(f % kVec4PerVertex);
+    float* thp = &th.x;
+    float* vp = &v4.x;
+    const float* gp = &g4.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double gg = gp[e];
+      if (gg == 0.0) continue;  // mapping.cpp:226
+      const double vn = rho * (double)vp[e] + (1.0 - rho) * gg * gg;
+      const double lr = (4 * j + e == 0) ? lr_sigma : lr_sh;
+      vp[e] = (float)vn;
+      thp[e] = (float)((double)thp[e] - lr * gg / sqrt(vn + eps));
+    }
+    theta[f] = th;
+    vstate[f] = v4;
+    grad[f] = zero;
+  }
+}
+
+// ------------------------------------------------------------------ K5 pose
+__global__ void __launch_bounds__(kThreads) k_pose_forward(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ pose, const int* __restrict__ pixels, int n,
+    double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, PoseCount* counts, int* err) {
+  __shared__ long long s_l[32];
+  __shared__ int s_i[32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int hit = 0;
+  long long samples = 0;
+  if (i < n) {
+    const int px = pixels[2 * i], py = pixels[2 * i + 1];
+    uint8_t fl = 0;
+    if (px < 0 || px >= cam.width || py < 0 || py >= cam.height) {
+      atomicOr(err, 2);
+    } else {
+      March m;
+      ray_from_pixel(cam, *pose, (double)px, (double)py, m);
+      Composite st;
+      double basis[9];
+      if (!render_forward<double>(g, p, m, st, basis)) atomicOr(err, 1);
+      if (st.count > 0) {
+        fl = kHit;
+        hit = 1;
+        samples = st.count;
+      }
+      ray_cd[i] = make_double4(st.C[0], st.C[1], st.C[2], st.D);
+    }
+    flags[i] = fl;
+  }
+  const int bh = block_sum(hit, s_i);
+  const long long bs = block_sum(samples, s_l);
+  if (threadIdx.x == 0) {
+    atomicAdd(&counts->m, bh);
+    atomicAdd((unsigned long long*)&counts->samples, (unsigned long long)bs);
+  }
+}
+
+// Per ray: 4 residual rows (r, g, b, depth), each a 6-vector [omega; tau], from
+// grad_wrt_ray with unit upstreams; spatial gradients contracted per corner.
+__global__ void __launch_bounds__(kThreads) k_pose_backward(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ pose, const int* __restrict__ pixels, int n,
+    const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags, double lambda_p,
+    double lambda_d, PosePartial* partials) {
+  __shared__ double s_d[32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double jtj[21], jtr[6], loss = 0.0;
+#pragma unroll
+  for (int k = 0; k < 21; ++k) jtj[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) jtr[k] = 0.0;
+  if (i < n && (flags[i] & kHit)) {
+    const int px = pixels[2 * i], py = pixels[2 * i + 1];
+    const double4 tg = rgbd[(long long)py * cam.width + px];
+    const double4 cd = ray_cd[i];
+    const double C[3] = {cd.x, cd.y, cd.z}, D = cd.w;
+    const double res[4] = {dsub(C[0], tg.x), dsub(C[1], tg.y), dsub(C[2], tg.z), dsub(D, tg.w)};
+    loss = dadd(dmul(lambda_p, dadd(dadd(dmul(res[0], res[0]), dmul(res[1], res[1])),
+                                    dmul(res[2], res[2]))),
+                dmul(dmul(lambda_d, res[3]), res[3]));
+    March m;
+    ray_from_pixel(cam, *pose, (double)px, (double)py, m);
+    double basis[9];
+    double Jo[4][3], Jd[4][3];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = 0.0;
+    if (sh_basis(m.d, basis) && march_begin(g, p, m)) {
+      double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
+      const double sgn[2] = {-1.0, 1.0};
+      Sample s;
+      while (march_next(g, m, s)) {
+        double w[8];
+        corner_weights(s, w);
+        Shade sh;
+        shade<double>(g, s, w, basis, sh);
+        const double sigma = (sh.sigma_raw < 0.0) ? 0.0 : sh.sigma_raw;
+        const double decay = exp(dmul(-sigma, s.delta));
+        const double wgt = dmul(T, dsub(1.0, decay));
+        const double T_next = dmul(T, decay);
+        double dsig[4];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          prefix[ch] = dadd(prefix[ch], dmul(sh.c[ch], wgt));
+          dsig[ch] = dmul(s.delta, dadd(dsub(dmul(sh.c[ch], T_next), C[ch]), prefix[ch]));
+        }
+        prefix_d = dadd(prefix_d, dmul(s.t, wgt));
+        dsig[3] = dmul(s.delta, dadd(dsub(dmul(s.t, T_next), D), prefix_d));
+        // Spatial gradients of sigma and of the three basis-contracted SH channels
+        // (voxel_grid.cpp:130-151), 8 corners.
+        const double wx[2] = {dsub(1.0, s.fx), s.fx}, wy[2] = {dsub(1.0, s.fy), s.fy},
+                     wz[2] = {dsub(1.0, s.fz), s.fz};
+        double Gs[3] = {0, 0, 0}, Gc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {
+          const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+          const double dw[3] = {dmul(dmul(dmul(sgn[dx], wy[dy]), wz[dz]), g.inv_voxel),
+                                dmul(dmul(dmul(wx[dx], sgn[dy]), wz[dz]), g.inv_voxel),
+                                dmul(dmul(dmul(wx[dx], wy[dy]), sgn[dz]), g.inv_voxel)};
+          const float* vp = (const float*)(g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex);
+          const double v0 = (double)__ldg(vp);
+          double shd[3];
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            double acc = 0.0;
+#pragma unroll
+            for (int mm = 0; mm < 9; ++mm) acc = fma(basis[mm], (double)__ldg(vp + 1 + ch * 9 + mm), acc);
+            shd[ch] = acc;
+          }
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            Gs[a] = fma(dw[a], v0, Gs[a]);
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) Gc[ch][a] = fma(dw[a], shd[ch], Gc[ch][a]);
+          }
+        }
+        const bool sgate = sh.sigma_raw > 0.0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            double gv = sgate ? dsig[r] * Gs[a] : 0.0;
+            if (r < 3 && !sh.clamped[r]) gv += wgt * Gc[r][a];
+            Jo[r][a] += gv;
+            Jd[r][a] = fma(s.t, gv, Jd[r][a]);
+          }
+        }
+        T = T_next;
+        if (T < p.eps) break;
+      }
+    }
+    // Chart (tracking.cpp:125-128): tau <- dL/do, omega <- d x (dL/dd - d (d.dL/dd)).
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double dd = dot3(m.d, Jd[r]);
+      double gp[3], om[3];
+      for (int a = 0; a < 3; ++a) gp[a] = Jd[r][a] - m.d[a] * dd;
+      cross3(m.d, gp, om);
+      const double J[6] = {om[0], om[1], om[2], Jo[r][0], Jo[r][1], Jo[r][2]};
+      const double lam = r < 3 ? lambda_p : lambda_d;
+      int idx = 0;
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+#pragma unroll
+        for (int b = a; b < 6; ++b) jtj[idx++] += lam * J[a] * J[b];
+        jtr[a] += lam * J[a] * res[r];
+      }
+    }
+  }
+  // Block reduction (fixed order) -> per-block partial.
+  PosePartial* out = partials + blockIdx.x;
+#pragma unroll 1
+  for (int k = 0; k < 21; ++k) {
+    const double v = block_sum(jtj[k], s_d);
+    if (threadIdx.x == 0) out->jtj[k] = v;
+  }
+#pragma unroll 1
+  for (int k = 0; k < 6; ++k) {
+    const double v = block_sum(jtr[k], s_d);
+    if (threadIdx.x == 0) out->jtr[k] = v;
+  }
+  const double bl = block_sum(loss, s_d);
+  if (threadIdx.x == 0) {
+    out->loss = bl;
+    out->samples = 0;
+    out->m = 0;
+    out->bad = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_pose_reduce(const PosePartial* __restrict__ parts,
+                                                     int nparts, PosePartial* out) {
+  // 28 values; thread v sums value v over the partials in order (deterministic).
+  const int v = threadIdx.x;
+  if (v >= 28) return;
+  double acc = 0.0;
+  for (int k = 0; k < nparts; ++k) {
+    const PosePartial& q = parts[k];
+    acc += v < 21 ? q.jtj[v] : (v < 27 ? q.jtr[v - 21] : q.loss);
+  }
+  if (v < 21)
+    out->jtj[v] = acc;
+  else if (v < 27)
+    out->jtr[v - 21] = acc;
+  else
+    out->loss = acc;
+}
+
+// ------------------------------------------------------------------ utilities
+__global__ void k_fill_payload(float* payload, long long nv, float sigma) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nv * kPayload;
+       e += (long long)gridDim.x * blockDim.x)
+    payload[e] = (e % kPayload == 0) ? sigma : 0.f;
+}
+__global__ void k_f64_to_f32(const double* in, float* out, long long n) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = (float)in[e];
+}
+__global__ void k_f32_to_f64(const float* in, double* out, long long n) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = (double)in[e];
+}
+__global__ void k_pack_occupancy(const uint8_t* occ, uint32_t* bits, long long n_cells) {
+  const long long wd = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (wd * 32 >= n_cells) return;
+  uint32_t b = 0;
+  for (int k = 0; k < 32; ++k) {
+    const long long c = wd * 32 + k;
+    if (c < n_cells && occ[c]) b |= 1u << k;
+  }
+  bits[wd] = b;
+}
+__global__ void k_unpack_occupancy(const uint32_t* bits, uint8_t* occ, long long n_cells) {
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells;
+       c += (long long)gridDim.x * blockDim.x)
+    occ[c] = (bits[c >> 5] >> (c & 31)) & 1u;
+}
+__global__ void k_pack_frames(const double* color, const double* depth, double4* rgbd,
+                              long long npix) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < npix;
+       q += (long long)gridDim.x * blockDim.x)
+    rgbd[q] = make_double4(color[3 * q], color[3 * q + 1], color[3 * q + 2], depth[q]);
+}
+// VoxelGrid::prune — voxel_grid.cpp:169-188 (peak of max(sigma,0) over 8 corners < tau).
+__global__ void k_prune(DevGrid g, uint32_t* bits, double tau, unsigned long long* count) {
+  const long long n_cells = (long long)(g.rx - 1) * (g.ry - 1) * (g.rz - 1);
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells;
+       c += (long long)gridDim.x * blockDim.x) {
+    if (!((bits[c >> 5] >> (c & 31)) & 1u)) continue;
+    const int cx = (int)(c % (g.rx - 1));
+    const long long r = c / (g.rx - 1);
+    const int cy = (int)(r % (g.ry - 1)), cz = (int)(r / (g.ry - 1));
+    const uint32_t base = (uint32_t)(cx + g.rx * (cy + (long long)g.ry * cz));
+    double peak = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      const double s = (double)((const float*)g.payload)[(size_t)corner_index(g, base, k) * kPayload];
+      const double sp = (s < 0.0) ? 0.0 : s;
+      peak = (peak < sp) ? sp : peak;
+    }
+    if (peak < tau) {
+      atomicAnd(bits + (c >> 5), ~(1u << (c & 31)));
+      atomicAdd(count, 1ull);
+    }
+  }
+}
+
+int grid_blocks(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  if (b > 148LL * 32) b = 148LL * 32;
+  return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+void launch_render_image(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                         const DevPose& pose, int stride, int out_w, int out_h, double* color,
+                         double* depth, int* err, cudaStream_t s) {
+  const long long n = (long long)out_w * out_h;
+  if (n == 0) return;
+  k_render_image<double><<<(unsigned)((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+      g, p, cam, pose, stride, out_w, out_h, color, depth, err);
+}
+void launch_debug_rays(const DevGrid& g, const DevParams& p, const double* rays, int n, int cap,
+                       int* counts, double* t, double* delta, uint32_t* cells, double* out,
+                       int* err, cudaStream_t s) {
+  if (n == 0) return;
+  k_debug_rays<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(g, p, rays, n, cap, counts, t,
+                                                                   delta, cells, out, err);
+}
+int map_forward_blocks(int n) { return (n + kThreads - 1) / kThreads; }
+void launch_map_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                        const double4* rgbd, const DevPose* poses, int n_frames,
+                        const int* batch, int n, double4* ray_cd, uint8_t* flags,
+                        MapPartial* partials, int* ray_count, int* err, bool fast,
+                        cudaStream_t s) {
+  const int blocks = map_forward_blocks(n);
+  if (fast)
+    k_map_forward<float><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, n_frames, batch, n,
+                                                     ray_cd, flags, partials, ray_count, err);
+  else
+    k_map_forward<double><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, n_frames, batch, n,
+                                                      ray_cd, flags, partials, ray_count, err);
+}
+void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s) {
+  k_map_reduce<<<1, 1024, 0, s>>>(partials, nparts, out);
+}
+void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                         const double4* rgbd, const DevPose* poses, const int* batch, int n,
+                         const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
+                         const int* global_counts, float4* grad, double lambda_d, bool fast,
+                         cudaStream_t s) {
+  const int blocks = (n + kThreads - 1) / kThreads;
+  if (fast)
+    k_map_backward<float><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
+                                                      flags, stats, global_counts, grad, lambda_d);
+  else
+    k_map_backward<double><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
+                                                       flags, stats, global_counts, grad,
+                                                       lambda_d);
+}
+void launch_map_backward_records(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                                 const double4* rgbd, const DevPose* poses, const int* batch,
+                                 int n, const double4* ray_cd, const uint8_t* flags,
+                                 const MapStats* stats, double lambda_d,
+                                 const long long* offsets, uint32_t* keys, uint32_t* ids,
+                                 double* values, cudaStream_t s) {
+  k_map_records<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
+      g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, lambda_d, offsets, keys, ids,
+      values);
+}
+void launch_segmented_reduce(const uint32_t* keys, const uint32_t* perm, const double* values,
+                             long long nrec, double* grad, cudaStream_t s) {
+  if (nrec == 0) return;
+  k_segmented_reduce<<<(unsigned)((nrec + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+      keys, perm, values, nrec, grad);
+}
+void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, long long v_end,
+                    double rho, double lr_sigma, double lr_sh, double eps,
+                    const MapStats* stats, cudaStream_t s) {
+  const long long f0 = v_begin * kVec4PerVertex, f1 = v_end * kVec4PerVertex;
+  if (f1 <= f0) return;
+  k_rmsprop<<<grid_blocks(f1 - f0, 256), 256, 0, s>>>(theta, grad, v, f0, f1, rho, lr_sigma,
+                                                      lr_sh, eps, stats);
+}
+void launch_pose_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                         const double4* rgbd, const DevPose* pose, const int* pixels, int n,
+                         double4* ray_cd, uint8_t* flags, PoseCount* counts, int* err,
+                         cudaStream_t s) {
+  k_pose_forward<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(g, p, cam, rgbd, pose, pixels,
+                                                                    n, ray_cd, flags, counts, err);
+}
+int pose_backward_blocks(int n) { return (n + kThreads - 1) / kThreads; }
+void launch_pose_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                          const double4* rgbd, const DevPose* pose, const int* pixels, int n,
+                          const double4* ray_cd, const uint8_t* flags, double lambda_p,
+                          double lambda_d, PosePartial* partials, cudaStream_t s) {
+  k_pose_backward<<<pose_backward_blocks(n), kThreads, 0, s>>>(
+      g, p, cam, rgbd, pose, pixels, n, ray_cd, flags, lambda_p, lambda_d, partials);
+}
+void launch_pose_reduce(const PosePartial* partials, int nparts, PosePartial* out,
+                        cudaStream_t s) {
+  k_pose_reduce<<<1, 32, 0, s>>>(partials, nparts, out);
+}
+void launch_fill_payload(float* payload, long long nv, float sigma, cudaStream_t s) {
+  k_fill_payload<<<grid_blocks(nv * kPayload, 256), 256, 0, s>>>(payload, nv, sigma);
+}
+void launch_f64_to_f32(const double* in, float* out, long long n, cudaStream_t s) {
+  if (n) k_f64_to_f32<<<grid_blocks(n, 256), 256, 0, s>>>(in, out, n);
+}
+void launch_f32_to_f64(const float* in, double* out, long long n, cudaStream_t s) {
+  if (n) k_f32_to_f64<<<grid_blocks(n, 256), 256, 0, s>>>(in, out, n);
+}
+void launch_pack_occupancy(const uint8_t* occ, uint32_t* bits, long long n_cells,
+                           cudaStream_t s) {
+  const long long words = (n_cells + 31) / 32;
+  if (words) k_pack_occupancy<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(occ, bits, n_cells);
+}
+void launch_unpack_occupancy(const uint32_t* bits, uint8_t* occ, long long n_cells,
+                             cudaStream_t s) {
+  if (n_cells) k_unpack_occupancy<<<grid_blocks(n_cells, 256), 256, 0, s>>>(bits, occ, n_cells);
+}
+void launch_pack_frames(const double* color, const double* depth, double4* rgbd, long long npix,
+                        cudaStream_t s) {
+  if (npix) k_pack_frames<<<grid_blocks(npix, 256), 256, 0, s>>>(color, depth, rgbd, npix);
+}
+void launch_prune(const DevGrid& g, uint32_t* bits, double tau, unsigned long long* count,
+                  cudaStream_t s) {
+  const long long n_cells = (long long)(g.rx - 1) * (g.ry - 1) * (g.rz - 1);
+  k_prune<<<grid_blocks(n_cells, 256), 256, 0, s>>>(g, bits, tau, count);
+}
+
+}  // namespace vrf

@@ -1,0 +1,344 @@
+// Mapping entry points of the C-ABI: mapping_step (mapping.cpp:114-233) on the
+// device, its deterministic sorted/segmented-reduce variant, and the phases the
+// multi-GPU driver composes with NCCL collectives.
+#include <cub/cub.cuh>
+
+#include "vrf_context.h"
+
+using namespace vrf;
+using namespace vrf_host;
+
+namespace {
+
+int validate_batch(vrf_context* ctx, const int32_t* batch, int n) {
+  // mapping.cpp:121-128 draws frame < K, px < W, py < H; anything else would make
+  // generate_ray throw std::out_of_range (camera.hpp:38-39).
+  for (int i = 0; i < n; ++i) {
+    const int32_t f = batch[3 * i], x = batch[3 * i + 1], y = batch[3 * i + 2];
+    if (f < 0 || f >= ctx->n_frames)
+      return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "mapping_step: keyframe index out of range");
+    if (x < 0 || x >= ctx->fintr.width || y < 0 || y >= ctx->fintr.height)
+      return set_err(ctx, VRF_ERR_OUT_OF_RANGE, "generate_ray: pixel outside image");
+  }
+  return VRF_OK;
+}
+
+int upload_batch(vrf_context* ctx, const int32_t* batch, int n, const int** dev) {
+  int rc = validate_batch(ctx, batch, n);
+  if (rc) return rc;
+  const size_t bytes = sizeof(int32_t) * 3 * (size_t)(n > 0 ? n : 1);
+  if ((rc = ensure(ctx, ctx->s_batch, bytes))) return rc;
+  if ((rc = ensure_pinned(ctx, bytes))) return rc;
+  if (n > 0) {
+    std::memcpy(ctx->h_pinned, batch, sizeof(int32_t) * 3 * (size_t)n);
+    CU(cudaMemcpyAsync(ctx->s_batch.ptr, ctx->h_pinned, sizeof(int32_t) * 3 * (size_t)n,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  }
+  *dev = (const int*)ctx->s_batch.ptr;
+  return VRF_OK;
+}
+
+int read_stats(vrf_context* ctx, MapStats* st) {
+  CU(cudaMemcpyAsync(st, ctx->d_stats, sizeof(MapStats), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+// MapStepStats + the reference's exceptions (mapping.cpp:117, 152, 198-203, 213-216).
+int finish_stats(vrf_context* ctx, const vrf_mapping_config* cfg, const MapStats& st,
+                 const int* batch_host, vrf_map_step_stats* out) {
+  vrf_map_step_stats s{};
+  s.rays_color = st.m_c;
+  s.rays_depth = st.m_d;
+  s.samples = st.samples;
+  s.bad_ray = st.bad == INT_MAX ? -1 : st.bad;
+  if (out) *out = s;
+  if (st.m_c == 0) return set_err(ctx, VRF_ERR_RUNTIME, "mapping_step: no ray hit the grid");
+  if (st.bad != INT_MAX) {
+    std::string msg = "mapping_step: non-finite loss";
+    if (batch_host) {
+      const int* b = batch_host + 3 * st.bad;
+      msg += " at keyframe " + std::to_string(b[0]) + " pixel (" + std::to_string(b[1]) + "," +
+             std::to_string(b[2]) + ")";
+    }
+    return set_err(ctx, VRF_ERR_RUNTIME, msg);
+  }
+  s.loss_photometric = st.lp / double(st.m_c);
+  s.loss_geometric = st.m_d > 0 ? st.lg / double(st.m_d) : 0.0;
+  s.loss_total = s.loss_photometric + cfg->lambda_d * s.loss_geometric;
+  s.psnr_estimate = psnr_from_lp(s.loss_photometric);
+  if (out) *out = s;
+  return VRF_OK;
+}
+
+// K3: deterministic fp64 gradient into s_grad64 [V][28], summed per vertex in
+// the reference's order (ray, sample, corner) — GradientBuffer::add with one
+// worker (gradients.cpp:28-41, mapping.cpp:205-207). Needs the forward state
+// (ray_cd, flags, per-ray counts in s_count) and the host copy of the stats.
+int grad_deterministic(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev,
+                       int n, const MapStats& st) {
+  DevParams p;
+  int rc = resolve_params(ctx, &cfg->render, &p);
+  if (rc) return rc;
+  if ((rc = ensure(ctx, ctx->s_grad64, sizeof(double) * 28 * (size_t)ctx->V))) return rc;
+  CU(cudaMemsetAsync(ctx->s_grad64.ptr, 0, sizeof(double) * 28 * (size_t)ctx->V, ctx->stream));
+  if (st.m_c == 0 || st.bad != INT_MAX || st.samples == 0) return VRF_OK;
+  const long long S = st.samples, R = 8 * S;
+  if (R >= 0x7FFFFFFFLL)
+    return set_err(ctx, VRF_ERR_RUNTIME, "deterministic mapping: batch has too many samples");
+  if ((rc = ensure(ctx, ctx->s_offsets, sizeof(long long) * (n + 1)))) return rc;
+  long long* offsets = (long long*)ctx->s_offsets.ptr;
+  size_t tmp_scan = 0, tmp_sort = 0;
+  CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, (const int*)ctx->s_count.ptr, offsets, n,
+                                   ctx->stream));
+  CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, (const uint32_t*)nullptr,
+                                     (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                     (uint32_t*)nullptr, (int)R, 0, 32, ctx->stream));
+  if ((rc = ensure(ctx, ctx->s_cub, std::max(tmp_scan, tmp_sort)))) return rc;
+  CU(cub::DeviceScan::ExclusiveSum(ctx->s_cub.ptr, tmp_scan, (const int*)ctx->s_count.ptr,
+                                   offsets, n, ctx->stream));
+  LAUNCHED(1);
+  if ((rc = ensure(ctx, ctx->s_keys, sizeof(uint32_t) * R))) return rc;
+  if ((rc = ensure(ctx, ctx->s_keys2, sizeof(uint32_t) * R))) return rc;
+  if ((rc = ensure(ctx, ctx->s_ids, sizeof(uint32_t) * R))) return rc;
+  if ((rc = ensure(ctx, ctx->s_ids2, sizeof(uint32_t) * R))) return rc;
+  if ((rc = ensure(ctx, ctx->s_values, sizeof(double) * 36 * S))) return rc;
+  launch_map_backward_records(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
+                              batch_dev, n, (const double4*)ctx->s_raycd.ptr,
+                              (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, cfg->lambda_d,
+                              offsets, (uint32_t*)ctx->s_keys.ptr, (uint32_t*)ctx->s_ids.ptr,
+                              (double*)ctx->s_values.ptr, ctx->stream);
+  LAUNCHED(1);
+  // LSD radix sort is stable: equal vertices keep (ray, sample, corner) order.
+  CU(cub::DeviceRadixSort::SortPairs(ctx->s_cub.ptr, tmp_sort, (const uint32_t*)ctx->s_keys.ptr,
+                                     (uint32_t*)ctx->s_keys2.ptr, (const uint32_t*)ctx->s_ids.ptr,
+                                     (uint32_t*)ctx->s_ids2.ptr, (int)R, 0, 32, ctx->stream));
+  LAUNCHED(1);
+  launch_segmented_reduce((const uint32_t*)ctx->s_keys2.ptr, (const uint32_t*)ctx->s_ids2.ptr,
+                          (const double*)ctx->s_values.ptr, R, (double*)ctx->s_grad64.ptr,
+                          ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  return VRF_OK;
+}
+
+// Fills ctx->grad (fp32) with this batch's gradient. Deterministic mode goes
+// through the sorted fp64 reduce, then rounds once to fp32.
+int map_gradient(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev, int n,
+                 MapStats* st_out, bool need_host_stats) {
+  const bool det = cfg->deterministic != 0;
+  int rc = map_forward_dev(ctx, cfg, batch_dev, n, /*fast=*/!det,
+                           det ? (int*)nullptr : (int*)nullptr);
+  if (rc) return rc;
+  if (!det) {
+    DevParams p;
+    if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
+    if (n > 0) {
+      launch_map_backward(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
+                          batch_dev, n, (const double4*)ctx->s_raycd.ptr,
+                          (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, nullptr,
+                          (float4*)ctx->grad, cfg->lambda_d, /*fast=*/true, ctx->stream);
+      LAUNCHED(1);
+    }
+    CU(cudaGetLastError());
+    if (need_host_stats && (rc = read_stats(ctx, st_out))) return rc;
+    return VRF_OK;
+  }
+  return VRF_OK;
+}
+
+int check_ready(vrf_context* ctx) {
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if (ctx->n_frames == 0) return set_err(ctx, VRF_ERR_RUNTIME, "mapping_step: no keyframes");
+  return VRF_OK;
+}
+
+// Deterministic forward: also records per-ray counts (s_count) for the offsets.
+int det_forward(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev, int n,
+                MapStats* st) {
+  int rc = ensure(ctx, ctx->s_count, sizeof(int) * (size_t)(n > 0 ? n : 1));
+  if (rc) return rc;
+  if ((rc = map_forward_dev(ctx, cfg, batch_dev, n, /*fast=*/false, (int*)ctx->s_count.ptr)))
+    return rc;
+  if ((rc = check_err_flag(ctx))) return rc;
+  return read_stats(ctx, st);
+}
+
+int step_impl(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev,
+              const int32_t* batch_host, int n, vrf_map_step_stats* out) {
+  cudaSetDevice(ctx->device);
+  int rc;
+  MapStats st;
+  if (cfg->deterministic) {
+    if ((rc = det_forward(ctx, cfg, batch_dev, n, &st))) return rc;
+    if ((rc = grad_deterministic(ctx, cfg, batch_dev, n, st))) return rc;
+    launch_f64_to_f32((const double*)ctx->s_grad64.ptr, ctx->grad, ctx->V * 28, ctx->stream);
+    LAUNCHED(1);
+  } else {
+    if ((rc = map_gradient(ctx, cfg, batch_dev, n, &st, false))) return rc;
+  }
+  // K4: RMSProp over every vertex (skip g == 0 == the reference's touched set).
+  launch_rmsprop((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, 0, ctx->V,
+                 cfg->rmsprop_decay, cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, ctx->d_stats,
+                 ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  if ((rc = check_err_flag(ctx))) return rc;
+  if ((rc = read_stats(ctx, &st))) return rc;
+  if (st.m_c == 0 || st.bad != INT_MAX) {
+    // No update happened (k_rmsprop gated on the stats) — clear the gradient.
+    CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * (size_t)ctx->Vpad, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  return finish_stats(ctx, cfg, st, batch_host, out);
+}
+
+}  // namespace
+
+extern "C" {
+
+int vrf_mapping_step(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* batch,
+                     int n_rays, vrf_map_step_stats* out) {
+  cudaSetDevice(ctx->device);
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  const int* dev = nullptr;
+  if ((rc = upload_batch(ctx, batch, n_rays, &dev))) return rc;
+  return step_impl(ctx, cfg, dev, batch, n_rays, out);
+}
+
+int vrf_mapping_step_device(vrf_context* ctx, const vrf_mapping_config* cfg,
+                            const int32_t* batch_dev, int n_rays, vrf_map_step_stats* out) {
+  cudaSetDevice(ctx->device);
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  return step_impl(ctx, cfg, batch_dev, nullptr, n_rays, out);
+}
+
+int vrf_mapping_gradient(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* batch,
+                         int n_rays, double* grad_out, vrf_map_step_stats* out) {
+  cudaSetDevice(ctx->device);
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  const int* dev = nullptr;
+  if ((rc = upload_batch(ctx, batch, n_rays, &dev))) return rc;
+  MapStats st;
+  if (cfg->deterministic) {
+    if ((rc = det_forward(ctx, cfg, dev, n_rays, &st))) return rc;
+    if ((rc = grad_deterministic(ctx, cfg, dev, n_rays, st))) return rc;
+  } else {
+    if ((rc = map_gradient(ctx, cfg, dev, n_rays, &st, false))) return rc;
+    if ((rc = ensure(ctx, ctx->s_grad64, sizeof(double) * 28 * (size_t)ctx->V))) return rc;
+    launch_f32_to_f64(ctx->grad, (double*)ctx->s_grad64.ptr, ctx->V * 28, ctx->stream);
+    LAUNCHED(1);
+    CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * (size_t)ctx->Vpad, ctx->stream));
+  }
+  if ((rc = check_err_flag(ctx))) return rc;
+  if ((rc = read_stats(ctx, &st))) return rc;
+  if ((rc = finish_stats(ctx, cfg, st, batch, out))) return rc;
+  CU(cudaMemcpyAsync(grad_out, ctx->s_grad64.ptr, sizeof(double) * 28 * (size_t)ctx->V,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_rmsprop_reset(vrf_context* ctx) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  CU(cudaMemsetAsync(ctx->rms, 0, sizeof(float) * 28 * (size_t)ctx->Vpad, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_rmsprop_download(vrf_context* ctx, double* v) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if ((rc = ensure(ctx, ctx->s_grad64, sizeof(double) * 28 * (size_t)ctx->V))) return rc;
+  launch_f32_to_f64(ctx->rms, (double*)ctx->s_grad64.ptr, ctx->V * 28, ctx->stream);
+  LAUNCHED(1);
+  CU(cudaMemcpyAsync(v, ctx->s_grad64.ptr, sizeof(double) * 28 * (size_t)ctx->V,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_rmsprop_upload(vrf_context* ctx, const double* v) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  const long long total = ctx->V * 28, chunk = 4LL << 20;
+  if ((rc = ensure(ctx, ctx->s_out, sizeof(double) * chunk))) return rc;
+  for (long long off = 0; off < total; off += chunk) {
+    const long long n = std::min(chunk, total - off);
+    CU(cudaMemcpyAsync(ctx->s_out.ptr, v + off, sizeof(double) * n, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    launch_f64_to_f32((const double*)ctx->s_out.ptr, ctx->rms + off, n, ctx->stream);
+    LAUNCHED(1);
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+// ---- multi-GPU phases (the caller owns the collectives)
+int vrf_map_forward(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* batch_dev,
+                    int n_rays, vrf_map_partials* out) {
+  cudaSetDevice(ctx->device);
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  if ((rc = map_forward_dev(ctx, cfg, batch_dev, n_rays, /*fast=*/true))) return rc;
+  if ((rc = check_err_flag(ctx))) return rc;
+  MapStats st;
+  if ((rc = read_stats(ctx, &st))) return rc;
+  ctx->last_batch = batch_dev;
+  ctx->last_n = n_rays;
+  out->rays_color = st.m_c;
+  out->rays_depth = st.m_d;
+  out->sum_photometric = st.lp;
+  out->sum_geometric = st.lg;
+  out->samples = st.samples;
+  out->bad_ray = st.bad == INT_MAX ? -1 : st.bad;
+  out->reserved = 0;
+  return VRF_OK;
+}
+
+int vrf_map_backward(vrf_context* ctx, const vrf_mapping_config* cfg, int32_t rays_color,
+                     int32_t rays_depth) {
+  cudaSetDevice(ctx->device);
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  if (!ctx->last_batch) return set_err(ctx, VRF_ERR_RUNTIME, "vrf_map_backward: no forward pass");
+  DevParams p;
+  if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
+  const int counts[2] = {rays_color, rays_depth};
+  CU(cudaMemcpyAsync(ctx->d_counts, counts, sizeof(counts), cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->last_n > 0) {
+    launch_map_backward(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
+                        ctx->last_batch, ctx->last_n, (const double4*)ctx->s_raycd.ptr,
+                        (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, ctx->d_counts,
+                        (float4*)ctx->grad, cfg->lambda_d, /*fast=*/true, ctx->stream);
+    LAUNCHED(1);
+  }
+  CU(cudaGetLastError());
+  return VRF_OK;
+}
+
+int vrf_map_apply(vrf_context* ctx, const vrf_mapping_config* cfg, int64_t vertex_begin,
+                  int64_t vertex_end) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if (vertex_begin < 0 || vertex_end > ctx->Vpad || vertex_begin > vertex_end)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_map_apply: bad vertex range");
+  const int64_t end = std::min<int64_t>(vertex_end, ctx->V);
+  launch_rmsprop((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, vertex_begin,
+                 end, cfg->rmsprop_decay, cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, nullptr,
+                 ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  return VRF_OK;
+}
+
+}  // extern "C"

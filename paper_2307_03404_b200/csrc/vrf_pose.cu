@@ -1,0 +1,431 @@
+// Tracking entry points of the C-ABI: pose_gradient (tracking.cpp:76-143), the
+// Gauss-Newton normal equations, track_frame with the reference's Adam loop
+// (tracking.cpp:170-252) and a Gauss-Newton/LM tracker.
+#include "vrf_context.h"
+
+using namespace vrf;
+using namespace vrf_host;
+
+namespace {
+
+// ---- rng.hpp:13-81 (xoshiro256** seeded through splitmix64): the reference's
+// pixel-draw stream, reproduced on the host so track_frame draws the same pixels.
+struct Xoshiro {
+  uint64_t s[4];
+  static uint64_t splitmix(uint64_t& x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  explicit Xoshiro(uint64_t seed) {
+    uint64_t x = seed;
+    for (auto& w : s) w = splitmix(x);
+  }
+  static uint64_t rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
+  uint64_t next() {
+    const uint64_t r = rotl(s[1] * 5, 7) * 9;
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return r;
+  }
+  uint64_t index(uint64_t n) { return (uint64_t)(((unsigned __int128)next() * n) >> 64); }
+};
+
+// tracking.cpp:147-166
+void draw_valid_pixels(const std::vector<double>& depth, int w, int h, int count, int max_redraws,
+                       Xoshiro& rng, std::vector<int32_t>& out) {
+  out.clear();
+  for (int i = 0; i < count; ++i) {
+    int px = 0, py = 0;
+    bool ok = false;
+    for (int a = 0; a < max_redraws; ++a) {
+      px = (int)rng.index((uint64_t)w);
+      py = (int)rng.index((uint64_t)h);
+      if (depth[(size_t)py * w + px] > 0.0) {
+        ok = true;
+        break;
+      }
+    }
+    if (ok) {
+      out.push_back(px);
+      out.push_back(py);
+    }
+  }
+}
+
+struct PoseResult {
+  double jtj[21], jtr[6], loss;
+  int m;
+  long long samples;
+};
+
+int pose_pass(vrf_context* ctx, int frame, const vrf_intrinsics* intr, const vrf_pose* pose,
+              const int32_t* pixels, int n, const vrf_tracking_loss* cfg, PoseResult* res) {
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if (frame < 0 || frame >= ctx->n_frames)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "pose_gradient: frame index out of range");
+  if ((rc = check_frames(ctx, intr))) return rc;
+  if (n <= 0) return set_err(ctx, VRF_ERR_RUNTIME, "pose_gradient: empty pixel set");
+  for (int i = 0; i < n; ++i)
+    if (pixels[2 * i] < 0 || pixels[2 * i] >= intr->width || pixels[2 * i + 1] < 0 ||
+        pixels[2 * i + 1] >= intr->height)
+      return set_err(ctx, VRF_ERR_OUT_OF_RANGE, "generate_ray: pixel outside image");
+  DevParams p;
+  if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
+  const size_t pix_bytes = sizeof(int32_t) * 2 * (size_t)n;
+  if ((rc = ensure(ctx, ctx->s_batch, pix_bytes))) return rc;
+  if ((rc = ensure(ctx, ctx->s_raycd, sizeof(double4) * n))) return rc;
+  if ((rc = ensure(ctx, ctx->s_flags, n))) return rc;
+  const int nb = pose_backward_blocks(n);
+  if ((rc = ensure(ctx, ctx->s_partials, sizeof(PosePartial) * nb))) return rc;
+  if ((rc = ensure_pinned(ctx, pix_bytes + sizeof(DevPose)))) return rc;
+  std::memcpy(ctx->h_pinned, pixels, pix_bytes);
+  const DevPose dp = dev_pose(pose);
+  std::memcpy((char*)ctx->h_pinned + pix_bytes, &dp, sizeof(DevPose));
+  CU(cudaMemcpyAsync(ctx->s_batch.ptr, ctx->h_pinned, pix_bytes, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(ctx->d_pose, (char*)ctx->h_pinned + pix_bytes, sizeof(DevPose),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemsetAsync(ctx->d_pcount, 0, sizeof(PoseCount), ctx->stream));
+  CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+  const long long npix = (long long)intr->width * intr->height;
+  const double4* rgbd = ctx->rgbd + npix * frame;
+  const DevGrid g = dev_grid(ctx);
+  const DevCam cam = dev_cam(intr);
+  launch_pose_forward(g, p, cam, rgbd, ctx->d_pose, (const int*)ctx->s_batch.ptr, n,
+                      (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr, ctx->d_pcount,
+                      ctx->d_err, ctx->stream);
+  launch_pose_backward(g, p, cam, rgbd, ctx->d_pose, (const int*)ctx->s_batch.ptr, n,
+                       (const double4*)ctx->s_raycd.ptr, (const uint8_t*)ctx->s_flags.ptr,
+                       cfg->lambda_p, cfg->lambda_d, (PosePartial*)ctx->s_partials.ptr,
+                       ctx->stream);
+  launch_pose_reduce((const PosePartial*)ctx->s_partials.ptr, nb, ctx->d_pose_out, ctx->stream);
+  LAUNCHED(3);
+  CU(cudaGetLastError());
+  if ((rc = check_err_flag(ctx))) return rc;
+  PosePartial out;
+  PoseCount cnt;
+  CU(cudaMemcpyAsync(&out, ctx->d_pose_out, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(&cnt, ctx->d_pcount, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(res->jtj, out.jtj, sizeof(res->jtj));
+  std::memcpy(res->jtr, out.jtr, sizeof(res->jtr));
+  res->loss = out.loss;
+  res->m = cnt.m;
+  res->samples = cnt.samples;
+  return VRF_OK;
+}
+
+int gradient_from(vrf_context* ctx, const PoseResult& r, vrf_pose_gradient_result* out) {
+  vrf_pose_gradient_result g{};
+  g.rays_used = r.m;
+  g.samples = r.samples;
+  if (r.m == 0) {
+    if (out) *out = g;
+    return set_err(ctx, VRF_ERR_RUNTIME, "untrackable frame: all sampled rays miss the grid");
+  }
+  // pose_gradient == (2/m) J^T r with rows weighted by sqrt(lambda) (tracking.cpp:117-128).
+  for (int a = 0; a < 3; ++a) {
+    g.d_omega[a] = 2.0 * r.jtr[a] / double(r.m);
+    g.d_tau[a] = 2.0 * r.jtr[3 + a] / double(r.m);
+  }
+  g.loss = r.loss / double(r.m);
+  if (out) *out = g;
+  bool finite = std::isfinite(g.loss);
+  for (int a = 0; a < 3; ++a)
+    finite = finite && std::isfinite(g.d_omega[a]) && std::isfinite(g.d_tau[a]);
+  if (!finite) return set_err(ctx, VRF_ERR_RUNTIME, "pose_gradient: non-finite result");
+  return VRF_OK;
+}
+
+// ---- pose.hpp:32-41, tracking.hpp:21-26 (same operation order as the oracle)
+void quat_normalize(double q[4]) {
+  const double x = q[1], y = q[2], z = q[3], w = q[0];
+  const double n2 = (x * x + z * z) + (y * y + w * w);
+  if (n2 > 0.0) {
+    const double s = std::sqrt(n2);
+    q[0] = w / s;
+    q[1] = x / s;
+    q[2] = y / s;
+    q[3] = z / s;
+  }
+}
+void exp_so3(const double w[3], double q[4]) {
+  const double angle = std::sqrt((w[0] * w[0] + w[1] * w[1]) + w[2] * w[2]);
+  if (angle < 1e-8) {
+    q[0] = 1.0;
+    q[1] = 0.5 * w[0];
+    q[2] = 0.5 * w[1];
+    q[3] = 0.5 * w[2];
+    quat_normalize(q);
+    return;
+  }
+  const double axis[3] = {w[0] / angle, w[1] / angle, w[2] / angle};
+  const double ha = 0.5 * angle, sh = std::sin(ha);
+  q[0] = std::cos(ha);
+  q[1] = sh * axis[0];
+  q[2] = sh * axis[1];
+  q[3] = sh * axis[2];
+}
+void apply_perturbation(const double om[3], const double ta[3], vrf_pose* pose) {
+  double e[4];
+  exp_so3(om, e);
+  const double* b = pose->q;
+  double q[4] = {e[0] * b[0] - e[1] * b[1] - e[2] * b[2] - e[3] * b[3],
+                 e[0] * b[1] + e[1] * b[0] + e[2] * b[3] - e[3] * b[2],
+                 e[0] * b[2] + e[2] * b[0] + e[3] * b[1] - e[1] * b[3],
+                 e[0] * b[3] + e[3] * b[0] + e[1] * b[2] - e[2] * b[1]};
+  quat_normalize(q);
+  for (int i = 0; i < 4; ++i) pose->q[i] = q[i];
+  for (int a = 0; a < 3; ++a) pose->t[a] = pose->t[a] + ta[a];
+}
+
+// (A + lambda diag(A) + 1e-12 I) x = -b, Cholesky on the 6x6 upper-packed A.
+bool solve_lm(const double jtj[21], const double jtr[6], double damping, double x[6]) {
+  double A[6][6];
+  int idx = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) A[a][b] = A[b][a] = jtj[idx++];
+  for (int a = 0; a < 6; ++a) A[a][a] += damping * A[a][a] + 1e-12;
+  double L[6][6] = {};
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = A[i][j];
+      for (int k = 0; k < j; ++k) s -= L[i][k] * L[j][k];
+      if (i == j) {
+        if (!(s > 0.0)) return false;
+        L[i][i] = std::sqrt(s);
+      } else {
+        L[i][j] = s / L[j][j];
+      }
+    }
+  double y[6];
+  for (int i = 0; i < 6; ++i) {
+    double s = -jtr[i];
+    for (int k = 0; k < i; ++k) s -= L[i][k] * y[k];
+    y[i] = s / L[i][i];
+  }
+  for (int i = 5; i >= 0; --i) {
+    double s = y[i];
+    for (int k = i + 1; k < 6; ++k) s -= L[k][i] * x[k];
+    x[i] = s / L[i][i];
+  }
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+void vrf_rng_seed(uint64_t seed, uint64_t state[4]) {
+  Xoshiro r(seed);
+  for (int i = 0; i < 4; ++i) state[i] = r.s[i];
+}
+uint64_t vrf_rng_next(uint64_t state[4]) {
+  Xoshiro r(0);
+  for (int i = 0; i < 4; ++i) r.s[i] = state[i];
+  const uint64_t v = r.next();
+  for (int i = 0; i < 4; ++i) state[i] = r.s[i];
+  return v;
+}
+void vrf_rng_draw_batch(uint64_t state[4], int n_frames, int width, int height, int n,
+                        int32_t* batch) {
+  Xoshiro r(0);
+  for (int i = 0; i < 4; ++i) r.s[i] = state[i];
+  for (int i = 0; i < n; ++i) {
+    batch[3 * i] = (int32_t)r.index((uint64_t)n_frames);
+    batch[3 * i + 1] = (int32_t)r.index((uint64_t)width);
+    batch[3 * i + 2] = (int32_t)r.index((uint64_t)height);
+  }
+  for (int i = 0; i < 4; ++i) state[i] = r.s[i];
+}
+int vrf_rng_draw_valid_pixels(uint64_t state[4], const double* depth, int width, int height,
+                              int count, int max_redraws, int32_t* pixels) {
+  Xoshiro r(0);
+  for (int i = 0; i < 4; ++i) r.s[i] = state[i];
+  int n = 0;
+  for (int i = 0; i < count; ++i) {
+    int px = 0, py = 0;
+    bool ok = false;
+    for (int a = 0; a < max_redraws; ++a) {
+      px = (int)r.index((uint64_t)width);
+      py = (int)r.index((uint64_t)height);
+      if (depth[(size_t)py * width + px] > 0.0) {
+        ok = true;
+        break;
+      }
+    }
+    if (ok) {
+      pixels[2 * n] = px;
+      pixels[2 * n + 1] = py;
+      ++n;
+    }
+  }
+  for (int i = 0; i < 4; ++i) state[i] = r.s[i];
+  return n;
+}
+
+int vrf_pose_gradient(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
+                      const vrf_pose* pose, const int32_t* pixels, int n,
+                      const vrf_tracking_loss* cfg, vrf_pose_gradient_result* out) {
+  cudaSetDevice(ctx->device);
+  PoseResult r;
+  int rc = pose_pass(ctx, frame, intr, pose, pixels, n, cfg, &r);
+  if (rc) return rc;
+  return gradient_from(ctx, r, out);
+}
+
+int vrf_pose_normal_equations(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
+                              const vrf_pose* pose, const int32_t* pixels, int n,
+                              const vrf_tracking_loss* cfg, vrf_normal_equations* out) {
+  cudaSetDevice(ctx->device);
+  PoseResult r;
+  int rc = pose_pass(ctx, frame, intr, pose, pixels, n, cfg, &r);
+  if (rc) return rc;
+  std::memcpy(out->jtj, r.jtj, sizeof(r.jtj));
+  std::memcpy(out->jtr, r.jtr, sizeof(r.jtr));
+  out->loss = r.loss;
+  out->rays_used = r.m;
+  out->reserved = 0;
+  out->samples = r.samples;
+  if (r.m == 0)
+    return set_err(ctx, VRF_ERR_RUNTIME, "untrackable frame: all sampled rays miss the grid");
+  return VRF_OK;
+}
+
+// tracking.cpp:170-252
+int vrf_track_frame(vrf_context* ctx, int frame, const vrf_intrinsics* intr, const vrf_pose* init,
+                    const vrf_tracking_config* cfg, vrf_track_frame_result* out,
+                    double* loss_trace) {
+  cudaSetDevice(ctx->device);
+  vrf_track_frame_result res{};
+  res.pose = *init;
+  *out = res;
+  if (cfg->iterations == 0) return VRF_OK;
+  if (frame < 0 || frame >= ctx->n_frames)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "track_frame: frame index out of range");
+  const std::vector<double>& depth = ctx->host_depth[frame];
+  Xoshiro rng(cfg->seed);
+  vrf_pose pose = *init, best_pose = *init;
+  double best_loss = INFINITY, initial_loss = 0.0;
+  int streak = 0;
+  double m_adam[6] = {0}, v_adam[6] = {0};
+  const vrf_tracking_loss lc{cfg->lambda_p, cfg->lambda_d, cfg->render};
+  std::vector<int32_t> px;
+  int rc;
+  for (int it = 0; it < cfg->iterations; ++it) {
+    draw_valid_pixels(depth, intr->width, intr->height, cfg->rays_per_iteration, cfg->max_redraws,
+                      rng, px);
+    if (px.empty())
+      return set_err(ctx, VRF_ERR_RUNTIME, "track_frame: no valid-depth pixels to sample");
+    PoseResult r;
+    vrf_pose_gradient_result g;
+    if ((rc = pose_pass(ctx, frame, intr, &pose, px.data(), (int)px.size() / 2, &lc, &r))) return rc;
+    if ((rc = gradient_from(ctx, r, &g))) return rc;
+    if (loss_trace) loss_trace[it] = g.loss;
+    res.final_loss = g.loss;
+    ++res.iterations_run;
+    if (it == 0) initial_loss = g.loss;
+    if (g.loss < best_loss) {
+      best_loss = g.loss;
+      best_pose = pose;
+    }
+    if (g.loss > cfg->divergence_factor * initial_loss) {
+      if (++streak >= cfg->divergence_patience) {
+        res.pose = *init;
+        res.failed = 1;
+        *out = res;
+        return VRF_OK;
+      }
+    } else {
+      streak = 0;
+    }
+    const double grad[6] = {g.d_omega[0], g.d_omega[1], g.d_omega[2],
+                            g.d_tau[0],   g.d_tau[1],   g.d_tau[2]};
+    for (int k = 0; k < 6; ++k) {
+      m_adam[k] = cfg->beta1 * m_adam[k] + (1.0 - cfg->beta1) * grad[k];
+      v_adam[k] = cfg->beta2 * v_adam[k] + (1.0 - cfg->beta2) * (grad[k] * grad[k]);
+    }
+    const double bc1 = 1.0 - std::pow(cfg->beta1, it + 1);
+    const double bc2 = 1.0 - std::pow(cfg->beta2, it + 1);
+    double om[3], ta[3];
+    for (int k = 0; k < 6; ++k) {
+      const double mhat = m_adam[k] / bc1, vhat = v_adam[k] / bc2;
+      const double lr = k < 3 ? cfg->lr_omega : cfg->lr_tau;
+      const double step = -lr * mhat / (std::sqrt(vhat) + cfg->adam_eps);
+      if (k < 3)
+        om[k] = step;
+      else
+        ta[k - 3] = step;
+    }
+    apply_perturbation(om, ta, &pose);
+    const double nom = std::sqrt((om[0] * om[0] + om[1] * om[1]) + om[2] * om[2]);
+    const double nta = std::sqrt((ta[0] * ta[0] + ta[1] * ta[1]) + ta[2] * ta[2]);
+    if (cfg->convergence_step > 0.0 && nom < cfg->convergence_step && nta < cfg->convergence_step)
+      break;
+  }
+  // Evaluate the final iterate (tracking.cpp:239-249).
+  draw_valid_pixels(depth, intr->width, intr->height, cfg->rays_per_iteration, cfg->max_redraws,
+                    rng, px);
+  if (!px.empty()) {
+    PoseResult r;
+    vrf_pose_gradient_result g;
+    if ((rc = pose_pass(ctx, frame, intr, &pose, px.data(), (int)px.size() / 2, &lc, &r))) return rc;
+    if ((rc = gradient_from(ctx, r, &g))) return rc;
+    if (g.loss < best_loss) {
+      best_loss = g.loss;
+      best_pose = pose;
+    }
+  }
+  res.pose = best_pose;
+  *out = res;
+  return VRF_OK;
+}
+
+// Gauss-Newton / LM: per iteration one normal-equation pass and a damped 6x6
+// solve; pixel draws from the same valid-depth sampler (seeded stream).
+int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
+                       const vrf_pose* init, const vrf_gn_config* cfg,
+                       vrf_track_frame_result* out) {
+  cudaSetDevice(ctx->device);
+  vrf_track_frame_result res{};
+  res.pose = *init;
+  *out = res;
+  if (cfg->iterations <= 0) return VRF_OK;
+  if (frame < 0 || frame >= ctx->n_frames)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "track_frame: frame index out of range");
+  const std::vector<double>& depth = ctx->host_depth[frame];
+  Xoshiro rng(cfg->seed);
+  const vrf_tracking_loss lc{cfg->lambda_p, cfg->lambda_d, cfg->render};
+  vrf_pose pose = *init;
+  std::vector<int32_t> px;
+  int rc;
+  for (int it = 0; it < cfg->iterations; ++it) {
+    draw_valid_pixels(depth, intr->width, intr->height, cfg->rays_per_iteration, cfg->max_redraws,
+                      rng, px);
+    if (px.empty())
+      return set_err(ctx, VRF_ERR_RUNTIME, "track_frame: no valid-depth pixels to sample");
+    PoseResult r;
+    if ((rc = pose_pass(ctx, frame, intr, &pose, px.data(), (int)px.size() / 2, &lc, &r))) return rc;
+    if (r.m == 0)
+      return set_err(ctx, VRF_ERR_RUNTIME, "untrackable frame: all sampled rays miss the grid");
+    res.final_loss = r.loss / r.m;
+    ++res.iterations_run;
+    double x[6];
+    if (!solve_lm(r.jtj, r.jtr, cfg->damping, x)) break;
+    apply_perturbation(x, x + 3, &pose);
+  }
+  res.pose = pose;
+  *out = res;
+  return VRF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+"""The C-ABI library loads and exports every symbol include/voxrf_b200.h declares
+(no compute calls: this runs without a GPU)."""
+import re
+from pathlib import Path
+
+import numpy as np
+
+from paper_2307_03404_b200 import _capi
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "voxrf_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(vrf_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _capi.load()
+    names = declared_symbols()
+    assert len(names) >= 35
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_capi.EXPORTED)
+
+
+def test_abi_version_and_host_rng_matches_oracle(oracle):
+    lib = _capi.load()
+    assert lib.vrf_abi_version() == 1
+    from paper_2307_03404_b200 import Rng
+    r = Rng(1)
+    b = r.draw_batch(3, 160, 120, 500)
+    assert np.array_equal(b, oracle.draw_batch(1, 3, 160, 120, 500))
+
+
+def test_context_create_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        return
+    from paper_2307_03404_b200 import Context
+    try:
+        Context(0)
+    except RuntimeError as e:
+        assert "no CPU fallback" in str(e)
+    else:
+        raise AssertionError("context creation must fail without a CUDA device")

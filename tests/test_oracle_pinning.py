@@ -1,0 +1,151 @@
+"""Pins the plain-C oracle (oracle/voxrf_oracle.c) to the reference itself.
+
+The reference's own translation units are compiled unchanged into
+oracle/_ref/libvoxrf_ref.so (oracle/Makefile); these tests run both on the same
+seeded inputs and require bit-identical results. They also run the reference's
+own 45 doctest cases against that build."""
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from paper_2307_03404_b200.api import MappingConfig, Pose, RenderParams, TrackingConfig
+from paper_2307_03404_b200 import synth
+
+from scenes import fresh_grid, random_rays, room_scene
+
+pytestmark = pytest.mark.ref
+
+
+def test_reference_unit_tests_pass_on_shim_build(ref):
+    """The reference's 45 doctest cases (proj/tests) against oracle/_ref. Exactly one
+    case fails, test_renderer.cpp:295-296, which compares a double image value with
+    float(ws.color_out.x()) — ImageF stores double (image.hpp:14), so the check can
+    only pass for float-representable values ('Suspect test')."""
+    binary = orc.HERE / "_ref" / "voxrf_ref_tests"
+    if not binary.exists():
+        orc.build(ref=True)
+    r = subprocess.run([str(binary)], capture_output=True, text=True, timeout=300)
+    assert "test cases: 45 | 44 passed | 1 failed" in r.stdout, r.stdout + r.stderr
+    failing = [ln for ln in r.stderr.splitlines() if "ERROR: CHECK" in ln]
+    assert failing and all("test_renderer.cpp:295" in ln or "test_renderer.cpp:296" in ln
+                           for ln in failing), r.stderr[:2000]
+
+
+def test_generate_ray_bit_exact(oracle, ref):
+    intr = synth.small_intrinsics()
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        pose = synth.look_at(rng.uniform(0, 4, 3), rng.uniform(0, 4, 3))
+        u, v = rng.uniform(0, intr.width), rng.uniform(0, intr.height)
+        o1, d1 = oracle.generate_ray(intr, pose, u, v)
+        o2 = np.zeros(3)
+        d2 = np.zeros(3)
+        assert ref.lib.ref_generate_ray(
+            orc.C.byref(orc.intr_s(intr)), orc.C.byref(orc.pose_s(pose)), orc.C.c_double(u),
+            orc.C.c_double(v), orc._ptr(o2), orc._ptr(d2)) == 0
+        assert np.array_equal(o1, o2) and np.array_equal(d1, d2)
+
+
+def test_sample_and_render_ray_bit_exact(oracle, ref):
+    grid, intr, frames = room_scene()
+    gh = ref.grid(grid)
+    try:
+        for row in random_rays(grid, 200):
+            t1, d1, _ = oracle.sample_ray(grid, row[:3], row[3:], RenderParams())
+            t2, d2 = ref.sample_ray(gh, row[:3], row[3:], RenderParams())
+            assert np.array_equal(t1, t2) and np.array_equal(d1, d2)
+            r1 = oracle.render_ray(grid, row[:3], row[3:], RenderParams())
+            r2 = ref.render_ray(gh, row[:3], row[3:], RenderParams())
+            assert bytes(r1) == bytes(r2)
+    finally:
+        ref.lib.ref_grid_destroy(gh)
+
+
+def test_render_image_bit_exact(oracle, ref):
+    grid, intr, frames = room_scene()
+    gh = ref.grid(grid)
+    try:
+        for stride in (1, 2):
+            c1, dd1 = oracle.render_image(grid, intr, frames[1].gt_pose, RenderParams(), stride)
+            c2, dd2 = ref.render_image(gh, intr, frames[1].gt_pose, RenderParams(), stride)
+            assert np.array_equal(c1, c2) and np.array_equal(dd1, dd2)
+    finally:
+        ref.lib.ref_grid_destroy(gh)
+
+
+def test_mapping_gradient_and_step_bit_exact(oracle, ref):
+    grid, intr, frames = room_scene()
+    g0 = fresh_grid(grid)
+    cfg = MappingConfig()
+    batch = oracle.draw_batch(11, len(frames), intr.width, intr.height, 256)
+    gh = ref.grid(g0)
+    fh = ref.frames(frames, intr)
+    try:
+        grad_ref, samples = ref.mapping_grad(gh, fh, intr, cfg, batch, g0.geom.num_vertices)
+        _, _, grad_or, st = oracle.mapping_step(g0, frames, intr, cfg, batch, apply=False,
+                                                want_grad=True)
+        assert samples == st.samples and samples > 0
+        assert np.array_equal(grad_ref, grad_or)
+        # Full mapping_step (reference draws the batch from Rng(11) itself).
+        mapper = ref.lib.ref_mapper_create(11)
+        st_ref = ref.mapping_step(gh, fh, intr, cfg, 256, threads=1, deterministic=True,
+                                  mapper=mapper)
+        new_ref = ref.read_grid(gh, g0.geom.num_vertices)
+        new_or, v_or, _, st_or = oracle.mapping_step(g0, frames, intr, cfg, batch)
+        assert np.array_equal(new_ref, new_or)
+        v_ref = np.zeros(new_ref.size)
+        assert ref.lib.ref_mapper_rms(mapper, orc._ptr(v_ref), v_ref.size) == 0
+        assert np.array_equal(v_ref, v_or.reshape(-1))
+        for f in ("loss_photometric", "loss_geometric", "loss_total", "rays_color", "rays_depth",
+                  "psnr_estimate"):
+            assert getattr(st_ref, f) == getattr(st_or, f), f
+        ref.lib.ref_mapper_destroy(mapper)
+    finally:
+        ref.lib.ref_grid_destroy(gh)
+        ref.lib.ref_frames_destroy(fh)
+
+
+def test_pose_gradient_and_normal_eqs(oracle, ref):
+    grid, intr, frames = room_scene()
+    frame = frames[1]
+    rng = np.random.default_rng(3)
+    px = np.stack([rng.integers(0, intr.width, 200), rng.integers(0, intr.height, 200)], 1)
+    pose = Pose(frame.gt_pose.q, tuple(np.asarray(frame.gt_pose.t) + [0.01, -0.02, 0.005]))
+    gh = ref.grid(grid)
+    fh = ref.frames([frame], intr)
+    try:
+        a = oracle.pose_gradient(grid, frame, intr, pose, px, 1.0, 1.0, RenderParams())
+        b = ref.pose_gradient(gh, fh, intr, pose, px, 1.0, 1.0, RenderParams(), threads=1)
+        assert bytes(a) == bytes(b)
+        n1 = oracle.normal_eqs(grid, frame, intr, pose, px, 1.0, 0.5, RenderParams())
+        n2 = ref.normal_eqs(gh, fh, intr, pose, px, 1.0, 0.5, RenderParams())
+        assert np.allclose(n1.jtj, n2.jtj, rtol=1e-12, atol=1e-14)
+        assert np.allclose(n1.jtr, n2.jtr, rtol=1e-12, atol=1e-14)
+        assert n1.rays_used == n2.rays_used
+        # (2/m) J^T r == pose_gradient (oracle vs reference)
+        n3 = ref.normal_eqs(gh, fh, intr, pose, px, 1.0, 1.0, RenderParams())
+        g = 2.0 * np.array(n3.jtr) / n3.rays_used
+        assert np.allclose(g[:3], b.d_omega, rtol=1e-10, atol=1e-13)
+        assert np.allclose(g[3:], b.d_tau, rtol=1e-10, atol=1e-13)
+    finally:
+        ref.lib.ref_grid_destroy(gh)
+        ref.lib.ref_frames_destroy(fh)
+
+
+def test_track_frame_bit_exact(oracle, ref):
+    grid, intr, frames = room_scene()
+    frame = frames[2]
+    init = Pose(frame.gt_pose.q, tuple(np.asarray(frame.gt_pose.t) + [0.02, 0.0, -0.01]))
+    tc = TrackingConfig(rays_per_iteration=128, iterations=6)
+    gh = ref.grid(grid)
+    fh = ref.frames([frame], intr)
+    try:
+        a, ta = oracle.track_frame(grid, frame, intr, init, tc)
+        b, tb = ref.track_frame(gh, fh, intr, init, tc)
+        assert bytes(a) == bytes(b)
+        assert np.array_equal(ta, tb)
+    finally:
+        ref.lib.ref_grid_destroy(gh)
+        ref.lib.ref_frames_destroy(fh)
