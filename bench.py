@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""Benchmark of the per-ray hot path (BASELINE.json metric) on B200.
+
+Workload (config 3, BASELINE.json configs[2]): Replica-shaped 1200x680 RGB-D
+keyframes rendered from a synthetic 257^3-vertex (256^3-cell) room map,
+incremental mapping fwd+bwd with the RGB+depth loss and sparse RMSProp, one
+`mapping_step` per step over a batch of --rays rays drawn uniformly over
+(keyframe, px, py) with the reference Rng. The mapping grid starts at
+sigma_init = 0.1, SH = 0, all cells active (map_scene, mapping.cpp:290-300).
+Tracking (config 2, configs[1]) on the fixed ground-truth map is reported in
+the same line under "tracking".
+
+value : composited samples/s over all ranks, batches already in HBM.
+e2e   : the same metric through the public API call (Context.mapping_step) with
+        the batch drawn on the host and copied H2D from pinned memory and the
+        step statistics read back D2H, every step.
+The grid (1.9 GB fp32 + 1.9 GB gradient + 1.9 GB RMSProp state) is far larger
+than L2 (126 MB), so no explicit L2 flush is needed between steps.
+
+`--impl reference` times the reference's own CPU mapping_step (oracle/_ref,
+the reference sources compiled unchanged) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "mapping samples/s & rays/s (fwd+bwd) and tracking frames/s at 1/2/4/8 B200"
+WORKLOAD = ("config3: Replica-shaped 1200x680 RGB-D, 256^3-cell (257^3-vertex) grid, "
+            "incremental mapping fwd+bwd with RGB+depth loss + RMSProp")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rays", type=int, default=1 << 20)
+    ap.add_argument("--res", type=int, default=257)
+    ap.add_argument("--keyframes", type=int, default=10)
+    ap.add_argument("--width", type=int, default=1200)
+    ap.add_argument("--height", type=int, default=680)
+    ap.add_argument("--track-frames", type=int, default=6)
+    ap.add_argument("--no-tracking", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- inputs
+def make_scene(args):
+    from paper_2307_03404_b200 import synth
+    from paper_2307_03404_b200.api import CameraIntrinsics
+
+    room = synth.Room().scaled(7.0 / 4.0, 6.0 / 4.0, 1.0)
+    gt = synth.scene_grid(args.res, room, seed=2, prune_tau=1e-3)
+    s = args.width / 1200.0
+    intr = CameraIntrinsics(600.0 * s, 600.0 * s, args.width / 2 - 0.5, args.height / 2 - 0.5,
+                            args.width, args.height, 6553.5)
+    path = synth.room_path(100, room, seed=4)
+    return room, gt, intr, path
+
+
+def render_frames(ctx, intr, poses):
+    from paper_2307_03404_b200 import synth
+    from paper_2307_03404_b200.api import Frame
+
+    out = []
+    for p in poses:
+        img = ctx.render_image(intr, p)
+        c, d = synth.quantize_frame(img.color, img.depth, intr.depth_scale)
+        out.append(Frame(c, d, 0.0, p))
+    return out
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        if kernel in d:
+            return d[kernel]
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.rows = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for n, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- CPU baseline
+def cpu_reference(args, gt, intr, keyframe_poses, frames, seconds):
+    """The reference's own mapping_step (oracle/_ref) on the host cores, on the same
+    workload (257^3 fp64 grid, 1200x680 keyframes), reference default batch of
+    4096 rays, timed like the reference times itself (steady clock)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+    from paper_2307_03404_b200.api import MappingConfig, VoxelGrid
+
+    if not orc.REF_SO.exists():
+        return None
+    ref = orc.RefLib()
+    nproc = os.cpu_count() or 1
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 64 << 30
+    vbytes = gt.geom.num_vertices * 28 * 8
+    # mapping.cpp:155-157 allocates one V x 28 fp64 GradientBuffer per worker.
+    threads = int(max(1, min(nproc, (avail - 3 * vbytes - (4 << 30)) // vbytes)))
+    grid = VoxelGrid(gt.geom, 0.1)
+    fh = ref.frames(frames, intr)
+    cfg = MappingConfig()
+    steps = 0
+    elapsed = 0.0
+    # Each repetition: a fresh sigma_init map and a fresh Rng(1), so every timed call
+    # is the reference's first mapping_step of map_scene (mapping.cpp:290-313) on the
+    # same 4096-ray batch; setup is outside the timed region.
+    while elapsed < seconds and steps < 20:
+        gh = ref.grid(grid)
+        mapper = ref.lib.ref_mapper_create(1)
+        t0 = time.perf_counter()
+        ref.mapping_step(gh, fh, intr, cfg, 4096, threads, False, mapper)
+        elapsed += time.perf_counter() - t0
+        steps += 1
+        ref.lib.ref_mapper_destroy(mapper)
+        ref.lib.ref_grid_destroy(gh)
+    ref.lib.ref_frames_destroy(fh)
+    return {"threads": threads, "steps": steps, "seconds": elapsed}
+
+
+def cpu_samples_per_step(args, gt, intr, frames):
+    """Composited samples of the reference's first 4096-ray batch (same Rng(1) draw),
+    counted by the oracle restatement (the reference does not report it)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+    from paper_2307_03404_b200.api import MappingConfig, VoxelGrid
+
+    o = orc.Oracle()
+    batch = o.draw_batch(1, len(frames), intr.width, intr.height, 4096)
+    g = VoxelGrid(gt.geom, 0.1)
+    _, _, _, st = o.mapping_step(g, frames, intr, MappingConfig(), batch, apply=False)
+    return int(st.samples), int(st.rays_color)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2307_03404_b200.api import RenderParams
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+
+    if not orc.REF_SO.exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    room, gt, intr, path = make_scene(args)
+    keyposes = path[::10][: args.keyframes]
+    # keyframes rendered by the reference's own render_image (CPU, all threads)
+    ref = orc.RefLib()
+    gh = ref.grid(gt)
+    frames = []
+    from paper_2307_03404_b200 import synth
+    from paper_2307_03404_b200.api import Frame
+    for p in keyposes:
+        c, d = ref.render_image(gh, intr, p, RenderParams(), 1, os.cpu_count() or 1)
+        c, d = synth.quantize_frame(c, d, intr.depth_scale)
+        frames.append(Frame(c, d, 0.0, p))
+    ref.lib.ref_grid_destroy(gh)
+    per_step, rays = cpu_samples_per_step(args, gt, intr, frames)
+    budget = max(5.0, min(args.cpu_seconds, 60.0))
+    r = cpu_reference(args, gt, intr, keyposes, frames, budget)
+    value = per_step * r["steps"] / r["seconds"]
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": r["steps"], "warmup": 0,
+        "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "rays_per_step": 4096, "grid_vertices": args.res ** 3,
+                   "keyframes": len(frames), "frame": f"{args.width}x{args.height}"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": r["threads"],
+                         "kind": "reference",
+                         "sample": f"{r['steps']} reference mapping_step calls x 4096 rays on the "
+                                   f"257^3 fp64 grid ({per_step} composited samples/step)"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+# ----------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+
+    from paper_2307_03404_b200 import Context, Rng
+    from paper_2307_03404_b200.api import GNConfig, MappingConfig, Pose
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+
+    room, gt, intr, path = make_scene(args)
+    keyposes = path[::10][: args.keyframes]
+
+    # ground-truth map context: renders the keyframes, later tracks against them
+    gt_ctx = Context(local)
+    gt_ctx.load_grid(gt)
+    frames = render_frames(gt_ctx, intr, keyposes)
+
+    ctx = Context(local, shard_multiple=world)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.init_grid(gt.geom, 0.1)
+    ctx.load_frames(intr, frames)
+    ctx.rmsprop_reset()
+    cfg = MappingConfig()
+    rng = Rng(1 + 7919 * rank)
+    nb = args.warmup + args.steps
+    host_batches = [rng.draw_batch(len(frames), intr.width, intr.height, args.rays)
+                    for _ in range(nb)]
+    dev_batches = [torch.from_numpy(b).to(f"cuda:{local}") for b in host_batches]
+    torch.cuda.synchronize()
+
+    mapper = None
+    if world > 1:
+        from paper_2307_03404_b200.distributed import DistributedMapper, GpuEngine
+        mapper = DistributedMapper(GpuEngine(ctx, cfg))
+
+    def one_step(i):
+        if mapper is not None:
+            return mapper.step(dev_batches[i], cfg.lambda_d)
+        return ctx.mapping_step_device(cfg, dev_batches[i].data_ptr(), args.rays)
+
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ctx.profile_enable(True)
+    launches0 = ctx.kernel_launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    samples = 0
+    rays_hit = 0
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(args.warmup, nb):
+            st = one_step(i)
+            samples += st.samples
+            rays_hit += st.rays_color
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.kernel_launches - launches0
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        if mapper is None:
+            pass
+    # mapper.step returns global samples already; single GPU: local == global
+    total_samples = samples
+    total_rays = args.rays * args.steps * world
+    value = total_samples / (ms / 1e3)
+
+    # ---- e2e through the public API (host batch, H2D + stats D2H every step)
+    e2e = None
+    if world == 1:
+        e_rng = Rng(99)
+        torch.cuda.synchronize()
+        e_samples = 0
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            b = e_rng.draw_batch(len(frames), intr.width, intr.height, args.rays)
+            st = ctx.mapping_step(cfg, b)
+            e_samples += st.samples
+        torch.cuda.synchronize()
+        e_s = time.perf_counter() - t0
+        e2e = {"value": e_samples / e_s, "unit": "samples/s",
+               "h2d_bytes_per_step": int(args.rays * 12), "d2h_bytes_per_step": 64,
+               "ms_per_step": 1e3 * e_s / args.steps}
+
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = load_peaks()
+    S = total_samples / world if world > 1 else total_samples
+    kern = {k: prof[k] for k in ("map_forward", "map_backward", "rmsprop")}
+    dom = max(kern, key=lambda k: kern[k][0])
+    bytes_per = {
+        "map_forward": 896.0 * S + 32.0 * (args.rays * args.steps),
+        "map_backward": 1792.0 * S,
+        "rmsprop": 96.0 * prof["touched_groups"],
+    }
+    k_ms, k_n = kern[dom]
+    achieved = bytes_per[dom] / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
+    step_bytes = 1792.0 * S + 32.0 * args.rays * args.steps + 96.0 * prof["touched_groups"]
+    roofline = {
+        "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": peak_kind,
+        "launches": k_n, "kernel_ms": {k: v[0] for k, v in kern.items()},
+        "step_algorithmic_GBps": step_bytes / (ms / 1e3) / 1e9,
+        "step_frac": step_bytes / (ms / 1e3) / 1e9 / peak,
+    }
+
+    # ---- tracking (config 2) on the fixed ground-truth map
+    tracking = None
+    if not args.no_tracking and rank == 0:
+        from paper_2307_03404_b200 import synth
+        tposes = path[1: 1 + args.track_frames + 1]
+        tframes = render_frames(gt_ctx, intr, tposes)
+        gt_ctx.load_frames(intr, tframes)
+        gn = GNConfig(rays_per_iteration=16384, iterations=10)
+        torch.cuda.synchronize()
+        errs = []
+        t0 = time.perf_counter()
+        prev = tposes[0]
+        for i in range(1, len(tframes)):
+            r = gt_ctx.track_frame_gn(i, intr, prev, gn)
+            prev = r.pose
+            errs.append(np.linalg.norm(np.asarray(r.pose.t) - np.asarray(tposes[i].t)))
+        dt = time.perf_counter() - t0
+        tracking = {"config": "config2: 1200x680, 257^3 map, GN/LM 16384 rays x 10 it",
+                    "frames_per_s": (len(tframes) - 1) / dt,
+                    "ms_per_frame": 1e3 * dt / (len(tframes) - 1),
+                    "ate_rmse_m": float(np.sqrt(np.mean(np.square(errs))))}
+
+    # ---- CPU baseline (rank 0, N=1)
+    cpu = None
+    if not args.no_cpu and world == 1 and rank == 0:
+        try:
+            per_step, _ = cpu_samples_per_step(args, gt, intr, frames)
+            r = cpu_reference(args, gt, intr, keyposes, frames, args.cpu_seconds)
+            if r:
+                cpu = {"value": per_step * r["steps"] / r["seconds"], "unit": "samples/s",
+                       "cores": r["threads"], "kind": "reference",
+                       "sample": f"{r['steps']} reference mapping_step calls x 4096 rays on the "
+                                 f"257^3 fp64 grid, fresh sigma_init=0.1 map "
+                                 f"({per_step} composited samples/step)"}
+        except Exception as e:  # the baseline must never hide our own number
+            cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "rays_per_step_per_gpu": args.rays,
+                       "grid_vertices": args.res ** 3, "keyframes": len(frames),
+                       "frame": f"{args.width}x{args.height}", "parallelism": f"dp{world}",
+                       "l2": "inputs larger than L2 (grid 1.9 GB fp32)"},
+            "rays_per_s": total_rays / (ms / 1e3),
+            "samples_per_ray": total_samples / max(1, rays_hit),
+            "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+            "cpu_baseline": cpu, "tracking": tracking, "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

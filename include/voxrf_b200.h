@@ -175,6 +175,13 @@ int vrf_set_stream(vrf_context* ctx, void* stream);
 int vrf_get_device_buffers(vrf_context* ctx, vrf_device_buffers* out);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t vrf_kernel_launch_count(const vrf_context* ctx);
+/* Per-kernel CUDA-event timing on the context stream (resets the counters).
+ * Slots: 0 map forward, 1 map backward (scatter), 2 RMSProp, 3 misc,
+ *        4 pose forward, 5 pose backward, 6 render, 7 deterministic reduce. */
+int vrf_profile_enable(vrf_context* ctx, int on);
+int vrf_profile_read(vrf_context* ctx, int slot, double* ms, int64_t* launches);
+/* float4 parameter groups RMSProp updated since vrf_profile_enable (96 B each). */
+int64_t vrf_profile_touched_groups(vrf_context* ctx);
 
 /* ---- grid: VoxelGrid (voxel_grid.hpp:112-175) */
 /* VoxelGrid(geom, sigma_init) — voxel_grid.cpp:74-81 (all cells active). */

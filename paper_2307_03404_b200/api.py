@@ -402,6 +402,21 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self._lib.vrf_kernel_launch_count(self._h))
 
+    PROFILE_SLOTS = ("map_forward", "map_backward", "rmsprop", "misc", "pose_forward",
+                     "pose_backward", "render", "deterministic_reduce")
+
+    def profile_enable(self, on: bool = True):
+        self._check(self._lib.vrf_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        out = {}
+        for i, name in enumerate(self.PROFILE_SLOTS):
+            ms, n = C.c_double(), C.c_int64()
+            self._check(self._lib.vrf_profile_read(self._h, i, C.byref(ms), C.byref(n)))
+            out[name] = (ms.value, n.value)
+        out["touched_groups"] = int(self._lib.vrf_profile_touched_groups(self._h))
+        return out
+
     def set_stream(self, stream_ptr: int):
         self._check(self._lib.vrf_set_stream(self._h, C.c_void_p(stream_ptr)))
 

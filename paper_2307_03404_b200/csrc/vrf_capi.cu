@@ -47,6 +47,8 @@ void vrf_context_destroy(vrf_context* ctx) {
   cudaFree(ctx->d_pcount);
   cudaFree(ctx->d_pose_out);
   cudaFree(ctx->d_pose);
+  cudaFree(ctx->d_touched);
+  prof_collect(ctx);
   for (DeviceScratch* s : {&ctx->s_batch, &ctx->s_raycd, &ctx->s_flags, &ctx->s_partials,
                            &ctx->s_count, &ctx->s_offsets, &ctx->s_keys, &ctx->s_keys2,
                            &ctx->s_ids, &ctx->s_ids2, &ctx->s_values, &ctx->s_grad64, &ctx->s_cub,
@@ -83,6 +85,39 @@ int vrf_get_device_buffers(vrf_context* ctx, vrf_device_buffers* out) {
 }
 
 int64_t vrf_kernel_launch_count(const vrf_context* ctx) { return ctx->launches; }
+
+int vrf_profile_enable(vrf_context* ctx, int on) {
+  cudaSetDevice(ctx->device);
+  CU(cudaStreamSynchronize(ctx->stream));
+  prof_collect(ctx);
+  for (int i = 0; i < 8; ++i) {
+    ctx->prof_ms[i] = 0.0;
+    ctx->prof_launches[i] = 0;
+  }
+  if (!ctx->d_touched) CU(cudaMalloc(&ctx->d_touched, sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(ctx->d_touched, 0, sizeof(unsigned long long), ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->profiling = on != 0;
+  return VRF_OK;
+}
+
+int vrf_profile_read(vrf_context* ctx, int slot, double* ms, int64_t* launches) {
+  if (slot < 0 || slot >= 8) return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "profile slot");
+  cudaSetDevice(ctx->device);
+  CU(cudaStreamSynchronize(ctx->stream));
+  prof_collect(ctx);
+  *ms = ctx->prof_ms[slot];
+  *launches = ctx->prof_launches[slot];
+  return VRF_OK;
+}
+
+int64_t vrf_profile_touched_groups(vrf_context* ctx) {
+  unsigned long long n = 0;
+  if (!ctx->d_touched) return 0;
+  cudaSetDevice(ctx->device);
+  if (cudaMemcpy(&n, ctx->d_touched, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return (int64_t)n;
+}
 
 // ----------------------------------------------------------------- grid
 int vrf_grid_init(vrf_context* ctx, const vrf_grid_geometry* geom, double sigma_init) {

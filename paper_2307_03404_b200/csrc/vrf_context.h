@@ -68,6 +68,13 @@ struct vrf_context {
   // multi-GPU phase state
   const int* last_batch = nullptr;
   int last_n = 0;
+
+  // profiling: CUDA events around kernels on the context stream (vrf_profile_*)
+  bool profiling = false;
+  double prof_ms[8] = {0};
+  long long prof_launches[8] = {0};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  unsigned long long* d_touched = nullptr;  // RMSProp float4 groups updated
 };
 
 namespace vrf_host {
@@ -235,6 +242,38 @@ inline int check_frames(vrf_context* ctx, const vrf_intrinsics* intr) {
   return VRF_OK;
 }
 
+// Kernel-time slots reported by vrf_profile_read.
+enum ProfSlot { kProfMapForward = 0, kProfMapBackward = 1, kProfRmsprop = 2, kProfMapMisc = 3,
+                kProfPoseForward = 4, kProfPoseBackward = 5, kProfRender = 6, kProfDet = 7 };
+
+inline cudaEvent_t prof_begin(vrf_context* ctx) {
+  if (!ctx->profiling) return nullptr;
+  cudaEvent_t b;
+  cudaEventCreate(&b);
+  cudaEventRecord(b, ctx->stream);
+  return b;
+}
+inline void prof_end(vrf_context* ctx, int slot, cudaEvent_t b) {
+  if (!ctx->profiling || !b) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, ctx->stream);
+  ctx->pending.push_back({slot, {b, e}});
+}
+// After a stream sync: fold the recorded intervals into the per-slot totals.
+inline void prof_collect(vrf_context* ctx) {
+  for (auto& p : ctx->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
+      ctx->prof_ms[p.first] += ms;
+      ctx->prof_launches[p.first] += 1;
+    }
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  ctx->pending.clear();
+}
+
 inline double psnr_from_lp(double lp) {  // mapping.cpp:107-110
   if (lp <= 0.0) return 99.0;
   return std::min(99.0, 10.0 * std::log10(3.0 / lp));
@@ -254,10 +293,12 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
   if ((rc = ensure(ctx, ctx->s_partials, sizeof(MapPartial) * nb))) return rc;
   CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
   if (n > 0) {
+    cudaEvent_t pb = prof_begin(ctx);
     launch_map_forward(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
                        batch_dev, n, (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
                        (MapPartial*)ctx->s_partials.ptr, ray_count, ctx->d_err, fast,
                        ctx->stream);
+    prof_end(ctx, kProfMapForward, pb);
     LAUNCHED(1);
   } else {
     CU(cudaMemsetAsync(ctx->s_partials.ptr, 0, sizeof(MapPartial), ctx->stream));

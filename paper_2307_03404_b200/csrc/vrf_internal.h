@@ -65,7 +65,7 @@ void launch_segmented_reduce(const uint32_t* sorted_keys, const uint32_t* perm,
                              cudaStream_t s);
 void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, long long v_end,
                     double rho, double lr_sigma, double lr_sh, double eps,
-                    const MapStats* stats, cudaStream_t s);
+                    const MapStats* stats, unsigned long long* touched, cudaStream_t s);
 void launch_pose_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                          const double4* rgbd, const DevPose* pose, const int* pixels, int n,
                          double4* ray_cd, uint8_t* flags, PoseCount* counts, int* err_flag,

@@ -448,16 +448,19 @@ __global__ void __launch_bounds__(256) k_rmsprop(float4* __restrict__ theta,
                                                  float4* __restrict__ vstate, long long f_begin,
                                                  long long f_end, double rho, double lr_sigma,
                                                  double lr_sh, double eps,
-                                                 const MapStats* __restrict__ stats) {
+                                                 const MapStats* __restrict__ stats,
+                                                 unsigned long long* __restrict__ touched) {
   if (stats) {
     const MapStats st = *stats;
     if (st.bad != INT_MAX || st.m_c == 0) return;
   }
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  unsigned int n_touched = 0;
   for (long long f = f_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; f < f_end;
        f += (long long)gridDim.x * blockDim.x) {
     const float4 g4 = grad[f];
     if (g4.x == 0.f && g4.y == 0.f && g4.z == 0.f && g4.w == 0.f) continue;
+    ++n_touched;
     float4 th = theta[f], v4 = vstate[f];
     const int j = (int)(f % kVec4PerVertex);
     float* thp = &th.x;
@@ -475,6 +478,10 @@ __global__ void __launch_bounds__(256) k_rmsprop(float4* __restrict__ theta,
     theta[f] = th;
     vstate[f] = v4;
     grad[f] = zero;
+  }
+  if (touched) {  // float4 groups updated (algorithmic optimizer bytes: 96 B each)
+    n_touched = warp_sum(n_touched);
+    if ((threadIdx.x & 31) == 0 && n_touched) atomicAdd(touched, (unsigned long long)n_touched);
   }
 }
 
@@ -801,11 +808,11 @@ void launch_segmented_reduce(const uint32_t* keys, const uint32_t* perm, const d
 }
 void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, long long v_end,
                     double rho, double lr_sigma, double lr_sh, double eps,
-                    const MapStats* stats, cudaStream_t s) {
+                    const MapStats* stats, unsigned long long* touched, cudaStream_t s) {
   const long long f0 = v_begin * kVec4PerVertex, f1 = v_end * kVec4PerVertex;
   if (f1 <= f0) return;
   k_rmsprop<<<grid_blocks(f1 - f0, 256), 256, 0, s>>>(theta, grad, v, f0, f1, rho, lr_sigma,
-                                                      lr_sh, eps, stats);
+                                                      lr_sh, eps, stats, touched);
 }
 void launch_pose_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                          const double4* rgbd, const DevPose* pose, const int* pixels, int n,

@@ -126,24 +126,21 @@ int grad_deterministic(vrf_context* ctx, const vrf_mapping_config* cfg, const in
 // through the sorted fp64 reduce, then rounds once to fp32.
 int map_gradient(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev, int n,
                  MapStats* st_out, bool need_host_stats) {
-  const bool det = cfg->deterministic != 0;
-  int rc = map_forward_dev(ctx, cfg, batch_dev, n, /*fast=*/!det,
-                           det ? (int*)nullptr : (int*)nullptr);
+  int rc = map_forward_dev(ctx, cfg, batch_dev, n, /*fast=*/true);
   if (rc) return rc;
-  if (!det) {
-    DevParams p;
-    if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
-    if (n > 0) {
-      launch_map_backward(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
-                          batch_dev, n, (const double4*)ctx->s_raycd.ptr,
-                          (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, nullptr,
-                          (float4*)ctx->grad, cfg->lambda_d, /*fast=*/true, ctx->stream);
-      LAUNCHED(1);
-    }
-    CU(cudaGetLastError());
-    if (need_host_stats && (rc = read_stats(ctx, st_out))) return rc;
-    return VRF_OK;
+  DevParams p;
+  if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
+  if (n > 0) {
+    cudaEvent_t pb = prof_begin(ctx);
+    launch_map_backward(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
+                        batch_dev, n, (const double4*)ctx->s_raycd.ptr,
+                        (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, nullptr,
+                        (float4*)ctx->grad, cfg->lambda_d, /*fast=*/true, ctx->stream);
+    prof_end(ctx, kProfMapBackward, pb);
+    LAUNCHED(1);
   }
+  CU(cudaGetLastError());
+  if (need_host_stats && (rc = read_stats(ctx, st_out))) return rc;
   return VRF_OK;
 }
 
@@ -171,21 +168,26 @@ int step_impl(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_
   int rc;
   MapStats st;
   if (cfg->deterministic) {
+    cudaEvent_t pb = prof_begin(ctx);
     if ((rc = det_forward(ctx, cfg, batch_dev, n, &st))) return rc;
     if ((rc = grad_deterministic(ctx, cfg, batch_dev, n, st))) return rc;
     launch_f64_to_f32((const double*)ctx->s_grad64.ptr, ctx->grad, ctx->V * 28, ctx->stream);
+    prof_end(ctx, kProfDet, pb);
     LAUNCHED(1);
   } else {
     if ((rc = map_gradient(ctx, cfg, batch_dev, n, &st, false))) return rc;
   }
   // K4: RMSProp over every vertex (skip g == 0 == the reference's touched set).
+  cudaEvent_t pr = prof_begin(ctx);
   launch_rmsprop((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, 0, ctx->V,
                  cfg->rmsprop_decay, cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, ctx->d_stats,
-                 ctx->stream);
+                 ctx->profiling ? ctx->d_touched : nullptr, ctx->stream);
+  prof_end(ctx, kProfRmsprop, pr);
   LAUNCHED(1);
   CU(cudaGetLastError());
   if ((rc = check_err_flag(ctx))) return rc;
   if ((rc = read_stats(ctx, &st))) return rc;
+  prof_collect(ctx);
   if (st.m_c == 0 || st.bad != INT_MAX) {
     // No update happened (k_rmsprop gated on the stats) — clear the gradient.
     CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * (size_t)ctx->Vpad, ctx->stream));
@@ -335,7 +337,7 @@ int vrf_map_apply(vrf_context* ctx, const vrf_mapping_config* cfg, int64_t verte
   const int64_t end = std::min<int64_t>(vertex_end, ctx->V);
   launch_rmsprop((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, vertex_begin,
                  end, cfg->rmsprop_decay, cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, nullptr,
-                 ctx->stream);
+                 ctx->profiling ? ctx->d_touched : nullptr, ctx->stream);
   LAUNCHED(1);
   CU(cudaGetLastError());
   return VRF_OK;
