@@ -30,6 +30,8 @@ int vrf_context_create(int device, vrf_context** out) {
     return VRF_ERR_CUDA;
   }
   ctx->stream = ctx->own_stream;
+  if (const char* mk = std::getenv("VRF_MAP_KERNEL"))
+    ctx->map_kernel = std::string(mk) == "warp" ? 1 : 0;
   *out = ctx;
   return VRF_OK;
 }
@@ -48,8 +50,10 @@ void vrf_context_destroy(vrf_context* ctx) {
   cudaFree(ctx->d_pose_out);
   cudaFree(ctx->d_pose);
   cudaFree(ctx->d_touched);
+  cudaFree(ctx->d_queue);
   prof_collect(ctx);
-  for (DeviceScratch* s : {&ctx->s_batch, &ctx->s_raycd, &ctx->s_flags, &ctx->s_partials,
+  for (DeviceScratch* s : {&ctx->s_order, &ctx->s_okeys, &ctx->s_okeys2, &ctx->s_oids,
+                           &ctx->s_otmp, &ctx->s_batch, &ctx->s_raycd, &ctx->s_flags, &ctx->s_partials,
                            &ctx->s_count, &ctx->s_offsets, &ctx->s_keys, &ctx->s_keys2,
                            &ctx->s_ids, &ctx->s_ids2, &ctx->s_values, &ctx->s_grad64, &ctx->s_cub,
                            &ctx->s_stage, &ctx->s_out})

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -75,6 +76,12 @@ struct vrf_context {
   long long prof_launches[8] = {0};
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   unsigned long long* d_touched = nullptr;  // RMSProp float4 groups updated
+
+  // warp-per-ray fast path: ray work queues (forward, backward) and ray order
+  int* d_queue = nullptr;
+  vrf_host::DeviceScratch s_order, s_okeys, s_okeys2, s_oids, s_otmp;
+  // fast-path mapping kernels: 0 = thread per ray (coherent order), 1 = warp per ray
+  int map_kernel = 0;
 };
 
 namespace vrf_host {
@@ -287,16 +294,48 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
   DevParams p;
   int rc = resolve_params(ctx, &cfg->render, &p);
   if (rc) return rc;
-  const int nb = map_forward_blocks(n > 0 ? n : 1);
-  if ((rc = ensure(ctx, ctx->s_raycd, sizeof(double4) * (n > 0 ? n : 1)))) return rc;
-  if ((rc = ensure(ctx, ctx->s_flags, n > 0 ? n : 1))) return rc;
+  const bool warp = fast && ctx->map_kernel == 1;
+  const int nb = warp ? warp_kernel_blocks() : map_forward_blocks(n > 0 ? n : 1);
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  if ((rc = ensure(ctx, ctx->s_raycd, sizeof(double4) * nn))) return rc;
+  if ((rc = ensure(ctx, ctx->s_flags, nn))) return rc;
   if ((rc = ensure(ctx, ctx->s_partials, sizeof(MapPartial) * nb))) return rc;
+  if (!ctx->d_queue) CU(cudaMalloc(&ctx->d_queue, sizeof(int) * 4));
   CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
-  if (n > 0) {
+  if (n > 0 && fast) {
+    // (keyframe, Morton tile) ray order for L2 locality, then the warp-per-ray march.
+    const size_t tmp = ray_order_tmp_bytes(n);
+    if ((rc = ensure(ctx, ctx->s_order, sizeof(uint32_t) * nn))) return rc;
+    if ((rc = ensure(ctx, ctx->s_okeys, sizeof(uint32_t) * nn))) return rc;
+    if ((rc = ensure(ctx, ctx->s_okeys2, sizeof(uint32_t) * nn))) return rc;
+    if ((rc = ensure(ctx, ctx->s_oids, sizeof(uint32_t) * nn))) return rc;
+    if ((rc = ensure(ctx, ctx->s_otmp, tmp))) return rc;
+    cudaEvent_t po = prof_begin(ctx);
+    launch_ray_order(batch_dev, n, (uint32_t*)ctx->s_okeys.ptr, (uint32_t*)ctx->s_oids.ptr,
+                     (uint32_t*)ctx->s_okeys2.ptr, (uint32_t*)ctx->s_order.ptr, ctx->s_otmp.ptr,
+                     tmp, ctx->stream);
+    prof_end(ctx, kProfMapMisc, po);
+    LAUNCHED(2);
+    CU(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int) * 4, ctx->stream));
+    cudaEvent_t pb = prof_begin(ctx);
+    if (warp)
+      launch_map_forward_w(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
+                           batch_dev, (const uint32_t*)ctx->s_order.ptr, n,
+                           (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
+                           (MapPartial*)ctx->s_partials.ptr, ctx->d_queue, ctx->d_err,
+                           ctx->stream);
+    else
+      launch_map_forward(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
+                         batch_dev, n, (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
+                         (MapPartial*)ctx->s_partials.ptr, nullptr, ctx->d_err, true,
+                         (const uint32_t*)ctx->s_order.ptr, ctx->stream);
+    prof_end(ctx, kProfMapForward, pb);
+    LAUNCHED(1);
+  } else if (n > 0) {
     cudaEvent_t pb = prof_begin(ctx);
     launch_map_forward(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
                        batch_dev, n, (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
-                       (MapPartial*)ctx->s_partials.ptr, ray_count, ctx->d_err, fast,
+                       (MapPartial*)ctx->s_partials.ptr, ray_count, ctx->d_err, false, nullptr,
                        ctx->stream);
     prof_end(ctx, kProfMapForward, pb);
     LAUNCHED(1);

@@ -46,14 +46,14 @@ void launch_map_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                         const double4* rgbd, const DevPose* poses, int n_frames,
                         const int* batch, int n, double4* ray_cd, uint8_t* flags,
                         MapPartial* partials, int* ray_count, int* err_flag, bool fast,
-                        cudaStream_t s);
+                        const uint32_t* order, cudaStream_t s);
 int map_forward_blocks(int n);
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s);
 void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                          const double4* rgbd, const DevPose* poses, const int* batch, int n,
                          const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
                          const int* global_counts, float4* grad, double lambda_d, bool fast,
-                         cudaStream_t s);
+                         const uint32_t* order, cudaStream_t s);
 void launch_map_backward_records(const DevGrid& g, const DevParams& p, const DevCam& cam,
                                  const double4* rgbd, const DevPose* poses, const int* batch,
                                  int n, const double4* ray_cd, const uint8_t* flags,
@@ -77,6 +77,22 @@ void launch_pose_backward(const DevGrid& g, const DevParams& p, const DevCam& ca
 int pose_backward_blocks(int n);
 void launch_pose_reduce(const PosePartial* partials, int nparts, PosePartial* out,
                         cudaStream_t s);
+
+// Warp-per-ray fast path (vrf_warp.cu).
+int warp_kernel_blocks();
+size_t ray_order_tmp_bytes(int n);
+void launch_ray_order(const int* batch, int n, uint32_t* keys, uint32_t* ids, uint32_t* keys2,
+                      uint32_t* order, void* tmp, size_t tmp_bytes, cudaStream_t s);
+void launch_map_forward_w(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                          const double4* rgbd, const DevPose* poses, int n_frames,
+                          const int* batch, const uint32_t* order, int n, double4* ray_cd,
+                          uint8_t* flags, MapPartial* partials, int* queue, int* err,
+                          cudaStream_t s);
+void launch_map_backward_w(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                           const double4* rgbd, const DevPose* poses, const int* batch,
+                           const uint32_t* order, int n, const double4* ray_cd,
+                           const uint8_t* flags, const MapStats* stats, const int* global_counts,
+                           float* grad, double lambda_d, int* queue, cudaStream_t s);
 
 // Utilities.
 void launch_fill_payload(float* payload, long long n_vertices, float sigma, cudaStream_t s);

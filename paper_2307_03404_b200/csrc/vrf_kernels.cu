@@ -164,15 +164,16 @@ __global__ void __launch_bounds__(kThreads) k_map_forward(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
     double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials,
-    int* __restrict__ ray_count, int* err) {
+    int* __restrict__ ray_count, int* err, const uint32_t* __restrict__ order) {
   __shared__ double s_d[32];
   __shared__ long long s_l[32];
   __shared__ int s_i[32];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (order && t < n) ? (int)order[t] : t;  // coherent ray order when given
   double lp = 0.0, lg = 0.0;
   long long samples = 0;
   int mc = 0, md = 0, bad = INT_MAX;
-  if (i < n) {
+  if (t < n) {
     const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
     uint8_t fl = 0;
     if (f < 0 || f >= n_frames || px < 0 || px >= cam.width || py < 0 || py >= cam.height) {
@@ -337,9 +338,10 @@ __global__ void __launch_bounds__(kThreads) k_map_backward(
     const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
     const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
     const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
-    float4* __restrict__ grad, double lambda_d) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+    float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int i = order ? (int)order[t] : t;  // coherent (keyframe, Morton tile) ray order
   const MapStats st = *stats;
   if (st.bad != INT_MAX) return;  // non-finite loss: the reference throws before updating
   const uint8_t fl = flags[i];
@@ -764,14 +766,16 @@ void launch_map_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                         const double4* rgbd, const DevPose* poses, int n_frames,
                         const int* batch, int n, double4* ray_cd, uint8_t* flags,
                         MapPartial* partials, int* ray_count, int* err, bool fast,
-                        cudaStream_t s) {
+                        const uint32_t* order, cudaStream_t s) {
   const int blocks = map_forward_blocks(n);
   if (fast)
     k_map_forward<float><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, n_frames, batch, n,
-                                                     ray_cd, flags, partials, ray_count, err);
+                                                     ray_cd, flags, partials, ray_count, err,
+                                                     order);
   else
     k_map_forward<double><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, n_frames, batch, n,
-                                                      ray_cd, flags, partials, ray_count, err);
+                                                      ray_cd, flags, partials, ray_count, err,
+                                                      order);
 }
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s) {
   k_map_reduce<<<1, 1024, 0, s>>>(partials, nparts, out);
@@ -780,15 +784,16 @@ void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam
                          const double4* rgbd, const DevPose* poses, const int* batch, int n,
                          const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
                          const int* global_counts, float4* grad, double lambda_d, bool fast,
-                         cudaStream_t s) {
+                         const uint32_t* order, cudaStream_t s) {
   const int blocks = (n + kThreads - 1) / kThreads;
   if (fast)
     k_map_backward<float><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
-                                                      flags, stats, global_counts, grad, lambda_d);
+                                                      flags, stats, global_counts, grad, lambda_d,
+                                                      order);
   else
     k_map_backward<double><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
                                                        flags, stats, global_counts, grad,
-                                                       lambda_d);
+                                                       lambda_d, order);
 }
 void launch_map_backward_records(const DevGrid& g, const DevParams& p, const DevCam& cam,
                                  const double4* rgbd, const DevPose* poses, const int* batch,

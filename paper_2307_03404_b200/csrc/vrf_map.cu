@@ -122,6 +122,26 @@ int grad_deterministic(vrf_context* ctx, const vrf_mapping_config* cfg, const in
   return VRF_OK;
 }
 
+// K2 on the coherent ray order of the preceding forward pass.
+void launch_backward_fast(vrf_context* ctx, const vrf_mapping_config* cfg, const DevParams& p,
+                          const int* batch_dev, int n, const int* global_counts) {
+  cudaEvent_t pb = prof_begin(ctx);
+  if (ctx->map_kernel == 1)
+    launch_map_backward_w(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
+                          batch_dev, (const uint32_t*)ctx->s_order.ptr, n,
+                          (const double4*)ctx->s_raycd.ptr, (const uint8_t*)ctx->s_flags.ptr,
+                          ctx->d_stats, global_counts, ctx->grad, cfg->lambda_d,
+                          ctx->d_queue + 1, ctx->stream);
+  else
+    launch_map_backward(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
+                        batch_dev, n, (const double4*)ctx->s_raycd.ptr,
+                        (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, global_counts,
+                        (float4*)ctx->grad, cfg->lambda_d, /*fast=*/true,
+                        (const uint32_t*)ctx->s_order.ptr, ctx->stream);
+  prof_end(ctx, kProfMapBackward, pb);
+  LAUNCHED(1);
+}
+
 // Fills ctx->grad (fp32) with this batch's gradient. Deterministic mode goes
 // through the sorted fp64 reduce, then rounds once to fp32.
 int map_gradient(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev, int n,
@@ -130,15 +150,7 @@ int map_gradient(vrf_context* ctx, const vrf_mapping_config* cfg, const int* bat
   if (rc) return rc;
   DevParams p;
   if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
-  if (n > 0) {
-    cudaEvent_t pb = prof_begin(ctx);
-    launch_map_backward(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
-                        batch_dev, n, (const double4*)ctx->s_raycd.ptr,
-                        (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, nullptr,
-                        (float4*)ctx->grad, cfg->lambda_d, /*fast=*/true, ctx->stream);
-    prof_end(ctx, kProfMapBackward, pb);
-    LAUNCHED(1);
-  }
+  if (n > 0) launch_backward_fast(ctx, cfg, p, batch_dev, n, nullptr);
   CU(cudaGetLastError());
   if (need_host_stats && (rc = read_stats(ctx, st_out))) return rc;
   return VRF_OK;
@@ -316,13 +328,8 @@ int vrf_map_backward(vrf_context* ctx, const vrf_mapping_config* cfg, int32_t ra
   if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
   const int counts[2] = {rays_color, rays_depth};
   CU(cudaMemcpyAsync(ctx->d_counts, counts, sizeof(counts), cudaMemcpyHostToDevice, ctx->stream));
-  if (ctx->last_n > 0) {
-    launch_map_backward(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
-                        ctx->last_batch, ctx->last_n, (const double4*)ctx->s_raycd.ptr,
-                        (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, ctx->d_counts,
-                        (float4*)ctx->grad, cfg->lambda_d, /*fast=*/true, ctx->stream);
-    LAUNCHED(1);
-  }
+  if (ctx->last_n > 0)
+    launch_backward_fast(ctx, cfg, p, ctx->last_batch, ctx->last_n, ctx->d_counts);
   CU(cudaGetLastError());
   return VRF_OK;
 }
