@@ -332,8 +332,79 @@ __device__ __forceinline__ void map_backward_ray(const DevGrid& g, const DevPara
   }
 }
 
-template <typename ShT>
-__global__ void __launch_bounds__(kThreads) k_map_backward(
+// Scatter corner k of the aggregated cell (slots: sigma, a_ch * basis_m).
+__device__ __forceinline__ void flush_corner(float4* __restrict__ grad, const DevGrid& g,
+                                             uint32_t base, float (&a)[4][8],
+                                             const float (&bf)[9], int k) {
+  const float s = a[0][k], r = a[1][k], gg = a[2][k], b = a[3][k];
+  a[0][k] = a[1][k] = a[2][k] = a[3][k] = 0.f;
+  if (s == 0.f && r == 0.f && gg == 0.f && b == 0.f) return;
+  float v[28];
+  v[0] = s;
+#pragma unroll
+  for (int mm = 0; mm < 9; ++mm) {
+    v[1 + mm] = r * bf[mm];
+    v[10 + mm] = gg * bf[mm];
+    v[19 + mm] = b * bf[mm];
+  }
+  float4* dst = grad + (size_t)corner_index(g, base, k) * kVec4PerVertex;
+#pragma unroll
+  for (int j = 0; j < kVec4PerVertex; ++j)
+    atomicAdd(dst + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+}
+
+// Face-adjacent move along the axis of corner bit BIT (+1 if POS): flush the 4
+// departing corners, carry the 4 shared ones to their new corner slots.
+template <int BIT, bool POS>
+__device__ __forceinline__ void shift_cell(float4* __restrict__ grad, const DevGrid& g,
+                                           uint32_t old_base, float (&a)[4][8],
+                                           const float (&bf)[9]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (((k & BIT) != 0) != POS) flush_corner(grad, g, old_base, a, bf, k);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (k & BIT) continue;
+    const int hi = k | BIT;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (POS) {
+        a[c][k] = a[c][hi];
+        a[c][hi] = 0.f;
+      } else {
+        a[c][hi] = a[c][k];
+        a[c][k] = 0.f;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void move_cell(float4* __restrict__ grad, const DevGrid& g,
+                                          uint32_t old_base, uint32_t new_base, float (&a)[4][8],
+                                          const float (&bf)[9]) {
+  // For valid cells a base difference of +-1 / +-rx / +-rx*ry is exactly a
+  // single-axis unit move (|dcx| <= rx-2, |dcx + rx dcy| < rx*ry).
+  const long long d = (long long)new_base - (long long)old_base;
+  if (d == 1)
+    shift_cell<1, true>(grad, g, old_base, a, bf);
+  else if (d == -1)
+    shift_cell<1, false>(grad, g, old_base, a, bf);
+  else if (d == g.rx)
+    shift_cell<2, true>(grad, g, old_base, a, bf);
+  else if (d == -(long long)g.rx)
+    shift_cell<2, false>(grad, g, old_base, a, bf);
+  else if (d == (long long)g.rxy)
+    shift_cell<4, true>(grad, g, old_base, a, bf);
+  else if (d == -(long long)g.rxy)
+    shift_cell<4, false>(grad, g, old_base, a, bf);
+  else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) flush_corner(grad, g, old_base, a, bf, k);
+  }
+}
+
+template <typename ShT, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
     const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
@@ -352,33 +423,47 @@ __global__ void __launch_bounds__(kThreads) k_map_backward(
   if (!map_upstream(st, global_counts, ray_cd[i], tg, fl, lambda_d, u)) return;
   March m;
   ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+  // Per-ray scatter aggregation. The 28-slot upstream of a sample is
+  // [dL/dsigma, dcol_ch * basis_m] and basis is constant along the ray, so the
+  // contribution to corner k over any run of samples factorises into
+  // a[0][k] = sum w_k up_sigma and a[1+ch][k] = sum w_k dcol_ch (clamp-gated):
+  // 32 registers instead of 224. Corners are flushed (red.global.add.v4.f32)
+  // only when the ray leaves them; corners shared with a face-adjacent next
+  // cell are carried over.
+  float a[4][8];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
+  float bf[9];
+  uint32_t cur = 0xffffffffu;
   map_backward_ray<ShT>(g, p, m, u,
                         [&](int, const Sample& s, const double w[8], double up0,
                             const double dcol[3], const bool clamped[3], const double basis[9]) {
-                          float up[28];
-                          up[0] = (float)up0;
-                          bool any = up0 != 0.0;
+                          if (cur == 0xffffffffu) {
 #pragma unroll
-                          for (int ch = 0; ch < 3; ++ch) {
-                            const bool live = !clamped[ch] && dcol[ch] != 0.0;
-                            any |= live;
-#pragma unroll
-                            for (int mm = 0; mm < 9; ++mm)
-                              up[1 + ch * 9 + mm] = live ? (float)dmul(dcol[ch], basis[mm]) : 0.f;
+                            for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
+                          } else if (s.base != cur) {
+                            move_cell(grad, g, cur, s.base, a, bf);
                           }
-                          if (!any) return;
+                          cur = s.base;
+                          const float u0 = (float)up0;
+                          const float u1 = clamped[0] ? 0.f : (float)dcol[0];
+                          const float u2 = clamped[1] ? 0.f : (float)dcol[1];
+                          const float u3 = clamped[2] ? 0.f : (float)dcol[2];
 #pragma unroll
                           for (int k = 0; k < 8; ++k) {
                             const float wk = (float)w[k];
-                            float4* dst = grad + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
-#pragma unroll
-                            for (int j = 0; j < kVec4PerVertex; ++j) {
-                              const float4 v = make_float4(wk * up[4 * j], wk * up[4 * j + 1],
-                                                           wk * up[4 * j + 2], wk * up[4 * j + 3]);
-                              atomicAdd(dst + j, v);  // red.global.add.v4.f32
-                            }
+                            a[0][k] = fmaf(wk, u0, a[0][k]);
+                            a[1][k] = fmaf(wk, u1, a[1][k]);
+                            a[2][k] = fmaf(wk, u2, a[2][k]);
+                            a[3][k] = fmaf(wk, u3, a[3][k]);
                           }
                         });
+  if (cur != 0xffffffffu) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) flush_corner(grad, g, cur, a, bf, k);
+  }
 }
 
 // ------------------------------------------------------------------ K3 deterministic records
@@ -786,14 +871,23 @@ void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam
                          const int* global_counts, float4* grad, double lambda_d, bool fast,
                          const uint32_t* order, cudaStream_t s) {
   const int blocks = (n + kThreads - 1) / kThreads;
-  if (fast)
-    k_map_backward<float><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
-                                                      flags, stats, global_counts, grad, lambda_d,
-                                                      order);
+  static const int minb = [] {
+    const char* e = getenv("VRF_BWD_MINB");
+    return e ? atoi(e) : 4;
+  }();
+#define VRF_BWD(T, MB)                                                                    \
+  k_map_backward<T, MB><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd, \
+                                                    flags, stats, global_counts, grad,       \
+                                                    lambda_d, order)
+  if (!fast)
+    VRF_BWD(double, 1);
+  else if (minb <= 2)
+    VRF_BWD(float, 2);
+  else if (minb == 3)
+    VRF_BWD(float, 3);
   else
-    k_map_backward<double><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
-                                                       flags, stats, global_counts, grad,
-                                                       lambda_d, order);
+    VRF_BWD(float, 4);
+#undef VRF_BWD
 }
 void launch_map_backward_records(const DevGrid& g, const DevParams& p, const DevCam& cam,
                                  const double4* rgbd, const DevPose* poses, const int* batch,
