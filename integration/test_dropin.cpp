@@ -1,0 +1,173 @@
+// The GPU drop-in (voxrf_gpu_backend.cpp, under the reference's own symbol
+// names) against the reference's original CPU implementation (renamed to
+// voxrf_ref_* by integration/Makefile), on identical inputs.
+#include <doctest.h>
+
+#include <cmath>
+
+#include "test_helpers.hpp"
+#include "voxrf/mapping.hpp"
+#include "voxrf/renderer.hpp"
+#include "voxrf/tracking.hpp"
+
+using namespace voxrf;
+
+extern "C" {
+Frame voxrf_ref_render_image(const VoxelGrid&, const CameraIntrinsics&, const Pose&,
+                             const RenderParams&, int, int);
+MapStepStats voxrf_ref_mapping_step(VoxelGrid&, const std::vector<const Frame*>&,
+                                    const CameraIntrinsics&, const MappingConfig&, RmspropState&,
+                                    Rng&);
+PoseGradient voxrf_ref_pose_gradient(const VoxelGrid&, const Frame&, const CameraIntrinsics&,
+                                     const Pose&, const std::vector<PixelSample>&,
+                                     const TrackingConfig&);
+TrackFrameResult voxrf_ref_track_frame(const VoxelGrid&, const Frame&, const CameraIntrinsics&,
+                                       const Pose&, const TrackingConfig&);
+TrackSequenceResult voxrf_ref_track_sequence(const VoxelGrid&, const Dataset&,
+                                             const TrackingConfig&);
+}
+
+namespace {
+
+// A smooth blob scene with fp32-exact payload (the device stores fp32).
+VoxelGrid blob_grid(int n, double voxel) {
+  GridGeometry geom{Eigen::Vector3i(n, n, n), {0, 0, 0}, voxel};
+  VoxelGrid grid(geom);
+  Rng rng(5);
+  const double c = 0.5 * (n - 1) * voxel;
+  for (int iz = 0; iz < n; ++iz)
+    for (int iy = 0; iy < n; ++iy)
+      for (int ix = 0; ix < n; ++ix) {
+        double* v = grid.vertex(geom.vertex_index(ix, iy, iz));
+        const Eigen::Vector3d p = geom.to_world(Eigen::Vector3d(ix, iy, iz));
+        const double r = (p - Eigen::Vector3d(c, c, c)).norm();
+        v[0] = float(std::max(0.0, 40.0 * (1.0 - std::abs(r - 0.3 * c * 2) / (2.0 * voxel))));
+        for (int m = 0; m < kShPerVertex; ++m) v[1 + m] = float(rng.uniform(-0.3, 0.3));
+      }
+  return grid;
+}
+
+double max_rel(const std::vector<double>& a, const std::vector<double>& b, double floor) {
+  double m = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i)
+    m = std::max(m, std::abs(a[i] - b[i]) / std::max({std::abs(a[i]), std::abs(b[i]), floor}));
+  return m;
+}
+
+struct Scene {
+  VoxelGrid grid;
+  CameraIntrinsics intr{60, 60, 24, 18, 48, 36};
+  std::vector<Frame> frames;
+};
+
+Scene make_scene() {
+  Scene s{blob_grid(17, 0.1), {}, {}};
+  const double c = 0.8;
+  for (int i = 0; i < 4; ++i) {
+    const double a = 0.15 * i;
+    const Pose pose = look_at({c + 1.2 * std::cos(a), c + 1.2 * std::sin(a), c + 0.1},
+                              {c, c, c});
+    Frame f = voxrf_ref_render_image(s.grid, s.intr, pose, RenderParams{}, 1, 1);
+    f.gt_pose = pose;
+    f.timestamp = i / 30.0;
+    s.frames.push_back(std::move(f));
+  }
+  return s;
+}
+
+}  // namespace
+
+TEST_SUITE_BEGIN("dropin");
+
+TEST_CASE("drop-in render_image matches the reference render_image") {
+  Scene s = make_scene();
+  for (int stride : {1, 2, 5}) {
+    const Frame a = render_image(s.grid, s.intr, *s.frames[1].gt_pose, RenderParams{}, stride);
+    const Frame b =
+        voxrf_ref_render_image(s.grid, s.intr, *s.frames[1].gt_pose, RenderParams{}, stride, 1);
+    REQUIRE(a.color.width == b.color.width);
+    CHECK(max_rel(a.color.data, b.color.data, 1e-6) < 1e-10);
+    CHECK(max_rel(a.depth.data, b.depth.data, 1e-6) < 1e-10);
+  }
+  CHECK_THROWS_AS(render_image(s.grid, s.intr, Pose{}, RenderParams{}, 0), std::invalid_argument);
+}
+
+TEST_CASE("drop-in mapping_step matches the reference mapping_step") {
+  Scene s = make_scene();
+  std::vector<const Frame*> kf;
+  for (const Frame& f : s.frames) kf.push_back(&f);
+  VoxelGrid ga(s.grid.geometry(), 0.1), gb(s.grid.geometry(), 0.1);
+  MappingConfig cfg;
+  cfg.rays_per_batch = 512;
+  cfg.deterministic = true;
+  RmspropState ra, rb;
+  Rng rnga(9), rngb(9);
+  for (int step = 0; step < 3; ++step) {
+    const MapStepStats a = mapping_step(ga, kf, s.intr, cfg, ra, rnga);
+    const MapStepStats b = voxrf_ref_mapping_step(gb, kf, s.intr, cfg, rb, rngb);
+    CHECK(a.rays_color == b.rays_color);
+    CHECK(a.rays_depth == b.rays_depth);
+    CHECK(a.loss_total == doctest::Approx(b.loss_total).epsilon(1e-5));
+    // fp32 device parameters vs the reference's fp64 grid
+    double worst = 0.0, scale = 0.0;
+    for (std::size_t i = 0; i < ga.data().size(); ++i) {
+      worst = std::max(worst, std::abs(ga.data()[i] - gb.data()[i]));
+      scale = std::max(scale, std::abs(gb.data()[i]));
+    }
+    CHECK(worst <= 2e-5 * scale);
+    // the next step starts from identical fp32-rounded parameters
+    for (std::size_t i = 0; i < gb.data().size(); ++i) gb.data()[i] = ga.data()[i];
+    rb.v = ra.v;
+  }
+  std::vector<const Frame*> none;
+  CHECK_THROWS_AS(mapping_step(ga, none, s.intr, cfg, ra, rnga), std::runtime_error);
+}
+
+TEST_CASE("drop-in pose_gradient and track_frame match the reference") {
+  Scene s = make_scene();
+  Rng rng(3);
+  std::vector<PixelSample> px;
+  for (int i = 0; i < 300; ++i)
+    px.push_back({int(rng.uniform_index(s.intr.width)), int(rng.uniform_index(s.intr.height))});
+  Pose pose = *s.frames[2].gt_pose;
+  pose.t += Eigen::Vector3d(0.01, -0.015, 0.005);
+  TrackingConfig tc;
+  const PoseGradient a = pose_gradient(s.grid, s.frames[2], s.intr, pose, px, tc);
+  const PoseGradient b = voxrf_ref_pose_gradient(s.grid, s.frames[2], s.intr, pose, px, tc);
+  CHECK(a.rays_used == b.rays_used);
+  CHECK(a.loss == doctest::Approx(b.loss).epsilon(1e-10));
+  CHECK((a.d_tau - b.d_tau).norm() <= 1e-8 * b.d_tau.norm() + 1e-14);
+  CHECK((a.d_omega - b.d_omega).norm() <= 1e-8 * b.d_omega.norm() + 1e-14);
+
+  tc.rays_per_iteration = 256;
+  tc.iterations = 12;
+  const TrackFrameResult ta = track_frame(s.grid, s.frames[2], s.intr, pose, tc);
+  const TrackFrameResult tb = voxrf_ref_track_frame(s.grid, s.frames[2], s.intr, pose, tc);
+  CHECK(ta.iterations_run == tb.iterations_run);
+  CHECK((ta.pose.t - tb.pose.t).norm() < 1e-6);
+  CHECK(std::abs(ta.pose.q.coeffs().dot(tb.pose.q.coeffs())) > 1.0 - 1e-12);
+  CHECK(max_rel(ta.loss_trace, tb.loss_trace, 1e-9) < 1e-8);
+
+  CHECK_THROWS_AS(pose_gradient(s.grid, s.frames[2], s.intr, pose, {}, tc), std::runtime_error);
+  CHECK_THROWS_AS(pose_gradient(s.grid, s.frames[2], s.intr, pose, {{s.intr.width, 0}}, tc),
+                  std::out_of_range);
+}
+
+TEST_CASE("drop-in track_sequence matches the reference trajectory") {
+  Scene s = make_scene();
+  Dataset ds;
+  ds.intrinsics = s.intr;
+  ds.frames = s.frames;
+  TrackingConfig tc;
+  tc.rays_per_iteration = 256;
+  tc.iterations = 8;
+  const TrackSequenceResult a = track_sequence(s.grid, ds, tc);
+  const TrackSequenceResult b = voxrf_ref_track_sequence(s.grid, ds, tc);
+  REQUIRE(a.trajectory.size() == b.trajectory.size());
+  for (std::size_t i = 0; i < a.trajectory.size(); ++i) {
+    CHECK((a.trajectory.poses[i].t - b.trajectory.poses[i].t).norm() < 1e-6);  // << 1 mm
+    CHECK(std::abs(a.trajectory.poses[i].q.coeffs().dot(b.trajectory.poses[i].q.coeffs())) > 1.0 - 1e-12);
+  }
+}
+
+TEST_SUITE_END();

@@ -1,0 +1,332 @@
+// The reference-side C++ binding of libvoxrf_b200: drop-in definitions of the
+// voxrf batch entry points with the reference's exact signatures, exception
+// types and messages, implemented on the C-ABI in include/voxrf_b200.h.
+//
+//   render_image   renderer.hpp:83-84   (renderer.cpp:149-174)
+//   mapping_step   mapping.hpp:80-82    (mapping.cpp:114-233)
+//   map_scene      mapping.hpp:98-99    (mapping.cpp:278-316)
+//   pose_gradient  tracking.hpp:70-73   (tracking.cpp:76-143)
+//   track_frame    tracking.hpp:82-84   (tracking.cpp:170-252)
+//   track_sequence tracking.hpp:102-103 (tracking.cpp:254-295)
+//
+// A maintainer compiles this TU against the reference headers
+// (proj/include/voxrf) and links it in place of those six definitions
+// (INTEGRATION.md); everything else (VoxelGrid, per-ray CPU functions used by
+// tests and gradcheck, dataset/eval/CLI) is unchanged.
+#include <chrono>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "voxrf/mapping.hpp"
+#include "voxrf/renderer.hpp"
+#include "voxrf/tracking.hpp"
+#include "voxrf_b200.h"
+
+namespace voxrf {
+namespace {
+
+vrf_context* ctx() {
+  static vrf_context* c = [] {
+    vrf_context* h = nullptr;
+    const char* dev = std::getenv("VOXRF_DEVICE");
+    const int rc = vrf_context_create(dev ? std::atoi(dev) : 0, &h);
+    if (rc != VRF_OK)
+      throw std::runtime_error("voxrf_b200: no usable CUDA device (status " +
+                               std::to_string(rc) + "); there is no CPU fallback");
+    return h;
+  }();
+  return c;
+}
+
+void check(int rc) {
+  if (rc == VRF_OK) return;
+  const std::string msg = vrf_last_error(ctx());
+  if (rc == VRF_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (rc == VRF_ERR_OUT_OF_RANGE) throw std::out_of_range(msg);
+  throw std::runtime_error(msg);
+}
+
+vrf_grid_geometry to_c(const GridGeometry& g) {
+  vrf_grid_geometry o{};
+  for (int a = 0; a < 3; ++a) {
+    o.res[a] = g.res[a];
+    o.origin[a] = g.origin[a];
+  }
+  o.voxel_size = g.voxel_size;
+  return o;
+}
+vrf_intrinsics to_c(const CameraIntrinsics& i) {
+  return vrf_intrinsics{i.fx, i.fy, i.cx, i.cy, i.width, i.height, i.depth_scale};
+}
+vrf_pose to_c(const Pose& p) {
+  return vrf_pose{{p.q.w(), p.q.x(), p.q.y(), p.q.z()}, {p.t.x(), p.t.y(), p.t.z()}};
+}
+Pose from_c(const vrf_pose& p) {
+  Pose o;
+  o.q = Eigen::Quaterniond(p.q[0], p.q[1], p.q[2], p.q[3]);
+  o.t = Eigen::Vector3d(p.t[0], p.t[1], p.t[2]);
+  return o;
+}
+vrf_render_params to_c(const RenderParams& r) {
+  return vrf_render_params{r.step, r.t_near, r.t_far, r.termination_eps};
+}
+
+void upload_grid(const VoxelGrid& grid) {
+  const vrf_grid_geometry g = to_c(grid.geometry());
+  check(vrf_grid_upload(ctx(), &g, grid.data().data(), grid.occupancy().data()));
+}
+
+void upload_frames(const CameraIntrinsics& intr, const std::vector<const Frame*>& frames) {
+  std::vector<const double*> colors, depths;
+  std::vector<vrf_pose> poses;
+  for (const Frame* f : frames) {
+    colors.push_back(f->color.data.data());
+    depths.push_back(f->depth.data.data());
+    poses.push_back(to_c(f->gt_pose ? *f->gt_pose : Pose{}));
+  }
+  const vrf_intrinsics ic = to_c(intr);
+  check(vrf_frames_upload(ctx(), &ic, int(frames.size()), colors.data(), depths.data(),
+                          poses.data()));
+}
+
+vrf_mapping_config to_c(const MappingConfig& c) {
+  vrf_mapping_config o{};
+  o.lambda_d = c.lambda_d;
+  o.lr_sigma = c.lr_sigma;
+  o.lr_sh = c.lr_sh;
+  o.rmsprop_decay = c.rmsprop_decay;
+  o.rmsprop_eps = c.rmsprop_eps;
+  o.deterministic = c.deterministic ? 1 : 0;
+  o.render = to_c(c.render);
+  return o;
+}
+
+// mapping.cpp:121-128: the batch is drawn single-threaded from the caller's Rng.
+std::vector<int32_t> draw_batch(Rng& rng, int n_frames, const CameraIntrinsics& intr, int n) {
+  std::vector<int32_t> b(3 * std::size_t(n));
+  for (int i = 0; i < n; ++i) {
+    b[3 * i] = int32_t(rng.uniform_index(std::uint64_t(n_frames)));
+    b[3 * i + 1] = int32_t(rng.uniform_index(std::uint64_t(intr.width)));
+    b[3 * i + 2] = int32_t(rng.uniform_index(std::uint64_t(intr.height)));
+  }
+  return b;
+}
+
+MapStepStats to_stats(const vrf_map_step_stats& s) {
+  MapStepStats o;
+  o.loss_photometric = s.loss_photometric;
+  o.loss_geometric = s.loss_geometric;
+  o.loss_total = s.loss_total;
+  o.rays_color = s.rays_color;
+  o.rays_depth = s.rays_depth;
+  o.psnr_estimate = s.psnr_estimate;
+  return o;
+}
+
+vrf_tracking_config to_c(const TrackingConfig& c) {
+  vrf_tracking_config o{};
+  o.rays_per_iteration = c.rays_per_iteration;
+  o.iterations = c.iterations;
+  o.lr_omega = c.lr_omega;
+  o.lr_tau = c.lr_tau;
+  o.beta1 = c.beta1;
+  o.beta2 = c.beta2;
+  o.adam_eps = c.adam_eps;
+  o.lambda_p = c.lambda_p;
+  o.lambda_d = c.lambda_d;
+  o.convergence_step = c.convergence_step;
+  o.divergence_factor = c.divergence_factor;
+  o.divergence_patience = c.divergence_patience;
+  o.max_redraws = c.max_redraws;
+  o.seed = c.seed;
+  o.render = to_c(c.render);
+  return o;
+}
+
+TrackFrameResult track_uploaded(int frame, const CameraIntrinsics& intr, const Pose& init,
+                                const TrackingConfig& config) {
+  const vrf_intrinsics ic = to_c(intr);
+  const vrf_pose pc = to_c(init);
+  const vrf_tracking_config tc = to_c(config);
+  vrf_track_frame_result r{};
+  std::vector<double> trace(std::size_t(std::max(config.iterations, 1)));
+  check(vrf_track_frame(ctx(), frame, &ic, &pc, &tc, &r, trace.data()));
+  TrackFrameResult out;
+  out.pose = from_c(r.pose);
+  out.failed = r.failed != 0;
+  out.iterations_run = r.iterations_run;
+  out.loss_trace.assign(trace.begin(), trace.begin() + r.iterations_run);
+  return out;
+}
+
+}  // namespace
+
+Frame render_image(const VoxelGrid& grid, const CameraIntrinsics& intr, const Pose& pose,
+                   const RenderParams& params, int stride, int /*threads*/) {
+  if (stride < 1) throw std::invalid_argument("render_image: stride must be >= 1");
+  const int out_w = (intr.width + stride - 1) / stride;
+  const int out_h = (intr.height + stride - 1) / stride;
+  Frame frame;
+  frame.color = ImageF(out_w, out_h, 3);
+  frame.depth = ImageF(out_w, out_h, 1);
+  frame.gt_pose = pose;
+  upload_grid(grid);
+  const vrf_intrinsics ic = to_c(intr);
+  const vrf_pose pc = to_c(pose);
+  const vrf_render_params rp = to_c(params);
+  check(vrf_render_image(ctx(), &ic, &pc, &rp, stride, frame.color.data.data(),
+                         frame.depth.data.data()));
+  return frame;
+}
+
+MapStepStats mapping_step(VoxelGrid& grid, const std::vector<const Frame*>& keyframes,
+                          const CameraIntrinsics& intrinsics, const MappingConfig& config,
+                          RmspropState& rmsprop, Rng& rng) {
+  if (keyframes.empty()) throw std::runtime_error("mapping_step: no keyframes");
+  const std::vector<int32_t> batch =
+      draw_batch(rng, int(keyframes.size()), intrinsics, config.rays_per_batch);
+  upload_grid(grid);
+  upload_frames(intrinsics, keyframes);
+  if (rmsprop.v.size() == grid.data().size())
+    check(vrf_rmsprop_upload(ctx(), rmsprop.v.data()));
+  else
+    check(vrf_rmsprop_reset(ctx()));
+  const vrf_mapping_config cc = to_c(config);
+  vrf_map_step_stats st{};
+  check(vrf_mapping_step(ctx(), &cc, batch.data(), config.rays_per_batch, &st));
+  // In-place contract (mapping.hpp:80): grid and RMSProp state are updated.
+  check(vrf_grid_download(ctx(), grid.data().data(), nullptr));
+  rmsprop.v.resize(grid.data().size());
+  check(vrf_rmsprop_download(ctx(), rmsprop.v.data()));
+  return to_stats(st);
+}
+
+MapResult map_scene(const Dataset& dataset, const MappingConfig& config,
+                    const std::optional<GridGeometry>& geometry) {
+  if (dataset.frames.empty()) throw std::runtime_error("map_scene: empty dataset");
+  std::vector<const Frame*> keyframes;
+  for (std::size_t i = 0; i < dataset.frames.size(); i += config.keyframe_stride) {
+    if (!dataset.frames[i].gt_pose)
+      throw std::runtime_error("map_scene: keyframe " + std::to_string(i) + " has no pose");
+    keyframes.push_back(&dataset.frames[i]);
+  }
+  const GridGeometry geom = geometry ? *geometry : fit_grid_geometry(dataset, keyframes, config);
+  MapResult result{VoxelGrid(geom, config.sigma_init), {}};
+  Rng rng(config.seed);
+  upload_frames(dataset.intrinsics, keyframes);
+  const vrf_mapping_config cc = to_c(config);
+  const auto t0 = std::chrono::steady_clock::now();
+  int iteration = 0;
+  for (int stage = 0; stage <= config.upsample_stages; ++stage) {
+    if (stage > 0) result.grid = result.grid.upsampled(config.max_resolution);
+    // The grid and its RMSProp state stay on the device for the whole stage.
+    upload_grid(result.grid);
+    check(vrf_rmsprop_reset(ctx()));
+    for (int it = 0; it < config.iterations_per_stage; ++it, ++iteration) {
+      const std::vector<int32_t> batch =
+          draw_batch(rng, int(keyframes.size()), dataset.intrinsics, config.rays_per_batch);
+      vrf_map_step_stats st{};
+      check(vrf_mapping_step(ctx(), &cc, batch.data(), config.rays_per_batch, &st));
+      if (config.prune_every > 0 && (iteration + 1) % config.prune_every == 0) {
+        int64_t off = 0;
+        check(vrf_grid_prune(ctx(), config.prune_threshold, &off));
+      }
+      MapLogRow row;
+      row.iteration = iteration;
+      row.stats = to_stats(st);
+      row.elapsed_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+              .count();
+      result.log.push_back(row);
+    }
+    std::vector<std::uint8_t> occ(result.grid.occupancy().size());
+    check(vrf_grid_download(ctx(), result.grid.data().data(), occ.data()));
+    const GridGeometry& g = result.grid.geometry();
+    for (int cz = 0; cz < g.res.z() - 1; ++cz)
+      for (int cy = 0; cy < g.res.y() - 1; ++cy)
+        for (int cx = 0; cx < g.res.x() - 1; ++cx)
+          result.grid.set_cell_active(cx, cy, cz, occ[g.cell_index(cx, cy, cz)] != 0);
+  }
+  return result;
+}
+
+PoseGradient pose_gradient(const VoxelGrid& grid, const Frame& frame,
+                           const CameraIntrinsics& intrinsics, const Pose& pose,
+                           const std::vector<PixelSample>& pixels, const TrackingConfig& config) {
+  if (pixels.empty()) throw std::runtime_error("pose_gradient: empty pixel set");
+  upload_grid(grid);
+  upload_frames(intrinsics, {&frame});
+  std::vector<int32_t> px(2 * pixels.size());
+  for (std::size_t i = 0; i < pixels.size(); ++i) {
+    px[2 * i] = pixels[i].px;
+    px[2 * i + 1] = pixels[i].py;
+  }
+  const vrf_intrinsics ic = to_c(intrinsics);
+  const vrf_pose pc = to_c(pose);
+  const vrf_tracking_loss lc{config.lambda_p, config.lambda_d, to_c(config.render)};
+  vrf_pose_gradient_result r{};
+  check(vrf_pose_gradient(ctx(), 0, &ic, &pc, px.data(), int(pixels.size()), &lc, &r));
+  PoseGradient out;
+  out.d_omega = Eigen::Vector3d(r.d_omega[0], r.d_omega[1], r.d_omega[2]);
+  out.d_tau = Eigen::Vector3d(r.d_tau[0], r.d_tau[1], r.d_tau[2]);
+  out.loss = r.loss;
+  out.rays_used = r.rays_used;
+  return out;
+}
+
+TrackFrameResult track_frame(const VoxelGrid& grid, const Frame& frame,
+                             const CameraIntrinsics& intrinsics, const Pose& init,
+                             const TrackingConfig& config) {
+  if (config.iterations == 0) {
+    TrackFrameResult r;
+    r.pose = init;
+    return r;
+  }
+  upload_grid(grid);
+  upload_frames(intrinsics, {&frame});
+  return track_uploaded(0, intrinsics, init, config);
+}
+
+TrackSequenceResult track_sequence(const VoxelGrid& grid, const Dataset& dataset,
+                                   const TrackingConfig& config) {
+  if (dataset.frames.empty()) throw std::runtime_error("track_sequence: empty dataset");
+  if (!dataset.frames.front().gt_pose)
+    throw std::runtime_error("track_sequence: first frame needs a pose");
+  upload_grid(grid);
+  std::vector<const Frame*> all;
+  for (const Frame& f : dataset.frames) all.push_back(&f);
+  upload_frames(dataset.intrinsics, all);
+
+  TrackSequenceResult result;
+  const Pose first = *dataset.frames.front().gt_pose;
+  result.trajectory.push(dataset.frames.front().timestamp, first);
+  result.status.push_back({0, 0, 0.0, 0.0, false});
+  Pose prev = first, prev_prev = first;
+  bool have_two = false;
+  for (std::size_t i = 1; i < dataset.frames.size(); ++i) {
+    Pose init = prev;
+    if (config.init_policy == TrackingConfig::Init::kConstantVelocity && have_two)
+      init = prev * (prev_prev.inverse() * prev);
+    TrackingConfig fc = config;
+    fc.seed = config.seed + 0x9e3779b9u * std::uint64_t(i);
+    const auto t0 = std::chrono::steady_clock::now();
+    const TrackFrameResult tf =
+        fc.iterations == 0 ? TrackFrameResult{init, {}, false, 0}
+                           : track_uploaded(int(i), dataset.intrinsics, init, fc);
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    result.trajectory.push(dataset.frames[i].timestamp, tf.pose);
+    result.status.push_back({int(i), tf.iterations_run,
+                             tf.loss_trace.empty() ? 0.0 : tf.loss_trace.back(), ms, tf.failed});
+    if (!tf.failed) {
+      prev_prev = prev;
+      prev = tf.pose;
+      have_two = true;
+    }
+  }
+  return result;
+}
+
+}  // namespace voxrf

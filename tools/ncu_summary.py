@@ -56,12 +56,23 @@ def main():
             if key in idx:
                 print(f"| {desc} (`{key}`) | {r[idx[key]]} | {units[idx[key]]} |")
         try:
-            rd = float(r[idx["dram__bytes_read.sum"]].replace(",", ""))
-            wr = float(r[idx["dram__bytes_write.sum"]].replace(",", ""))
-            u = units[idx["dram__bytes_read.sum"]]
-            print(f"\nDRAM traffic per launch: {rd + wr:.3f} {u}\n")
+            rd = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]])
+            wr = to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
+            print(f"\nDRAM traffic per launch (read + write): {(rd + wr) / 1e9:.3f} GB\n")
+            if len(sys.argv) > 3:  # profiles/traffic.json entry for bench.py roofline.traffic
+                import json
+                from pathlib import Path
+                p = Path(sys.argv[3])
+                d = json.loads(p.read_text()) if p.exists() else {}
+                d[sys.argv[4] if len(sys.argv) > 4 else name] = rd + wr
+                p.write_text(json.dumps(d, indent=1) + "\n")
         except (KeyError, ValueError):
             pass
+
+
+def to_bytes(v, unit):
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    return float(v.replace(",", "")) * scale.get(unit.strip(), 1)
 
 
 if __name__ == "__main__":
