@@ -220,6 +220,23 @@ class Oracle:
         _check(rc, f"mapping_step (bad_ray={st.bad_ray}, rays_color={st.rays_color})")
         return data, v, grad, st
 
+    def mapping_grad_global(self, grid, frames, intr, cfg, batch, m_color, m_depth):
+        data = np.ascontiguousarray(grid.data, np.float64)
+        active = np.ascontiguousarray(grid.active, np.uint8)
+        gs = Grid(geometry(grid.geom), data.ctypes.data, active.ctypes.data)
+        fh = _FramesHold(frames)
+        grad = np.zeros_like(data)
+        b = np.ascontiguousarray(batch, np.int32).reshape(-1, 3)
+        st = MapStats()
+        mc = MapCfg(cfg.lambda_d, cfg.lr_sigma, cfg.lr_sh, cfg.rmsprop_decay, cfg.rmsprop_eps,
+                    params_s(cfg.render))
+        rc = self.lib.or_mapping_grad_global(C.byref(gs), fh.arr, len(frames),
+                                             C.byref(intr_s(intr)), C.byref(mc), _ptr(b),
+                                             b.shape[0], int(m_color), int(m_depth), _ptr(grad),
+                                             C.byref(st))
+        _check(rc, "mapping_grad_global")
+        return grad, st
+
     def pose_gradient(self, grid, frame, intr, pose, pixels, lambda_p, lambda_d, params):
         h = _GridHold(grid)
         fh = _FramesHold([frame])

@@ -578,10 +578,35 @@ static int depth_valid(const or_frame* f, const or_intrinsics* in, int x, int y)
   return f->depth[(size_t)y * in->width + x] > 0.0; /* frame.hpp:18 */
 }
 
+static int mapping_step_impl(or_grid* g, const or_frame* frames, int n_frames,
+                             const or_intrinsics* intr, const or_mapping_config* cfg,
+                             const int32_t* batch, int n_rays, double* rms_v, double* grad_out,
+                             int apply, or_map_stats* st, int m_color_global,
+                             int m_depth_global);
+
 int or_mapping_step(or_grid* g, const or_frame* frames, int n_frames,
                     const or_intrinsics* intr, const or_mapping_config* cfg,
                     const int32_t* batch, int n_rays, double* rms_v, double* grad_out,
                     int apply, or_map_stats* st) {
+  return mapping_step_impl(g, frames, n_frames, intr, cfg, batch, n_rays, rms_v, grad_out,
+                           apply, st, 0, 0);
+}
+
+/* A rank's share of a ray-sharded step: the gradient of this
+ * rank's rays with the upstream normalised by the GLOBAL hit counts. */
+int or_mapping_grad_global(or_grid* g, const or_frame* frames, int n_frames,
+                           const or_intrinsics* intr, const or_mapping_config* cfg,
+                           const int32_t* batch, int n_rays, int m_color, int m_depth,
+                           double* grad_out, or_map_stats* st) {
+  return mapping_step_impl(g, frames, n_frames, intr, cfg, batch, n_rays, NULL, grad_out, 0, st,
+                           m_color, m_depth);
+}
+
+static int mapping_step_impl(or_grid* g, const or_frame* frames, int n_frames,
+                             const or_intrinsics* intr, const or_mapping_config* cfg,
+                             const int32_t* batch, int n_rays, double* rms_v, double* grad_out,
+                             int apply, or_map_stats* st, int m_color_global,
+                             int m_depth_global) {
   memset(st, 0, sizeof(*st));
   st->bad_ray = -1;
   if (n_frames <= 0) return OR_RUNTIME; /* "mapping_step: no keyframes" */
@@ -605,6 +630,10 @@ int or_mapping_step(or_grid* g, const or_frame* frames, int n_frames,
   }
   st->rays_color = m_color;
   st->rays_depth = m_depth;
+  if (m_color_global > 0) { /* ray-sharded step: normalise by the global counts */
+    m_color = m_color_global;
+    m_depth = m_depth_global;
+  }
   if (rc == OR_OK && m_color == 0) rc = OR_RUNTIME; /* "mapping_step: no ray hit the grid" */
 
   double* buf = NULL;

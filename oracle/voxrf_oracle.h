@@ -135,6 +135,12 @@ int or_mapping_step(or_grid* g, const or_frame* frames, int n_frames,
                     const or_intrinsics* intr, const or_mapping_config* cfg,
                     const int32_t* batch, int n_rays, double* rms_v, double* grad_out,
                     int apply, or_map_stats* stats);
+/* One rank's share of a ray-sharded step: this batch's gradient with the upstream
+ * normalised by the global hit counts (no update). */
+int or_mapping_grad_global(or_grid* g, const or_frame* frames, int n_frames,
+                           const or_intrinsics* intr, const or_mapping_config* cfg,
+                           const int32_t* batch, int n_rays, int m_color, int m_depth,
+                           double* grad_out, or_map_stats* stats);
 /* tracking.cpp:76-143 */
 int or_pose_gradient(const or_grid* g, const or_frame* frame, const or_intrinsics* intr,
                      const or_pose* pose, const int32_t* pixels, int n,

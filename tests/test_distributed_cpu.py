@@ -1,0 +1,128 @@
+"""Multi-GPU mapping orchestration (paper_2307_03404_b200/distributed.py) on CPU:
+world size 2 over gloo, with an oracle-backed engine standing in for the GPU
+context. One ray-sharded step (forward -> all-reduce of the partials -> backward
+with the GLOBAL hit counts -> reduce-scatter -> RMSProp on the owned vertex
+shard -> all-gather) must equal a single-process mapping_step over the
+concatenated batch."""
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+class OracleEngine:
+    """CPU engine with the GpuEngine interface (oracle restatement underneath)."""
+
+    def __init__(self, grid, frames, intr, cfg, world):
+        import oracle as orc
+        self.o = orc.Oracle()
+        self.grid, self.frames, self.intr, self.cfg = grid, frames, intr, cfg
+        self.num_vertices = grid.geom.num_vertices
+        self.padded = (self.num_vertices + world - 1) // world * world
+        self.payload = torch.zeros(self.padded * 28, dtype=torch.float64)
+        self.payload[: self.num_vertices * 28] = torch.from_numpy(grid.data.reshape(-1))
+        self.grad = torch.zeros(self.padded * 28, dtype=torch.float64)
+        self.v = torch.zeros(self.padded * 28, dtype=torch.float64)
+        self.batch = None
+
+    def _grid(self):
+        g = self.grid.copy()
+        g.data = self.payload[: self.num_vertices * 28].numpy().reshape(-1, 28).copy()
+        return g
+
+    def forward(self, batch):
+        self.batch = batch.numpy()
+        try:
+            _, _, _, st = self.o.mapping_step(self._grid(), self.frames, self.intr, self.cfg,
+                                              self.batch, apply=False)
+        except RuntimeError:  # no local hit
+            return 0, 0, -1, 0.0, 0.0, 0
+        return (st.rays_color, st.rays_depth, st.bad_ray,
+                st.loss_photometric * st.rays_color,
+                st.loss_geometric * max(st.rays_depth, 1) if st.rays_depth else 0.0, st.samples)
+
+    def backward(self, m_color, m_depth):
+        grad, _ = self.o.mapping_grad_global(self._grid(), self.frames, self.intr, self.cfg,
+                                             self.batch, m_color, m_depth)
+        self.grad[: self.num_vertices * 28] += torch.from_numpy(grad.reshape(-1))
+
+    def apply(self, v0, v1):
+        """mapping.cpp:218-231 on the owned vertex shard."""
+        s = slice(v0 * 28, min(v1, self.num_vertices) * 28)
+        g, v, th = self.grad[s], self.v[s], self.payload[s]
+        nz = g != 0
+        slot = (torch.arange(s.start, s.stop) % 28)
+        lr = torch.where(slot == 0, torch.tensor(self.cfg.lr_sigma, dtype=torch.float64),
+                         torch.tensor(self.cfg.lr_sh, dtype=torch.float64))
+        rho = self.cfg.rmsprop_decay
+        vn = rho * v + (1.0 - rho) * g * g
+        v[nz] = vn[nz]
+        th[nz] = th[nz] - lr[nz] * g[nz] / torch.sqrt(v[nz] + self.cfg.rmsprop_eps)
+        self.grad[v0 * 28: v1 * 28] = 0.0
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "oracle"))
+    sys.path.insert(0, str(ROOT / "tests"))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2307_03404_b200.api import MappingConfig
+    from paper_2307_03404_b200.distributed import DistributedMapper
+    from scenes import fresh_grid, room_scene
+
+    grid, intr, frames = room_scene()
+    g0 = fresh_grid(grid)
+    cfg = MappingConfig()
+    import oracle as orc
+    full = orc.Oracle().draw_batch(31, len(frames), intr.width, intr.height, 400)
+    mine = torch.from_numpy(np.array_split(full, world)[rank].copy())
+    eng = OracleEngine(g0, frames, intr, cfg, world)
+    res = DistributedMapper(eng).step(mine, cfg.lambda_d)
+    if rank == 0:
+        np.save(Path(out_dir) / "dist_payload.npy", eng.payload[: eng.num_vertices * 28].numpy())
+        np.save(Path(out_dir) / "dist_stats.npy",
+                np.array([res.loss_total, res.rays_color, res.rays_depth, res.samples]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_ray_sharded_step_equals_single_process(tmp_path, oracle):
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    from paper_2307_03404_b200.api import MappingConfig
+    from scenes import fresh_grid, room_scene
+
+    grid, intr, frames = room_scene()
+    g0 = fresh_grid(grid)
+    full = oracle.draw_batch(31, len(frames), intr.width, intr.height, 400)
+    data, _, _, st = oracle.mapping_step(g0, frames, intr, MappingConfig(), full)
+    got = np.load(tmp_path / "dist_payload.npy").reshape(-1, 28)
+    np.testing.assert_allclose(got, data, rtol=1e-9, atol=1e-9 * np.abs(data).max())
+    stats = np.load(tmp_path / "dist_stats.npy")
+    assert stats[1] == st.rays_color and stats[2] == st.rays_depth and stats[3] == st.samples
+    assert abs(stats[0] - st.loss_total) <= 1e-12 * st.loss_total
+
+
+def test_shard_ranges_cover_padded_vertices():
+    from paper_2307_03404_b200.distributed import shard_range
+    for world in (1, 2, 4, 8):
+        padded = 4913 + (-4913) % world
+        spans = [shard_range(padded, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == padded
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
