@@ -61,7 +61,8 @@ struct Scene {
 };
 
 Scene make_scene() {
-  Scene s{blob_grid(17, 0.1), {}, {}};
+  Scene s{blob_grid(17, 0.1)};
+  REQUIRE(s.intr.width == 48);
   const double c = 0.8;
   for (int i = 0; i < 4; ++i) {
     const double a = 0.15 * i;
@@ -86,6 +87,7 @@ TEST_CASE("drop-in render_image matches the reference render_image") {
     const Frame b =
         voxrf_ref_render_image(s.grid, s.intr, *s.frames[1].gt_pose, RenderParams{}, stride, 1);
     REQUIRE(a.color.width == b.color.width);
+    REQUIRE(a.color.data.size() > 0);
     CHECK(max_rel(a.color.data, b.color.data, 1e-6) < 1e-10);
     CHECK(max_rel(a.depth.data, b.depth.data, 1e-6) < 1e-10);
   }
