@@ -382,7 +382,9 @@ def run_ours(args):
         tframes = render_frames(gt_ctx, intr, tposes)
         gt_ctx.load_frames(intr, tframes)
         gn = GNConfig(rays_per_iteration=16384, iterations=10)
+        gt_ctx.track_frame_gn(1, intr, tposes[0], gn)  # warm-up (allocations)
         torch.cuda.synchronize()
+        gt_ctx.profile_enable(True)
         errs = []
         t0 = time.perf_counter()
         prev = tposes[0]
@@ -391,9 +393,13 @@ def run_ours(args):
             prev = r.pose
             errs.append(np.linalg.norm(np.asarray(r.pose.t) - np.asarray(tposes[i].t)))
         dt = time.perf_counter() - t0
+        tp = gt_ctx.profile_read()
+        gt_ctx.profile_enable(False)
+        nf = len(tframes) - 1
         tracking = {"config": "config2: 1200x680, 257^3 map, GN/LM 16384 rays x 10 it",
-                    "frames_per_s": (len(tframes) - 1) / dt,
-                    "ms_per_frame": 1e3 * dt / (len(tframes) - 1),
+                    "frames_per_s": nf / dt, "ms_per_frame": 1e3 * dt / nf,
+                    "kernel_ms_per_frame": {k: tp[k][0] / nf for k in ("pose_forward",
+                                                                       "pose_backward")},
                     "ate_rmse_m": float(np.sqrt(np.mean(np.square(errs))))}
 
     # ---- CPU baseline (rank 0, N=1)

@@ -16,7 +16,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libvoxrf_b200.so"
-SOURCES = ["vrf_kernels.cu", "vrf_warp.cu", "vrf_capi.cu", "vrf_map.cu", "vrf_pose.cu"]
+SOURCES = ["vrf_kernels.cu", "vrf_warp.cu", "vrf_track.cu", "vrf_capi.cu", "vrf_map.cu", "vrf_pose.cu"]
 HEADERS = ["vrf_device.cuh", "vrf_internal.h", "vrf_context.h"]
 
 NVCC_FLAGS = [

@@ -51,6 +51,12 @@ void vrf_context_destroy(vrf_context* ctx) {
   cudaFree(ctx->d_pose);
   cudaFree(ctx->d_touched);
   cudaFree(ctx->d_queue);
+  cudaFree(ctx->d_nblocks);
+  cudaFree(ctx->d_frame);
+  cudaFree(ctx->d_gn_pose);
+  cudaFree(ctx->d_gn_seed);
+  cudaFree(ctx->d_gn_hist);
+  if (ctx->gn_graph) cudaGraphExecDestroy(ctx->gn_graph);
   prof_collect(ctx);
   for (DeviceScratch* s : {&ctx->s_order, &ctx->s_okeys, &ctx->s_okeys2, &ctx->s_oids,
                            &ctx->s_otmp, &ctx->s_batch, &ctx->s_raycd, &ctx->s_flags, &ctx->s_partials,
@@ -131,6 +137,7 @@ int vrf_grid_init(vrf_context* ctx, const vrf_grid_geometry* geom, double sigma_
   launch_fill_payload(ctx->payload, ctx->V, (float)sigma_init, ctx->stream);
   LAUNCHED(1);
   CU(cudaMemsetAsync(ctx->occ, 0xFF, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1), ctx->stream));
+  update_blocks(ctx);
   CU(cudaStreamSynchronize(ctx->stream));
   return VRF_OK;
 }
@@ -166,6 +173,7 @@ int vrf_grid_upload(vrf_context* ctx, const vrf_grid_geometry* geom, const doubl
     LAUNCHED(1);
   }
   if ((rc = upload_occupancy_u8(ctx, occupancy))) return rc;
+  update_blocks(ctx);
   CU(cudaStreamSynchronize(ctx->stream));
   return VRF_OK;
 }
@@ -185,6 +193,7 @@ int vrf_grid_upload_f32(vrf_context* ctx, const vrf_grid_geometry* geom, const f
   } else {
     CU(cudaMemsetAsync(ctx->occ, 0xFF, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1), ctx->stream));
   }
+  update_blocks(ctx);
   CU(cudaStreamSynchronize(ctx->stream));
   return VRF_OK;
 }
@@ -241,6 +250,7 @@ int vrf_grid_prune(vrf_context* ctx, double tau, int64_t* deactivated) {
   CU(cudaMemsetAsync(ctx->s_out.ptr, 0, sizeof(unsigned long long), ctx->stream));
   launch_prune(dev_grid(ctx), ctx->occ, tau, (unsigned long long*)ctx->s_out.ptr, ctx->stream);
   LAUNCHED(1);
+  update_blocks(ctx);
   unsigned long long n = 0;
   CU(cudaMemcpyAsync(&n, ctx->s_out.ptr, sizeof(n), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));

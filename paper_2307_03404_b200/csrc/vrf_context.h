@@ -43,6 +43,10 @@ struct vrf_context {
   float* grad = nullptr;
   float* rms = nullptr;
   uint32_t* occ = nullptr;
+  uint32_t* bocc = nullptr;  // 8^3-cell block occupancy (empty-space skipping)
+  int bdim[3] = {0, 0, 0};
+  bool all_blocks_active = false;
+  unsigned int* d_nblocks = nullptr;
 
   // frames
   int n_frames = 0;
@@ -82,6 +86,17 @@ struct vrf_context {
   vrf_host::DeviceScratch s_order, s_okeys, s_okeys2, s_oids, s_otmp;
   // fast-path mapping kernels: 0 = thread per ray (coherent order), 1 = warp per ray
   int map_kernel = 0;
+
+  // tracking device state: frame index, Gauss-Newton pose / seed / history, and the
+  // CUDA graph of one GN frame (re-captured when its key changes)
+  int* d_frame = nullptr;
+  DevPose* d_gn_pose = nullptr;
+  unsigned long long* d_gn_seed = nullptr;
+  double* d_gn_hist = nullptr;
+  int gn_hist_cap = 0;
+  long long grid_generation = 0;
+  cudaGraphExec_t gn_graph = nullptr;
+  std::vector<unsigned char> gn_key;
 };
 
 namespace vrf_host {
@@ -128,8 +143,10 @@ inline void free_grid(vrf_context* ctx) {
   cudaFree(ctx->grad);
   cudaFree(ctx->rms);
   cudaFree(ctx->occ);
+  cudaFree(ctx->bocc);
   ctx->payload = ctx->grad = ctx->rms = nullptr;
   ctx->occ = nullptr;
+  ctx->bocc = nullptr;
   ctx->has_grid = false;
 }
 
@@ -155,10 +172,15 @@ inline int alloc_grid(vrf_context* ctx, const vrf_grid_geometry* g) {
   ctx->C = (long long)(g->res[0] - 1) * (g->res[1] - 1) * (g->res[2] - 1);
   const long long m = ctx->shard_multiple;
   ctx->Vpad = (ctx->V + m - 1) / m * m;
+  ++ctx->grid_generation;  // invalidates captured graphs that baked the old pointers
   CU(cudaMalloc(&ctx->payload, sizeof(float) * 28 * ctx->Vpad));
   CU(cudaMalloc(&ctx->grad, sizeof(float) * 28 * ctx->Vpad));
   CU(cudaMalloc(&ctx->rms, sizeof(float) * 28 * ctx->Vpad));
   CU(cudaMalloc(&ctx->occ, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1)));
+  for (int a = 0; a < 3; ++a)
+    ctx->bdim[a] = (g->res[a] - 1 + (1 << kBlockLog2) - 1) >> kBlockLog2;
+  const long long nblk = (long long)ctx->bdim[0] * ctx->bdim[1] * ctx->bdim[2];
+  CU(cudaMalloc(&ctx->bocc, sizeof(uint32_t) * ((nblk + 31) / 32 + 1)));
   CU(cudaMemsetAsync(ctx->payload, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
   CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
   CU(cudaMemsetAsync(ctx->rms, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
@@ -188,7 +210,27 @@ inline DevGrid dev_grid(const vrf_context* ctx) {
   g.inv_voxel = 1.0 / q.voxel_size;
   g.payload = reinterpret_cast<const float4*>(ctx->payload);
   g.occ = ctx->occ;
+  g.bocc = ctx->bocc;
+  g.bx = ctx->bdim[0];
+  g.by = ctx->bdim[1];
+  g.bz = ctx->bdim[2];
+  g.all_blocks_active = ctx->all_blocks_active ? 1 : 0;
   return g;
+}
+
+// Rebuild the 8^3-cell block occupancy after any change of the cell occupancy
+// (synchronous: occupancy changes are per upload / prune, not per step).
+inline int update_blocks(vrf_context* ctx) {
+  if (!ctx->d_nblocks) CU(cudaMalloc(&ctx->d_nblocks, sizeof(unsigned int)));
+  launch_block_occupancy(ctx->occ, ctx->geom.res[0], ctx->geom.res[1], ctx->geom.res[2],
+                         ctx->bdim[0], ctx->bdim[1], ctx->bdim[2], ctx->bocc, ctx->d_nblocks,
+                         ctx->stream);
+  ctx->launches += 1;
+  unsigned int n = 0;
+  CU(cudaMemcpyAsync(&n, ctx->d_nblocks, sizeof(n), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->all_blocks_active = (long long)n == (long long)ctx->bdim[0] * ctx->bdim[1] * ctx->bdim[2];
+  return VRF_OK;
 }
 
 // RenderParams::effective_step/effective_t_far (renderer.hpp:18-24) and the

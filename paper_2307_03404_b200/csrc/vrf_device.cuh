@@ -44,7 +44,14 @@ struct DevGrid {
   double inv_voxel;       // 1 / voxel (spatial gradient scale, voxel_grid.cpp:136)
   const float4* __restrict__ payload;  // [V][7]
   const uint32_t* __restrict__ occ;    // 1 bit per cell, cell_index order
+  // Coarse occupancy: 1 bit per block of kBlock^3 cells (any active cell -> 1);
+  // lets the march jump over empty blocks without changing the sample set.
+  const uint32_t* __restrict__ bocc;
+  int bx, by, bz;
+  int all_blocks_active;  // host-known: no empty block, the jump can be compiled out
 };
+
+constexpr int kBlockLog2 = 3;  // 8^3-cell blocks
 
 // RenderParams after effective_step / effective_t_far (renderer.hpp:18-24).
 struct DevParams {
@@ -159,6 +166,7 @@ struct Sample {
   double fx, fy, fz;
   uint32_t base;   // vertex_index(cell)
   uint32_t cell;   // cell_index(cell)
+  int cx, cy, cz;  // cell coordinates
 };
 
 // try_locate — voxel_grid.cpp:83-105 — for the segment midpoint, plus the
@@ -179,6 +187,9 @@ __device__ __forceinline__ bool locate(const DevGrid& g, const double p[3], Samp
   s.fz = dsub(gz, (double)cz);
   s.base = (uint32_t)(cx + g.rx * (cy + (long long)g.ry * cz));
   s.cell = (uint32_t)(cx + (g.rx - 1) * (cy + (long long)(g.ry - 1) * cz));
+  s.cx = cx;
+  s.cy = cy;
+  s.cz = cz;
   return true;
 }
 
@@ -186,7 +197,38 @@ __device__ __forceinline__ bool cell_active(const DevGrid& g, uint32_t cell) {
   return (__ldg(g.occ + (cell >> 5)) >> (cell & 31)) & 1u;
 }
 
+__device__ __forceinline__ bool block_active(const DevGrid& g, int cx, int cy, int cz) {
+  const int b = (cx >> kBlockLog2) + g.bx * ((cy >> kBlockLog2) + g.by * (cz >> kBlockLog2));
+  return (__ldg(g.bocc + (b >> 5)) >> (b & 31)) & 1u;
+}
+
+// The sample at s lies in an all-inactive 8^3-cell block: return the first
+// segment index whose midpoint may lie beyond the block. Every segment between
+// has its midpoint inside the (convex) block box — the ray is inside the box at
+// s.t and until the box exit t_out — and would be dropped by the occupancy test,
+// so skipping them leaves the schedule unchanged. A 1e-6 m margin keeps the
+// jump clear of the exit face.
+__device__ __forceinline__ long long skip_empty_block(const DevGrid& g, const March& m,
+                                                      const Sample& s) {
+  const double ext = (double)(1 << kBlockLog2) * g.voxel;
+  const int b[3] = {s.cx >> kBlockLog2, s.cy >> kBlockLog2, s.cz >> kBlockLog2};
+  const double org[3] = {g.ox, g.oy, g.oz};
+  double t_out = 1e300;
+  for (int a = 0; a < 3; ++a) {
+    if (m.d[a] == 0.0) continue;
+    const double face = org[a] + (m.d[a] > 0.0 ? (b[a] + 1) : b[a]) * ext;
+    const double t = (face - m.o[a]) / m.d[a];
+    t_out = t < t_out ? t : t_out;
+  }
+  // midpoint of segment k is ~ lo + (k + 0.5) step; stay below t_out - margin
+  const double kf = floor((t_out - 1e-6 - m.lo) / m.step - 0.5);
+  const long long k_new = kf > (double)m.nseg ? m.nseg : (long long)kf;
+  return k_new > m.k ? k_new : m.k;
+}
+
 // Next scheduled, in-bounds, active sample — renderer.cpp:62-79 evaluated lazily.
+// SKIP = false compiles out the empty-block jump (grids with every block occupied).
+template <bool SKIP = true>
 __device__ __forceinline__ bool march_next(const DevGrid& g, March& m, Sample& s) {
   while (m.k < m.nseg) {
     const double s0 = dadd(m.lo, dmul((double)m.k, m.step));
@@ -199,7 +241,10 @@ __device__ __forceinline__ bool march_next(const DevGrid& g, March& m, Sample& s
     const double p[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
                          dadd(m.o[2], dmul(tm, m.d[2]))};
     if (!locate(g, p, s)) continue;
-    if (!cell_active(g, s.cell)) continue;
+    if (!cell_active(g, s.cell)) {
+      if (SKIP && !block_active(g, s.cx, s.cy, s.cz)) m.k = skip_empty_block(g, m, s);
+      continue;
+    }
     s.t = tm;
     s.delta = len;
     return true;
@@ -293,6 +338,43 @@ __device__ __forceinline__ double composite_step(Composite& st, const Shade& sh,
   ++st.count;
   if (st.T < eps) st.terminated = true;
   return w;
+}
+
+__device__ __forceinline__ void ray_from_pixel(const DevCam& cam, const DevPose& pose, double u,
+                                               double v, March& m) {
+  generate_dir(cam, pose, u, v, m.d);
+  m.o[0] = pose.t[0];
+  m.o[1] = pose.t[1];
+  m.o[2] = pose.t[2];
+}
+
+// Forward render of one ray: composite until termination. Returns false if the
+// SH basis precondition fails (sh_eval throws, voxel_grid.cpp:35-36).
+template <typename ShT>
+__device__ __forceinline__ bool render_forward(const DevGrid& g, const DevParams& p, March& m,
+                                               Composite& st, double basis[9]) {
+  st.T = 1.0;
+  st.C[0] = st.C[1] = st.C[2] = 0.0;
+  st.D = 0.0;
+  st.count = 0;
+  st.terminated = false;
+  if (!sh_basis(m.d, basis)) return false;
+  if (!march_begin(g, p, m)) return true;
+  Sample s;
+  while (march_next(g, m, s)) {
+    double w[8];
+    corner_weights(s, w);
+    Shade sh;
+    shade<ShT>(g, s, w, basis, sh);
+    double decay;
+    composite_step(st, sh, s.t, s.delta, p.eps, decay);
+    if (st.terminated) break;
+  }
+  if (st.count == 0) {
+    st.C[0] = st.C[1] = st.C[2] = 0.0;
+    st.D = 0.0;
+  }
+  return true;
 }
 
 // ---------------------------------------------------------------- reductions

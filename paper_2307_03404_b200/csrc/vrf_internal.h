@@ -69,20 +69,39 @@ void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, l
 void launch_pose_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                          const double4* rgbd, const DevPose* pose, const int* pixels, int n,
                          double4* ray_cd, uint8_t* flags, PoseCount* counts, int* err_flag,
-                         cudaStream_t s);
+                         const uint32_t* order, cudaStream_t s);
 void launch_pose_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                           const double4* rgbd, const DevPose* pose, const int* pixels, int n,
                           const double4* ray_cd, const uint8_t* flags, double lambda_p,
-                          double lambda_d, PosePartial* partials, cudaStream_t s);
+                          double lambda_d, PosePartial* partials, const uint32_t* order,
+                          cudaStream_t s);
 int pose_backward_blocks(int n);
 void launch_pose_reduce(const PosePartial* partials, int nparts, PosePartial* out,
                         cudaStream_t s);
+
+// Tracking (vrf_track.cu).
+int pose_fused_blocks(int n);
+void launch_pose_fused(bool fp64_sh, const DevGrid& g, const DevParams& p, const DevCam& cam,
+                       const double4* rgbd_base, const int* frame_idx, long long npix,
+                       const DevPose* pose, const int* pixels, const uint32_t* order, int n,
+                       double lambda_p, double lambda_d, PosePartial* partials, int* err,
+                       cudaStream_t s);
+void launch_pose_reduce2(const PosePartial* partials, int nparts, PosePartial* out,
+                         cudaStream_t s);
+void launch_draw_strat(const double4* rgbd_base, const int* frame_idx, long long npix, int width,
+                       int height, int tiles_log2, int max_redraws,
+                       const unsigned long long* seed, int iteration, int* pixels, int n,
+                       cudaStream_t s);
+void launch_gn_step(const PosePartial* ne, DevPose* pose, double damping, double* hist,
+                    int iteration, cudaStream_t s);
 
 // Warp-per-ray fast path (vrf_warp.cu).
 int warp_kernel_blocks();
 size_t ray_order_tmp_bytes(int n);
 void launch_ray_order(const int* batch, int n, uint32_t* keys, uint32_t* ids, uint32_t* keys2,
                       uint32_t* order, void* tmp, size_t tmp_bytes, cudaStream_t s);
+void launch_pixel_order(const int* pixels, int n, uint32_t* keys, uint32_t* ids, uint32_t* keys2,
+                        uint32_t* order, void* tmp, size_t tmp_bytes, cudaStream_t s);
 void launch_map_forward_w(const DevGrid& g, const DevParams& p, const DevCam& cam,
                           const double4* rgbd, const DevPose* poses, int n_frames,
                           const int* batch, const uint32_t* order, int n, double4* ray_cd,
@@ -106,5 +125,7 @@ void launch_pack_frames(const double* color, const double* depth, double4* rgbd,
                         cudaStream_t s);
 void launch_prune(const DevGrid& g, uint32_t* occ_bits, double tau, unsigned long long* count,
                   cudaStream_t s);
+void launch_block_occupancy(const uint32_t* occ, int rx, int ry, int rz, int bx, int by, int bz,
+                            uint32_t* bocc, unsigned int* n_active, cudaStream_t s);
 
 }  // namespace vrf

@@ -82,45 +82,54 @@ int pose_pass(vrf_context* ctx, int frame, const vrf_intrinsics* intr, const vrf
   if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
   const size_t pix_bytes = sizeof(int32_t) * 2 * (size_t)n;
   if ((rc = ensure(ctx, ctx->s_batch, pix_bytes))) return rc;
-  if ((rc = ensure(ctx, ctx->s_raycd, sizeof(double4) * n))) return rc;
-  if ((rc = ensure(ctx, ctx->s_flags, n))) return rc;
-  const int nb = pose_backward_blocks(n);
+  const int nb = pose_fused_blocks(n);
   if ((rc = ensure(ctx, ctx->s_partials, sizeof(PosePartial) * nb))) return rc;
-  if ((rc = ensure_pinned(ctx, pix_bytes + sizeof(DevPose)))) return rc;
+  if ((rc = ensure_pinned(ctx, pix_bytes + sizeof(DevPose) + sizeof(int)))) return rc;
+  if (!ctx->d_frame) CU(cudaMalloc(&ctx->d_frame, sizeof(int)));
   std::memcpy(ctx->h_pinned, pixels, pix_bytes);
   const DevPose dp = dev_pose(pose);
   std::memcpy((char*)ctx->h_pinned + pix_bytes, &dp, sizeof(DevPose));
+  std::memcpy((char*)ctx->h_pinned + pix_bytes + sizeof(DevPose), &frame, sizeof(int));
   CU(cudaMemcpyAsync(ctx->s_batch.ptr, ctx->h_pinned, pix_bytes, cudaMemcpyHostToDevice,
                      ctx->stream));
   CU(cudaMemcpyAsync(ctx->d_pose, (char*)ctx->h_pinned + pix_bytes, sizeof(DevPose),
                      cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMemsetAsync(ctx->d_pcount, 0, sizeof(PoseCount), ctx->stream));
+  CU(cudaMemcpyAsync(ctx->d_frame, (char*)ctx->h_pinned + pix_bytes + sizeof(DevPose),
+                     sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
   const long long npix = (long long)intr->width * intr->height;
-  const double4* rgbd = ctx->rgbd + npix * frame;
   const DevGrid g = dev_grid(ctx);
   const DevCam cam = dev_cam(intr);
-  launch_pose_forward(g, p, cam, rgbd, ctx->d_pose, (const int*)ctx->s_batch.ptr, n,
-                      (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr, ctx->d_pcount,
-                      ctx->d_err, ctx->stream);
-  launch_pose_backward(g, p, cam, rgbd, ctx->d_pose, (const int*)ctx->s_batch.ptr, n,
-                       (const double4*)ctx->s_raycd.ptr, (const uint8_t*)ctx->s_flags.ptr,
-                       cfg->lambda_p, cfg->lambda_d, (PosePartial*)ctx->s_partials.ptr,
-                       ctx->stream);
-  launch_pose_reduce((const PosePartial*)ctx->s_partials.ptr, nb, ctx->d_pose_out, ctx->stream);
-  LAUNCHED(3);
+  // coherent (Morton 4x4-tile) pixel order for the per-ray kernels
+  const size_t tmp = ray_order_tmp_bytes(n);
+  if ((rc = ensure(ctx, ctx->s_order, sizeof(uint32_t) * n))) return rc;
+  if ((rc = ensure(ctx, ctx->s_okeys, sizeof(uint32_t) * n))) return rc;
+  if ((rc = ensure(ctx, ctx->s_okeys2, sizeof(uint32_t) * n))) return rc;
+  if ((rc = ensure(ctx, ctx->s_oids, sizeof(uint32_t) * n))) return rc;
+  if ((rc = ensure(ctx, ctx->s_otmp, tmp))) return rc;
+  const uint32_t* order = (const uint32_t*)ctx->s_order.ptr;
+  launch_pixel_order((const int*)ctx->s_batch.ptr, n, (uint32_t*)ctx->s_okeys.ptr,
+                     (uint32_t*)ctx->s_oids.ptr, (uint32_t*)ctx->s_okeys2.ptr,
+                     (uint32_t*)ctx->s_order.ptr, ctx->s_otmp.ptr, tmp, ctx->stream);
+  // K5: forward + Jacobian in one pass per ray, FP64 SH (the reference-parity path)
+  cudaEvent_t pb = prof_begin(ctx);
+  launch_pose_fused(/*fp64_sh=*/true, g, p, cam, ctx->rgbd, ctx->d_frame, npix, ctx->d_pose,
+                    (const int*)ctx->s_batch.ptr, order, n, cfg->lambda_p, cfg->lambda_d,
+                    (PosePartial*)ctx->s_partials.ptr, ctx->d_err, ctx->stream);
+  prof_end(ctx, kProfPoseBackward, pb);
+  launch_pose_reduce2((const PosePartial*)ctx->s_partials.ptr, nb, ctx->d_pose_out, ctx->stream);
+  LAUNCHED(4);
   CU(cudaGetLastError());
   if ((rc = check_err_flag(ctx))) return rc;
   PosePartial out;
-  PoseCount cnt;
   CU(cudaMemcpyAsync(&out, ctx->d_pose_out, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaMemcpyAsync(&cnt, ctx->d_pcount, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  prof_collect(ctx);
   std::memcpy(res->jtj, out.jtj, sizeof(res->jtj));
   std::memcpy(res->jtr, out.jtr, sizeof(res->jtr));
   res->loss = out.loss;
-  res->m = cnt.m;
-  res->samples = cnt.samples;
+  res->m = out.m;
+  res->samples = out.samples;
   return VRF_OK;
 }
 
@@ -402,28 +411,105 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
   if (cfg->iterations <= 0) return VRF_OK;
   if (frame < 0 || frame >= ctx->n_frames)
     return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "track_frame: frame index out of range");
-  const std::vector<double>& depth = ctx->host_depth[frame];
-  Xoshiro rng(cfg->seed);
-  const vrf_tracking_loss lc{cfg->lambda_p, cfg->lambda_d, cfg->render};
-  vrf_pose pose = *init;
-  std::vector<int32_t> px;
-  int rc;
-  for (int it = 0; it < cfg->iterations; ++it) {
-    draw_valid_pixels(depth, intr->width, intr->height, cfg->rays_per_iteration, cfg->max_redraws,
-                      rng, px);
-    if (px.empty())
-      return set_err(ctx, VRF_ERR_RUNTIME, "track_frame: no valid-depth pixels to sample");
-    PoseResult r;
-    if ((rc = pose_pass(ctx, frame, intr, &pose, px.data(), (int)px.size() / 2, &lc, &r))) return rc;
-    if (r.m == 0)
-      return set_err(ctx, VRF_ERR_RUNTIME, "untrackable frame: all sampled rays miss the grid");
-    res.final_loss = r.loss / r.m;
-    ++res.iterations_run;
-    double x[6];
-    if (!solve_lm(r.jtj, r.jtr, cfg->damping, x)) break;
-    apply_perturbation(x, x + 3, &pose);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if ((rc = check_frames(ctx, intr))) return rc;
+  DevParams p;
+  if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
+  // stratified draws over a 2^L x 2^L tile grid: n = 4^L rays per iteration
+  int L = 0;
+  while ((4LL << (2 * L)) <= (long long)std::max(cfg->rays_per_iteration, 1)) ++L;
+  const int n = 1 << (2 * L);
+  const int iters = cfg->iterations;
+  const int nb = pose_fused_blocks(n);
+  if ((rc = ensure(ctx, ctx->s_batch, sizeof(int32_t) * 2 * (size_t)n))) return rc;
+  if ((rc = ensure(ctx, ctx->s_partials, sizeof(PosePartial) * nb))) return rc;
+  if (!ctx->d_frame) CU(cudaMalloc(&ctx->d_frame, sizeof(int)));
+  if (!ctx->d_gn_pose) CU(cudaMalloc(&ctx->d_gn_pose, sizeof(DevPose)));
+  if (!ctx->d_gn_seed) CU(cudaMalloc(&ctx->d_gn_seed, sizeof(unsigned long long)));
+  if (ctx->gn_hist_cap < iters) {
+    cudaFree(ctx->d_gn_hist);
+    CU(cudaMalloc(&ctx->d_gn_hist, sizeof(double) * 2 * iters));
+    ctx->gn_hist_cap = iters;
+    if (ctx->gn_graph) cudaGraphExecDestroy(ctx->gn_graph);
+    ctx->gn_graph = nullptr;
   }
-  res.pose = pose;
+  const DevGrid g = dev_grid(ctx);
+  const DevCam cam = dev_cam(intr);
+  const long long npix = (long long)intr->width * intr->height;
+  // graph key: everything baked into the captured kernel parameters
+  std::vector<unsigned char> key;
+  auto put = [&key](const void* v, size_t b) {
+    key.insert(key.end(), (const unsigned char*)v, (const unsigned char*)v + b);
+  };
+  put(&g, sizeof(g));
+  put(&p, sizeof(p));
+  put(&cam, sizeof(cam));
+  put(&n, sizeof(n));
+  put(&iters, sizeof(iters));
+  put(&cfg->lambda_p, sizeof(double));
+  put(&cfg->lambda_d, sizeof(double));
+  put(&cfg->damping, sizeof(double));
+  put(&cfg->max_redraws, sizeof(int));
+  put(&ctx->rgbd, sizeof(void*));
+  put(&ctx->s_batch.ptr, sizeof(void*));
+  put(&ctx->s_partials.ptr, sizeof(void*));
+  put(&ctx->stream, sizeof(void*));
+  put(&ctx->grid_generation, sizeof(long long));
+  if (!ctx->gn_graph || key != ctx->gn_key) {
+    if (ctx->gn_graph) cudaGraphExecDestroy(ctx->gn_graph);
+    ctx->gn_graph = nullptr;
+    cudaGraph_t graph;
+    CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    for (int it = 0; it < iters; ++it) {
+      launch_draw_strat(ctx->rgbd, ctx->d_frame, npix, intr->width, intr->height, L,
+                        cfg->max_redraws, ctx->d_gn_seed, it, (int*)ctx->s_batch.ptr, n,
+                        ctx->stream);
+      launch_pose_fused(/*fp64_sh=*/false, g, p, cam, ctx->rgbd, ctx->d_frame, npix,
+                        ctx->d_gn_pose, (const int*)ctx->s_batch.ptr, nullptr, n, cfg->lambda_p,
+                        cfg->lambda_d, (PosePartial*)ctx->s_partials.ptr, ctx->d_err,
+                        ctx->stream);
+      launch_pose_reduce2((const PosePartial*)ctx->s_partials.ptr, nb, ctx->d_pose_out,
+                          ctx->stream);
+      launch_gn_step(ctx->d_pose_out, ctx->d_gn_pose, cfg->damping, ctx->d_gn_hist, it,
+                     ctx->stream);
+    }
+    CU(cudaStreamEndCapture(ctx->stream, &graph));
+    CU(cudaGraphInstantiate(&ctx->gn_graph, graph, 0));
+    cudaGraphDestroy(graph);
+    ctx->gn_key = key;
+  }
+  // per-frame inputs: init pose, frame index, seed
+  if ((rc = ensure_pinned(ctx, sizeof(DevPose) + 16 + sizeof(double) * 2 * iters))) return rc;
+  char* h = (char*)ctx->h_pinned;
+  const DevPose dp = dev_pose(init);
+  const unsigned long long seed = cfg->seed ^ (0x9e3779b97f4a7c15ULL * (unsigned long long)(frame + 1));
+  std::memcpy(h, &dp, sizeof(DevPose));
+  std::memcpy(h + sizeof(DevPose), &frame, sizeof(int));
+  std::memcpy(h + sizeof(DevPose) + 8, &seed, sizeof(seed));
+  CU(cudaMemcpyAsync(ctx->d_gn_pose, h, sizeof(DevPose), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->d_frame, h + sizeof(DevPose), sizeof(int), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(ctx->d_gn_seed, h + sizeof(DevPose) + 8, sizeof(seed),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+  cudaEvent_t pb = prof_begin(ctx);
+  CU(cudaGraphLaunch(ctx->gn_graph, ctx->stream));
+  prof_end(ctx, kProfPoseBackward, pb);
+  LAUNCHED(4LL * iters);
+  DevPose fin;
+  double* hist = (double*)(h + sizeof(DevPose) + 16);
+  CU(cudaMemcpyAsync(&fin, ctx->d_gn_pose, sizeof(DevPose), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(hist, ctx->d_gn_hist, sizeof(double) * 2 * iters, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  if ((rc = check_err_flag(ctx))) return rc;  // syncs the stream
+  prof_collect(ctx);
+  if (hist[1] == 0.0)
+    return set_err(ctx, VRF_ERR_RUNTIME, "untrackable frame: all sampled rays miss the grid");
+  for (int a = 0; a < 4; ++a) res.pose.q[a] = fin.q[a];
+  for (int a = 0; a < 3; ++a) res.pose.t[a] = fin.t[a];
+  res.iterations_run = iters;
+  res.final_loss = hist[2 * (iters - 1)];
   *out = res;
   return VRF_OK;
 }

@@ -390,7 +390,22 @@ __global__ void k_ray_keys(const int* __restrict__ batch, int n, uint32_t* keys,
   ids[i] = (uint32_t)i;
 }
 
+// Tracking pixels (px, py): Morton order of 4x4-pixel tiles.
+__global__ void k_pixel_keys(const int* __restrict__ px, int n, uint32_t* keys, uint32_t* ids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t x = (uint32_t)px[2 * i] >> 2, y = (uint32_t)px[2 * i + 1] >> 2;
+  keys[i] = spread_bits(x) | (spread_bits(y) << 1);
+  ids[i] = (uint32_t)i;
+}
+
 }  // namespace
+
+void launch_pixel_order(const int* pixels, int n, uint32_t* keys, uint32_t* ids, uint32_t* keys2,
+                        uint32_t* order, void* tmp, size_t tmp_bytes, cudaStream_t s) {
+  k_pixel_keys<<<(n + 255) / 256, 256, 0, s>>>(pixels, n, keys, ids);
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, ids, order, n, 0, 32, s);
+}
 
 int warp_kernel_blocks() { return 148 * 8; }
 
