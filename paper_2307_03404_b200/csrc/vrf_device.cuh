@@ -274,9 +274,60 @@ struct Shade {
   bool clamped[3];
 };
 
+// Fast path (fp32 SH): the colour is contracted with the basis per corner,
+// c_ch = 0.5 + sum_k w_k (sum_m basis_m v_k[ch,m]), so only 3 accumulators are
+// live instead of 27. sigma_raw stays the FP64 reference-order replay, so T and
+// the termination decision are unchanged; colour differs from the reference's
+// accumulate-then-contract order at the fp32 rounding level (~1e-7).
+__device__ __forceinline__ void shade_fast(const DevGrid& g, const Sample& s, const double w[8],
+                                           const float bf[9], Shade& out) {
+  double sraw = 0.0;
+  float cr = 0.f, cg = 0.f, cb = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4* vp = g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
+    float v[28];
+#pragma unroll
+    for (int j = 0; j < kVec4PerVertex; ++j) {
+      const float4 a = __ldg(vp + j);
+      v[4 * j] = a.x;
+      v[4 * j + 1] = a.y;
+      v[4 * j + 2] = a.z;
+      v[4 * j + 3] = a.w;
+    }
+    sraw = dadd(sraw, dmul(w[k], (double)v[0]));
+    float dr = 0.f, dg = 0.f, db = 0.f;
+#pragma unroll
+    for (int m = 0; m < 9; ++m) {
+      dr = fmaf(bf[m], v[1 + m], dr);
+      dg = fmaf(bf[m], v[10 + m], dg);
+      db = fmaf(bf[m], v[19 + m], db);
+    }
+    const float wk = (float)w[k];
+    cr = fmaf(wk, dr, cr);
+    cg = fmaf(wk, dg, cg);
+    cb = fmaf(wk, db, cb);
+  }
+  out.sigma_raw = sraw;
+  const float cc[3] = {cr, cg, cb};
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const double v = 0.5 + (double)cc[ch];
+    out.clamped[ch] = (v <= 0.0 || v >= 1.0);
+    out.c[ch] = (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);
+  }
+}
+
 template <typename ShT>
 __device__ __forceinline__ void shade(const DevGrid& g, const Sample& s, const double w[8],
                                       const double basis[9], Shade& out) {
+  if constexpr (sizeof(ShT) == 4) {
+    float bf[9];
+#pragma unroll
+    for (int m = 0; m < 9; ++m) bf[m] = (float)basis[m];
+    shade_fast(g, s, w, bf, out);
+    return;
+  }
   double sraw = 0.0;
   ShT sh[27];
 #pragma unroll
