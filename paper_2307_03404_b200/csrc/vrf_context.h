@@ -208,6 +208,7 @@ inline DevGrid dev_grid(const vrf_context* ctx) {
   g.hz = q.origin[2] + ((double)q.res[2] - 1.0) * q.voxel_size;
   g.voxel = q.voxel_size;
   g.inv_voxel = 1.0 / q.voxel_size;
+  g.rcp_voxel = 1.0 / q.voxel_size;
   g.payload = reinterpret_cast<const float4*>(ctx->payload);
   g.occ = ctx->occ;
   g.bocc = ctx->bocc;

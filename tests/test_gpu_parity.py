@@ -35,6 +35,35 @@ def test_sample_schedule_and_cell_ids_bit_exact(ctx, oracle):
         assert np.array_equal(cells[i, :counts[i]], c0)
 
 
+def test_cell_location_on_lattice_faces_bit_exact(ctx, oracle):
+    """Axis-aligned rays whose segment midpoints land on cell faces (g within an
+    ulp of an integer, voxel 0.1 not representable): exact faces resolve to the
+    lower cell (voxel_grid.cpp:88-90); the device's division-free locate must
+    agree with the reference's IEEE division bit for bit."""
+    rng = np.random.default_rng(11)
+    geom = synth.GridGeometry((33, 33, 33), (0.0, 0.0, 0.0), 0.1)
+    grid = VoxelGrid(geom, 1.0)
+    grid.active[rng.uniform(size=geom.num_cells) < 0.3] = 0
+    ctx.load_grid(grid)
+    rays = []
+    for axis in range(3):
+        for sgn in (1.0, -1.0):
+            for _ in range(40):
+                o = rng.integers(1, 32, 3) * 0.1 + rng.choice([0.0, 0.05], 3)
+                o[axis] = -0.1 if sgn > 0 else 3.3
+                d = np.zeros(3)
+                d[axis] = sgn
+                rays.append(np.concatenate([o, d]))
+    rays = np.array(rays)
+    params = RenderParams(step=0.2, t_near=0.0)
+    counts, t, delta, cells = ctx.sample_rays(rays, params, cap=64)
+    for i, row in enumerate(rays):
+        t0, d0, c0 = oracle.sample_ray(grid, row[:3], row[3:], params)
+        assert counts[i] == len(t0)
+        assert np.array_equal(cells[i, :counts[i]], c0)
+        assert np.array_equal(t[i, :counts[i]], t0)
+
+
 def test_render_rays_match_oracle(ctx, oracle):
     grid, intr, frames = room_scene()
     ctx.load_grid(grid)
