@@ -59,7 +59,8 @@ void launch_map_backward_records(const DevGrid& g, const DevParams& p, const Dev
                                  int n, const double4* ray_cd, const uint8_t* flags,
                                  const MapStats* stats, double lambda_d,
                                  const long long* ray_offsets, uint32_t* keys, uint32_t* ids,
-                                 double* values, cudaStream_t s);
+                                 double* values, int r0, int r1, long long sid_base,
+                                 cudaStream_t s);
 void launch_segmented_reduce(const uint32_t* sorted_keys, const uint32_t* perm,
                              const double* values, long long nrec, double* grad_out_f64,
                              cudaStream_t s);

@@ -437,9 +437,11 @@ __global__ void __launch_bounds__(kThreads) k_map_records(
     const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
     const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
     const MapStats* __restrict__ stats, double lambda_d, const long long* __restrict__ offsets,
-    uint32_t* __restrict__ keys, uint32_t* __restrict__ ids, double* __restrict__ values) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+    uint32_t* __restrict__ keys, uint32_t* __restrict__ ids, double* __restrict__ values,
+    int r0, int r1, long long sid_base) {
+  // rays [r0, r1) of the batch; sample ids relative to this chunk's first sample
+  const int i = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1 || i >= n) return;
   const MapStats st = *stats;
   if (st.bad != INT_MAX) return;
   const uint8_t fl = flags[i];
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(kThreads) k_map_records(
   if (!map_upstream(st, nullptr, ray_cd[i], tg, fl, lambda_d, u)) return;
   March m;
   ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
-  const long long base = offsets[i];
+  const long long base = offsets[i] - sid_base;
   map_backward_ray<double>(
       g, p, m, u,
       [&](int idx, const Sample& s, const double w[8], double up0, const double dcol[3],
@@ -470,6 +472,8 @@ __global__ void __launch_bounds__(kThreads) k_map_records(
 }
 
 // In-order fp64 sums over runs of equal vertex keys (GradientBuffer::add order).
+// Each segment continues the vertex's running sum from earlier ray chunks, so
+// chunking the batch keeps the single sequential (ray, sample, corner) order.
 __global__ void __launch_bounds__(kThreads) k_segmented_reduce(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rec, const double* __restrict__ values,
     long long nrec, double* __restrict__ grad) {
@@ -478,8 +482,9 @@ __global__ void __launch_bounds__(kThreads) k_segmented_reduce(
   const uint32_t key = keys[r];
   if (r > 0 && keys[r - 1] == key) return;  // not a segment head
   double acc[28];
+  const double* run = grad + (size_t)key * 28;
 #pragma unroll
-  for (int c = 0; c < 28; ++c) acc[c] = 0.0;
+  for (int c = 0; c < 28; ++c) acc[c] = run[c];
   for (long long q = r; q < nrec && keys[q] == key; ++q) {
     const uint32_t id = rec[q];
     const double* v = values + (long long)(id >> 3) * 36;
@@ -878,10 +883,12 @@ void launch_map_backward_records(const DevGrid& g, const DevParams& p, const Dev
                                  int n, const double4* ray_cd, const uint8_t* flags,
                                  const MapStats* stats, double lambda_d,
                                  const long long* offsets, uint32_t* keys, uint32_t* ids,
-                                 double* values, cudaStream_t s) {
-  k_map_records<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
+                                 double* values, int r0, int r1, long long sid_base,
+                                 cudaStream_t s) {
+  if (r1 <= r0) return;
+  k_map_records<<<(r1 - r0 + kThreads - 1) / kThreads, kThreads, 0, s>>>(
       g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, lambda_d, offsets, keys, ids,
-      values);
+      values, r0, r1, sid_base);
 }
 void launch_segmented_reduce(const uint32_t* keys, const uint32_t* perm, const double* values,
                              long long nrec, double* grad, cudaStream_t s) {

@@ -83,42 +83,62 @@ int grad_deterministic(vrf_context* ctx, const vrf_mapping_config* cfg, const in
   if ((rc = ensure(ctx, ctx->s_grad64, sizeof(double) * 28 * (size_t)ctx->V))) return rc;
   CU(cudaMemsetAsync(ctx->s_grad64.ptr, 0, sizeof(double) * 28 * (size_t)ctx->V, ctx->stream));
   if (st.m_c == 0 || st.bad != INT_MAX || st.samples == 0) return VRF_OK;
-  const long long S = st.samples, R = 8 * S;
-  if (R >= 0x7FFFFFFFLL)
-    return set_err(ctx, VRF_ERR_RUNTIME, "deterministic mapping: batch has too many samples");
   if ((rc = ensure(ctx, ctx->s_offsets, sizeof(long long) * (n + 1)))) return rc;
   long long* offsets = (long long*)ctx->s_offsets.ptr;
-  size_t tmp_scan = 0, tmp_sort = 0;
+  size_t tmp_scan = 0;
   CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, (const int*)ctx->s_count.ptr, offsets, n,
                                    ctx->stream));
-  CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, (const uint32_t*)nullptr,
-                                     (uint32_t*)nullptr, (const uint32_t*)nullptr,
-                                     (uint32_t*)nullptr, (int)R, 0, 32, ctx->stream));
-  if ((rc = ensure(ctx, ctx->s_cub, std::max(tmp_scan, tmp_sort)))) return rc;
+  if ((rc = ensure(ctx, ctx->s_cub, tmp_scan))) return rc;
   CU(cub::DeviceScan::ExclusiveSum(ctx->s_cub.ptr, tmp_scan, (const int*)ctx->s_count.ptr,
                                    offsets, n, ctx->stream));
   LAUNCHED(1);
-  if ((rc = ensure(ctx, ctx->s_keys, sizeof(uint32_t) * R))) return rc;
-  if ((rc = ensure(ctx, ctx->s_keys2, sizeof(uint32_t) * R))) return rc;
-  if ((rc = ensure(ctx, ctx->s_ids, sizeof(uint32_t) * R))) return rc;
-  if ((rc = ensure(ctx, ctx->s_ids2, sizeof(uint32_t) * R))) return rc;
-  if ((rc = ensure(ctx, ctx->s_values, sizeof(double) * 36 * S))) return rc;
-  launch_map_backward_records(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
-                              batch_dev, n, (const double4*)ctx->s_raycd.ptr,
-                              (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, cfg->lambda_d,
-                              offsets, (uint32_t*)ctx->s_keys.ptr, (uint32_t*)ctx->s_ids.ptr,
-                              (double*)ctx->s_values.ptr, ctx->stream);
-  LAUNCHED(1);
-  // LSD radix sort is stable: equal vertices keep (ray, sample, corner) order.
-  CU(cub::DeviceRadixSort::SortPairs(ctx->s_cub.ptr, tmp_sort, (const uint32_t*)ctx->s_keys.ptr,
-                                     (uint32_t*)ctx->s_keys2.ptr, (const uint32_t*)ctx->s_ids.ptr,
-                                     (uint32_t*)ctx->s_ids2.ptr, (int)R, 0, 32, ctx->stream));
-  LAUNCHED(1);
-  launch_segmented_reduce((const uint32_t*)ctx->s_keys2.ptr, (const uint32_t*)ctx->s_ids2.ptr,
-                          (const double*)ctx->s_values.ptr, R, (double*)ctx->s_grad64.ptr,
-                          ctx->stream);
-  LAUNCHED(1);
-  CU(cudaGetLastError());
+  // Chunk the batch by rays so the records (36 doubles per sample + 8 keys/ids)
+  // stay bounded; every chunk continues each vertex's running fp64 sum.
+  std::vector<int> counts((size_t)n);
+  CU(cudaMemcpyAsync(counts.data(), ctx->s_count.ptr, sizeof(int) * (size_t)n,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  const char* chunk_env = std::getenv("VRF_DET_CHUNK");  // tests force small chunks
+  const long long kChunkSamples = chunk_env ? std::max(1LL, std::atoll(chunk_env))
+                                            : (1LL << 22);  // 4M samples: 1.2 GB of records
+  long long sid_base = 0;
+  for (int r0 = 0; r0 < n;) {
+    int r1 = r0;
+    long long S = 0;
+    while (r1 < n && (S == 0 || S + counts[r1] <= kChunkSamples)) S += counts[r1++];
+    if (S > 0) {
+      const long long R = 8 * S;
+      if (R >= 0x7FFFFFFFLL)
+        return set_err(ctx, VRF_ERR_RUNTIME, "deterministic mapping: one ray has too many samples");
+      size_t tmp_sort = 0;
+      CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, (const uint32_t*)nullptr,
+                                         (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                         (uint32_t*)nullptr, (int)R, 0, 32, ctx->stream));
+      if ((rc = ensure(ctx, ctx->s_cub, tmp_sort))) return rc;
+      if ((rc = ensure(ctx, ctx->s_keys, sizeof(uint32_t) * R))) return rc;
+      if ((rc = ensure(ctx, ctx->s_keys2, sizeof(uint32_t) * R))) return rc;
+      if ((rc = ensure(ctx, ctx->s_ids, sizeof(uint32_t) * R))) return rc;
+      if ((rc = ensure(ctx, ctx->s_ids2, sizeof(uint32_t) * R))) return rc;
+      if ((rc = ensure(ctx, ctx->s_values, sizeof(double) * 36 * S))) return rc;
+      launch_map_backward_records(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
+                                  batch_dev, n, (const double4*)ctx->s_raycd.ptr,
+                                  (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, cfg->lambda_d,
+                                  offsets, (uint32_t*)ctx->s_keys.ptr, (uint32_t*)ctx->s_ids.ptr,
+                                  (double*)ctx->s_values.ptr, r0, r1, sid_base, ctx->stream);
+      // LSD radix sort is stable: equal vertices keep (ray, sample, corner) order.
+      CU(cub::DeviceRadixSort::SortPairs(
+          ctx->s_cub.ptr, tmp_sort, (const uint32_t*)ctx->s_keys.ptr,
+          (uint32_t*)ctx->s_keys2.ptr, (const uint32_t*)ctx->s_ids.ptr,
+          (uint32_t*)ctx->s_ids2.ptr, (int)R, 0, 32, ctx->stream));
+      launch_segmented_reduce((const uint32_t*)ctx->s_keys2.ptr, (const uint32_t*)ctx->s_ids2.ptr,
+                              (const double*)ctx->s_values.ptr, R, (double*)ctx->s_grad64.ptr,
+                              ctx->stream);
+      LAUNCHED(3);
+      CU(cudaGetLastError());
+    }
+    sid_base += S;
+    r0 = r1;
+  }
   return VRF_OK;
 }
 

@@ -150,6 +150,22 @@ def test_deterministic_gradient_is_bit_reproducible(ctx, oracle):
     assert np.array_equal(a, b)
 
 
+def test_deterministic_gradient_chunked_equals_unchunked(ctx, oracle, monkeypatch):
+    """Deterministic mode split into many ray chunks keeps the single sequential
+    accumulation order: bit-identical to the one-chunk result."""
+    grid, intr, frames = room_scene()
+    g0 = fresh_grid(grid, seed=6)
+    cfg = MappingConfig(deterministic=True)
+    batch = oracle.draw_batch(8, len(frames), intr.width, intr.height, 700)
+    ctx.load_grid(g0)
+    ctx.load_frames(intr, frames)
+    whole, _ = ctx.mapping_gradient(cfg, batch)
+    monkeypatch.setenv("VRF_DET_CHUNK", "500")
+    chunked, st = ctx.mapping_gradient(cfg, batch)
+    assert st.samples > 5 * 500  # really several chunks
+    assert np.array_equal(whole, chunked)
+
+
 def test_mapping_step_matches_oracle(ctx, oracle):
     """One full mapping_step (RGB+depth loss, RMSProp) vs the oracle, then a second
     step on top (RMSProp state carried on device)."""
