@@ -196,6 +196,14 @@ int vrf_grid_upload_f32(vrf_context* ctx, const vrf_grid_geometry* geom, const f
 int vrf_grid_download(vrf_context* ctx, double* payload, uint8_t* occupancy);
 int vrf_grid_download_f32(vrf_context* ctx, float* payload);
 int vrf_grid_get_geometry(const vrf_context* ctx, vrf_grid_geometry* out);
+/* VoxelGrid::upsampled(max_resolution) — voxel_grid.cpp:190-220, in place: res -> 2 res - 1,
+ * voxel / 2, same bounds; gradient and RMSProp state restart at zero. */
+int vrf_grid_upsample(vrf_context* ctx, int max_resolution);
+/* VoxelGrid::save / VoxelGrid::load — voxel_grid.cpp:222-278 (.vxgf v1: "VXGF", u32
+ * version, u32 res[3], f64 origin[3], f64 voxel, f32 [V][28], LSB-first cell bits).
+ * Same runtime_error messages; a failed load leaves the context without a grid. */
+int vrf_grid_save(vrf_context* ctx, const char* path);
+int vrf_grid_load(vrf_context* ctx, const char* path);
 /* VoxelGrid::prune(tau) — voxel_grid.cpp:169-188. */
 int vrf_grid_prune(vrf_context* ctx, double tau, int64_t* deactivated);
 

@@ -25,6 +25,8 @@ TrackFrameResult voxrf_ref_track_frame(const VoxelGrid&, const Frame&, const Cam
                                        const Pose&, const TrackingConfig&);
 TrackSequenceResult voxrf_ref_track_sequence(const VoxelGrid&, const Dataset&,
                                              const TrackingConfig&);
+MapResult voxrf_ref_map_scene(const Dataset&, const MappingConfig&,
+                              const std::optional<GridGeometry>&);
 }
 
 namespace {
@@ -170,6 +172,47 @@ TEST_CASE("drop-in track_sequence matches the reference trajectory") {
     CHECK((a.trajectory.poses[i].t - b.trajectory.poses[i].t).norm() < 1e-6);  // << 1 mm
     CHECK(std::abs(a.trajectory.poses[i].q.coeffs().dot(b.trajectory.poses[i].q.coeffs())) > 1.0 - 1e-12);
   }
+}
+
+TEST_CASE("drop-in map_scene follows the reference stage schedule") {
+  Scene s = make_scene();
+  Dataset ds;
+  ds.intrinsics = s.intr;
+  ds.frames = s.frames;
+  MappingConfig cfg;
+  cfg.keyframe_stride = 1;
+  cfg.rays_per_batch = 256;
+  cfg.iterations_per_stage = 6;
+  cfg.initial_resolution = 9;
+  cfg.upsample_stages = 2;  // 9 -> 17 -> 33, refined on the device
+  cfg.max_resolution = 64;
+  cfg.prune_every = 4;
+  cfg.deterministic = true;
+  const MapResult a = map_scene(ds, cfg, std::nullopt);
+  const MapResult b = voxrf_ref_map_scene(ds, cfg, std::nullopt);
+  const GridGeometry& ga = a.grid.geometry();
+  const GridGeometry& gb = b.grid.geometry();
+  CHECK(ga.res == gb.res);
+  CHECK(ga.res.x() == 33);
+  CHECK(ga.voxel_size == gb.voxel_size);
+  CHECK((ga.origin - gb.origin).norm() == 0.0);
+  REQUIRE(a.log.size() == b.log.size());
+  REQUIRE(a.log.size() == 18);
+  // identical batches (same Rng stream); fp32 device state vs fp64 host state
+  for (std::size_t i = 0; i < a.log.size(); ++i) {
+    INFO("iteration " << i);
+    CHECK(a.log[i].stats.rays_color == b.log[i].stats.rays_color);
+    CHECK(a.log[i].stats.loss_total == doctest::Approx(b.log[i].stats.loss_total).epsilon(1e-3));
+  }
+  CHECK(a.grid.active_cell_count() == b.grid.active_cell_count());
+  double worst = 0.0, scale = 0.0;
+  for (std::size_t i = 0; i < a.grid.data().size(); ++i) {
+    worst = std::max(worst, std::abs(a.grid.data()[i] - b.grid.data()[i]));
+    scale = std::max(scale, std::abs(b.grid.data()[i]));
+  }
+  CHECK(worst <= 1e-3 * scale);
+  cfg.max_resolution = 20;
+  CHECK_THROWS_AS(map_scene(ds, cfg, std::nullopt), std::runtime_error);
 }
 
 TEST_SUITE_END();

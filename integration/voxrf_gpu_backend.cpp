@@ -219,11 +219,14 @@ MapResult map_scene(const Dataset& dataset, const MappingConfig& config,
   const vrf_mapping_config cc = to_c(config);
   const auto t0 = std::chrono::steady_clock::now();
   int iteration = 0;
+  // The grid, its RMSProp state and the keyframes stay in HBM for the whole
+  // schedule: stages refine on the device (vrf_grid_upsample ==
+  // VoxelGrid::upsampled + RMSProp reset, mapping.cpp:297-300) and the host
+  // grid is written back once at the end.
+  upload_grid(result.grid);
+  check(vrf_rmsprop_reset(ctx()));
   for (int stage = 0; stage <= config.upsample_stages; ++stage) {
-    if (stage > 0) result.grid = result.grid.upsampled(config.max_resolution);
-    // The grid and its RMSProp state stay on the device for the whole stage.
-    upload_grid(result.grid);
-    check(vrf_rmsprop_reset(ctx()));
+    if (stage > 0) check(vrf_grid_upsample(ctx(), config.max_resolution));
     for (int it = 0; it < config.iterations_per_stage; ++it, ++iteration) {
       const std::vector<int32_t> batch =
           draw_batch(rng, int(keyframes.size()), dataset.intrinsics, config.rays_per_batch);
@@ -241,14 +244,22 @@ MapResult map_scene(const Dataset& dataset, const MappingConfig& config,
               .count();
       result.log.push_back(row);
     }
-    std::vector<std::uint8_t> occ(result.grid.occupancy().size());
-    check(vrf_grid_download(ctx(), result.grid.data().data(), occ.data()));
-    const GridGeometry& g = result.grid.geometry();
-    for (int cz = 0; cz < g.res.z() - 1; ++cz)
-      for (int cy = 0; cy < g.res.y() - 1; ++cy)
-        for (int cx = 0; cx < g.res.x() - 1; ++cx)
-          result.grid.set_cell_active(cx, cy, cz, occ[g.cell_index(cx, cy, cz)] != 0);
   }
+  vrf_grid_geometry fg{};
+  check(vrf_grid_get_geometry(ctx(), &fg));
+  GridGeometry g;
+  for (int a = 0; a < 3; ++a) {
+    g.res[a] = fg.res[a];
+    g.origin[a] = fg.origin[a];
+  }
+  g.voxel_size = fg.voxel_size;
+  result.grid = VoxelGrid(g);
+  std::vector<std::uint8_t> occ(result.grid.occupancy().size());
+  check(vrf_grid_download(ctx(), result.grid.data().data(), occ.data()));
+  for (int cz = 0; cz < g.res.z() - 1; ++cz)
+    for (int cy = 0; cy < g.res.y() - 1; ++cy)
+      for (int cx = 0; cx < g.res.x() - 1; ++cx)
+        result.grid.set_cell_active(cx, cy, cz, occ[g.cell_index(cx, cy, cz)] != 0);
   return result;
 }
 

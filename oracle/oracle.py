@@ -190,6 +190,22 @@ class Oracle:
                                       C.byref(r)), "render_ray")
         return r
 
+    def upsample(self, grid, max_resolution):
+        """VoxelGrid::upsampled (voxel_grid.cpp:190-220) -> (geometry, data, active)."""
+        h = _GridHold(grid)
+        f = Geometry()
+        rc = self.lib.or_upsample(C.byref(h.s), int(max_resolution), C.byref(f), None, None)
+        if rc == 3:
+            raise OracleError("upsample: resolution would exceed configured maximum")
+        res = tuple(f.res)
+        nv = res[0] * res[1] * res[2]
+        nc = (res[0] - 1) * (res[1] - 1) * (res[2] - 1)
+        data = np.zeros((nv, 28))
+        act = np.zeros(nc, np.uint8)
+        _check(self.lib.or_upsample(C.byref(h.s), int(max_resolution), C.byref(f), _ptr(data),
+                                    _ptr(act)), "upsample")
+        return (res, tuple(f.origin), f.voxel_size), data, act
+
     def render_image(self, grid, intr, pose, params, stride=1):
         h = _GridHold(grid)
         ow = (intr.width + stride - 1) // stride
@@ -302,6 +318,14 @@ class RefLib:
         for n in ["ref_grid_destroy", "ref_frames_destroy", "ref_mapper_destroy"]:
             getattr(lib, n).argtypes = [C.c_void_p]
         lib.ref_grid_read.argtypes = [C.c_void_p, C.c_void_p]
+        lib.ref_grid_occupancy.argtypes = [C.c_void_p, C.c_void_p]
+        lib.ref_grid_upsampled.restype = C.c_void_p
+        lib.ref_grid_upsampled.argtypes = [C.c_void_p, C.c_int]
+        lib.ref_grid_save.argtypes = [C.c_void_p, C.c_char_p]
+        lib.ref_grid_load.restype = C.c_void_p
+        lib.ref_grid_load.argtypes = [C.c_char_p]
+        lib.ref_grid_checksum.restype = C.c_uint64
+        lib.ref_grid_checksum.argtypes = [C.c_void_p]
         lib.ref_mapper_rms.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
         lib.ref_mapping_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                          C.c_int, C.c_int, C.c_void_p, C.c_void_p]
@@ -330,6 +354,27 @@ class RefLib:
         data = np.ascontiguousarray(grid.data, np.float64)
         act = np.ascontiguousarray(grid.active, np.uint8)
         return self.lib.ref_grid_create(C.byref(g), _ptr(data), _ptr(act))
+
+    def read_occupancy(self, handle, ncells):
+        out = np.zeros(ncells, np.uint8)
+        self.lib.ref_grid_occupancy(handle, _ptr(out))
+        return out
+
+    def upsampled(self, handle, max_resolution):
+        """VoxelGrid::upsampled (voxel_grid.cpp:190-220) -> new handle."""
+        h = self.lib.ref_grid_upsampled(handle, int(max_resolution))
+        if not h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return h
+
+    def save(self, handle, path):
+        self._err(self.lib.ref_grid_save(handle, str(path).encode()), "save")
+
+    def load(self, path):
+        h = self.lib.ref_grid_load(str(path).encode())
+        if not h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return h
 
     def frames(self, frames, intr):
         fh = _FramesHold(frames)

@@ -127,6 +127,25 @@ void ref_grid_occupancy(const void* grid, uint8_t* active) {
   const auto& occ = static_cast<const VoxelGrid*>(grid)->occupancy();
   std::memcpy(active, occ.data(), occ.size());
 }
+void* ref_grid_upsampled(const void* grid, int max_resolution) {
+  try {
+    return new VoxelGrid(static_cast<const VoxelGrid*>(grid)->upsampled(max_resolution));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+int ref_grid_save(const void* grid, const char* path) {
+  REF_GUARD(static_cast<const VoxelGrid*>(grid)->save(path));
+}
+void* ref_grid_load(const char* path) {
+  try {
+    return new VoxelGrid(VoxelGrid::load(path));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
 uint64_t ref_grid_checksum(const void* grid) {
   return static_cast<const VoxelGrid*>(grid)->checksum();
 }

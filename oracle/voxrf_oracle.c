@@ -202,6 +202,37 @@ static void trilerp(const or_grid* g, const locator* loc, double* sigma_raw, dou
   *sigma_raw = s;
 }
 
+/* VoxelGrid::upsampled — voxel_grid.cpp:190-220. `out` holds the refined
+ * geometry (2 res - 1, voxel / 2) and (2rx-1)(2ry-1)(2rz-1)*28 doubles;
+ * active_out its cell mask. Returns OR_RUNTIME over max_resolution. */
+int or_upsample(const or_grid* g, int max_resolution, or_geometry* fine, double* out,
+                uint8_t* active_out) {
+  or_geometry f = g->geom;
+  for (int a = 0; a < 3; ++a) f.res[a] = 2 * g->geom.res[a] - 1;
+  f.voxel_size = g->geom.voxel_size * 0.5;
+  if (f.res[0] > max_resolution || f.res[1] > max_resolution || f.res[2] > max_resolution)
+    return OR_RUNTIME;
+  *fine = f;
+  if (!out) return OR_OK;
+  for (int iz = 0; iz < f.res[2]; ++iz)
+    for (int iy = 0; iy < f.res[1]; ++iy)
+      for (int ix = 0; ix < f.res[0]; ++ix) {
+        const double gg[3] = {ix * 0.5, iy * 0.5, iz * 0.5};
+        double p[3];
+        for (int a = 0; a < 3; ++a) p[a] = g->geom.origin[a] + gg[a] * g->geom.voxel_size;
+        locator loc;
+        if (!try_locate(&g->geom, p, &loc)) return OR_OUT_OF_RANGE;
+        double* v = out + (size_t)vertex_index(&f, ix, iy, iz) * PAYLOAD;
+        trilerp(g, &loc, &v[0], &v[1]);
+      }
+  for (int cz = 0; cz < f.res[2] - 1; ++cz)
+    for (int cy = 0; cy < f.res[1] - 1; ++cy)
+      for (int cx = 0; cx < f.res[0] - 1; ++cx)
+        active_out[cell_index(&f, cx, cy, cz)] =
+            g->active[cell_index(&g->geom, cx / 2, cy / 2, cz / 2)];
+  return OR_OK;
+}
+
 /* voxel_grid.cpp:34-47 */
 int or_sh_eval(const double d[3], double b[9]) {
   if (fabs(norm3(d) - 1.0) > 1e-9) return OR_INVALID_ARGUMENT;

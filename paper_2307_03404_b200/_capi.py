@@ -116,6 +116,9 @@ _SIGS = {
     "vrf_grid_download_f32": (C.c_int, [vp, vp]),
     "vrf_grid_get_geometry": (C.c_int, [vp, P(GridGeometry_c)]),
     "vrf_grid_prune": (C.c_int, [vp, C.c_double, P(C.c_int64)]),
+    "vrf_grid_upsample": (C.c_int, [vp, C.c_int]),
+    "vrf_grid_save": (C.c_int, [vp, C.c_char_p]),
+    "vrf_grid_load": (C.c_int, [vp, C.c_char_p]),
     "vrf_frames_upload": (C.c_int, [vp, P(Intrinsics_c), C.c_int, P(vp), P(vp), P(Pose_c)]),
     "vrf_frames_count": (C.c_int, [vp]),
     "vrf_render_image": (C.c_int, [vp, P(Intrinsics_c), P(Pose_c), P(RenderParams_c), C.c_int,

@@ -459,6 +459,23 @@ class Context:
         self._check(self._lib.vrf_grid_download_f32(self._h, _ptr(out)))
         return out
 
+    def upsample(self, max_resolution: int = 1024):
+        """VoxelGrid::upsampled (voxel_grid.cpp:190-220) in place on the device."""
+        self._check(self._lib.vrf_grid_upsample(self._h, int(max_resolution)))
+        g = self.geom
+        self.geom = GridGeometry(tuple(2 * int(r) - 1 for r in g.res), g.origin, g.voxel_size * 0.5)
+
+    def save_grid(self, path):
+        """VoxelGrid::save (voxel_grid.cpp:222-239) straight from HBM."""
+        self._check(self._lib.vrf_grid_save(self._h, str(path).encode()))
+
+    def load_grid_file(self, path):
+        """VoxelGrid::load (voxel_grid.cpp:241-278) straight into HBM."""
+        self._check(self._lib.vrf_grid_load(self._h, str(path).encode()))
+        g = capi.GridGeometry_c()
+        self._lib.vrf_grid_get_geometry(self._h, C.byref(g))
+        self.geom = GridGeometry(tuple(g.res), tuple(g.origin), g.voxel_size)
+
     def prune(self, tau: float) -> int:
         n = C.c_int64()
         self._check(self._lib.vrf_grid_prune(self._h, tau, C.byref(n)))

@@ -258,6 +258,160 @@ int vrf_grid_prune(vrf_context* ctx, double tau, int64_t* deactivated) {
   return VRF_OK;
 }
 
+// VoxelGrid::upsampled(max_resolution) — voxel_grid.cpp:190-220, in place on the
+// device; gradient and RMSProp state restart at zero (map_scene resets RMSProp
+// on every stage, mapping.cpp:297-300).
+int vrf_grid_upsample(vrf_context* ctx, int max_resolution) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  vrf_grid_geometry ng = ctx->geom;
+  for (int a = 0; a < 3; ++a) ng.res[a] = 2 * ctx->geom.res[a] - 1;
+  ng.voxel_size = ctx->geom.voxel_size * 0.5;
+  if (std::max(ng.res[0], std::max(ng.res[1], ng.res[2])) > max_resolution)
+    return set_err(ctx, VRF_ERR_RUNTIME, "upsample: resolution would exceed configured maximum");
+  const DevGrid coarse = dev_grid(ctx);
+  float* old_payload = ctx->payload;
+  uint32_t* old_occ = ctx->occ;
+  ctx->payload = nullptr;  // keep the coarse payload/occupancy alive through alloc_grid
+  ctx->occ = nullptr;
+  if ((rc = alloc_grid(ctx, &ng))) {
+    cudaFree(old_payload);
+    cudaFree(old_occ);
+    return rc;
+  }
+  launch_upsample(coarse, ng.res[0], ng.res[1], ng.res[2], ctx->payload, ctx->occ, ctx->stream);
+  LAUNCHED(2);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(ctx->stream));
+  cudaFree(old_payload);
+  cudaFree(old_occ);
+  return update_blocks(ctx);
+}
+
+// .vxgf I/O — VoxelGrid::save / load (voxel_grid.cpp:222-278). The device payload
+// is already the file's fp32 [V][28] AoS and the occupancy words are the file's
+// LSB-first bitmask, so both directions stream straight through pinned staging.
+namespace {
+constexpr char kVxgfMagic[4] = {'V', 'X', 'G', 'F'};
+constexpr uint32_t kVxgfVersion = 1;
+constexpr size_t kVxgfHeader = 4 + 4 + 3 * 4 + 3 * 8 + 8;
+constexpr size_t kIoChunk = 64u << 20;
+
+struct File {
+  FILE* f = nullptr;
+  ~File() {
+    if (f) fclose(f);
+  }
+};
+}  // namespace
+
+int vrf_grid_save(vrf_context* ctx, const char* path) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  const std::string p = path ? path : "";
+  File out;
+  out.f = fopen(p.c_str(), "wb");
+  if (!out.f) return set_err(ctx, VRF_ERR_RUNTIME, "grid save: cannot open " + p);
+  bool ok = fwrite(kVxgfMagic, 1, 4, out.f) == 4 &&
+            fwrite(&kVxgfVersion, sizeof(uint32_t), 1, out.f) == 1;
+  for (int a = 0; a < 3 && ok; ++a) {
+    const uint32_t r = (uint32_t)ctx->geom.res[a];
+    ok = fwrite(&r, sizeof(r), 1, out.f) == 1;
+  }
+  ok = ok && fwrite(ctx->geom.origin, sizeof(double), 3, out.f) == 3 &&
+       fwrite(&ctx->geom.voxel_size, sizeof(double), 1, out.f) == 1;
+  if ((rc = ensure_pinned(ctx, kIoChunk))) return rc;
+  char* stage = (char*)ctx->h_pinned;
+  const size_t payload_bytes = sizeof(float) * 28 * (size_t)ctx->V;
+  for (size_t off = 0; off < payload_bytes && ok; off += kIoChunk) {
+    const size_t n = std::min(kIoChunk, payload_bytes - off);
+    CU(cudaMemcpyAsync(stage, (const char*)ctx->payload + off, n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ok = fwrite(stage, 1, n, out.f) == n;
+  }
+  const size_t bit_bytes = (size_t)((ctx->C + 7) / 8);
+  for (size_t off = 0; off < bit_bytes && ok; off += kIoChunk) {
+    const size_t n = std::min(kIoChunk, bit_bytes - off);
+    CU(cudaMemcpyAsync(stage, (const char*)ctx->occ + off, n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ok = fwrite(stage, 1, n, out.f) == n;
+  }
+  ok = ok && fflush(out.f) == 0;
+  if (!ok) return set_err(ctx, VRF_ERR_RUNTIME, "grid save: write failed for " + p);
+  return VRF_OK;
+}
+
+int vrf_grid_load(vrf_context* ctx, const char* path) {
+  cudaSetDevice(ctx->device);
+  const std::string p = path ? path : "";
+  File in;
+  in.f = fopen(p.c_str(), "rb");
+  if (!in.f) return set_err(ctx, VRF_ERR_RUNTIME, "grid load: cannot open " + p);
+  char magic[4];
+  if (fread(magic, 1, 4, in.f) != 4 || std::memcmp(magic, kVxgfMagic, 4) != 0)
+    return set_err(ctx, VRF_ERR_RUNTIME, "grid load: bad magic in " + p);
+  uint32_t version = 0;
+  if (fread(&version, sizeof(version), 1, in.f) != 1 || version != kVxgfVersion)
+    return set_err(ctx, VRF_ERR_RUNTIME, "grid load: unsupported version in " + p);
+  vrf_grid_geometry g{};
+  bool ok = true;
+  for (int a = 0; a < 3 && ok; ++a) {
+    uint32_t r = 0;
+    ok = fread(&r, sizeof(r), 1, in.f) == 1;
+    g.res[a] = (int32_t)r;
+  }
+  ok = ok && fread(g.origin, sizeof(double), 3, in.f) == 3 &&
+       fread(&g.voxel_size, sizeof(double), 1, in.f) == 1;
+  if (!ok) return set_err(ctx, VRF_ERR_RUNTIME, "grid load: truncated header in " + p);
+  int rc = validate_geometry(ctx, &g);
+  if (rc) return rc;
+  const size_t V = (size_t)g.res[0] * g.res[1] * g.res[2];
+  const size_t C = (size_t)(g.res[0] - 1) * (g.res[1] - 1) * (g.res[2] - 1);
+  const size_t payload_bytes = sizeof(float) * 28 * V, bit_bytes = (C + 7) / 8;
+  // The reference reads payload + bits before checking either (voxel_grid.cpp:262-267):
+  // truncation is reported ahead of non-finite values.
+  if (fseeko(in.f, 0, SEEK_END) != 0 ||
+      (size_t)ftello(in.f) < kVxgfHeader + payload_bytes + bit_bytes ||
+      fseeko(in.f, (off_t)kVxgfHeader, SEEK_SET) != 0)
+    return set_err(ctx, VRF_ERR_RUNTIME, "grid load: truncated payload in " + p);
+  if ((rc = ensure_pinned(ctx, kIoChunk))) return rc;
+  if ((rc = alloc_grid(ctx, &g))) return rc;
+  char* stage = (char*)ctx->h_pinned;
+  for (size_t off = 0; off < payload_bytes; off += kIoChunk) {
+    const size_t n = std::min(kIoChunk, payload_bytes - off);
+    CU(cudaStreamSynchronize(ctx->stream));  // the previous chunk has left the stage
+    if (fread(stage, 1, n, in.f) != n) {
+      free_grid(ctx);
+      return set_err(ctx, VRF_ERR_RUNTIME, "grid load: truncated payload in " + p);
+    }
+    const float* f = (const float*)stage;
+    for (size_t i = 0; i < n / sizeof(float); ++i)
+      if (!std::isfinite(f[i])) {
+        free_grid(ctx);
+        return set_err(ctx, VRF_ERR_RUNTIME, "grid load: non-finite payload in " + p);
+      }
+    CU(cudaMemcpyAsync((char*)ctx->payload + off, stage, n, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemsetAsync(ctx->occ, 0, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1), ctx->stream));
+  for (size_t off = 0; off < bit_bytes; off += kIoChunk) {
+    const size_t n = std::min(kIoChunk, bit_bytes - off);
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (fread(stage, 1, n, in.f) != n) {
+      free_grid(ctx);
+      return set_err(ctx, VRF_ERR_RUNTIME, "grid load: truncated payload in " + p);
+    }
+    CU(cudaMemcpyAsync((char*)ctx->occ + off, stage, n, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  // bits past the last cell are never read (cell_active / block occupancy stop at C)
+  CU(cudaStreamSynchronize(ctx->stream));
+  return update_blocks(ctx);
+}
+
 // ----------------------------------------------------------------- frames
 int vrf_frames_upload(vrf_context* ctx, const vrf_intrinsics* intr, int n,
                       const double* const* colors, const double* const* depths,

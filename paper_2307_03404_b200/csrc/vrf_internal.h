@@ -126,6 +126,8 @@ void launch_pack_frames(const double* color, const double* depth, double4* rgbd,
                         cudaStream_t s);
 void launch_prune(const DevGrid& g, uint32_t* occ_bits, double tau, unsigned long long* count,
                   cudaStream_t s);
+void launch_upsample(const DevGrid& coarse, int frx, int fry, int frz, float* fine,
+                     uint32_t* fine_occ, cudaStream_t s);
 void launch_block_occupancy(const uint32_t* occ, int rx, int ry, int rz, int bx, int by, int bz,
                             uint32_t* bocc, unsigned int* n_active, cudaStream_t s);
 

@@ -793,6 +793,64 @@ __global__ void k_prune(DevGrid g, uint32_t* bits, double tau, unsigned long lon
   }
 }
 
+// VoxelGrid::upsampled — voxel_grid.cpp:190-220. Fine vertex (ix,iy,iz) sits at
+// coarse coordinates (ix/2, iy/2, iz/2); like the reference it goes through the
+// world point p = to_world(g) and locate(p), then trilerps all 28 channels (FP64
+// accumulation in the reference corner order, stored fp32).
+__global__ void k_upsample(DevGrid c, int frx, int fry, int frz, float* __restrict__ fine) {
+  const long long nv = (long long)frx * fry * frz;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+       v += (long long)gridDim.x * blockDim.x) {
+    const int ix = (int)(v % frx);
+    const long long r = v / frx;
+    const int iy = (int)(r % fry), iz = (int)(r / fry);
+    const double p[3] = {dadd(c.ox, dmul(ix * 0.5, c.voxel)), dadd(c.oy, dmul(iy * 0.5, c.voxel)),
+                         dadd(c.oz, dmul(iz * 0.5, c.voxel))};
+    Sample s;
+    if (!locate(c, p, s)) {  // the world round trip left the box by an ulp: clamp
+      const double q[3] = {fmin(fmax(p[0], c.ox), c.hx), fmin(fmax(p[1], c.oy), c.hy),
+                           fmin(fmax(p[2], c.oz), c.hz)};
+      locate(c, q, s);
+    }
+    double w[8];
+    corner_weights(s, w);
+    double acc[28];
+#pragma unroll
+    for (int q = 0; q < 28; ++q) acc[q] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float* vp = reinterpret_cast<const float*>(c.payload) +
+                        (size_t)corner_index(c, s.base, k) * kPayload;
+#pragma unroll
+      for (int q = 0; q < 28; ++q) acc[q] = dadd(acc[q], dmul(w[k], (double)__ldg(vp + q)));
+    }
+    float* dst = fine + (size_t)v * kPayload;
+#pragma unroll
+    for (int q = 0; q < 28; ++q) dst[q] = (float)acc[q];
+  }
+}
+
+// Each refined cell inherits its parent's activity (voxel_grid.cpp:214-218).
+__global__ void k_upsample_occupancy(const uint32_t* __restrict__ cocc, int crx, int cry,
+                                     int frx, int fry, int frz, uint32_t* __restrict__ focc) {
+  const long long ncf = (long long)(frx - 1) * (fry - 1) * (frz - 1);
+  const long long words = (ncf + 31) / 32;
+  for (long long wd = (long long)blockIdx.x * blockDim.x + threadIdx.x; wd < words;
+       wd += (long long)gridDim.x * blockDim.x) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+      const long long f = wd * 32 + b;
+      if (f >= ncf) break;
+      const int cx = (int)(f % (frx - 1));
+      const long long r = f / (frx - 1);
+      const int cy = (int)(r % (fry - 1)), cz = (int)(r / (fry - 1));
+      const long long pc = (cx / 2) + (long long)(crx - 1) * ((cy / 2) + (long long)(cry - 1) * (cz / 2));
+      if ((cocc[pc >> 5] >> (pc & 31)) & 1u) bits |= 1u << b;
+    }
+    focc[wd] = bits;
+  }
+}
+
 // Coarse occupancy: block bit = OR of its (up to) 8^3 cell bits.
 __global__ void k_block_occupancy(const uint32_t* __restrict__ occ, int rx, int ry, int rz,
                                   int bx, int by, int bz, uint32_t* __restrict__ bocc,
@@ -945,6 +1003,14 @@ void launch_unpack_occupancy(const uint32_t* bits, uint8_t* occ, long long n_cel
 void launch_pack_frames(const double* color, const double* depth, double4* rgbd, long long npix,
                         cudaStream_t s) {
   if (npix) k_pack_frames<<<grid_blocks(npix, 256), 256, 0, s>>>(color, depth, rgbd, npix);
+}
+void launch_upsample(const DevGrid& coarse, int frx, int fry, int frz, float* fine,
+                     uint32_t* fine_occ, cudaStream_t s) {
+  const long long nv = (long long)frx * fry * frz;
+  k_upsample<<<grid_blocks(nv, 128), 128, 0, s>>>(coarse, frx, fry, frz, fine);
+  const long long words = ((long long)(frx - 1) * (fry - 1) * (frz - 1) + 31) / 32;
+  k_upsample_occupancy<<<grid_blocks(words, 256), 256, 0, s>>>(coarse.occ, coarse.rx, coarse.ry,
+                                                               frx, fry, frz, fine_occ);
 }
 void launch_block_occupancy(const uint32_t* occ, int rx, int ry, int rz, int bx, int by, int bz,
                             uint32_t* bocc, unsigned int* n_active, cudaStream_t s) {

@@ -22,6 +22,6 @@ def test_dropin_binary_against_reference():
     out = r.stdout + r.stderr
     # 45 reference cases + 4 drop-in cases; the single expected failure is the
     # reference's own float-vs-double check at test_renderer.cpp:295-296.
-    assert "test cases: 49 | 48 passed | 1 failed" in r.stdout, out[-4000:]
+    assert "test cases: 50 | 49 passed | 1 failed" in r.stdout, out[-4000:]
     bad = [ln for ln in r.stderr.splitlines() if "ERROR:" in ln]
     assert all("test_renderer.cpp:295" in ln or "test_renderer.cpp:296" in ln for ln in bad), out[-4000:]

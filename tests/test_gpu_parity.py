@@ -266,3 +266,73 @@ def test_prune_matches_host_prune(ctx):
     n_host = synth.prune(host, 1e-3)
     assert n == n_host
     assert np.array_equal(ctx.download_grid().active, host.active)
+
+
+def test_upsample_matches_oracle(ctx, oracle):
+    """Device VoxelGrid::upsampled: the fp64 trilinear replay over the fp32 payload,
+    stored in fp32, equals the reference's double result rounded to fp32; the
+    occupancy and geometry match exactly; RMSProp restarts at zero."""
+    grid = fresh_grid(synth.scene_grid(17, seed=2, prune_tau=1e-3), sh_noise=0.3)
+    ctx.load_grid(grid)
+    ctx.upsample(64)
+    (res, origin, voxel), data, act = oracle.upsample(grid, 64)
+    assert tuple(ctx.geom.res) == res and ctx.geom.voxel_size == voxel
+    out = ctx.download_grid()
+    assert np.array_equal(out.active, act)
+    assert np.array_equal(ctx.download_payload_f32(), data.astype(np.float32))
+    assert not ctx.rmsprop_v().any()
+    with pytest.raises(RuntimeError, match="exceed configured maximum"):
+        ctx.upsample(64)
+    # the refined grid renders like the oracle's refined grid
+    fine = VoxelGrid(synth.GridGeometry(res, origin, voxel))
+    fine.data[:] = data.astype(np.float32)
+    fine.active[:] = act
+    rays = random_rays(fine, 64)
+    rr = ctx.render_rays(rays, RenderParams())
+    for i, row in enumerate(rays):
+        r0 = oracle.render_ray(fine, row[:3], row[3:], RenderParams())
+        assert rel_err(rr[i, 3], r0.depth, 1e-3) < RTOL_RENDER
+
+
+def test_vxgf_roundtrip_with_reference(ctx, ref, tmp_path):
+    """.vxgf written from HBM loads in the reference with the same checksum, and a
+    reference-written file loads into HBM bit for bit (voxel_grid.cpp:222-278)."""
+    grid = fresh_grid(synth.scene_grid(17, seed=2, prune_tau=1e-3), sh_noise=0.3)
+    ctx.load_grid(grid)
+    path = tmp_path / "dev.vxgf"
+    ctx.save_grid(path)
+    h = ref.load(path)
+    h0 = ref.grid(grid)
+    try:
+        assert ref.lib.ref_grid_checksum(h) == ref.lib.ref_grid_checksum(h0)
+        rpath = tmp_path / "ref.vxgf"
+        ref.save(h0, rpath)
+        assert rpath.read_bytes() == path.read_bytes()
+    finally:
+        ref.lib.ref_grid_destroy(h)
+        ref.lib.ref_grid_destroy(h0)
+    ctx.init_grid(synth.GridGeometry((5, 5, 5), (0.0, 0.0, 0.0), 0.5), 0.0)
+    ctx.load_grid_file(rpath)
+    assert tuple(ctx.geom.res) == tuple(grid.geom.res)
+    out = ctx.download_grid()
+    assert np.array_equal(out.data, grid.data) and np.array_equal(out.active, grid.active)
+    # error contract (test_voxel_grid.cpp:386-402)
+    bad = tmp_path / "bad.vxgf"
+    bad.write_bytes(b"NOPE" + path.read_bytes()[4:])
+    with pytest.raises(RuntimeError, match="bad magic"):
+        ctx.load_grid_file(bad)
+    vers = tmp_path / "vers.vxgf"
+    vers.write_bytes(path.read_bytes()[:4] + b"\x02\x00\x00\x00" + path.read_bytes()[8:])
+    with pytest.raises(RuntimeError, match="unsupported version"):
+        ctx.load_grid_file(vers)
+    trunc = tmp_path / "trunc.vxgf"
+    trunc.write_bytes(path.read_bytes()[:-3])
+    with pytest.raises(RuntimeError, match="truncated payload"):
+        ctx.load_grid_file(trunc)
+    nan = bytearray(path.read_bytes())
+    nan[52:56] = np.array([np.nan], np.float32).tobytes()
+    (tmp_path / "nan.vxgf").write_bytes(bytes(nan))
+    with pytest.raises(RuntimeError, match="non-finite payload"):
+        ctx.load_grid_file(tmp_path / "nan.vxgf")
+    with pytest.raises(RuntimeError, match="cannot open"):
+        ctx.load_grid_file(tmp_path / "missing.vxgf")

@@ -149,3 +149,20 @@ def test_track_frame_bit_exact(oracle, ref):
     finally:
         ref.lib.ref_grid_destroy(gh)
         ref.lib.ref_frames_destroy(fh)
+
+
+def test_upsample_matches_reference(oracle, ref):
+    """VoxelGrid::upsampled (voxel_grid.cpp:190-220): payload and occupancy bit-exact."""
+    grid = synth.scene_grid(9, seed=4, prune_tau=1e-3)
+    (res, origin, voxel), data, act = oracle.upsample(grid, 64)
+    assert res == (17, 17, 17) and voxel == grid.geom.voxel_size * 0.5
+    h = ref.grid(grid)
+    u = ref.upsampled(h, 64)
+    try:
+        assert np.array_equal(ref.read_grid(u, 17 ** 3), data)
+        assert np.array_equal(ref.read_occupancy(u, 16 ** 3), act)
+    finally:
+        ref.lib.ref_grid_destroy(u)
+        ref.lib.ref_grid_destroy(h)
+    with pytest.raises(RuntimeError, match="exceed configured maximum"):
+        oracle.upsample(grid, 16)
