@@ -212,6 +212,14 @@ int vrf_frames_upload(vrf_context* ctx, const vrf_intrinsics* intr, int n,
                       const double* const* colors, const double* const* depths,
                       const vrf_pose* poses);
 int vrf_frames_count(const vrf_context* ctx);
+/* Slot-addressed frame store for online use (the SLAM driver): reserve capacity
+ * slots of intr's size, then write one slot at a time (keyframes appended as they
+ * are selected, a tracking slot overwritten per frame). vrf_frames_count is the
+ * high-water mark of written slots; mapping batches address slots by index. */
+int vrf_frames_reserve(vrf_context* ctx, const vrf_intrinsics* intr, int capacity);
+int vrf_frame_set(vrf_context* ctx, int slot, const double* color, const double* depth,
+                  const vrf_pose* pose);
+int vrf_frame_set_pose(vrf_context* ctx, int slot, const vrf_pose* pose);
 
 /* ---- renderer: render_image — renderer.hpp:83-84 (renderer.cpp:149-174).
  * color: ceil(H/stride)*ceil(W/stride)*3, depth: ceil(H/stride)*ceil(W/stride). */
@@ -226,6 +234,12 @@ int vrf_render_image(vrf_context* ctx, const vrf_intrinsics* intr, const vrf_pos
 int vrf_mapping_step(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* batch,
                      int n_rays, vrf_map_step_stats* out);
 /* Same, batch already in device memory. */
+/* map_scene's inner loop (mapping.cpp:302-312): n_steps mapping_step calls, batch i
+ * drawn from the reference Rng stream `rng_state` (advanced in place) over the first
+ * n_keyframes frame slots. The host draw of batch i+1 overlaps the device work of
+ * step i (pinned double buffer). out: n_steps stats; stops at the first error. */
+int vrf_mapping_steps(vrf_context* ctx, const vrf_mapping_config* cfg, uint64_t rng_state[4],
+                      int n_keyframes, int n_rays, int n_steps, vrf_map_step_stats* out);
 int vrf_mapping_step_device(vrf_context* ctx, const vrf_mapping_config* cfg,
                             const int32_t* batch_dev, int n_rays, vrf_map_step_stats* out);
 /* The merged grid gradient of one batch (no update): double [V][28] host. */

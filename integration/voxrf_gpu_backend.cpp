@@ -13,6 +13,7 @@
 // (proj/include/voxrf) and links it in place of those six definitions
 // (INTEGRATION.md); everything else (VoxelGrid, per-ray CPU functions used by
 // tests and gradcheck, dataset/eval/CLI) is unchanged.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <stdexcept>
@@ -214,7 +215,6 @@ MapResult map_scene(const Dataset& dataset, const MappingConfig& config,
   }
   const GridGeometry geom = geometry ? *geometry : fit_grid_geometry(dataset, keyframes, config);
   MapResult result{VoxelGrid(geom, config.sigma_init), {}};
-  Rng rng(config.seed);
   upload_frames(dataset.intrinsics, keyframes);
   const vrf_mapping_config cc = to_c(config);
   const auto t0 = std::chrono::steady_clock::now();
@@ -225,24 +225,33 @@ MapResult map_scene(const Dataset& dataset, const MappingConfig& config,
   // grid is written back once at the end.
   upload_grid(result.grid);
   check(vrf_rmsprop_reset(ctx()));
+  uint64_t rs[4];
+  vrf_rng_seed(config.seed, rs);  // == Rng(config.seed), mapping.cpp:292
+  const int kf = int(keyframes.size());
   for (int stage = 0; stage <= config.upsample_stages; ++stage) {
     if (stage > 0) check(vrf_grid_upsample(ctx(), config.max_resolution));
-    for (int it = 0; it < config.iterations_per_stage; ++it, ++iteration) {
-      const std::vector<int32_t> batch =
-          draw_batch(rng, int(keyframes.size()), dataset.intrinsics, config.rays_per_batch);
-      vrf_map_step_stats st{};
-      check(vrf_mapping_step(ctx(), &cc, batch.data(), config.rays_per_batch, &st));
-      if (config.prune_every > 0 && (iteration + 1) % config.prune_every == 0) {
+    int left = config.iterations_per_stage;
+    while (left > 0) {
+      // one pipelined vrf_mapping_steps call up to the next prune point
+      int n = left;
+      if (config.prune_every > 0)
+        n = std::min(n, config.prune_every - iteration % config.prune_every);
+      std::vector<vrf_map_step_stats> st(n);
+      check(vrf_mapping_steps(ctx(), &cc, rs, kf, config.rays_per_batch, n, st.data()));
+      const double ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      for (int k = 0; k < n; ++k, ++iteration) {
+        MapLogRow row;
+        row.iteration = iteration;
+        row.stats = to_stats(st[k]);
+        row.elapsed_ms = ms;
+        result.log.push_back(row);
+      }
+      left -= n;
+      if (config.prune_every > 0 && iteration % config.prune_every == 0) {
         int64_t off = 0;
         check(vrf_grid_prune(ctx(), config.prune_threshold, &off));
       }
-      MapLogRow row;
-      row.iteration = iteration;
-      row.stats = to_stats(st);
-      row.elapsed_ms =
-          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
-              .count();
-      result.log.push_back(row);
     }
   }
   vrf_grid_geometry fg{};

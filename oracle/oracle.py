@@ -355,6 +355,15 @@ class RefLib:
         act = np.ascontiguousarray(grid.active, np.uint8)
         return self.lib.ref_grid_create(C.byref(g), _ptr(data), _ptr(act))
 
+    def fit_grid_geometry(self, frames_h, intr, initial_resolution, bounds_margin):
+        g = Geometry()
+        self.lib.ref_fit_grid_geometry.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                                   C.c_void_p]
+        self._err(self.lib.ref_fit_grid_geometry(frames_h, C.byref(intr_s(intr)),
+                                                 int(initial_resolution), float(bounds_margin),
+                                                 C.byref(g)), "fit_grid_geometry")
+        return tuple(g.res), tuple(g.origin), g.voxel_size
+
     def read_occupancy(self, handle, ncells):
         out = np.zeros(ncells, np.uint8)
         self.lib.ref_grid_occupancy(handle, _ptr(out))

@@ -164,6 +164,25 @@ void* ref_frames_create(const or_frame* frames, int n, int width, int height) {
 }
 void ref_frames_destroy(void* fs) { delete static_cast<RefFrames*>(fs); }
 
+// fit_grid_geometry (mapping.cpp:235-276) over every frame of the handle.
+int ref_fit_grid_geometry(const void* frames, const or_intrinsics* intr, int initial_resolution,
+                          double bounds_margin, or_geometry* out) {
+  REF_GUARD({
+    const auto* fs = static_cast<const RefFrames*>(frames);
+    Dataset ds;
+    ds.intrinsics = to_intr(*intr);
+    MappingConfig cfg;
+    cfg.initial_resolution = initial_resolution;
+    cfg.bounds_margin = bounds_margin;
+    const GridGeometry g = fit_grid_geometry(ds, fs->ptrs, cfg);
+    for (int a = 0; a < 3; ++a) {
+      out->res[a] = g.res[a];
+      out->origin[a] = g.origin[a];
+    }
+    out->voxel_size = g.voxel_size;
+  });
+}
+
 // ---- renderer.cpp
 int ref_sample_ray(const void* grid, const double o[3], const double d[3],
                    const or_render_params* p, int cap, double* t, double* delta, int* count) {

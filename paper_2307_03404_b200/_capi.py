@@ -121,9 +121,14 @@ _SIGS = {
     "vrf_grid_load": (C.c_int, [vp, C.c_char_p]),
     "vrf_frames_upload": (C.c_int, [vp, P(Intrinsics_c), C.c_int, P(vp), P(vp), P(Pose_c)]),
     "vrf_frames_count": (C.c_int, [vp]),
+    "vrf_frames_reserve": (C.c_int, [vp, P(Intrinsics_c), C.c_int]),
+    "vrf_frame_set": (C.c_int, [vp, C.c_int, vp, vp, P(Pose_c)]),
+    "vrf_frame_set_pose": (C.c_int, [vp, C.c_int, P(Pose_c)]),
     "vrf_render_image": (C.c_int, [vp, P(Intrinsics_c), P(Pose_c), P(RenderParams_c), C.c_int,
                                    vp, vp]),
     "vrf_mapping_step": (C.c_int, [vp, P(MappingConfig_c), vp, C.c_int, P(MapStepStats_c)]),
+    "vrf_mapping_steps": (C.c_int, [vp, P(MappingConfig_c), P(C.c_uint64), C.c_int, C.c_int,
+                                    C.c_int, P(MapStepStats_c)]),
     "vrf_mapping_step_device": (C.c_int, [vp, P(MappingConfig_c), vp, C.c_int,
                                           P(MapStepStats_c)]),
     "vrf_mapping_gradient": (C.c_int, [vp, P(MappingConfig_c), vp, C.c_int, vp,

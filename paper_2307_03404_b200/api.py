@@ -497,6 +497,28 @@ class Context:
         self.intrinsics = intrinsics
         self.n_frames = n
 
+    def reserve_frames(self, intrinsics: CameraIntrinsics, capacity: int):
+        """Slot store for online use (see vrf_frames_reserve)."""
+        ic = intrinsics._c()
+        self._check(self._lib.vrf_frames_reserve(self._h, C.byref(ic), int(capacity)))
+        self.intrinsics = intrinsics
+        self.n_frames = 0
+
+    def set_frame(self, slot: int, frame: Frame, pose: Optional[Pose] = None):
+        """Write one frame slot; pose defaults to frame.gt_pose."""
+        h, w = self.intrinsics.height, self.intrinsics.width
+        c_ = np.ascontiguousarray(frame.color, dtype=np.float64)
+        d_ = np.ascontiguousarray(frame.depth, dtype=np.float64)
+        if c_.shape != (h, w, 3) or d_.shape != (h, w):
+            raise ValueError("frame size does not match the intrinsics")
+        pc = (pose or frame.gt_pose or Pose())._c()
+        self._check(self._lib.vrf_frame_set(self._h, int(slot), _ptr(c_), _ptr(d_), C.byref(pc)))
+        self.n_frames = max(self.n_frames, int(slot) + 1)
+
+    def set_frame_pose(self, slot: int, pose: Pose):
+        pc = pose._c()
+        self._check(self._lib.vrf_frame_set_pose(self._h, int(slot), C.byref(pc)))
+
     # ---- renderer
     def render_image(self, intr: CameraIntrinsics, pose: Pose, params: RenderParams = None,
                      stride: int = 1) -> Frame:
@@ -544,6 +566,15 @@ class Context:
         self._check(self._lib.vrf_mapping_step(self._h, C.byref(cc), _ptr(b), b.shape[0],
                                                C.byref(st)))
         return _stats(st)
+
+    def mapping_steps(self, config: MappingConfig, rng: "Rng", n_keyframes: int, n_steps: int):
+        """n_steps mapping_step calls with batches drawn from rng (map_scene's inner
+        loop, mapping.cpp:302-312), host draws overlapped with device steps."""
+        st = (capi.MapStepStats_c * max(n_steps, 1))()
+        cc = config._c()
+        self._check(self._lib.vrf_mapping_steps(self._h, C.byref(cc), rng.state, int(n_keyframes),
+                                                int(config.rays_per_batch), int(n_steps), st))
+        return [_stats(st[i]) for i in range(n_steps)]
 
     def mapping_step_device(self, config: MappingConfig, batch_dev_ptr: int, n: int) -> MapStepStats:
         st = capi.MapStepStats_c()
@@ -760,3 +791,89 @@ def track_sequence(grid: VoxelGrid, frames: Sequence[Frame], intrinsics: CameraI
         if not tf.failed:
             prev_prev, prev, have_two = prev, tf.pose, True
     return poses, status
+
+
+def generate_ray(intr: CameraIntrinsics, pose: Pose, px: float, py: float):
+    """generate_ray — camera.hpp:33-41 (host helper for geometry fitting)."""
+    v = np.array([(px - intr.cx) / intr.fx, (py - intr.cy) / intr.fy, 1.0])
+    v = v / math.sqrt(float(v @ v))
+    return np.asarray(pose.t, np.float64), pose.rotation() @ v
+
+
+def fit_grid_geometry(frames: Sequence[Frame], keyframes: Sequence[int],
+                      intrinsics: CameraIntrinsics, config: MappingConfig) -> GridGeometry:
+    """fit_grid_geometry — mapping.cpp:235-276: bounds of the back-projected valid
+    depth (every 8th pixel) and camera centres, plus the margin."""
+    lo = np.full(3, np.inf)
+    hi = -lo
+    ys = np.arange(0, intrinsics.height, 8)
+    xs = np.arange(0, intrinsics.width, 8)
+    for k in keyframes:
+        f = frames[k]
+        if f.gt_pose is None:
+            continue
+        t = np.asarray(f.gt_pose.t, np.float64)
+        lo, hi = np.minimum(lo, t), np.maximum(hi, t)
+        d = np.asarray(f.depth)[np.ix_(ys, xs)]
+        yy, xx = np.meshgrid(ys, xs, indexing="ij")
+        ok = d > 0.0
+        if not ok.any():
+            continue
+        cam = np.stack([(xx[ok] - intrinsics.cx) / intrinsics.fx,
+                        (yy[ok] - intrinsics.cy) / intrinsics.fy, np.ones(int(ok.sum()))], 1)
+        cam /= np.sqrt(np.sum(cam * cam, 1, keepdims=True))
+        p = t + d[ok][:, None] * (cam @ f.gt_pose.rotation().T)
+        lo, hi = np.minimum(lo, p.min(0)), np.maximum(hi, p.max(0))
+    if not (np.all(np.isfinite(lo)) and np.all(np.isfinite(hi))):
+        raise RuntimeError("fit_grid_geometry: no valid depth to bound the scene")
+    margin = (hi - lo) * config.bounds_margin
+    lo, hi = lo - margin, hi + margin
+    voxel = float(np.max(hi - lo)) / float(config.initial_resolution - 1)
+    res, origin = [], []
+    for a in range(3):
+        cells = max(1, int(math.ceil((hi[a] - lo[a]) / voxel - 1e-9)))
+        res.append(cells + 1)
+        origin.append(float(lo[a] - 0.5 * (cells * voxel - (hi[a] - lo[a]))))
+    g = GridGeometry(tuple(res), tuple(origin), voxel)
+    g.validate()
+    return g
+
+
+def map_scene(frames: Sequence[Frame], intrinsics: CameraIntrinsics, config: MappingConfig,
+              geometry: Optional[GridGeometry] = None, ctx: Optional[Context] = None):
+    """map_scene — mapping.hpp:98-99 (mapping.cpp:278-316). The grid, RMSProp state
+    and keyframes stay in HBM for the whole stage schedule (device upsampling
+    between stages); returns (grid, log rows (iteration, stats, elapsed_ms))."""
+    import time
+    if not frames:
+        raise RuntimeError("map_scene: empty dataset")
+    keys = list(range(0, len(frames), config.keyframe_stride))
+    for i in keys:
+        if frames[i].gt_pose is None:
+            raise RuntimeError(f"map_scene: keyframe {i} has no pose")
+    geom = geometry or fit_grid_geometry(frames, keys, intrinsics, config)
+    ctx = ctx or default_context()
+    ctx.init_grid(geom, config.sigma_init)
+    ctx.load_frames(intrinsics, [frames[i] for i in keys])
+    rng = Rng(config.seed)
+    log = []
+    t0 = time.perf_counter()
+    it_global = 0
+    for stage in range(config.upsample_stages + 1):
+        if stage > 0:
+            ctx.upsample(config.max_resolution)
+        left = config.iterations_per_stage
+        while left > 0:
+            # run up to the next prune point in one pipelined call
+            n = left
+            if config.prune_every > 0:
+                n = min(n, config.prune_every - it_global % config.prune_every)
+            stats = ctx.mapping_steps(config, rng, len(keys), n)
+            ms = (time.perf_counter() - t0) * 1e3
+            for st in stats:
+                log.append((it_global, st, ms))
+                it_global += 1
+            left -= n
+            if config.prune_every > 0 and it_global % config.prune_every == 0:
+                ctx.prune(config.prune_threshold)
+    return ctx.download_grid(), log

@@ -62,9 +62,10 @@ void vrf_context_destroy(vrf_context* ctx) {
                            &ctx->s_otmp, &ctx->s_batch, &ctx->s_raycd, &ctx->s_flags, &ctx->s_partials,
                            &ctx->s_count, &ctx->s_offsets, &ctx->s_keys, &ctx->s_keys2,
                            &ctx->s_ids, &ctx->s_ids2, &ctx->s_values, &ctx->s_grad64, &ctx->s_cub,
-                           &ctx->s_stage, &ctx->s_out})
+                           &ctx->s_stage, &ctx->s_out, &ctx->s_batch2})
     cudaFree(s->ptr);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  if (ctx->h_pipe) cudaFreeHost(ctx->h_pipe);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -450,10 +451,72 @@ int vrf_frames_upload(vrf_context* ctx, const vrf_intrinsics* intr, int n,
   }
   ctx->fintr = *intr;
   ctx->n_frames = n;
+  ctx->frame_capacity = n;
   return VRF_OK;
 }
 
 int vrf_frames_count(const vrf_context* ctx) { return ctx->n_frames; }
+
+int vrf_frames_reserve(vrf_context* ctx, const vrf_intrinsics* intr, int capacity) {
+  cudaSetDevice(ctx->device);
+  if (capacity < 0 || !intr || intr->width <= 0 || intr->height <= 0)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "intrinsics: empty image size");
+  CU(cudaStreamSynchronize(ctx->stream));
+  cudaFree(ctx->rgbd);
+  cudaFree(ctx->poses);
+  ctx->rgbd = nullptr;
+  ctx->poses = nullptr;
+  ctx->n_frames = 0;
+  ctx->frame_capacity = 0;
+  ctx->host_depth.assign(capacity, {});
+  const long long npix = (long long)intr->width * intr->height;
+  if (capacity > 0) {
+    CU(cudaMalloc(&ctx->rgbd, sizeof(double4) * npix * capacity));
+    CU(cudaMalloc(&ctx->poses, sizeof(DevPose) * capacity));
+  }
+  ctx->fintr = *intr;
+  ctx->frame_capacity = capacity;
+  return VRF_OK;
+}
+
+int vrf_frame_set(vrf_context* ctx, int slot, const double* color, const double* depth,
+                  const vrf_pose* pose) {
+  cudaSetDevice(ctx->device);
+  if (slot < 0 || slot >= ctx->frame_capacity)
+    return set_err(ctx, VRF_ERR_OUT_OF_RANGE, "frames: slot out of range");
+  const long long npix = (long long)ctx->fintr.width * ctx->fintr.height;
+  int rc = ensure(ctx, ctx->s_stage, sizeof(double) * npix * 4);
+  if (rc) return rc;
+  if ((rc = ensure_pinned(ctx, sizeof(DevPose)))) return rc;
+  double* st = (double*)ctx->s_stage.ptr;
+  CU(cudaMemcpyAsync(st, color, sizeof(double) * npix * 3, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(st + npix * 3, depth, sizeof(double) * npix, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  launch_pack_frames(st, st + npix * 3, ctx->rgbd + npix * slot, npix, ctx->stream);
+  LAUNCHED(1);
+  const DevPose dp = dev_pose(pose);
+  std::memcpy(ctx->h_pinned, &dp, sizeof(dp));
+  CU(cudaMemcpyAsync(ctx->poses + slot, ctx->h_pinned, sizeof(DevPose), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  ctx->host_depth[slot].assign(depth, depth + npix);
+  ctx->n_frames = std::max(ctx->n_frames, slot + 1);
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_frame_set_pose(vrf_context* ctx, int slot, const vrf_pose* pose) {
+  cudaSetDevice(ctx->device);
+  if (slot < 0 || slot >= ctx->n_frames)
+    return set_err(ctx, VRF_ERR_OUT_OF_RANGE, "frames: slot out of range");
+  int rc = ensure_pinned(ctx, sizeof(DevPose));
+  if (rc) return rc;
+  const DevPose dp = dev_pose(pose);
+  std::memcpy(ctx->h_pinned, &dp, sizeof(dp));
+  CU(cudaMemcpyAsync(ctx->poses + slot, ctx->h_pinned, sizeof(DevPose), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
 
 // ----------------------------------------------------------------- render_image
 int vrf_render_image(vrf_context* ctx, const vrf_intrinsics* intr, const vrf_pose* pose,

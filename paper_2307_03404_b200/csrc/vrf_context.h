@@ -49,7 +49,8 @@ struct vrf_context {
   unsigned int* d_nblocks = nullptr;
 
   // frames
-  int n_frames = 0;
+  int n_frames = 0;         // slots in use (high-water mark of vrf_frame_set)
+  int frame_capacity = 0;   // allocated slots
   vrf_intrinsics fintr{};
   double4* rgbd = nullptr;
   DevPose* poses = nullptr;
@@ -65,10 +66,13 @@ struct vrf_context {
   // pinned host staging
   void* h_pinned = nullptr;
   size_t h_pinned_bytes = 0;
+  // pinned double buffer of the pipelined mapping loop (vrf_mapping_steps)
+  void* h_pipe = nullptr;
+  size_t h_pipe_bytes = 0;
 
   // grow-only scratch
   vrf_host::DeviceScratch s_batch, s_raycd, s_flags, s_partials, s_count, s_offsets, s_keys, s_keys2,
-      s_ids, s_ids2, s_values, s_grad64, s_cub, s_stage, s_out;
+      s_ids, s_ids2, s_values, s_grad64, s_cub, s_stage, s_out, s_batch2;
 
   // multi-GPU phase state
   const int* last_batch = nullptr;

@@ -13,6 +13,7 @@
 //   K5 k_pose_forward/     per-ray 4x6 Jacobian of [C; D] w.r.t. [omega; tau] ->
 //      k_pose_backward     J^T J (21) + J^T r (6) + loss      gradients.cpp:116-143,
 //                                                tracking.cpp:104-130
+#include <cstdlib>
 #include <climits>
 
 #include "vrf_internal.h"
@@ -366,7 +367,92 @@ __device__ __forceinline__ void move_cell(float4* __restrict__ grad, const DevGr
   }
 }
 
-template <typename ShT, int MINB, bool SKIP>
+// Fast-path backward of one ray (fp32 SH, fp32 gradient accumulation). Same
+// schedule, sigma_raw replay, T and termination as the forward pass (all FP64,
+// reference order), so exactly the forward's samples are visited. The colour /
+// depth terms of dL/dsigma_i use the running form
+//   sum_ch upc_ch (c_ch T_{i+1} - C_ch + prefix_ch) = uc_i T_{i+1} + Q_i,
+//   Q_i = sum_ch upc_ch (prefix_ch,i - C_ch),  uc_i = sum_ch upc_ch c_ch,i
+// (gradients.cpp:69-97 regrouped), which keeps 3 FP64 scalars live instead of 11.
+// Per-ray scatter aggregation: the 28-slot upstream of a sample is
+// [dL/dsigma, dcol_ch * basis_m] and basis is constant along the ray, so the
+// contribution to corner k over any run of samples factorises into
+// a[0][k] = sum w_k up_sigma and a[1+ch][k] = sum w_k dcol_ch (clamp-gated):
+// 32 registers instead of 224. Corners are flushed (red.global.add.v4.f32)
+// only when the ray leaves them; corners shared with a face-adjacent next cell
+// are carried over.
+template <bool SKIP>
+__device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevParams& p, March& m,
+                                                  const MapUp& u, float4* __restrict__ grad) {
+  float bf[9];
+  {
+    double basis[9];
+    if (!sh_basis(m.d, basis)) return;
+#pragma unroll
+    for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
+  }
+  if (!march_begin(g, p, m)) return;
+  const double upc0 = u.upc[0], upc1 = u.upc[1], upc2 = u.upc[2];
+  const bool use_depth = u.use_depth;
+  const double upd = use_depth ? u.upd : 0.0;
+  double T = 1.0;
+  double Q = -(upc0 * u.C[0] + upc1 * u.C[1] + upc2 * u.C[2]);
+  double Qd = -upd * u.D;
+  float a[4][8];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
+  uint32_t cur = 0xffffffffu;
+  Sample s;
+  while (march_next<SKIP>(g, m, s)) {
+    Shade sh;
+    {
+      double w[8];
+      corner_weights(s, w);
+      shade_fast(g, s, w, bf, sh);
+    }
+    const double sigma = (sh.sigma_raw < 0.0) ? 0.0 : sh.sigma_raw;
+    const double decay = exp(dmul(-sigma, s.delta));
+    const double wgt = dmul(T, dsub(1.0, decay));
+    const double T_next = dmul(T, decay);
+    const double uc = upc0 * sh.c[0] + upc1 * sh.c[1] + upc2 * sh.c[2];
+    Q += uc * wgt;
+    double ds = uc * T_next + Q;
+    if (use_depth) {
+      Qd += upd * (s.t * wgt);
+      ds += upd * (s.t * T_next) + Qd;
+    }
+    ds *= s.delta;
+    if (s.base != cur) {
+      if (cur != 0xffffffffu) move_cell(grad, g, cur, s.base, a, bf);
+      cur = s.base;
+    }
+    const float wf = (float)wgt;
+    const float u0 = sh.sigma_raw > 0.0 ? (float)ds : 0.f;
+    const float u1 = sh.clamped[0] ? 0.f : (float)upc0 * wf;
+    const float u2 = sh.clamped[1] ? 0.f : (float)upc1 * wf;
+    const float u3 = sh.clamped[2] ? 0.f : (float)upc2 * wf;
+    const float fx = (float)s.fx, fy = (float)s.fy, fz = (float)s.fz;
+    const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
+      a[0][k] = fmaf(wk, u0, a[0][k]);
+      a[1][k] = fmaf(wk, u1, a[1][k]);
+      a[2][k] = fmaf(wk, u2, a[2][k]);
+      a[3][k] = fmaf(wk, u3, a[3][k]);
+    }
+    T = T_next;
+    if (T < p.eps) break;
+  }
+  if (cur != 0xffffffffu) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) flush_corner(grad, g, cur, a, bf, k);
+  }
+}
+
+template <int MINB, bool SKIP>
 __global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
@@ -386,47 +472,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
   if (!map_upstream(st, global_counts, ray_cd[i], tg, fl, lambda_d, u)) return;
   March m;
   ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
-  // Per-ray scatter aggregation. The 28-slot upstream of a sample is
-  // [dL/dsigma, dcol_ch * basis_m] and basis is constant along the ray, so the
-  // contribution to corner k over any run of samples factorises into
-  // a[0][k] = sum w_k up_sigma and a[1+ch][k] = sum w_k dcol_ch (clamp-gated):
-  // 32 registers instead of 224. Corners are flushed (red.global.add.v4.f32)
-  // only when the ray leaves them; corners shared with a face-adjacent next
-  // cell are carried over.
-  float a[4][8];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
-  float bf[9];
-  uint32_t cur = 0xffffffffu;
-  map_backward_ray<ShT, SKIP>(g, p, m, u,
-                        [&](int, const Sample& s, const double w[8], double up0,
-                            const double dcol[3], const bool clamped[3], const double basis[9]) {
-                          if (cur == 0xffffffffu) {
-#pragma unroll
-                            for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
-                          } else if (s.base != cur) {
-                            move_cell(grad, g, cur, s.base, a, bf);
-                          }
-                          cur = s.base;
-                          const float u0 = (float)up0;
-                          const float u1 = clamped[0] ? 0.f : (float)dcol[0];
-                          const float u2 = clamped[1] ? 0.f : (float)dcol[1];
-                          const float u3 = clamped[2] ? 0.f : (float)dcol[2];
-#pragma unroll
-                          for (int k = 0; k < 8; ++k) {
-                            const float wk = (float)w[k];
-                            a[0][k] = fmaf(wk, u0, a[0][k]);
-                            a[1][k] = fmaf(wk, u1, a[1][k]);
-                            a[2][k] = fmaf(wk, u2, a[2][k]);
-                            a[3][k] = fmaf(wk, u3, a[3][k]);
-                          }
-                        });
-  if (cur != 0xffffffffu) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) flush_corner(grad, g, cur, a, bf, k);
-  }
+  map_backward_fast<SKIP>(g, p, m, u, grad);
 }
 
 // ------------------------------------------------------------------ K3 deterministic records
@@ -923,18 +969,31 @@ void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam
                          const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
                          const int* global_counts, float4* grad, double lambda_d, bool fast,
                          const uint32_t* order, cudaStream_t s) {
-  // 4 CTAs x 128 threads per SM: 128 registers (measured best of 2/3/4, r01).
+  // 4 CTAs x 128 threads per SM: 128 registers (measured best of 2/3/4, r01);
+  // VRF_BWD_MINB=3 selects the 168-register build for A/B runs.
   // The empty-block jump is compiled in only when the grid has empty blocks.
   (void)fast;
+  static const int minb = [] {
+    const char* e = std::getenv("VRF_BWD_MINB");
+    return (e && std::atoi(e) == 3) ? 3 : 4;
+  }();
   const int blocks = (n + kThreads - 1) / kThreads;
-  if (g.all_blocks_active)
-    k_map_backward<float, 4, false><<<blocks, kThreads, 0, s>>>(
-        g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
-        order);
-  else
-    k_map_backward<float, 4, true><<<blocks, kThreads, 0, s>>>(
-        g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
-        order);
+#define VRF_BWD_LAUNCH(MB, SK)                                                                 \
+  k_map_backward<MB, SK><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd, \
+                                                     flags, stats, global_counts, grad,        \
+                                                     lambda_d, order)
+  if (minb == 3) {
+    if (g.all_blocks_active)
+      VRF_BWD_LAUNCH(3, false);
+    else
+      VRF_BWD_LAUNCH(3, true);
+  } else {
+    if (g.all_blocks_active)
+      VRF_BWD_LAUNCH(4, false);
+    else
+      VRF_BWD_LAUNCH(4, true);
+  }
+#undef VRF_BWD_LAUNCH
 }
 void launch_map_backward_records(const DevGrid& g, const DevParams& p, const DevCam& cam,
                                  const double4* rgbd, const DevPose* poses, const int* batch,

@@ -242,6 +242,79 @@ int vrf_mapping_step(vrf_context* ctx, const vrf_mapping_config* cfg, const int3
   return step_impl(ctx, cfg, dev, batch, n_rays, out);
 }
 
+// map_scene's inner loop (mapping.cpp:302-312): n_steps mapping_step calls whose
+// batches come from the reference Rng stream (mapping.cpp:121-128). The host
+// draws batch i+1 into the other half of a pinned double buffer while the device
+// runs step i, so the single-threaded draw is off the critical path; each step
+// still uploads its batch and reads its stats back.
+int vrf_mapping_steps(vrf_context* ctx, const vrf_mapping_config* cfg, uint64_t rng_state[4],
+                      int n_keyframes, int n_rays, int n_steps, vrf_map_step_stats* out) {
+  cudaSetDevice(ctx->device);
+  int rc = check_ready(ctx);
+  if (rc) return rc;
+  if (n_keyframes < 1 || n_keyframes > ctx->n_frames)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "mapping_step: keyframe index out of range");
+  if (n_rays < 0 || n_steps < 0)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "mapping_step: negative batch size");
+  const int W = ctx->fintr.width, H = ctx->fintr.height;
+  if (cfg->deterministic || n_rays == 0) {  // sequential: the sorted reduce syncs anyway
+    std::vector<int32_t> b((size_t)3 * (n_rays > 0 ? n_rays : 1));
+    for (int i = 0; i < n_steps; ++i) {
+      vrf_rng_draw_batch(rng_state, n_keyframes, W, H, n_rays, b.data());
+      if ((rc = vrf_mapping_step(ctx, cfg, b.data(), n_rays, out ? out + i : nullptr))) return rc;
+    }
+    return VRF_OK;
+  }
+  const size_t bbytes = sizeof(int32_t) * 3 * (size_t)n_rays;
+  const size_t half = (bbytes + 255) / 256 * 256;
+  const size_t need = 2 * half + 2 * 256;
+  if (ctx->h_pipe_bytes < need) {
+    if (ctx->h_pipe) CU(cudaFreeHost(ctx->h_pipe));
+    ctx->h_pipe = nullptr;
+    ctx->h_pipe_bytes = 0;
+    CU(cudaMallocHost(&ctx->h_pipe, need));
+    ctx->h_pipe_bytes = need;
+  }
+  if ((rc = ensure(ctx, ctx->s_batch, bbytes))) return rc;
+  if ((rc = ensure(ctx, ctx->s_batch2, bbytes))) return rc;
+  char* hp = (char*)ctx->h_pipe;
+  int32_t* hb[2] = {(int32_t*)hp, (int32_t*)(hp + half)};
+  MapStats* h_st = (MapStats*)(hp + 2 * half);
+  int* h_err = (int*)(hp + 2 * half + 256);
+  const int* db[2] = {(const int*)ctx->s_batch.ptr, (const int*)ctx->s_batch2.ptr};
+  DevParams p;
+  if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
+  vrf_rng_draw_batch(rng_state, n_keyframes, W, H, n_rays, hb[0]);
+  for (int i = 0; i < n_steps; ++i) {
+    const int c = i & 1;
+    CU(cudaMemcpyAsync((void*)db[c], hb[c], bbytes, cudaMemcpyHostToDevice, ctx->stream));
+    if ((rc = map_gradient(ctx, cfg, db[c], n_rays, nullptr, false))) return rc;
+    cudaEvent_t pr = prof_begin(ctx);
+    launch_rmsprop((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, 0, ctx->V,
+                   cfg->rmsprop_decay, cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, ctx->d_stats,
+                   ctx->profiling ? ctx->d_touched : nullptr, ctx->stream);
+    prof_end(ctx, kProfRmsprop, pr);
+    LAUNCHED(1);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(h_st, ctx->d_stats, sizeof(MapStats), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(h_err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (i + 1 < n_steps)  // overlaps the device work of step i
+      vrf_rng_draw_batch(rng_state, n_keyframes, W, H, n_rays, hb[c ^ 1]);
+    CU(cudaStreamSynchronize(ctx->stream));
+    prof_collect(ctx);
+    if (*h_err & 2) return set_err(ctx, VRF_ERR_OUT_OF_RANGE, "generate_ray: pixel outside image");
+    if (*h_err & 1)
+      return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "sh_eval: direction must be unit length");
+    const MapStats st = *h_st;
+    if (st.m_c == 0 || st.bad != INT_MAX) {
+      CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * (size_t)ctx->Vpad, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+    }
+    if ((rc = finish_stats(ctx, cfg, st, hb[c], out ? out + i : nullptr))) return rc;
+  }
+  return VRF_OK;
+}
+
 int vrf_mapping_step_device(vrf_context* ctx, const vrf_mapping_config* cfg,
                             const int32_t* batch_dev, int n_rays, vrf_map_step_stats* out) {
   cudaSetDevice(ctx->device);

@@ -1,0 +1,117 @@
+"""Interleaved SLAM driver (config 5).
+
+The reference is offline only: map_scene with GT poses, then track_sequence
+against the finished map. This driver composes the same two
+hot paths online, the way the paper runs them: every frame is tracked against
+the map being built (device Gauss-Newton, Context.track_frame_gn), and every
+``keyframe_stride``-th frame joins the keyframe set at its *estimated* pose and
+triggers ``map_steps`` mapping_step calls over all keyframes so far.
+
+Device residency: the grid, its RMSProp state, the keyframes and the tracking
+frame live in one Context (frame slots: 0..max_keyframes-1 keyframes, slot
+max_keyframes the frame being tracked). Per frame the host uploads only that
+frame (its RGB-D image, as a sensor would deliver it) and reads back a pose.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from .api import (CameraIntrinsics, Context, Frame, GNConfig, GridGeometry, MappingConfig, Pose,
+                  Rng, pose_compose, pose_inverse)
+
+
+@dataclass
+class SlamConfig:
+    keyframe_stride: int = 10
+    map_steps: int = 10                 # mapping_step calls per new keyframe
+    bootstrap_steps: int = 200          # mapping_step calls on frame 0 before tracking
+    max_keyframes: int = 256
+    constant_velocity: bool = True      # track_sequence init policy (tracking.cpp:271-272)
+    tracking: GNConfig = field(default_factory=GNConfig)
+    mapping: MappingConfig = field(default_factory=lambda: MappingConfig(rays_per_batch=65536))
+
+
+@dataclass
+class SlamFrameLog:
+    frame: int
+    keyframe: bool
+    track_ms: float
+    map_ms: float
+    final_loss: float
+
+
+class SlamSystem:
+    """Online tracking + keyframe mapping on one device context."""
+
+    def __init__(self, ctx: Context, intrinsics: CameraIntrinsics, geometry: GridGeometry,
+                 config: SlamConfig):
+        self.ctx = ctx
+        self.intr = intrinsics
+        self.cfg = config
+        ctx.init_grid(geometry, config.mapping.sigma_init)
+        ctx.reserve_frames(intrinsics, config.max_keyframes + 1)
+        self.track_slot = config.max_keyframes
+        self.n_keyframes = 0
+        self.rng = Rng(config.mapping.seed)
+        self.poses: List[Pose] = []
+        self.log: List[SlamFrameLog] = []
+
+    def _map(self, steps: int):
+        m = self.cfg.mapping
+        for _ in range(steps):
+            batch = self.rng.draw_batch(self.n_keyframes, self.intr.width, self.intr.height,
+                                        m.rays_per_batch)
+            self.ctx.mapping_step(m, batch)
+
+    def _add_keyframe(self, frame: Frame, pose: Pose):
+        if self.n_keyframes >= self.cfg.max_keyframes:
+            raise RuntimeError("slam: keyframe capacity exhausted")
+        self.ctx.set_frame(self.n_keyframes, frame, pose)
+        self.n_keyframes += 1
+
+    def process(self, frame: Frame, init_pose: Optional[Pose] = None) -> Pose:
+        """Track (or, for the first frame, anchor at init_pose) and map."""
+        i = len(self.poses)
+        t0 = time.perf_counter()
+        if i == 0:
+            pose = init_pose or frame.gt_pose
+            if pose is None:
+                raise RuntimeError("slam: the first frame needs a pose")
+            loss = 0.0
+            t1 = time.perf_counter()
+            self._add_keyframe(frame, pose)
+            self._map(self.cfg.bootstrap_steps)
+            self.poses.append(pose)
+            self.log.append(SlamFrameLog(0, True, 0.0, (time.perf_counter() - t1) * 1e3, loss))
+            return pose
+        prev = self.poses[-1]
+        init = prev
+        if self.cfg.constant_velocity and i >= 2:
+            init = pose_compose(prev, pose_compose(pose_inverse(self.poses[-2]), prev))
+        self.ctx.set_frame(self.track_slot, frame, init)
+        r = self.ctx.track_frame_gn(self.track_slot, self.intr, init, self.cfg.tracking)
+        pose = r.pose
+        t1 = time.perf_counter()
+        key = i % self.cfg.keyframe_stride == 0
+        if key:
+            self._add_keyframe(frame, pose)
+            self._map(self.cfg.map_steps)
+        t2 = time.perf_counter()
+        self.poses.append(pose)
+        self.log.append(SlamFrameLog(i, key, (t1 - t0) * 1e3, (t2 - t1) * 1e3,
+                                     r.loss_trace[-1] if r.loss_trace else 0.0))
+        return pose
+
+
+def run_slam(ctx: Context, intrinsics: CameraIntrinsics, geometry: GridGeometry, frames,
+             config: SlamConfig = None):
+    """Runs the loop over an iterable of Frames (gt_pose used for frame 0 only).
+    Returns (estimated poses, per-frame log)."""
+    s = SlamSystem(ctx, intrinsics, geometry, config or SlamConfig())
+    for f in frames:
+        s.process(f)
+    return s.poses, s.log

@@ -189,6 +189,29 @@ def room_path(n, room: Room, seed=4, step_m=0.01, step_deg=0.5, height=1.5):
     return poses
 
 
+def ellipse_trajectory(n, room: Room, height=1.5, fps=30.0, a_frac=0.3, b_frac=0.25,
+                       look_out=0.6, pitch=-0.15):
+    """Closed-loop ellipse (config 5): the camera circles the room
+    centre once over n frames, heading along the tangent turned outward by
+    ``look_out`` rad toward the walls. Returns (poses, timestamps)."""
+    lo, hi = np.array(room.room_min), np.array(room.room_max)
+    c = 0.5 * (lo + hi)
+    a = a_frac * (hi[0] - lo[0])
+    b = b_frac * (hi[1] - lo[1])
+    poses, ts = [], []
+    for i in range(n):
+        th = 2.0 * math.pi * i / n
+        eye = np.array([c[0] + a * math.cos(th), c[1] + b * math.sin(th), height])
+        tangent = np.array([-a * math.sin(th), b * math.cos(th), 0.0])
+        tangent /= np.linalg.norm(tangent)
+        outward = np.array([tangent[1], -tangent[0], 0.0])
+        fwd = math.cos(look_out) * tangent + math.sin(look_out) * outward
+        target = eye + np.array([fwd[0], fwd[1], pitch])
+        poses.append(look_at(eye, target))
+        ts.append(i / fps)
+    return poses, ts
+
+
 def quantize_frame(color: np.ndarray, depth: np.ndarray, depth_scale: float):
     """quantize_color / quantize_depth — image.cpp:15-30."""
     c8 = np.clip(np.floor(color * 255.0 + 0.5), 0, 255) / 255.0

@@ -336,3 +336,38 @@ def test_vxgf_roundtrip_with_reference(ctx, ref, tmp_path):
         ctx.load_grid_file(tmp_path / "nan.vxgf")
     with pytest.raises(RuntimeError, match="cannot open"):
         ctx.load_grid_file(tmp_path / "missing.vxgf")
+
+
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_mapping_steps_pipeline_equals_step_loop(ctx, deterministic):
+    """vrf_mapping_steps (draw of batch i+1 overlapped with step i) == the plain
+    loop of Rng draw + mapping_step (mapping.cpp:302-312)."""
+    from paper_2307_03404_b200.api import Rng
+    grid, intr, frames = room_scene()
+    cfg = MappingConfig(rays_per_batch=700, deterministic=deterministic)
+    start = fresh_grid(grid)
+    ctx.load_grid(start)
+    ctx.load_frames(intr, frames)
+    ctx.rmsprop_reset()
+    r1 = Rng(5)
+    a = ctx.mapping_steps(cfg, r1, len(frames), 4)
+    ga = ctx.download_grid().data
+    ctx.load_grid(start)
+    ctx.rmsprop_reset()
+    r2 = Rng(5)
+    b = [ctx.mapping_step(cfg, r2.draw_batch(len(frames), intr.width, intr.height, 700))
+         for _ in range(4)]
+    gb = ctx.download_grid().data
+    assert r1.next_u64() == r2.next_u64()
+    for x, y in zip(a, b):
+        assert x.rays_color == y.rays_color and x.samples == y.samples
+        if deterministic:
+            assert x.loss_total == y.loss_total
+        else:
+            assert x.loss_total == pytest.approx(y.loss_total, rel=1e-5)
+    if deterministic:
+        assert np.array_equal(ga, gb)
+    else:
+        assert np.max(np.abs(ga - gb)) <= 1e-4 * np.max(np.abs(gb))
+    with pytest.raises(ValueError, match="keyframe index out of range"):
+        ctx.mapping_steps(cfg, r1, len(frames) + 1, 1)

@@ -166,3 +166,20 @@ def test_upsample_matches_reference(oracle, ref):
         ref.lib.ref_grid_destroy(h)
     with pytest.raises(RuntimeError, match="exceed configured maximum"):
         oracle.upsample(grid, 16)
+
+
+def test_fit_grid_geometry_matches_reference(ref):
+    """api.fit_grid_geometry (host, mapping.cpp:235-276) == the reference's."""
+    from paper_2307_03404_b200.api import fit_grid_geometry
+    grid, intr, frames = room_scene()
+    fh = ref.frames(frames, intr)
+    try:
+        for res0, margin in [(33, 0.05), (17, 0.2)]:
+            cfg = MappingConfig(initial_resolution=res0, bounds_margin=margin)
+            g = fit_grid_geometry(frames, list(range(len(frames))), intr, cfg)
+            r = ref.fit_grid_geometry(fh, intr, res0, margin)
+            assert tuple(g.res) == r[0]
+            assert np.allclose(g.origin, r[1], rtol=0, atol=1e-12)
+            assert g.voxel_size == pytest.approx(r[2], rel=1e-14)
+    finally:
+        ref.lib.ref_frames_destroy(fh)
