@@ -26,7 +26,8 @@ from paper_2307_03404_b200.slam import SlamConfig, SlamSystem  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--frames", type=int, default=2000)
+    ap.add_argument("--frames", type=int, default=2000, help="frames processed")
+    ap.add_argument("--loop", type=int, default=2000, help="frames in the closed loop")
     ap.add_argument("--res", type=int, default=257)
     ap.add_argument("--width", type=int, default=1200)
     ap.add_argument("--height", type=int, default=680)
@@ -36,6 +37,10 @@ def main():
     ap.add_argument("--bootstrap", type=int, default=200)
     ap.add_argument("--track-rays", type=int, default=16384)
     ap.add_argument("--track-iters", type=int, default=10)
+    ap.add_argument("--sigma-init", type=float, default=0.1)
+    ap.add_argument("--trace", action="store_true", help="print per-frame position error")
+    ap.add_argument("--gt-map", action="store_true",
+                    help="plumbing check: track against the ground-truth map, no mapping")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
 
@@ -44,7 +49,8 @@ def main():
     s = args.width / 1200.0
     intr = synth.CameraIntrinsics(600.0 * s, 600.0 * s, args.width / 2 - 0.5,
                                   args.height / 2 - 0.5, args.width, args.height, 6553.5)
-    poses, ts = synth.ellipse_trajectory(args.frames, room)
+    poses, ts = synth.ellipse_trajectory(args.loop, room)
+    poses, ts = poses[:args.frames], ts[:args.frames]
     sensor = Context(0)
     sensor.load_grid(gt)
 
@@ -59,9 +65,13 @@ def main():
                      max_keyframes=(args.frames + args.stride - 1) // args.stride + 1,
                      tracking=GNConfig(rays_per_iteration=args.track_rays,
                                        iterations=args.track_iters),
-                     mapping=MappingConfig(rays_per_batch=args.map_rays, sigma_init=0.1))
+                     mapping=MappingConfig(rays_per_batch=args.map_rays,
+                                           sigma_init=args.sigma_init))
     ctx = Context(0)
     slam = SlamSystem(ctx, intr, geom, cfg)
+    if args.gt_map:
+        ctx.load_grid(gt)
+        cfg.bootstrap_steps = cfg.map_steps = 0
     slam_s = 0.0
     gen_s = 0.0
     for i in range(args.frames):
@@ -73,6 +83,10 @@ def main():
         gen_s += t1 - t0
         if i > 0:
             slam_s += t2 - t1
+        if args.trace and (i % 10 == 0 or i < 10):
+            e = np.linalg.norm(np.asarray(slam.poses[-1].t) - np.asarray(poses[i].t))
+            print(f"frame {i}: pos err {e:.4f} m, loss {slam.log[-1].final_loss:.4g}",
+                  file=sys.stderr)
     est = slam.poses
     ate, pairs = metrics.ate_rmse(est, ts, poses, ts, align=True)
     ate_u, _ = metrics.ate_rmse(est, ts, poses, ts, align=False)
@@ -88,7 +102,8 @@ def main():
     logs = slam.log[1:]
     n = len(logs)
     out = {
-        "config": "config5: SLAM, 1200x680, 257^3 grid, closed-loop ellipse",
+        "config": f"config5: SLAM, {args.width}x{args.height}, {args.res}^3 grid, "
+                  f"closed-loop ellipse of {args.loop} frames",
         "frames": args.frames, "keyframes": slam.n_keyframes,
         "frames_per_s": n / slam_s if slam_s > 0 else None,
         "track_ms_per_frame": float(np.mean([l.track_ms for l in logs])) if n else None,
