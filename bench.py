@@ -39,6 +39,9 @@ sys.path.insert(0, str(ROOT))
 METRIC = "mapping samples/s & rays/s (fwd+bwd) and tracking frames/s at 1/2/4/8 B200"
 WORKLOAD = ("config3: Replica-shaped 1200x680 RGB-D, 256^3-cell (257^3-vertex) grid, "
             "incremental mapping fwd+bwd with RGB+depth loss + RMSProp")
+WORKLOAD4 = ("config4: 512^3-cell (513^3-vertex) sparse grid (config-2 room map upsampled on "
+             "the device and pruned to its near-surface shell, re-initialised to sigma_init), "
+             "200 keyframes of 1200x680, 8M rays/batch per GPU, mapping fwd+bwd + RMSProp")
 
 
 def parse():
@@ -47,16 +50,25 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rays", type=int, default=1 << 20)
+    ap.add_argument("--config", type=int, default=3, choices=[3, 4],
+                    help="3: the headline 257^3 mapping workload; 4: 513^3 sparse, 8M rays")
+    ap.add_argument("--rays", type=int, default=None)
     ap.add_argument("--res", type=int, default=257)
-    ap.add_argument("--keyframes", type=int, default=10)
+    ap.add_argument("--keyframes", type=int, default=None)
     ap.add_argument("--width", type=int, default=1200)
     ap.add_argument("--height", type=int, default=680)
     ap.add_argument("--track-frames", type=int, default=6)
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.rays is None:
+        a.rays = (8 << 20) if a.config == 4 else (1 << 20)
+    if a.keyframes is None:
+        a.keyframes = 200 if a.config == 4 else 10
+    if a.config == 4:
+        a.no_tracking = True
+    return a
 
 
 # ----------------------------------------------------------------- inputs
@@ -93,12 +105,15 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, config: int = 3):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` from the
+    committed ncu capture of this workload (profiles/traffic.json), else None."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
         d = json.loads(p.read_text())
-        if kernel in d:
-            return d[kernel]
+        key = kernel if config == 3 else f"config{config}:{kernel}"
+        if key in d:
+            return d[key]
     return None
 
 
@@ -221,6 +236,9 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     room, gt, intr, path = make_scene(args)
+    if args.config == 4:
+        from paper_2307_03404_b200 import synth
+        path = synth.room_path(10 * args.keyframes, room, seed=4)
     keyposes = path[::10][: args.keyframes]
     # keyframes rendered by the reference's own render_image (CPU, all threads)
     ref = orc.RefLib()
@@ -272,6 +290,9 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     room, gt, intr, path = make_scene(args)
+    if args.config == 4:
+        from paper_2307_03404_b200 import synth
+        path = synth.room_path(10 * args.keyframes, room, seed=4)
     keyposes = path[::10][: args.keyframes]
 
     # ground-truth map context: renders the keyframes, later tracks against them
@@ -281,7 +302,15 @@ def run_ours(args):
 
     ctx = Context(local, shard_multiple=world)
     ctx.set_stream(stream.cuda_stream)
-    ctx.init_grid(gt.geom, 0.1)
+    if args.config == 4:
+        # 513^3: refine the room map on the device, prune to the near-surface
+        # shell (voxel_grid.cpp:169-220), then restart the payload at sigma_init.
+        ctx.load_grid(gt)
+        ctx.upsample(1024)
+        ctx.prune(1e-3)
+        ctx.fill_grid(0.1)
+    else:
+        ctx.init_grid(gt.geom, 0.1)
     ctx.load_frames(intr, frames)
     ctx.rmsprop_reset()
     cfg = MappingConfig()
@@ -372,7 +401,7 @@ def run_ours(args):
     step_bytes = 1792.0 * S + 32.0 * args.rays * args.steps + 96.0 * prof["touched_groups"]
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": peak_kind,
+        "frac": achieved / peak, "traffic": ncu_traffic(dom, args.config), "peak_source": peak_kind,
         "launches": k_n, "kernel_ms": {k: v[0] for k, v in kern.items()},
         "step_algorithmic_GBps": step_bytes / (ms / 1e3) / 1e9,
         "step_frac": step_bytes / (ms / 1e3) / 1e9 / peak,
@@ -408,7 +437,11 @@ def run_ours(args):
 
     # ---- CPU baseline (rank 0, N=1)
     cpu = None
-    if not args.no_cpu and world == 1 and rank == 0:
+    if args.config == 4 and world == 1 and rank == 0:
+        cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "reference",
+               "sample": "n/a: the fp64 reference needs >= 30 GB grid + 30 GB RMSProp + "
+                         "30 GB per worker gradient buffer at 513^3 (SURVEY.md 8d)"}
+    elif not args.no_cpu and world == 1 and rank == 0:
         try:
             per_step, _ = cpu_samples_per_step(args, gt, intr, frames)
             r = cpu_reference(args, gt, intr, keyposes, frames, args.cpu_seconds)
@@ -428,10 +461,12 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "rays_per_step_per_gpu": args.rays,
-                       "grid_vertices": args.res ** 3, "keyframes": len(frames),
+            "config": {"workload": WORKLOAD4 if args.config == 4 else WORKLOAD,
+                       "rays_per_step_per_gpu": args.rays,
+                       "grid_vertices": ctx.geom.num_vertices, "keyframes": len(frames),
                        "frame": f"{args.width}x{args.height}", "parallelism": f"dp{world}",
-                       "l2": "inputs larger than L2 (grid 1.9 GB fp32)"},
+                       "l2": f"inputs larger than L2 (grid "
+                             f"{ctx.geom.num_vertices * 112 / 1e9:.1f} GB fp32)"},
             "rays_per_s": total_rays / (ms / 1e3),
             "samples_per_ray": total_samples / max(1, rays_hit),
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline,

@@ -186,6 +186,9 @@ int64_t vrf_profile_touched_groups(vrf_context* ctx);
 /* ---- grid: VoxelGrid (voxel_grid.hpp:112-175) */
 /* VoxelGrid(geom, sigma_init) — voxel_grid.cpp:74-81 (all cells active). */
 int vrf_grid_init(vrf_context* ctx, const vrf_grid_geometry* geom, double sigma_init);
+/* Reset the payload to VoxelGrid(geom, sigma_init)'s (voxel_grid.cpp:74-81) keeping the
+ * current occupancy; gradient and RMSProp state restart at zero. */
+int vrf_grid_fill(vrf_context* ctx, double sigma_init);
 /* Upload VoxelGrid::data() (double [V][28]) and occupancy() (uint8 per cell). */
 int vrf_grid_upload(vrf_context* ctx, const vrf_grid_geometry* geom, const double* payload,
                     const uint8_t* occupancy);

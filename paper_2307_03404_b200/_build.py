@@ -25,6 +25,8 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O2",
     "-Xptxas", "-v",
 ]
+# experiments only (e.g. -DVRF_QSTATS); part of the build digest
+NVCC_FLAGS += os.environ.get("VRF_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _nvcc() -> str:

@@ -431,6 +431,10 @@ class Context:
         self._check(self._lib.vrf_grid_init(self._h, C.byref(g), float(sigma_init)))
         self.geom = geom
 
+    def fill_grid(self, sigma_init: float):
+        """Payload := VoxelGrid(geom, sigma_init)'s, occupancy kept (vrf_grid_fill)."""
+        self._check(self._lib.vrf_grid_fill(self._h, float(sigma_init)))
+
     def load_grid(self, grid: VoxelGrid):
         data = np.ascontiguousarray(grid.data, dtype=np.float64)
         occ = np.ascontiguousarray(grid.active, dtype=np.uint8)

@@ -62,7 +62,8 @@ void vrf_context_destroy(vrf_context* ctx) {
                            &ctx->s_otmp, &ctx->s_batch, &ctx->s_raycd, &ctx->s_flags, &ctx->s_partials,
                            &ctx->s_count, &ctx->s_offsets, &ctx->s_keys, &ctx->s_keys2,
                            &ctx->s_ids, &ctx->s_ids2, &ctx->s_values, &ctx->s_grad64, &ctx->s_cub,
-                           &ctx->s_stage, &ctx->s_out, &ctx->s_batch2})
+                           &ctx->s_stage, &ctx->s_out, &ctx->s_batch2, &ctx->s_rec,
+                           &ctx->s_reccount})
     cudaFree(s->ptr);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   if (ctx->h_pipe) cudaFreeHost(ctx->h_pipe);
@@ -139,6 +140,21 @@ int vrf_grid_init(vrf_context* ctx, const vrf_grid_geometry* geom, double sigma_
   LAUNCHED(1);
   CU(cudaMemsetAsync(ctx->occ, 0xFF, sizeof(uint32_t) * ((ctx->C + 31) / 32 + 1), ctx->stream));
   update_blocks(ctx);
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+// VoxelGrid(geom, sigma_init) payload (voxel_grid.cpp:74-81) over the current
+// geometry, keeping the occupancy (e.g. a pruned shell); gradient and RMSProp
+// state restart at zero.
+int vrf_grid_fill(vrf_context* ctx, double sigma_init) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  launch_fill_payload(ctx->payload, ctx->V, (float)sigma_init, ctx->stream);
+  LAUNCHED(1);
+  CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
+  CU(cudaMemsetAsync(ctx->rms, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return VRF_OK;
 }

@@ -72,7 +72,9 @@ struct vrf_context {
 
   // grow-only scratch
   vrf_host::DeviceScratch s_batch, s_raycd, s_flags, s_partials, s_count, s_offsets, s_keys, s_keys2,
-      s_ids, s_ids2, s_values, s_grad64, s_cub, s_stage, s_out, s_batch2;
+      s_ids, s_ids2, s_values, s_grad64, s_cub, s_stage, s_out, s_batch2, s_rec, s_reccount;
+  // fast-path sample records of the last forward (0 = recompute-march backward)
+  int rec_K = 0;
 
   // multi-GPU phase state
   const int* last_batch = nullptr;
@@ -364,8 +366,31 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
     prof_end(ctx, kProfMapMisc, po);
     LAUNCHED(2);
     CU(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int) * 4, ctx->stream));
+    // Sample records for the reverse-order backward: up to K per ray within a
+    // memory budget (VRF_REC_GB, default 16 GB; 0 disables); longer rays overflow
+    // to the recompute-march backward.
+    ctx->rec_K = 0;
+    if (!warp) {
+      static const double budget_gb = [] {
+        const char* e = std::getenv("VRF_REC_GB");
+        return e ? std::atof(e) : 16.0;
+      }();
+      long long K = (long long)(budget_gb * 1e9) / ((long long)nn * (long long)sizeof(SampleRec));
+      K = std::min(K, 1024LL) & ~3LL;
+      if (K >= 16) {
+        if ((rc = ensure(ctx, ctx->s_rec, sizeof(SampleRec) * nn * (size_t)K))) return rc;
+        if ((rc = ensure(ctx, ctx->s_reccount, sizeof(int) * nn))) return rc;
+        ctx->rec_K = (int)K;
+      }
+    }
     cudaEvent_t pb = prof_begin(ctx);
-    if (warp)
+    if (ctx->rec_K > 0)
+      launch_map_forward_rec(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
+                             batch_dev, n, (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
+                             (MapPartial*)ctx->s_partials.ptr, ctx->d_err,
+                             (const uint32_t*)ctx->s_order.ptr, (SampleRec*)ctx->s_rec.ptr,
+                             ctx->rec_K, (int*)ctx->s_reccount.ptr, ctx->stream);
+    else if (warp)
       launch_map_forward_w(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
                            batch_dev, (const uint32_t*)ctx->s_order.ptr, n,
                            (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
@@ -379,6 +404,7 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
     prof_end(ctx, kProfMapForward, pb);
     LAUNCHED(1);
   } else if (n > 0) {
+    ctx->rec_K = 0;
     cudaEvent_t pb = prof_begin(ctx);
     launch_map_forward(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
                        batch_dev, n, (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,

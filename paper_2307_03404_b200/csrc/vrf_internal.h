@@ -33,7 +33,17 @@ struct PoseCount {
   long long samples;
 };
 
-enum FlagBits : uint8_t { kHit = 1, kDepthValid = 2 };
+enum FlagBits : uint8_t { kHit = 1, kDepthValid = 2, kOverflow = 4 };
+
+// Per-sample record of the fast mapping forward (24 B), consumed by the
+// reverse-order backward: weight w_i, T_{i+1}, clamped colour, and
+// kf = (segment index << 4) | clamp bits (0-2) | sigma_raw > 0 (bit 3).
+struct SampleRec {
+  float w, tn, c0, c1, c2;
+  uint32_t kf;
+};
+static_assert(sizeof(SampleRec) == 24, "SampleRec layout");
+constexpr uint32_t kRecSigmaPos = 8;
 
 // Launchers (vrf_kernels.cu). All take the context stream.
 void launch_render_image(const DevGrid& g, const DevParams& p, const DevCam& cam,
@@ -49,10 +59,26 @@ void launch_map_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                         const uint32_t* order, cudaStream_t s);
 int map_forward_blocks(int n);
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s);
+// Fast forward that also stores up to K SampleRec per ray, sample-major
+// (rec[c * n + slot], slot = coherent order index); rays with more samples get
+// kOverflow. rec_count[slot] = samples stored.
+void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                            const double4* rgbd, const DevPose* poses, int n_frames,
+                            const int* batch, int n, double4* ray_cd, uint8_t* flags,
+                            MapPartial* partials, int* err, const uint32_t* order, SampleRec* rec,
+                            int K, int* rec_count, cudaStream_t s);
+// Backward over the records (no payload gathers); kOverflow rays are
+// left to launch_map_backward(..., overflow_only = true).
+void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                             const double4* rgbd, const DevPose* poses, const int* batch, int n,
+                             const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
+                             const int* global_counts, float4* grad, double lambda_d,
+                             const uint32_t* order, const SampleRec* rec, int K,
+                             const int* rec_count, cudaStream_t s);
 void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                          const double4* rgbd, const DevPose* poses, const int* batch, int n,
                          const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
-                         const int* global_counts, float4* grad, double lambda_d, bool fast,
+                         const int* global_counts, float4* grad, double lambda_d, bool overflow_only,
                          const uint32_t* order, cudaStream_t s);
 void launch_map_backward_records(const DevGrid& g, const DevParams& p, const DevCam& cam,
                                  const double4* rgbd, const DevPose* poses, const int* batch,

@@ -13,6 +13,7 @@
 //   K5 k_pose_forward/     per-ray 4x6 Jacobian of [C; D] w.r.t. [omega; tau] ->
 //      k_pose_backward     J^T J (21) + J^T r (6) + loss      gradients.cpp:116-143,
 //                                                tracking.cpp:104-130
+#include <cstdio>
 #include <cstdlib>
 #include <climits>
 
@@ -171,6 +172,124 @@ __global__ void __launch_bounds__(kThreads) k_map_forward(
     }
     flags[i] = fl;
     if (ray_count) ray_count[i] = (fl & kHit) ? (int)samples : 0;
+  }
+  const double blp = block_sum(lp, s_d);
+  const double blg = block_sum(lg, s_d);
+  const long long bs = block_sum(samples, s_l);
+  const int bmc = block_sum(mc, s_i);
+  const int bmd = block_sum(md, s_i);
+  const int bbad = block_min(bad, s_i);
+  if (threadIdx.x == 0) {
+    MapPartial q;
+    q.lp = blp;
+    q.lg = blg;
+    q.samples = bs;
+    q.m_c = bmc;
+    q.m_d = bmd;
+    q.bad = bbad;
+    q.pad = 0;
+    partials[blockIdx.x] = q;
+  }
+}
+
+// Fast forward (fp32 SH) that records every composited sample for the
+// backward: identical march, sigma_raw replay, compositing and termination as
+// k_map_forward<float>; per sample it stores w_i, T_{i+1}, the clamped colour
+// and (segment index, clamp / sigma gates) — 24 B — so the backward never
+// gathers the 896 B of corner payload again. Records are sample-major
+// (rec[c * n + slot]): the lanes of a warp composite their c-th samples in the
+// same loop iteration, so each record store is one coalesced 768 B warp access.
+__global__ void __launch_bounds__(kThreads) k_map_forward_rec(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
+    double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
+    const uint32_t* __restrict__ order, SampleRec* __restrict__ rec, int K,
+    int* __restrict__ rec_count) {
+  __shared__ double s_d[32];
+  __shared__ long long s_l[32];
+  __shared__ int s_i[32];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (order && t < n) ? (int)order[t] : t;
+  double lp = 0.0, lg = 0.0;
+  long long samples = 0;
+  int mc = 0, md = 0, bad = INT_MAX;
+  if (t < n) {
+    const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
+    uint8_t fl = 0;
+    int stored = 0;
+    if (f < 0 || f >= n_frames || px < 0 || px >= cam.width || py < 0 || py >= cam.height) {
+      atomicOr(err, 2);  // generate_ray: pixel outside image
+    } else {
+      March m;
+      ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+      Composite st;
+      st.T = 1.0;
+      st.C[0] = st.C[1] = st.C[2] = 0.0;
+      st.D = 0.0;
+      st.count = 0;
+      st.terminated = false;
+      float bf[9];
+      bool basis_ok;
+      {
+        double basis[9];
+        basis_ok = sh_basis(m.d, basis);
+#pragma unroll
+        for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
+      }
+      if (!basis_ok) {
+        atomicOr(err, 1);
+      } else if (march_begin(g, p, m)) {
+        Sample s;
+        while (march_next(g, m, s)) {
+          Shade sh;
+          {
+            double w[8];
+            corner_weights(s, w);
+            shade_fast(g, s, w, bf, sh);
+          }
+          double decay;
+          const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
+          if (st.count <= K) {
+            const uint32_t kf = ((uint32_t)(m.k - 1) << 4) | (sh.clamped[0] ? 1u : 0u) |
+                                (sh.clamped[1] ? 2u : 0u) | (sh.clamped[2] ? 4u : 0u) |
+                                (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
+            float2* d = reinterpret_cast<float2*>(rec + (size_t)(st.count - 1) * n + t);
+            d[0] = make_float2((float)wgt, (float)st.T);
+            d[1] = make_float2((float)sh.c[0], (float)sh.c[1]);
+            d[2] = make_float2((float)sh.c[2], __uint_as_float(kf));
+          }
+          if (st.terminated) break;
+        }
+      }
+      if (st.count == 0) {
+        st.C[0] = st.C[1] = st.C[2] = 0.0;
+        st.D = 0.0;
+      }
+      const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+      if (st.count > 0) {
+        fl |= kHit;
+        if (st.count > K) fl |= kOverflow;
+        stored = st.count > K ? 0 : st.count;
+        mc = 1;
+        samples = st.count;
+        const double r0 = dsub(st.C[0], tg.x), r1 = dsub(st.C[1], tg.y), r2 = dsub(st.C[2], tg.z);
+        const double sq = dadd(dadd(dmul(r0, r0), dmul(r1, r1)), dmul(r2, r2));
+        if (!isfinite(sq) || !isfinite(st.D)) {
+          bad = i;
+        } else {
+          lp = sq;
+          if (tg.w > 0.0) {
+            fl |= kDepthValid;
+            md = 1;
+            const double dr = dsub(st.D, tg.w);
+            lg = dmul(dr, dr);
+          }
+        }
+      }
+      ray_cd[i] = make_double4(st.C[0], st.C[1], st.C[2], st.D);
+    }
+    flags[i] = fl;
+    rec_count[t] = stored;
   }
   const double blp = block_sum(lp, s_d);
   const double blg = block_sum(lg, s_d);
@@ -458,7 +577,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
     const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
     const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
     const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
-    float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order) {
+    float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
+    bool overflow_only) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int i = order ? (int)order[t] : t;  // coherent (keyframe, Morton tile) ray order
@@ -466,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
   if (st.bad != INT_MAX) return;  // non-finite loss: the reference throws before updating
   const uint8_t fl = flags[i];
   if (!(fl & kHit)) return;
+  if (overflow_only && !(fl & kOverflow)) return;  // recorded rays: k_map_backward_rec
   const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
   const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
   MapUp u;
@@ -473,6 +594,108 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
   March m;
   ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
   map_backward_fast<SKIP>(g, p, m, u, grad);
+}
+
+// Backward over the forward's SampleRec (fast path): no payload gathers.
+// Walking each ray's samples last to first turns the prefix form of
+// gradients.cpp:69-97 into a suffix form without cancellation,
+// -C + prefix_i = -sum_{j>i} c_j w_j:
+//   dL/dsigma_i = delta_i [sum_ch upc_ch (c_ch,i T_{i+1} - Sc_ch) + upd (t_i T_{i+1} - Sd)],
+// Sc / Sd the running suffix sums. Sample positions (t_i, delta_i, cell,
+// trilinear weights) are re-derived exactly from the stored segment index
+// (renderer.cpp:66-73: s0 = lo + k step). The reverse walk also staggers the
+// lanes of a warp along their rays, so neighbouring rays do not hit the same
+// vertices with atomics at the same time (forward order measured 10% slower, r01).
+// Measured alternative (r01): queueing departing corners per warp and draining
+// them with all lanes cut divergence but not time — the scatter is bound by L2
+// atomic throughput (~2 corner flushes per sample; 38% distinct within a warp's
+// 176-entry window), so fewer instructions do not help without merging.
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
+    const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
+    const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
+    float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
+    const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int i = order ? (int)order[t] : t;
+  const MapStats st = *stats;
+  if (st.bad != INT_MAX) return;  // non-finite loss: the reference throws before updating
+  const uint8_t fl = flags[i];
+  if (!(fl & kHit) || (fl & kOverflow)) return;
+  const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
+  const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+  MapUp u;
+  if (!map_upstream(st, global_counts, ray_cd[i], tg, fl, lambda_d, u)) return;
+  March m;
+  ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+  float bf[9];
+  {
+    double basis[9];
+    if (!sh_basis(m.d, basis)) return;
+#pragma unroll
+    for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
+  }
+  if (!march_begin(g, p, m)) return;
+  const double upc0 = u.upc[0], upc1 = u.upc[1], upc2 = u.upc[2];
+  const bool use_depth = u.use_depth;
+  const double upd = use_depth ? u.upd : 0.0;
+  double Sc0 = 0.0, Sc1 = 0.0, Sc2 = 0.0, Sd = 0.0;
+  float a[4][8];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
+  uint32_t cur = 0xffffffffu;
+  for (int c = rec_count[t] - 1; c >= 0; --c) {
+    const float2* q = reinterpret_cast<const float2*>(rec + (size_t)c * n + t);
+    const float2 q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
+    const uint32_t kf = __float_as_uint(q2.y);
+    const double kseg = (double)(kf >> 4);
+    const double s0 = dadd(m.lo, dmul(kseg, m.step));
+    const double s0s = dadd(s0, m.step);
+    const double s1 = (m.hi < s0s) ? m.hi : s0s;
+    const double delta = dsub(s1, s0);
+    const double tm = dmul(0.5, dadd(s0, s1));
+    const double pp[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
+                          dadd(m.o[2], dmul(tm, m.d[2]))};
+    Sample s;
+    locate(g, pp, s);
+    const double w = (double)q0.x, Tn = (double)q0.y;
+    const double c0 = (double)q1.x, c1 = (double)q1.y, c2 = (double)q2.x;
+    double ds = upc0 * (c0 * Tn - Sc0) + upc1 * (c1 * Tn - Sc1) + upc2 * (c2 * Tn - Sc2);
+    if (use_depth) ds += upd * (tm * Tn - Sd);
+    ds *= delta;
+    Sc0 += c0 * w;
+    Sc1 += c1 * w;
+    Sc2 += c2 * w;
+    Sd += tm * w;
+    if (s.base != cur) {
+      if (cur != 0xffffffffu) move_cell(grad, g, cur, s.base, a, bf);
+      cur = s.base;
+    }
+    const float wf = q0.x;
+    const float u0 = (kf & kRecSigmaPos) ? (float)ds : 0.f;
+    const float u1 = (kf & 1u) ? 0.f : (float)upc0 * wf;
+    const float u2 = (kf & 2u) ? 0.f : (float)upc1 * wf;
+    const float u3 = (kf & 4u) ? 0.f : (float)upc2 * wf;
+    const float fx = (float)s.fx, fy = (float)s.fy, fz = (float)s.fz;
+    const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
+      a[0][k] = fmaf(wk, u0, a[0][k]);
+      a[1][k] = fmaf(wk, u1, a[1][k]);
+      a[2][k] = fmaf(wk, u2, a[2][k]);
+      a[3][k] = fmaf(wk, u3, a[3][k]);
+    }
+  }
+  if (cur != 0xffffffffu) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) flush_corner(grad, g, cur, a, bf, k);
+  }
 }
 
 // ------------------------------------------------------------------ K3 deterministic records
@@ -961,18 +1184,51 @@ void launch_map_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                                                       ray_cd, flags, partials, ray_count, err,
                                                       order);
 }
+void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                            const double4* rgbd, const DevPose* poses, int n_frames,
+                            const int* batch, int n, double4* ray_cd, uint8_t* flags,
+                            MapPartial* partials, int* err, const uint32_t* order, SampleRec* rec,
+                            int K, int* rec_count, cudaStream_t s) {
+  k_map_forward_rec<<<map_forward_blocks(n), kThreads, 0, s>>>(g, p, cam, rgbd, poses, n_frames,
+                                                               batch, n, ray_cd, flags, partials,
+                                                               err, order, rec, K, rec_count);
+}
+void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                             const double4* rgbd, const DevPose* poses, const int* batch, int n,
+                             const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
+                             const int* global_counts, float4* grad, double lambda_d,
+                             const uint32_t* order, const SampleRec* rec, int K,
+                             const int* rec_count, cudaStream_t s) {
+  static const int minb = [] {
+    const char* e = std::getenv("VRF_REC_MINB");
+    return e ? std::atoi(e) : 3;
+  }();
+  const int blocks = (n + kThreads - 1) / kThreads;
+  if (minb == 3)
+    k_map_backward_rec<3><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
+                                                      flags, stats, global_counts, grad, lambda_d,
+                                                      order, rec, K, rec_count);
+  else if (minb == 2)
+    k_map_backward_rec<2><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
+                                                      flags, stats, global_counts, grad, lambda_d,
+                                                      order, rec, K, rec_count);
+  else
+    k_map_backward_rec<4><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
+                                                      flags, stats, global_counts, grad, lambda_d,
+                                                      order, rec, K, rec_count);
+
+}
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s) {
   k_map_reduce<<<1, 1024, 0, s>>>(partials, nparts, out);
 }
 void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                          const double4* rgbd, const DevPose* poses, const int* batch, int n,
                          const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
-                         const int* global_counts, float4* grad, double lambda_d, bool fast,
-                         const uint32_t* order, cudaStream_t s) {
+                         const int* global_counts, float4* grad, double lambda_d,
+                         bool overflow_only, const uint32_t* order, cudaStream_t s) {
   // 4 CTAs x 128 threads per SM: 128 registers (measured best of 2/3/4, r01);
   // VRF_BWD_MINB=3 selects the 168-register build for A/B runs.
   // The empty-block jump is compiled in only when the grid has empty blocks.
-  (void)fast;
   static const int minb = [] {
     const char* e = std::getenv("VRF_BWD_MINB");
     return (e && std::atoi(e) == 3) ? 3 : 4;
@@ -981,7 +1237,7 @@ void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam
 #define VRF_BWD_LAUNCH(MB, SK)                                                                 \
   k_map_backward<MB, SK><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd, \
                                                      flags, stats, global_counts, grad,        \
-                                                     lambda_d, order)
+                                                     lambda_d, order, overflow_only)
   if (minb == 3) {
     if (g.all_blocks_active)
       VRF_BWD_LAUNCH(3, false);

@@ -152,12 +152,24 @@ void launch_backward_fast(vrf_context* ctx, const vrf_mapping_config* cfg, const
                           (const double4*)ctx->s_raycd.ptr, (const uint8_t*)ctx->s_flags.ptr,
                           ctx->d_stats, global_counts, ctx->grad, cfg->lambda_d,
                           ctx->d_queue + 1, ctx->stream);
-  else
+  else {
+    if (ctx->rec_K > 0) {
+      launch_map_backward_rec(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
+                              batch_dev, n, (const double4*)ctx->s_raycd.ptr,
+                              (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, global_counts,
+                              (float4*)ctx->grad, cfg->lambda_d,
+                              (const uint32_t*)ctx->s_order.ptr,
+                              (const SampleRec*)ctx->s_rec.ptr, ctx->rec_K,
+                              (const int*)ctx->s_reccount.ptr, ctx->stream);
+      LAUNCHED(1);
+    }
+    // without records: every ray; with records: only the rays that overflowed K
     launch_map_backward(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
                         batch_dev, n, (const double4*)ctx->s_raycd.ptr,
                         (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, global_counts,
-                        (float4*)ctx->grad, cfg->lambda_d, /*fast=*/true,
+                        (float4*)ctx->grad, cfg->lambda_d, /*overflow_only=*/ctx->rec_K > 0,
                         (const uint32_t*)ctx->s_order.ptr, ctx->stream);
+  }
   prof_end(ctx, kProfMapBackward, pb);
   LAUNCHED(1);
 }
