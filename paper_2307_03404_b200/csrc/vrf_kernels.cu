@@ -649,9 +649,24 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
   uint32_t cur = 0xffffffffu;
-  for (int c = rec_count[t] - 1; c >= 0; --c) {
+  // records are prefetched one iteration ahead: the dependent load of the next
+  // (uncoalesced, mostly L2/DRAM) record overlaps this sample's math and scatter
+  int c = rec_count[t] - 1;
+  float2 n0 = make_float2(0.f, 0.f), n1 = n0, n2 = n0;
+  if (c >= 0) {
     const float2* q = reinterpret_cast<const float2*>(rec + (size_t)c * n + t);
-    const float2 q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
+    n0 = __ldg(q);
+    n1 = __ldg(q + 1);
+    n2 = __ldg(q + 2);
+  }
+  for (; c >= 0; --c) {
+    const float2 q0 = n0, q1 = n1, q2 = n2;
+    if (c > 0) {
+      const float2* q = reinterpret_cast<const float2*>(rec + (size_t)(c - 1) * n + t);
+      n0 = __ldg(q);
+      n1 = __ldg(q + 1);
+      n2 = __ldg(q + 2);
+    }
     const uint32_t kf = __float_as_uint(q2.y);
     const double kseg = (double)(kf >> 4);
     const double s0 = dadd(m.lo, dmul(kseg, m.step));
