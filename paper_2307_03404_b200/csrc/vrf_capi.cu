@@ -23,7 +23,6 @@ int vrf_context_create(int device, vrf_context** out) {
       cudaMalloc(&ctx->d_err, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&ctx->d_stats, sizeof(MapStats)) != cudaSuccess ||
       cudaMalloc(&ctx->d_counts, sizeof(int) * 2) != cudaSuccess ||
-      cudaMalloc(&ctx->d_pcount, sizeof(PoseCount)) != cudaSuccess ||
       cudaMalloc(&ctx->d_pose_out, sizeof(PosePartial)) != cudaSuccess ||
       cudaMalloc(&ctx->d_pose, sizeof(DevPose)) != cudaSuccess) {
     delete ctx;
@@ -46,7 +45,6 @@ void vrf_context_destroy(vrf_context* ctx) {
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_stats);
   cudaFree(ctx->d_counts);
-  cudaFree(ctx->d_pcount);
   cudaFree(ctx->d_pose_out);
   cudaFree(ctx->d_pose);
   cudaFree(ctx->d_touched);

@@ -24,7 +24,6 @@ struct DeviceScratch {
 
 using vrf::DevPose;
 using vrf::MapStats;
-using vrf::PoseCount;
 using vrf::PosePartial;
 
 struct vrf_context {
@@ -60,7 +59,6 @@ struct vrf_context {
   int* d_err = nullptr;
   MapStats* d_stats = nullptr;
   int* d_counts = nullptr;
-  PoseCount* d_pcount = nullptr;
   PosePartial* d_pose_out = nullptr;
   DevPose* d_pose = nullptr;
   // pinned host staging

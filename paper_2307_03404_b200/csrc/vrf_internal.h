@@ -27,12 +27,6 @@ struct PosePartial {
   int bad;
 };
 
-struct PoseCount {
-  int m;
-  int pad;
-  long long samples;
-};
-
 enum FlagBits : uint8_t { kHit = 1, kDepthValid = 2, kOverflow = 4 };
 
 // Per-sample record of the fast mapping forward (24 B), consumed by the
@@ -93,19 +87,6 @@ void launch_segmented_reduce(const uint32_t* sorted_keys, const uint32_t* perm,
 void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, long long v_end,
                     double rho, double lr_sigma, double lr_sh, double eps,
                     const MapStats* stats, unsigned long long* touched, cudaStream_t s);
-void launch_pose_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
-                         const double4* rgbd, const DevPose* pose, const int* pixels, int n,
-                         double4* ray_cd, uint8_t* flags, PoseCount* counts, int* err_flag,
-                         const uint32_t* order, cudaStream_t s);
-void launch_pose_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
-                          const double4* rgbd, const DevPose* pose, const int* pixels, int n,
-                          const double4* ray_cd, const uint8_t* flags, double lambda_p,
-                          double lambda_d, PosePartial* partials, const uint32_t* order,
-                          cudaStream_t s);
-int pose_backward_blocks(int n);
-void launch_pose_reduce(const PosePartial* partials, int nparts, PosePartial* out,
-                        cudaStream_t s);
-
 // Tracking (vrf_track.cu).
 int pose_fused_blocks(int n);
 void launch_pose_fused(bool fp64_sh, const DevGrid& g, const DevParams& p, const DevCam& cam,

@@ -1,18 +1,19 @@
 // sm_100a kernels of the per-ray hot path.
 //
 //   K1 k_render_image      render_image          renderer.cpp:149-174 (+51-140)
-//   K0+fwd k_map_forward   mapping_step pass 1+2 forward, hit counts M_c/M_d,
-//                          loss partials        mapping.cpp:130-200
-//   K2 k_map_backward      recompute-march + prefix-form dL/dsigma, dL/dc +
-//                          trilinear adjoint scatter (red.global.add.v4.f32)
-//                                                gradients.cpp:69-114, mapping.cpp:172-195
+//   K0+fwd k_map_forward_rec  mapping_step forward (hit counts M_c/M_d, loss
+//                          partials) + 24 B per-sample records  mapping.cpp:130-200
+//   K2 k_map_backward_rec  reverse walk over the records: suffix-form dL/dsigma,
+//                          dL/dc + aggregated trilinear adjoint scatter
+//                          (red.global.add.v4.f32)   gradients.cpp:69-114, mapping.cpp:172-195
+//      k_map_backward      recompute-march variant (rays longer than the record cap)
+//      k_map_forward       forward without records (deterministic mode, >cap budgets)
 //   K3 k_map_records +     deterministic mode: per-sample fp64 records, stable
 //      k_segmented_reduce  radix sort by vertex, in-order fp64 segment sums
 //                                                gradients.cpp:28-57 (sorted merge)
 //   K4 k_rmsprop           sparse RMSProp (skip g == 0), clears g   mapping.cpp:218-231
-//   K5 k_pose_forward/     per-ray 4x6 Jacobian of [C; D] w.r.t. [omega; tau] ->
-//      k_pose_backward     J^T J (21) + J^T r (6) + loss      gradients.cpp:116-143,
-//                                                tracking.cpp:104-130
+//   K5 (vrf_track.cu)      fused pose forward + Jacobian -> J^T J, J^T r
+//   utilities              prune, upsample, block occupancy, pack / convert
 #include <cstdio>
 #include <cstdlib>
 #include <climits>
@@ -824,199 +825,6 @@ __global__ void __launch_bounds__(256) k_rmsprop(float4* __restrict__ theta,
   }
 }
 
-// ------------------------------------------------------------------ K5 pose
-__global__ void __launch_bounds__(kThreads) k_pose_forward(
-    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
-    const DevPose* __restrict__ pose, const int* __restrict__ pixels, int n,
-    double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, PoseCount* counts, int* err,
-    const uint32_t* __restrict__ order) {
-  __shared__ long long s_l[32];
-  __shared__ int s_i[32];
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = (order && t < n) ? (int)order[t] : t;  // coherent pixel order
-  int hit = 0;
-  long long samples = 0;
-  if (t < n) {
-    const int px = pixels[2 * i], py = pixels[2 * i + 1];
-    uint8_t fl = 0;
-    if (px < 0 || px >= cam.width || py < 0 || py >= cam.height) {
-      atomicOr(err, 2);
-    } else {
-      March m;
-      ray_from_pixel(cam, *pose, (double)px, (double)py, m);
-      Composite st;
-      double basis[9];
-      if (!render_forward<double>(g, p, m, st, basis)) atomicOr(err, 1);
-      if (st.count > 0) {
-        fl = kHit;
-        hit = 1;
-        samples = st.count;
-      }
-      ray_cd[i] = make_double4(st.C[0], st.C[1], st.C[2], st.D);
-    }
-    flags[i] = fl;
-  }
-  const int bh = block_sum(hit, s_i);
-  const long long bs = block_sum(samples, s_l);
-  if (threadIdx.x == 0) {
-    atomicAdd(&counts->m, bh);
-    atomicAdd((unsigned long long*)&counts->samples, (unsigned long long)bs);
-  }
-}
-
-// Per ray: 4 residual rows (r, g, b, depth), each a 6-vector [omega; tau], from
-// grad_wrt_ray with unit upstreams; spatial gradients contracted per corner.
-__global__ void __launch_bounds__(kThreads) k_pose_backward(
-    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
-    const DevPose* __restrict__ pose, const int* __restrict__ pixels, int n,
-    const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags, double lambda_p,
-    double lambda_d, PosePartial* partials, const uint32_t* __restrict__ order) {
-  __shared__ double s_d[32];
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = (order && t < n) ? (int)order[t] : t;  // coherent pixel order
-  double jtj[21], jtr[6], loss = 0.0;
-#pragma unroll
-  for (int k = 0; k < 21; ++k) jtj[k] = 0.0;
-#pragma unroll
-  for (int k = 0; k < 6; ++k) jtr[k] = 0.0;
-  if (t < n && (flags[i] & kHit)) {
-    const int px = pixels[2 * i], py = pixels[2 * i + 1];
-    const double4 tg = rgbd[(long long)py * cam.width + px];
-    const double4 cd = ray_cd[i];
-    const double C[3] = {cd.x, cd.y, cd.z}, D = cd.w;
-    const double res[4] = {dsub(C[0], tg.x), dsub(C[1], tg.y), dsub(C[2], tg.z), dsub(D, tg.w)};
-    loss = dadd(dmul(lambda_p, dadd(dadd(dmul(res[0], res[0]), dmul(res[1], res[1])),
-                                    dmul(res[2], res[2]))),
-                dmul(dmul(lambda_d, res[3]), res[3]));
-    March m;
-    ray_from_pixel(cam, *pose, (double)px, (double)py, m);
-    double basis[9];
-    double Jo[4][3], Jd[4][3];
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = 0.0;
-    if (sh_basis(m.d, basis) && march_begin(g, p, m)) {
-      double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
-      const double sgn[2] = {-1.0, 1.0};
-      Sample s;
-      while (march_next(g, m, s)) {
-        double w[8];
-        corner_weights(s, w);
-        Shade sh;
-        shade<double>(g, s, w, basis, sh);
-        const double sigma = (sh.sigma_raw < 0.0) ? 0.0 : sh.sigma_raw;
-        const double decay = exp(dmul(-sigma, s.delta));
-        const double wgt = dmul(T, dsub(1.0, decay));
-        const double T_next = dmul(T, decay);
-        double dsig[4];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          prefix[ch] = dadd(prefix[ch], dmul(sh.c[ch], wgt));
-          dsig[ch] = dmul(s.delta, dadd(dsub(dmul(sh.c[ch], T_next), C[ch]), prefix[ch]));
-        }
-        prefix_d = dadd(prefix_d, dmul(s.t, wgt));
-        dsig[3] = dmul(s.delta, dadd(dsub(dmul(s.t, T_next), D), prefix_d));
-        // Spatial gradients of sigma and of the three basis-contracted SH channels
-        // (voxel_grid.cpp:130-151), 8 corners.
-        const double wx[2] = {dsub(1.0, s.fx), s.fx}, wy[2] = {dsub(1.0, s.fy), s.fy},
-                     wz[2] = {dsub(1.0, s.fz), s.fz};
-        double Gs[3] = {0, 0, 0}, Gc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-#pragma unroll 1
-        for (int k = 0; k < 8; ++k) {
-          const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
-          const double dw[3] = {dmul(dmul(dmul(sgn[dx], wy[dy]), wz[dz]), g.inv_voxel),
-                                dmul(dmul(dmul(wx[dx], sgn[dy]), wz[dz]), g.inv_voxel),
-                                dmul(dmul(dmul(wx[dx], wy[dy]), sgn[dz]), g.inv_voxel)};
-          const float* vp = (const float*)(g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex);
-          const double v0 = (double)__ldg(vp);
-          double shd[3];
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            double acc = 0.0;
-#pragma unroll
-            for (int mm = 0; mm < 9; ++mm) acc = fma(basis[mm], (double)__ldg(vp + 1 + ch * 9 + mm), acc);
-            shd[ch] = acc;
-          }
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            Gs[a] = fma(dw[a], v0, Gs[a]);
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) Gc[ch][a] = fma(dw[a], shd[ch], Gc[ch][a]);
-          }
-        }
-        const bool sgate = sh.sigma_raw > 0.0;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            double gv = sgate ? dsig[r] * Gs[a] : 0.0;
-            if (r < 3 && !sh.clamped[r]) gv += wgt * Gc[r][a];
-            Jo[r][a] += gv;
-            Jd[r][a] = fma(s.t, gv, Jd[r][a]);
-          }
-        }
-        T = T_next;
-        if (T < p.eps) break;
-      }
-    }
-    // Chart (tracking.cpp:125-128): tau <- dL/do, omega <- d x (dL/dd - d (d.dL/dd)).
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const double dd = dot3(m.d, Jd[r]);
-      double gp[3], om[3];
-      for (int a = 0; a < 3; ++a) gp[a] = Jd[r][a] - m.d[a] * dd;
-      cross3(m.d, gp, om);
-      const double J[6] = {om[0], om[1], om[2], Jo[r][0], Jo[r][1], Jo[r][2]};
-      const double lam = r < 3 ? lambda_p : lambda_d;
-      int idx = 0;
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-#pragma unroll
-        for (int b = a; b < 6; ++b) jtj[idx++] += lam * J[a] * J[b];
-        jtr[a] += lam * J[a] * res[r];
-      }
-    }
-  }
-  // Block reduction (fixed order) -> per-block partial.
-  PosePartial* out = partials + blockIdx.x;
-#pragma unroll 1
-  for (int k = 0; k < 21; ++k) {
-    const double v = block_sum(jtj[k], s_d);
-    if (threadIdx.x == 0) out->jtj[k] = v;
-  }
-#pragma unroll 1
-  for (int k = 0; k < 6; ++k) {
-    const double v = block_sum(jtr[k], s_d);
-    if (threadIdx.x == 0) out->jtr[k] = v;
-  }
-  const double bl = block_sum(loss, s_d);
-  if (threadIdx.x == 0) {
-    out->loss = bl;
-    out->samples = 0;
-    out->m = 0;
-    out->bad = 0;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_pose_reduce(const PosePartial* __restrict__ parts,
-                                                     int nparts, PosePartial* out) {
-  // 28 values; thread v sums value v over the partials in order (deterministic).
-  const int v = threadIdx.x;
-  if (v >= 28) return;
-  double acc = 0.0;
-  for (int k = 0; k < nparts; ++k) {
-    const PosePartial& q = parts[k];
-    acc += v < 21 ? q.jtj[v] : (v < 27 ? q.jtr[v - 21] : q.loss);
-  }
-  if (v < 21)
-    out->jtj[v] = acc;
-  else if (v < 27)
-    out->jtr[v - 21] = acc;
-  else
-    out->loss = acc;
-}
-
 // ------------------------------------------------------------------ utilities
 __global__ void k_fill_payload(float* payload, long long nv, float sigma) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nv * kPayload;
@@ -1291,26 +1099,6 @@ void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, l
   if (f1 <= f0) return;
   k_rmsprop<<<grid_blocks(f1 - f0, 256), 256, 0, s>>>(theta, grad, v, f0, f1, rho, lr_sigma,
                                                       lr_sh, eps, stats, touched);
-}
-void launch_pose_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
-                         const double4* rgbd, const DevPose* pose, const int* pixels, int n,
-                         double4* ray_cd, uint8_t* flags, PoseCount* counts, int* err,
-                         const uint32_t* order, cudaStream_t s) {
-  k_pose_forward<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
-      g, p, cam, rgbd, pose, pixels, n, ray_cd, flags, counts, err, order);
-}
-int pose_backward_blocks(int n) { return (n + kThreads - 1) / kThreads; }
-void launch_pose_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
-                          const double4* rgbd, const DevPose* pose, const int* pixels, int n,
-                          const double4* ray_cd, const uint8_t* flags, double lambda_p,
-                          double lambda_d, PosePartial* partials, const uint32_t* order,
-                          cudaStream_t s) {
-  k_pose_backward<<<pose_backward_blocks(n), kThreads, 0, s>>>(
-      g, p, cam, rgbd, pose, pixels, n, ray_cd, flags, lambda_p, lambda_d, partials, order);
-}
-void launch_pose_reduce(const PosePartial* partials, int nparts, PosePartial* out,
-                        cudaStream_t s) {
-  k_pose_reduce<<<1, 32, 0, s>>>(partials, nparts, out);
 }
 void launch_fill_payload(float* payload, long long nv, float sigma, cudaStream_t s) {
   k_fill_payload<<<grid_blocks(nv * kPayload, 256), 256, 0, s>>>(payload, nv, sigma);
