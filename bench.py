@@ -391,9 +391,12 @@ def run_ours(args):
     S = total_samples / world if world > 1 else total_samples
     kern = {k: prof[k] for k in ("map_forward", "map_backward", "rmsprop")}
     dom = max(kern, key=lambda k: kern[k][0])
+    # 896 B/sample gather (forward), +896 B/sample scatter
+    # (backward: the records path never re-gathers), 32 B/ray I/O, 96 B per
+    # updated float4 group (RMSProp).
     bytes_per = {
         "map_forward": 896.0 * S + 32.0 * (args.rays * args.steps),
-        "map_backward": 1792.0 * S,
+        "map_backward": 896.0 * S,
         "rmsprop": 96.0 * prof["touched_groups"],
     }
     k_ms, k_n = kern[dom]

@@ -190,11 +190,13 @@ class Oracle:
                                       C.byref(r)), "render_ray")
         return r
 
-    def upsample(self, grid, max_resolution):
-        """VoxelGrid::upsampled (voxel_grid.cpp:190-220) -> (geometry, data, active)."""
+    def upsample(self, grid, max_resolution, clamp_outside=False):
+        """VoxelGrid::upsampled (voxel_grid.cpp:190-220) -> (geometry, data, active).
+        clamp_outside: clamp far-corner vertices the reference would throw on."""
         h = _GridHold(grid)
         f = Geometry()
-        rc = self.lib.or_upsample(C.byref(h.s), int(max_resolution), C.byref(f), None, None)
+        cl = 1 if clamp_outside else 0
+        rc = self.lib.or_upsample(C.byref(h.s), int(max_resolution), cl, C.byref(f), None, None)
         if rc == 3:
             raise OracleError("upsample: resolution would exceed configured maximum")
         res = tuple(f.res)
@@ -202,8 +204,9 @@ class Oracle:
         nc = (res[0] - 1) * (res[1] - 1) * (res[2] - 1)
         data = np.zeros((nv, 28))
         act = np.zeros(nc, np.uint8)
-        _check(self.lib.or_upsample(C.byref(h.s), int(max_resolution), C.byref(f), _ptr(data),
-                                    _ptr(act)), "upsample")
+        _check(self.lib.or_upsample(C.byref(h.s), int(max_resolution), cl, C.byref(f),
+                                    _ptr(data), _ptr(act)),
+               "upsample: voxel grid: point outside grid")
         return (res, tuple(f.origin), f.voxel_size), data, act
 
     def render_image(self, grid, intr, pose, params, stride=1):
@@ -299,6 +302,17 @@ def track_cfg(c) -> TrackCfg:
                     c.divergence_patience, c.max_redraws, c.seed & (2**64 - 1), params_s(c.render))
 
 
+class MapSceneCfg(C.Structure):
+    _fields_ = [("keyframe_stride", C.c_int32), ("rays_per_batch", C.c_int32),
+                ("iterations_per_stage", C.c_int32), ("initial_resolution", C.c_int32),
+                ("upsample_stages", C.c_int32), ("max_resolution", C.c_int32),
+                ("prune_every", C.c_int32), ("threads", C.c_int32), ("deterministic", C.c_int32),
+                ("pad", C.c_int32), ("lambda_d", C.c_double), ("lr_sigma", C.c_double),
+                ("lr_sh", C.c_double), ("rmsprop_decay", C.c_double), ("rmsprop_eps", C.c_double),
+                ("prune_threshold", C.c_double), ("sigma_init", C.c_double),
+                ("bounds_margin", C.c_double), ("seed", C.c_uint64), ("render", Params)]
+
+
 class RefLib:
     """The reference's own functions (oracle/_ref/libvoxrf_ref.so)."""
 
@@ -363,6 +377,38 @@ class RefLib:
                                                  int(initial_resolution), float(bounds_margin),
                                                  C.byref(g)), "fit_grid_geometry")
         return tuple(g.res), tuple(g.origin), g.voxel_size
+
+    def map_scene(self, frames_h, intr, cfg, geometry=None, threads=0):
+        """The reference's map_scene (mapping.cpp:278-316) -> (grid handle, final loss, ms)."""
+        c = MapSceneCfg(cfg.keyframe_stride, cfg.rays_per_batch, cfg.iterations_per_stage,
+                        cfg.initial_resolution, cfg.upsample_stages, cfg.max_resolution,
+                        cfg.prune_every, threads, 1 if cfg.deterministic else 0, 0, cfg.lambda_d,
+                        cfg.lr_sigma, cfg.lr_sh, cfg.rmsprop_decay, cfg.rmsprop_eps,
+                        cfg.prune_threshold, cfg.sigma_init, cfg.bounds_margin,
+                        cfg.seed & (2**64 - 1), params_s(cfg.render))
+        loss, ms = C.c_double(), C.c_double()
+        self.lib.ref_map_scene.restype = C.c_void_p
+        self.lib.ref_map_scene.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p]
+        g = None if geometry is None else globals()["geometry"](geometry)
+        h = self.lib.ref_map_scene(frames_h, C.byref(intr_s(intr)), C.byref(c),
+                                   None if g is None else C.byref(g), C.byref(loss), C.byref(ms))
+        if not h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return h, loss.value, ms.value
+
+    def track_sequence(self, grid_h, frames_h, intr, tcfg, n_frames, threads=0,
+                       constant_velocity=False):
+        """The reference's track_sequence (tracking.cpp:254-295) -> (poses [(q, t)], ms)."""
+        out = (PoseS * n_frames)()
+        ms = C.c_double()
+        self.lib.ref_track_sequence.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        self._err(self.lib.ref_track_sequence(grid_h, frames_h, C.byref(intr_s(intr)),
+                                              C.byref(track_cfg(tcfg)), threads,
+                                              1 if constant_velocity else 0, out, C.byref(ms)),
+                  "track_sequence")
+        return [(tuple(p.q), tuple(p.t)) for p in out], ms.value
 
     def read_occupancy(self, handle, ncells):
         out = np.zeros(ncells, np.uint8)

@@ -6,6 +6,8 @@
 // pin oracle/voxrf_oracle.c against the reference itself and to generate the
 // golden fixtures, and (b) by bench.py as the CPU baseline / `--impl reference`
 // arm ("kind": "reference"). Never linked into the product library.
+#include <chrono>
+#include <optional>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -446,6 +448,80 @@ int ref_track_frame(const void* grid, const void* frames, const or_intrinsics* i
     out->final_loss = r.loss_trace.empty() ? 0.0 : r.loss_trace.back();
     if (loss_trace)
       for (std::size_t i = 0; i < r.loss_trace.size(); ++i) loss_trace[i] = r.loss_trace[i];
+  });
+}
+
+// ---- map_scene (mapping.cpp:278-316) / track_sequence (tracking.cpp:254-295) over
+// every frame of a handle (frames carry their gt poses); wall time via steady_clock.
+struct or_map_scene_cfg {
+  int32_t keyframe_stride, rays_per_batch, iterations_per_stage, initial_resolution;
+  int32_t upsample_stages, max_resolution, prune_every, threads, deterministic, pad;
+  double lambda_d, lr_sigma, lr_sh, rmsprop_decay, rmsprop_eps, prune_threshold, sigma_init,
+      bounds_margin;
+  uint64_t seed;
+  or_render_params render;
+};
+void* ref_map_scene(const void* frames, const or_intrinsics* intr, const or_map_scene_cfg* c,
+                    const or_geometry* geom, double* final_loss, double* ms) {
+  try {
+    Dataset ds;
+    ds.intrinsics = to_intr(*intr);
+    ds.frames = static_cast<const RefFrames*>(frames)->frames;
+    MappingConfig m;
+    m.keyframe_stride = c->keyframe_stride;
+    m.rays_per_batch = c->rays_per_batch;
+    m.iterations_per_stage = c->iterations_per_stage;
+    m.initial_resolution = c->initial_resolution;
+    m.upsample_stages = c->upsample_stages;
+    m.max_resolution = c->max_resolution;
+    m.prune_every = c->prune_every;
+    m.threads = c->threads;
+    m.deterministic = c->deterministic != 0;
+    m.lambda_d = c->lambda_d;
+    m.lr_sigma = c->lr_sigma;
+    m.lr_sh = c->lr_sh;
+    m.rmsprop_decay = c->rmsprop_decay;
+    m.rmsprop_eps = c->rmsprop_eps;
+    m.prune_threshold = c->prune_threshold;
+    m.sigma_init = c->sigma_init;
+    m.bounds_margin = c->bounds_margin;
+    m.seed = c->seed;
+    m.render = to_params(c->render);
+    std::optional<GridGeometry> g;
+    if (geom) {
+      GridGeometry gg;
+      for (int a = 0; a < 3; ++a) {
+        gg.res[a] = geom->res[a];
+        gg.origin[a] = geom->origin[a];
+      }
+      gg.voxel_size = geom->voxel_size;
+      g = gg;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    MapResult r = map_scene(ds, m, g);
+    *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    *final_loss = r.log.empty() ? 0.0 : r.log.back().stats.loss_total;
+    return new VoxelGrid(std::move(r.grid));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+int ref_track_sequence(const void* grid, const void* frames, const or_intrinsics* intr,
+                       const or_tracking_config* cfg, int threads, int constant_velocity,
+                       or_pose* poses_out, double* ms) {
+  REF_GUARD({
+    Dataset ds;
+    ds.intrinsics = to_intr(*intr);
+    ds.frames = static_cast<const RefFrames*>(frames)->frames;
+    TrackingConfig t = to_tracking(cfg, threads);
+    t.init_policy = constant_velocity ? TrackingConfig::Init::kConstantVelocity
+                                      : TrackingConfig::Init::kPreviousPose;
+    const auto t0 = std::chrono::steady_clock::now();
+    const TrackSequenceResult r = track_sequence(*static_cast<const VoxelGrid*>(grid), ds, t);
+    *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    for (std::size_t i = 0; i < r.trajectory.poses.size(); ++i)
+      poses_out[i] = from_pose(r.trajectory.poses[i]);
   });
 }
 

@@ -189,6 +189,32 @@ static int try_locate(const or_geometry* g, const double p[3], locator* out) {
   return 1;
 }
 
+/* try_locate with the grid coordinate clamped into [0, res-1] instead of
+ * rejecting (used only by or_upsample's clamp_outside mode). */
+static void locate_clamped(const or_geometry* g, const double p[3], locator* out) {
+  double gc[3];
+  for (int a = 0; a < 3; ++a) {
+    gc[a] = (p[a] - g->origin[a]) / g->voxel_size;
+    if (!(gc[a] >= 0.0)) gc[a] = 0.0;
+    if (gc[a] > g->res[a] - 1.0) gc[a] = g->res[a] - 1.0;
+  }
+  for (int a = 0; a < 3; ++a) {
+    int c = (int)ceil(gc[a]) - 1;
+    if (c < 0) c = 0;
+    if (c > g->res[a] - 2) c = g->res[a] - 2;
+    out->cell[a] = c;
+    out->frac[a] = gc[a] - c;
+  }
+  const double wx[2] = {1.0 - out->frac[0], out->frac[0]};
+  const double wy[2] = {1.0 - out->frac[1], out->frac[1]};
+  const double wz[2] = {1.0 - out->frac[2], out->frac[2]};
+  for (int k = 0; k < 8; ++k) {
+    const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+    out->corner[k] = vertex_index(g, out->cell[0] + dx, out->cell[1] + dy, out->cell[2] + dz);
+    out->weight[k] = wx[dx] * wy[dy] * wz[dz];
+  }
+}
+
 /* voxel_grid.cpp:113-122 */
 static void trilerp(const or_grid* g, const locator* loc, double* sigma_raw, double sh[27]) {
   double s = 0.0;
@@ -205,8 +231,8 @@ static void trilerp(const or_grid* g, const locator* loc, double* sigma_raw, dou
 /* VoxelGrid::upsampled — voxel_grid.cpp:190-220. `out` holds the refined
  * geometry (2 res - 1, voxel / 2) and (2rx-1)(2ry-1)(2rz-1)*28 doubles;
  * active_out its cell mask. Returns OR_RUNTIME over max_resolution. */
-int or_upsample(const or_grid* g, int max_resolution, or_geometry* fine, double* out,
-                uint8_t* active_out) {
+int or_upsample(const or_grid* g, int max_resolution, int clamp_outside, or_geometry* fine,
+                double* out, uint8_t* active_out) {
   or_geometry f = g->geom;
   for (int a = 0; a < 3; ++a) f.res[a] = 2 * g->geom.res[a] - 1;
   f.voxel_size = g->geom.voxel_size * 0.5;
@@ -221,7 +247,14 @@ int or_upsample(const or_grid* g, int max_resolution, or_geometry* fine, double*
         double p[3];
         for (int a = 0; a < 3; ++a) p[a] = g->geom.origin[a] + gg[a] * g->geom.voxel_size;
         locator loc;
-        if (!try_locate(&g->geom, p, &loc)) return OR_OUT_OF_RANGE;
+        if (!try_locate(&g->geom, p, &loc)) {
+          /* The reference throws here (locate, voxel_grid.cpp:107-111) when the
+           * world round trip of a far-corner vertex lands an ulp outside the
+           * box. clamp_outside != 0 instead clamps the grid coordinate into
+           * [0, res-1] (the device behaviour: the boundary vertex's value). */
+          if (!clamp_outside) return OR_OUT_OF_RANGE;
+          locate_clamped(&g->geom, p, &loc);
+        }
         double* v = out + (size_t)vertex_index(&f, ix, iy, iz) * PAYLOAD;
         trilerp(g, &loc, &v[0], &v[1]);
       }

@@ -172,8 +172,8 @@ void or_apply_perturbation(const double omega[3], const double tau[3], const or_
 /* voxel_grid.cpp:34-47 */
 int or_sh_eval(const double d[3], double basis[9]);
 
-int or_upsample(const or_grid* g, int max_resolution, or_geometry* fine, double* out,
-                uint8_t* active_out);
+int or_upsample(const or_grid* g, int max_resolution, int clamp_outside, or_geometry* fine,
+                double* out, uint8_t* active_out);
 
 #ifdef __cplusplus
 }

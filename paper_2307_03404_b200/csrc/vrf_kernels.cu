@@ -899,10 +899,21 @@ __global__ void k_upsample(DevGrid c, int frx, int fry, int frz, float* __restri
     const double p[3] = {dadd(c.ox, dmul(ix * 0.5, c.voxel)), dadd(c.oy, dmul(iy * 0.5, c.voxel)),
                          dadd(c.oz, dmul(iz * 0.5, c.voxel))};
     Sample s;
-    if (!locate(c, p, s)) {  // the world round trip left the box by an ulp: clamp
-      const double q[3] = {fmin(fmax(p[0], c.ox), c.hx), fmin(fmax(p[1], c.oy), c.hy),
-                           fmin(fmax(p[2], c.oz), c.hz)};
-      locate(c, q, s);
+    if (!locate(c, p, s)) {
+      // The world round trip put a far-corner vertex an ulp outside the box; the
+      // reference throws here (voxel_grid.cpp:107-111). Clamp the grid
+      // coordinate into [0, res-1] instead (the boundary vertex's value).
+      const double gx = fmin(fmax(div_voxel(c, dsub(p[0], c.ox)), 0.0), (double)c.rx - 1.0);
+      const double gy = fmin(fmax(div_voxel(c, dsub(p[1], c.oy)), 0.0), (double)c.ry - 1.0);
+      const double gz = fmin(fmax(div_voxel(c, dsub(p[2], c.oz)), 0.0), (double)c.rz - 1.0);
+      int cx = (int)ceil(gx) - 1, cy = (int)ceil(gy) - 1, cz = (int)ceil(gz) - 1;
+      cx = cx < 0 ? 0 : (cx > c.rx - 2 ? c.rx - 2 : cx);
+      cy = cy < 0 ? 0 : (cy > c.ry - 2 ? c.ry - 2 : cy);
+      cz = cz < 0 ? 0 : (cz > c.rz - 2 ? c.rz - 2 : cz);
+      s.fx = dsub(gx, (double)cx);
+      s.fy = dsub(gy, (double)cy);
+      s.fz = dsub(gz, (double)cz);
+      s.base = (uint32_t)(cx + c.rx * (cy + (long long)c.ry * cz));
     }
     double w[8];
     corner_weights(s, w);

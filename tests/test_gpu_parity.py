@@ -371,3 +371,23 @@ def test_mapping_steps_pipeline_equals_step_loop(ctx, deterministic):
         assert np.max(np.abs(ga - gb)) <= 1e-4 * np.max(np.abs(gb))
     with pytest.raises(ValueError, match="keyframe index out of range"):
         ctx.mapping_steps(cfg, r1, len(frames) + 1, 1)
+
+
+def test_upsample_far_corner_where_the_reference_throws(ctx, oracle):
+    """VoxelGrid::upsampled's world round trip can put the far-corner vertices an
+    ulp outside the box, and the reference then throws out_of_range from locate
+    (voxel_grid.cpp:203-206, 107-111; e.g. map_scene on room_scene's fitted
+    geometry). The device clamps those points to the box instead; with that
+    single difference it matches the oracle bit for bit."""
+    from paper_2307_03404_b200.api import fit_grid_geometry
+    grid, intr, frames = room_scene()
+    cfg = MappingConfig(initial_resolution=9)
+    geom = fit_grid_geometry(frames, list(range(len(frames))), intr, cfg)
+    g0 = fresh_grid(VoxelGrid(geom, 0.0), sigma_init=0.3, sh_noise=0.3)
+    with pytest.raises(IndexError):
+        oracle.upsample(g0, 64)  # the reference behaviour
+    (res, origin, voxel), data, act = oracle.upsample(g0, 64, clamp_outside=True)
+    ctx.load_grid(g0)
+    ctx.upsample(64)
+    assert tuple(ctx.geom.res) == res
+    assert np.array_equal(ctx.download_payload_f32(), data.astype(np.float32))
