@@ -56,57 +56,40 @@ __global__ void __launch_bounds__(kT) k_pose_fused(
       const DevPose pose = *pose_ptr;
       March m;
       ray_from_pixel(cam, pose, (double)px, (double)py, m);
-      Composite st;
       double basis[9];
-      if (!render_forward<ShT>(g, p, m, st, basis)) atomicOr(err, 1);
-      if (st.count > 0) {
-        hit = 1;
-        samples = st.count;
-        const double4 tg = rgbd[(long long)py * cam.width + px];
-        const double C[3] = {st.C[0], st.C[1], st.C[2]}, D = st.D;
-        const double res[4] = {dsub(C[0], tg.x), dsub(C[1], tg.y), dsub(C[2], tg.z),
-                               dsub(D, tg.w)};
-        // tracking.cpp:117: lambda_p |cres|^2 + lambda_d dres^2
-        loss = dadd(dmul(lambda_p, dadd(dadd(dmul(res[0], res[0]), dmul(res[1], res[1])),
-                                        dmul(res[2], res[2]))),
-                    dmul(dmul(lambda_d, res[3]), res[3]));
-        double Jo[4][3], Jd[4][3];
+      // One march: compositing and the Jacobian together. dC/dsigma_i =
+      // delta_i (c_i T_{i+1} - C + prefix_i) (gradients.cpp:69-97) is linear in
+      // the not-yet-known totals C, D, so the per-axis sums split into
+      //   J = sum_i [delta_i (c_i T_{i+1} + prefix_i) g_i + w_i Gc_i] - C sum_i delta_i g_i
+      // (g_i = gated spatial gradient of sigma) and C is applied after the ray.
+      double Jo[4][3], Jd[4][3], Bo[3] = {0, 0, 0}, Bd[3] = {0, 0, 0};
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = 0.0;
-        march_begin(g, p, m);
-        double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
+        for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = 0.0;
+      double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
+      int count = 0;
+      if (!sh_basis(m.d, basis)) {
+        atomicOr(err, 1);
+      } else if (march_begin(g, p, m)) {
         const double sgn[2] = {-1.0, 1.0};
+        ShT bs[9];
+#pragma unroll
+        for (int mm = 0; mm < 9; ++mm) bs[mm] = ShT(basis[mm]);
         Sample s;
         while (march_next(g, m, s)) {
-          double w[8];
-          corner_weights(s, w);
-          Shade sh;
-          shade<ShT>(g, s, w, basis, sh);
-          const double sigma = (sh.sigma_raw < 0.0) ? 0.0 : sh.sigma_raw;
-          const double decay = exp(dmul(-sigma, s.delta));
-          const double wgt = dmul(T, dsub(1.0, decay));
-          const double T_next = dmul(T, decay);
-          double dsig[4];
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            prefix[ch] = dadd(prefix[ch], dmul(sh.c[ch], wgt));
-            dsig[ch] = dmul(s.delta, dadd(dsub(dmul(sh.c[ch], T_next), C[ch]), prefix[ch]));
-          }
-          prefix_d = dadd(prefix_d, dmul(s.t, wgt));
-          dsig[3] = dmul(s.delta, dadd(dsub(dmul(s.t, T_next), D), prefix_d));
-          // spatial gradients of sigma and the basis-contracted SH channels
-          // (voxel_grid.cpp:130-151), contracted per corner
+          // trilerp + SH colour (renderer.cpp:98-112) and the spatial gradients
+          // of sigma and the basis-contracted SH channels (voxel_grid.cpp:130-151)
+          // from the same 8 corner loads
           const double wx[2] = {dsub(1.0, s.fx), s.fx}, wy[2] = {dsub(1.0, s.fy), s.fy},
                        wz[2] = {dsub(1.0, s.fz), s.fz};
+          double sraw = 0.0;
+          ShT csh[3] = {ShT(0), ShT(0), ShT(0)};
           double Gs[3] = {0, 0, 0}, Gc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-          ShT bs[9];
-#pragma unroll
-          for (int mm = 0; mm < 9; ++mm) bs[mm] = ShT(basis[mm]);
 #pragma unroll 1
           for (int k = 0; k < 8; ++k) {
             const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+            const double wk = dmul(dmul(wx[dx], wy[dy]), wz[dz]);
             const double dw[3] = {sgn[dx] * wy[dy] * wz[dz] * g.inv_voxel,
                                   wx[dx] * sgn[dy] * wz[dz] * g.inv_voxel,
                                   wx[dx] * wy[dy] * sgn[dz] * g.inv_voxel};
@@ -120,6 +103,7 @@ __global__ void __launch_bounds__(kT) k_pose_fused(
               v[4 * j + 2] = a.z;
               v[4 * j + 3] = a.w;
             }
+            sraw = dadd(sraw, dmul(wk, (double)v[0]));
             double shd[3];
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
@@ -127,6 +111,7 @@ __global__ void __launch_bounds__(kT) k_pose_fused(
 #pragma unroll
               for (int mm = 0; mm < 9; ++mm) acc = fma(bs[mm], (ShT)v[1 + ch * 9 + mm], acc);
               shd[ch] = (double)acc;
+              csh[ch] = fma(ShT(wk), acc, csh[ch]);
             }
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -135,13 +120,40 @@ __global__ void __launch_bounds__(kT) k_pose_fused(
               for (int ch = 0; ch < 3; ++ch) Gc[ch][a] = fma(dw[a], shd[ch], Gc[ch][a]);
             }
           }
-          const bool sgate = sh.sigma_raw > 0.0;
+          double c[3];
+          bool clamped[3];
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const double v = 0.5 + (double)csh[ch];
+            clamped[ch] = (v <= 0.0 || v >= 1.0);
+            c[ch] = (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);
+          }
+          const double sigma = (sraw < 0.0) ? 0.0 : sraw;
+          const double decay = exp(dmul(-sigma, s.delta));
+          const double wgt = dmul(T, dsub(1.0, decay));
+          const double T_next = dmul(T, decay);
+          ++count;
+          double dsig[4];
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            prefix[ch] = dadd(prefix[ch], dmul(c[ch], wgt));
+            dsig[ch] = s.delta * (c[ch] * T_next + prefix[ch]);
+          }
+          prefix_d = dadd(prefix_d, dmul(s.t, wgt));
+          dsig[3] = s.delta * (s.t * T_next + prefix_d);
+          const bool sgate = sraw > 0.0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const double gs = sgate ? s.delta * Gs[a] : 0.0;
+            Bo[a] += gs;
+            Bd[a] = fma(s.t, gs, Bd[a]);
+          }
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
               double gv = sgate ? dsig[r] * Gs[a] : 0.0;
-              if (r < 3 && !sh.clamped[r]) gv += wgt * Gc[r][a];
+              if (r < 3 && !clamped[r]) gv += wgt * Gc[r][a];
               Jo[r][a] += gv;
               Jd[r][a] = fma(s.t, gv, Jd[r][a]);
             }
@@ -149,6 +161,26 @@ __global__ void __launch_bounds__(kT) k_pose_fused(
           T = T_next;
           if (T < p.eps) break;
         }
+      }
+      if (count > 0) {
+        hit = 1;
+        samples = count;
+        const double4 tg = rgbd[(long long)py * cam.width + px];
+        // Ĉ = prefix, D̂ = prefix_d (renderer.cpp:120-126, same accumulation order)
+        const double C[4] = {prefix[0], prefix[1], prefix[2], prefix_d};
+        const double res[4] = {dsub(C[0], tg.x), dsub(C[1], tg.y), dsub(C[2], tg.z),
+                               dsub(C[3], tg.w)};
+        // tracking.cpp:117: lambda_p |cres|^2 + lambda_d dres^2
+        loss = dadd(dmul(lambda_p, dadd(dadd(dmul(res[0], res[0]), dmul(res[1], res[1])),
+                                        dmul(res[2], res[2]))),
+                    dmul(dmul(lambda_d, res[3]), res[3]));
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            Jo[r][a] -= C[r] * Bo[a];
+            Jd[r][a] -= C[r] * Bd[a];
+          }
         // chart (tracking.cpp:125-128): tau <- dL/do, omega <- d x (dL/dd - d (d.dL/dd))
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
