@@ -406,6 +406,7 @@ def run_ours(args):
         "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "traffic": ncu_traffic(dom, args.config), "peak_source": peak_kind,
         "launches": k_n, "kernel_ms": {k: v[0] for k, v in kern.items()},
+        "other_ms": {k: prof[k][0] for k in ("map_misc",) if k in prof},
         "step_algorithmic_GBps": step_bytes / (ms / 1e3) / 1e9,
         "step_frac": step_bytes / (ms / 1e3) / 1e9 / peak,
     }
