@@ -44,6 +44,8 @@ struct vrf_context {
   uint32_t* occ = nullptr;
   uint32_t* bocc = nullptr;  // 8^3-cell block occupancy (empty-space skipping)
   int bdim[3] = {0, 0, 0};
+  uint32_t* socc = nullptr;  // 64^3-cell superblock occupancy
+  int sdim[3] = {0, 0, 0};
   bool all_blocks_active = false;
   unsigned int* d_nblocks = nullptr;
 
@@ -148,9 +150,11 @@ inline void free_grid(vrf_context* ctx) {
   cudaFree(ctx->rms);
   cudaFree(ctx->occ);
   cudaFree(ctx->bocc);
+  cudaFree(ctx->socc);
   ctx->payload = ctx->grad = ctx->rms = nullptr;
   ctx->occ = nullptr;
   ctx->bocc = nullptr;
+  ctx->socc = nullptr;
   ctx->has_grid = false;
 }
 
@@ -185,6 +189,10 @@ inline int alloc_grid(vrf_context* ctx, const vrf_grid_geometry* g) {
     ctx->bdim[a] = (g->res[a] - 1 + (1 << kBlockLog2) - 1) >> kBlockLog2;
   const long long nblk = (long long)ctx->bdim[0] * ctx->bdim[1] * ctx->bdim[2];
   CU(cudaMalloc(&ctx->bocc, sizeof(uint32_t) * ((nblk + 31) / 32 + 1)));
+  constexpr int kS = kSuperLog2 - kBlockLog2;
+  for (int a = 0; a < 3; ++a) ctx->sdim[a] = (ctx->bdim[a] + (1 << kS) - 1) >> kS;
+  const long long nsup = (long long)ctx->sdim[0] * ctx->sdim[1] * ctx->sdim[2];
+  CU(cudaMalloc(&ctx->socc, sizeof(uint32_t) * ((nsup + 31) / 32 + 1)));
   CU(cudaMemsetAsync(ctx->payload, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
   CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
   CU(cudaMemsetAsync(ctx->rms, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
@@ -219,6 +227,10 @@ inline DevGrid dev_grid(const vrf_context* ctx) {
   g.bx = ctx->bdim[0];
   g.by = ctx->bdim[1];
   g.bz = ctx->bdim[2];
+  g.socc = ctx->socc;
+  g.sx = ctx->sdim[0];
+  g.sy = ctx->sdim[1];
+  g.sz = ctx->sdim[2];
   g.all_blocks_active = ctx->all_blocks_active ? 1 : 0;
   return g;
 }
@@ -230,6 +242,8 @@ inline int update_blocks(vrf_context* ctx) {
   launch_block_occupancy(ctx->occ, ctx->geom.res[0], ctx->geom.res[1], ctx->geom.res[2],
                          ctx->bdim[0], ctx->bdim[1], ctx->bdim[2], ctx->bocc, ctx->d_nblocks,
                          ctx->stream);
+  launch_super_occupancy(ctx->bocc, ctx->bdim[0], ctx->bdim[1], ctx->bdim[2], ctx->sdim[0],
+                         ctx->sdim[1], ctx->sdim[2], ctx->socc, ctx->stream);
   ctx->launches += 1;
   unsigned int n = 0;
   CU(cudaMemcpyAsync(&n, ctx->d_nblocks, sizeof(n), cudaMemcpyDeviceToHost, ctx->stream));

@@ -50,9 +50,13 @@ struct DevGrid {
   const uint32_t* __restrict__ bocc;
   int bx, by, bz;
   int all_blocks_active;  // host-known: no empty block, the jump can be compiled out
+  // Second level: 1 bit per superblock of 8^3 blocks (64^3 cells).
+  const uint32_t* __restrict__ socc;
+  int sx, sy, sz;
 };
 
 constexpr int kBlockLog2 = 3;  // 8^3-cell blocks
+constexpr int kSuperLog2 = 6;  // 64^3-cell superblocks
 
 // RenderParams after effective_step / effective_t_far (renderer.hpp:18-24).
 struct DevParams {
@@ -129,6 +133,7 @@ struct March {
   double o[3], d[3];
   double lo, hi, step;
   long long nseg, k;
+  double inv_d[3], inv_step;  // for the (margin-guarded) empty-space jumps only
 };
 
 // Slab clip + range clamp + segment count — renderer.cpp:12-29, 51-73.
@@ -158,6 +163,8 @@ __device__ __forceinline__ bool march_begin(const DevGrid& g, const DevParams& p
   m.step = p.step;
   m.nseg = (long long)ceil(dsub(ddiv(dsub(m.hi, m.lo), p.step), 1e-12));
   m.k = 0;
+  for (int a = 0; a < 3; ++a) m.inv_d[a] = m.d[a] == 0.0 ? 0.0 : 1.0 / m.d[a];
+  m.inv_step = 1.0 / p.step;
   return true;
 }
 
@@ -213,26 +220,32 @@ __device__ __forceinline__ bool block_active(const DevGrid& g, int cx, int cy, i
   return (__ldg(g.bocc + (b >> 5)) >> (b & 31)) & 1u;
 }
 
-// The sample at s lies in an all-inactive 8^3-cell block: return the first
-// segment index whose midpoint may lie beyond the block. Every segment between
-// has its midpoint inside the (convex) block box — the ray is inside the box at
-// s.t and until the box exit t_out — and would be dropped by the occupancy test,
-// so skipping them leaves the schedule unchanged. A 1e-6 m margin keeps the
-// jump clear of the exit face.
-__device__ __forceinline__ long long skip_empty_block(const DevGrid& g, const March& m,
-                                                      const Sample& s) {
-  const double ext = (double)(1 << kBlockLog2) * g.voxel;
-  const int b[3] = {s.cx >> kBlockLog2, s.cy >> kBlockLog2, s.cz >> kBlockLog2};
+__device__ __forceinline__ bool super_active(const DevGrid& g, int cx, int cy, int cz) {
+  const int b = (cx >> kSuperLog2) + g.sx * ((cy >> kSuperLog2) + g.sy * (cz >> kSuperLog2));
+  return (__ldg(g.socc + (b >> 5)) >> (b & 31)) & 1u;
+}
+
+// The sample at s lies in an all-inactive box of 2^L cells per axis (an 8^3
+// block, or a 64^3 superblock): return the first segment index whose midpoint
+// may lie beyond the box. Every segment in between has its midpoint inside the
+// (convex) box — the ray is inside it at s.t and until the box exit t_out — and
+// would be dropped by the occupancy test, so skipping them leaves the schedule
+// unchanged. A 1e-6 m margin keeps the jump clear of the exit face and absorbs
+// the rounding of the reciprocal-based exit time.
+__device__ __forceinline__ long long skip_empty_box(const DevGrid& g, const March& m,
+                                                    const Sample& s, int L) {
+  const double ext = (double)(1 << L) * g.voxel;
+  const int b[3] = {s.cx >> L, s.cy >> L, s.cz >> L};
   const double org[3] = {g.ox, g.oy, g.oz};
   double t_out = 1e300;
   for (int a = 0; a < 3; ++a) {
     if (m.d[a] == 0.0) continue;
     const double face = org[a] + (m.d[a] > 0.0 ? (b[a] + 1) : b[a]) * ext;
-    const double t = (face - m.o[a]) / m.d[a];
+    const double t = (face - m.o[a]) * m.inv_d[a];
     t_out = t < t_out ? t : t_out;
   }
   // midpoint of segment k is ~ lo + (k + 0.5) step; stay below t_out - margin
-  const double kf = floor((t_out - 1e-6 - m.lo) / m.step - 0.5);
+  const double kf = floor((t_out - 1e-6 - m.lo) * m.inv_step - 0.5);
   const long long k_new = kf > (double)m.nseg ? m.nseg : (long long)kf;
   return k_new > m.k ? k_new : m.k;
 }
@@ -253,7 +266,9 @@ __device__ __forceinline__ bool march_next(const DevGrid& g, March& m, Sample& s
                          dadd(m.o[2], dmul(tm, m.d[2]))};
     if (!locate(g, p, s)) continue;
     if (!cell_active(g, s.cell)) {
-      if (SKIP && !block_active(g, s.cx, s.cy, s.cz)) m.k = skip_empty_block(g, m, s);
+      if (SKIP && !block_active(g, s.cx, s.cy, s.cz))
+        m.k = skip_empty_box(g, m, s,
+                             super_active(g, s.cx, s.cy, s.cz) ? kBlockLog2 : kSuperLog2);
       continue;
     }
     s.t = tm;

@@ -135,6 +135,9 @@ void launch_prune(const DevGrid& g, uint32_t* occ_bits, double tau, unsigned lon
                   cudaStream_t s);
 void launch_upsample(const DevGrid& coarse, int frx, int fry, int frz, float* fine,
                      uint32_t* fine_occ, cudaStream_t s);
+// Superblock bit = OR of its (up to) 8^3 block bits.
+void launch_super_occupancy(const uint32_t* bocc, int bx, int by, int bz, int sx, int sy, int sz,
+                            uint32_t* socc, cudaStream_t s);
 void launch_block_occupancy(const uint32_t* occ, int rx, int ry, int rz, int bx, int by, int bz,
                             uint32_t* bocc, unsigned int* n_active, cudaStream_t s);
 

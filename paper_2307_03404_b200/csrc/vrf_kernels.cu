@@ -978,6 +978,29 @@ __global__ void k_block_occupancy(const uint32_t* __restrict__ occ, int rx, int 
   }
 }
 
+__global__ void k_super_occupancy(const uint32_t* __restrict__ bocc, int bx, int by, int bz,
+                                  int sx, int sy, int sz, uint32_t* __restrict__ socc) {
+  constexpr int kS = kSuperLog2 - kBlockLog2;
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;  // one 32-superblock word
+  const int ns = sx * sy * sz;
+  if (w * 32 >= ns) return;
+  uint32_t bits = 0;
+  for (int q = 0; q < 32; ++q) {
+    const int sidx = w * 32 + q;
+    if (sidx >= ns) break;
+    const int ix = sidx % sx, iy = (sidx / sx) % sy, iz = sidx / (sx * sy);
+    bool any = false;
+    for (int z = iz << kS; z < min((iz + 1) << kS, bz) && !any; ++z)
+      for (int y = iy << kS; y < min((iy + 1) << kS, by) && !any; ++y)
+        for (int x = ix << kS; x < min((ix + 1) << kS, bx) && !any; ++x) {
+          const int b = x + bx * (y + by * z);
+          any = (bocc[b >> 5] >> (b & 31)) & 1u;
+        }
+    if (any) bits |= 1u << q;
+  }
+  socc[w] = bits;
+}
+
 int grid_blocks(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   if (b > 148LL * 32) b = 148LL * 32;
@@ -1148,6 +1171,11 @@ void launch_block_occupancy(const uint32_t* occ, int rx, int ry, int rz, int bx,
   cudaMemsetAsync(n_active, 0, sizeof(unsigned int), s);
   k_block_occupancy<<<(nb + 127) / 128, 128, 0, s>>>(occ, rx, ry, rz, bx, by, bz, bocc,
                                                      n_active);
+}
+void launch_super_occupancy(const uint32_t* bocc, int bx, int by, int bz, int sx, int sy, int sz,
+                            uint32_t* socc, cudaStream_t s) {
+  const int words = (sx * sy * sz + 31) / 32;
+  k_super_occupancy<<<(words + 63) / 64, 64, 0, s>>>(bocc, bx, by, bz, sx, sy, sz, socc);
 }
 void launch_prune(const DevGrid& g, uint32_t* bits, double tau, unsigned long long* count,
                   cudaStream_t s) {

@@ -391,3 +391,32 @@ def test_upsample_far_corner_where_the_reference_throws(ctx, oracle):
     ctx.upsample(64)
     assert tuple(ctx.geom.res) == res
     assert np.array_equal(ctx.download_payload_f32(), data.astype(np.float32))
+
+
+def test_sparse_schedule_with_superblock_jumps_bit_exact(ctx, oracle):
+    """Empty-space jumps over 8^3 blocks and 64^3 superblocks leave the sample
+    schedule unchanged (renderer.cpp:62-79): a 129^3 grid whose only active cells
+    form a thin spherical shell, random rays from inside and outside it."""
+    rng = np.random.default_rng(21)
+    n = 129
+    geom = synth.GridGeometry((n, n, n), (-3.2, -3.2, -3.2), 0.05)
+    grid = VoxelGrid(geom, 2.0)
+    c = (np.arange(n - 1) + 0.5) * 0.05 - 3.2
+    zz, yy, xx = np.meshgrid(c, c, c, indexing="ij")
+    r = np.sqrt(xx ** 2 + yy ** 2 + zz ** 2)
+    grid.active[:] = (np.abs(r - 1.5) < 0.08).reshape(-1).astype(np.uint8)
+    ctx.load_grid(grid)
+    o = rng.uniform(-2.5, 2.5, (200, 3))
+    d = rng.normal(size=(200, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rays = np.concatenate([o, d], axis=1)
+    params = RenderParams(termination_eps=0.0)  # never terminate: walk every segment
+    counts, t, delta, cells = ctx.sample_rays(rays, params, cap=4096)
+    nonempty = 0
+    for i, row in enumerate(rays):
+        t0, d0, c0 = oracle.sample_ray(grid, row[:3], row[3:], params, cap=4096)
+        assert counts[i] == len(t0)
+        assert np.array_equal(t[i, :counts[i]], t0)
+        assert np.array_equal(cells[i, :counts[i]], c0)
+        nonempty += len(t0) > 0
+    assert nonempty > 30
