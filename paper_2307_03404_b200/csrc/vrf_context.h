@@ -46,6 +46,9 @@ struct vrf_context {
   int bdim[3] = {0, 0, 0};
   uint32_t* socc = nullptr;  // 64^3-cell superblock occupancy
   int sdim[3] = {0, 0, 0};
+  uint32_t* tb = nullptr;    // touched 8^3-vertex blocks of the pending gradient
+  int tdim[3] = {0, 0, 0};
+  bool touched_valid = false;  // every nonzero gradient group lies in a marked block
   bool all_blocks_active = false;
   unsigned int* d_nblocks = nullptr;
 
@@ -151,10 +154,13 @@ inline void free_grid(vrf_context* ctx) {
   cudaFree(ctx->occ);
   cudaFree(ctx->bocc);
   cudaFree(ctx->socc);
+  cudaFree(ctx->tb);
   ctx->payload = ctx->grad = ctx->rms = nullptr;
   ctx->occ = nullptr;
   ctx->bocc = nullptr;
   ctx->socc = nullptr;
+  ctx->tb = nullptr;
+  ctx->touched_valid = false;
   ctx->has_grid = false;
 }
 
@@ -193,6 +199,11 @@ inline int alloc_grid(vrf_context* ctx, const vrf_grid_geometry* g) {
   for (int a = 0; a < 3; ++a) ctx->sdim[a] = (ctx->bdim[a] + (1 << kS) - 1) >> kS;
   const long long nsup = (long long)ctx->sdim[0] * ctx->sdim[1] * ctx->sdim[2];
   CU(cudaMalloc(&ctx->socc, sizeof(uint32_t) * ((nsup + 31) / 32 + 1)));
+  for (int a = 0; a < 3; ++a) ctx->tdim[a] = (g->res[a] + (1 << kTouchLog2) - 1) >> kTouchLog2;
+  const long long ntb = (long long)ctx->tdim[0] * ctx->tdim[1] * ctx->tdim[2];
+  CU(cudaMalloc(&ctx->tb, sizeof(uint32_t) * ((ntb + 31) / 32 + 1)));
+  CU(cudaMemsetAsync(ctx->tb, 0, sizeof(uint32_t) * ((ntb + 31) / 32 + 1), ctx->stream));
+  ctx->touched_valid = false;
   CU(cudaMemsetAsync(ctx->payload, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
   CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
   CU(cudaMemsetAsync(ctx->rms, 0, sizeof(float) * 28 * ctx->Vpad, ctx->stream));
@@ -231,6 +242,10 @@ inline DevGrid dev_grid(const vrf_context* ctx) {
   g.sx = ctx->sdim[0];
   g.sy = ctx->sdim[1];
   g.sz = ctx->sdim[2];
+  g.tb = ctx->tb;
+  g.tbx = ctx->tdim[0];
+  g.tby = ctx->tdim[1];
+  g.tbz = ctx->tdim[2];
   g.all_blocks_active = ctx->all_blocks_active ? 1 : 0;
   return g;
 }

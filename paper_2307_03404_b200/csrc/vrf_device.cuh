@@ -53,10 +53,35 @@ struct DevGrid {
   // Second level: 1 bit per superblock of 8^3 blocks (64^3 cells).
   const uint32_t* __restrict__ socc;
   int sx, sy, sz;
+  // Touched vertex blocks (8^3 vertices): set by the fast scatter, consumed
+  // (and cleared) by the block-sparse RMSProp.
+  uint32_t* tb;
+  int tbx, tby, tbz;
 };
 
 constexpr int kBlockLog2 = 3;  // 8^3-cell blocks
 constexpr int kSuperLog2 = 6;  // 64^3-cell superblocks
+constexpr int kTouchLog2 = 3;  // 8^3-vertex touched blocks
+
+// Marks the touched blocks of every corner vertex of cell (cx, cy, cz): the
+// cell's own block, plus the +1 neighbours when a corner sits on the block's
+// upper face. `last` caches the last interior block id to skip repeats; the
+// atomic is skipped when the bit is already set.
+__device__ __forceinline__ void mark_touched(const DevGrid& g, int cx, int cy, int cz, int& last) {
+  constexpr int M = (1 << kTouchLog2) - 1;
+  const int bx = cx >> kTouchLog2, by = cy >> kTouchLog2, bz = cz >> kTouchLog2;
+  const int ex = (cx & M) == M, ey = (cy & M) == M, ez = (cz & M) == M;
+  const int id = bx + g.tbx * (by + g.tby * bz);
+  if (!(ex | ey | ez) && id == last) return;
+  last = (ex | ey | ez) ? -1 : id;
+  for (int dz = 0; dz <= ez; ++dz)
+    for (int dy = 0; dy <= ey; ++dy)
+      for (int dx = 0; dx <= ex; ++dx) {
+        const int b = (bx + dx) + g.tbx * ((by + dy) + g.tby * (bz + dz));
+        const uint32_t bit = 1u << (b & 31);
+        if (!(*((volatile uint32_t*)g.tb + (b >> 5)) & bit)) atomicOr(g.tb + (b >> 5), bit);
+      }
+}
 
 // RenderParams after effective_step / effective_t_far (renderer.hpp:18-24).
 struct DevParams {

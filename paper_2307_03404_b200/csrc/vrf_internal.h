@@ -84,6 +84,11 @@ void launch_map_backward_records(const DevGrid& g, const DevParams& p, const Dev
 void launch_segmented_reduce(const uint32_t* sorted_keys, const uint32_t* perm,
                              const double* values, long long nrec, double* grad_out_f64,
                              cudaStream_t s);
+// Block-sparse RMSProp over the touched 8^3-vertex blocks; clears the bitmap.
+void launch_rmsprop_blocks(float4* theta, float4* grad, float4* v, uint32_t* tb, int rx, int ry,
+                           int rz, int tbx, int tby, int tbz, double rho, double lr_sigma,
+                           double lr_sh, double eps, const MapStats* stats,
+                           unsigned long long* touched, cudaStream_t s);
 void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, long long v_end,
                     double rho, double lr_sigma, double lr_sh, double eps,
                     const MapStats* stats, unsigned long long* touched, cudaStream_t s);

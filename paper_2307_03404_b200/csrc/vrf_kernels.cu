@@ -524,6 +524,7 @@ __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevPar
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
   uint32_t cur = 0xffffffffu;
+  int last_tb = -1;
   Sample s;
   while (march_next<SKIP>(g, m, s)) {
     Shade sh;
@@ -547,6 +548,7 @@ __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevPar
     if (s.base != cur) {
       if (cur != 0xffffffffu) move_cell(grad, g, cur, s.base, a, bf);
       cur = s.base;
+      mark_touched(g, s.cx, s.cy, s.cz, last_tb);
     }
     const float wf = (float)wgt;
     const float u0 = sh.sigma_raw > 0.0 ? (float)ds : 0.f;
@@ -650,6 +652,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
   uint32_t cur = 0xffffffffu;
+  int last_tb = -1;
   // records are prefetched one iteration ahead: the dependent load of the next
   // (uncoalesced, mostly L2/DRAM) record overlaps this sample's math and scatter
   int c = rec_count[t] - 1;
@@ -691,6 +694,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
     if (s.base != cur) {
       if (cur != 0xffffffffu) move_cell(grad, g, cur, s.base, a, bf);
       cur = s.base;
+      mark_touched(g, s.cx, s.cy, s.cz, last_tb);
     }
     const float wf = q0.x;
     const float u0 = (kf & kRecSigmaPos) ? (float)ds : 0.f;
@@ -820,6 +824,56 @@ __global__ void __launch_bounds__(256) k_rmsprop(float4* __restrict__ theta,
     grad[f] = zero;
   }
   if (touched) {  // float4 groups updated (algorithmic optimizer bytes: 96 B each)
+    n_touched = warp_sum(n_touched);
+    if ((threadIdx.x & 31) == 0 && n_touched) atomicAdd(touched, (unsigned long long)n_touched);
+  }
+}
+
+// Block-sparse K4: one CTA per touched 8^3-vertex block (untouched blocks exit
+// at once), same per-group update as k_rmsprop. Every nonzero gradient group lies
+// in a block the scatter marked (mark_touched), so visiting only those blocks
+// updates exactly the reference's touched set (mapping.cpp:218-231).
+__global__ void __launch_bounds__(256) k_rmsprop_blocks(
+    float4* __restrict__ theta, float4* __restrict__ grad, float4* __restrict__ vstate,
+    const uint32_t* __restrict__ tb, int rx, int ry, int rz, int tbx, int tby, double rho,
+    double lr_sigma, double lr_sh, double eps, const MapStats* __restrict__ stats,
+    unsigned long long* __restrict__ touched) {
+  const int b = blockIdx.x;
+  if (!((tb[b >> 5] >> (b & 31)) & 1u)) return;
+  if (stats) {
+    const MapStats st = *stats;
+    if (st.bad != INT_MAX || st.m_c == 0) return;
+  }
+  constexpr int E = 1 << kTouchLog2;
+  const int bx = b % tbx, by = (b / tbx) % tby, bz = b / (tbx * tby);
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  unsigned int n_touched = 0;
+  for (int q = threadIdx.x; q < E * E * E * kVec4PerVertex; q += blockDim.x) {
+    const int vl = q / kVec4PerVertex, j = q % kVec4PerVertex;
+    const int x = bx * E + (vl % E), y = by * E + ((vl / E) % E), z = bz * E + vl / (E * E);
+    if (x >= rx || y >= ry || z >= rz) continue;
+    const long long f = ((long long)x + (long long)rx * (y + (long long)ry * z)) * kVec4PerVertex + j;
+    const float4 g4 = grad[f];
+    if (g4.x == 0.f && g4.y == 0.f && g4.z == 0.f && g4.w == 0.f) continue;
+    ++n_touched;
+    float4 th = theta[f], v4 = vstate[f];
+    float* thp = &th.x;
+    float* vp = &v4.x;
+    const float* gp = &g4.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double gg = gp[e];
+      if (gg == 0.0) continue;  // mapping.cpp:226
+      const double vn = rho * (double)vp[e] + (1.0 - rho) * gg * gg;
+      const double lr = (4 * j + e == 0) ? lr_sigma : lr_sh;
+      vp[e] = (float)vn;
+      thp[e] = (float)((double)thp[e] - lr * gg / sqrt(vn + eps));
+    }
+    theta[f] = th;
+    vstate[f] = v4;
+    grad[f] = zero;
+  }
+  if (touched) {
     n_touched = warp_sum(n_touched);
     if ((threadIdx.x & 31) == 0 && n_touched) atomicAdd(touched, (unsigned long long)n_touched);
   }
@@ -1133,6 +1187,15 @@ void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, l
   if (f1 <= f0) return;
   k_rmsprop<<<grid_blocks(f1 - f0, 256), 256, 0, s>>>(theta, grad, v, f0, f1, rho, lr_sigma,
                                                       lr_sh, eps, stats, touched);
+}
+void launch_rmsprop_blocks(float4* theta, float4* grad, float4* v, uint32_t* tb, int rx, int ry,
+                           int rz, int tbx, int tby, int tbz, double rho, double lr_sigma,
+                           double lr_sh, double eps, const MapStats* stats,
+                           unsigned long long* touched, cudaStream_t s) {
+  const int nb = tbx * tby * tbz;
+  k_rmsprop_blocks<<<nb, 256, 0, s>>>(theta, grad, v, tb, rx, ry, rz, tbx, tby, rho, lr_sigma,
+                                      lr_sh, eps, stats, touched);
+  cudaMemsetAsync(tb, 0, sizeof(uint32_t) * ((nb + 31) / 32 + 1), s);
 }
 void launch_fill_payload(float* payload, long long nv, float sigma, cudaStream_t s) {
   k_fill_payload<<<grid_blocks(nv * kPayload, 256), 256, 0, s>>>(payload, nv, sigma);

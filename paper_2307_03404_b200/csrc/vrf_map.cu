@@ -77,6 +77,7 @@ int finish_stats(vrf_context* ctx, const vrf_mapping_config* cfg, const MapStats
 // (ray_cd, flags, per-ray counts in s_count) and the host copy of the stats.
 int grad_deterministic(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev,
                        int n, const MapStats& st) {
+  ctx->touched_valid = false;  // the fp64 -> fp32 copy writes every vertex
   DevParams p;
   int rc = resolve_params(ctx, &cfg->render, &p);
   if (rc) return rc;
@@ -174,6 +175,29 @@ void launch_backward_fast(vrf_context* ctx, const vrf_mapping_config* cfg, const
   LAUNCHED(1);
 }
 
+// K4 over the whole grid, or block-sparse when the fast scatter marked every
+// touched block of this gradient (ctx->touched_valid).
+void launch_rmsprop_step(vrf_context* ctx, const vrf_mapping_config* cfg) {
+  cudaEvent_t pr = prof_begin(ctx);
+  static const bool force_full = std::getenv("VRF_RMSPROP_FULL") != nullptr;  // A/B, tests
+  if (ctx->touched_valid && !force_full) {
+    launch_rmsprop_blocks((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, ctx->tb,
+                          ctx->geom.res[0], ctx->geom.res[1], ctx->geom.res[2], ctx->tdim[0],
+                          ctx->tdim[1], ctx->tdim[2], cfg->rmsprop_decay, cfg->lr_sigma,
+                          cfg->lr_sh, cfg->rmsprop_eps, ctx->d_stats,
+                          ctx->profiling ? ctx->d_touched : nullptr, ctx->stream);
+  } else {
+    launch_rmsprop((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, 0, ctx->V,
+                   cfg->rmsprop_decay, cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, ctx->d_stats,
+                   ctx->profiling ? ctx->d_touched : nullptr, ctx->stream);
+    const long long ntb = (long long)ctx->tdim[0] * ctx->tdim[1] * ctx->tdim[2];
+    cudaMemsetAsync(ctx->tb, 0, sizeof(uint32_t) * ((ntb + 31) / 32 + 1), ctx->stream);
+  }
+  ctx->touched_valid = false;
+  prof_end(ctx, kProfRmsprop, pr);
+  LAUNCHED(1);
+}
+
 // Fills ctx->grad (fp32) with this batch's gradient. Deterministic mode goes
 // through the sorted fp64 reduce, then rounds once to fp32.
 int map_gradient(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev, int n,
@@ -183,6 +207,8 @@ int map_gradient(vrf_context* ctx, const vrf_mapping_config* cfg, const int* bat
   DevParams p;
   if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
   if (n > 0) launch_backward_fast(ctx, cfg, p, batch_dev, n, nullptr);
+  // the thread-per-ray scatter kernels mark the touched blocks; the warp variant does not
+  ctx->touched_valid = ctx->map_kernel == 0;
   CU(cudaGetLastError());
   if (need_host_stats && (rc = read_stats(ctx, st_out))) return rc;
   return VRF_OK;
@@ -221,13 +247,8 @@ int step_impl(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_
   } else {
     if ((rc = map_gradient(ctx, cfg, batch_dev, n, &st, false))) return rc;
   }
-  // K4: RMSProp over every vertex (skip g == 0 == the reference's touched set).
-  cudaEvent_t pr = prof_begin(ctx);
-  launch_rmsprop((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, 0, ctx->V,
-                 cfg->rmsprop_decay, cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, ctx->d_stats,
-                 ctx->profiling ? ctx->d_touched : nullptr, ctx->stream);
-  prof_end(ctx, kProfRmsprop, pr);
-  LAUNCHED(1);
+  // K4: RMSProp over the touched groups (g != 0 == the reference's touched set).
+  launch_rmsprop_step(ctx, cfg);
   CU(cudaGetLastError());
   if ((rc = check_err_flag(ctx))) return rc;
   if ((rc = read_stats(ctx, &st))) return rc;
@@ -301,12 +322,7 @@ int vrf_mapping_steps(vrf_context* ctx, const vrf_mapping_config* cfg, uint64_t 
     const int c = i & 1;
     CU(cudaMemcpyAsync((void*)db[c], hb[c], bbytes, cudaMemcpyHostToDevice, ctx->stream));
     if ((rc = map_gradient(ctx, cfg, db[c], n_rays, nullptr, false))) return rc;
-    cudaEvent_t pr = prof_begin(ctx);
-    launch_rmsprop((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, 0, ctx->V,
-                   cfg->rmsprop_decay, cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, ctx->d_stats,
-                   ctx->profiling ? ctx->d_touched : nullptr, ctx->stream);
-    prof_end(ctx, kProfRmsprop, pr);
-    LAUNCHED(1);
+    launch_rmsprop_step(ctx, cfg);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(h_st, ctx->d_stats, sizeof(MapStats), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(h_err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -436,6 +452,8 @@ int vrf_map_backward(vrf_context* ctx, const vrf_mapping_config* cfg, int32_t ra
   if (ctx->last_n > 0)
     launch_backward_fast(ctx, cfg, p, ctx->last_batch, ctx->last_n, ctx->d_counts);
   CU(cudaGetLastError());
+  // the reduce-scatter brings other ranks' gradients: vrf_map_apply scans its shard
+  ctx->touched_valid = false;
   return VRF_OK;
 }
 

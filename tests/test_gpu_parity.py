@@ -3,6 +3,9 @@
 Bars (BASELINE.json north_star): bit-exact sample schedules / cell ids /
 occupancy decisions; colour and depth within 1e-4 relative; gradients within
 1e-3 relative in deterministic mode; pose within 1 mm / 0.05 deg."""
+import os
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -420,3 +423,33 @@ def test_sparse_schedule_with_superblock_jumps_bit_exact(ctx, oracle):
         assert np.array_equal(cells[i, :counts[i]], c0)
         nonempty += len(t0) > 0
     assert nonempty > 30
+
+
+def test_block_sparse_rmsprop_matches_full_scan(tmp_path):
+    """The block-sparse RMSProp (touched 8^3-vertex blocks marked by the scatter)
+    updates exactly the groups the full scan updates: two fast mapping steps with
+    and without VRF_RMSPROP_FULL agree to fp32 atomics-order noise."""
+    import subprocess
+    import sys as _sys
+    script = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, "."); sys.path.insert(0, "oracle")
+from scenes import room_scene, fresh_grid
+from paper_2307_03404_b200 import Context, MappingConfig, Rng
+grid, intr, frames = room_scene(res=33)
+ctx = Context(0)
+ctx.load_grid(fresh_grid(grid)); ctx.load_frames(intr, frames); ctx.rmsprop_reset()
+ctx.mapping_steps(MappingConfig(rays_per_batch=2000), Rng(3), len(frames), 2)
+np.save(sys.argv[1], ctx.download_payload_f32())
+'''
+    outs = []
+    for full in (False, True):
+        env = dict(os.environ)
+        if full:
+            env["VRF_RMSPROP_FULL"] = "1"
+        f = tmp_path / f"p{int(full)}.npy"
+        subprocess.run([_sys.executable, "-c", script, str(f)], check=True, env=env,
+                       cwd=str(Path(__file__).resolve().parent.parent))
+        outs.append(np.load(f))
+    a, b = outs
+    assert np.max(np.abs(a - b)) <= 1e-4 * np.max(np.abs(b))
