@@ -32,12 +32,14 @@ def main():
     ap.add_argument("--width", type=int, default=1200)
     ap.add_argument("--height", type=int, default=680)
     ap.add_argument("--stride", type=int, default=10)
-    ap.add_argument("--map-steps", type=int, default=10)
-    ap.add_argument("--map-rays", type=int, default=65536)
-    ap.add_argument("--bootstrap", type=int, default=200)
+    ap.add_argument("--map-steps", type=int, default=100)
+    ap.add_argument("--map-rays", type=int, default=16384)
+    ap.add_argument("--bootstrap", type=int, default=3000)
     ap.add_argument("--track-rays", type=int, default=16384)
     ap.add_argument("--track-iters", type=int, default=10)
     ap.add_argument("--sigma-init", type=float, default=0.1)
+    ap.add_argument("--track-lambda-d", type=float, default=0.1,
+                    help="tracking depth weight (r01 sweep: 1.0 drifts, 0.1 holds 2 cm ATE)")
     ap.add_argument("--trace", action="store_true", help="print per-frame position error")
     ap.add_argument("--gt-map", action="store_true",
                     help="plumbing check: track against the ground-truth map, no mapping")
@@ -64,7 +66,8 @@ def main():
                      bootstrap_steps=args.bootstrap,
                      max_keyframes=(args.frames + args.stride - 1) // args.stride + 1,
                      tracking=GNConfig(rays_per_iteration=args.track_rays,
-                                       iterations=args.track_iters),
+                                       iterations=args.track_iters,
+                                       lambda_d=args.track_lambda_d),
                      mapping=MappingConfig(rays_per_batch=args.map_rays,
                                            sigma_init=args.sigma_init))
     ctx = Context(0)
