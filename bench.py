@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--dist-path", action="store_true",
+                    help="run the NCCL-composed distributed step even at world size 1 "
+                         "(launch under torchrun; validates the N>1 code path on one GPU)")
     a = ap.parse_args()
     if a.rays is None:
         a.rays = (8 << 20) if a.config == 4 else (1 << 20)
@@ -282,7 +285,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if world > 1:
+    use_dist = world > 1 or args.dist_path
+    if use_dist:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
@@ -322,7 +326,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     mapper = None
-    if world > 1:
+    if use_dist:
         from paper_2307_03404_b200.distributed import DistributedMapper, GpuEngine
         mapper = DistributedMapper(GpuEngine(ctx, cfg))
 
@@ -370,7 +374,7 @@ def run_ours(args):
     # it H2D from pinned memory and reads its stats back D2H; the draw of batch
     # i+1 overlaps the device work of step i.
     e2e = None
-    if world == 1:
+    if mapper is None:
         e_cfg = MappingConfig(rays_per_batch=args.rays)
         e_rng = Rng(99)
         ctx.mapping_steps(e_cfg, e_rng, len(frames), args.warmup)
@@ -385,6 +389,49 @@ def run_ours(args):
                "ms_per_step": 1e3 * e_s / args.steps,
                "api": "Context.mapping_steps (vrf_mapping_steps: host Rng draw + H2D + "
                       "step + stats D2H per step)"}
+    else:
+        # N ranks: each draws its own batch on the host (reference Rng stream per
+        # rank), copies it H2D from pinned memory, runs the distributed step
+        # (all-reduce of counts/losses, reduce-scatter, sharded RMSProp,
+        # all-gather) and reads the global stats back; wall time, max over ranks.
+        from concurrent.futures import ThreadPoolExecutor
+        e_rng = Rng(99 + 7919 * rank)
+        pins = [torch.empty((args.rays, 3), dtype=torch.int32).pin_memory() for _ in range(2)]
+        dbuf = torch.empty((args.rays, 3), dtype=torch.int32, device=f"cuda:{local}")
+        pool = ThreadPoolExecutor(1)  # the ctypes draw releases the GIL
+
+        def draw(k):
+            pins[k].numpy()[:] = e_rng.draw_batch(len(frames), intr.width, intr.height,
+                                                  args.rays)
+            return k
+
+        nxt = [pool.submit(draw, 0)]
+
+        def e_step():
+            k = nxt[0].result()
+            dbuf.copy_(pins[k], non_blocking=True)
+            torch.cuda.current_stream().synchronize()  # pins[k] is free again
+            nxt[0] = pool.submit(draw, k ^ 1)  # next batch drawn while this step runs
+            return mapper.step(dbuf, cfg.lambda_d)
+
+        for _ in range(args.warmup):
+            e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        e_samples = 0
+        for _ in range(args.steps):
+            e_samples += e_step().samples
+        torch.cuda.synchronize()
+        e_s = torch.tensor([time.perf_counter() - t0], device=f"cuda:{local}")
+        dist.all_reduce(e_s, op=dist.ReduceOp.MAX)
+        e_s = float(e_s.item())
+        e2e = {"value": e_samples / e_s, "unit": "samples/s",
+               "h2d_bytes_per_step": int(args.rays * 12) * world,
+               "d2h_bytes_per_step": 48 * world,
+               "ms_per_step": 1e3 * e_s / args.steps,
+               "api": "DistributedMapper.step per rank (host Rng draw + pinned H2D + "
+                      "NCCL-composed step + global stats D2H), max over ranks"}
 
     # ---- roofline of the dominant kernel
     peak, peak_kind = load_peaks()
