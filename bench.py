@@ -194,22 +194,37 @@ def cpu_reference(args, gt, intr, keyframe_poses, frames, seconds):
     grid = VoxelGrid(gt.geom, 0.1)
     fh = ref.frames(frames, intr)
     cfg = MappingConfig()
-    steps = 0
-    elapsed = 0.0
-    # Each repetition: a fresh sigma_init map and a fresh Rng(1), so every timed call
-    # is the reference's first mapping_step of map_scene (mapping.cpp:290-313) on the
+
+    # Each call: a fresh sigma_init map and a fresh Rng(1), so every timed call is
+    # the reference's first mapping_step of map_scene (mapping.cpp:290-313) on the
     # same 4096-ray batch; setup is outside the timed region.
-    while elapsed < seconds and steps < 20:
+    def one(nthreads):
         gh = ref.grid(grid)
         mapper = ref.lib.ref_mapper_create(1)
         t0 = time.perf_counter()
-        ref.mapping_step(gh, fh, intr, cfg, 4096, threads, False, mapper)
-        elapsed += time.perf_counter() - t0
-        steps += 1
+        ref.mapping_step(gh, fh, intr, cfg, 4096, nthreads, False, mapper)
+        dt = time.perf_counter() - t0
         ref.lib.ref_mapper_destroy(mapper)
         ref.lib.ref_grid_destroy(gh)
+        return dt
+
+    # The reference zero-fills one V x 28 fp64 buffer per worker every step
+    # (mapping.cpp:155-157), so all cores is not its fastest setting at 257^3:
+    # sweep a few thread counts and keep the fastest (the fairest CPU figure).
+    cands = sorted({t for t in (1, 2, 4, threads) if t <= threads})
+    sweep = {}
+    for t in cands:
+        sweep[t] = one(t)
+        if len(sweep) >= 2 and sweep[t] > min(sweep.values()) * 1.3:
+            break  # past the optimum
+    best = min(sweep, key=sweep.get)
+    steps, elapsed = 1, sweep[best]
+    while elapsed < seconds and steps < 20:
+        elapsed += one(best)
+        steps += 1
     ref.lib.ref_frames_destroy(fh)
-    return {"threads": threads, "steps": steps, "seconds": elapsed}
+    return {"threads": best, "steps": steps, "seconds": elapsed,
+            "sweep_s": {str(k): round(v, 3) for k, v in sweep.items()}}
 
 
 def cpu_samples_per_step(args, gt, intr, frames):
@@ -268,7 +283,8 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": r["threads"],
                          "kind": "reference",
                          "sample": f"{r['steps']} reference mapping_step calls x 4096 rays on the "
-                                   f"257^3 fp64 grid ({per_step} composited samples/step)"},
+                                   f"257^3 fp64 grid ({per_step} composited samples/step); "
+                                   f"threads = fastest of the sweep {r['sweep_s']} (s/step)"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))
@@ -500,7 +516,8 @@ def run_ours(args):
                        "cores": r["threads"], "kind": "reference",
                        "sample": f"{r['steps']} reference mapping_step calls x 4096 rays on the "
                                  f"257^3 fp64 grid, fresh sigma_init=0.1 map "
-                                 f"({per_step} composited samples/step)"}
+                                 f"({per_step} composited samples/step); threads = fastest "
+                                 f"of the sweep {r['sweep_s']} (s/step)"}
         except Exception as e:  # the baseline must never hide our own number
             cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "reference",
                    "sample": f"failed: {e}"}
