@@ -15,6 +15,8 @@
 //   K5 (vrf_track.cu)      fused pose forward + Jacobian -> J^T J, J^T r
 //   utilities              prune, upsample, block occupancy, pack / convert
 #include <cstdio>
+#include <string>
+#include <type_traits>
 #include <cstdlib>
 #include <climits>
 
@@ -416,36 +418,90 @@ __device__ __forceinline__ void map_backward_ray(const DevGrid& g, const DevPara
   }
 }
 
+// Scatter sinks: where an aggregated corner (4 factors x SH basis = 28 slots)
+// goes. RedSink issues 7 red.global.add.v4.f32 from registers (default).
+// BulkSink writes the 112-B vertex gradient into a per-thread shared-memory ring
+// and issues ONE cp.reduce.async.bulk (.add.f32, SASS UBLKRED) per corner, so
+// the L2 sees one 112-B reduction instead of seven 16-B ones. Microbenchmark
+// (tools/microbench/bulk_red.cu, 1M threads x 64 coherent flushes, all lanes
+// active): 29 G vertex-flushes/s with red.v4 against 50 G/s bulk. Inside the
+// divergent backward it loses (UBLKRED is uniform-datapath: serialised over the
+// active lanes), so it stays an A/B option (VRF_SCATTER=bulk).
+struct RedSink {
+  float4* __restrict__ grad;
+  __device__ __forceinline__ void operator()(uint32_t v, float s, float r, float gg, float b,
+                                             const float (&bf)[9]) {
+    float4* dst = grad + (size_t)v * kVec4PerVertex;
+    float x[28];
+    x[0] = s;
+#pragma unroll
+    for (int mm = 0; mm < 9; ++mm) {
+      x[1 + mm] = r * bf[mm];
+      x[10 + mm] = gg * bf[mm];
+      x[19 + mm] = b * bf[mm];
+    }
+#pragma unroll
+    for (int j = 0; j < kVec4PerVertex; ++j)
+      atomicAdd(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
+  }
+  __device__ __forceinline__ void finish() {}
+};
+
+constexpr int kBulkSlots = 2;  // per-thread ring of 112-B staging slots
+struct BulkSink {
+  float4* __restrict__ grad;
+  float4* ring;  // this thread's kBulkSlots x 7 float4 in shared memory
+  int slot;
+  __device__ __forceinline__ void operator()(uint32_t v, float s, float r, float gg, float b,
+                                             const float (&bf)[9]) {
+    float4* my = ring + slot * kVec4PerVertex;
+    slot = (slot + 1) % kBulkSlots;
+    // the bulk op that last used this slot must have finished reading it
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kBulkSlots - 1) : "memory");
+    float x[28];
+    x[0] = s;
+#pragma unroll
+    for (int mm = 0; mm < 9; ++mm) {
+      x[1 + mm] = r * bf[mm];
+      x[10 + mm] = gg * bf[mm];
+      x[19 + mm] = b * bf[mm];
+    }
+#pragma unroll
+    for (int j = 0; j < kVec4PerVertex; ++j)
+      my[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(my);
+    asm volatile(
+        "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+            grad + (size_t)v * kVec4PerVertex),
+        "r"(sa), "n"(kVec4PerVertex * 16)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  // all reductions complete (and the ring no longer read) before the thread exits
+  __device__ __forceinline__ void finish() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+};
+
 // Scatter corner k of the aggregated cell (slots: sigma, a_ch * basis_m).
-__device__ __forceinline__ void flush_corner(float4* __restrict__ grad, const DevGrid& g,
-                                             uint32_t base, float (&a)[4][8],
-                                             const float (&bf)[9], int k) {
+template <typename Sink>
+__device__ __forceinline__ void flush_corner(Sink& sink, const DevGrid& g, uint32_t base,
+                                             float (&a)[4][8], const float (&bf)[9], int k) {
   const float s = a[0][k], r = a[1][k], gg = a[2][k], b = a[3][k];
   a[0][k] = a[1][k] = a[2][k] = a[3][k] = 0.f;
   if (s == 0.f && r == 0.f && gg == 0.f && b == 0.f) return;
-  float v[28];
-  v[0] = s;
-#pragma unroll
-  for (int mm = 0; mm < 9; ++mm) {
-    v[1 + mm] = r * bf[mm];
-    v[10 + mm] = gg * bf[mm];
-    v[19 + mm] = b * bf[mm];
-  }
-  float4* dst = grad + (size_t)corner_index(g, base, k) * kVec4PerVertex;
-#pragma unroll
-  for (int j = 0; j < kVec4PerVertex; ++j)
-    atomicAdd(dst + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+  sink(corner_index(g, base, k), s, r, gg, b, bf);
 }
 
 // Face-adjacent move along the axis of corner bit BIT (+1 if POS): flush the 4
 // departing corners, carry the 4 shared ones to their new corner slots.
-template <int BIT, bool POS>
-__device__ __forceinline__ void shift_cell(float4* __restrict__ grad, const DevGrid& g,
-                                           uint32_t old_base, float (&a)[4][8],
-                                           const float (&bf)[9]) {
+template <int BIT, bool POS, typename Sink>
+__device__ __forceinline__ void shift_cell(Sink& sink, const DevGrid& g, uint32_t old_base,
+                                           float (&a)[4][8], const float (&bf)[9]) {
 #pragma unroll
   for (int k = 0; k < 8; ++k)
-    if (((k & BIT) != 0) != POS) flush_corner(grad, g, old_base, a, bf, k);
+    if (((k & BIT) != 0) != POS) flush_corner(sink, g, old_base, a, bf, k);
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     if (k & BIT) continue;
@@ -463,27 +519,28 @@ __device__ __forceinline__ void shift_cell(float4* __restrict__ grad, const DevG
   }
 }
 
-__device__ __forceinline__ void move_cell(float4* __restrict__ grad, const DevGrid& g,
-                                          uint32_t old_base, uint32_t new_base, float (&a)[4][8],
+template <typename Sink>
+__device__ __forceinline__ void move_cell(Sink& sink, const DevGrid& g, uint32_t old_base,
+                                          uint32_t new_base, float (&a)[4][8],
                                           const float (&bf)[9]) {
   // For valid cells a base difference of +-1 / +-rx / +-rx*ry is exactly a
   // single-axis unit move (|dcx| <= rx-2, |dcx + rx dcy| < rx*ry).
   const long long d = (long long)new_base - (long long)old_base;
   if (d == 1)
-    shift_cell<1, true>(grad, g, old_base, a, bf);
+    shift_cell<1, true>(sink, g, old_base, a, bf);
   else if (d == -1)
-    shift_cell<1, false>(grad, g, old_base, a, bf);
+    shift_cell<1, false>(sink, g, old_base, a, bf);
   else if (d == g.rx)
-    shift_cell<2, true>(grad, g, old_base, a, bf);
+    shift_cell<2, true>(sink, g, old_base, a, bf);
   else if (d == -(long long)g.rx)
-    shift_cell<2, false>(grad, g, old_base, a, bf);
+    shift_cell<2, false>(sink, g, old_base, a, bf);
   else if (d == (long long)g.rxy)
-    shift_cell<4, true>(grad, g, old_base, a, bf);
+    shift_cell<4, true>(sink, g, old_base, a, bf);
   else if (d == -(long long)g.rxy)
-    shift_cell<4, false>(grad, g, old_base, a, bf);
+    shift_cell<4, false>(sink, g, old_base, a, bf);
   else {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) flush_corner(grad, g, old_base, a, bf, k);
+    for (int k = 0; k < 8; ++k) flush_corner(sink, g, old_base, a, bf, k);
   }
 }
 
@@ -525,6 +582,7 @@ __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevPar
     for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
   uint32_t cur = 0xffffffffu;
   int last_tb = -1;
+  RedSink sink{grad};
   Sample s;
   while (march_next<SKIP>(g, m, s)) {
     Shade sh;
@@ -546,7 +604,7 @@ __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevPar
     }
     ds *= s.delta;
     if (s.base != cur) {
-      if (cur != 0xffffffffu) move_cell(grad, g, cur, s.base, a, bf);
+      if (cur != 0xffffffffu) move_cell(sink, g, cur, s.base, a, bf);
       cur = s.base;
       mark_touched(g, s.cx, s.cy, s.cz, last_tb);
     }
@@ -570,7 +628,7 @@ __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevPar
   }
   if (cur != 0xffffffffu) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) flush_corner(grad, g, cur, a, bf, k);
+    for (int k = 0; k < 8; ++k) flush_corner(sink, g, cur, a, bf, k);
   }
 }
 
@@ -613,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
 // them with all lanes cut divergence but not time — the scatter is bound by L2
 // atomic throughput (~2 corner flushes per sample; 38% distinct within a warp's
 // 176-entry window), so fewer instructions do not help without merging.
-template <int MINB>
+template <int MINB, bool BULK>
 __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
@@ -621,6 +679,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
     const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
     float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
     const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
+  __shared__ __align__(16) float4 s_ring[BULK ? kThreads : 1][kBulkSlots][kVec4PerVertex];
+  using Sink = typename std::conditional<BULK, BulkSink, RedSink>::type;
+  Sink sink;
+  if constexpr (BULK)
+    sink = BulkSink{grad, &s_ring[threadIdx.x][0][0], 0};
+  else
+    sink = RedSink{grad};
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int i = order ? (int)order[t] : t;
@@ -692,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
     Sc2 += c2 * w;
     Sd += tm * w;
     if (s.base != cur) {
-      if (cur != 0xffffffffu) move_cell(grad, g, cur, s.base, a, bf);
+      if (cur != 0xffffffffu) move_cell(sink, g, cur, s.base, a, bf);
       cur = s.base;
       mark_touched(g, s.cx, s.cy, s.cz, last_tb);
     }
@@ -714,8 +779,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
   }
   if (cur != 0xffffffffu) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) flush_corner(grad, g, cur, a, bf, k);
+    for (int k = 0; k < 8; ++k) flush_corner(sink, g, cur, a, bf, k);
   }
+  sink.finish();
 }
 
 // ------------------------------------------------------------------ K3 deterministic records
@@ -1114,20 +1180,24 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
     const char* e = std::getenv("VRF_REC_MINB");
     return e ? std::atoi(e) : 3;
   }();
+  // scatter sink: per-float4 red (default) or the bulk reduce (VRF_SCATTER=bulk, A/B).
+  // r01: red 17.6 ms vs bulk 21.5 ms per 1M-ray backward — UBLKRED is a uniform-
+  // datapath op, so a divergent flush serialises it over the active lanes.
+  static const bool bulk = [] {
+    const char* e = std::getenv("VRF_SCATTER");
+    return e && std::string(e) == "bulk";
+  }();
   const int blocks = (n + kThreads - 1) / kThreads;
-  if (minb == 3)
-    k_map_backward_rec<3><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
-                                                      flags, stats, global_counts, grad, lambda_d,
-                                                      order, rec, K, rec_count);
-  else if (minb == 2)
-    k_map_backward_rec<2><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
-                                                      flags, stats, global_counts, grad, lambda_d,
-                                                      order, rec, K, rec_count);
-  else
-    k_map_backward_rec<4><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
-                                                      flags, stats, global_counts, grad, lambda_d,
-                                                      order, rec, K, rec_count);
-
+#define VRF_REC_LAUNCH(MB, BK)                                                                  \
+  k_map_backward_rec<MB, BK><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd, \
+                                                         flags, stats, global_counts, grad,       \
+                                                         lambda_d, order, rec, K, rec_count)
+  if (minb == 4) {
+    if (bulk) VRF_REC_LAUNCH(4, true); else VRF_REC_LAUNCH(4, false);
+  } else {
+    if (bulk) VRF_REC_LAUNCH(3, true); else VRF_REC_LAUNCH(3, false);
+  }
+#undef VRF_REC_LAUNCH
 }
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s) {
   k_map_reduce<<<1, 1024, 0, s>>>(partials, nparts, out);
