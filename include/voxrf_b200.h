@@ -173,7 +173,8 @@ int vrf_set_shard_multiple(vrf_context* ctx, int world_size);
 /* Run on an external stream (e.g. torch.cuda.current_stream()); NULL = own stream. */
 int vrf_set_stream(vrf_context* ctx, void* stream);
 int vrf_get_device_buffers(vrf_context* ctx, vrf_device_buffers* out);
-/* Number of kernels this context launched since creation (bench evidence). */
+/* Number of this library's own kernels the context launched since creation
+ * (bench evidence; cub sorts and memsets are not counted). */
 int64_t vrf_kernel_launch_count(const vrf_context* ctx);
 /* Per-kernel CUDA-event timing on the context stream (resets the counters).
  * Slots: 0 map forward, 1 map backward (scatter), 2 RMSProp, 3 misc,

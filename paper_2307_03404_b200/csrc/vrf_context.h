@@ -391,7 +391,7 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
                      (uint32_t*)ctx->s_okeys2.ptr, (uint32_t*)ctx->s_order.ptr, ctx->s_otmp.ptr,
                      tmp, ctx->stream);
     prof_end(ctx, kProfMapMisc, po);
-    LAUNCHED(2);
+    LAUNCHED(1);  // k_ray_keys (the cub radix sort behind it is a library launch)
     CU(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int) * 4, ctx->stream));
     // Sample records for the reverse-order backward: up to K per ray within a
     // memory budget (VRF_REC_GB, default 16 GB; 0 disables); longer rays overflow

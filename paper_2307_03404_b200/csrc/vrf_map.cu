@@ -92,7 +92,7 @@ int grad_deterministic(vrf_context* ctx, const vrf_mapping_config* cfg, const in
   if ((rc = ensure(ctx, ctx->s_cub, tmp_scan))) return rc;
   CU(cub::DeviceScan::ExclusiveSum(ctx->s_cub.ptr, tmp_scan, (const int*)ctx->s_count.ptr,
                                    offsets, n, ctx->stream));
-  LAUNCHED(1);
+  // (cub kernels are library launches: not counted in vrf_kernel_launch_count)
   // Chunk the batch by rays so the records (36 doubles per sample + 8 keys/ids)
   // stay bounded; every chunk continues each vertex's running fp64 sum.
   std::vector<int> counts((size_t)n);
@@ -134,7 +134,7 @@ int grad_deterministic(vrf_context* ctx, const vrf_mapping_config* cfg, const in
       launch_segmented_reduce((const uint32_t*)ctx->s_keys2.ptr, (const uint32_t*)ctx->s_ids2.ptr,
                               (const double*)ctx->s_values.ptr, R, (double*)ctx->s_grad64.ptr,
                               ctx->stream);
-      LAUNCHED(3);
+      LAUNCHED(2);  // k_map_records + k_segmented_reduce (the cub sort is not ours)
       CU(cudaGetLastError());
     }
     sid_base += S;
