@@ -78,6 +78,7 @@ struct vrf_context {
       s_ids, s_ids2, s_values, s_grad64, s_cub, s_stage, s_out, s_batch2, s_rec, s_reccount;
   // fast-path sample records of the last forward (0 = recompute-march backward)
   int rec_K = 0;
+  int max_ray_samples = 0;  // longest ray seen by a mapping forward (sizes rec_K)
 
   // multi-GPU phase state
   const int* last_batch = nullptr;
@@ -393,19 +394,38 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
     prof_end(ctx, kProfMapMisc, po);
     LAUNCHED(1);  // k_ray_keys (the cub radix sort behind it is a library launch)
     CU(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int) * 4, ctx->stream));
-    // Sample records for the reverse-order backward: up to K per ray within a
-    // memory budget (VRF_REC_GB, default 16 GB; 0 disables); longer rays overflow
-    // to the recompute-march backward.
+    // Sample records for the backward: up to K per ray. K covers the longest
+    // ray seen so far (x1.25, rounded up to a power of two so the buffer rarely
+    // regrows; 1024 before the first step), within a memory budget (VRF_REC_GB;
+    // default 35 % of the free HBM plus the record buffer already held, checked
+    // only when the held buffer is too small). Longer rays overflow to the
+    // recompute-march backward.
     ctx->rec_K = 0;
     if (!warp) {
-      static const double budget_gb = [] {
+      static const double env_gb = [] {
         const char* e = std::getenv("VRF_REC_GB");
-        return e ? std::atof(e) : 16.0;
+        return e ? std::atof(e) : -1.0;
       }();
-      long long K = (long long)(budget_gb * 1e9) / ((long long)nn * (long long)sizeof(SampleRec));
-      K = std::min(K, 1024LL) & ~3LL;
+      long long need = 1024;
+      if (ctx->max_ray_samples > 0) {
+        need = 64;
+        while (need < ctx->max_ray_samples * 5LL / 4 && need < 1024) need *= 2;
+      }
+      long long K = need;
+      const size_t nn32 = (nn + 31) & ~(size_t)31;  // warp-tiled record layout
+      const double per_level = (double)nn32 * (double)sizeof(SampleRec);
+      if ((double)ctx->s_rec.bytes < per_level * (double)need) {
+        double budget = env_gb * 1e9;
+        if (env_gb < 0.0) {
+          size_t free_b = 0, total_b = 0;
+          CU(cudaMemGetInfo(&free_b, &total_b));
+          budget = 0.35 * (double)free_b + (double)ctx->s_rec.bytes;
+        }
+        K = std::min(K, (long long)(budget / per_level));
+      }
+      K &= ~3LL;
       if (K >= 16) {
-        if ((rc = ensure(ctx, ctx->s_rec, sizeof(SampleRec) * nn * (size_t)K))) return rc;
+        if ((rc = ensure(ctx, ctx->s_rec, sizeof(SampleRec) * nn32 * (size_t)K))) return rc;
         if ((rc = ensure(ctx, ctx->s_reccount, sizeof(int) * nn))) return rc;
         ctx->rec_K = (int)K;
       }

@@ -13,7 +13,7 @@ struct MapPartial {
   double lp, lg;
   long long samples;
   int m_c, m_d, bad;
-  int pad;
+  int max_count;  // longest composited sample run of one ray (record-cap sizing)
 };
 using MapStats = MapPartial;  // reduced: bad = first bad ray (INT_MAX if none)
 
@@ -53,8 +53,8 @@ void launch_map_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                         const uint32_t* order, cudaStream_t s);
 int map_forward_blocks(int n);
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s);
-// Fast forward that also stores up to K SampleRec per ray, sample-major
-// (rec[c * n + slot], slot = coherent order index); rays with more samples get
+// Fast forward that also stores up to K SampleRec per ray, warp-tiled sample-major
+// (rec_index(slot, c, K), slot = coherent order index); rays with more samples get
 // kOverflow. rec_count[slot] = samples stored.
 void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
                             const double4* rgbd, const DevPose* poses, int n_frames,

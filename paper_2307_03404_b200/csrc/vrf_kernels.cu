@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward(
   const int bmc = block_sum(mc, s_i);
   const int bmd = block_sum(md, s_i);
   const int bbad = block_min(bad, s_i);
+  const int bmax = -block_min(-(int)samples, s_i);
   if (threadIdx.x == 0) {
     MapPartial q;
     q.lp = blp;
@@ -190,18 +191,27 @@ __global__ void __launch_bounds__(kThreads) k_map_forward(
     q.m_c = bmc;
     q.m_d = bmd;
     q.bad = bbad;
-    q.pad = 0;
+    q.max_count = bmax;
     partials[blockIdx.x] = q;
   }
+}
+
+// Record slot of sample c of the ray in slot t: warp-tiled sample-major
+// ("AoSoA"): the 32 rays of a warp own one contiguous K x 32 x 24 B region, and
+// within it sample c of all 32 lanes is contiguous. A warp's c-th stores are one
+// coalesced 768 B access, and each warp walks its own region (few TLB pages;
+// the plain c * n + t layout strode n x 24 B between a ray's samples).
+__device__ __forceinline__ size_t rec_index(int t, int c, int K) {
+  return ((size_t)(t >> 5) * (size_t)K + (size_t)c) * 32 + (size_t)(t & 31);
 }
 
 // Fast forward (fp32 SH) that records every composited sample for the
 // backward: identical march, sigma_raw replay, compositing and termination as
 // k_map_forward<float>; per sample it stores w_i, T_{i+1}, the clamped colour
 // and (segment index, clamp / sigma gates) — 24 B — so the backward never
-// gathers the 896 B of corner payload again. Records are sample-major
-// (rec[c * n + slot]): the lanes of a warp composite their c-th samples in the
-// same loop iteration, so each record store is one coalesced 768 B warp access.
+// gathers the 896 B of corner payload again. Records are warp-tiled
+// sample-major (rec_index): the lanes of a warp composite their c-th samples in
+// the same loop iteration, so each record store is one coalesced 768 B access.
 __global__ void __launch_bounds__(kThreads) k_map_forward_rec(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
@@ -256,7 +266,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec(
             const uint32_t kf = ((uint32_t)(m.k - 1) << 4) | (sh.clamped[0] ? 1u : 0u) |
                                 (sh.clamped[1] ? 2u : 0u) | (sh.clamped[2] ? 4u : 0u) |
                                 (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
-            float2* d = reinterpret_cast<float2*>(rec + (size_t)(st.count - 1) * n + t);
+            float2* d = reinterpret_cast<float2*>(rec + rec_index(t, st.count - 1, K));
             d[0] = make_float2((float)wgt, (float)st.T);
             d[1] = make_float2((float)sh.c[0], (float)sh.c[1]);
             d[2] = make_float2((float)sh.c[2], __uint_as_float(kf));
@@ -300,6 +310,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec(
   const int bmc = block_sum(mc, s_i);
   const int bmd = block_sum(md, s_i);
   const int bbad = block_min(bad, s_i);
+  const int bmax = -block_min(-(int)samples, s_i);
   if (threadIdx.x == 0) {
     MapPartial q;
     q.lp = blp;
@@ -308,7 +319,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec(
     q.m_c = bmc;
     q.m_d = bmd;
     q.bad = bbad;
-    q.pad = 0;
+    q.max_count = bmax;
     partials[blockIdx.x] = q;
   }
 }
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(1024) k_map_reduce(const MapPartial* __restric
   __shared__ int s_i[32];
   double lp = 0.0, lg = 0.0;
   long long samples = 0;
-  int mc = 0, md = 0, bad = INT_MAX;
+  int mc = 0, md = 0, bad = INT_MAX, mx = 0;
   for (int k = threadIdx.x; k < nparts; k += blockDim.x) {
     const MapPartial q = parts[k];
     lp += q.lp;
@@ -330,6 +341,7 @@ __global__ void __launch_bounds__(1024) k_map_reduce(const MapPartial* __restric
     mc += q.m_c;
     md += q.m_d;
     bad = min(bad, q.bad);
+    mx = max(mx, q.max_count);
   }
   const double blp = block_sum(lp, s_d);
   const double blg = block_sum(lg, s_d);
@@ -337,6 +349,7 @@ __global__ void __launch_bounds__(1024) k_map_reduce(const MapPartial* __restric
   const int bmc = block_sum(mc, s_i);
   const int bmd = block_sum(md, s_i);
   const int bbad = block_min(bad, s_i);
+  const int bmx = -block_min(-mx, s_i);
   if (threadIdx.x == 0) {
     MapStats r;
     r.lp = blp;
@@ -345,7 +358,7 @@ __global__ void __launch_bounds__(1024) k_map_reduce(const MapPartial* __restric
     r.m_c = bmc;
     r.m_d = bmd;
     r.bad = bbad;
-    r.pad = 0;
+    r.max_count = bmx;
     *out = r;
   }
 }
@@ -723,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
   int c = rec_count[t] - 1;
   float2 n0 = make_float2(0.f, 0.f), n1 = n0, n2 = n0;
   if (c >= 0) {
-    const float2* q = reinterpret_cast<const float2*>(rec + (size_t)c * n + t);
+    const float2* q = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
     n0 = __ldg(q);
     n1 = __ldg(q + 1);
     n2 = __ldg(q + 2);
@@ -731,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
   for (; c >= 0; --c) {
     const float2 q0 = n0, q1 = n1, q2 = n2;
     if (c > 0) {
-      const float2* q = reinterpret_cast<const float2*>(rec + (size_t)(c - 1) * n + t);
+      const float2* q = reinterpret_cast<const float2*>(rec + rec_index(t, c - 1, K));
       n0 = __ldg(q);
       n1 = __ldg(q + 1);
       n2 = __ldg(q + 2);

@@ -41,6 +41,7 @@ int upload_batch(vrf_context* ctx, const int32_t* batch, int n, const int** dev)
 int read_stats(vrf_context* ctx, MapStats* st) {
   CU(cudaMemcpyAsync(st, ctx->d_stats, sizeof(MapStats), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  ctx->max_ray_samples = std::max(ctx->max_ray_samples, st->max_count);
   return VRF_OK;
 }
 
@@ -334,6 +335,7 @@ int vrf_mapping_steps(vrf_context* ctx, const vrf_mapping_config* cfg, uint64_t 
     if (*h_err & 1)
       return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "sh_eval: direction must be unit length");
     const MapStats st = *h_st;
+    ctx->max_ray_samples = std::max(ctx->max_ray_samples, st.max_count);
     if (st.m_c == 0 || st.bad != INT_MAX) {
       CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * (size_t)ctx->Vpad, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
