@@ -135,6 +135,16 @@ def config2(ref, cores, n_frames=4):
     gn_s = time.perf_counter() - t0
     fh = ref.frames(frames, intr)
     gh = ref.grid(gt)
+    # render_image (A20) at 1200x680 on the same map: GPU vs the reference's own
+    ctx.render_image(intr, poses[0])
+    t0 = time.perf_counter()
+    for pz in poses:
+        gimg = ctx.render_image(intr, pz)
+    gpu_render_s = (time.perf_counter() - t0) / len(poses)
+    t0 = time.perf_counter()
+    rc, rd = ref.render_image(gh, intr, poses[-1], api.RenderParams(), 1, cores)
+    cpu_render_s = time.perf_counter() - t0
+    render_diff = float(np.max(np.abs(gimg.depth - rd)))
     cpu_p, cpu_ms = ref.track_sequence(gh, fh, intr, tcfg, n_frames, threads=cores)
     ref.lib.ref_grid_destroy(gh)
     ref.lib.ref_frames_destroy(fh)
@@ -147,6 +157,8 @@ def config2(ref, cores, n_frames=4):
                          "gpu_vs_cpu_max_dt_m": dt, "gpu_vs_cpu_max_drot_deg": dr},
         "gn_16384x10": {"gpu_frames_per_s": (n_frames - 1) / gn_s,
                         "ate_vs_gt_m": ate_rmse(gn_poses, ts, poses, ts, align=False)[0]},
+        "render_image_1200x680": {"gpu_ms": 1e3 * gpu_render_s, "cpu_ms": 1e3 * cpu_render_s,
+                                  "cpu_cores": cores, "max_depth_diff_m": render_diff},
     }
 
 
