@@ -30,6 +30,7 @@ class SlamConfig:
     map_steps: int = 10                 # mapping_step calls per new keyframe
     bootstrap_steps: int = 200          # mapping_step calls on frame 0 before tracking
     max_keyframes: int = 256
+    window: int = 0                     # map over the last `window` keyframes (0 = all)
     constant_velocity: bool = True      # track_sequence init policy (tracking.cpp:271-272)
     tracking: GNConfig = field(default_factory=GNConfig)
     mapping: MappingConfig = field(default_factory=lambda: MappingConfig(rays_per_batch=65536))
@@ -62,9 +63,11 @@ class SlamSystem:
 
     def _map(self, steps: int):
         m = self.cfg.mapping
+        w = self.n_keyframes if self.cfg.window <= 0 else min(self.cfg.window, self.n_keyframes)
+        first = self.n_keyframes - w
         for _ in range(steps):
-            batch = self.rng.draw_batch(self.n_keyframes, self.intr.width, self.intr.height,
-                                        m.rays_per_batch)
+            batch = self.rng.draw_batch(w, self.intr.width, self.intr.height, m.rays_per_batch)
+            batch[:, 0] += first  # keyframe slots [first, n_keyframes)
             self.ctx.mapping_step(m, batch)
 
     def _add_keyframe(self, frame: Frame, pose: Pose):
