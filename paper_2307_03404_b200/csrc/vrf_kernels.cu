@@ -532,29 +532,30 @@ __device__ __forceinline__ void shift_cell(Sink& sink, const DevGrid& g, uint32_
   }
 }
 
+// Move of the aggregated cell by (dx, dy, dz): a neighbouring cell (face, edge
+// or vertex adjacent) is reached as up to three unit face shifts, so every
+// corner shared with the new cell is carried and only the corners the ray
+// leaves are flushed (an edge move flushes 6, not 8; corners that are zero —
+// fresh slots of an intermediate cell — are skipped by flush_corner). Anything
+// farther (a block jump) flushes all 8.
 template <typename Sink>
 __device__ __forceinline__ void move_cell(Sink& sink, const DevGrid& g, uint32_t old_base,
-                                          uint32_t new_base, float (&a)[4][8],
+                                          int dx, int dy, int dz, float (&a)[4][8],
                                           const float (&bf)[9]) {
-  // For valid cells a base difference of +-1 / +-rx / +-rx*ry is exactly a
-  // single-axis unit move (|dcx| <= rx-2, |dcx + rx dcy| < rx*ry).
-  const long long d = (long long)new_base - (long long)old_base;
-  if (d == 1)
-    shift_cell<1, true>(sink, g, old_base, a, bf);
-  else if (d == -1)
-    shift_cell<1, false>(sink, g, old_base, a, bf);
-  else if (d == g.rx)
-    shift_cell<2, true>(sink, g, old_base, a, bf);
-  else if (d == -(long long)g.rx)
-    shift_cell<2, false>(sink, g, old_base, a, bf);
-  else if (d == (long long)g.rxy)
-    shift_cell<4, true>(sink, g, old_base, a, bf);
-  else if (d == -(long long)g.rxy)
-    shift_cell<4, false>(sink, g, old_base, a, bf);
-  else {
+  if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) flush_corner(sink, g, old_base, a, bf, k);
+    return;
   }
+  uint32_t b = old_base;
+  if (dx > 0) shift_cell<1, true>(sink, g, b, a, bf);
+  if (dx < 0) shift_cell<1, false>(sink, g, b, a, bf);
+  b += dx;
+  if (dy > 0) shift_cell<2, true>(sink, g, b, a, bf);
+  if (dy < 0) shift_cell<2, false>(sink, g, b, a, bf);
+  b += dy * g.rx;
+  if (dz > 0) shift_cell<4, true>(sink, g, b, a, bf);
+  if (dz < 0) shift_cell<4, false>(sink, g, b, a, bf);
 }
 
 // Fast-path backward of one ray (fp32 SH, fp32 gradient accumulation). Same
@@ -594,6 +595,7 @@ __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevPar
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
   uint32_t cur = 0xffffffffu;
+  int pcx = 0, pcy = 0, pcz = 0;
   int last_tb = -1;
   RedSink sink{grad};
   Sample s;
@@ -617,8 +619,12 @@ __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevPar
     }
     ds *= s.delta;
     if (s.base != cur) {
-      if (cur != 0xffffffffu) move_cell(sink, g, cur, s.base, a, bf);
+      if (cur != 0xffffffffu)
+        move_cell(sink, g, cur, s.cx - pcx, s.cy - pcy, s.cz - pcz, a, bf);
       cur = s.base;
+      pcx = s.cx;
+      pcy = s.cy;
+      pcz = s.cz;
       mark_touched(g, s.cx, s.cy, s.cz, last_tb);
     }
     const float wf = (float)wgt;
@@ -730,6 +736,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
   uint32_t cur = 0xffffffffu;
+  int pcx = 0, pcy = 0, pcz = 0;
   int last_tb = -1;
   // records are prefetched one iteration ahead: the dependent load of the next
   // (uncoalesced, mostly L2/DRAM) record overlaps this sample's math and scatter
@@ -770,8 +777,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
     Sc2 += c2 * w;
     Sd += tm * w;
     if (s.base != cur) {
-      if (cur != 0xffffffffu) move_cell(sink, g, cur, s.base, a, bf);
+      if (cur != 0xffffffffu)
+        move_cell(sink, g, cur, s.cx - pcx, s.cy - pcy, s.cz - pcz, a, bf);
       cur = s.base;
+      pcx = s.cx;
+      pcy = s.cy;
+      pcz = s.cz;
       mark_touched(g, s.cx, s.cy, s.cz, last_tb);
     }
     const float wf = q0.x;
