@@ -237,13 +237,13 @@ int vrf_render_image(vrf_context* ctx, const vrf_intrinsics* intr, const vrf_pos
  * Mutates the device grid and RMSProp state in place, like the reference. */
 int vrf_mapping_step(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* batch,
                      int n_rays, vrf_map_step_stats* out);
-/* Same, batch already in device memory. */
 /* map_scene's inner loop (mapping.cpp:302-312): n_steps mapping_step calls, batch i
  * drawn from the reference Rng stream `rng_state` (advanced in place) over the first
  * n_keyframes frame slots. The host draw of batch i+1 overlaps the device work of
  * step i (pinned double buffer). out: n_steps stats; stops at the first error. */
 int vrf_mapping_steps(vrf_context* ctx, const vrf_mapping_config* cfg, uint64_t rng_state[4],
                       int n_keyframes, int n_rays, int n_steps, vrf_map_step_stats* out);
+/* vrf_mapping_step with the batch already in device memory. */
 int vrf_mapping_step_device(vrf_context* ctx, const vrf_mapping_config* cfg,
                             const int32_t* batch_dev, int n_rays, vrf_map_step_stats* out);
 /* The merged grid gradient of one batch (no update): double [V][28] host. */
