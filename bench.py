@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--exchange", default="sparse", choices=["sparse", "dense"],
+                    help="N>1 gradient exchange: touched 8^3-vertex blocks only, or the "
+                         "whole grid")
     ap.add_argument("--dist-path", action="store_true",
                     help="run the NCCL-composed distributed step even at world size 1 "
                          "(launch under torchrun; validates the N>1 code path on one GPU)")
@@ -348,7 +351,7 @@ def run_ours(args):
 
     def one_step(i):
         if mapper is not None:
-            return mapper.step(dev_batches[i], cfg.lambda_d)
+            return mapper.step(dev_batches[i], cfg.lambda_d, sparse=args.exchange == "sparse")
         return ctx.mapping_step_device(cfg, dev_batches[i].data_ptr(), args.rays)
 
     for i in range(args.warmup):
@@ -428,7 +431,7 @@ def run_ours(args):
             dbuf.copy_(pins[k], non_blocking=True)
             torch.cuda.current_stream().synchronize()  # pins[k] is free again
             nxt[0] = pool.submit(draw, k ^ 1)  # next batch drawn while this step runs
-            return mapper.step(dbuf, cfg.lambda_d)
+            return mapper.step(dbuf, cfg.lambda_d, sparse=args.exchange == "sparse")
 
         for _ in range(args.warmup):
             e_step()
@@ -532,6 +535,7 @@ def run_ours(args):
                        "rays_per_step_per_gpu": args.rays,
                        "grid_vertices": ctx.geom.num_vertices, "keyframes": len(frames),
                        "frame": f"{args.width}x{args.height}", "parallelism": f"dp{world}",
+                       "exchange": (args.exchange if mapper is not None else "none"),
                        "l2": f"inputs larger than L2 (grid "
                              f"{ctx.geom.num_vertices * 112 / 1e9:.1f} GB fp32)"},
             "rays_per_s": total_rays / (ms / 1e3),

@@ -170,7 +170,9 @@ int vrf_abi_version(void);
 /* Pads the gradient/RMSProp buffers to a multiple of world_size vertices so
  * NCCL reduce-scatter shards are equal; call before vrf_grid_*. */
 int vrf_set_shard_multiple(vrf_context* ctx, int world_size);
-/* Run on an external stream (e.g. torch.cuda.current_stream()); NULL = own stream. */
+/* Run on an external stream (e.g. torch.cuda.current_stream()); NULL = the context's
+ * own non-blocking stream. For the legacy default stream pass cudaStreamLegacy
+ * ((void*)1), not NULL. */
 int vrf_set_stream(vrf_context* ctx, void* stream);
 int vrf_get_device_buffers(vrf_context* ctx, vrf_device_buffers* out);
 /* Number of this library's own kernels the context launched since creation
@@ -263,6 +265,20 @@ int vrf_map_backward(vrf_context* ctx, const vrf_mapping_config* cfg, int32_t ra
                      int32_t rays_depth);
 int vrf_map_apply(vrf_context* ctx, const vrf_mapping_config* cfg, int64_t vertex_begin,
                   int64_t vertex_end);
+/* Block-sparse variant of the exchange (distributed.py): the backward marks the
+ * touched 8^3-vertex blocks; the caller max-all-reduces the per-block flags,
+ * packs the touched blocks' gradients into [n][512][28] fp32 (ids_dev: int32
+ * block ids, < 0 = padding; which 0 = gradient, 1 = payload), reduce-scatters
+ * them by block owner, applies RMSProp to its own blocks, packs and all-gathers
+ * the updated payload blocks, unpacks them and clears the gradient. */
+int vrf_blocks_count(vrf_context* ctx, int32_t* n_blocks);
+int vrf_blocks_touched(vrf_context* ctx, uint8_t* flags_dev);
+int vrf_blocks_pack(vrf_context* ctx, const int32_t* ids_dev, int n, int which, float* out_dev);
+int vrf_blocks_unpack_payload(vrf_context* ctx, const int32_t* ids_dev, int n,
+                              const float* in_dev);
+int vrf_blocks_apply(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* ids_dev,
+                     int n, const float* grad_packed_dev);
+int vrf_grad_clear(vrf_context* ctx);
 
 /* ---- tracking */
 /* pose_gradient — tracking.hpp:70-73 (tracking.cpp:76-143); pixels: n (px, py). */

@@ -140,6 +140,12 @@ _SIGS = {
     "vrf_map_forward": (C.c_int, [vp, P(MappingConfig_c), vp, C.c_int, P(MapPartials_c)]),
     "vrf_map_backward": (C.c_int, [vp, P(MappingConfig_c), C.c_int32, C.c_int32]),
     "vrf_map_apply": (C.c_int, [vp, P(MappingConfig_c), C.c_int64, C.c_int64]),
+    "vrf_blocks_count": (C.c_int, [vp, P(C.c_int32)]),
+    "vrf_blocks_touched": (C.c_int, [vp, vp]),
+    "vrf_blocks_pack": (C.c_int, [vp, vp, C.c_int, C.c_int, vp]),
+    "vrf_blocks_unpack_payload": (C.c_int, [vp, vp, C.c_int, vp]),
+    "vrf_blocks_apply": (C.c_int, [vp, P(MappingConfig_c), vp, C.c_int, vp]),
+    "vrf_grad_clear": (C.c_int, [vp]),
     "vrf_pose_gradient": (C.c_int, [vp, C.c_int, P(Intrinsics_c), P(Pose_c), vp, C.c_int,
                                     P(TrackingLoss_c), P(PoseGradient_c)]),
     "vrf_pose_normal_equations": (C.c_int, [vp, C.c_int, P(Intrinsics_c), P(Pose_c), vp,

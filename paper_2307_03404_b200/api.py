@@ -418,7 +418,12 @@ class Context:
         return out
 
     def set_stream(self, stream_ptr: int):
-        self._check(self._lib.vrf_set_stream(self._h, C.c_void_p(stream_ptr)))
+        """Run on an external CUDA stream, e.g. torch.cuda.current_stream().cuda_stream.
+        Handle 0 (torch's default stream) means the legacy default stream, passed as
+        cudaStreamLegacy (1): NULL would select the context's own non-blocking stream,
+        which does not order itself with torch's work."""
+        ptr = int(stream_ptr) if stream_ptr else 1  # cudaStreamLegacy
+        self._check(self._lib.vrf_set_stream(self._h, C.c_void_p(ptr)))
 
     def device_buffers(self):
         b = capi.DeviceBuffers_c()
@@ -626,6 +631,31 @@ class Context:
         self._check(self._lib.vrf_map_apply(self._h, C.byref(cc), v_begin, v_end))
 
     # ---- tracking
+    # ---- block-sparse multi-GPU exchange (device pointers; see distributed.py)
+    def blocks_count(self) -> int:
+        n = C.c_int32()
+        self._check(self._lib.vrf_blocks_count(self._h, C.byref(n)))
+        return int(n.value)
+
+    def blocks_touched(self, flags_ptr: int):
+        self._check(self._lib.vrf_blocks_touched(self._h, C.c_void_p(flags_ptr)))
+
+    def blocks_pack(self, ids_ptr: int, n: int, which: int, out_ptr: int):
+        self._check(self._lib.vrf_blocks_pack(self._h, C.c_void_p(ids_ptr), int(n), int(which),
+                                              C.c_void_p(out_ptr)))
+
+    def blocks_unpack_payload(self, ids_ptr: int, n: int, in_ptr: int):
+        self._check(self._lib.vrf_blocks_unpack_payload(self._h, C.c_void_p(ids_ptr), int(n),
+                                                        C.c_void_p(in_ptr)))
+
+    def blocks_apply(self, config: MappingConfig, ids_ptr: int, n: int, grad_ptr: int):
+        cc = config._c()
+        self._check(self._lib.vrf_blocks_apply(self._h, C.byref(cc), C.c_void_p(ids_ptr), int(n),
+                                               C.c_void_p(grad_ptr)))
+
+    def grad_clear(self):
+        self._check(self._lib.vrf_grad_clear(self._h))
+
     def pose_gradient(self, frame: int, intr: CameraIntrinsics, pose: Pose, pixels: np.ndarray,
                       config: TrackingConfig) -> PoseGradient:
         px = np.ascontiguousarray(pixels, dtype=np.int32).reshape(-1, 2)

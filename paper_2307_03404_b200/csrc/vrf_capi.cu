@@ -434,6 +434,7 @@ int vrf_frames_upload(vrf_context* ctx, const vrf_intrinsics* intr, int n,
   cudaSetDevice(ctx->device);
   if (n < 0 || !intr || intr->width <= 0 || intr->height <= 0)
     return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "intrinsics: empty image size");
+  CU(cudaStreamSynchronize(ctx->stream));
   cudaFree(ctx->rgbd);
   cudaFree(ctx->poses);
   ctx->rgbd = nullptr;

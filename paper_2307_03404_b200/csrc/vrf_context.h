@@ -127,20 +127,49 @@ inline int set_err(vrf_context* c, int code, const std::string& m) {
 
 #define LAUNCHED(n) (ctx->launches += (n))
 
+// Grow-only scratch. Work already queued on the context stream may still be
+// using the old buffer (the multi-GPU phases return without a host sync), and
+// cudaFree does not order itself after it: drain the stream before freeing.
 inline int ensure(vrf_context* ctx, DeviceScratch& s, size_t bytes) {
   if (s.bytes >= bytes) return VRF_OK;
-  if (s.ptr) CU(cudaFree(s.ptr));
+  if (s.ptr) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaFree(s.ptr));
+  }
   s.ptr = nullptr;
   s.bytes = 0;
-  const size_t want = bytes < 256 ? 256 : bytes + bytes / 4;
+  // 25 % headroom against regrowth, but none on multi-GB buffers
+  const size_t want = bytes < 256 ? 256 : (bytes > (1ull << 30) ? bytes : bytes + bytes / 4);
   CU(cudaMalloc(&s.ptr, want));
   s.bytes = want;
   return VRF_OK;
 }
 
+// Like ensure, but an out-of-memory result is not an error: returns false (and
+// clears the sticky CUDA error) so the caller can shrink the request.
+inline bool try_ensure(cudaStream_t stream, DeviceScratch& s, size_t bytes) {
+  if (s.bytes >= bytes) return true;
+  if (s.ptr) {
+    cudaStreamSynchronize(stream);
+    cudaFree(s.ptr);
+  }
+  s.ptr = nullptr;
+  s.bytes = 0;
+  if (cudaMalloc(&s.ptr, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    s.ptr = nullptr;
+    return false;
+  }
+  s.bytes = bytes;
+  return true;
+}
+
 inline int ensure_pinned(vrf_context* ctx, size_t bytes) {
   if (ctx->h_pinned_bytes >= bytes) return VRF_OK;
-  if (ctx->h_pinned) CU(cudaFreeHost(ctx->h_pinned));
+  if (ctx->h_pinned) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaFreeHost(ctx->h_pinned));
+  }
   ctx->h_pinned = nullptr;
   const size_t want = bytes < 4096 ? 4096 : bytes + bytes / 4;
   CU(cudaMallocHost(&ctx->h_pinned, want));
@@ -149,6 +178,7 @@ inline int ensure_pinned(vrf_context* ctx, size_t bytes) {
 }
 
 inline void free_grid(vrf_context* ctx) {
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);  // queued work may still use them
   cudaFree(ctx->payload);
   cudaFree(ctx->grad);
   cudaFree(ctx->rms);
@@ -395,11 +425,11 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
     LAUNCHED(1);  // k_ray_keys (the cub radix sort behind it is a library launch)
     CU(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int) * 4, ctx->stream));
     // Sample records for the backward: up to K per ray. K covers the longest
-    // ray seen so far (x1.25, rounded up to a power of two so the buffer rarely
-    // regrows; 1024 before the first step), within a memory budget (VRF_REC_GB;
-    // default 35 % of the free HBM plus the record buffer already held, checked
-    // only when the held buffer is too small). Longer rays overflow to the
-    // recompute-march backward.
+    // ray seen so far (x1.25, rounded up to a power of two; 1024 before the first
+    // step), within a memory budget (VRF_REC_GB; default 30 % of the free HBM
+    // plus the record buffer already held). The buffer regrows only when that
+    // at least doubles K, so steps do not reallocate. Longer rays overflow to
+    // the recompute-march backward.
     ctx->rec_K = 0;
     if (!warp) {
       static const double env_gb = [] {
@@ -411,23 +441,31 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
         need = 64;
         while (need < ctx->max_ray_samples * 5LL / 4 && need < 1024) need *= 2;
       }
-      long long K = need;
       const size_t nn32 = (nn + 31) & ~(size_t)31;  // warp-tiled record layout
       const double per_level = (double)nn32 * (double)sizeof(SampleRec);
-      if ((double)ctx->s_rec.bytes < per_level * (double)need) {
+      // K the held buffer already covers; regrow only for a real shortfall
+      // (2x), so a budget-limited cap does not reallocate every step
+      const long long held_K = (long long)((double)ctx->s_rec.bytes / per_level);
+      long long K = std::min(need, held_K);
+      if (held_K < 16 || need >= 2 * held_K) {
         double budget = env_gb * 1e9;
         if (env_gb < 0.0) {
           size_t free_b = 0, total_b = 0;
           CU(cudaMemGetInfo(&free_b, &total_b));
-          budget = 0.35 * (double)free_b + (double)ctx->s_rec.bytes;
+          budget = 0.30 * (double)free_b + (double)ctx->s_rec.bytes;
         }
-        K = std::min(K, (long long)(budget / per_level));
+        const long long cand = std::min(need, (long long)(budget / per_level));
+        if (held_K < 16 || cand >= 2 * held_K) K = cand;  // grow only by a real factor
       }
       K &= ~3LL;
+      // other allocators (e.g. torch's caching allocator in the multi-GPU
+      // driver) may hold memory the budget counted: halve on out-of-memory
+      while (K >= 16 &&
+             !try_ensure(ctx->stream, ctx->s_rec, sizeof(SampleRec) * nn32 * (size_t)K))
+        K /= 2;
       if (K >= 16) {
-        if ((rc = ensure(ctx, ctx->s_rec, sizeof(SampleRec) * nn32 * (size_t)K))) return rc;
         if ((rc = ensure(ctx, ctx->s_reccount, sizeof(int) * nn))) return rc;
-        ctx->rec_K = (int)K;
+        ctx->rec_K = (int)(K & ~3LL);
       }
     }
     cudaEvent_t pb = prof_begin(ctx);

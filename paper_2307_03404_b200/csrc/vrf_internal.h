@@ -89,6 +89,15 @@ void launch_rmsprop_blocks(float4* theta, float4* grad, float4* v, uint32_t* tb,
                            int rz, int tbx, int tby, int tbz, double rho, double lr_sigma,
                            double lr_sh, double eps, const MapStats* stats,
                            unsigned long long* touched, cudaStream_t s);
+// Block-sparse multi-GPU exchange (8^3-vertex blocks, packed [n][512][28] fp32; id < 0 = pad).
+void launch_touched_flags(const uint32_t* tb, int nb, uint8_t* flags, cudaStream_t s);
+void launch_blocks_pack(const float4* src, const int* ids, int n, int rx, int ry, int rz, int tbx,
+                        int tby, float4* out, cudaStream_t s);
+void launch_blocks_unpack(float4* dst, const int* ids, int n, int rx, int ry, int rz, int tbx,
+                          int tby, const float4* in, cudaStream_t s);
+void launch_blocks_apply(float4* theta, float4* v, const int* ids, int n, int rx, int ry, int rz,
+                         int tbx, int tby, const float4* packed, double rho, double lr_sigma,
+                         double lr_sh, double eps, cudaStream_t s);
 void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, long long v_end,
                     double rho, double lr_sigma, double lr_sh, double eps,
                     const MapStats* stats, unsigned long long* touched, cudaStream_t s);

@@ -969,6 +969,94 @@ __global__ void __launch_bounds__(256) k_rmsprop_blocks(
   }
 }
 
+// ------------------------------------------------------------------ block-sparse exchange
+// Multi-GPU block-sparse gradient exchange (distributed.py): the touched 8^3-
+// vertex blocks are packed into [n][512][28] fp32 (local x-fastest vertex order,
+// vertices outside the grid zero), reduced across ranks block-wise, applied by
+// the owning rank and the updated payload blocks gathered back. id < 0 = padding.
+constexpr int kBlockVerts = 1 << (3 * kTouchLog2);
+
+__global__ void k_touched_flags(const uint32_t* __restrict__ tb, int nb, uint8_t* __restrict__ f) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) f[b] = (tb[b >> 5] >> (b & 31)) & 1u;
+}
+
+__device__ __forceinline__ long long block_vertex(int b, int vl, int rx, int ry, int rz, int tbx,
+                                                  int tby) {
+  constexpr int E = 1 << kTouchLog2;
+  const int bx = b % tbx, by = (b / tbx) % tby, bz = b / (tbx * tby);
+  const int x = bx * E + (vl % E), y = by * E + ((vl / E) % E), z = bz * E + vl / (E * E);
+  if (x >= rx || y >= ry || z >= rz) return -1;
+  return (long long)x + (long long)rx * (y + (long long)ry * z);
+}
+
+// which: 0 = gradient, 1 = payload.
+__global__ void k_blocks_pack(const float4* __restrict__ src, const int* __restrict__ ids, int n,
+                              int rx, int ry, int rz, int tbx, int tby, float4* __restrict__ out) {
+  const long long total = (long long)n * kBlockVerts * kVec4PerVertex;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(q % kVec4PerVertex);
+    const long long r = q / kVec4PerVertex;
+    const int vl = (int)(r % kBlockVerts), e = (int)(r / kBlockVerts);
+    const int b = ids[e];
+    const long long v = b < 0 ? -1 : block_vertex(b, vl, rx, ry, rz, tbx, tby);
+    out[q] = v < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : src[v * kVec4PerVertex + j];
+  }
+}
+
+__global__ void k_blocks_unpack(float4* __restrict__ dst, const int* __restrict__ ids, int n, int rx,
+                                int ry, int rz, int tbx, int tby, const float4* __restrict__ in) {
+  const long long total = (long long)n * kBlockVerts * kVec4PerVertex;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(q % kVec4PerVertex);
+    const long long r = q / kVec4PerVertex;
+    const int vl = (int)(r % kBlockVerts), e = (int)(r / kBlockVerts);
+    const int b = ids[e];
+    if (b < 0) continue;
+    const long long v = block_vertex(b, vl, rx, ry, rz, tbx, tby);
+    if (v >= 0) dst[v * kVec4PerVertex + j] = in[q];
+  }
+}
+
+// RMSProp (mapping.cpp:218-231) on the vertices of the listed blocks with the
+// packed, rank-reduced gradient; same per-element rule as k_rmsprop.
+__global__ void k_blocks_apply(float4* __restrict__ theta, float4* __restrict__ vstate,
+                               const int* __restrict__ ids, int n, int rx, int ry, int rz, int tbx,
+                               int tby, const float4* __restrict__ packed, double rho,
+                               double lr_sigma, double lr_sh, double eps) {
+  const long long total = (long long)n * kBlockVerts * kVec4PerVertex;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(q % kVec4PerVertex);
+    const long long r = q / kVec4PerVertex;
+    const int vl = (int)(r % kBlockVerts), e = (int)(r / kBlockVerts);
+    const int b = ids[e];
+    if (b < 0) continue;
+    const long long v = block_vertex(b, vl, rx, ry, rz, tbx, tby);
+    if (v < 0) continue;
+    const float4 g4 = packed[q];
+    if (g4.x == 0.f && g4.y == 0.f && g4.z == 0.f && g4.w == 0.f) continue;
+    const long long f = v * kVec4PerVertex + j;
+    float4 th = theta[f], v4 = vstate[f];
+    float* thp = &th.x;
+    float* vp = &v4.x;
+    const float* gp = &g4.x;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double gg = gp[c];
+      if (gg == 0.0) continue;  // mapping.cpp:226
+      const double vn = rho * (double)vp[c] + (1.0 - rho) * gg * gg;
+      const double lr = (4 * j + c == 0) ? lr_sigma : lr_sh;
+      vp[c] = (float)vn;
+      thp[c] = (float)((double)thp[c] - lr * gg / sqrt(vn + eps));
+    }
+    theta[f] = th;
+    vstate[f] = v4;
+  }
+}
+
 // ------------------------------------------------------------------ utilities
 __global__ void k_fill_payload(float* payload, long long nv, float sigma) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nv * kPayload;
@@ -1290,6 +1378,29 @@ void launch_rmsprop_blocks(float4* theta, float4* grad, float4* v, uint32_t* tb,
   k_rmsprop_blocks<<<nb, 256, 0, s>>>(theta, grad, v, tb, rx, ry, rz, tbx, tby, rho, lr_sigma,
                                       lr_sh, eps, stats, touched);
   cudaMemsetAsync(tb, 0, sizeof(uint32_t) * ((nb + 31) / 32 + 1), s);
+}
+void launch_touched_flags(const uint32_t* tb, int nb, uint8_t* flags, cudaStream_t s) {
+  k_touched_flags<<<(nb + 255) / 256, 256, 0, s>>>(tb, nb, flags);
+}
+void launch_blocks_pack(const float4* src, const int* ids, int n, int rx, int ry, int rz, int tbx,
+                        int tby, float4* out, cudaStream_t s) {
+  const long long total = (long long)n * kBlockVerts * kVec4PerVertex;
+  if (total > 0)
+    k_blocks_pack<<<grid_blocks(total, 256), 256, 0, s>>>(src, ids, n, rx, ry, rz, tbx, tby, out);
+}
+void launch_blocks_unpack(float4* dst, const int* ids, int n, int rx, int ry, int rz, int tbx,
+                          int tby, const float4* in, cudaStream_t s) {
+  const long long total = (long long)n * kBlockVerts * kVec4PerVertex;
+  if (total > 0)
+    k_blocks_unpack<<<grid_blocks(total, 256), 256, 0, s>>>(dst, ids, n, rx, ry, rz, tbx, tby, in);
+}
+void launch_blocks_apply(float4* theta, float4* v, const int* ids, int n, int rx, int ry, int rz,
+                         int tbx, int tby, const float4* packed, double rho, double lr_sigma,
+                         double lr_sh, double eps, cudaStream_t s) {
+  const long long total = (long long)n * kBlockVerts * kVec4PerVertex;
+  if (total > 0)
+    k_blocks_apply<<<grid_blocks(total, 256), 256, 0, s>>>(theta, v, ids, n, rx, ry, rz, tbx, tby,
+                                                           packed, rho, lr_sigma, lr_sh, eps);
 }
 void launch_fill_payload(float* payload, long long nv, float sigma, cudaStream_t s) {
   k_fill_payload<<<grid_blocks(nv * kPayload, 256), 256, 0, s>>>(payload, nv, sigma);

@@ -303,6 +303,7 @@ int vrf_mapping_steps(vrf_context* ctx, const vrf_mapping_config* cfg, uint64_t 
   const size_t half = (bbytes + 255) / 256 * 256;
   const size_t need = 2 * half + 2 * 256;
   if (ctx->h_pipe_bytes < need) {
+    CU(cudaStreamSynchronize(ctx->stream));
     if (ctx->h_pipe) CU(cudaFreeHost(ctx->h_pipe));
     ctx->h_pipe = nullptr;
     ctx->h_pipe_bytes = 0;
@@ -455,6 +456,78 @@ int vrf_map_backward(vrf_context* ctx, const vrf_mapping_config* cfg, int32_t ra
     launch_backward_fast(ctx, cfg, p, ctx->last_batch, ctx->last_n, ctx->d_counts);
   CU(cudaGetLastError());
   // the reduce-scatter brings other ranks' gradients: vrf_map_apply scans its shard
+  ctx->touched_valid = false;
+  return VRF_OK;
+}
+
+// ---- block-sparse exchange (distributed.py): 8^3-vertex blocks, packed
+// [n][512][28] fp32 device buffers owned by the caller (the NCCL tensors).
+int vrf_blocks_count(vrf_context* ctx, int32_t* n_blocks) {
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  *n_blocks = ctx->tdim[0] * ctx->tdim[1] * ctx->tdim[2];
+  return VRF_OK;
+}
+
+int vrf_blocks_touched(vrf_context* ctx, uint8_t* flags_dev) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  launch_touched_flags(ctx->tb, ctx->tdim[0] * ctx->tdim[1] * ctx->tdim[2], flags_dev,
+                       ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  return VRF_OK;
+}
+
+int vrf_blocks_pack(vrf_context* ctx, const int32_t* ids_dev, int n, int which, float* out_dev) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if (which != 0 && which != 1)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_blocks_pack: which must be 0 or 1");
+  launch_blocks_pack((const float4*)(which == 0 ? ctx->grad : ctx->payload), ids_dev, n,
+                     ctx->geom.res[0], ctx->geom.res[1], ctx->geom.res[2], ctx->tdim[0],
+                     ctx->tdim[1], (float4*)out_dev, ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  return VRF_OK;
+}
+
+int vrf_blocks_unpack_payload(vrf_context* ctx, const int32_t* ids_dev, int n,
+                              const float* in_dev) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  launch_blocks_unpack((float4*)ctx->payload, ids_dev, n, ctx->geom.res[0], ctx->geom.res[1],
+                       ctx->geom.res[2], ctx->tdim[0], ctx->tdim[1], (const float4*)in_dev,
+                       ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  return VRF_OK;
+}
+
+int vrf_blocks_apply(vrf_context* ctx, const vrf_mapping_config* cfg, const int32_t* ids_dev,
+                     int n, const float* grad_packed_dev) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  launch_blocks_apply((float4*)ctx->payload, (float4*)ctx->rms, ids_dev, n, ctx->geom.res[0],
+                      ctx->geom.res[1], ctx->geom.res[2], ctx->tdim[0], ctx->tdim[1],
+                      (const float4*)grad_packed_dev, cfg->rmsprop_decay, cfg->lr_sigma,
+                      cfg->lr_sh, cfg->rmsprop_eps, ctx->stream);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  return VRF_OK;
+}
+
+int vrf_grad_clear(vrf_context* ctx) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  CU(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * 28 * (size_t)ctx->Vpad, ctx->stream));
+  const long long ntb = (long long)ctx->tdim[0] * ctx->tdim[1] * ctx->tdim[2];
+  CU(cudaMemsetAsync(ctx->tb, 0, sizeof(uint32_t) * ((ntb + 31) / 32 + 1), ctx->stream));
   ctx->touched_valid = false;
   return VRF_OK;
 }

@@ -428,6 +428,7 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
   if (!ctx->d_gn_pose) CU(cudaMalloc(&ctx->d_gn_pose, sizeof(DevPose)));
   if (!ctx->d_gn_seed) CU(cudaMalloc(&ctx->d_gn_seed, sizeof(unsigned long long)));
   if (ctx->gn_hist_cap < iters) {
+    CU(cudaStreamSynchronize(ctx->stream));
     cudaFree(ctx->d_gn_hist);
     CU(cudaMalloc(&ctx->d_gn_hist, sizeof(double) * 2 * iters));
     ctx->gn_hist_cap = iters;

@@ -74,6 +74,33 @@ class GpuEngine:
     def apply(self, v0, v1):
         self.ctx.map_apply(self.cfg, v0, v1)
 
+    # ---- block-sparse exchange (8^3-vertex blocks, packed [n][512][28] fp32)
+    BLOCK_FLOATS = 512 * 28
+
+    @property
+    def n_blocks(self) -> int:
+        return self.ctx.blocks_count()
+
+    def touched_flags(self):
+        f = torch.empty(self.n_blocks, dtype=torch.uint8, device=self.grad.device)
+        self.ctx.blocks_touched(f.data_ptr())
+        return f
+
+    def pack(self, ids, which):
+        out = torch.empty(ids.numel() * self.BLOCK_FLOATS, dtype=torch.float32,
+                          device=self.grad.device)
+        self.ctx.blocks_pack(ids.data_ptr(), ids.numel(), which, out.data_ptr())
+        return out
+
+    def apply_blocks(self, ids, packed_grad):
+        self.ctx.blocks_apply(self.cfg, ids.data_ptr(), ids.numel(), packed_grad.data_ptr())
+
+    def unpack_payload(self, ids, packed):
+        self.ctx.blocks_unpack_payload(ids.data_ptr(), ids.numel(), packed.data_ptr())
+
+    def clear_grad(self):
+        self.ctx.grad_clear()
+
 
 class DistributedMapper:
     def __init__(self, engine, group=None):
@@ -86,7 +113,10 @@ class DistributedMapper:
                                  device=engine.grad.device)
         self._rs = hasattr(dist, "reduce_scatter_tensor") and dist.get_backend(group) == "nccl"
 
-    def step(self, batch, lambda_d: float) -> StepResult:
+    def step(self, batch, lambda_d: float, sparse: bool = False) -> StepResult:
+        """One ray-sharded mapping step. sparse: exchange only the 8^3-vertex
+        blocks some rank touched (block-sparse reduce-scatter / all-gather, see
+        _exchange_sparse); otherwise the dense reduce-scatter / all-gather."""
         m_c, m_d, bad, lp, lg, samples = self.e.forward(batch)
         dev = self.e.grad.device
         ints = torch.tensor([m_c, m_d, 1 if bad >= 0 else 0, samples], dtype=torch.int64,
@@ -100,7 +130,20 @@ class DistributedMapper:
         if n_bad:
             raise RuntimeError("mapping_step: non-finite loss")
         self.e.backward(M_c, M_d)
+        if sparse:
+            self._exchange_sparse()
+        else:
+            self._exchange_dense()
+        lp_sum, lg_sum = flts.tolist()
+        l_p = lp_sum / M_c
+        l_g = lg_sum / M_d if M_d > 0 else 0.0
+        return StepResult(l_p, l_g, l_p + lambda_d * l_g, M_c, M_d, S)
+
+    def _exchange_dense(self):
         s0, s1 = self.v0 * 28, self.v1 * 28
+        if self.world == 1:  # the local gradient is the global one: apply in place
+            self.e.apply(self.v0, self.v1)
+            return
         if self._rs:
             dist.reduce_scatter_tensor(self.shard, self.e.grad, group=self.group)
         else:  # gloo has no reduce-scatter: all-reduce and keep the owned slice
@@ -116,7 +159,43 @@ class DistributedMapper:
             parts = list(self.e.payload.view(self.world, -1).unbind(0))
             dist.all_gather(parts, mine, group=self.group)
             self.e.payload.copy_(torch.cat(parts))
-        lp_sum, lg_sum = flts.tolist()
-        l_p = lp_sum / M_c
-        l_g = lg_sum / M_d if M_d > 0 else 0.0
-        return StepResult(l_p, l_g, l_p + lambda_d * l_g, M_c, M_d, S)
+
+    def _exchange_sparse(self):
+        """Block-sparse exchange. Blocks have a STATIC owner (id % world), so each
+        block's RMSProp state lives on one rank across steps. The touched flags
+        are max-all-reduced (same list on every rank); each owner's touched blocks
+        are padded to the largest owner count M so the packed gradient
+        [world][M][512][28] reduce-scatters into equal shards; the owner applies
+        RMSProp to its M blocks and the updated payload blocks are all-gathered
+        and unpacked everywhere. Untouched blocks have zero gradient on every
+        rank, so the result equals the dense exchange."""
+        flags = self.e.touched_flags()
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=self.group)
+        ids = torch.nonzero(flags).flatten().to(torch.int32)
+        dev = flags.device
+        groups = [ids[(ids % self.world) == r] for r in range(self.world)]
+        M = max(int(g.numel()) for g in groups)
+        if M > 0:
+            pad = torch.full((self.world, M), -1, dtype=torch.int32, device=dev)
+            for r, g in enumerate(groups):
+                pad[r, : g.numel()] = g
+            all_ids = pad.flatten().contiguous()
+            mine_ids = pad[self.rank].contiguous()
+            packed = self.e.pack(all_ids, 0)
+            shard = torch.empty(M * self.e.BLOCK_FLOATS, dtype=packed.dtype, device=dev)
+            if self._rs:
+                dist.reduce_scatter_tensor(shard, packed, group=self.group)
+            else:
+                dist.all_reduce(packed, group=self.group)
+                shard.copy_(packed.view(self.world, -1)[self.rank])
+            self.e.apply_blocks(mine_ids, shard)
+            theta = self.e.pack(mine_ids, 1)
+            gathered = torch.empty(self.world * theta.numel(), dtype=theta.dtype, device=dev)
+            if hasattr(dist, "all_gather_into_tensor") and dist.get_backend(self.group) == "nccl":
+                dist.all_gather_into_tensor(gathered, theta, group=self.group)
+            else:
+                parts = list(gathered.view(self.world, -1).unbind(0))
+                dist.all_gather(parts, theta, group=self.group)
+                gathered = torch.cat(parts)
+            self.e.unpack_payload(all_ids, gathered)
+        self.e.clear_grad()

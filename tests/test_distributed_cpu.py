@@ -76,8 +76,86 @@ class OracleEngine:
         th[nz] = th[nz] - lr[nz] * g[nz] / torch.sqrt(v[nz] + self.cfg.rmsprop_eps)
         self.grad[v0 * 28: v1 * 28] = 0.0
 
+    # ---- block-sparse exchange: 8^3-vertex blocks, packed [n][512][28]
+    BLOCK_FLOATS = 512 * 28
 
-def _worker(rank, world, port, out_dir):
+    def _block_vertices(self):
+        if not hasattr(self, "_bv"):
+            rx, ry, rz = self.grid.geom.res
+            tb = [(r + 7) // 8 for r in (rx, ry, rz)]
+            nb = tb[0] * tb[1] * tb[2]
+            vl = np.arange(512)
+            lx, ly, lz = vl % 8, (vl // 8) % 8, vl // 64
+            b = np.arange(nb)
+            bx, by, bz = b % tb[0], (b // tb[0]) % tb[1], b // (tb[0] * tb[1])
+            x = bx[:, None] * 8 + lx[None]
+            y = by[:, None] * 8 + ly[None]
+            z = bz[:, None] * 8 + lz[None]
+            inside = (x < rx) & (y < ry) & (z < rz)
+            self._bv = np.where(inside, x + rx * (y + ry * z), -1)
+        return self._bv
+
+    @property
+    def n_blocks(self):
+        return self._block_vertices().shape[0]
+
+    def touched_flags(self):
+        bv = self._block_vertices()
+        g = self.grad[: self.num_vertices * 28].view(-1, 28).abs().sum(1).numpy() != 0
+        gv = np.concatenate([g, [False]])  # index -1 -> False
+        return torch.from_numpy(gv[bv].any(1).astype(np.uint8))
+
+    def pack(self, ids, which):
+        src = (self.grad if which == 0 else self.payload)[: self.num_vertices * 28].view(-1, 28)
+        bv = self._block_vertices()
+        out = torch.zeros(ids.numel(), 512, 28, dtype=src.dtype)
+        for e, b in enumerate(ids.tolist()):
+            if b < 0:
+                continue
+            v = torch.from_numpy(bv[b])
+            ok = v >= 0
+            out[e, ok] = src[v[ok]]
+        return out.flatten()
+
+    def apply_blocks(self, ids, packed):
+        bv = self._block_vertices()
+        pk = packed.view(-1, 512, 28)
+        th = self.payload[: self.num_vertices * 28].view(-1, 28)
+        vv = self.v[: self.num_vertices * 28].view(-1, 28)
+        lr = torch.full((28,), self.cfg.lr_sh, dtype=torch.float64)
+        lr[0] = self.cfg.lr_sigma
+        rho = self.cfg.rmsprop_decay
+        for e, b in enumerate(ids.tolist()):
+            if b < 0:
+                continue
+            v = torch.from_numpy(bv[b])
+            ok = v >= 0
+            g = pk[e, ok]
+            rows = v[ok]
+            nz = g != 0
+            vn = rho * vv[rows] + (1.0 - rho) * g * g
+            vnew = torch.where(nz, vn, vv[rows])
+            tnew = torch.where(nz, th[rows] - lr * g / torch.sqrt(vnew + self.cfg.rmsprop_eps),
+                               th[rows])
+            vv[rows] = vnew
+            th[rows] = tnew
+
+    def unpack_payload(self, ids, packed):
+        bv = self._block_vertices()
+        pk = packed.view(-1, 512, 28)
+        th = self.payload[: self.num_vertices * 28].view(-1, 28)
+        for e, b in enumerate(ids.tolist()):
+            if b < 0:
+                continue
+            v = torch.from_numpy(bv[b])
+            ok = v >= 0
+            th[v[ok]] = pk[e, ok]
+
+    def clear_grad(self):
+        self.grad.zero_()
+
+
+def _worker(rank, world, port, out_dir, sparse=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -94,7 +172,7 @@ def _worker(rank, world, port, out_dir):
     full = orc.Oracle().draw_batch(31, len(frames), intr.width, intr.height, 400)
     mine = torch.from_numpy(np.array_split(full, world)[rank].copy())
     eng = OracleEngine(g0, frames, intr, cfg, world)
-    res = DistributedMapper(eng).step(mine, cfg.lambda_d)
+    res = DistributedMapper(eng).step(mine, cfg.lambda_d, sparse=sparse)
     if rank == 0:
         np.save(Path(out_dir) / "dist_payload.npy", eng.payload[: eng.num_vertices * 28].numpy())
         np.save(Path(out_dir) / "dist_stats.npy",
@@ -103,8 +181,11 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_ray_sharded_step_equals_single_process(tmp_path, oracle):
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+@pytest.mark.parametrize("sparse", [False, True])
+def test_ray_sharded_step_equals_single_process(tmp_path, oracle, sparse):
+    """Dense exchange, and the block-sparse one (touched 8^3-vertex blocks with
+    static owners): both equal the single-process step."""
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), sparse), nprocs=2, join=True)
     from paper_2307_03404_b200.api import MappingConfig
     from scenes import fresh_grid, room_scene
 

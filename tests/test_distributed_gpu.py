@@ -28,7 +28,8 @@ def _port():
     return p
 
 
-def test_nccl_world1_step_equals_single_gpu_step(oracle):
+@pytest.mark.parametrize("sparse", [False, True])
+def test_nccl_world1_step_equals_single_gpu_step(oracle, sparse):
     grid, intr, frames = room_scene()
     g0 = fresh_grid(grid)
     cfg = MappingConfig()
@@ -44,7 +45,10 @@ def test_nccl_world1_step_equals_single_gpu_step(oracle):
         a.load_frames(intr, frames)
         a.rmsprop_reset()
         mapper = DistributedMapper(GpuEngine(a, cfg))
-        res = mapper.step(torch.from_numpy(batch).cuda(), cfg.lambda_d)
+        res = mapper.step(torch.from_numpy(batch).cuda(), cfg.lambda_d, sparse=sparse)
+        # a second step: the RMSProp state carried on the block owners
+        res = mapper.step(torch.from_numpy(batch[::-1].copy()).cuda(), cfg.lambda_d,
+                          sparse=sparse)
         torch.cuda.synchronize()
         got = a.download_grid().data
 
@@ -52,11 +56,13 @@ def test_nccl_world1_step_equals_single_gpu_step(oracle):
         b.load_grid(g0)
         b.load_frames(intr, frames)
         b.rmsprop_reset()
-        st = b.mapping_step(cfg, batch)
+        b.mapping_step(cfg, batch)
+        st = b.mapping_step(cfg, batch[::-1].copy())
         want = b.download_grid().data
     finally:
         dist.destroy_process_group()
     assert res.rays_color == st.rays_color and res.rays_depth == st.rays_depth
     assert res.samples == st.samples
-    assert abs(res.loss_total - st.loss_total) <= 1e-9 * st.loss_total
+    # two steps: the first update carries fp32 atomics-order noise into the second loss
+    assert abs(res.loss_total - st.loss_total) <= 1e-6 * st.loss_total
     np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
