@@ -63,7 +63,11 @@ class SlamSystem:
 
     def _map(self, steps: int):
         m = self.cfg.mapping
-        w = self.n_keyframes if self.cfg.window <= 0 else min(self.cfg.window, self.n_keyframes)
+        if self.cfg.window <= 0 or self.cfg.window >= self.n_keyframes:
+            # all keyframes: map_scene's pipelined inner loop (host draws overlap steps)
+            self.ctx.mapping_steps(m, self.rng, self.n_keyframes, steps)
+            return
+        w = self.cfg.window
         first = self.n_keyframes - w
         for _ in range(steps):
             batch = self.rng.draw_batch(w, self.intr.width, self.intr.height, m.rays_per_batch)

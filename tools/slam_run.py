@@ -32,8 +32,8 @@ def main():
     ap.add_argument("--width", type=int, default=1200)
     ap.add_argument("--height", type=int, default=680)
     ap.add_argument("--stride", type=int, default=10)
-    ap.add_argument("--map-steps", type=int, default=100)
-    ap.add_argument("--map-rays", type=int, default=16384)
+    ap.add_argument("--map-steps", type=int, default=25)
+    ap.add_argument("--map-rays", type=int, default=65536)
     ap.add_argument("--bootstrap", type=int, default=3000)
     ap.add_argument("--track-rays", type=int, default=16384)
     ap.add_argument("--track-iters", type=int, default=10)

@@ -24,15 +24,16 @@ if "--smi" in sys.argv:
                            stdout=subprocess.DEVNULL)
 cfg = MappingConfig()
 rng = Rng(1)
-bs = [torch.from_numpy(rng.draw_batch(10, 1200, 680, 1 << 20)).cuda() for _ in range(8)]
-for i in range(3): ctx.mapping_step_device(cfg, bs[i].data_ptr(), 1 << 20)
+NR = int(os.environ.get("RAYS", 1 << 20))
+bs = [torch.from_numpy(rng.draw_batch(10, 1200, 680, NR)).cuda() for _ in range(8)]
+for i in range(3): ctx.mapping_step_device(cfg, bs[i].data_ptr(), NR)
 torch.cuda.synchronize()
 ctx.profile_enable(True)
 t0 = time.perf_counter()
 tt = []
 for i in range(3, 8):
     a = time.perf_counter()
-    ctx.mapping_step_device(cfg, bs[i].data_ptr(), 1 << 20)
+    ctx.mapping_step_device(cfg, bs[i].data_ptr(), NR)
     tt.append(time.perf_counter() - a)
 torch.cuda.synchronize()
 dt = time.perf_counter() - t0
@@ -42,7 +43,7 @@ print({k: (round(v[0] / 5, 3) if isinstance(v, tuple) else v) for k, v in pr.ite
 ctx.profile_enable(False)
 t0 = time.perf_counter()
 for i in range(3, 8):
-    ctx.mapping_step_device(cfg, bs[i].data_ptr(), 1 << 20)
+    ctx.mapping_step_device(cfg, bs[i].data_ptr(), NR)
 torch.cuda.synchronize()
 print("wall per step ms, profiling off", 1e3 * (time.perf_counter() - t0) / 5)
 if smi:
