@@ -499,9 +499,20 @@ def run_ours(args):
         tp = gt_ctx.profile_read()
         gt_ctx.profile_enable(False)
         nf = len(tframes) - 1
+        g_ms = tp["pose_backward"][0]  # the GN CUDA graphs, CUDA events
+        t_samples = tp.get("track_samples", 0)
+        t_rays = nf * gn.iterations * gn.rays_per_iteration
+        # SURVEY.md 8d tracking bytes: 896 B per composited sample + 32 B per ray
+        t_bytes = 896.0 * t_samples + 32.0 * t_rays
+        t_gbps = t_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else 0.0
         tracking = {"config": "config2: 1200x680, 257^3 map, GN/LM 16384 rays x 10 it",
                     "frames_per_s": nf / dt, "ms_per_frame": 1e3 * dt / nf,
-                    "kernel_ms_per_frame": tp["pose_backward"][0] / nf,  # the GN CUDA graph
+                    "kernel_ms_per_frame": g_ms / nf,
+                    "rays_per_s": t_rays / (g_ms / 1e3) if g_ms > 0 else None,
+                    "samples_per_s": t_samples / (g_ms / 1e3) if g_ms > 0 else None,
+                    "roofline": {"bound": "hbm", "achieved": t_gbps, "peak": peak,
+                                 "unit": "GB/s", "frac": t_gbps / peak,
+                                 "kernel": "k_pose_group (GN graph)"},
                     "ate_rmse_m": float(np.sqrt(np.mean(np.square(errs))))}
 
     # ---- CPU baseline (rank 0, N=1)

@@ -185,6 +185,8 @@ int vrf_profile_enable(vrf_context* ctx, int on);
 int vrf_profile_read(vrf_context* ctx, int slot, double* ms, int64_t* launches);
 /* float4 parameter groups RMSProp updated since vrf_profile_enable (96 B each). */
 int64_t vrf_profile_touched_groups(vrf_context* ctx);
+/* Composited samples of the Gauss-Newton tracking frames since vrf_profile_enable. */
+int64_t vrf_profile_track_samples(vrf_context* ctx);
 
 /* ---- grid: VoxelGrid (voxel_grid.hpp:112-175) */
 /* VoxelGrid(geom, sigma_init) — voxel_grid.cpp:74-81 (all cells active). */

@@ -109,6 +109,7 @@ _SIGS = {
     "vrf_profile_enable": (C.c_int, [vp, C.c_int]),
     "vrf_profile_read": (C.c_int, [vp, C.c_int, P(C.c_double), P(C.c_int64)]),
     "vrf_profile_touched_groups": (C.c_int64, [vp]),
+    "vrf_profile_track_samples": (C.c_int64, [vp]),
     "vrf_grid_init": (C.c_int, [vp, P(GridGeometry_c), C.c_double]),
     "vrf_grid_fill": (C.c_int, [vp, C.c_double]),
     "vrf_grid_upload": (C.c_int, [vp, P(GridGeometry_c), vp, vp]),

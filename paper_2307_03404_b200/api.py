@@ -415,6 +415,7 @@ class Context:
             self._check(self._lib.vrf_profile_read(self._h, i, C.byref(ms), C.byref(n)))
             out[name] = (ms.value, n.value)
         out["touched_groups"] = int(self._lib.vrf_profile_touched_groups(self._h))
+        out["track_samples"] = int(self._lib.vrf_profile_track_samples(self._h))
         return out
 
     def set_stream(self, stream_ptr: int):

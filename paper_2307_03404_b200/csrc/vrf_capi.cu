@@ -108,8 +108,11 @@ int vrf_profile_enable(vrf_context* ctx, int on) {
   CU(cudaMemsetAsync(ctx->d_touched, 0, sizeof(unsigned long long), ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->profiling = on != 0;
+  ctx->prof_track_samples = 0;
   return VRF_OK;
 }
+
+int64_t vrf_profile_track_samples(vrf_context* ctx) { return ctx->prof_track_samples; }
 
 int vrf_profile_read(vrf_context* ctx, int slot, double* ms, int64_t* launches) {
   if (slot < 0 || slot >= 8) return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "profile slot");

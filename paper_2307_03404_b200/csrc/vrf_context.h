@@ -90,6 +90,7 @@ struct vrf_context {
   long long prof_launches[8] = {0};
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   unsigned long long* d_touched = nullptr;  // RMSProp float4 groups updated
+  long long prof_track_samples = 0;          // composited samples of GN tracking frames
 
   // warp-per-ray fast path: ray work queues (forward, backward) and ray order
   int* d_queue = nullptr;

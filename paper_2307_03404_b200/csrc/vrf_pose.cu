@@ -430,7 +430,7 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
   if (ctx->gn_hist_cap < iters) {
     CU(cudaStreamSynchronize(ctx->stream));
     cudaFree(ctx->d_gn_hist);
-    CU(cudaMalloc(&ctx->d_gn_hist, sizeof(double) * 2 * iters));
+    CU(cudaMalloc(&ctx->d_gn_hist, sizeof(double) * 3 * iters));
     ctx->gn_hist_cap = iters;
     if (ctx->gn_graph) cudaGraphExecDestroy(ctx->gn_graph);
     ctx->gn_graph = nullptr;
@@ -481,7 +481,7 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
     ctx->gn_key = key;
   }
   // per-frame inputs: init pose, frame index, seed
-  if ((rc = ensure_pinned(ctx, sizeof(DevPose) + 16 + sizeof(double) * 2 * iters))) return rc;
+  if ((rc = ensure_pinned(ctx, sizeof(DevPose) + 16 + sizeof(double) * 3 * iters))) return rc;
   char* h = (char*)ctx->h_pinned;
   const DevPose dp = dev_pose(init);
   const unsigned long long seed = cfg->seed ^ (0x9e3779b97f4a7c15ULL * (unsigned long long)(frame + 1));
@@ -501,7 +501,7 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
   DevPose fin;
   double* hist = (double*)(h + sizeof(DevPose) + 16);
   CU(cudaMemcpyAsync(&fin, ctx->d_gn_pose, sizeof(DevPose), cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaMemcpyAsync(hist, ctx->d_gn_hist, sizeof(double) * 2 * iters, cudaMemcpyDeviceToHost,
+  CU(cudaMemcpyAsync(hist, ctx->d_gn_hist, sizeof(double) * 3 * iters, cudaMemcpyDeviceToHost,
                      ctx->stream));
   if ((rc = check_err_flag(ctx))) return rc;  // syncs the stream
   prof_collect(ctx);
@@ -510,7 +510,9 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
   for (int a = 0; a < 4; ++a) res.pose.q[a] = fin.q[a];
   for (int a = 0; a < 3; ++a) res.pose.t[a] = fin.t[a];
   res.iterations_run = iters;
-  res.final_loss = hist[2 * (iters - 1)];
+  res.final_loss = hist[3 * (iters - 1)];
+  if (ctx->profiling)  // composited samples of the frame's iterations (bench roofline)
+    for (int it = 0; it < iters; ++it) ctx->prof_track_samples += (long long)hist[3 * it + 2];
   *out = res;
   return VRF_OK;
 }

@@ -622,8 +622,9 @@ __global__ void k_gn_step(const PosePartial* __restrict__ ne, DevPose* pose, dou
                           double* hist, int iteration) {
   if (threadIdx.x != 0) return;
   const PosePartial r = *ne;
-  hist[2 * iteration] = r.m > 0 ? r.loss / r.m : 0.0;
-  hist[2 * iteration + 1] = r.m;
+  hist[3 * iteration] = r.m > 0 ? r.loss / r.m : 0.0;
+  hist[3 * iteration + 1] = r.m;
+  hist[3 * iteration + 2] = (double)r.samples;
   if (r.m == 0) return;
   double A[6][6];
   int idx = 0;
