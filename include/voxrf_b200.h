@@ -228,6 +228,12 @@ int vrf_frames_reserve(vrf_context* ctx, const vrf_intrinsics* intr, int capacit
 int vrf_frame_set(vrf_context* ctx, int slot, const double* color, const double* depth,
                   const vrf_pose* pose);
 int vrf_frame_set_pose(vrf_context* ctx, int slot, const vrf_pose* pose);
+/* vrf_frame_set from the sensor format the reference's dataset stores (8-bit RGB
+ * H*W*3, 16-bit depth units H*W; image.cpp:53-55, 79): converted on the device as
+ * colour / 255.0 and depth / intrinsics.depth_scale — 5 B/pixel over PCIe
+ * instead of 32. */
+int vrf_frame_set_u8u16(vrf_context* ctx, int slot, const uint8_t* rgb, const uint16_t* depth,
+                        const vrf_pose* pose);
 
 /* ---- renderer: render_image — renderer.hpp:83-84 (renderer.cpp:149-174).
  * color: ceil(H/stride)*ceil(W/stride)*3, depth: ceil(H/stride)*ceil(W/stride). */

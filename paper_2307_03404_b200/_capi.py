@@ -126,6 +126,7 @@ _SIGS = {
     "vrf_frames_reserve": (C.c_int, [vp, P(Intrinsics_c), C.c_int]),
     "vrf_frame_set": (C.c_int, [vp, C.c_int, vp, vp, P(Pose_c)]),
     "vrf_frame_set_pose": (C.c_int, [vp, C.c_int, P(Pose_c)]),
+    "vrf_frame_set_u8u16": (C.c_int, [vp, C.c_int, vp, vp, P(Pose_c)]),
     "vrf_render_image": (C.c_int, [vp, P(Intrinsics_c), P(Pose_c), P(RenderParams_c), C.c_int,
                                    vp, vp]),
     "vrf_mapping_step": (C.c_int, [vp, P(MappingConfig_c), vp, C.c_int, P(MapStepStats_c)]),

@@ -188,6 +188,10 @@ class Frame:
     depth: np.ndarray
     timestamp: float = 0.0
     gt_pose: Optional[Pose] = None
+    # optional sensor-format copies (8-bit RGB, 16-bit depth units) for the cheap
+    # upload path (Context.set_frame_u8u16)
+    color_u8: Optional[np.ndarray] = None
+    depth_u16: Optional[np.ndarray] = None
 
     def depth_valid(self, x: int, y: int) -> bool:
         return bool(self.depth[y, x] > 0.0)
@@ -523,6 +527,20 @@ class Context:
             raise ValueError("frame size does not match the intrinsics")
         pc = (pose or frame.gt_pose or Pose())._c()
         self._check(self._lib.vrf_frame_set(self._h, int(slot), _ptr(c_), _ptr(d_), C.byref(pc)))
+        self.n_frames = max(self.n_frames, int(slot) + 1)
+
+    def set_frame_u8u16(self, slot: int, rgb: np.ndarray, depth_units: np.ndarray,
+                        pose: Pose):
+        """Write one frame slot from sensor data: uint8 RGB (H, W, 3) and uint16 depth
+        units (H, W), converted on the device like the reference's PNG loaders."""
+        h, w = self.intrinsics.height, self.intrinsics.width
+        c_ = np.ascontiguousarray(rgb, dtype=np.uint8)
+        d_ = np.ascontiguousarray(depth_units, dtype=np.uint16)
+        if c_.shape != (h, w, 3) or d_.shape != (h, w):
+            raise ValueError("frame size does not match the intrinsics")
+        pc = pose._c()
+        self._check(self._lib.vrf_frame_set_u8u16(self._h, int(slot), _ptr(c_), _ptr(d_),
+                                                  C.byref(pc)))
         self.n_frames = max(self.n_frames, int(slot) + 1)
 
     def set_frame_pose(self, slot: int, pose: Pose):

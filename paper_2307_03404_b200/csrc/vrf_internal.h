@@ -147,6 +147,9 @@ void launch_pack_frames(const double* color, const double* depth, double4* rgbd,
                         cudaStream_t s);
 void launch_prune(const DevGrid& g, uint32_t* occ_bits, double tau, unsigned long long* count,
                   cudaStream_t s);
+void launch_pack_frames_u8(const uint8_t* rgb, const uint16_t* depth, double depth_scale,
+                           double4* rgbd, long long npix, cudaStream_t s);
+void launch_extract_depth(const double4* rgbd, double* out, long long npix, cudaStream_t s);
 void launch_upsample(const DevGrid& coarse, int frx, int fry, int frz, float* fine,
                      uint32_t* fine_occ, cudaStream_t s);
 // Superblock bit = OR of its (up to) 8^3 block bits.

@@ -1094,6 +1094,24 @@ __global__ void k_pack_frames(const double* color, const double* depth, double4*
        q += (long long)gridDim.x * blockDim.x)
     rgbd[q] = make_double4(color[3 * q], color[3 * q + 1], color[3 * q + 2], depth[q]);
 }
+// Sensor-format frame (8-bit RGB, 16-bit depth units), converted exactly as the
+// reference's PNG loaders do (image.cpp:53-55 colour / 255.0, :79 depth /
+// depth_scale; IEEE double division).
+__global__ void k_pack_frames_u8(const uint8_t* __restrict__ rgb, const uint16_t* __restrict__ d,
+                                 double depth_scale, double4* rgbd, long long npix) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < npix;
+       q += (long long)gridDim.x * blockDim.x)
+    rgbd[q] = make_double4(__ddiv_rn((double)rgb[3 * q], 255.0),
+                           __ddiv_rn((double)rgb[3 * q + 1], 255.0),
+                           __ddiv_rn((double)rgb[3 * q + 2], 255.0),
+                           __ddiv_rn((double)d[q], depth_scale));
+}
+__global__ void k_extract_depth(const double4* __restrict__ rgbd, double* __restrict__ out,
+                                long long npix) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < npix;
+       q += (long long)gridDim.x * blockDim.x)
+    out[q] = rgbd[q].w;
+}
 // VoxelGrid::prune — voxel_grid.cpp:169-188 (peak of max(sigma,0) over 8 corners < tau).
 __global__ void k_prune(DevGrid g, uint32_t* bits, double tau, unsigned long long* count) {
   const long long n_cells = (long long)(g.rx - 1) * (g.ry - 1) * (g.rz - 1);
@@ -1423,6 +1441,14 @@ void launch_unpack_occupancy(const uint32_t* bits, uint8_t* occ, long long n_cel
 void launch_pack_frames(const double* color, const double* depth, double4* rgbd, long long npix,
                         cudaStream_t s) {
   if (npix) k_pack_frames<<<grid_blocks(npix, 256), 256, 0, s>>>(color, depth, rgbd, npix);
+}
+void launch_pack_frames_u8(const uint8_t* rgb, const uint16_t* depth, double depth_scale,
+                           double4* rgbd, long long npix, cudaStream_t s) {
+  if (npix)
+    k_pack_frames_u8<<<grid_blocks(npix, 256), 256, 0, s>>>(rgb, depth, depth_scale, rgbd, npix);
+}
+void launch_extract_depth(const double4* rgbd, double* out, long long npix, cudaStream_t s) {
+  if (npix) k_extract_depth<<<grid_blocks(npix, 256), 256, 0, s>>>(rgbd, out, npix);
 }
 void launch_upsample(const DevGrid& coarse, int frx, int fry, int frz, float* fine,
                      uint32_t* fine_occ, cudaStream_t s) {

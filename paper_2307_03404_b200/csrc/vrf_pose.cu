@@ -321,7 +321,18 @@ int vrf_track_frame(vrf_context* ctx, int frame, const vrf_intrinsics* intr, con
   if (cfg->iterations == 0) return VRF_OK;
   if (frame < 0 || frame >= ctx->n_frames)
     return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "track_frame: frame index out of range");
-  const std::vector<double>& depth = ctx->host_depth[frame];
+  std::vector<double>& depth = ctx->host_depth[frame];
+  if (depth.empty()) {  // frame written in sensor format: fetch its depth channel once
+    const long long npix = (long long)ctx->fintr.width * ctx->fintr.height;
+    int rc2 = ensure(ctx, ctx->s_out, sizeof(double) * (size_t)npix);
+    if (rc2) return rc2;
+    launch_extract_depth(ctx->rgbd + npix * frame, (double*)ctx->s_out.ptr, npix, ctx->stream);
+    LAUNCHED(1);
+    depth.resize((size_t)npix);
+    CU(cudaMemcpyAsync(depth.data(), ctx->s_out.ptr, sizeof(double) * (size_t)npix,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
   Xoshiro rng(cfg->seed);
   vrf_pose pose = *init, best_pose = *init;
   double best_loss = INFINITY, initial_loss = 0.0;

@@ -74,10 +74,16 @@ class SlamSystem:
             batch[:, 0] += first  # keyframe slots [first, n_keyframes)
             self.ctx.mapping_step(m, batch)
 
+    def _put(self, slot: int, frame: Frame, pose: Pose):
+        if frame.color_u8 is not None and frame.depth_u16 is not None:
+            self.ctx.set_frame_u8u16(slot, frame.color_u8, frame.depth_u16, pose)  # 5 B/px
+        else:
+            self.ctx.set_frame(slot, frame, pose)
+
     def _add_keyframe(self, frame: Frame, pose: Pose):
         if self.n_keyframes >= self.cfg.max_keyframes:
             raise RuntimeError("slam: keyframe capacity exhausted")
-        self.ctx.set_frame(self.n_keyframes, frame, pose)
+        self._put(self.n_keyframes, frame, pose)
         self.n_keyframes += 1
 
     def process(self, frame: Frame, init_pose: Optional[Pose] = None) -> Pose:
@@ -99,7 +105,7 @@ class SlamSystem:
         init = prev
         if self.cfg.constant_velocity and i >= 2:
             init = pose_compose(prev, pose_compose(pose_inverse(self.poses[-2]), prev))
-        self.ctx.set_frame(self.track_slot, frame, init)
+        self._put(self.track_slot, frame, init)
         r = self.ctx.track_frame_gn(self.track_slot, self.intr, init, self.cfg.tracking)
         pose = r.pose
         t1 = time.perf_counter()

@@ -219,6 +219,16 @@ def quantize_frame(color: np.ndarray, depth: np.ndarray, depth_scale: float):
     return c8, du / depth_scale
 
 
+def sensor_frame(color: np.ndarray, depth: np.ndarray, depth_scale: float, timestamp=0.0,
+                 pose=None) -> Frame:
+    """A Frame as an RGB-D sensor / the reference's PNG dataset delivers it: 8-bit
+    colour and 16-bit depth units (image.cpp:13-30), plus the decoded doubles."""
+    c8 = np.clip(np.floor(color * 255.0 + 0.5), 0, 255).astype(np.uint8)
+    du = np.where(depth > 0, np.clip(np.floor(depth * depth_scale + 0.5), 0, 65535),
+                  0).astype(np.uint16)
+    return Frame(c8 / 255.0, du / depth_scale, timestamp, pose, c8, du)
+
+
 def replica_intrinsics() -> CameraIntrinsics:
     return CameraIntrinsics(600.0, 600.0, 599.5, 339.5, 1200, 680, 6553.5)
 

@@ -453,3 +453,24 @@ np.save(sys.argv[1], ctx.download_payload_f32())
         outs.append(np.load(f))
     a, b = outs
     assert np.max(np.abs(a - b)) <= 1e-4 * np.max(np.abs(b))
+
+
+def test_sensor_format_frames_equal_the_double_path(ctx, oracle):
+    """vrf_frame_set_u8u16 (8-bit RGB, 16-bit depth) converts exactly like the
+    reference's PNG loaders: tracking on it equals tracking on the double frame
+    (including the Adam path's host depth, fetched back from the device)."""
+    from paper_2307_03404_b200.api import TrackingConfig
+    grid, intr, frames = room_scene()
+    ctx.load_grid(grid)
+    ctx.reserve_frames(intr, 2)
+    f = frames[1]
+    rgb = np.clip(np.floor(f.color * 255.0 + 0.5), 0, 255).astype(np.uint8)
+    du = np.where(f.depth > 0, np.floor(f.depth * intr.depth_scale + 0.5), 0).astype(np.uint16)
+    ctx.set_frame(0, f, f.gt_pose)
+    ctx.set_frame_u8u16(1, rgb, du, f.gt_pose)
+    cfg = TrackingConfig(rays_per_iteration=256, iterations=5)
+    init = frames[0].gt_pose
+    a = ctx.track_frame(0, intr, init, cfg)
+    b = ctx.track_frame(1, intr, init, cfg)
+    assert np.array_equal(np.asarray(a.pose.t), np.asarray(b.pose.t))
+    assert a.loss_trace == b.loss_trace

@@ -59,8 +59,7 @@ def main():
 
     def frame(i):
         img = sensor.render_image(intr, poses[i])
-        c, d = synth.quantize_frame(img.color, img.depth, intr.depth_scale)
-        return Frame(c, d, ts[i], poses[i])
+        return synth.sensor_frame(img.color, img.depth, intr.depth_scale, ts[i], poses[i])
 
     geom = GridGeometry(gt.geom.res, gt.geom.origin, gt.geom.voxel_size)
     cfg = SlamConfig(keyframe_stride=args.stride, map_steps=args.map_steps, window=args.window,
