@@ -540,7 +540,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32",
             "data": "synthetic",
             "config": {"workload": WORKLOAD4 if args.config == 4 else WORKLOAD,
                        "rays_per_step_per_gpu": args.rays,
