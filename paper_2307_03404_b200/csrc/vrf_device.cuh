@@ -72,14 +72,20 @@ __device__ __forceinline__ void mark_touched(const DevGrid& g, int cx, int cy, i
   const int bx = cx >> kTouchLog2, by = cy >> kTouchLog2, bz = cz >> kTouchLog2;
   const int ex = (cx & M) == M, ey = (cy & M) == M, ez = (cz & M) == M;
   const int id = bx + g.tbx * (by + g.tby * bz);
-  if (!(ex | ey | ez) && id == last) return;
-  last = (ex | ey | ez) ? -1 : id;
+  // a cell on the +x/+y/+z face layer of its block also owns vertices of the
+  // next block(s): the key carries the edge flags, so runs of cells in the same
+  // (block, face layer) are marked once
+  const int key = (id << 3) | ex | (ey << 1) | (ez << 2);
+  if (key == last) return;
+  last = key;
   for (int dz = 0; dz <= ez; ++dz)
     for (int dy = 0; dy <= ey; ++dy)
       for (int dx = 0; dx <= ex; ++dx) {
         const int b = (bx + dx) + g.tbx * ((by + dy) + g.tby * (bz + dz));
         const uint32_t bit = 1u << (b & 31);
-        if (!(*((volatile uint32_t*)g.tb + (b >> 5)) & bit)) atomicOr(g.tb + (b >> 5), bit);
+        // L1-cached check: bits are only ever set during the pass, so a stale
+        // word can only cost a redundant atomicOr, never a missed mark
+        if (!(__ldca(g.tb + (b >> 5)) & bit)) atomicOr(g.tb + (b >> 5), bit);
       }
 }
 
