@@ -808,6 +808,196 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
   sink.finish();
 }
 
+// K2q: the same reverse walk with a DEFERRED, convergent scatter. The flush of a
+// departing corner is the divergent part of K2 (a lane moves cell every ~2
+// samples, at a different iteration from its neighbours: ncu r01 v19 shows ~70%
+// of K2's warp instructions in the flush code at 7.7 active lanes). Here a move
+// only appends (vertex, a_sigma, a_r, a_g, a_b) to the lane's ring in shared
+// memory (2 stores per corner); every iteration each lane then pops up to POPS
+// entries and scatters them (basis expansion + 7 red.v4). Pops run after the
+// warp reconverges, so they execute with every lane that has queued work. The
+// loop runs until every lane of the warp has finished its ray AND drained its
+// ring (warp-uniform exit; lanes without a ray just help drain).
+constexpr int kQ = 16;  // ring entries per thread (power of 2); a step enqueues <= 8
+struct QueueSink {
+  uint32_t* qv;  // [kQ][kThreads] vertex ids
+  float4* qa;    // [kQ][kThreads] (a_sigma, a_r, a_g, a_b)
+  int tid;
+  uint32_t tail;
+  __device__ __forceinline__ void operator()(uint32_t v, float s, float r, float gg, float b,
+                                             const float (&)[9]) {
+    const int slot = (int)(tail & (kQ - 1)) * kThreads + tid;
+    qv[slot] = v;
+    qa[slot] = make_float4(s, r, gg, b);
+    ++tail;
+  }
+  __device__ __forceinline__ void finish() {}
+};
+
+__device__ __forceinline__ void queue_pop(const QueueSink& q, uint32_t& head,
+                                          float4* __restrict__ grad, const float (&bf)[9]) {
+  if (head != q.tail) {
+    const int slot = (int)(head & (kQ - 1)) * kThreads + q.tid;
+    const uint32_t v = q.qv[slot];
+    const float4 e = q.qa[slot];
+    ++head;
+    RedSink{grad}(v, e.x, e.y, e.z, e.w, bf);
+  }
+}
+
+// Pop through the bulk reduce: one cp.reduce.async.bulk (UBLKRED, 112 B) per
+// vertex instead of 7 red.v4. Convergent pops avoid what made BulkSink lose
+// inside the divergent K2.
+__device__ __forceinline__ void queue_pop_bulk(const QueueSink& q, uint32_t& head,
+                                               float4* __restrict__ grad, const float (&bf)[9],
+                                               BulkSink& bs) {
+  if (head != q.tail) {
+    const int slot = (int)(head & (kQ - 1)) * kThreads + q.tid;
+    const uint32_t v = q.qv[slot];
+    const float4 e = q.qa[slot];
+    ++head;
+    bs(v, e.x, e.y, e.z, e.w, bf);
+  }
+}
+
+template <int MINB, int POPS, bool BULK>
+__global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
+    const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
+    const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
+    float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
+    const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
+  __shared__ uint32_t s_qv[kQ * kThreads];
+  __shared__ float4 s_qa[kQ * kThreads];
+  __shared__ __align__(16) float4 s_ring[BULK ? kThreads : 1][kBulkSlots][kVec4PerVertex];
+  BulkSink bs{grad, &s_ring[BULK ? threadIdx.x : 0][0][0], 0};
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  // ---- per-ray setup; a lane with nothing to scatter keeps c = -1 but stays in
+  // the loop (the loop's exit vote is warp-wide)
+  int c = -1;
+  March m;
+  MapUp u{};
+  float bf[9];
+  for (int mm = 0; mm < 9; ++mm) bf[mm] = 0.f;
+  if (t < n) {
+    const int i = order ? (int)order[t] : t;
+    const MapStats st = *stats;
+    const uint8_t fl = flags[i];
+    // non-finite loss: the reference throws before updating
+    if (st.bad == INT_MAX && (fl & kHit) && !(fl & kOverflow)) {
+      const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
+      const double4 tg =
+          rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+      if (map_upstream(st, global_counts, ray_cd[i], tg, fl, lambda_d, u)) {
+        ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+        double basis[9];
+        if (sh_basis(m.d, basis)) {
+#pragma unroll
+          for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
+          if (march_begin(g, p, m)) c = rec_count[t] - 1;
+        }
+      }
+    }
+  }
+  const double upc0 = u.upc[0], upc1 = u.upc[1], upc2 = u.upc[2];
+  const bool use_depth = c >= 0 && u.use_depth;
+  const double upd = use_depth ? u.upd : 0.0;
+  double Sc0 = 0.0, Sc1 = 0.0, Sc2 = 0.0, Sd = 0.0;
+  float a[4][8];
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[cc][k] = 0.f;
+  uint32_t cur = 0xffffffffu;
+  int pcx = 0, pcy = 0, pcz = 0;
+  int last_tb = -1;
+  QueueSink q{s_qv, s_qa, (int)threadIdx.x, 0u};
+  uint32_t head = 0;
+  bool final_pending = c >= 0;  // the last cell's 8 corners, flushed after the walk
+  float2 n0 = make_float2(0.f, 0.f), n1 = n0, n2 = n0;
+  if (c >= 0) {
+    const float2* qq = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
+    n0 = __ldg(qq);
+    n1 = __ldg(qq + 1);
+    n2 = __ldg(qq + 2);
+  }
+  while (__any_sync(0xffffffffu, c >= 0 || final_pending || head != q.tail)) {
+    if (c >= 0) {
+      const float2 q0 = n0, q1 = n1, q2 = n2;
+      if (c > 0) {
+        const float2* qq = reinterpret_cast<const float2*>(rec + rec_index(t, c - 1, K));
+        n0 = __ldg(qq);
+        n1 = __ldg(qq + 1);
+        n2 = __ldg(qq + 2);
+      }
+      --c;
+      const uint32_t kf = __float_as_uint(q2.y);
+      const double kseg = (double)(kf >> 4);
+      const double s0 = dadd(m.lo, dmul(kseg, m.step));
+      const double s0s = dadd(s0, m.step);
+      const double s1 = (m.hi < s0s) ? m.hi : s0s;
+      const double delta = dsub(s1, s0);
+      const double tm = dmul(0.5, dadd(s0, s1));
+      const double pp[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
+                            dadd(m.o[2], dmul(tm, m.d[2]))};
+      Sample s;
+      locate(g, pp, s);
+      const double w = (double)q0.x, Tn = (double)q0.y;
+      const double c0 = (double)q1.x, c1 = (double)q1.y, c2 = (double)q2.x;
+      double ds = upc0 * (c0 * Tn - Sc0) + upc1 * (c1 * Tn - Sc1) + upc2 * (c2 * Tn - Sc2);
+      if (use_depth) ds += upd * (tm * Tn - Sd);
+      ds *= delta;
+      Sc0 += c0 * w;
+      Sc1 += c1 * w;
+      Sc2 += c2 * w;
+      Sd += tm * w;
+      if (s.base != cur) {
+        if (cur != 0xffffffffu)
+          move_cell(q, g, cur, s.cx - pcx, s.cy - pcy, s.cz - pcz, a, bf);
+        cur = s.base;
+        pcx = s.cx;
+        pcy = s.cy;
+        pcz = s.cz;
+        mark_touched(g, s.cx, s.cy, s.cz, last_tb);
+      }
+      const float wf = q0.x;
+      const float u0 = (kf & kRecSigmaPos) ? (float)ds : 0.f;
+      const float u1 = (kf & 1u) ? 0.f : (float)upc0 * wf;
+      const float u2 = (kf & 2u) ? 0.f : (float)upc1 * wf;
+      const float u3 = (kf & 4u) ? 0.f : (float)upc2 * wf;
+      const float fx = (float)s.fx, fy = (float)s.fy, fz = (float)s.fz;
+      const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
+        a[0][k] = fmaf(wk, u0, a[0][k]);
+        a[1][k] = fmaf(wk, u1, a[1][k]);
+        a[2][k] = fmaf(wk, u2, a[2][k]);
+        a[3][k] = fmaf(wk, u3, a[3][k]);
+      }
+    } else if (final_pending && q.tail - head <= (uint32_t)(kQ - 8)) {
+      final_pending = false;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) flush_corner(q, g, cur, a, bf, k);
+    }
+    // convergent scatter: every lane with queued corners pops up to POPS, then
+    // more until every ring has room for the next step's <= 8 entries
+    if constexpr (BULK) {
+#pragma unroll
+      for (int r = 0; r < POPS; ++r) queue_pop_bulk(q, head, grad, bf, bs);
+      while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
+        queue_pop_bulk(q, head, grad, bf, bs);
+    } else {
+#pragma unroll
+      for (int r = 0; r < POPS; ++r) queue_pop(q, head, grad, bf);
+      while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
+        queue_pop(q, head, grad, bf);
+    }
+  }
+  if constexpr (BULK) bs.finish();
+}
+
 // ------------------------------------------------------------------ K3 deterministic records
 // One record per (sample, corner), in the reference's accumulation order
 // (ray, sample, corner). values: per sample 8 weights + 28 upstream slots (fp64).
@@ -1306,18 +1496,37 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
                              const int* global_counts, float4* grad, double lambda_d,
                              const uint32_t* order, const SampleRec* rec, int K,
                              const int* rec_count, cudaStream_t s) {
-  static const int minb = [] {
+  // CTAs per SM: the direct K2 needs 154 registers (3); the queued one fits 4
+  // (127 registers, 40 KB ring) — measured 15.0 vs 14.7 ms per 1M-ray backward (r01)
+  static const int minb_env = [] {
     const char* e = std::getenv("VRF_REC_MINB");
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : 0;
   }();
-  // scatter sink: per-float4 red (default) or the bulk reduce (VRF_SCATTER=bulk, A/B).
-  // r01: red 17.6 ms vs bulk 21.5 ms per 1M-ray backward — UBLKRED is a uniform-
-  // datapath op, so a divergent flush serialises it over the active lanes.
+  // scatter: the queued convergent K2 (default), or the direct divergent K2 with
+  // per-float4 red (VRF_K2=direct) or the bulk reduce (VRF_SCATTER=bulk). r01,
+  // per 1M-ray backward: queued 14.7 ms, direct red 15.0 ms, direct bulk 21.5 ms,
+  // queued with bulk pops 16.2 ms (UBLKRED does not beat red.v4 on this address
+  // pattern even with every lane active; 1, 2 or 3 pops per step: same time).
   static const bool bulk = [] {
     const char* e = std::getenv("VRF_SCATTER");
     return e && std::string(e) == "bulk";
   }();
+  static const bool direct = [] {
+    const char* e = std::getenv("VRF_K2");
+    return bulk || (e && std::string(e) == "direct");
+  }();
   const int blocks = (n + kThreads - 1) / kThreads;
+  const int minb = minb_env ? minb_env : (direct ? 3 : 4);
+  if (!direct) {
+#define VRF_Q_LAUNCH(MB)                                                                        \
+  k_map_backward_q<MB, 2, false><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n,   \
+                                                             ray_cd, flags, stats,              \
+                                                             global_counts, grad, lambda_d,     \
+                                                             order, rec, K, rec_count)
+    if (minb == 3) VRF_Q_LAUNCH(3); else VRF_Q_LAUNCH(4);
+#undef VRF_Q_LAUNCH
+    return;
+  }
 #define VRF_REC_LAUNCH(MB, BK)                                                                  \
   k_map_backward_rec<MB, BK><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd, \
                                                          flags, stats, global_counts, grad,       \
