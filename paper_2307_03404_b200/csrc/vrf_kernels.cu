@@ -15,6 +15,7 @@
 //   K5 (vrf_track.cu)      fused pose forward + Jacobian -> J^T J, J^T r
 //   utilities              prune, upsample, block occupancy, pack / convert
 #include <cstdio>
+#include <cstring>
 #include <string>
 #include <type_traits>
 #include <cstdlib>
@@ -699,6 +700,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
     float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
     const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
   __shared__ __align__(16) float4 s_ring[BULK ? kThreads : 1][kBulkSlots][kVec4PerVertex];
+  __shared__ __align__(16) float4 s_stage[BULK ? 1 : kThreads][kVec4PerVertex];  // per-warp merge
+  float4 (*stage)[kVec4PerVertex] = &s_stage[BULK ? 0 : (threadIdx.x & ~31)];
   using Sink = typename std::conditional<BULK, BulkSink, RedSink>::type;
   Sink sink;
   if constexpr (BULK)
@@ -819,6 +822,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
 // loop runs until every lane of the warp has finished its ray AND drained its
 // ring (warp-uniform exit; lanes without a ray just help drain).
 constexpr int kQ = 16;  // ring entries per thread (power of 2); a step enqueues <= 8
+constexpr int kQSmemBytes = kQ * kThreads * (16 + 4);
 struct QueueSink {
   uint32_t* qv;  // [kQ][kThreads] vertex ids
   float4* qa;    // [kQ][kThreads] (a_sigma, a_r, a_g, a_b)
@@ -831,9 +835,19 @@ struct QueueSink {
     qa[slot] = make_float4(s, r, gg, b);
     ++tail;
   }
-  __device__ __forceinline__ void finish() {}
 };
 
+#ifdef VRF_QSTATS
+__device__ unsigned long long g_qstats[4];  // pops, merged-away pops, rounds, active lanes
+#endif
+// One pop round: the lane's oldest queued corner -> basis expansion + 7 red.v4.
+// Measured alternative (r01, VRF_QSTATS counters): the ~28 lanes popping together
+// often hold the same vertex (33% of pops duplicate another lane's vertex in the
+// same round). Merging those groups (__match_any_sync, members stage their
+// 28-vector in shared memory, the leader sums and issues the only reds) cut the
+// L2 reductions by a third and L2 busy 69% -> 50%, but K2 did not get faster
+// (14.7 ms either way): the added merge instructions (7.3G vs 5.3G warp
+// instructions) moved the limit to issue/latency.
 __device__ __forceinline__ void queue_pop(const QueueSink& q, uint32_t& head,
                                           float4* __restrict__ grad, const float (&bf)[9]) {
   if (head != q.tail) {
@@ -841,6 +855,17 @@ __device__ __forceinline__ void queue_pop(const QueueSink& q, uint32_t& head,
     const uint32_t v = q.qv[slot];
     const float4 e = q.qa[slot];
     ++head;
+#ifdef VRF_QSTATS
+    const unsigned act = __activemask();
+    const unsigned grp = __match_any_sync(act, v);
+    const int lane = threadIdx.x & 31;
+    if (lane == __ffs(act) - 1) {
+      atomicAdd(&g_qstats[2], 1ull);
+      atomicAdd(&g_qstats[3], (unsigned long long)__popc(act));
+    }
+    atomicAdd(&g_qstats[0], 1ull);
+    if (lane != __ffs(grp) - 1) atomicAdd(&g_qstats[1], 1ull);
+#endif
     RedSink{grad}(v, e.x, e.y, e.z, e.w, bf);
   }
 }
@@ -868,8 +893,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
     float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
     const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
-  __shared__ uint32_t s_qv[kQ * kThreads];
-  __shared__ float4 s_qa[kQ * kThreads];
+  // dynamic shared memory (kQSmemBytes): the rings, [kQ][kThreads] float4 + u32
+  extern __shared__ __align__(16) float4 s_dyn[];
+  float4* s_qa = s_dyn;
+  uint32_t* s_qv = reinterpret_cast<uint32_t*>(s_dyn + kQ * kThreads);
   __shared__ __align__(16) float4 s_ring[BULK ? kThreads : 1][kBulkSlots][kVec4PerVertex];
   BulkSink bs{grad, &s_ring[BULK ? threadIdx.x : 0][0][0], 0};
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1519,12 +1546,28 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
   const int minb = minb_env ? minb_env : (direct ? 3 : 4);
   if (!direct) {
 #define VRF_Q_LAUNCH(MB)                                                                        \
-  k_map_backward_q<MB, 2, false><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n,   \
-                                                             ray_cd, flags, stats,              \
-                                                             global_counts, grad, lambda_d,     \
-                                                             order, rec, K, rec_count)
+  do {                                                                                          \
+    static const bool attr = [] {                                                               \
+      return cudaFuncSetAttribute(k_map_backward_q<MB, 2, false>,                               \
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
+                                  kQSmemBytes) == cudaSuccess;                                  \
+    }();                                                                                        \
+    (void)attr;                                                                                 \
+    k_map_backward_q<MB, 2, false><<<blocks, kThreads, kQSmemBytes, s>>>(                       \
+        g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d, \
+        order, rec, K, rec_count);                                                              \
+  } while (0)
     if (minb == 3) VRF_Q_LAUNCH(3); else VRF_Q_LAUNCH(4);
 #undef VRF_Q_LAUNCH
+#ifdef VRF_QSTATS
+    unsigned long long qs[4];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(qs, g_qstats, sizeof(qs));
+    std::fprintf(stderr, "qstats pops %llu dup %llu rounds %llu lanes/round %.2f\n", qs[0], qs[1],
+                 qs[2], qs[2] ? (double)qs[3] / qs[2] : 0.0);
+    std::memset(qs, 0, sizeof(qs));
+    cudaMemcpyToSymbol(g_qstats, qs, sizeof(qs));
+#endif
     return;
   }
 #define VRF_REC_LAUNCH(MB, BK)                                                                  \
