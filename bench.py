@@ -61,9 +61,11 @@ def parse():
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    ap.add_argument("--exchange", default="sparse", choices=["sparse", "dense"],
-                    help="N>1 gradient exchange: touched 8^3-vertex blocks only, or the "
-                         "whole grid")
+    ap.add_argument("--exchange", default="sparse", choices=["sparse", "dense", "p2p"],
+                    help="N>1 gradient exchange: NCCL over the touched 8^3-vertex blocks "
+                         "(sparse), NCCL over the whole grid (dense), or the fused "
+                         "peer-memory kernel (p2p: one kernel sums, updates and "
+                         "broadcasts the touched blocks over NVLink)")
     ap.add_argument("--dist-path", action="store_true",
                     help="run the NCCL-composed distributed step even at world size 1 "
                          "(launch under torchrun; validates the N>1 code path on one GPU)")
@@ -351,7 +353,7 @@ def run_ours(args):
 
     def one_step(i):
         if mapper is not None:
-            return mapper.step(dev_batches[i], cfg.lambda_d, sparse=args.exchange == "sparse")
+            return mapper.step(dev_batches[i], cfg.lambda_d, exchange=args.exchange)
         return ctx.mapping_step_device(cfg, dev_batches[i].data_ptr(), args.rays)
 
     for i in range(args.warmup):
@@ -431,7 +433,7 @@ def run_ours(args):
             dbuf.copy_(pins[k], non_blocking=True)
             torch.cuda.current_stream().synchronize()  # pins[k] is free again
             nxt[0] = pool.submit(draw, k ^ 1)  # next batch drawn while this step runs
-            return mapper.step(dbuf, cfg.lambda_d, sparse=args.exchange == "sparse")
+            return mapper.step(dbuf, cfg.lambda_d, exchange=args.exchange)
 
         for _ in range(args.warmup):
             e_step()

@@ -288,6 +288,30 @@ int vrf_blocks_apply(vrf_context* ctx, const vrf_mapping_config* cfg, const int3
                      int n, const float* grad_packed_dev);
 int vrf_grad_clear(vrf_context* ctx);
 
+/* Fused exchange over peer memory (NVLink / NVSwitch), replacing the NCCL
+ * block-sparse exchange above with ONE kernel: the owner of each touched
+ * 8^3-vertex block (static owner id % world) reads every rank's gradient for the
+ * block over peer memory, sums them in rank order, applies RMSProp
+ * (mapping.cpp:218-231) to its payload and RMSProp state, and stores the updated
+ * payload block into every rank's payload. Ordering is the caller's: call it
+ * after a stream-ordered barrier that follows every rank's vrf_map_backward
+ * (e.g. a one-element NCCL all-reduce on the same stream), then barrier again
+ * before any rank reads its payload or clears its gradient (vrf_grad_clear).
+ * Peer pointers are device pointers valid on this context's device: the other
+ * contexts' buffers of the same process (vrf_peer_buffers_get), or IPC-opened
+ * buffers of other processes (vrf_ipc_export on every rank, exchange the bytes,
+ * vrf_peers_open_ipc). The table is dropped when the grid is re-allocated. */
+#define VRF_MAX_PEERS 8
+#define VRF_IPC_HANDLE_BYTES 192 /* 3 x cudaIpcMemHandle_t: gradient, payload, touched bitmap */
+typedef struct {
+  uint64_t grad, payload, tb; /* device addresses */
+} vrf_peer_buffers;
+int vrf_peer_buffers_get(vrf_context* ctx, vrf_peer_buffers* out);
+int vrf_peers_set(vrf_context* ctx, int world, int rank, const vrf_peer_buffers* peers);
+int vrf_ipc_export(vrf_context* ctx, uint8_t* handles);
+int vrf_peers_open_ipc(vrf_context* ctx, int world, int rank, const uint8_t* handles);
+int vrf_exchange_p2p(vrf_context* ctx, const vrf_mapping_config* cfg);
+
 /* ---- tracking */
 /* pose_gradient — tracking.hpp:70-73 (tracking.cpp:76-143); pixels: n (px, py). */
 int vrf_pose_gradient(vrf_context* ctx, int frame, const vrf_intrinsics* intr,

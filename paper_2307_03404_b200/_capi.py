@@ -89,6 +89,14 @@ class DeviceBuffers_c(C.Structure):
                 ("stream", C.c_void_p)]
 
 
+class PeerBuffers_c(C.Structure):
+    _fields_ = [("grad", C.c_uint64), ("payload", C.c_uint64), ("tb", C.c_uint64)]
+
+
+IPC_HANDLE_BYTES = 192
+MAX_PEERS = 8
+
+
 class MapPartials_c(C.Structure):
     _fields_ = [("rays_color", C.c_int32), ("rays_depth", C.c_int32),
                 ("sum_photometric", C.c_double), ("sum_geometric", C.c_double),
@@ -148,6 +156,11 @@ _SIGS = {
     "vrf_blocks_unpack_payload": (C.c_int, [vp, vp, C.c_int, vp]),
     "vrf_blocks_apply": (C.c_int, [vp, P(MappingConfig_c), vp, C.c_int, vp]),
     "vrf_grad_clear": (C.c_int, [vp]),
+    "vrf_peer_buffers_get": (C.c_int, [vp, P(PeerBuffers_c)]),
+    "vrf_peers_set": (C.c_int, [vp, C.c_int, C.c_int, P(PeerBuffers_c)]),
+    "vrf_ipc_export": (C.c_int, [vp, vp]),
+    "vrf_peers_open_ipc": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+    "vrf_exchange_p2p": (C.c_int, [vp, P(MappingConfig_c)]),
     "vrf_pose_gradient": (C.c_int, [vp, C.c_int, P(Intrinsics_c), P(Pose_c), vp, C.c_int,
                                     P(TrackingLoss_c), P(PoseGradient_c)]),
     "vrf_pose_normal_equations": (C.c_int, [vp, C.c_int, P(Intrinsics_c), P(Pose_c), vp,

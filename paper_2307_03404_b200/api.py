@@ -675,6 +675,34 @@ class Context:
     def grad_clear(self):
         self._check(self._lib.vrf_grad_clear(self._h))
 
+    # ---- fused peer-memory exchange (vrf_exchange_p2p)
+    def peer_buffers(self):
+        b = capi.PeerBuffers_c()
+        self._check(self._lib.vrf_peer_buffers_get(self._h, C.byref(b)))
+        return b
+
+    def peers_set(self, rank: int, peers) -> None:
+        """peers: one PeerBuffers_c per rank (rank order), valid on this device."""
+        arr = (capi.PeerBuffers_c * len(peers))(*peers)
+        self._check(self._lib.vrf_peers_set(self._h, len(peers), int(rank), arr))
+
+    def ipc_export(self) -> bytes:
+        buf = (C.c_uint8 * capi.IPC_HANDLE_BYTES)()
+        self._check(self._lib.vrf_ipc_export(self._h, buf))
+        return bytes(buf)
+
+    def peers_open_ipc(self, rank: int, handles) -> None:
+        """handles: every rank's ipc_export() bytes, rank order."""
+        blob = b"".join(handles)
+        if len(blob) != capi.IPC_HANDLE_BYTES * len(handles):
+            raise ValueError("peers_open_ipc: malformed handles")
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        self._check(self._lib.vrf_peers_open_ipc(self._h, len(handles), int(rank), buf))
+
+    def exchange_p2p(self, config: MappingConfig):
+        cc = config._c()
+        self._check(self._lib.vrf_exchange_p2p(self._h, C.byref(cc)))
+
     def pose_gradient(self, frame: int, intr: CameraIntrinsics, pose: Pose, pixels: np.ndarray,
                       config: TrackingConfig) -> PoseGradient:
         px = np.ascontiguousarray(pixels, dtype=np.int32).reshape(-1, 2)

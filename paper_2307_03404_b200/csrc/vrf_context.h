@@ -47,6 +47,10 @@ struct vrf_context {
   uint32_t* socc = nullptr;  // 64^3-cell superblock occupancy
   int sdim[3] = {0, 0, 0};
   uint32_t* tb = nullptr;    // touched 8^3-vertex blocks of the pending gradient
+  // fused peer-memory exchange (vrf_peers_set / vrf_peers_open_ipc / vrf_exchange_p2p)
+  vrf::PeerTable peers{};
+  bool peers_set = false;
+  void* ipc_open[vrf::kMaxPeers][3] = {};  // IPC-opened peer buffers (closed with the grid)
   int tdim[3] = {0, 0, 0};
   bool touched_valid = false;  // every nonzero gradient group lies in a marked block
   bool all_blocks_active = false;
@@ -178,8 +182,19 @@ inline int ensure_pinned(vrf_context* ctx, size_t bytes) {
   return VRF_OK;
 }
 
+inline void close_peers(vrf_context* ctx) {
+  for (auto& row : ctx->ipc_open)
+    for (void*& p : row) {
+      if (p) cudaIpcCloseMemHandle(p);
+      p = nullptr;
+    }
+  ctx->peers = PeerTable{};
+  ctx->peers_set = false;
+}
+
 inline void free_grid(vrf_context* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);  // queued work may still use them
+  close_peers(ctx);  // the peer table points at this grid's buffers
   cudaFree(ctx->payload);
   cudaFree(ctx->grad);
   cudaFree(ctx->rms);

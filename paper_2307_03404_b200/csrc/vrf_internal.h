@@ -95,6 +95,18 @@ void launch_blocks_pack(const float4* src, const int* ids, int n, int rx, int ry
                         int tby, float4* out, cudaStream_t s);
 void launch_blocks_unpack(float4* dst, const int* ids, int n, int rx, int ry, int rz, int tbx,
                           int tby, const float4* in, cudaStream_t s);
+// Fused peer-memory exchange (vrf_exchange_p2p): per-rank device pointers as seen
+// from the launching device (UVA; IPC-opened for other processes' buffers).
+constexpr int kMaxPeers = 8;
+struct PeerTable {
+  float4* grad[kMaxPeers];
+  float4* payload[kMaxPeers];
+  const uint32_t* tb[kMaxPeers];
+  int world, rank;
+};
+void launch_exchange_p2p(const PeerTable& pt, float4* v, int nb, int rx, int ry, int rz, int tbx,
+                         int tby, double rho, double lr_sigma, double lr_sh, double eps,
+                         const MapStats* stats, cudaStream_t s);
 void launch_blocks_apply(float4* theta, float4* v, const int* ids, int n, int rx, int ry, int rz,
                          int tbx, int tby, const float4* packed, double rho, double lr_sigma,
                          double lr_sh, double eps, cudaStream_t s);

@@ -1274,6 +1274,77 @@ __global__ void k_blocks_apply(float4* __restrict__ theta, float4* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ fused peer exchange
+// One kernel for the whole multi-GPU gradient exchange + update:
+// the block-sparse path's pack -> reduce-scatter -> RMSProp -> pack ->
+// all-gather -> unpack, done over NVLink peer memory. CTA i handles block
+// b = rank + world * i (static owner, as the NCCL path). If any rank's
+// touched-block bitmap marks b, the CTA reads b's gradient from every rank that
+// touched it (P2P loads, summed in rank order: deterministic for a fixed world
+// size), applies RMSProp (mapping.cpp:218-231; same per-element rule as
+// k_rmsprop) to its own payload / RMSProp state, and stores the updated payload
+// group into every rank's payload (P2P stores). Every rank holds the same
+// payload before the step, so reading theta locally is exact.
+__global__ void __launch_bounds__(256) k_exchange_p2p(PeerTable pt, float4* __restrict__ vstate,
+                                                      int nb, int rx, int ry, int rz, int tbx,
+                                                      int tby, double rho, double lr_sigma,
+                                                      double lr_sh, double eps,
+                                                      const MapStats* __restrict__ stats) {
+  const int b = pt.rank + pt.world * blockIdx.x;
+  if (b >= nb) return;
+  if (stats) {
+    const MapStats st = *stats;
+    if (st.bad != INT_MAX || st.m_c == 0) return;
+  }
+  __shared__ unsigned s_mask;
+  if (threadIdx.x == 0) {
+    unsigned m = 0;
+    for (int r = 0; r < pt.world; ++r)
+      m |= ((__ldcv(pt.tb[r] + (b >> 5)) >> (b & 31)) & 1u) << r;
+    s_mask = m;
+  }
+  __syncthreads();
+  const unsigned mask = s_mask;
+  if (!mask) return;
+  float4* theta = pt.payload[pt.rank];
+  for (int q = threadIdx.x; q < kBlockVerts * kVec4PerVertex; q += blockDim.x) {
+    const int vl = q / kVec4PerVertex, j = q % kVec4PerVertex;
+    const long long v = block_vertex(b, vl, rx, ry, rz, tbx, tby);
+    if (v < 0) continue;
+    const long long f = v * kVec4PerVertex + j;
+    float4 parts[kMaxPeers];
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)  // all loads in flight before the sum
+      parts[r] = (r < pt.world && ((mask >> r) & 1u)) ? __ldcv(pt.grad[r] + f)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 g4 = parts[0];
+#pragma unroll
+    for (int r = 1; r < kMaxPeers; ++r) {
+      g4.x += parts[r].x;
+      g4.y += parts[r].y;
+      g4.z += parts[r].z;
+      g4.w += parts[r].w;
+    }
+    if (g4.x == 0.f && g4.y == 0.f && g4.z == 0.f && g4.w == 0.f) continue;
+    float4 th = theta[f], v4 = vstate[f];
+    float* thp = &th.x;
+    float* vp = &v4.x;
+    const float* gp = &g4.x;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double gg = gp[c];
+      if (gg == 0.0) continue;  // mapping.cpp:226
+      const double vn = rho * (double)vp[c] + (1.0 - rho) * gg * gg;
+      const double lr = (4 * j + c == 0) ? lr_sigma : lr_sh;
+      vp[c] = (float)vn;
+      thp[c] = (float)((double)thp[c] - lr * gg / sqrt(vn + eps));
+    }
+    vstate[f] = v4;
+    for (int r = 0; r < pt.world; ++r) __stcg(pt.payload[r] + f, th);
+  }
+  __threadfence_system();  // peer stores visible before the caller's barrier
+}
+
 // ------------------------------------------------------------------ utilities
 __global__ void k_fill_payload(float* payload, long long nv, float sigma) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nv * kPayload;
@@ -1671,6 +1742,14 @@ void launch_blocks_apply(float4* theta, float4* v, const int* ids, int n, int rx
   if (total > 0)
     k_blocks_apply<<<grid_blocks(total, 256), 256, 0, s>>>(theta, v, ids, n, rx, ry, rz, tbx, tby,
                                                            packed, rho, lr_sigma, lr_sh, eps);
+}
+void launch_exchange_p2p(const PeerTable& pt, float4* v, int nb, int rx, int ry, int rz, int tbx,
+                         int tby, double rho, double lr_sigma, double lr_sh, double eps,
+                         const MapStats* stats, cudaStream_t s) {
+  const int grid = (nb + pt.world - 1) / pt.world;
+  if (grid > 0)
+    k_exchange_p2p<<<grid, 256, 0, s>>>(pt, v, nb, rx, ry, rz, tbx, tby, rho, lr_sigma, lr_sh, eps,
+                                        stats);
 }
 void launch_fill_payload(float* payload, long long nv, float sigma, cudaStream_t s) {
   k_fill_payload<<<grid_blocks(nv * kPayload, 256), 256, 0, s>>>(payload, nv, sigma);

@@ -1,6 +1,9 @@
 // Mapping entry points of the C-ABI: mapping_step (mapping.cpp:114-233) on the
 // device, its deterministic sorted/segmented-reduce variant, and the phases the
 // multi-GPU driver composes with NCCL collectives.
+#include <cstring>
+#include <string>
+
 #include <cub/cub.cuh>
 
 #include "vrf_context.h"
@@ -549,3 +552,113 @@ int vrf_map_apply(vrf_context* ctx, const vrf_mapping_config* cfg, int64_t verte
 }
 
 }  // extern "C"
+
+// ---- fused peer-memory exchange (distributed.py exchange="p2p")
+int vrf_peer_buffers_get(vrf_context* ctx, vrf_peer_buffers* out) {
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  out->grad = (uint64_t)(uintptr_t)ctx->grad;
+  out->payload = (uint64_t)(uintptr_t)ctx->payload;
+  out->tb = (uint64_t)(uintptr_t)ctx->tb;
+  return VRF_OK;
+}
+
+namespace {
+// Validates and installs the peer table (does not touch IPC mappings).
+int set_peer_table(vrf_context* ctx, int world, int rank, const vrf_peer_buffers* peers) {
+  if (world < 1 || world > VRF_MAX_PEERS || rank < 0 || rank >= world || !peers)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_peers_set: bad world/rank/peers");
+  if (peers[rank].grad != (uint64_t)(uintptr_t)ctx->grad ||
+      peers[rank].payload != (uint64_t)(uintptr_t)ctx->payload ||
+      peers[rank].tb != (uint64_t)(uintptr_t)ctx->tb)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT,
+                   "vrf_peers_set: entry [rank] must be this context's own buffers");
+  PeerTable pt{};
+  for (int r = 0; r < world; ++r) {
+    pt.grad[r] = reinterpret_cast<float4*>((uintptr_t)peers[r].grad);
+    pt.payload[r] = reinterpret_cast<float4*>((uintptr_t)peers[r].payload);
+    pt.tb[r] = reinterpret_cast<const uint32_t*>((uintptr_t)peers[r].tb);
+    if (!pt.grad[r] || !pt.payload[r] || !pt.tb[r])
+      return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_peers_set: null peer buffer");
+  }
+  pt.world = world;
+  pt.rank = rank;
+  ctx->peers = pt;
+  ctx->peers_set = true;
+  return VRF_OK;
+}
+}  // namespace
+
+int vrf_peers_set(vrf_context* ctx, int world, int rank, const vrf_peer_buffers* peers) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  close_peers(ctx);
+  return set_peer_table(ctx, world, rank, peers);
+}
+
+int vrf_ipc_export(vrf_context* ctx, uint8_t* handles) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  void* bufs[3] = {ctx->grad, ctx->payload, ctx->tb};
+  for (int k = 0; k < 3; ++k) {
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, bufs[k]));
+    std::memcpy(handles + k * sizeof(cudaIpcMemHandle_t), &h, sizeof(h));
+  }
+  return VRF_OK;
+}
+
+int vrf_peers_open_ipc(vrf_context* ctx, int world, int rank, const uint8_t* handles) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  static_assert(3 * sizeof(cudaIpcMemHandle_t) == VRF_IPC_HANDLE_BYTES, "IPC handle size");
+  if (world < 1 || world > VRF_MAX_PEERS || rank < 0 || rank >= world || !handles)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_peers_open_ipc: bad world/rank/handles");
+  close_peers(ctx);
+  vrf_peer_buffers peers[VRF_MAX_PEERS];
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      vrf_peer_buffers_get(ctx, &peers[r]);
+      continue;
+    }
+    uint64_t* dst[3] = {&peers[r].grad, &peers[r].payload, &peers[r].tb};
+    for (int k = 0; k < 3; ++k) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + (size_t)r * VRF_IPC_HANDLE_BYTES + k * sizeof(h), sizeof(h));
+      void* p = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        close_peers(ctx);
+        return set_err(ctx, VRF_ERR_CUDA,
+                       std::string("vrf_peers_open_ipc: cudaIpcOpenMemHandle: ") +
+                           cudaGetErrorString(e));
+      }
+      ctx->ipc_open[r][k] = p;
+      *dst[k] = (uint64_t)(uintptr_t)p;
+    }
+  }
+  rc = set_peer_table(ctx, world, rank, peers);
+  if (rc) close_peers(ctx);
+  return rc;
+}
+
+int vrf_exchange_p2p(vrf_context* ctx, const vrf_mapping_config* cfg) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if (!ctx->peers_set)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT,
+                   "vrf_exchange_p2p: no peer table (vrf_peers_set / vrf_peers_open_ipc)");
+  const int nb = ctx->tdim[0] * ctx->tdim[1] * ctx->tdim[2];
+  cudaEvent_t pr = prof_begin(ctx);
+  launch_exchange_p2p(ctx->peers, (float4*)ctx->rms, nb, ctx->geom.res[0], ctx->geom.res[1],
+                      ctx->geom.res[2], ctx->tdim[0], ctx->tdim[1], cfg->rmsprop_decay,
+                      cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, nullptr, ctx->stream);
+  prof_end(ctx, kProfRmsprop, pr);
+  LAUNCHED(1);
+  CU(cudaGetLastError());
+  return VRF_OK;
+}

@@ -101,6 +101,16 @@ class GpuEngine:
     def clear_grad(self):
         self.ctx.grad_clear()
 
+    # ---- fused peer-memory exchange (one kernel, vrf_exchange_p2p)
+    def ipc_export(self) -> bytes:
+        return self.ctx.ipc_export()
+
+    def open_peers(self, rank, handles):
+        self.ctx.peers_open_ipc(rank, handles)
+
+    def exchange_p2p(self):
+        self.ctx.exchange_p2p(self.cfg)
+
 
 class DistributedMapper:
     def __init__(self, engine, group=None):
@@ -113,10 +123,13 @@ class DistributedMapper:
                                  device=engine.grad.device)
         self._rs = hasattr(dist, "reduce_scatter_tensor") and dist.get_backend(group) == "nccl"
 
-    def step(self, batch, lambda_d: float, sparse: bool = False) -> StepResult:
-        """One ray-sharded mapping step. sparse: exchange only the 8^3-vertex
-        blocks some rank touched (block-sparse reduce-scatter / all-gather, see
-        _exchange_sparse); otherwise the dense reduce-scatter / all-gather."""
+    def step(self, batch, lambda_d: float, sparse: bool = False,
+             exchange: str = None) -> StepResult:
+        """One ray-sharded mapping step. exchange: "dense" (reduce-scatter /
+        all-gather of the whole gradient / payload), "sparse" (only the 8^3-vertex
+        blocks some rank touched, _exchange_sparse) or "p2p" (the fused peer-memory
+        kernel, _exchange_p2p). The older flag sparse=True means "sparse"."""
+        exchange = exchange or ("sparse" if sparse else "dense")
         m_c, m_d, bad, lp, lg, samples = self.e.forward(batch)
         dev = self.e.grad.device
         ints = torch.tensor([m_c, m_d, 1 if bad >= 0 else 0, samples], dtype=torch.int64,
@@ -130,14 +143,47 @@ class DistributedMapper:
         if n_bad:
             raise RuntimeError("mapping_step: non-finite loss")
         self.e.backward(M_c, M_d)
-        if sparse:
+        if exchange == "p2p":
+            self._exchange_p2p()
+        elif exchange == "sparse":
             self._exchange_sparse()
-        else:
+        elif exchange == "dense":
             self._exchange_dense()
+        else:
+            raise ValueError(f"unknown exchange {exchange!r}")
         lp_sum, lg_sum = flts.tolist()
         l_p = lp_sum / M_c
         l_g = lg_sum / M_d if M_d > 0 else 0.0
         return StepResult(l_p, l_g, l_p + lambda_d * l_g, M_c, M_d, S)
+
+    def _barrier(self):
+        """Stream-ordered barrier: with NCCL a one-element all-reduce on the current
+        stream (every rank's earlier kernels are complete when it returns on the
+        device); other backends synchronise the device and barrier on the host."""
+        if dist.get_backend(self.group) == "nccl":
+            if not hasattr(self, "_tok"):
+                self._tok = torch.zeros(1, dtype=torch.int32, device=self.e.grad.device)
+            dist.all_reduce(self._tok, group=self.group)
+        else:
+            torch.cuda.synchronize(self.e.grad.device)
+            dist.barrier(group=self.group)
+
+    def _exchange_p2p(self):
+        """Fused exchange over peer memory: every rank's backward done (barrier) ->
+        ONE kernel per rank: the owner of each touched block sums all ranks'
+        gradients over NVLink, applies RMSProp and writes the payload block into
+        every rank -> barrier -> local gradient clear. The peer table (IPC handles
+        of every rank's gradient / payload / touched bitmap) is set up once."""
+        if not getattr(self, "_peers_open", False):
+            mine = self.e.ipc_export()
+            handles = [None] * self.world
+            dist.all_gather_object(handles, mine, group=self.group)
+            self.e.open_peers(self.rank, handles)
+            self._peers_open = True
+        self._barrier()
+        self.e.exchange_p2p()
+        self._barrier()
+        self.e.clear_grad()
 
     def _exchange_dense(self):
         s0, s1 = self.v0 * 28, self.v1 * 28

@@ -68,12 +68,13 @@ def test_nccl_world1_step_equals_single_gpu_step(oracle, sparse):
     np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
 
 
-def _world2_worker(rank, port, sparse, batch, out_dir):
+def _world2_worker(rank, port, exchange, batch, out_dir):
     """One rank of a world-2 job on the same device. gloo carries the collectives
     on the host (CUDA tensors are staged through pinned memory), so the two ranks'
     kernels never wait on each other; what runs on the device is the real
     GpuEngine at world 2: owned-shard RMSProp, block ownership id % world, packs
-    of blocks this rank did not touch, unpack of other ranks' blocks."""
+    of blocks this rank did not touch, unpack of other ranks' blocks; for
+    exchange="p2p" the CUDA IPC peer table and the fused peer-memory kernel."""
     import sys
     sys.path.insert(0, os.path.dirname(__file__))
     from scenes import fresh_grid as _fresh, room_scene as _room
@@ -96,7 +97,7 @@ def _world2_worker(rank, port, sparse, batch, out_dir):
         for k in range(2):
             b = mine if k == 0 else mine[::-1].copy()
             r = mapper.step(torch.from_numpy(np.ascontiguousarray(b)).cuda(), cfg.lambda_d,
-                            sparse=sparse)
+                            exchange=exchange)
             results.append([r.loss_total, r.rays_color, r.rays_depth, r.samples])
         torch.cuda.synchronize()
         np.save(os.path.join(out_dir, f"payload{rank}.npy"), a.download_grid().data)
@@ -105,15 +106,15 @@ def _world2_worker(rank, port, sparse, batch, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("sparse", [False, True])
-def test_world2_step_equals_single_gpu_step(oracle, sparse, tmp_path):
+@pytest.mark.parametrize("exchange", ["dense", "sparse", "p2p"])
+def test_world2_step_equals_single_gpu_step(oracle, exchange, tmp_path):
     """Two ray-sharded ranks (half the batch each) must produce the single-GPU
     mapping_step over the whole batch: equal payloads on both ranks, the global
     hit/sample counts exactly, the loss and payload to fp32-atomics tolerance."""
     import torch.multiprocessing as mp
     grid, intr, frames = room_scene()
     batch = oracle.draw_batch(5, len(frames), intr.width, intr.height, 4096)
-    mp.start_processes(_world2_worker, args=(_port(), sparse, batch, str(tmp_path)), nprocs=2,
+    mp.start_processes(_world2_worker, args=(_port(), exchange, batch, str(tmp_path)), nprocs=2,
                        join=True, start_method="spawn")
     p0, p1 = (np.load(tmp_path / f"payload{r}.npy") for r in range(2))
     s0, s1 = (np.load(tmp_path / f"stats{r}.npy") for r in range(2))
@@ -142,3 +143,56 @@ def test_world2_step_equals_single_gpu_step(oracle, sparse, tmp_path):
     for k in range(2):
         assert abs(s0[k, 0] - want_stats[k][0]) <= 1e-6 * want_stats[k][0]
     np.testing.assert_allclose(p0, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
+
+
+def test_p2p_exchange_virtual_ranks_equal_single_gpu_step(oracle):
+    """The fused peer-memory exchange kernel (vrf_exchange_p2p) with N = 3
+    contexts of one process standing in for 3 ranks (peer table = the other
+    contexts' buffers; no kernel waits on another: the phases run in order on
+    one stream). Must equal one context's mapping_step over the whole batch."""
+    grid, intr, frames = room_scene()
+    cfg = MappingConfig()
+    world = 3
+    batch = oracle.draw_batch(11, len(frames), intr.width, intr.height, 3 * 1024)
+    stream = torch.cuda.current_stream().cuda_stream
+    ctxs = []
+    for r in range(world):
+        c = Context(0)
+        c.set_stream(stream)
+        c.load_grid(fresh_grid(grid))
+        c.load_frames(intr, frames)
+        c.rmsprop_reset()
+        ctxs.append(c)
+    peers = [c.peer_buffers() for c in ctxs]
+    for r, c in enumerate(ctxs):
+        c.peers_set(r, peers)
+    parts = np.array_split(batch, world)
+    dev = [torch.from_numpy(np.ascontiguousarray(p)).cuda() for p in parts]
+    got_stats = []
+    for k in range(2):
+        fw = [c.map_forward(cfg, d.data_ptr(), d.shape[0]) for c, d in zip(ctxs, dev)]
+        M_c = sum(p.rays_color for p in fw)
+        M_d = sum(p.rays_depth for p in fw)
+        got_stats.append((M_c, M_d, sum(p.samples for p in fw)))
+        for c in ctxs:
+            c.map_backward(cfg, M_c, M_d)
+        for c in ctxs:
+            c.exchange_p2p(cfg)
+        for c in ctxs:
+            c.grad_clear()
+    torch.cuda.synchronize()
+    pay = [c.download_grid().data for c in ctxs]
+    for p in pay[1:]:
+        assert np.array_equal(pay[0], p)
+
+    b = Context(0)
+    b.load_grid(fresh_grid(grid))
+    b.load_frames(intr, frames)
+    b.rmsprop_reset()
+    for k in range(2):
+        st = b.mapping_step(cfg, batch)
+        assert (st.rays_color, st.rays_depth) == got_stats[k][:2]
+        if k == 0:
+            assert st.samples == got_stats[k][2]
+    want = b.download_grid().data
+    np.testing.assert_allclose(pay[0], want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
