@@ -61,11 +61,12 @@ def parse():
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    ap.add_argument("--exchange", default="sparse", choices=["sparse", "dense", "p2p"],
+    ap.add_argument("--exchange", default="p2p", choices=["sparse", "dense", "p2p"],
                     help="N>1 gradient exchange: NCCL over the touched 8^3-vertex blocks "
                          "(sparse), NCCL over the whole grid (dense), or the fused "
                          "peer-memory kernel (p2p: one kernel sums, updates and "
-                         "broadcasts the touched blocks over NVLink)")
+                         "broadcasts the touched blocks over NVLink; falls back to sparse "
+                         "when a rank cannot open its peers over CUDA IPC)")
     ap.add_argument("--dist-path", action="store_true",
                     help="run the NCCL-composed distributed step even at world size 1 "
                          "(launch under torchrun; validates the N>1 code path on one GPU)")
@@ -296,6 +297,14 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------- ours
+def _exchange_used(args, mapper):
+    if mapper is None:
+        return "none"
+    if args.exchange == "p2p" and not getattr(mapper, "_peers_open", False):
+        return f"sparse (p2p unavailable: {getattr(mapper, 'p2p_error', None)})"
+    return args.exchange
+
+
 def run_ours(args):
     import torch
 
@@ -548,7 +557,7 @@ def run_ours(args):
                        "rays_per_step_per_gpu": args.rays,
                        "grid_vertices": ctx.geom.num_vertices, "keyframes": len(frames),
                        "frame": f"{args.width}x{args.height}", "parallelism": f"dp{world}",
-                       "exchange": (args.exchange if mapper is not None else "none"),
+                       "exchange": _exchange_used(args, mapper),
                        "l2": f"inputs larger than L2 (grid "
                              f"{ctx.geom.num_vertices * 112 / 1e9:.1f} GB fp32)"},
             "rays_per_s": total_rays / (ms / 1e3),

@@ -143,6 +143,8 @@ class DistributedMapper:
         if n_bad:
             raise RuntimeError("mapping_step: non-finite loss")
         self.e.backward(M_c, M_d)
+        if exchange == "p2p" and not self.prepare_p2p():
+            exchange = "sparse"  # peer memory unavailable on some rank (p2p_error)
         if exchange == "p2p":
             self._exchange_p2p()
         elif exchange == "sparse":
@@ -168,6 +170,33 @@ class DistributedMapper:
             torch.cuda.synchronize(self.e.grad.device)
             dist.barrier(group=self.group)
 
+    def prepare_p2p(self) -> bool:
+        """Opens every rank's gradient / payload / touched bitmap over CUDA IPC.
+        Collective: every rank must call it. Returns False on every rank if any
+        rank could not open its peers (then the step falls back to the NCCL
+        block-sparse exchange; the reason is kept in p2p_error)."""
+        if getattr(self, "_peers_open", None) is not None:
+            return self._peers_open
+        err = ""
+        try:
+            mine = self.e.ipc_export()
+        except RuntimeError as e:
+            mine, err = b"", str(e)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, mine, group=self.group)
+        if not err and all(handles):
+            try:
+                self.e.open_peers(self.rank, handles)
+            except RuntimeError as e:
+                err = str(e)
+        elif not err:
+            err = "a peer could not export its buffers"
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=self.e.grad.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        self._peers_open = bool(ok.item())
+        self.p2p_error = err or (None if self._peers_open else "a peer could not open the table")
+        return self._peers_open
+
     def _exchange_p2p(self):
         """Fused exchange over peer memory: every rank's backward done (barrier) ->
         ONE kernel per rank: the owner of each touched block sums all ranks'
@@ -175,11 +204,7 @@ class DistributedMapper:
         every rank -> barrier -> local gradient clear. The peer table (IPC handles
         of every rank's gradient / payload / touched bitmap) is set up once."""
         if not getattr(self, "_peers_open", False):
-            mine = self.e.ipc_export()
-            handles = [None] * self.world
-            dist.all_gather_object(handles, mine, group=self.group)
-            self.e.open_peers(self.rank, handles)
-            self._peers_open = True
+            raise RuntimeError("p2p exchange without a peer table (prepare_p2p)")
         self._barrier()
         self.e.exchange_p2p()
         self._barrier()
