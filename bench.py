@@ -178,7 +178,7 @@ class Clocks:
 
 
 # ----------------------------------------------------------------- CPU baseline
-def cpu_reference(args, gt, intr, keyframe_poses, frames, seconds):
+def cpu_reference(args, gt, intr, keyframe_poses, frames, seconds, fixed=None):
     """The reference's own mapping_step (oracle/_ref) on the host cores, on the same
     workload (257^3 fp64 grid, 1200x680 keyframes), reference default batch of
     4096 rays, timed like the reference times itself (steady clock)."""
@@ -217,6 +217,8 @@ def cpu_reference(args, gt, intr, keyframe_poses, frames, seconds):
     # The reference zero-fills one V x 28 fp64 buffer per worker every step
     # (mapping.cpp:155-157), so all cores is not its fastest setting at 257^3:
     # sweep a few thread counts and keep the fastest (the fairest CPU figure).
+    # fixed = (warmup, steps): the --impl reference arm's contract — the sweep
+    # calls are warm-up (at least `warmup` calls), then exactly `steps` timed calls.
     cands = sorted({t for t in (1, 2, 4, threads) if t <= threads})
     sweep = {}
     for t in cands:
@@ -224,10 +226,19 @@ def cpu_reference(args, gt, intr, keyframe_poses, frames, seconds):
         if len(sweep) >= 2 and sweep[t] > min(sweep.values()) * 1.3:
             break  # past the optimum
     best = min(sweep, key=sweep.get)
-    steps, elapsed = 1, sweep[best]
-    while elapsed < seconds and steps < 20:
-        elapsed += one(best)
-        steps += 1
+    if fixed is not None:
+        warmup, k = fixed
+        for _ in range(max(0, warmup - len(sweep))):
+            one(best)
+        steps, elapsed = 0, 0.0
+        for _ in range(k):
+            elapsed += one(best)
+            steps += 1
+    else:
+        steps, elapsed = 1, sweep[best]
+        while elapsed < seconds and steps < 20:
+            elapsed += one(best)
+            steps += 1
     ref.lib.ref_frames_destroy(fh)
     return {"threads": best, "steps": steps, "seconds": elapsed,
             "sweep_s": {str(k): round(v, 3) for k, v in sweep.items()}}
@@ -257,7 +268,7 @@ def run_reference(args):
     import oracle as orc
 
     if not orc.REF_SO.exists():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref not built"})
         return
     room, gt, intr, path = make_scene(args)
     if args.config == 4:
@@ -276,12 +287,14 @@ def run_reference(args):
         frames.append(Frame(c, d, 0.0, p))
     ref.lib.ref_grid_destroy(gh)
     per_step, rays = cpu_samples_per_step(args, gt, intr, frames)
-    budget = max(5.0, min(args.cpu_seconds, 60.0))
-    r = cpu_reference(args, gt, intr, keyposes, frames, budget)
+    # exactly --warmup untimed + --steps timed reference mapping_step calls (each a
+    # bounded 4096-ray sample of the workload, ~3.5 s on one core)
+    r = cpu_reference(args, gt, intr, keyposes, frames, 0.0,
+                      fixed=(args.warmup, max(1, args.steps)))
     value = per_step * r["steps"] / r["seconds"]
-    print(json.dumps({
+    emit({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
-        "n_gpus": args.gpus, "steps": r["steps"], "warmup": 0,
+        "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
         "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "rays_per_step": 4096, "grid_vertices": args.res ** 3,
@@ -293,7 +306,7 @@ def run_reference(args):
                                    f"threads = fastest of the sweep {r['sweep_s']} (s/step)"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-    }))
+    })
 
 
 # ----------------------------------------------------------------- ours
@@ -565,13 +578,32 @@ def run_ours(args):
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
             "cpu_baseline": cpu, "tracking": tracking, "clocks": clk.summary(),
         }
-        print(json.dumps(line))
+        emit(line)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
 
 
+_JSON_FD = None
+
+
+def emit(obj):
+    """The one JSON line, on the original stdout. Everything else the run prints
+    to fd 1 (NCCL's version banner on communicator init, library messages) is
+    redirected to stderr by main(), so stdout carries exactly this line."""
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line)
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         run_reference(args)

@@ -45,3 +45,12 @@ def test_context_create_fails_loudly_without_gpu():
         assert "no CPU fallback" in str(e)
     else:
         raise AssertionError("context creation must fail without a CUDA device")
+
+
+def test_bench_and_entry_compile():
+    """bench.py and __graft_entry__.py are only run on the GPU box: at least
+    byte-compile them here."""
+    import py_compile
+    root = Path(__file__).resolve().parent.parent
+    for name in ("bench.py", "__graft_entry__.py"):
+        py_compile.compile(str(root / name), doraise=True)
