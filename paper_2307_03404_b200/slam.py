@@ -31,6 +31,7 @@ class SlamConfig:
     bootstrap_steps: int = 200          # mapping_step calls on frame 0 before tracking
     max_keyframes: int = 256
     window: int = 0                     # map over the last `window` keyframes (0 = all)
+    recent_fraction: float = 0.0        # share of each mapping batch drawn from the newest keyframe
     constant_velocity: bool = True      # track_sequence init policy (tracking.cpp:271-272)
     tracking: GNConfig = field(default_factory=GNConfig)
     mapping: MappingConfig = field(default_factory=lambda: MappingConfig(rays_per_batch=65536))
@@ -63,6 +64,19 @@ class SlamSystem:
 
     def _map(self, steps: int):
         m = self.cfg.mapping
+        f = self.cfg.recent_fraction
+        if f > 0.0 and self.n_keyframes > 1:
+            # newest keyframe over-sampled: the region the camera just entered is
+            # the least constrained part of the map
+            n_new = int(round(f * m.rays_per_batch))
+            w = self.intr.width
+            h = self.intr.height
+            for _ in range(steps):
+                a = self.rng.draw_batch(1, w, h, n_new)
+                a[:, 0] = self.n_keyframes - 1
+                b = self.rng.draw_batch(self.n_keyframes, w, h, m.rays_per_batch - n_new)
+                self.ctx.mapping_step(m, np.concatenate([a, b]))
+            return
         if self.cfg.window <= 0 or self.cfg.window >= self.n_keyframes:
             # all keyframes: map_scene's pipelined inner loop (host draws overlap steps)
             self.ctx.mapping_steps(m, self.rng, self.n_keyframes, steps)
