@@ -331,8 +331,10 @@ struct GroupMarch {
 //   * the Jacobian terms are linear in each corner's spatial gradients, so every
 //     lane accumulates its own partial Jo / Jd / B and the group reduces once
 //     per ray.
-template <typename ShT, int LPR, bool PAR = true>
-__global__ void __launch_bounds__(kT) k_pose_group(
+// MINB = 3 CTAs/SM (168 registers). r01: capping registers for more warps lost
+// (4 CTAs, 128 regs + spills: 494 frames/s; 5: 460; 7: 458; 3: 525).
+template <typename ShT, int LPR, bool PAR = true, int MINB = 3>
+__global__ void __launch_bounds__(kT, MINB) k_pose_group(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd_base,
     const int* __restrict__ frame_idx, long long npix, const DevPose* __restrict__ pose_ptr,
     const int* __restrict__ pixels, const uint32_t* __restrict__ order, int n, double lambda_p,
