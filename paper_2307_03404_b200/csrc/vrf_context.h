@@ -83,6 +83,7 @@ struct vrf_context {
   // fast-path sample records of the last forward (0 = recompute-march backward)
   int rec_K = 0;
   int max_ray_samples = 0;  // longest ray seen by a mapping forward (sizes rec_K)
+  long long rec_need_tried = 0;  // last record depth the budget was evaluated for
 
   // multi-GPU phase state
   const int* last_batch = nullptr;
@@ -463,7 +464,10 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
       // (2x), so a budget-limited cap does not reallocate every step
       const long long held_K = (long long)((double)ctx->s_rec.bytes / per_level);
       long long K = std::min(need, held_K);
-      if (held_K < 16 || need >= 2 * held_K) {
+      // (the budget is re-derived once per new `need`, not every step: a
+      // budget-capped buffer would otherwise query cudaMemGetInfo each step)
+      if (held_K < 16 || (need >= 2 * held_K && need != ctx->rec_need_tried)) {
+        ctx->rec_need_tried = need;
         double budget = env_gb * 1e9;
         if (env_gb < 0.0) {
           size_t free_b = 0, total_b = 0;
