@@ -270,3 +270,112 @@ class DistributedMapper:
                 gathered = torch.cat(parts)
             self.e.unpack_payload(all_ids, gathered)
         self.e.clear_grad()
+
+
+# ---------------------------------------------------------------- tracking
+def lm_step(jtj: np.ndarray, jtr: np.ndarray, damping: float, pose):
+    """The damped Gauss-Newton step of k_gn_step on the host: solve
+    (A + damping diag(A) + 1e-12 I) x = -J^T r, then apply x = [omega; tau] as
+    PosePerturbation::applied_to (tracking.hpp:21-26): q <- normalize(exp(omega) q),
+    t <- t + tau, exp_so3 as pose.hpp:32-41. Returns the new pose, or None if the
+    system is not positive definite (the pose is then kept)."""
+    from .api import Pose
+    A = np.array(jtj, dtype=np.float64).reshape(6, 6).copy()
+    A[np.diag_indices(6)] += damping * np.diag(A) + 1e-12
+    try:
+        L = np.linalg.cholesky(A)
+    except np.linalg.LinAlgError:
+        return None
+    x = np.linalg.solve(L.T, np.linalg.solve(L, -np.asarray(jtr, dtype=np.float64)))
+    w = x[:3]
+    angle = float(np.sqrt((w[0] * w[0] + w[1] * w[1]) + w[2] * w[2]))
+    if angle < 1e-8:
+        e = np.array([1.0, 0.5 * w[0], 0.5 * w[1], 0.5 * w[2]])
+        e /= np.linalg.norm(e)
+    else:
+        ha = 0.5 * angle
+        e = np.concatenate([[np.cos(ha)], np.sin(ha) / angle * w])
+    b = np.asarray(pose.q, dtype=np.float64)
+    q = np.array([e[0] * b[0] - e[1] * b[1] - e[2] * b[2] - e[3] * b[3],
+                  e[0] * b[1] + e[1] * b[0] + e[2] * b[3] - e[3] * b[2],
+                  e[0] * b[2] + e[2] * b[0] + e[3] * b[1] - e[1] * b[3],
+                  e[0] * b[3] + e[3] * b[0] + e[1] * b[2] - e[2] * b[1]])
+    q /= np.linalg.norm(q)
+    return Pose(tuple(q), tuple(np.asarray(pose.t, dtype=np.float64) + x[3:]))
+
+
+@dataclass
+class TrackResult:
+    pose: object
+    loss_trace: list
+    rays_used: list
+
+
+class DistributedTracker:
+    """Ray-sharded Gauss-Newton / LM tracking (the north star's
+    "tracking all-reduces only the 21+6-float normal equations"). Each rank draws
+    its own valid-depth pixels (tracking.cpp:147-166 rule, rank-specific stream),
+    evaluates their normal equations on its device (vrf_pose_normal_equations:
+    one march per ray, per-ray 4x6 Jacobian, J^T J / J^T r sums), the 21 + 6 sums,
+    the loss and the hit count are all-reduced (29 fp64 = 232 B), and every rank
+    takes the identical damped step (lm_step). Worth it only when one frame's
+    rays per iteration exceed what one GPU turns around in a few microseconds
+    (>= 64K rays); below that, tracking runs as replicas."""
+
+    def __init__(self, engine_ctx, intrinsics, config, group=None):
+        from .api import TrackingConfig
+        self.ctx = engine_ctx
+        self.intr = intrinsics
+        self.cfg = config
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.loss_cfg = TrackingConfig(lambda_p=config.lambda_p, lambda_d=config.lambda_d,
+                                       render=config.render)
+        self.device = torch.device("cuda", engine_ctx.device) \
+            if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+    def _normal_equations(self, slot, pose, pixels):
+        return self.ctx.pose_normal_equations(slot, self.intr, pose, pixels, self.loss_cfg)
+
+    def track(self, slot: int, depth: np.ndarray, init_pose, frame_seed: int = 0) -> TrackResult:
+        """Tracks the frame in context slot `slot` (its depth image on the host for
+        the pixel draws) from init_pose; cfg.iterations steps."""
+        from .api import Rng
+        n_local = self.cfg.rays_per_iteration // self.world + \
+            (1 if self.rank < self.cfg.rays_per_iteration % self.world else 0)
+        rng = Rng(self.cfg.seed + 0x9E3779B9 * frame_seed + 7919 * self.rank)
+        pose = init_pose
+        trace, used = [], []
+        for _ in range(self.cfg.iterations):
+            px = rng.draw_valid_pixels(depth, n_local, self.cfg.max_redraws)
+            v = np.zeros(29)
+            ne = None
+            if len(px):
+                try:
+                    ne = self._normal_equations(slot, pose, px)
+                except RuntimeError as e:  # this rank's rays all missed: others may not
+                    if "untrackable" not in str(e):
+                        raise
+            if ne is not None:
+                iu = np.triu_indices(6)
+                v[:21] = ne.jtj[iu]
+                v[21:27] = ne.jtr
+                v[27] = ne.loss
+                v[28] = ne.rays_used
+            t = torch.from_numpy(v).to(self.device)
+            dist.all_reduce(t, group=self.group)
+            v = t.cpu().numpy()
+            m = int(round(v[28]))
+            trace.append(v[27] / m if m else 0.0)
+            used.append(m)
+            if m == 0:  # tracking.cpp:97 on the global sample
+                raise RuntimeError("untrackable frame: all sampled rays miss the grid")
+            jtj = np.zeros((6, 6))
+            jtj[np.triu_indices(6)] = v[:21]
+            jtj = jtj + np.triu(jtj, 1).T
+            nxt = lm_step(jtj, v[21:27], self.cfg.damping, pose)
+            if nxt is None:
+                break
+            pose = nxt
+        return TrackResult(pose, trace, used)

@@ -207,3 +207,70 @@ def test_shard_ranges_cover_padded_vertices():
         spans = [shard_range(padded, world, r) for r in range(world)]
         assert spans[0][0] == 0 and spans[-1][1] == padded
         assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+class _LinearPoseCtx:
+    """Stands in for a device context in the tracker: normal equations of a
+    linear translation model r_p = J_p (t - t_true), J_p fixed per pixel."""
+    device = 0
+
+    def __init__(self, t_true):
+        self.t_true = np.asarray(t_true)
+
+    def pose_normal_equations(self, slot, intr, pose, pixels, cfg):
+        from paper_2307_03404_b200.api import NormalEquations
+        jtj = np.zeros((6, 6))
+        jtr = np.zeros(6)
+        loss = 0.0
+        for px, py in pixels:
+            g = np.random.default_rng(int(px) * 7919 + int(py))
+            J = np.zeros((4, 6))
+            J[:, 3:] = g.normal(size=(4, 3))
+            r = J[:, 3:] @ (np.asarray(pose.t) - self.t_true)
+            jtj += J.T @ J
+            jtr += J.T @ r
+            loss += float(r @ r)
+        return NormalEquations(jtj, jtr, loss, len(pixels), 0)
+
+
+def _tracker_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    sys.path.insert(0, str(ROOT))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2307_03404_b200.api import GNConfig, Pose
+        from paper_2307_03404_b200.distributed import DistributedTracker
+        t_true = (0.3, -0.2, 1.1)
+        tr = DistributedTracker(_LinearPoseCtx(t_true), None,
+                                GNConfig(rays_per_iteration=64, iterations=3, damping=0.0))
+        depth = np.ones((12, 16))
+        res = tr.track(0, depth, Pose((1.0, 0.0, 0.0, 0.0), (0.0, 0.0, 0.0)))
+        out[rank] = (tuple(res.pose.t), tuple(res.pose.q), res.rays_used)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_tracker_gloo_world2():
+    """Ray-sharded GN tracking: the all-reduced normal equations of 2 ranks x 32
+    pixels solve the linear model exactly, and both ranks take the same step."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_tracker_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    (t0, q0, u0), (t1, q1, u1) = out[0], out[1]
+    assert t0 == t1 and q0 == q1
+    assert u0 == [64, 64, 64]
+    np.testing.assert_allclose(t0, (0.3, -0.2, 1.1), atol=1e-9)
+    np.testing.assert_allclose(q0, (1.0, 0.0, 0.0, 0.0), atol=1e-12)
+
+
+def test_lm_step_matches_closed_form():
+    """lm_step: pure translation system -> t + x exactly; small rotation -> exp map."""
+    from paper_2307_03404_b200.api import Pose
+    from paper_2307_03404_b200.distributed import lm_step
+    A = np.diag([2.0, 2.0, 2.0, 4.0, 4.0, 4.0])
+    b = -A @ np.array([0.0, 0.0, 0.1, 0.01, -0.02, 0.03])  # J^T r = -A x
+    p = lm_step(A, b, 0.0, Pose((1.0, 0.0, 0.0, 0.0), (1.0, 2.0, 3.0)))
+    np.testing.assert_allclose(p.t, (1.01, 1.98, 3.03), atol=1e-12)
+    np.testing.assert_allclose(p.q, (np.cos(0.05), 0.0, 0.0, np.sin(0.05)), atol=1e-12)

@@ -196,3 +196,46 @@ def test_p2p_exchange_virtual_ranks_equal_single_gpu_step(oracle):
             assert st.samples == got_stats[k][2]
     want = b.download_grid().data
     np.testing.assert_allclose(pay[0], want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
+
+
+def _track_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from scenes import room_scene as _room
+    from paper_2307_03404_b200.api import GNConfig, Pose
+    from paper_2307_03404_b200.distributed import DistributedTracker
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        grid, intr, frames = _room(res=33, width=64, height=48)
+        ctx = Context(0)
+        ctx.load_grid(grid)
+        ctx.load_frames(intr, frames)
+        gt = np.asarray(frames[1].gt_pose.t)
+        init = Pose(frames[1].gt_pose.q, tuple(gt + [0.03, -0.02, 0.01]))
+        tr = DistributedTracker(ctx, intr, GNConfig(rays_per_iteration=2048, iterations=8))
+        r = tr.track(1, frames[1].depth, init, frame_seed=1)
+        np.save(os.path.join(out_dir, f"pose{world}_{rank}.npy"),
+                np.concatenate([r.pose.q, r.pose.t, [sum(r.rays_used)]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_distributed_tracker_converges(world, tmp_path):
+    """Ray-sharded GN tracking on the device: every rank's normal equations
+    (vrf_pose_normal_equations) all-reduced, one identical LM step per iteration.
+    World 2 runs two processes on one device with host (gloo) all-reduces."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_track_worker, args=(world, _port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    res = [np.load(tmp_path / f"pose{world}_{r}.npy") for r in range(world)]
+    for r in res[1:]:
+        assert np.array_equal(res[0], r)
+    _, _, frames = room_scene(res=33, width=64, height=48)
+    gt = np.asarray(frames[1].gt_pose.t)
+    err0 = np.linalg.norm([0.03, -0.02, 0.01])
+    assert np.linalg.norm(res[0][4:7] - gt) < 0.2 * err0
+    assert res[0][7] > 0.9 * 8 * 2048
