@@ -472,21 +472,21 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
     if (ctx->gn_graph) cudaGraphExecDestroy(ctx->gn_graph);
     ctx->gn_graph = nullptr;
     cudaGraph_t graph;
-    CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    // capture on the context's own (non-blocking) stream: the legacy default
+    // stream a caller may have selected with vrf_set_stream cannot be captured;
+    // the graph is then launched on whichever stream the context runs on
+    cudaStream_t cs = ctx->own_stream;
+    CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < iters; ++it) {
       launch_draw_strat(ctx->rgbd, ctx->d_frame, npix, intr->width, intr->height, L,
-                        cfg->max_redraws, ctx->d_gn_seed, it, (int*)ctx->s_batch.ptr, n,
-                        ctx->stream);
+                        cfg->max_redraws, ctx->d_gn_seed, it, (int*)ctx->s_batch.ptr, n, cs);
       launch_pose_fused(/*fp64_sh=*/false, g, p, cam, ctx->rgbd, ctx->d_frame, npix,
                         ctx->d_gn_pose, (const int*)ctx->s_batch.ptr, nullptr, n, cfg->lambda_p,
-                        cfg->lambda_d, (PosePartial*)ctx->s_partials.ptr, ctx->d_err,
-                        ctx->stream);
-      launch_pose_reduce2((const PosePartial*)ctx->s_partials.ptr, nb, ctx->d_pose_out,
-                          ctx->stream);
-      launch_gn_step(ctx->d_pose_out, ctx->d_gn_pose, cfg->damping, ctx->d_gn_hist, it,
-                     ctx->stream);
+                        cfg->lambda_d, (PosePartial*)ctx->s_partials.ptr, ctx->d_err, cs);
+      launch_pose_reduce2((const PosePartial*)ctx->s_partials.ptr, nb, ctx->d_pose_out, cs);
+      launch_gn_step(ctx->d_pose_out, ctx->d_gn_pose, cfg->damping, ctx->d_gn_hist, it, cs);
     }
-    CU(cudaStreamEndCapture(ctx->stream, &graph));
+    CU(cudaStreamEndCapture(cs, &graph));
     CU(cudaGraphInstantiate(&ctx->gn_graph, graph, 0));
     cudaGraphDestroy(graph);
     ctx->gn_key = key;

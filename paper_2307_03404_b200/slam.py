@@ -32,6 +32,7 @@ class SlamConfig:
     max_keyframes: int = 256
     window: int = 0                     # map over the last `window` keyframes (0 = all)
     recent_fraction: float = 0.0        # share of each mapping batch drawn from the newest keyframe
+    exchange: str = "p2p"               # multi-GPU mapping exchange (distributed=True)
     constant_velocity: bool = True      # track_sequence init policy (tracking.cpp:271-272)
     tracking: GNConfig = field(default_factory=GNConfig)
     mapping: MappingConfig = field(default_factory=lambda: MappingConfig(rays_per_batch=65536))
@@ -50,7 +51,15 @@ class SlamSystem:
     """Online tracking + keyframe mapping on one device context."""
 
     def __init__(self, ctx: Context, intrinsics: CameraIntrinsics, geometry: GridGeometry,
-                 config: SlamConfig):
+                 config: SlamConfig, distributed: bool = False):
+        """distributed: one process per GPU (torch.distributed initialised, the
+        context created with shard_multiple=world and running on torch's current
+        stream). Every rank holds the whole grid and every keyframe and tracks
+        every frame as a replica (the GN frame graph is deterministic and the maps
+        are identical after each exchange, so the replicas agree without
+        communication); each keyframe's mapping steps are ray-sharded: a rank draws
+        rays_per_batch / world rays from its own stream and the gradients are
+        combined by the mapper's exchange (default: the fused peer-memory kernel)."""
         self.ctx = ctx
         self.intr = intrinsics
         self.cfg = config
@@ -58,12 +67,46 @@ class SlamSystem:
         ctx.reserve_frames(intrinsics, config.max_keyframes + 1)
         self.track_slot = config.max_keyframes
         self.n_keyframes = 0
-        self.rng = Rng(config.mapping.seed)
+        self.mapper = None
+        rank = 0
+        if distributed:
+            import torch.distributed as dist
+            from .distributed import DistributedMapper, GpuEngine
+            ctx.rmsprop_reset()
+            self.mapper = DistributedMapper(GpuEngine(ctx, config.mapping))
+            rank = dist.get_rank()
+        self.rng = Rng(config.mapping.seed + 7919 * rank)
         self.poses: List[Pose] = []
         self.log: List[SlamFrameLog] = []
 
+    def _draw(self, n: int) -> np.ndarray:
+        """One mapping batch of n rays under the keyframe policy (recent share,
+        window, or uniform over all keyframes)."""
+        w, h = self.intr.width, self.intr.height
+        f = self.cfg.recent_fraction
+        if f > 0.0 and self.n_keyframes > 1:
+            n_new = int(round(f * n))
+            a = self.rng.draw_batch(1, w, h, n_new)
+            a[:, 0] = self.n_keyframes - 1
+            b = self.rng.draw_batch(self.n_keyframes, w, h, n - n_new)
+            return np.concatenate([a, b])
+        if self.cfg.window <= 0 or self.cfg.window >= self.n_keyframes:
+            return self.rng.draw_batch(self.n_keyframes, w, h, n)
+        first = self.n_keyframes - self.cfg.window
+        b = self.rng.draw_batch(self.cfg.window, w, h, n)
+        b[:, 0] += first
+        return b
+
     def _map(self, steps: int):
         m = self.cfg.mapping
+        if self.mapper is not None:
+            import torch
+            world = self.mapper.world
+            n = m.rays_per_batch // world + (1 if self.mapper.rank < m.rays_per_batch % world else 0)
+            for _ in range(steps):
+                b = torch.from_numpy(self._draw(n)).to(self.mapper.e.grad.device)
+                self.mapper.step(b, m.lambda_d, exchange=self.cfg.exchange)
+            return
         f = self.cfg.recent_fraction
         if f > 0.0 and self.n_keyframes > 1:
             # newest keyframe over-sampled: the region the camera just entered is

@@ -56,3 +56,53 @@ def test_slam_maps_and_tracks_online():
     # the bootstrap map renders the first view far better than the sigma_init fog
     q = metrics.evaluate_map_quality(ctx, intr, frames, [0], images=1, pixels_per_image=2000)
     assert q.psnr_db > 14.0
+
+
+def _slam_worker(rank, world, port, out_dir):
+    import os
+    import sys
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(__file__))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gt, intr, frames, poses, ts = _scene(8)
+        cfg = SlamConfig(keyframe_stride=4, map_steps=10, bootstrap_steps=100, max_keyframes=4,
+                         tracking=GNConfig(rays_per_iteration=4096, iterations=6, lambda_d=0.1),
+                         mapping=MappingConfig(rays_per_batch=4096))
+        ctx = Context(0, shard_multiple=world)
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        slam = SlamSystem(ctx, intr,
+                          GridGeometry(gt.geom.res, gt.geom.origin, gt.geom.voxel_size), cfg,
+                          distributed=True)
+        for f in frames:
+            slam.process(f)
+        torch.cuda.synchronize()
+        np.save(os.path.join(out_dir, f"poses{rank}.npy"),
+                np.array([list(p.q) + list(p.t) for p in slam.poses]))
+        np.save(os.path.join(out_dir, f"grid{rank}.npy"), ctx.download_grid().data)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slam_distributed_replicas_agree(tmp_path):
+    """Multi-GPU SLAM (slam.SlamSystem(distributed=True)): two ranks on one
+    device (gloo host collectives, CUDA IPC peer table for the fused exchange).
+    Keyframe mapping is ray-sharded, tracking runs as replicas: both ranks must
+    hold the same map and the same trajectory."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.start_processes(_slam_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    p0, p1 = (np.load(tmp_path / f"poses{r}.npy") for r in range(2))
+    g0, g1 = (np.load(tmp_path / f"grid{r}.npy") for r in range(2))
+    assert np.array_equal(g0, g1)
+    assert np.array_equal(p0, p1)
+    assert p0.shape == (8, 7) and np.all(np.isfinite(p0))

@@ -9,6 +9,7 @@ depth L1 on held-out views rendered from the SLAM map.
 """
 import argparse
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -47,7 +48,19 @@ def main():
     ap.add_argument("--gt-map", action="store_true",
                     help="plumbing check: track against the ground-truth map, no mapping")
     ap.add_argument("--out", default="")
+    ap.add_argument("--distributed", action="store_true",
+                    help="one process per GPU under torchrun: ray-sharded keyframe mapping "
+                         "(fused peer-memory exchange), tracking replicas")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    distributed = args.distributed or world > 1
+    if distributed:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
 
     room = synth.Room().scaled(7.0 / 4.0, 6.0 / 4.0, 1.0)
     gt = synth.scene_grid(args.res, room, seed=2, prune_tau=1e-3)
@@ -56,7 +69,7 @@ def main():
                                   args.height / 2 - 0.5, args.width, args.height, 6553.5)
     poses, ts = synth.ellipse_trajectory(args.loop, room)
     poses, ts = poses[:args.frames], ts[:args.frames]
-    sensor = Context(0)
+    sensor = Context(local)
     sensor.load_grid(gt)
 
     def frame(i):
@@ -72,8 +85,12 @@ def main():
                                        lambda_d=args.track_lambda_d),
                      mapping=MappingConfig(rays_per_batch=args.map_rays,
                                            sigma_init=args.sigma_init))
-    ctx = Context(0)
-    slam = SlamSystem(ctx, intr, geom, cfg)
+    if distributed:
+        ctx = Context(local, shard_multiple=world)
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    else:
+        ctx = Context(local)
+    slam = SlamSystem(ctx, intr, geom, cfg, distributed=distributed)
     if args.gt_map:
         ctx.load_grid(gt)
         cfg.bootstrap_steps = cfg.map_steps = 0
@@ -110,6 +127,8 @@ def main():
         "config": f"config5: SLAM, {args.width}x{args.height}, {args.res}^3 grid, "
                   f"closed-loop ellipse of {args.loop} frames",
         "frames": args.frames, "keyframes": slam.n_keyframes,
+        "mapping": ("ray-sharded over %d GPUs, %s exchange; tracking replicas" % (world, cfg.exchange))
+        if distributed else "1 GPU",
         "frames_per_s": n / slam_s if slam_s > 0 else None,
         "track_ms_per_frame": float(np.mean([l.track_ms for l in logs])) if n else None,
         "map_ms_per_keyframe": float(np.mean([l.map_ms for l in logs if l.keyframe]))
@@ -124,6 +143,11 @@ def main():
                      "track": f"GN {args.track_rays} rays x {args.track_iters} it"},
         "sensor_render_s": gen_s,
     }
+    out["n_gpus"] = world
+    if distributed:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
     line = json.dumps(out)
     print(line)
     if args.out:
