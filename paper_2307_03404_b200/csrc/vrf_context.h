@@ -419,7 +419,10 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
   int rc = resolve_params(ctx, &cfg->render, &p);
   if (rc) return rc;
   const bool warp = fast && ctx->map_kernel == 1;
-  const int nb = warp ? warp_kernel_blocks() : map_forward_blocks(n > 0 ? n : 1);
+  // (the record path may run the 8-lanes-per-ray K0g: size the partials for it)
+  const int nb = warp ? warp_kernel_blocks()
+                      : std::max(map_forward_blocks(n > 0 ? n : 1),
+                                 fast ? map_forward_rec_blocks(n > 0 ? n : 1) : 0);
   const size_t nn = (size_t)(n > 0 ? n : 1);
   if ((rc = ensure(ctx, ctx->s_raycd, sizeof(double4) * nn))) return rc;
   if ((rc = ensure(ctx, ctx->s_flags, nn))) return rc;
@@ -520,7 +523,11 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
   } else {
     CU(cudaMemsetAsync(ctx->s_partials.ptr, 0, sizeof(MapPartial), ctx->stream));
   }
-  launch_map_reduce((const MapPartial*)ctx->s_partials.ptr, n > 0 ? nb : 0, ctx->d_stats,
+  // partials the launched forward wrote (K0g: 16 rays per CTA)
+  const int nparts = warp ? nb
+                          : ((n > 0 && fast && ctx->rec_K > 0) ? map_forward_rec_blocks(n)
+                                                                 : map_forward_blocks(n > 0 ? n : 1));
+  launch_map_reduce((const MapPartial*)ctx->s_partials.ptr, n > 0 ? nparts : 0, ctx->d_stats,
                     ctx->stream);
   LAUNCHED(1);
   CU(cudaGetLastError());

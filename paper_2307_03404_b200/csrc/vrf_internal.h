@@ -56,6 +56,8 @@ void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cu
 // Fast forward that also stores up to K SampleRec per ray, warp-tiled sample-major
 // (rec_index(slot, c, K), slot = coherent order index); rays with more samples get
 // kOverflow. rec_count[slot] = samples stored.
+// CTAs of the K0 launch for n rays (the small-batch K0g has 16 rays per CTA).
+int map_forward_rec_blocks(int n);
 void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
                             const double4* rgbd, const DevPose* poses, int n_frames,
                             const int* batch, int n, double4* ray_cd, uint8_t* flags,

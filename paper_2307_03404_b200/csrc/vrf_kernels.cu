@@ -432,6 +432,178 @@ __device__ __forceinline__ void map_backward_ray(const DevGrid& g, const DevPara
   }
 }
 
+// K0g: K0 for small batches, 8 lanes per ray. Below ~1e5 rays the thread-per-
+// ray K0 leaves one warp per SM sub-partition and each sample is a serial chain
+// of 56 gathers and the FP64 march (16K rays: ~10 us per sample). Here the ray
+// group locates 8 segments at once (GroupMarch) and each lane gathers one
+// trilinear corner. sigma_raw is summed from the lanes' w_k * sigma_k products
+// in corner order and the colour from their (w_k, basis-contracted corner
+// colour) pairs, again in corner order, so samples, T, records and outputs are
+// bit-identical to K0 (k_map_forward_rec). Lane 0 of the group writes.
+constexpr int kFwdLanes = 8;
+__global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
+    double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
+    const uint32_t* __restrict__ order, SampleRec* __restrict__ rec, int K,
+    int* __restrict__ rec_count) {
+  constexpr int LPR = kFwdLanes;
+  __shared__ double s_d[32];
+  __shared__ long long s_l[32];
+  __shared__ int s_i[32];
+  const int lane = threadIdx.x & 31, sub = lane & (LPR - 1), gbase = lane & ~(LPR - 1);
+  const unsigned gmask = ((1u << LPR) - 1u) << gbase;
+  const bool lead = sub == 0;
+  const int t = blockIdx.x * (kThreads / LPR) + threadIdx.x / LPR;
+  const int i = (order && t < n) ? (int)order[t] : t;
+  double lp = 0.0, lg = 0.0;
+  long long samples = 0;
+  int mc = 0, md = 0, bad = INT_MAX;
+  if (t < n) {
+    const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
+    uint8_t fl = 0;
+    int stored = 0;
+    if (f < 0 || f >= n_frames || px < 0 || px >= cam.width || py < 0 || py >= cam.height) {
+      if (lead) atomicOr(err, 2);  // generate_ray: pixel outside image
+    } else {
+      March m;
+      ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+      Composite st;
+      st.T = 1.0;
+      st.C[0] = st.C[1] = st.C[2] = 0.0;
+      st.D = 0.0;
+      st.count = 0;
+      st.terminated = false;
+      float bf[9];
+      bool basis_ok;
+      {
+        double basis[9];
+        basis_ok = sh_basis(m.d, basis);
+#pragma unroll
+        for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
+      }
+      if (!basis_ok) {
+        if (lead) atomicOr(err, 1);
+      } else if (march_begin(g, p, m)) {
+        Sample s;
+        GroupMarch<LPR> gm;
+        const int k = sub, dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+        while (gm.next(g, m, s, sub, gbase, gmask)) {
+          // this lane's corner: weight (corner_weights order), payload, contraction
+          const double wxk = dx ? s.fx : dsub(1.0, s.fx);
+          const double wyk = dy ? s.fy : dsub(1.0, s.fy);
+          const double wzk = dz ? s.fz : dsub(1.0, s.fz);
+          const double wk = dmul(dmul(wxk, wyk), wzk);
+          const float4* vp = g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
+          float v[28];
+#pragma unroll
+          for (int j = 0; j < kVec4PerVertex; ++j) {
+            const float4 a = __ldg(vp + j);
+            v[4 * j] = a.x;
+            v[4 * j + 1] = a.y;
+            v[4 * j + 2] = a.z;
+            v[4 * j + 3] = a.w;
+          }
+          const double pk = dmul(wk, (double)v[0]);
+          float dr = 0.f, dg = 0.f, db = 0.f;
+#pragma unroll
+          for (int mm = 0; mm < 9; ++mm) {
+            dr = fmaf(bf[mm], v[1 + mm], dr);
+            dg = fmaf(bf[mm], v[10 + mm], dg);
+            db = fmaf(bf[mm], v[19 + mm], db);
+          }
+          const float wkf = (float)wk;
+          Shade sh;
+          double sraw = 0.0;
+          float cr = 0.f, cg = 0.f, cb = 0.f;
+#pragma unroll
+          for (int j = 0; j < LPR; ++j) {  // corner order, identical on every lane
+            sraw = dadd(sraw, __shfl_sync(gmask, pk, gbase + j));
+            const float wj = __shfl_sync(gmask, wkf, gbase + j);
+            cr = fmaf(wj, __shfl_sync(gmask, dr, gbase + j), cr);
+            cg = fmaf(wj, __shfl_sync(gmask, dg, gbase + j), cg);
+            cb = fmaf(wj, __shfl_sync(gmask, db, gbase + j), cb);
+          }
+          sh.sigma_raw = sraw;
+          const float col[3] = {cr, cg, cb};
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const double cv = 0.5 + (double)col[ch];
+            sh.clamped[ch] = (cv <= 0.0 || cv >= 1.0);
+            sh.c[ch] = (cv < 0.0) ? 0.0 : ((1.0 < cv) ? 1.0 : cv);
+          }
+          double decay;
+          const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
+          if (lead && st.count <= K) {
+            const uint32_t kf = ((uint32_t)gm.seg << 4) | (sh.clamped[0] ? 1u : 0u) |
+                                (sh.clamped[1] ? 2u : 0u) | (sh.clamped[2] ? 4u : 0u) |
+                                (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
+            float2* d = reinterpret_cast<float2*>(rec + rec_index(t, st.count - 1, K));
+            d[0] = make_float2((float)wgt, (float)st.T);
+            d[1] = make_float2((float)sh.c[0], (float)sh.c[1]);
+            d[2] = make_float2((float)sh.c[2], __uint_as_float(kf));
+          }
+          if (st.terminated) break;
+        }
+      }
+      if (st.count == 0) {
+        st.C[0] = st.C[1] = st.C[2] = 0.0;
+        st.D = 0.0;
+      }
+      const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+      if (st.count > 0) {
+        fl |= kHit;
+        if (st.count > K) fl |= kOverflow;
+        stored = st.count > K ? 0 : st.count;
+        mc = 1;
+        samples = st.count;
+        const double r0 = dsub(st.C[0], tg.x), r1 = dsub(st.C[1], tg.y), r2 = dsub(st.C[2], tg.z);
+        const double sq = dadd(dadd(dmul(r0, r0), dmul(r1, r1)), dmul(r2, r2));
+        if (!isfinite(sq) || !isfinite(st.D)) {
+          bad = i;
+        } else {
+          lp = sq;
+          if (tg.w > 0.0) {
+            fl |= kDepthValid;
+            md = 1;
+            const double dr = dsub(st.D, tg.w);
+            lg = dmul(dr, dr);
+          }
+        }
+      }
+      if (lead) ray_cd[i] = make_double4(st.C[0], st.C[1], st.C[2], st.D);
+    }
+    if (lead) {
+      flags[i] = fl;
+      rec_count[t] = stored;
+    }
+  }
+  if (!lead) {  // one contribution per ray
+    lp = lg = 0.0;
+    samples = 0;
+    mc = md = 0;
+    bad = INT_MAX;
+  }
+  const double blp = block_sum(lp, s_d);
+  const double blg = block_sum(lg, s_d);
+  const long long bs = block_sum(samples, s_l);
+  const int bmc = block_sum(mc, s_i);
+  const int bmd = block_sum(md, s_i);
+  const int bbad = block_min(bad, s_i);
+  const int bmax = -block_min(-(int)samples, s_i);
+  if (threadIdx.x == 0) {
+    MapPartial q;
+    q.lp = blp;
+    q.lg = blg;
+    q.samples = bs;
+    q.m_c = bmc;
+    q.m_d = bmd;
+    q.bad = bbad;
+    q.max_count = bmax;
+    partials[blockIdx.x] = q;
+  }
+}
+
 // Scatter sinks: where an aggregated corner (4 factors x SH basis = 28 slots)
 // goes. RedSink issues 7 red.global.add.v4.f32 from registers (default).
 // BulkSink writes the 112-B vertex gradient into a per-thread shared-memory ring
@@ -1579,11 +1751,31 @@ void launch_map_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                                                       ray_cd, flags, partials, ray_count, err,
                                                       order);
 }
+// Rays up to which K0 runs 8 lanes per ray (K0g); VRF_FWD_GROUP_MAX overrides.
+// r01 (config-3 scene, forward ms, K0g vs K0): 4K rays 0.67 vs 2.08, 16K 0.99
+// vs 1.91, 32K 1.60 vs 1.87, 48K 2.18 vs 1.82 -> crossover ~40K.
+int fwd_group_max() {
+  static const int v = [] {
+    const char* e = std::getenv("VRF_FWD_GROUP_MAX");
+    return e ? std::atoi(e) : 40000;
+  }();
+  return v;
+}
+int map_forward_rec_blocks(int n) {
+  return n <= fwd_group_max() ? (n + kThreads / kFwdLanes - 1) / (kThreads / kFwdLanes)
+                              : map_forward_blocks(n);
+}
 void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
                             const double4* rgbd, const DevPose* poses, int n_frames,
                             const int* batch, int n, double4* ray_cd, uint8_t* flags,
                             MapPartial* partials, int* err, const uint32_t* order, SampleRec* rec,
                             int K, int* rec_count, cudaStream_t s) {
+  if (n <= fwd_group_max()) {
+    k_map_forward_rec_g<<<map_forward_rec_blocks(n), kThreads, 0, s>>>(
+        g, p, cam, rgbd, poses, n_frames, batch, n, ray_cd, flags, partials, err, order, rec, K,
+        rec_count);
+    return;
+  }
   k_map_forward_rec<<<map_forward_blocks(n), kThreads, 0, s>>>(g, p, cam, rgbd, poses, n_frames,
                                                                batch, n, ray_cd, flags, partials,
                                                                err, order, rec, K, rec_count);

@@ -247,75 +247,6 @@ __global__ void __launch_bounds__(kT) k_pose_fused(
   }
 }
 
-// ------------------------------------------------------------------ group march
-// The LPR lanes of a ray group march together: a batch evaluates the next LPR
-// segments at once (lane j: segment k + j — position, locate, occupancy), a
-// group ballot marks the active ones, and next() hands them out in segment
-// order (the sample's fields are shuffled from the lane that located it).
-// Segments are independent given the occupancy, so this yields exactly the
-// sequential march_next sequence (renderer.cpp:62-79): inactive / out-of-grid
-// segments are dropped in order, and an all-inactive batch whose last
-// empty-block lane lies in an empty 8^3 block / 64^3 superblock jumps past
-// that box (skip_empty_box: only segments whose midpoints stay inside the empty
-// box are skipped). Empty space inside occupied blocks then costs one batch per
-// LPR segments instead of one iteration per segment.
-template <int LPR>
-struct GroupMarch {
-  Sample mine;       // this lane's segment of the current batch
-  unsigned act = 0;  // active segments of the batch not yet handed out (group bits)
-
-  __device__ __forceinline__ bool next(const DevGrid& g, March& m, Sample& s, int sub, int gbase,
-                                       unsigned gmask) {
-    constexpr unsigned kLow = (LPR == 32) ? 0xffffffffu : ((1u << LPR) - 1u);
-    while (act == 0) {
-      if (m.k >= m.nseg) return false;
-      const long long kk = m.k + sub;
-      bool a = false, eb = false;
-      if (kk < m.nseg) {
-        const double s0 = dadd(m.lo, dmul((double)kk, m.step));
-        const double s0s = dadd(s0, m.step);
-        const double s1 = (m.hi < s0s) ? m.hi : s0s;
-        const double len = dsub(s1, s0);
-        if (len >= 1e-12) {
-          const double tm = dmul(0.5, dadd(s0, s1));
-          const double p[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
-                               dadd(m.o[2], dmul(tm, m.d[2]))};
-          if (locate(g, p, mine)) {
-            if (cell_active(g, mine.cell)) {
-              a = true;
-              mine.t = tm;
-              mine.delta = len;
-            } else {
-              eb = !block_active(g, mine.cx, mine.cy, mine.cz);
-            }
-          }
-        }
-      }
-      act = (__ballot_sync(gmask, a) >> gbase) & kLow;
-      const unsigned ebm = (__ballot_sync(gmask, eb) >> gbase) & kLow;
-      m.k += LPR;
-      if (act == 0 && ebm) {
-        const int j = 31 - __clz(ebm);
-        long long kn = 0;
-        if (sub == j)
-          kn = skip_empty_box(g, m, mine,
-                              super_active(g, mine.cx, mine.cy, mine.cz) ? kBlockLog2 : kSuperLog2);
-        kn = __shfl_sync(gmask, kn, gbase + j);
-        if (kn > m.k) m.k = kn;
-      }
-    }
-    const int src = gbase + (__ffs(act) - 1);
-    act &= act - 1;
-    s.t = __shfl_sync(gmask, mine.t, src);
-    s.delta = __shfl_sync(gmask, mine.delta, src);
-    s.fx = __shfl_sync(gmask, mine.fx, src);
-    s.fy = __shfl_sync(gmask, mine.fy, src);
-    s.fz = __shfl_sync(gmask, mine.fz, src);
-    s.base = __shfl_sync(gmask, mine.base, src);
-    return true;
-  }
-};
-
 // ------------------------------------------------------------------ corner-parallel
 // LPR lanes per ray (LPR = 8: one trilinear corner per lane). The tracking batch
 // is small (16,384 rays = 111 threads per SM at one thread per ray), so the

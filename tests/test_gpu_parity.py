@@ -474,3 +474,39 @@ def test_sensor_format_frames_equal_the_double_path(ctx, oracle):
     b = ctx.track_frame(1, intr, init, cfg)
     assert np.array_equal(np.asarray(a.pose.t), np.asarray(b.pose.t))
     assert a.loss_trace == b.loss_trace
+
+
+def test_small_batch_group_forward_equals_thread_forward(tmp_path):
+    """K0g (8 lanes per ray, small batches) against the thread-per-ray K0
+    (VRF_FWD_GROUP_MAX=0 forces it): the same composited samples and hit counts,
+    the same loss to the last bits of the fixed-order block sums, and one fast
+    mapping step's gradient to fp32 atomics-order noise."""
+    import subprocess
+    import sys as _sys
+    script = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, "."); sys.path.insert(0, "oracle")
+from scenes import room_scene, fresh_grid
+from paper_2307_03404_b200 import Context, MappingConfig
+import oracle as orc
+grid, intr, frames = room_scene(res=33)
+ctx = Context(0)
+ctx.load_grid(fresh_grid(grid)); ctx.load_frames(intr, frames)
+batch = orc.Oracle().draw_batch(5, len(frames), intr.width, intr.height, 3000)
+g, st = ctx.mapping_gradient(MappingConfig(), batch)
+np.savez(sys.argv[1], g=g, s=np.array([st.samples, st.rays_color, st.rays_depth]),
+         l=np.array([st.loss_photometric, st.loss_geometric]))
+'''
+    outs = []
+    for thread in (False, True):
+        env = dict(os.environ)
+        if thread:
+            env["VRF_FWD_GROUP_MAX"] = "0"
+        f = tmp_path / f"k{int(thread)}.npz"
+        subprocess.run([_sys.executable, "-c", script, str(f)], check=True, env=env,
+                       cwd=str(Path(__file__).resolve().parent.parent))
+        outs.append(np.load(f))
+    a, b = outs
+    assert np.array_equal(a["s"], b["s"])
+    np.testing.assert_allclose(a["l"], b["l"], rtol=1e-13)
+    assert np.max(np.abs(a["g"] - b["g"])) <= 1e-4 * np.max(np.abs(b["g"]))
