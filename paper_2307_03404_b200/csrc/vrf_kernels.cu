@@ -983,6 +983,143 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
   sink.finish();
 }
 
+// K2g: the record walk for small batches, 8 lanes per ray. Below ~40K rays the
+// thread-per-ray K2 runs one warp per SM sub-partition or less and each ray's
+// ~200 records are a serial chain. Here the ray's records are split into 8
+// contiguous chunks. Pass 1: every lane sums its chunk's c_ch w and t w. A
+// shuffle suffix-scan gives each lane the sums of the records after its chunk
+// (the starting Sc / Sd of the reverse walk). Pass 2: every lane walks its chunk
+// backwards exactly as K2 does (suffix-form dL/dsigma, per-lane corner
+// aggregation, face-shift carries, red.v4 flushes; chunk ends flush their
+// cell). Same gradient up to fp32 summation order.
+__global__ void __launch_bounds__(kThreads) k_map_backward_g(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
+    const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
+    const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
+    float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
+    const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
+  constexpr int LPR = 8;
+  const int lane = threadIdx.x & 31, sub = lane & (LPR - 1), gbase = lane & ~(LPR - 1);
+  const unsigned gmask = ((1u << LPR) - 1u) << gbase;
+  const int t = blockIdx.x * (kThreads / LPR) + threadIdx.x / LPR;
+  if (t >= n) return;  // group-uniform
+  const int i = order ? (int)order[t] : t;
+  const MapStats st = *stats;
+  if (st.bad != INT_MAX) return;
+  const uint8_t fl = flags[i];
+  if (!(fl & kHit) || (fl & kOverflow)) return;
+  const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
+  const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+  MapUp u;
+  if (!map_upstream(st, global_counts, ray_cd[i], tg, fl, lambda_d, u)) return;
+  March m;
+  ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+  float bf[9];
+  {
+    double basis[9];
+    if (!sh_basis(m.d, basis)) return;
+#pragma unroll
+    for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
+  }
+  if (!march_begin(g, p, m)) return;
+  const int cnt = rec_count[t];
+  const int L = (cnt + LPR - 1) / LPR;
+  const int c0 = sub * L, c1 = min(cnt, c0 + L);  // this lane's records [c0, c1)
+  // pass 1: chunk sums of c_ch w and t w
+  double P0 = 0.0, P1 = 0.0, P2 = 0.0, Pd = 0.0;
+  for (int c = c0; c < c1; ++c) {
+    const float2* q = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
+    const float2 q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
+    const double kseg = (double)(__float_as_uint(q2.y) >> 4);
+    const double s0 = dadd(m.lo, dmul(kseg, m.step));
+    const double s0s = dadd(s0, m.step);
+    const double s1 = (m.hi < s0s) ? m.hi : s0s;
+    const double tm = dmul(0.5, dadd(s0, s1));
+    const double w = (double)q0.x;
+    P0 += (double)q1.x * w;
+    P1 += (double)q1.y * w;
+    P2 += (double)q2.x * w;
+    Pd += tm * w;
+  }
+  // suffix sums of the later chunks (lanes sub+1 .. 7)
+  double Sc0 = 0.0, Sc1 = 0.0, Sc2 = 0.0, Sd = 0.0;
+#pragma unroll
+  for (int j = LPR - 1; j > 0; --j) {
+    const double a0 = __shfl_sync(gmask, P0, gbase + j), a1 = __shfl_sync(gmask, P1, gbase + j);
+    const double a2 = __shfl_sync(gmask, P2, gbase + j), ad = __shfl_sync(gmask, Pd, gbase + j);
+    if (j > sub) {
+      Sc0 += a0;
+      Sc1 += a1;
+      Sc2 += a2;
+      Sd += ad;
+    }
+  }
+  const double upc0 = u.upc[0], upc1 = u.upc[1], upc2 = u.upc[2];
+  const bool use_depth = u.use_depth;
+  const double upd = use_depth ? u.upd : 0.0;
+  float a[4][8];
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[cc][k] = 0.f;
+  uint32_t cur = 0xffffffffu;
+  int pcx = 0, pcy = 0, pcz = 0;
+  int last_tb = -1;
+  RedSink sink{grad};
+  for (int c = c1 - 1; c >= c0; --c) {
+    const float2* q = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
+    const float2 q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
+    const uint32_t kf = __float_as_uint(q2.y);
+    const double kseg = (double)(kf >> 4);
+    const double s0 = dadd(m.lo, dmul(kseg, m.step));
+    const double s0s = dadd(s0, m.step);
+    const double s1 = (m.hi < s0s) ? m.hi : s0s;
+    const double delta = dsub(s1, s0);
+    const double tm = dmul(0.5, dadd(s0, s1));
+    const double pp[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
+                          dadd(m.o[2], dmul(tm, m.d[2]))};
+    Sample s;
+    locate(g, pp, s);
+    const double w = (double)q0.x, Tn = (double)q0.y;
+    const double cr = (double)q1.x, cg = (double)q1.y, cb = (double)q2.x;
+    double ds = upc0 * (cr * Tn - Sc0) + upc1 * (cg * Tn - Sc1) + upc2 * (cb * Tn - Sc2);
+    if (use_depth) ds += upd * (tm * Tn - Sd);
+    ds *= delta;
+    Sc0 += cr * w;
+    Sc1 += cg * w;
+    Sc2 += cb * w;
+    Sd += tm * w;
+    if (s.base != cur) {
+      if (cur != 0xffffffffu) move_cell(sink, g, cur, s.cx - pcx, s.cy - pcy, s.cz - pcz, a, bf);
+      cur = s.base;
+      pcx = s.cx;
+      pcy = s.cy;
+      pcz = s.cz;
+      mark_touched(g, s.cx, s.cy, s.cz, last_tb);
+    }
+    const float wf = q0.x;
+    const float u0 = (kf & kRecSigmaPos) ? (float)ds : 0.f;
+    const float u1 = (kf & 1u) ? 0.f : (float)upc0 * wf;
+    const float u2 = (kf & 2u) ? 0.f : (float)upc1 * wf;
+    const float u3 = (kf & 4u) ? 0.f : (float)upc2 * wf;
+    const float fx = (float)s.fx, fy = (float)s.fy, fz = (float)s.fz;
+    const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
+      a[0][k] = fmaf(wk, u0, a[0][k]);
+      a[1][k] = fmaf(wk, u1, a[1][k]);
+      a[2][k] = fmaf(wk, u2, a[2][k]);
+      a[3][k] = fmaf(wk, u3, a[3][k]);
+    }
+  }
+  if (cur != 0xffffffffu) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) flush_corner(sink, g, cur, a, bf, k);
+  }
+}
+
 // K2q: the same reverse walk with a DEFERRED, convergent scatter. The flush of a
 // departing corner is the divergent part of K2 (a lane moves cell every ~2
 // samples, at a different iteration from its neighbours: ncu r01 v19 shows ~70%
@@ -1780,6 +1917,17 @@ void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& 
                                                                batch, n, ray_cd, flags, partials,
                                                                err, order, rec, K, rec_count);
 }
+// Rays up to which K2 runs 8 lanes per ray (K2g); VRF_BWD_GROUP_MAX overrides.
+// r01 (config-3 scene, backward ms, K2g vs K2q): 4K rays 0.19 vs 1.07, 16K 0.41
+// vs 1.04, 32K 0.67 vs 1.22, 64K 1.19 vs 1.80, 128K 2.17 vs 2.50, 256K 4.23 vs
+// 4.13 -> crossover ~200K.
+static int bwd_group_max() {
+  static const int v = [] {
+    const char* e = std::getenv("VRF_BWD_GROUP_MAX");
+    return e ? std::atoi(e) : 160000;
+  }();
+  return v;
+}
 void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
                              const double4* rgbd, const DevPose* poses, const int* batch, int n,
                              const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
@@ -1807,6 +1955,12 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
   }();
   const int blocks = (n + kThreads - 1) / kThreads;
   const int minb = minb_env ? minb_env : (direct ? 3 : 4);
+  if (n <= bwd_group_max()) {  // small batch: 8 lanes per ray (K2g)
+    k_map_backward_g<<<(n + kThreads / 8 - 1) / (kThreads / 8), kThreads, 0, s>>>(
+        g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
+        order, rec, K, rec_count);
+    return;
+  }
   if (!direct) {
 #define VRF_Q_LAUNCH(MB)                                                                        \
   do {                                                                                          \

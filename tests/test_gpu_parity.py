@@ -476,9 +476,9 @@ def test_sensor_format_frames_equal_the_double_path(ctx, oracle):
     assert a.loss_trace == b.loss_trace
 
 
-def test_small_batch_group_forward_equals_thread_forward(tmp_path):
-    """K0g (8 lanes per ray, small batches) against the thread-per-ray K0
-    (VRF_FWD_GROUP_MAX=0 forces it): the same composited samples and hit counts,
+def test_small_batch_group_kernels_equal_thread_kernels(tmp_path):
+    """K0g / K2g (8 lanes per ray, small batches) against the thread-per-ray K0 /
+    K2 (VRF_FWD_GROUP_MAX=VRF_BWD_GROUP_MAX=0): the same composited samples and hit counts,
     the same loss to the last bits of the fixed-order block sums, and one fast
     mapping step's gradient to fp32 atomics-order noise."""
     import subprocess
@@ -502,6 +502,7 @@ np.savez(sys.argv[1], g=g, s=np.array([st.samples, st.rays_color, st.rays_depth]
         env = dict(os.environ)
         if thread:
             env["VRF_FWD_GROUP_MAX"] = "0"
+            env["VRF_BWD_GROUP_MAX"] = "0"
         f = tmp_path / f"k{int(thread)}.npz"
         subprocess.run([_sys.executable, "-c", script, str(f)], check=True, env=env,
                        cwd=str(Path(__file__).resolve().parent.parent))
