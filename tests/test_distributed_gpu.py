@@ -198,7 +198,7 @@ def test_p2p_exchange_virtual_ranks_equal_single_gpu_step(oracle):
     np.testing.assert_allclose(pay[0], want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
 
 
-def _track_worker(rank, world, port, out_dir):
+def _track_worker(rank, world, port, out_dir, backend="gloo"):
     import sys
     sys.path.insert(0, os.path.dirname(__file__))
     from scenes import room_scene as _room
@@ -207,7 +207,7 @@ def _track_worker(rank, world, port, out_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world))
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group(backend, rank=rank, world_size=world)
     try:
         grid, intr, frames = _room(res=33, width=64, height=48)
         ctx = Context(0)
@@ -223,13 +223,13 @@ def _track_worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_distributed_tracker_converges(world, tmp_path):
+@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo")])
+def test_distributed_tracker_converges(world, backend, tmp_path):
     """Ray-sharded GN tracking on the device: every rank's normal equations
     (vrf_pose_normal_equations) all-reduced, one identical LM step per iteration.
     World 2 runs two processes on one device with host (gloo) all-reduces."""
     import torch.multiprocessing as mp
-    mp.start_processes(_track_worker, args=(world, _port(), str(tmp_path)), nprocs=world,
+    mp.start_processes(_track_worker, args=(world, _port(), str(tmp_path), backend), nprocs=world,
                        join=True, start_method="spawn")
     res = [np.load(tmp_path / f"pose{world}_{r}.npy") for r in range(world)]
     for r in res[1:]:
