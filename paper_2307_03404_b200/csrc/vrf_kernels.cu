@@ -1132,6 +1132,7 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 // ring (warp-uniform exit; lanes without a ray just help drain).
 constexpr int kQ = 16;  // ring entries per thread (power of 2); a step enqueues <= 8
 constexpr int kQSmemBytes = kQ * kThreads * (16 + 4);
+constexpr int kQMergeSmemBytes = kQSmemBytes + kThreads * kVec4PerVertex * 16;
 struct QueueSink {
   uint32_t* qv;  // [kQ][kThreads] vertex ids
   float4* qa;    // [kQ][kThreads] (a_sigma, a_r, a_g, a_b)
@@ -1149,14 +1150,69 @@ struct QueueSink {
 #ifdef VRF_QSTATS
 __device__ unsigned long long g_qstats[4];  // pops, merged-away pops, rounds, active lanes
 #endif
-// One pop round: the lane's oldest queued corner -> basis expansion + 7 red.v4.
-// Measured alternative (r01, VRF_QSTATS counters): the ~28 lanes popping together
-// often hold the same vertex (33% of pops duplicate another lane's vertex in the
-// same round). Merging those groups (__match_any_sync, members stage their
-// 28-vector in shared memory, the leader sums and issues the only reds) cut the
-// L2 reductions by a third and L2 busy 69% -> 50%, but K2 did not get faster
-// (14.7 ms either way): the added merge instructions (7.3G vs 5.3G warp
-// instructions) moved the limit to issue/latency.
+// One pop round: the lane's oldest queued corner -> basis expansion + 7 red.v4
+// (VRF_K2_MERGE=0). The default pops through queue_pop_merge: the ~28 lanes
+// popping together often hold the same vertex (33% of pops duplicate another
+// lane's vertex in the same round, VRF_QSTATS counters), so merging them cuts
+// the L2 reductions by a third (L2 busy 69% -> 50%). At config 3 that only
+// moves the limit to issue (14.7 ms either way); at config 4, where the 15 GB
+// gradient misses L2, it saves DRAM read-modify-writes (29.3 -> 25.7 ms).
+// MERGE variant: lanes popping the same vertex in a round are grouped
+// (__match_any_sync); members stage their expanded 28-vector in the warp's
+// shared buffer, the leader sums the group and issues the only 7 red.v4.
+__device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& head,
+                                                float4* __restrict__ grad, const float (&bf)[9],
+                                                float4 (*stage)[kVec4PerVertex]) {
+  if (head != q.tail) {
+    const int slot = (int)(head & (kQ - 1)) * kThreads + q.tid;
+    const uint32_t v = q.qv[slot];
+    const float4 e = q.qa[slot];
+    ++head;
+    const unsigned act = __activemask();
+    const unsigned grp = __match_any_sync(act, v);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(grp) - 1;
+    float x[28];
+    x[0] = e.x;
+#pragma unroll
+    for (int mm = 0; mm < 9; ++mm) {
+      x[1 + mm] = e.y * bf[mm];
+      x[10 + mm] = e.z * bf[mm];
+      x[19 + mm] = e.w * bf[mm];
+    }
+    if (grp != (1u << lane)) {
+      if (lane != leader) {
+#pragma unroll
+        for (int j = 0; j < kVec4PerVertex; ++j)
+          stage[lane][j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+      }
+      __syncwarp(grp);
+      if (lane == leader) {
+        unsigned rest = grp & ~(1u << lane);
+        while (rest) {
+          const int o = __ffs(rest) - 1;
+          rest &= rest - 1;
+#pragma unroll
+          for (int j = 0; j < kVec4PerVertex; ++j) {
+            const float4 y = stage[o][j];
+            x[4 * j] += y.x;
+            x[4 * j + 1] += y.y;
+            x[4 * j + 2] += y.z;
+            x[4 * j + 3] += y.w;
+          }
+        }
+      }
+      __syncwarp(grp);
+    }
+    if (lane == leader) {
+      float4* dst = grad + (size_t)v * kVec4PerVertex;
+#pragma unroll
+      for (int j = 0; j < kVec4PerVertex; ++j)
+        atomicAdd(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
+    }
+  }
+}
+
 __device__ __forceinline__ void queue_pop(const QueueSink& q, uint32_t& head,
                                           float4* __restrict__ grad, const float (&bf)[9]) {
   if (head != q.tail) {
@@ -1194,7 +1250,7 @@ __device__ __forceinline__ void queue_pop_bulk(const QueueSink& q, uint32_t& hea
   }
 }
 
-template <int MINB, int POPS, bool BULK>
+template <int MINB, int POPS, bool BULK, bool MERGE = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
@@ -1206,6 +1262,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
   extern __shared__ __align__(16) float4 s_dyn[];
   float4* s_qa = s_dyn;
   uint32_t* s_qv = reinterpret_cast<uint32_t*>(s_dyn + kQ * kThreads);
+  // MERGE: per-warp staging [32][7] float4 after the rings
+  float4 (*stage)[kVec4PerVertex] = reinterpret_cast<float4 (*)[kVec4PerVertex]>(
+      s_dyn + kQ * kThreads + kQ * kThreads / 4) + (threadIdx.x & ~31);
   __shared__ __align__(16) float4 s_ring[BULK ? kThreads : 1][kBulkSlots][kVec4PerVertex];
   BulkSink bs{grad, &s_ring[BULK ? threadIdx.x : 0][0][0], 0};
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1324,6 +1383,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
       for (int r = 0; r < POPS; ++r) queue_pop_bulk(q, head, grad, bf, bs);
       while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
         queue_pop_bulk(q, head, grad, bf, bs);
+    } else if constexpr (MERGE) {
+#pragma unroll
+      for (int r = 0; r < POPS; ++r) queue_pop_merge(q, head, grad, bf, stage);
+      while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
+        queue_pop_merge(q, head, grad, bf, stage);
     } else {
 #pragma unroll
       for (int r = 0; r < POPS; ++r) queue_pop(q, head, grad, bf);
@@ -1974,7 +2038,27 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
         g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d, \
         order, rec, K, rec_count);                                                              \
   } while (0)
-    if (minb == 3) VRF_Q_LAUNCH(3); else VRF_Q_LAUNCH(4);
+    // same-round duplicate merging (default; VRF_K2_MERGE=0 for the plain pops).
+    // r01 v23: config 3 K2 14.63 vs 14.68 ms, config 4 (sparse 513^3, 8M rays)
+    // 25.7 vs 29.3 ms: the merged reductions save DRAM read-modify-writes when
+    // the gradient does not fit in L2.
+    static const bool merge = [] {
+      const char* e = std::getenv("VRF_K2_MERGE");
+      return !(e && std::string(e) == "0");
+    }();
+    if (merge && minb_env == 0) {  // 3 CTAs/SM (168 registers)
+      static const bool attr = cudaFuncSetAttribute(k_map_backward_q<3, 2, false, true>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    kQMergeSmemBytes) == cudaSuccess;
+      (void)attr;
+      k_map_backward_q<3, 2, false, true><<<blocks, kThreads, kQMergeSmemBytes, s>>>(
+          g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
+          order, rec, K, rec_count);
+    } else if (minb == 3) {
+      VRF_Q_LAUNCH(3);
+    } else {
+      VRF_Q_LAUNCH(4);
+    }
 #undef VRF_Q_LAUNCH
 #ifdef VRF_QSTATS
     unsigned long long qs[4];
