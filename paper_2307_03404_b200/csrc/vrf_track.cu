@@ -22,6 +22,7 @@
 #include <climits>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "vrf_internal.h"
 
@@ -296,11 +297,13 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
       March m;
       ray_from_pixel(cam, pose, (double)px, (double)py, m);
       double basis[9];
-      double Jo[4][3], Jd[4][3], Bo[3] = {0, 0, 0}, Bd[3] = {0, 0, 0};
+      // Jacobian partials: fp32 on the fast (GN) path, fp64 on the parity path
+      using JT = typename std::conditional<sizeof(ShT) == 4, float, double>::type;
+      JT Jo[4][3], Jd[4][3], Bo[3] = {0, 0, 0}, Bd[3] = {0, 0, 0};
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = 0.0;
+        for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = JT(0);
       double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
       int count = 0;
       if (!sh_basis(m.d, basis)) {
@@ -317,15 +320,18 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
                        wz[2] = {dsub(1.0, s.fz), s.fz};
           double pk[CPL];
           ShT cp[3] = {ShT(0), ShT(0), ShT(0)};
-          double Gs[3] = {0, 0, 0}, Gc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+          JT Gs[3] = {0, 0, 0}, Gc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+          const JT wxj[2] = {JT(wx[0]), JT(wx[1])}, wyj[2] = {JT(wy[0]), JT(wy[1])},
+                   wzj[2] = {JT(wz[0]), JT(wz[1])};
+          const JT iv = JT(g.inv_voxel);
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
             const int k = sub + LPR * c;
             const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
             const double wk = dmul(dmul(wx[dx], wy[dy]), wz[dz]);
-            const double dw[3] = {sgn[dx] * wy[dy] * wz[dz] * g.inv_voxel,
-                                  wx[dx] * sgn[dy] * wz[dz] * g.inv_voxel,
-                                  wx[dx] * wy[dy] * sgn[dz] * g.inv_voxel};
+            const JT dw[3] = {JT(sgn[dx]) * wyj[dy] * wzj[dz] * iv,
+                              wxj[dx] * JT(sgn[dy]) * wzj[dz] * iv,
+                              wxj[dx] * wyj[dy] * JT(sgn[dz]) * iv};
             const float4* vp4 = g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
             float v[28];
 #pragma unroll
@@ -337,18 +343,18 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
               v[4 * j + 3] = a.w;
             }
             pk[c] = dmul(wk, (double)v[0]);
-            double shd[3];
+            JT shd[3];
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
               ShT acc = ShT(0);
 #pragma unroll
               for (int mm = 0; mm < 9; ++mm) acc = fma(bs[mm], (ShT)v[1 + ch * 9 + mm], acc);
-              shd[ch] = (double)acc;
+              shd[ch] = JT(acc);
               cp[ch] = fma(ShT(wk), acc, cp[ch]);
             }
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-              Gs[a] = fma(dw[a], (double)v[0], Gs[a]);
+              Gs[a] = fma(dw[a], JT(v[0]), Gs[a]);
 #pragma unroll
               for (int ch = 0; ch < 3; ++ch) Gc[ch][a] = fma(dw[a], shd[ch], Gc[ch][a]);
             }
@@ -377,29 +383,29 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
           const double wgt = dmul(T, dsub(1.0, decay));
           const double T_next = dmul(T, decay);
           ++count;
-          double dsig[4];
+          JT dsig[4];
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
             prefix[ch] = dadd(prefix[ch], dmul(c[ch], wgt));
-            dsig[ch] = s.delta * (c[ch] * T_next + prefix[ch]);
+            dsig[ch] = JT(s.delta * (c[ch] * T_next + prefix[ch]));
           }
           prefix_d = dadd(prefix_d, dmul(s.t, wgt));
-          dsig[3] = s.delta * (s.t * T_next + prefix_d);
+          dsig[3] = JT(s.delta * (s.t * T_next + prefix_d));
           const bool sgate = sraw > 0.0;
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
-            const double gs = sgate ? s.delta * Gs[a] : 0.0;
+            const JT gs = sgate ? JT(s.delta) * Gs[a] : JT(0);
             Bo[a] += gs;
-            Bd[a] = fma(s.t, gs, Bd[a]);
+            Bd[a] = fma(JT(s.t), gs, Bd[a]);
           }
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-              double gv = sgate ? dsig[r] * Gs[a] : 0.0;
-              if (r < 3 && !clamped[r]) gv += wgt * Gc[r][a];
+              JT gv = sgate ? dsig[r] * Gs[a] : JT(0);
+              if (r < 3 && !clamped[r]) gv += JT(wgt) * Gc[r][a];
               Jo[r][a] += gv;
-              Jd[r][a] = fma(s.t, gv, Jd[r][a]);
+              Jd[r][a] = fma(JT(s.t), gv, Jd[r][a]);
             }
           }
           T = T_next;
@@ -435,8 +441,8 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
           double jo[3], jd[3];
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
-            jo[a] = Jo[r][a] - C[r] * Bo[a];
-            jd[a] = Jd[r][a] - C[r] * Bd[a];
+            jo[a] = (double)Jo[r][a] - C[r] * (double)Bo[a];
+            jd[a] = (double)Jd[r][a] - C[r] * (double)Bd[a];
           }
           // chart (tracking.cpp:125-128): tau <- dL/do, omega <- d x (dL/dd - d (d.dL/dd))
           const double dd = dot3(m.d, jd);
