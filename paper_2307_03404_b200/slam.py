@@ -33,6 +33,8 @@ class SlamConfig:
     window: int = 0                     # map over the last `window` keyframes (0 = all)
     recent_fraction: float = 0.0        # share of each mapping batch drawn from the newest keyframe
     exchange: str = "p2p"               # multi-GPU mapping exchange (distributed=True)
+    coarse_levels: int = 0              # bootstrap coarse-to-fine: start at (res-1)/2^L+1 and
+                                        # upsample L times (voxel_grid.cpp:190-220) during it
     constant_velocity: bool = True      # track_sequence init policy (tracking.cpp:271-272)
     tracking: GNConfig = field(default_factory=GNConfig)
     mapping: MappingConfig = field(default_factory=lambda: MappingConfig(rays_per_batch=65536))
@@ -63,6 +65,13 @@ class SlamSystem:
         self.ctx = ctx
         self.intr = intrinsics
         self.cfg = config
+        self.distributed = distributed
+        L = config.coarse_levels
+        if L > 0:
+            if any((int(r) - 1) % (1 << L) for r in geometry.res):
+                raise ValueError("slam: coarse_levels needs (res - 1) divisible by 2^L")
+            geometry = GridGeometry(tuple(((int(r) - 1) >> L) + 1 for r in geometry.res),
+                                    geometry.origin, geometry.voxel_size * (1 << L))
         ctx.init_grid(geometry, config.mapping.sigma_init)
         ctx.reserve_frames(intrinsics, config.max_keyframes + 1)
         self.track_slot = config.max_keyframes
@@ -154,7 +163,15 @@ class SlamSystem:
             loss = 0.0
             t1 = time.perf_counter()
             self._add_keyframe(frame, pose)
-            self._map(self.cfg.bootstrap_steps)
+            L = self.cfg.coarse_levels
+            per = self.cfg.bootstrap_steps // (L + 1)
+            for lv in range(L + 1):
+                self._map(per if lv < L else self.cfg.bootstrap_steps - per * L)
+                if lv < L:
+                    self.ctx.upsample()  # resets the RMSProp state, as the reference
+                    if self.mapper is not None:  # new grid buffers: new engine and peers
+                        from .distributed import DistributedMapper, GpuEngine
+                        self.mapper = DistributedMapper(GpuEngine(self.ctx, self.cfg.mapping))
             self.poses.append(pose)
             self.log.append(SlamFrameLog(0, True, 0.0, (time.perf_counter() - t1) * 1e3, loss))
             return pose

@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--track-iters", type=int, default=10)
     ap.add_argument("--sigma-init", type=float, default=0.1)
     ap.add_argument("--window", type=int, default=0, help="map over the last N keyframes")
+    ap.add_argument("--coarse", type=int, default=0,
+                    help="bootstrap coarse-to-fine: start at (res-1)/2^L+1, upsample L times")
     ap.add_argument("--recent", type=float, default=0.0,
                     help="share of each mapping batch drawn from the newest keyframe")
     ap.add_argument("--track-lambda-d", type=float, default=0.1,
@@ -78,7 +80,8 @@ def main():
 
     geom = GridGeometry(gt.geom.res, gt.geom.origin, gt.geom.voxel_size)
     cfg = SlamConfig(keyframe_stride=args.stride, map_steps=args.map_steps, window=args.window,
-                     recent_fraction=args.recent, bootstrap_steps=args.bootstrap,
+                     recent_fraction=args.recent, coarse_levels=args.coarse,
+                     bootstrap_steps=args.bootstrap,
                      max_keyframes=(args.frames + args.stride - 1) // args.stride + 1,
                      tracking=GNConfig(rays_per_iteration=args.track_rays,
                                        iterations=args.track_iters,
@@ -137,7 +140,7 @@ def main():
         "ate_rmse_m": ate, "ate_unaligned_m": ate_u, "pose_pairs": pairs, **rpe,
         "psnr_db": q.psnr_db, "depth_l1_m": q.depth_l1_m,
         "settings": {"stride": args.stride, "map_steps": args.map_steps, "window": args.window,
-                     "recent_fraction": args.recent,
+                     "recent_fraction": args.recent, "coarse_levels": args.coarse,
                      "track_lambda_d": args.track_lambda_d,
                      "map_rays": args.map_rays, "bootstrap_steps": args.bootstrap,
                      "track": f"GN {args.track_rays} rays x {args.track_iters} it"},
