@@ -71,6 +71,7 @@ def _slam_worker(rank, world, port, out_dir):
     try:
         gt, intr, frames, poses, ts = _scene(8)
         cfg = SlamConfig(keyframe_stride=4, map_steps=10, bootstrap_steps=100, max_keyframes=4,
+                         coarse_levels=1,  # also exercises the mapper rebuild after upsample
                          tracking=GNConfig(rays_per_iteration=4096, iterations=6, lambda_d=0.1),
                          mapping=MappingConfig(rays_per_batch=4096))
         ctx = Context(0, shard_multiple=world)
