@@ -538,6 +538,25 @@ def run_ours(args):
                                  "unit": "GB/s", "frac": t_gbps / peak,
                                  "kernel": "k_pose_group (GN graph)"},
                     "ate_rmse_m": float(np.sqrt(np.mean(np.square(errs))))}
+        # the same kernel at a throughput-sized batch (262,144 rays per iteration):
+        # at 16K rays one GN iteration is a single latency-bound wave, so the
+        # config-2 roofline fraction says little about the kernel itself
+        from paper_2307_03404_b200.api import GNConfig as _GN
+        big = _GN(rays_per_iteration=1 << 18, iterations=gn.iterations, lambda_d=gn.lambda_d)
+        gt_ctx.track_frame_gn(1, intr, tposes[0], big)
+        torch.cuda.synchronize()
+        gt_ctx.profile_enable(True)
+        gt_ctx.track_frame_gn(1, intr, tposes[0], big)
+        bp = gt_ctx.profile_read()
+        gt_ctx.profile_enable(False)
+        b_ms, b_samples = bp["pose_backward"][0], bp.get("track_samples", 0)
+        if b_ms > 0:
+            b_gbps = (896.0 * b_samples + 32.0 * big.iterations * big.rays_per_iteration) / \
+                (b_ms / 1e3) / 1e9
+            tracking["throughput_probe"] = {
+                "rays_per_iteration": big.rays_per_iteration, "iterations": big.iterations,
+                "samples_per_s": b_samples / (b_ms / 1e3), "achieved_GBps": b_gbps,
+                "frac": b_gbps / peak}
 
     # ---- CPU baseline (rank 0, N=1)
     cpu = None
