@@ -355,6 +355,13 @@ inline DevPose dev_pose(const vrf_pose* p) {
 }
 
 // Device error flags -> the reference's exception classes.
+inline int err_from_flag(vrf_context* ctx, int flag) {
+  if (flag & 2) return set_err(ctx, VRF_ERR_OUT_OF_RANGE, "generate_ray: pixel outside image");
+  if (flag & 1)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "sh_eval: direction must be unit length");
+  return VRF_OK;
+}
+
 inline int check_err_flag(vrf_context* ctx) {
   int flag = 0;
   CU(cudaMemcpyAsync(&flag, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

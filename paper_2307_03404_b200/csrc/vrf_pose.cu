@@ -120,10 +120,13 @@ int pose_pass(vrf_context* ctx, int frame, const vrf_intrinsics* intr, const vrf
   launch_pose_reduce2((const PosePartial*)ctx->s_partials.ptr, nb, ctx->d_pose_out, ctx->stream);
   LAUNCHED(4);
   CU(cudaGetLastError());
-  if ((rc = check_err_flag(ctx))) return rc;
+  // error flag and result in one round trip (one host sync per pose pass)
   PosePartial out;
+  int flag = 0;
+  CU(cudaMemcpyAsync(&flag, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaMemcpyAsync(&out, ctx->d_pose_out, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  if ((rc = err_from_flag(ctx, flag))) return rc;
   prof_collect(ctx);
   std::memcpy(res->jtj, out.jtj, sizeof(res->jtj));
   std::memcpy(res->jtr, out.jtr, sizeof(res->jtr));
