@@ -511,3 +511,22 @@ np.savez(sys.argv[1], g=g, s=np.array([st.samples, st.rays_color, st.rays_depth]
     assert np.array_equal(a["s"], b["s"])
     np.testing.assert_allclose(a["l"], b["l"], rtol=1e-13)
     assert np.max(np.abs(a["g"] - b["g"])) <= 1e-4 * np.max(np.abs(b["g"]))
+
+
+@pytest.mark.parametrize("n_rays", [60000, 200000])
+def test_fast_gradient_matches_deterministic_at_larger_batches(ctx, oracle, n_rays):
+    """The fast gradient against the deterministic FP64 one at batch sizes where
+    the kernel variants switch: 60K rays run K0 (thread) + K2g (8 lanes), 200K
+    run K0 + the merged queued K2q. Tolerance: the fast path's fp32 records and
+    reductions (1e-3 relative to the gradient scale)."""
+    grid, intr, frames = room_scene(res=33, width=64, height=48)
+    g0 = fresh_grid(grid, seed=9)
+    batch = oracle.draw_batch(21, len(frames), intr.width, intr.height, n_rays)
+    ctx.load_grid(g0)
+    ctx.load_frames(intr, frames)
+    fast, sf = ctx.mapping_gradient(MappingConfig(), batch)
+    det, sd = ctx.mapping_gradient(MappingConfig(deterministic=True), batch)
+    assert sf.samples == sd.samples and sf.rays_color == sd.rays_color
+    scale = np.abs(det).max()
+    assert np.max(np.abs(fast - det)) <= 1e-3 * scale
+    assert np.array_equal(fast != 0, det != 0)
