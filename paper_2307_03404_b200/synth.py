@@ -243,3 +243,20 @@ def frames_from_renders(renders, poses, depth_scale):
         c, d = quantize_frame(color, depth, depth_scale)
         out.append(Frame(c, d, 0.0, pose))
     return out
+
+
+def synth_from_grid(ctx, grid, poses, timestamps, intrinsics, params=None):
+    """synth_from_grid — dataset.cpp:443-462, on the device: render every pose of
+    the trajectory from `grid` (K1, one full-resolution render_image per frame),
+    then quantise colour and depth like the reference's PNG path (quantize_color /
+    quantize_depth, image.cpp:26-30). grid=None renders the grid already loaded in
+    ctx. Returns the Frames (gt_pose and timestamp set)."""
+    if grid is not None:
+        ctx.load_grid(grid)
+    out = []
+    for pose, ts in zip(poses, timestamps):
+        img = ctx.render_image(intrinsics, pose, params) if params is not None else \
+            ctx.render_image(intrinsics, pose)
+        c, d = quantize_frame(img.color, img.depth, intrinsics.depth_scale)
+        out.append(Frame(c, d, float(ts), pose))
+    return out

@@ -530,3 +530,17 @@ def test_fast_gradient_matches_deterministic_at_larger_batches(ctx, oracle, n_ra
     scale = np.abs(det).max()
     assert np.max(np.abs(fast - det)) <= 1e-3 * scale
     assert np.array_equal(fast != 0, det != 0)
+
+
+def test_synth_from_grid_matches_oracle_renders(ctx, oracle):
+    """synth_from_grid (dataset.cpp:443-462) on the device: the quantised frames
+    equal the oracle's render_image quantised the same way (renders agree to
+    1e-12, so only exact quantisation ties could differ)."""
+    grid, intr, frames = room_scene(res=33, width=64, height=48)
+    poses = [f.gt_pose for f in frames]
+    got = synth.synth_from_grid(ctx, grid, poses, [0.0, 1.0, 2.0][:len(poses)], intr)
+    for f, p in zip(got, poses):
+        c, d = oracle.render_image(grid, intr, p, RenderParams())
+        cq, dq = synth.quantize_frame(c, d, intr.depth_scale)
+        assert np.mean(f.color != cq) < 1e-3 and np.mean(f.depth != dq) < 1e-3
+        assert f.gt_pose is p
