@@ -505,6 +505,308 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
   }
 }
 
+// Warp-synchronous k_pose_group for the GN path (fp32 SH, 8 lanes per ray).
+// In k_pose_group the four ray groups of a warp march independently, so the
+// group-masked ballots of GroupMarch run while the groups are diverged and the
+// compiler emulates them (WARPSYNC.COLLECTIVE; ~17% of the kernel's stall
+// samples, r01). Here the groups advance in lockstep rounds: in each round a
+// group without a pending sample evaluates its next 8 segments, then every
+// group with a pending sample shades one. All ballots and shuffles run with
+// the full warp mask. The arithmetic (sample order, sigma in corner order,
+// colour in lane order, Jacobian partials) is the same as k_pose_group<float>.
+__global__ void __launch_bounds__(kT, 3) k_pose_group_u(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd_base,
+    const int* __restrict__ frame_idx, long long npix, const DevPose* __restrict__ pose_ptr,
+    const int* __restrict__ pixels, const uint32_t* __restrict__ order, int n, double lambda_p,
+    double lambda_d, PosePartial* __restrict__ partials, int* err) {
+  constexpr int LPR = 8;
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ double s_d[kT / 32][32];
+  __shared__ long long s_l[kT / 32];
+  __shared__ int s_i[kT / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int sub = lane & (LPR - 1), gbase = lane & ~(LPR - 1);
+  const int t = blockIdx.x * (kT / LPR) + threadIdx.x / LPR;
+  const int i = (order && t < n) ? (int)order[t] : t;
+  const double4* rgbd = rgbd_base + npix * (long long)(*frame_idx);
+  double jtj[21], jtr[6], loss = 0.0;
+#pragma unroll
+  for (int k = 0; k < 21; ++k) jtj[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) jtr[k] = 0.0;
+  int hit = 0;
+  long long samples = 0;
+  const int px = t < n ? pixels[2 * i] : -1, py = t < n ? pixels[2 * i + 1] : -1;
+  bool alive = false;
+  March m;
+  float bs[9];
+  if (t < n && px >= 0) {
+    if (px >= cam.width || py < 0 || py >= cam.height) {
+      if (sub == 0) atomicOr(err, 2);
+    } else {
+      const DevPose pose = *pose_ptr;
+      ray_from_pixel(cam, pose, (double)px, (double)py, m);
+      double basis[9];
+      if (!sh_basis(m.d, basis)) {
+        if (sub == 0) atomicOr(err, 1);
+      } else if (march_begin(g, p, m)) {
+        alive = true;
+#pragma unroll
+        for (int mm = 0; mm < 9; ++mm) bs[mm] = (float)basis[mm];
+      }
+    }
+  }
+  float Jo[4][3], Jd[4][3], Bo[3] = {0.f, 0.f, 0.f}, Bd[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = 0.f;
+  double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
+  int count = 0;
+  const int kc = sub, dx = kc & 1, dy = (kc >> 1) & 1, dz = (kc >> 2) & 1;
+  const double sgn[2] = {-1.0, 1.0};
+  Sample mine;
+  unsigned act = 0;
+  while (__any_sync(FULL, alive)) {
+    // ---- round A: groups without a pending sample locate their next 8 segments
+    const bool need = alive && act == 0;
+    bool a = false, eb = false;
+    if (need) {
+      const long long kk = m.k + sub;
+      if (kk < m.nseg) {
+        const double s0 = dadd(m.lo, dmul((double)kk, m.step));
+        const double s0s = dadd(s0, m.step);
+        const double s1 = (m.hi < s0s) ? m.hi : s0s;
+        const double len = dsub(s1, s0);
+        if (len >= 1e-12) {
+          const double tm = dmul(0.5, dadd(s0, s1));
+          const double pp[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
+                                dadd(m.o[2], dmul(tm, m.d[2]))};
+          if (locate(g, pp, mine)) {
+            if (cell_active(g, mine.cell)) {
+              a = true;
+              mine.t = tm;
+              mine.delta = len;
+            } else {
+              eb = !block_active(g, mine.cx, mine.cy, mine.cz);
+            }
+          }
+        }
+      }
+    }
+    const unsigned ba = __ballot_sync(FULL, a), be = __ballot_sync(FULL, eb);
+    int jskip = -1;
+    if (need) {
+      act = (ba >> gbase) & 0xffu;
+      const unsigned ebm = (be >> gbase) & 0xffu;
+      m.k += LPR;
+      if (act == 0 && ebm) jskip = 31 - __clz(ebm);
+    }
+    long long kn = 0;
+    if (jskip >= 0 && sub == jskip)
+      kn = skip_empty_box(g, m, mine,
+                          super_active(g, mine.cx, mine.cy, mine.cz) ? kBlockLog2 : kSuperLog2);
+    kn = __shfl_sync(FULL, kn, gbase + (jskip >= 0 ? jskip : 0));
+    if (jskip >= 0 && kn > m.k) m.k = kn;
+    if (need && act == 0 && m.k >= m.nseg) alive = false;  // ray exhausted
+    // ---- round B: groups with a pending sample shade the first one
+    const bool has = alive && act != 0;
+    if (!__any_sync(FULL, has)) continue;
+    const int src = gbase + (has ? (__ffs(act) - 1) : 0);
+    if (has) act &= act - 1;
+    Sample s;
+    s.t = __shfl_sync(FULL, mine.t, src);
+    s.delta = __shfl_sync(FULL, mine.delta, src);
+    s.fx = __shfl_sync(FULL, mine.fx, src);
+    s.fy = __shfl_sync(FULL, mine.fy, src);
+    s.fz = __shfl_sync(FULL, mine.fz, src);
+    s.base = __shfl_sync(FULL, mine.base, src);
+    double pk = 0.0;
+    float cp[3] = {0.f, 0.f, 0.f};
+    float Gs[3] = {0.f, 0.f, 0.f}, Gc[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+    double wx[2] = {0, 0}, wy[2] = {0, 0}, wz[2] = {0, 0};
+    if (has) {
+      wx[0] = dsub(1.0, s.fx);
+      wx[1] = s.fx;
+      wy[0] = dsub(1.0, s.fy);
+      wy[1] = s.fy;
+      wz[0] = dsub(1.0, s.fz);
+      wz[1] = s.fz;
+      const float wxj[2] = {(float)wx[0], (float)wx[1]}, wyj[2] = {(float)wy[0], (float)wy[1]},
+                  wzj[2] = {(float)wz[0], (float)wz[1]};
+      const float iv = (float)g.inv_voxel;
+      const double wk = dmul(dmul(wx[dx], wy[dy]), wz[dz]);
+      const float dw[3] = {(float)sgn[dx] * wyj[dy] * wzj[dz] * iv,
+                           wxj[dx] * (float)sgn[dy] * wzj[dz] * iv,
+                           wxj[dx] * wyj[dy] * (float)sgn[dz] * iv};
+      const float4* vp4 = g.payload + (size_t)corner_index(g, s.base, kc) * kVec4PerVertex;
+      float v[28];
+#pragma unroll
+      for (int j = 0; j < kVec4PerVertex; ++j) {
+        const float4 q = __ldg(vp4 + j);
+        v[4 * j] = q.x;
+        v[4 * j + 1] = q.y;
+        v[4 * j + 2] = q.z;
+        v[4 * j + 3] = q.w;
+      }
+      pk = dmul(wk, (double)v[0]);
+      float shd[3];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        float acc = 0.f;
+#pragma unroll
+        for (int mm = 0; mm < 9; ++mm) acc = fmaf(bs[mm], v[1 + ch * 9 + mm], acc);
+        shd[ch] = acc;
+        cp[ch] = fmaf((float)wk, acc, cp[ch]);
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        Gs[q] = fmaf(dw[q], v[0], Gs[q]);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) Gc[ch][q] = fmaf(dw[q], shd[ch], Gc[ch][q]);
+      }
+    }
+    // sigma_raw in corner order (the reference's), colour in lane order
+    double sraw = 0.0;
+#pragma unroll
+    for (int j = 0; j < LPR; ++j) sraw = dadd(sraw, __shfl_sync(FULL, pk, gbase + j));
+    float csum[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < LPR; ++j)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) csum[ch] += __shfl_sync(FULL, cp[ch], gbase + j);
+    if (has) {
+      double c[3];
+      bool clamped[3];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const double cv = 0.5 + (double)csum[ch];
+        clamped[ch] = (cv <= 0.0 || cv >= 1.0);
+        c[ch] = (cv < 0.0) ? 0.0 : ((1.0 < cv) ? 1.0 : cv);
+      }
+      const double sigma = (sraw < 0.0) ? 0.0 : sraw;
+      const double decay = exp(dmul(-sigma, s.delta));
+      const double wgt = dmul(T, dsub(1.0, decay));
+      const double T_next = dmul(T, decay);
+      ++count;
+      float dsig[4];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        prefix[ch] = dadd(prefix[ch], dmul(c[ch], wgt));
+        dsig[ch] = (float)(s.delta * (c[ch] * T_next + prefix[ch]));
+      }
+      prefix_d = dadd(prefix_d, dmul(s.t, wgt));
+      dsig[3] = (float)(s.delta * (s.t * T_next + prefix_d));
+      const bool sgate = sraw > 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const float gs = sgate ? (float)s.delta * Gs[q] : 0.f;
+        Bo[q] += gs;
+        Bd[q] = fmaf((float)s.t, gs, Bd[q]);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          float gv = sgate ? dsig[r] * Gs[q] : 0.f;
+          if (r < 3 && !clamped[r]) gv += (float)wgt * Gc[r][q];
+          Jo[r][q] += gv;
+          Jd[r][q] = fmaf((float)s.t, gv, Jd[r][q]);
+        }
+      }
+      T = T_next;
+      if (T < p.eps) alive = false;
+    }
+  }
+  // group reduction of the lane partials (fixed butterfly order, full-warp shuffles)
+#pragma unroll
+  for (int off = LPR / 2; off > 0; off >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      Bo[q] += __shfl_xor_sync(FULL, Bo[q], off);
+      Bd[q] += __shfl_xor_sync(FULL, Bd[q], off);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        Jo[r][q] += __shfl_xor_sync(FULL, Jo[r][q], off);
+        Jd[r][q] += __shfl_xor_sync(FULL, Jd[r][q], off);
+      }
+    }
+  }
+  if (count > 0 && sub == 0) {
+    hit = 1;
+    samples = count;
+    const double4 tg = rgbd[(long long)py * cam.width + px];
+    const double C[4] = {prefix[0], prefix[1], prefix[2], prefix_d};
+    const double res[4] = {dsub(C[0], tg.x), dsub(C[1], tg.y), dsub(C[2], tg.z),
+                           dsub(C[3], tg.w)};
+    loss = dadd(dmul(lambda_p, dadd(dadd(dmul(res[0], res[0]), dmul(res[1], res[1])),
+                                    dmul(res[2], res[2]))),
+                dmul(dmul(lambda_d, res[3]), res[3]));
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double jo[3], jd[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        jo[q] = (double)Jo[r][q] - C[r] * (double)Bo[q];
+        jd[q] = (double)Jd[r][q] - C[r] * (double)Bd[q];
+      }
+      const double dd = dot3(m.d, jd);
+      double gp[3], om[3];
+      for (int q = 0; q < 3; ++q) gp[q] = jd[q] - m.d[q] * dd;
+      cross3(m.d, gp, om);
+      const double J[6] = {om[0], om[1], om[2], jo[0], jo[1], jo[2]};
+      const double lam = r < 3 ? lambda_p : lambda_d;
+      int idx = 0;
+#pragma unroll
+      for (int a2 = 0; a2 < 6; ++a2) {
+#pragma unroll
+        for (int b2 = a2; b2 < 6; ++b2) jtj[idx++] += lam * J[a2] * J[b2];
+        jtr[a2] += lam * J[a2] * res[r];
+      }
+    }
+  }
+  double vals[28];
+#pragma unroll
+  for (int k = 0; k < 21; ++k) vals[k] = jtj[k];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) vals[21 + k] = jtr[k];
+  vals[27] = loss;
+#pragma unroll
+  for (int k = 0; k < 28; ++k) {
+    double v = warp_sum(vals[k]);
+    if (lane == 0) s_d[wid][k] = v;
+  }
+  long long sw = warp_sum(samples);
+  int hw = warp_sum(hit);
+  if (lane == 0) {
+    s_l[wid] = sw;
+    s_i[wid] = hw;
+  }
+  __syncthreads();
+  if (threadIdx.x < 28) {
+    double acc = 0.0;
+    for (int w = 0; w < kT / 32; ++w) acc += s_d[w][threadIdx.x];
+    PosePartial* out = partials + blockIdx.x;
+    if (threadIdx.x < 21)
+      out->jtj[threadIdx.x] = acc;
+    else if (threadIdx.x < 27)
+      out->jtr[threadIdx.x - 21] = acc;
+    else
+      out->loss = acc;
+  }
+  if (threadIdx.x == 32) {
+    long long sl = 0;
+    int sm = 0;
+    for (int w = 0; w < kT / 32; ++w) {
+      sl += s_l[w];
+      sm += s_i[w];
+    }
+    partials[blockIdx.x].samples = sl;
+    partials[blockIdx.x].m = sm;
+    partials[blockIdx.x].bad = 0;
+  }
+}
+
 // Fixed-order reduction of the CTA partials: thread t folds partials t, t+256,
 // ... (strided, fixed), then the block folds the 256 thread sums in a fixed
 // tree — deterministic, and parallel (one thread per field walking all
@@ -714,6 +1016,15 @@ static bool pose_march_serial() {
   return v;
 }
 
+// VRF_POSE_UNIFORM=0: the group-independent k_pose_group on the GN path (A/B).
+static bool pose_uniform() {
+  static const bool v = [] {
+    const char* e = getenv("VRF_POSE_UNIFORM");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
+
 int pose_fused_blocks(int n) {
   const int lpr = pose_kernel();
   const int rays_per_block = lpr == 0 ? kT : kT / lpr;
@@ -747,6 +1058,8 @@ void launch_pose_fused(bool fp64_sh, const DevGrid& g, const DevParams& p, const
         k_pose_group<double, 8><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       else if (pose_march_serial())
         k_pose_group<float, 8, false><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
+      else if (pose_uniform())
+        k_pose_group_u<<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       else
         k_pose_group<float, 8><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
   }
