@@ -514,6 +514,7 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
 // group with a pending sample shades one. All ballots and shuffles run with
 // the full warp mask. The arithmetic (sample order, sigma in corner order,
 // colour in lane order, Jacobian partials) is the same as k_pose_group<float>.
+template <typename ShT>
 __global__ void __launch_bounds__(kT, 3) k_pose_group_u(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd_base,
     const int* __restrict__ frame_idx, long long npix, const DevPose* __restrict__ pose_ptr,
@@ -521,6 +522,7 @@ __global__ void __launch_bounds__(kT, 3) k_pose_group_u(
     double lambda_d, PosePartial* __restrict__ partials, int* err) {
   constexpr int LPR = 8;
   constexpr unsigned FULL = 0xffffffffu;
+  using JT = typename std::conditional<sizeof(ShT) == 4, float, double>::type;
   __shared__ double s_d[kT / 32][32];
   __shared__ long long s_l[kT / 32];
   __shared__ int s_i[kT / 32];
@@ -539,7 +541,7 @@ __global__ void __launch_bounds__(kT, 3) k_pose_group_u(
   const int px = t < n ? pixels[2 * i] : -1, py = t < n ? pixels[2 * i + 1] : -1;
   bool alive = false;
   March m;
-  float bs[9];
+  ShT bs[9];
   if (t < n && px >= 0) {
     if (px >= cam.width || py < 0 || py >= cam.height) {
       if (sub == 0) atomicOr(err, 2);
@@ -552,15 +554,15 @@ __global__ void __launch_bounds__(kT, 3) k_pose_group_u(
       } else if (march_begin(g, p, m)) {
         alive = true;
 #pragma unroll
-        for (int mm = 0; mm < 9; ++mm) bs[mm] = (float)basis[mm];
+        for (int mm = 0; mm < 9; ++mm) bs[mm] = ShT(basis[mm]);
       }
     }
   }
-  float Jo[4][3], Jd[4][3], Bo[3] = {0.f, 0.f, 0.f}, Bd[3] = {0.f, 0.f, 0.f};
+  JT Jo[4][3], Jd[4][3], Bo[3] = {0, 0, 0}, Bd[3] = {0, 0, 0};
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = 0.f;
+    for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = JT(0);
   double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
   int count = 0;
   const int kc = sub, dx = kc & 1, dy = (kc >> 1) & 1, dz = (kc >> 2) & 1;
@@ -622,8 +624,8 @@ __global__ void __launch_bounds__(kT, 3) k_pose_group_u(
     s.fz = __shfl_sync(FULL, mine.fz, src);
     s.base = __shfl_sync(FULL, mine.base, src);
     double pk = 0.0;
-    float cp[3] = {0.f, 0.f, 0.f};
-    float Gs[3] = {0.f, 0.f, 0.f}, Gc[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+    ShT cp[3] = {ShT(0), ShT(0), ShT(0)};
+    JT Gs[3] = {0, 0, 0}, Gc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
     double wx[2] = {0, 0}, wy[2] = {0, 0}, wz[2] = {0, 0};
     if (has) {
       wx[0] = dsub(1.0, s.fx);
@@ -632,13 +634,12 @@ __global__ void __launch_bounds__(kT, 3) k_pose_group_u(
       wy[1] = s.fy;
       wz[0] = dsub(1.0, s.fz);
       wz[1] = s.fz;
-      const float wxj[2] = {(float)wx[0], (float)wx[1]}, wyj[2] = {(float)wy[0], (float)wy[1]},
-                  wzj[2] = {(float)wz[0], (float)wz[1]};
-      const float iv = (float)g.inv_voxel;
+      const JT wxj[2] = {JT(wx[0]), JT(wx[1])}, wyj[2] = {JT(wy[0]), JT(wy[1])},
+               wzj[2] = {JT(wz[0]), JT(wz[1])};
+      const JT iv = JT(g.inv_voxel);
       const double wk = dmul(dmul(wx[dx], wy[dy]), wz[dz]);
-      const float dw[3] = {(float)sgn[dx] * wyj[dy] * wzj[dz] * iv,
-                           wxj[dx] * (float)sgn[dy] * wzj[dz] * iv,
-                           wxj[dx] * wyj[dy] * (float)sgn[dz] * iv};
+      const JT dw[3] = {JT(sgn[dx]) * wyj[dy] * wzj[dz] * iv, wxj[dx] * JT(sgn[dy]) * wzj[dz] * iv,
+                        wxj[dx] * wyj[dy] * JT(sgn[dz]) * iv};
       const float4* vp4 = g.payload + (size_t)corner_index(g, s.base, kc) * kVec4PerVertex;
       float v[28];
 #pragma unroll
@@ -650,27 +651,27 @@ __global__ void __launch_bounds__(kT, 3) k_pose_group_u(
         v[4 * j + 3] = q.w;
       }
       pk = dmul(wk, (double)v[0]);
-      float shd[3];
+      JT shd[3];
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        float acc = 0.f;
+        ShT acc = ShT(0);
 #pragma unroll
-        for (int mm = 0; mm < 9; ++mm) acc = fmaf(bs[mm], v[1 + ch * 9 + mm], acc);
-        shd[ch] = acc;
-        cp[ch] = fmaf((float)wk, acc, cp[ch]);
+        for (int mm = 0; mm < 9; ++mm) acc = fma(bs[mm], (ShT)v[1 + ch * 9 + mm], acc);
+        shd[ch] = JT(acc);
+        cp[ch] = fma(ShT(wk), acc, cp[ch]);
       }
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        Gs[q] = fmaf(dw[q], v[0], Gs[q]);
+        Gs[q] = fma(dw[q], JT(v[0]), Gs[q]);
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) Gc[ch][q] = fmaf(dw[q], shd[ch], Gc[ch][q]);
+        for (int ch = 0; ch < 3; ++ch) Gc[ch][q] = fma(dw[q], shd[ch], Gc[ch][q]);
       }
     }
     // sigma_raw in corner order (the reference's), colour in lane order
     double sraw = 0.0;
 #pragma unroll
     for (int j = 0; j < LPR; ++j) sraw = dadd(sraw, __shfl_sync(FULL, pk, gbase + j));
-    float csum[3] = {0.f, 0.f, 0.f};
+    ShT csum[3] = {ShT(0), ShT(0), ShT(0)};
 #pragma unroll
     for (int j = 0; j < LPR; ++j)
 #pragma unroll
@@ -689,29 +690,29 @@ __global__ void __launch_bounds__(kT, 3) k_pose_group_u(
       const double wgt = dmul(T, dsub(1.0, decay));
       const double T_next = dmul(T, decay);
       ++count;
-      float dsig[4];
+      JT dsig[4];
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
         prefix[ch] = dadd(prefix[ch], dmul(c[ch], wgt));
-        dsig[ch] = (float)(s.delta * (c[ch] * T_next + prefix[ch]));
+        dsig[ch] = JT(s.delta * (c[ch] * T_next + prefix[ch]));
       }
       prefix_d = dadd(prefix_d, dmul(s.t, wgt));
-      dsig[3] = (float)(s.delta * (s.t * T_next + prefix_d));
+      dsig[3] = JT(s.delta * (s.t * T_next + prefix_d));
       const bool sgate = sraw > 0.0;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const float gs = sgate ? (float)s.delta * Gs[q] : 0.f;
+        const JT gs = sgate ? JT(s.delta) * Gs[q] : JT(0);
         Bo[q] += gs;
-        Bd[q] = fmaf((float)s.t, gs, Bd[q]);
+        Bd[q] = fma(JT(s.t), gs, Bd[q]);
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-          float gv = sgate ? dsig[r] * Gs[q] : 0.f;
-          if (r < 3 && !clamped[r]) gv += (float)wgt * Gc[r][q];
+          JT gv = sgate ? dsig[r] * Gs[q] : JT(0);
+          if (r < 3 && !clamped[r]) gv += JT(wgt) * Gc[r][q];
           Jo[r][q] += gv;
-          Jd[r][q] = fmaf((float)s.t, gv, Jd[r][q]);
+          Jd[r][q] = fma(JT(s.t), gv, Jd[r][q]);
         }
       }
       T = T_next;
@@ -1054,12 +1055,14 @@ void launch_pose_fused(bool fp64_sh, const DevGrid& g, const DevParams& p, const
         k_pose_group<float, 4><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       break;
     default:
+      // the FP64 parity path keeps k_pose_group (a k_pose_group_u<double> build
+      // broke Adam parity in r01 and was not pursued)
       if (fp64_sh)
         k_pose_group<double, 8><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       else if (pose_march_serial())
         k_pose_group<float, 8, false><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       else if (pose_uniform())
-        k_pose_group_u<<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
+        k_pose_group_u<float><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       else
         k_pose_group<float, 8><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
   }
