@@ -1055,8 +1055,9 @@ void launch_pose_fused(bool fp64_sh, const DevGrid& g, const DevParams& p, const
         k_pose_group<float, 4><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       break;
     default:
-      // the FP64 parity path keeps k_pose_group (a k_pose_group_u<double> build
-      // broke Adam parity in r01 and was not pursued)
+      // The FP64 parity path keeps k_pose_group. Open item from r01: a
+      // k_pose_group_u<double> build composited only the first sample of each
+      // ray on the pose_pass path (samples == rays), which broke Adam parity.
       if (fp64_sh)
         k_pose_group<double, 8><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       else if (pose_march_serial())
