@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--cpu-amortised-rays", type=int, default=65536,
+                    help="rays of the second CPU baseline point (0: skip)")
     ap.add_argument("--exchange", default="p2p", choices=["sparse", "dense", "p2p"],
                     help="N>1 gradient exchange: NCCL over the touched 8^3-vertex blocks "
                          "(sparse), NCCL over the whole grid (dense), or the fused "
@@ -177,8 +179,27 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
+def snapshot_state(ctx, torch, device):
+    """Device copies of the payload and RMSProp state (the gradient is zero between
+    steps). Returns (views, copies) for restore_state."""
+    from paper_2307_03404_b200.distributed import _CudaArray as DeviceView
+
+    b = ctx.device_buffers()
+    n = int(b.num_vertices) * 28
+    views = [torch.as_tensor(DeviceView(b.payload, n), device=f"cuda:{device}"),
+             torch.as_tensor(DeviceView(b.rms_v, n), device=f"cuda:{device}")]
+    return views, [v.clone() for v in views]
+
+
+def restore_state(snap):
+    views, copies = snap
+    for v, c in zip(views, copies):
+        v.copy_(c)
+
+
 # ----------------------------------------------------------------- CPU baseline
-def cpu_reference(args, gt, intr, keyframe_poses, frames, seconds, fixed=None):
+def cpu_reference(args, gt, intr, keyframe_poses, frames, seconds, fixed=None,
+                  amortised_rays=0):
     """The reference's own mapping_step (oracle/_ref) on the host cores, on the same
     workload (257^3 fp64 grid, 1200x680 keyframes), reference default batch of
     4096 rays, timed like the reference times itself (steady clock)."""
@@ -239,9 +260,21 @@ def cpu_reference(args, gt, intr, keyframe_poses, frames, seconds, fixed=None):
         while elapsed < seconds and steps < 20:
             elapsed += one(best)
             steps += 1
+    out = {"threads": best, "steps": steps, "seconds": elapsed,
+           "sweep_s": {str(k): round(v, 3) for k, v in sweep.items()}}
+    if amortised_rays:
+        # a second point where the per-worker zero-fill amortises: one step of
+        # amortised_rays rays on every worker the host memory allows
+        gh = ref.grid(grid)
+        mapper = ref.lib.ref_mapper_create(1)
+        t0 = time.perf_counter()
+        ref.mapping_step(gh, fh, intr, cfg, amortised_rays, threads, False, mapper)
+        out["amortised"] = {"rays": amortised_rays, "threads": threads,
+                            "seconds": time.perf_counter() - t0}
+        ref.lib.ref_mapper_destroy(mapper)
+        ref.lib.ref_grid_destroy(gh)
     ref.lib.ref_frames_destroy(fh)
-    return {"threads": best, "steps": steps, "seconds": elapsed,
-            "sweep_s": {str(k): round(v, 3) for k, v in sweep.items()}}
+    return out
 
 
 def cpu_samples_per_step(args, gt, intr, frames):
@@ -381,6 +414,9 @@ def run_ours(args):
     for i in range(args.warmup):
         one_step(i)
     torch.cuda.synchronize()
+    # the map state the timed steps start from: e2e below restarts from it and
+    # replays the same batches, so e2e / value isolates the API and copy cost
+    snap = snapshot_state(ctx, torch, local)
     if dist:
         dist.barrier()
     ctx.profile_enable(True)
@@ -416,11 +452,21 @@ def run_ours(args):
     # every step draws its batch on the host from the reference Rng stream, copies
     # it H2D from pinned memory and reads its stats back D2H; the draw of batch
     # i+1 overlaps the device work of step i.
+    # The e2e steps start from the timed steps' starting state (restored from a
+    # device snapshot) and draw the same batches: the same Rng stream advanced
+    # past the warm-up draws.
+    def timed_stream():
+        r = Rng(1 + 7919 * rank)
+        for _ in range(args.warmup):
+            r.draw_batch(len(frames), intr.width, intr.height, args.rays)
+        return r
+
     e2e = None
     if mapper is None:
         e_cfg = MappingConfig(rays_per_batch=args.rays)
-        e_rng = Rng(99)
-        ctx.mapping_steps(e_cfg, e_rng, len(frames), args.warmup)
+        ctx.mapping_steps(e_cfg, Rng(99), len(frames), 1)  # pinned buffers (allocation)
+        restore_state(snap)
+        e_rng = timed_stream()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e_stats = ctx.mapping_steps(e_cfg, e_rng, len(frames), args.steps)
@@ -430,6 +476,7 @@ def run_ours(args):
         e2e = {"value": e_samples / e_s, "unit": "samples/s",
                "h2d_bytes_per_step": int(args.rays * 12), "d2h_bytes_per_step": 44,
                "ms_per_step": 1e3 * e_s / args.steps,
+               "same_state_and_batches_as_value": e_samples == total_samples,
                "api": "Context.mapping_steps (vrf_mapping_steps: host Rng draw + H2D + "
                       "step + stats D2H per step)"}
     else:
@@ -438,7 +485,8 @@ def run_ours(args):
         # (all-reduce of counts/losses, reduce-scatter, sharded RMSProp,
         # all-gather) and reads the global stats back; wall time, max over ranks.
         from concurrent.futures import ThreadPoolExecutor
-        e_rng = Rng(99 + 7919 * rank)
+        restore_state(snap)
+        e_rng = timed_stream()
         pins = [torch.empty((args.rays, 3), dtype=torch.int32).pin_memory() for _ in range(2)]
         dbuf = torch.empty((args.rays, 3), dtype=torch.int32, device=f"cuda:{local}")
         pool = ThreadPoolExecutor(1)  # the ctypes draw releases the GIL
@@ -457,8 +505,6 @@ def run_ours(args):
             nxt[0] = pool.submit(draw, k ^ 1)  # next batch drawn while this step runs
             return mapper.step(dbuf, cfg.lambda_d, exchange=args.exchange)
 
-        for _ in range(args.warmup):
-            e_step()
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
@@ -538,6 +584,27 @@ def run_ours(args):
                                  "unit": "GB/s", "frac": t_gbps / peak,
                                  "kernel": "k_pose_group (GN graph)"},
                     "ate_rmse_m": float(np.sqrt(np.mean(np.square(errs))))}
+        # e2e: frames arrive as sensor data (8-bit RGB + 16-bit depth units, the
+        # reference dataset's format): each frame is uploaded (H2D, converted on
+        # the device) and tracked, and its pose read back, inside the timed loop
+        sens = [synth.sensor_frame(f.color, f.depth, intr.depth_scale, pose=f.gt_pose)
+                for f in tframes]
+        gt_ctx.reserve_frames(intr, 1)
+        gt_ctx.set_frame_u8u16(0, sens[0].color_u8, sens[0].depth_u16, tposes[0])
+        gt_ctx.track_frame_gn(0, intr, tposes[0], gn)  # warm-up (slot, graph)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        prev = tposes[0]
+        for i in range(1, len(sens)):
+            gt_ctx.set_frame_u8u16(0, sens[i].color_u8, sens[i].depth_u16, prev)
+            prev = gt_ctx.track_frame_gn(0, intr, prev, gn).pose
+        e_dt = time.perf_counter() - t0
+        tracking["e2e"] = {
+            "frames_per_s": nf / e_dt, "ms_per_frame": 1e3 * e_dt / nf,
+            "h2d_bytes_per_frame": intr.width * intr.height * 5, "d2h_bytes_per_frame": 56,
+            "api": "Context.set_frame_u8u16 (sensor frame H2D + device decode) + "
+                   "Context.track_frame_gn (one CUDA graph) + pose D2H, per frame"}
+        gt_ctx.load_frames(intr, tframes)
         # the same kernel at a throughput-sized batch (262,144 rays per iteration):
         # at 16K rays one GN iteration is a single latency-bound wave, so the
         # config-2 roofline fraction says little about the kernel itself
@@ -567,7 +634,8 @@ def run_ours(args):
     elif not args.no_cpu and world == 1 and rank == 0:
         try:
             per_step, _ = cpu_samples_per_step(args, gt, intr, frames)
-            r = cpu_reference(args, gt, intr, keyposes, frames, args.cpu_seconds)
+            r = cpu_reference(args, gt, intr, keyposes, frames, args.cpu_seconds,
+                              amortised_rays=args.cpu_amortised_rays)
             if r:
                 cpu = {"value": per_step * r["steps"] / r["seconds"], "unit": "samples/s",
                        "cores": r["threads"], "kind": "reference",
@@ -575,6 +643,23 @@ def run_ours(args):
                                  f"257^3 fp64 grid, fresh sigma_init=0.1 map "
                                  f"({per_step} composited samples/step); threads = fastest "
                                  f"of the sweep {r['sweep_s']} (s/step)"}
+                if "amortised" in r:
+                    a = r["amortised"]
+                    # composited samples of that batch, counted on the device (the
+                    # schedules are bit-exact with the reference's, tests/)
+                    cctx = Context(local)
+                    cctx.init_grid(gt.geom, 0.1)
+                    cctx.load_frames(intr, frames)
+                    ab = Rng(1).draw_batch(len(frames), intr.width, intr.height, a["rays"])
+                    ast_ = cctx.mapping_step(MappingConfig(), ab)
+                    cctx.close()
+                    cpu["amortised"] = {
+                        "value": ast_.samples / a["seconds"], "unit": "samples/s",
+                        "cores": a["threads"], "kind": "reference",
+                        "sample": f"1 reference mapping_step x {a['rays']} rays (the first "
+                                  f"Rng(1) batch, {ast_.samples} composited samples) on "
+                                  f"{a['threads']} workers: the per-worker 3.8 GB zero-fill "
+                                  f"(mapping.cpp:155-157) amortised over 16x the batch"}
         except Exception as e:  # the baseline must never hide our own number
             cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "reference",
                    "sample": f"failed: {e}"}
@@ -618,16 +703,44 @@ def emit(obj):
         os.write(_JSON_FD, line)
 
 
+def launch_ranks(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: re-launch this script as
+    N ranks (one process per GPU) under torch.distributed.run on this node. Fails
+    loudly when the node has fewer than N GPUs — never a silent N=1 run."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but this node has {have} GPU(s); "
+                         "refusing to run a smaller world\n")
+        return 2
+    import socket
+    with socket.socket() as so:  # a free rendezvous port on the loopback interface
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    # the ranks inherit the original stdout: rank 0 prints the one JSON line there
+    return subprocess.call(cmd, stdout=_JSON_FD, stderr=2)
+
+
 def main():
     global _JSON_FD
     sys.stdout.flush()
     _JSON_FD = os.dup(1)
     os.dup2(2, 1)
     args = parse()
+    world = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+        run_reference(args)  # rank 0 alone (the CPU reference has no device ranks)
+        return
+    if world is None and args.gpus > 1:
+        sys.exit(launch_ranks(args))
+    if world is not None and int(world) != args.gpus and not args.dist_path:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        sys.exit(2)
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -132,14 +132,25 @@ typedef struct {
   double final_loss;
 } vrf_track_frame_result;
 
-/* Gauss-Newton / Levenberg-Marquardt tracker (new; the reference only has Adam). */
+/* Pose kernels (K5). PARITY: FP64 SH and Jacobian partials, the reference-parity
+ * path of pose_gradient / track_frame. GN: the Gauss-Newton tracker's kernel (fp32
+ * SH contraction and lane Jacobian partials; FP64 march, sigma replay, T and
+ * compositing). GN_CHECK: a second implementation of GN's arithmetic with
+ * group-independent control flow, bit-identical to GN by test. */
+#define VRF_POSE_KERNEL_PARITY 0
+#define VRF_POSE_KERNEL_GN 1
+#define VRF_POSE_KERNEL_GN_CHECK 2
+
+/* Gauss-Newton / Levenberg-Marquardt tracker (new; the reference only has Adam).
+ * Every iteration draws exactly rays_per_iteration pixels, stratified over a
+ * 2^L x 2^L tile grid with 4^L <= rays_per_iteration. */
 typedef struct {
   int32_t rays_per_iteration, iterations;
   double lambda_p, lambda_d;
   double damping;        /* LM: (JtJ + damping*diag(JtJ) + 1e-12 I) delta = -Jtr */
   int32_t max_redraws;
-  int32_t reserved;
-  uint64_t seed;         /* device Philox stream for the valid-depth pixel draws */
+  int32_t kernel;        /* VRF_POSE_KERNEL_GN (default) or VRF_POSE_KERNEL_GN_CHECK */
+  uint64_t seed;         /* device counter-based stream for the valid-depth pixel draws */
   vrf_render_params render;
 } vrf_gn_config;
 
@@ -175,6 +186,12 @@ int vrf_set_shard_multiple(vrf_context* ctx, int world_size);
  * ((void*)1), not NULL. */
 int vrf_set_stream(vrf_context* ctx, void* stream);
 int vrf_get_device_buffers(vrf_context* ctx, vrf_device_buffers* out);
+/* Sample records of the fast mapping path (K0 writes up to K per ray, K2 walks
+ * them; rays with more samples take the recompute-march backward). budget_gb <= 0:
+ * 30 % of free HBM; max_k < 0: K from the longest ray seen (<= 1024); max_k == 0:
+ * no records (every ray takes the recompute-march backward); max_k >= 4: at most
+ * max_k records per ray. */
+int vrf_set_record_limits(vrf_context* ctx, double budget_gb, int max_k);
 /* Number of this library's own kernels the context launched since creation
  * (bench evidence; cub sorts and memsets are not counted). */
 int64_t vrf_kernel_launch_count(const vrf_context* ctx);
@@ -320,6 +337,12 @@ int vrf_pose_gradient(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
 int vrf_pose_normal_equations(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
                               const vrf_pose* pose, const int32_t* pixels, int n,
                               const vrf_tracking_loss* cfg, vrf_normal_equations* out);
+/* The same normal equations through a chosen pose kernel (VRF_POSE_KERNEL_*):
+ * the parity tests evaluate the Gauss-Newton kernel on fixed pixels with it. */
+int vrf_pose_normal_equations_ex(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
+                                 const vrf_pose* pose, const int32_t* pixels, int n,
+                                 const vrf_tracking_loss* cfg, int kernel,
+                                 vrf_normal_equations* out);
 /* track_frame — tracking.hpp:82-84 (tracking.cpp:170-252): Adam, pixel draws from
  * the reference Rng stream (xoshiro256**, seed cfg->seed). loss_trace: iterations. */
 int vrf_track_frame(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
@@ -330,6 +353,32 @@ int vrf_track_frame(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
 int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
                        const vrf_pose* init, const vrf_gn_config* cfg,
                        vrf_track_frame_result* out);
+/* Per-iteration record of the last vrf_track_frame_gn call: hist[3 i .. 3 i + 2] =
+ * (loss / m, m, composited samples) of iteration i, as evaluated before its step.
+ * Copies min(cap, 3 * iterations) doubles; returns the iteration count. */
+int vrf_track_frame_gn_history(vrf_context* ctx, double* hist, int cap);
+
+/* ---- evaluation: evaluate_map_quality (eval.cpp:210-240) with the views rendered
+ * and scored on the device. n_views views at poses[v] against the reference images
+ * colors[v] (H*W*3) / depths[v] (H*W), host memory. samples: n_samples (view, x, y)
+ * triples — the PSNR pixel draws (vrf_rng_draw_eval_samples). Sums over the pixels
+ * the render hit (rendered depth > 0): squared colour error over the samples
+ * (psnr, eval.cpp:64-97) and |D - D*| over valid reference depth (depth_l1,
+ * eval.cpp:99-122). */
+typedef struct {
+  double sum_sq_color;   /* sum over hit samples of sum_ch (C - C*)^2 */
+  int64_t color_samples;
+  double sum_abs_depth;  /* sum over hit pixels with D* > 0 of |D - D*| */
+  int64_t depth_pixels;
+} vrf_view_metrics;
+int vrf_evaluate_views(vrf_context* ctx, const vrf_intrinsics* intr, int n_views,
+                       const vrf_pose* poses, const double* const* colors,
+                       const double* const* depths, const vrf_render_params* params,
+                       const int32_t* samples, int n_samples, vrf_view_metrics* out);
+/* eval.cpp:72-83's draws: per image draw, image = U[n_images), then pixels_per_image
+ * (x = U[width), y = U[height)); out: images * pixels_per_image (image, x, y). */
+void vrf_rng_draw_eval_samples(uint64_t state[4], int n_images, int width, int height,
+                               int images, int pixels_per_image, int32_t* out);
 
 /* ---- host helpers: the reference's Rng stream (rng.hpp:13-81, xoshiro256**) */
 void vrf_rng_seed(uint64_t seed, uint64_t state[4]);

@@ -356,6 +356,17 @@ class RefLib:
                                             C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         lib.ref_track_frame.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        # eval.cpp / trajectory.cpp
+        vp = C.c_void_p
+        lib.ref_ate_rmse.argtypes = [vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp]
+        lib.ref_rpe.argtypes = [vp, vp, C.c_int, vp, vp, C.c_int, C.c_double, vp, vp, vp]
+        lib.ref_psnr.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                 C.c_uint64, vp, vp]
+        lib.ref_depth_l1.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp]
+        lib.ref_evaluate_map_quality.argtypes = [vp, vp, vp, vp, C.c_int, vp, C.c_int, C.c_int,
+                                                 C.c_uint64, C.c_int, vp, vp, vp, vp]
+        lib.ref_save_tum.argtypes = [C.c_char_p, vp, vp, C.c_int]
+        lib.ref_load_tum.argtypes = [C.c_char_p, C.c_int, vp, vp]
         self.lib = lib
 
     def _err(self, rc, what):
@@ -515,3 +526,77 @@ class RefLib:
                                            C.byref(pose_s(init)), C.byref(track_cfg(tcfg)), threads,
                                            C.byref(out), _ptr(trace)), "track_frame")
         return out, trace[:out.iterations_run]
+
+    # ---- eval.cpp / trajectory.cpp
+    @staticmethod
+    def _traj(poses, ts):
+        arr = (PoseS * max(len(poses), 1))(*[pose_s(p) for p in poses])
+        return np.ascontiguousarray(ts, np.float64), arr
+
+    def ate_rmse(self, est, est_ts, ref, ref_ts, align=True):
+        """eval.cpp:140-172 -> (rmse, pairs)."""
+        et, ea = self._traj(est, est_ts)
+        rt, ra = self._traj(ref, ref_ts)
+        out, pairs = C.c_double(), C.c_int()
+        self._err(self.lib.ref_ate_rmse(_ptr(et), ea, len(est), _ptr(rt), ra, len(ref),
+                                        1 if align else 0, C.byref(out), C.byref(pairs)),
+                  "ate_rmse")
+        return out.value, pairs.value
+
+    def rpe(self, est, est_ts, ref, ref_ts, interval_m=1.0):
+        """eval.cpp:174-208 -> (rpe_t, rpe_r_deg, pairs)."""
+        et, ea = self._traj(est, est_ts)
+        rt, ra = self._traj(ref, ref_ts)
+        t, r, n = C.c_double(), C.c_double(), C.c_int()
+        self._err(self.lib.ref_rpe(_ptr(et), ea, len(est), _ptr(rt), ra, len(ref),
+                                   float(interval_m), C.byref(t), C.byref(r), C.byref(n)), "rpe")
+        return t.value, r.value, n.value
+
+    def psnr(self, rendered, reference, masks=None, images=10, pixels_per_image=10000, seed=0):
+        """eval.cpp:64-97 -> (psnr_db, samples)."""
+        a = np.ascontiguousarray(np.stack(rendered), np.float64)
+        b = np.ascontiguousarray(np.stack(reference), np.float64)
+        m = None if masks is None else np.ascontiguousarray(np.stack(masks), np.float64)
+        n, h, w = a.shape[:3]
+        out, cnt = C.c_double(), C.c_int()
+        self._err(self.lib.ref_psnr(_ptr(a), _ptr(b), None if m is None else _ptr(m), n, w, h,
+                                    images, pixels_per_image, seed & (2**64 - 1), C.byref(out),
+                                    C.byref(cnt)), "psnr")
+        return out.value, cnt.value
+
+    def depth_l1(self, rendered, reference, masks=None):
+        """eval.cpp:99-122 -> (l1_m, pixels)."""
+        a = np.ascontiguousarray(np.stack(rendered), np.float64)
+        b = np.ascontiguousarray(np.stack(reference), np.float64)
+        m = None if masks is None else np.ascontiguousarray(np.stack(masks), np.float64)
+        n, h, w = a.shape
+        out, cnt = C.c_double(), C.c_int()
+        self._err(self.lib.ref_depth_l1(_ptr(a), _ptr(b), None if m is None else _ptr(m), n, w,
+                                        h, C.byref(out), C.byref(cnt)), "depth_l1")
+        return out.value, cnt.value
+
+    def evaluate_map_quality(self, grid_h, frames_h, intr, indices, params, images=10,
+                             pixels_per_image=10000, seed=0, threads=0):
+        """eval.cpp:210-240 -> (psnr_db, depth_l1_m, color_samples, depth_pixels)."""
+        idx = np.ascontiguousarray(indices, np.int32)
+        p, l1 = C.c_double(), C.c_double()
+        ns, npx = C.c_int(), C.c_int()
+        self._err(self.lib.ref_evaluate_map_quality(
+            grid_h, frames_h, C.byref(intr_s(intr)), _ptr(idx), len(idx),
+            C.byref(params_s(params)), images, pixels_per_image, seed & (2**64 - 1), threads,
+            C.byref(p), C.byref(l1), C.byref(ns), C.byref(npx)), "evaluate_map_quality")
+        return p.value, l1.value, ns.value, npx.value
+
+    def save_tum(self, path, poses, ts):
+        """trajectory.cpp:10-23."""
+        t, a = self._traj(poses, ts)
+        self._err(self.lib.ref_save_tum(str(path).encode(), _ptr(t), a, len(poses)), "save_tum")
+
+    def load_tum(self, path, cap=100000):
+        """trajectory.cpp:25-46 -> (poses [(q, t)], timestamps)."""
+        ts = np.zeros(cap)
+        arr = (PoseS * cap)()
+        n = self.lib.ref_load_tum(str(path).encode(), cap, _ptr(ts), arr)
+        if n < 0:
+            _check(-n, "load_tum: " + self.lib.ref_last_error().decode())
+        return [(tuple(arr[i].q), tuple(arr[i].t)) for i in range(min(n, cap))], ts[:n]

@@ -14,10 +14,12 @@
 #include <string>
 #include <vector>
 
+#include "voxrf/eval.hpp"
 #include "voxrf/gradients.hpp"
 #include "voxrf/mapping.hpp"
 #include "voxrf/renderer.hpp"
 #include "voxrf/tracking.hpp"
+#include "voxrf/trajectory.hpp"
 
 #include "voxrf_oracle.h"  // POD structs shared with the restatement
 
@@ -523,6 +525,109 @@ int ref_track_sequence(const void* grid, const void* frames, const or_intrinsics
     for (std::size_t i = 0; i < r.trajectory.poses.size(); ++i)
       poses_out[i] = from_pose(r.trajectory.poses[i]);
   });
+}
+
+// ---- eval.cpp / trajectory.cpp (metrics and TUM I/O around the hot path)
+namespace {
+Trajectory to_traj(const double* ts, const or_pose* poses, int n) {
+  Trajectory t;
+  for (int i = 0; i < n; ++i) t.push(ts[i], to_pose(poses[i]));
+  return t;
+}
+std::vector<ImageF> to_images(const double* data, int n, int w, int h, int c) {
+  std::vector<ImageF> out;
+  for (int k = 0; k < n; ++k) {
+    ImageF im(w, h, c);
+    std::memcpy(im.data.data(), data + (size_t)k * w * h * c, sizeof(double) * w * h * c);
+    out.push_back(std::move(im));
+  }
+  return out;
+}
+std::vector<const ImageF*> ptrs(const std::vector<ImageF>& v) {
+  std::vector<const ImageF*> p;
+  for (const ImageF& i : v) p.push_back(&i);
+  return p;
+}
+}  // namespace
+
+int ref_ate_rmse(const double* est_ts, const or_pose* est, int n_est, const double* ref_ts,
+                 const or_pose* ref, int n_ref, int align, double* out, int* pairs) {
+  REF_GUARD({
+    *out = ate_rmse(to_traj(est_ts, est, n_est), to_traj(ref_ts, ref, n_ref), align != 0, pairs);
+  });
+}
+int ref_rpe(const double* est_ts, const or_pose* est, int n_est, const double* ref_ts,
+            const or_pose* ref, int n_ref, double interval_m, double* rpe_t, double* rpe_r_deg,
+            int* pairs) {
+  REF_GUARD({
+    const RpeResult r = rpe(to_traj(est_ts, est, n_est), to_traj(ref_ts, ref, n_ref), interval_m);
+    *rpe_t = r.rpe_t;
+    *rpe_r_deg = r.rpe_r_deg;
+    *pairs = r.pairs;
+  });
+}
+// n images of w x h: rendered / reference colour n*h*w*3; masks n*h*w or NULL
+int ref_psnr(const double* rendered, const double* reference, const double* masks, int n, int w,
+             int h, int images, int pixels_per_image, uint64_t seed, double* out, int* samples) {
+  REF_GUARD({
+    const auto a = to_images(rendered, n, w, h, 3), b = to_images(reference, n, w, h, 3);
+    std::vector<ImageF> m;
+    if (masks) m = to_images(masks, n, w, h, 1);
+    PixelSampleSpec spec;
+    spec.images = images;
+    spec.pixels_per_image = pixels_per_image;
+    spec.seed = seed;
+    *out = psnr(ptrs(a), ptrs(b), ptrs(m), spec, samples);
+  });
+}
+int ref_depth_l1(const double* rendered, const double* reference, const double* masks, int n,
+                 int w, int h, double* out, int* pixels) {
+  REF_GUARD({
+    const auto a = to_images(rendered, n, w, h, 1), b = to_images(reference, n, w, h, 1);
+    std::vector<ImageF> m;
+    if (masks) m = to_images(masks, n, w, h, 1);
+    *out = depth_l1(ptrs(a), ptrs(b), ptrs(m), pixels);
+  });
+}
+// evaluate_map_quality over frames[idx] of a frames handle (no exact depth)
+int ref_evaluate_map_quality(const void* grid, const void* frames, const or_intrinsics* intr,
+                             const int* idx, int n_idx, const or_render_params* p, int images,
+                             int pixels_per_image, uint64_t seed, int threads, double* psnr_db,
+                             double* depth_l1_m, int* color_samples, int* depth_pixels) {
+  REF_GUARD({
+    Dataset ds;
+    ds.intrinsics = to_intr(*intr);
+    ds.frames = static_cast<const RefFrames*>(frames)->frames;
+    MapQualityOptions o;
+    o.sampling.images = images;
+    o.sampling.pixels_per_image = pixels_per_image;
+    o.sampling.seed = seed;
+    o.render = to_params(*p);
+    o.threads = threads;
+    const MapQuality q = evaluate_map_quality(*static_cast<const VoxelGrid*>(grid), ds,
+                                              std::vector<int>(idx, idx + n_idx), o);
+    *psnr_db = q.psnr_db;
+    *depth_l1_m = q.depth_l1_m;
+    *color_samples = q.color_samples;
+    *depth_pixels = q.depth_pixels;
+  });
+}
+int ref_save_tum(const char* path, const double* ts, const or_pose* poses, int n) {
+  REF_GUARD({ save_tum(path, to_traj(ts, poses, n)); });
+}
+// returns the pose count (<= cap written), or -status
+int ref_load_tum(const char* path, int cap, double* ts, or_pose* poses) {
+  try {
+    const Trajectory t = load_tum(path);
+    for (int i = 0; i < (int)t.size() && i < cap; ++i) {
+      ts[i] = t.timestamps[i];
+      poses[i] = from_pose(t.poses[i]);
+    }
+    return (int)t.size();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -OR_RUNTIME;
+  }
 }
 
 }  // extern "C"

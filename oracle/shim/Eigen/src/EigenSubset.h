@@ -350,6 +350,14 @@ class Matrix {
     for (int i = 0; i < R && i < C; ++i) s = s + (*this)(i, i);
     return s;
   }
+  // Eigen determinant_impl<3>: sum of bruteforce_det3_helper(m, a, b, c) =
+  // m(0,a) * (m(1,b) m(2,c) - m(1,c) m(2,b)) over the first column's cofactors
+  T determinant() const {
+    static_assert(R == 3 && C == 3, "shim: 3x3 determinant only");
+    const Matrix& m = *this;
+    auto h = [&m](int a, int b, int c) { return m(0, a) * (m(1, b) * m(2, c) - m(1, c) * m(2, b)); };
+    return h(0, 1, 2) - h(1, 0, 2) + h(2, 0, 1);
+  }
 
   CommaInitializer<Matrix> operator<<(const T& s) { return CommaInitializer<Matrix>(*this, s); }
   template <typename S, typename = std::enable_if_t<std::is_arithmetic_v<S> && !std::is_same_v<S, T>>>
@@ -576,7 +584,6 @@ AngleAxis<T>::AngleAxis(const Quaternion<T>& q) {
 using Quaterniond = Quaternion<double>;
 using AngleAxisd = AngleAxis<double>;
 
-// 3x3 SVD used only by eval.cpp's ATE alignment (off the hot path); not built.
-enum { ComputeFullU = 1, ComputeFullV = 2 };
-
 }  // namespace Eigen
+
+#include "EigenEval.h"

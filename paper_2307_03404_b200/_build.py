@@ -16,7 +16,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libvoxrf_b200.so"
-SOURCES = ["vrf_kernels.cu", "vrf_warp.cu", "vrf_track.cu", "vrf_capi.cu", "vrf_map.cu", "vrf_pose.cu"]
+SOURCES = ["vrf_kernels.cu", "vrf_order.cu", "vrf_track.cu", "vrf_capi.cu", "vrf_map.cu", "vrf_pose.cu",
+           "vrf_eval.cu"]
 HEADERS = ["vrf_device.cuh", "vrf_internal.h", "vrf_context.h"]
 
 NVCC_FLAGS = [
@@ -45,21 +46,26 @@ def _digest() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every CUDA source for sm_100a and link the C-ABI library."""
-    LIBDIR.mkdir(exist_ok=True)
-    stamp = LIBDIR / "build.sha256"
-    digest = _digest()
-    if LIB.exists() and stamp.exists() and stamp.read_text() == digest and not force:
-        return LIB
+def build(force: bool = False, verbose: bool = False, libdir: Path = LIBDIR,
+          defines=()) -> Path:
+    """Compile every CUDA source for sm_100a and link the C-ABI library. libdir /
+    defines: an A/B variant of the same sources (tools/ab/), loaded with VRF_LIB."""
+    libdir = Path(libdir)
+    libdir.mkdir(parents=True, exist_ok=True)
+    lib = libdir / LIB.name
+    flags = [*NVCC_FLAGS, *(f"-D{d}" for d in defines)]
+    stamp = libdir / "build.sha256"
+    digest = _digest() + " ".join(defines)
+    if lib.exists() and stamp.exists() and stamp.read_text() == digest and not force:
+        return lib
     nvcc = _nvcc()
-    objdir = LIBDIR / "obj"
+    objdir = libdir / "obj"
     objdir.mkdir(exist_ok=True)
     log = []
     procs = []
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc, *flags, "-c", str(CSRC / src), "-o", str(obj)]
         procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE,
                                                  stderr=subprocess.STDOUT, text=True)))
     for src, cmd, p in procs:
@@ -67,18 +73,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         log.append(f"$ {' '.join(cmd)}\n{out}")
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{out}")
-    objs = [str(objdir / (Path(s).stem + ".o")) for s in SOURCES]
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB), *objs,
+    objs = [str(objdir / (Path(x).stem + ".o")) for x in SOURCES]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib), *objs,
            "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")
-    (LIBDIR / "ptxas.log").write_text("\n".join(log))
+    (libdir / "ptxas.log").write_text("\n".join(log))
     stamp.write_text(digest)
     if verbose:
         print("\n".join(log))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -7,13 +7,22 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libvoxrf_b200.so"
+import os
+
+# VRF_LIB: another build of this same library (A/B experiments, tools/ab/).
+_LIB_PATH = Path(os.environ.get("VRF_LIB") or
+                 Path(__file__).resolve().parent / "_lib" / "libvoxrf_b200.so")
 
 VRF_OK = 0
 VRF_ERR_INVALID_ARGUMENT = 1
 VRF_ERR_OUT_OF_RANGE = 2
 VRF_ERR_RUNTIME = 3
 VRF_ERR_CUDA = 4
+
+# pose kernels (include/voxrf_b200.h VRF_POSE_KERNEL_*)
+POSE_KERNEL_PARITY = 0
+POSE_KERNEL_GN = 1
+POSE_KERNEL_GN_CHECK = 2
 
 
 class GridGeometry_c(C.Structure):
@@ -79,8 +88,13 @@ class TrackFrameResult_c(C.Structure):
 class GnConfig_c(C.Structure):
     _fields_ = [("rays_per_iteration", C.c_int32), ("iterations", C.c_int32),
                 ("lambda_p", C.c_double), ("lambda_d", C.c_double), ("damping", C.c_double),
-                ("max_redraws", C.c_int32), ("reserved", C.c_int32), ("seed", C.c_uint64),
+                ("max_redraws", C.c_int32), ("kernel", C.c_int32), ("seed", C.c_uint64),
                 ("render", RenderParams_c)]
+
+
+class ViewMetrics_c(C.Structure):
+    _fields_ = [("sum_sq_color", C.c_double), ("color_samples", C.c_int64),
+                ("sum_abs_depth", C.c_double), ("depth_pixels", C.c_int64)]
 
 
 class DeviceBuffers_c(C.Structure):
@@ -112,6 +126,7 @@ _SIGS = {
     "vrf_last_error": (C.c_char_p, [vp]),
     "vrf_set_shard_multiple": (C.c_int, [vp, C.c_int]),
     "vrf_set_stream": (C.c_int, [vp, vp]),
+    "vrf_set_record_limits": (C.c_int, [vp, C.c_double, C.c_int]),
     "vrf_get_device_buffers": (C.c_int, [vp, P(DeviceBuffers_c)]),
     "vrf_kernel_launch_count": (C.c_int64, [vp]),
     "vrf_profile_enable": (C.c_int, [vp, C.c_int]),
@@ -165,10 +180,18 @@ _SIGS = {
                                     P(TrackingLoss_c), P(PoseGradient_c)]),
     "vrf_pose_normal_equations": (C.c_int, [vp, C.c_int, P(Intrinsics_c), P(Pose_c), vp,
                                             C.c_int, P(TrackingLoss_c), P(NormalEquations_c)]),
+    "vrf_pose_normal_equations_ex": (C.c_int, [vp, C.c_int, P(Intrinsics_c), P(Pose_c), vp,
+                                               C.c_int, P(TrackingLoss_c), C.c_int,
+                                               P(NormalEquations_c)]),
     "vrf_track_frame": (C.c_int, [vp, C.c_int, P(Intrinsics_c), P(Pose_c),
                                   P(TrackingConfig_c), P(TrackFrameResult_c), vp]),
     "vrf_track_frame_gn": (C.c_int, [vp, C.c_int, P(Intrinsics_c), P(Pose_c), P(GnConfig_c),
                                      P(TrackFrameResult_c)]),
+    "vrf_track_frame_gn_history": (C.c_int, [vp, P(C.c_double), C.c_int]),
+    "vrf_evaluate_views": (C.c_int, [vp, P(Intrinsics_c), C.c_int, vp, vp, vp,
+                                     P(RenderParams_c), vp, C.c_int, P(ViewMetrics_c)]),
+    "vrf_rng_draw_eval_samples": (None, [P(C.c_uint64), C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, vp]),
     "vrf_rng_seed": (None, [C.c_uint64, P(C.c_uint64)]),
     "vrf_rng_next": (C.c_uint64, [P(C.c_uint64)]),
     "vrf_rng_draw_batch": (None, [P(C.c_uint64), C.c_int, C.c_int, C.c_int, C.c_int, vp]),

@@ -273,7 +273,9 @@ class TrackingConfig:
 
 @dataclass
 class GNConfig:
-    """Gauss-Newton / LM tracker settings (new; the reference only has Adam)."""
+    """Gauss-Newton / LM tracker settings (new; the reference only has Adam).
+
+    Every iteration evaluates exactly rays_per_iteration stratified pixel draws."""
     rays_per_iteration: int = 16384
     iterations: int = 10
     lambda_p: float = 1.0
@@ -282,10 +284,12 @@ class GNConfig:
     max_redraws: int = 50
     seed: int = 7
     render: RenderParams = field(default_factory=RenderParams)
+    # capi.POSE_KERNEL_GN (k_pose_group_u) or POSE_KERNEL_GN_CHECK (its checker)
+    kernel: int = capi.POSE_KERNEL_GN
 
     def _c(self):
         return capi.GnConfig_c(self.rays_per_iteration, self.iterations, self.lambda_p,
-                               self.lambda_d, self.damping, self.max_redraws, 0,
+                               self.lambda_d, self.damping, self.max_redraws, self.kernel,
                                self.seed & (2**64 - 1), self.render._c())
 
 
@@ -338,6 +342,14 @@ class Rng:
         out = np.empty((n, 3), dtype=np.int32)
         capi.load().vrf_rng_draw_batch(self.state, n_frames, width, height, n,
                                        out.ctypes.data_as(C.c_void_p))
+        return out
+
+    def draw_eval_samples(self, n_images: int, width: int, height: int, images: int,
+                          pixels_per_image: int) -> np.ndarray:
+        """eval.cpp:72-83's draws: (image, x, y) rows, images x pixels_per_image."""
+        out = np.zeros((images * pixels_per_image, 3), np.int32)
+        capi.load().vrf_rng_draw_eval_samples(self.state, n_images, width, height, images,
+                                              pixels_per_image, out.ctypes.data_as(C.c_void_p))
         return out
 
     def draw_valid_pixels(self, depth: np.ndarray, count: int, max_redraws: int) -> np.ndarray:
@@ -408,6 +420,12 @@ class Context:
 
     PROFILE_SLOTS = ("map_forward", "map_backward", "rmsprop", "misc", "pose_forward",
                      "pose_backward", "render", "deterministic_reduce")
+
+    def set_record_limits(self, budget_gb: float = -1.0, max_k: int = -1):
+        """Sample-record sizing of the fast mapping path (vrf_set_record_limits):
+        max_k = 0 disables records, max_k >= 4 caps records per ray (longer rays
+        take the recompute-march backward); negative values are automatic."""
+        self._check(self._lib.vrf_set_record_limits(self._h, float(budget_gb), int(max_k)))
 
     def profile_enable(self, on: bool = True):
         self._check(self._lib.vrf_profile_enable(self._h, 1 if on else 0))
@@ -714,15 +732,41 @@ class Context:
                             out.samples)
 
     def pose_normal_equations(self, frame: int, intr: CameraIntrinsics, pose: Pose,
-                              pixels: np.ndarray, config: TrackingConfig) -> NormalEquations:
+                              pixels: np.ndarray, config: TrackingConfig,
+                              kernel: int = capi.POSE_KERNEL_PARITY) -> NormalEquations:
+        """JᵀJ / Jᵀr over the given pixels; kernel selects the pose kernel
+        (POSE_KERNEL_PARITY: FP64, POSE_KERNEL_GN: the Gauss-Newton tracker's)."""
         px = np.ascontiguousarray(pixels, dtype=np.int32).reshape(-1, 2)
         out = capi.NormalEquations_c()
         ic, pc, lc = intr._c(), pose._c(), config._loss_c()
-        self._check(self._lib.vrf_pose_normal_equations(self._h, frame, C.byref(ic), C.byref(pc),
-                                                        _ptr(px), px.shape[0], C.byref(lc),
-                                                        C.byref(out)))
+        self._check(self._lib.vrf_pose_normal_equations_ex(self._h, frame, C.byref(ic),
+                                                           C.byref(pc), _ptr(px), px.shape[0],
+                                                           C.byref(lc), kernel, C.byref(out)))
         return NormalEquations(unpack_sym6(out.jtj), np.array(out.jtr), out.loss, out.rays_used,
                                out.samples)
+
+    def evaluate_views(self, intr: CameraIntrinsics, poses: Sequence[Pose], colors, depths,
+                       samples: np.ndarray, params: Optional[RenderParams] = None):
+        """vrf_evaluate_views: renders each view on the device and scores it there
+        against (colors[v], depths[v]). Returns (sum_sq_color, color_samples,
+        sum_abs_depth, depth_pixels)."""
+        n = len(poses)
+        h, w = intr.height, intr.width
+        cs = [np.ascontiguousarray(c, np.float64) for c in colors]
+        ds = [np.ascontiguousarray(d, np.float64) for d in depths]
+        for c, d in zip(cs, ds):
+            if c.shape != (h, w, 3) or d.shape != (h, w):
+                raise ValueError("evaluate_map_quality: image dimensions differ")
+        pa = (capi.Pose_c * n)(*[p._c() for p in poses])
+        cp = (C.c_void_p * n)(*[c.ctypes.data for c in cs])
+        dp = (C.c_void_p * n)(*[d.ctypes.data for d in ds])
+        smp = np.ascontiguousarray(samples, np.int32).reshape(-1, 3)
+        out = capi.ViewMetrics_c()
+        ic, rp = intr._c(), (params or RenderParams())._c()
+        self._check(self._lib.vrf_evaluate_views(self._h, C.byref(ic), n, pa, cp, dp,
+                                                 C.byref(rp), _ptr(smp), smp.shape[0],
+                                                 C.byref(out)))
+        return out.sum_sq_color, out.color_samples, out.sum_abs_depth, out.depth_pixels
 
     def track_frame(self, frame: int, intr: CameraIntrinsics, init: Pose,
                     config: TrackingConfig) -> TrackFrameResult:
@@ -742,6 +786,14 @@ class Context:
                                                  C.byref(gc), C.byref(out)))
         return TrackFrameResult(Pose._from_c(out.pose), [out.final_loss], bool(out.failed),
                                 out.iterations_run)
+
+    def track_frame_gn_history(self) -> np.ndarray:
+        """(loss/m, m, samples) per iteration of the last track_frame_gn call."""
+        n = self._lib.vrf_track_frame_gn_history(self._h, None, 0)
+        h = np.zeros(3 * max(n, 1))
+        self._lib.vrf_track_frame_gn_history(self._h, h.ctypes.data_as(C.POINTER(C.c_double)),
+                                             3 * n)
+        return h[:3 * n].reshape(n, 3)
 
 
 def unpack_sym6(packed) -> np.ndarray:
@@ -841,7 +893,7 @@ def pose_inverse(p: Pose) -> Pose:
 
 
 def track_sequence(grid: VoxelGrid, frames: Sequence[Frame], intrinsics: CameraIntrinsics,
-                   config: TrackingConfig):
+                   config: TrackingConfig, ctx: Optional[Context] = None):
     """track_sequence — tracking.hpp:102-103 (tracking.cpp:254-295). Returns
     (poses, status) with status rows (frame, iterations, final_loss, elapsed_ms, failed)."""
     import time
@@ -849,7 +901,7 @@ def track_sequence(grid: VoxelGrid, frames: Sequence[Frame], intrinsics: CameraI
         raise RuntimeError("track_sequence: empty dataset")
     if frames[0].gt_pose is None:
         raise RuntimeError("track_sequence: first frame needs a pose")
-    ctx = default_context()
+    ctx = ctx if ctx is not None else default_context()
     ctx.load_grid(grid)
     ctx.load_frames(intrinsics, frames)
     first = frames[0].gt_pose

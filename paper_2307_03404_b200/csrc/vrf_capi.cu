@@ -29,8 +29,6 @@ int vrf_context_create(int device, vrf_context** out) {
     return VRF_ERR_CUDA;
   }
   ctx->stream = ctx->own_stream;
-  if (const char* mk = std::getenv("VRF_MAP_KERNEL"))
-    ctx->map_kernel = std::string(mk) == "warp" ? 1 : 0;
   *out = ctx;
   return VRF_OK;
 }
@@ -48,7 +46,6 @@ void vrf_context_destroy(vrf_context* ctx) {
   cudaFree(ctx->d_pose_out);
   cudaFree(ctx->d_pose);
   cudaFree(ctx->d_touched);
-  cudaFree(ctx->d_queue);
   cudaFree(ctx->d_nblocks);
   cudaFree(ctx->d_frame);
   cudaFree(ctx->d_gn_pose);
@@ -74,6 +71,15 @@ const char* vrf_last_error(const vrf_context* ctx) { return ctx ? ctx->err.c_str
 int vrf_set_shard_multiple(vrf_context* ctx, int world_size) {
   if (world_size < 1) return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "world_size must be >= 1");
   ctx->shard_multiple = world_size;
+  return VRF_OK;
+}
+
+int vrf_set_record_limits(vrf_context* ctx, double budget_gb, int max_k) {
+  if (max_k > 0 && max_k < 4)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_set_record_limits: max_k must be 0 or >= 4");
+  ctx->rec_budget_gb = budget_gb;
+  ctx->rec_max_k = max_k;
+  ctx->rec_need_tried = 0;
   return VRF_OK;
 }
 

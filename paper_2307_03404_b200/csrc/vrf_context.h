@@ -84,6 +84,8 @@ struct vrf_context {
   int rec_K = 0;
   int max_ray_samples = 0;  // longest ray seen by a mapping forward (sizes rec_K)
   long long rec_need_tried = 0;  // last record depth the budget was evaluated for
+  double rec_budget_gb = -1.0;   // vrf_set_record_limits: <= 0 automatic (30 % of free HBM)
+  int rec_max_k = -1;            // vrf_set_record_limits: < 0 automatic, 0 no records
 
   // multi-GPU phase state
   const int* last_batch = nullptr;
@@ -97,11 +99,8 @@ struct vrf_context {
   unsigned long long* d_touched = nullptr;  // RMSProp float4 groups updated
   long long prof_track_samples = 0;          // composited samples of GN tracking frames
 
-  // warp-per-ray fast path: ray work queues (forward, backward) and ray order
-  int* d_queue = nullptr;
+  // coherent ray order (vrf_order.cu): keys, ids, sorted order, cub scratch
   vrf_host::DeviceScratch s_order, s_okeys, s_okeys2, s_oids, s_otmp;
-  // fast-path mapping kernels: 0 = thread per ray (coherent order), 1 = warp per ray
-  int map_kernel = 0;
 
   // tracking device state: frame index, Gauss-Newton pose / seed / history, and the
   // CUDA graph of one GN frame (re-captured when its key changes)
@@ -110,6 +109,7 @@ struct vrf_context {
   unsigned long long* d_gn_seed = nullptr;
   double* d_gn_hist = nullptr;
   int gn_hist_cap = 0;
+  std::vector<double> gn_last_hist;  // (loss/m, m, samples) per iteration of the last GN frame
   long long grid_generation = 0;
   cudaGraphExec_t gn_graph = nullptr;
   std::vector<unsigned char> gn_key;
@@ -425,19 +425,16 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
   DevParams p;
   int rc = resolve_params(ctx, &cfg->render, &p);
   if (rc) return rc;
-  const bool warp = fast && ctx->map_kernel == 1;
   // (the record path may run the 8-lanes-per-ray K0g: size the partials for it)
-  const int nb = warp ? warp_kernel_blocks()
-                      : std::max(map_forward_blocks(n > 0 ? n : 1),
-                                 fast ? map_forward_rec_blocks(n > 0 ? n : 1) : 0);
+  const int nb = std::max(map_forward_blocks(n > 0 ? n : 1),
+                          fast ? map_forward_rec_blocks(n > 0 ? n : 1) : 0);
   const size_t nn = (size_t)(n > 0 ? n : 1);
   if ((rc = ensure(ctx, ctx->s_raycd, sizeof(double4) * nn))) return rc;
   if ((rc = ensure(ctx, ctx->s_flags, nn))) return rc;
   if ((rc = ensure(ctx, ctx->s_partials, sizeof(MapPartial) * nb))) return rc;
-  if (!ctx->d_queue) CU(cudaMalloc(&ctx->d_queue, sizeof(int) * 4));
   CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
   if (n > 0 && fast) {
-    // (keyframe, Morton tile) ray order for L2 locality, then the warp-per-ray march.
+    // (keyframe, Morton tile) ray order for L2 locality.
     const size_t tmp = ray_order_tmp_bytes(n);
     if ((rc = ensure(ctx, ctx->s_order, sizeof(uint32_t) * nn))) return rc;
     if ((rc = ensure(ctx, ctx->s_okeys, sizeof(uint32_t) * nn))) return rc;
@@ -450,7 +447,6 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
                      tmp, ctx->stream);
     prof_end(ctx, kProfMapMisc, po);
     LAUNCHED(1);  // k_ray_keys (the cub radix sort behind it is a library launch)
-    CU(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int) * 4, ctx->stream));
     // Sample records for the backward: up to K per ray. K covers the longest
     // ray seen so far (x1.25, rounded up to a power of two; 1024 before the first
     // step), within a memory budget (VRF_REC_GB; default 30 % of the free HBM
@@ -458,11 +454,8 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
     // at least doubles K, so steps do not reallocate. Longer rays overflow to
     // the recompute-march backward.
     ctx->rec_K = 0;
-    if (!warp) {
-      static const double env_gb = [] {
-        const char* e = std::getenv("VRF_REC_GB");
-        return e ? std::atof(e) : -1.0;
-      }();
+    if (ctx->rec_max_k != 0) {
+      const double env_gb = ctx->rec_budget_gb > 0.0 ? ctx->rec_budget_gb : -1.0;
       long long need = 1024;
       if (ctx->max_ray_samples > 0) {
         need = 64;
@@ -487,13 +480,16 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
         const long long cand = std::min(need, (long long)(budget / per_level));
         if (held_K < 16 || cand >= 2 * held_K) K = cand;  // grow only by a real factor
       }
+      // an explicit cap (tests force the overflow backward with a small K)
+      const long long kmin = ctx->rec_max_k > 0 ? 4 : 16;
+      if (ctx->rec_max_k > 0) K = std::min<long long>(std::max(K, kmin), ctx->rec_max_k);
       K &= ~3LL;
       // other allocators (e.g. torch's caching allocator in the multi-GPU
       // driver) may hold memory the budget counted: halve on out-of-memory
-      while (K >= 16 &&
+      while (K >= kmin &&
              !try_ensure(ctx->stream, ctx->s_rec, sizeof(SampleRec) * nn32 * (size_t)K))
         K /= 2;
-      if (K >= 16) {
+      if (K >= kmin) {
         if ((rc = ensure(ctx, ctx->s_reccount, sizeof(int) * nn))) return rc;
         ctx->rec_K = (int)(K & ~3LL);
       }
@@ -505,12 +501,6 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
                              (MapPartial*)ctx->s_partials.ptr, ctx->d_err,
                              (const uint32_t*)ctx->s_order.ptr, (SampleRec*)ctx->s_rec.ptr,
                              ctx->rec_K, (int*)ctx->s_reccount.ptr, ctx->stream);
-    else if (warp)
-      launch_map_forward_w(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
-                           batch_dev, (const uint32_t*)ctx->s_order.ptr, n,
-                           (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
-                           (MapPartial*)ctx->s_partials.ptr, ctx->d_queue, ctx->d_err,
-                           ctx->stream);
     else
       launch_map_forward(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
                          batch_dev, n, (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
@@ -531,9 +521,8 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
     CU(cudaMemsetAsync(ctx->s_partials.ptr, 0, sizeof(MapPartial), ctx->stream));
   }
   // partials the launched forward wrote (K0g: 16 rays per CTA)
-  const int nparts = warp ? nb
-                          : ((n > 0 && fast && ctx->rec_K > 0) ? map_forward_rec_blocks(n)
-                                                                 : map_forward_blocks(n > 0 ? n : 1));
+  const int nparts = (n > 0 && fast && ctx->rec_K > 0) ? map_forward_rec_blocks(n)
+                                                       : map_forward_blocks(n > 0 ? n : 1);
   launch_map_reduce((const MapPartial*)ctx->s_partials.ptr, n > 0 ? nparts : 0, ctx->d_stats,
                     ctx->stream);
   LAUNCHED(1);

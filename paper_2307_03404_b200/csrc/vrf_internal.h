@@ -117,7 +117,11 @@ void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, l
                     const MapStats* stats, unsigned long long* touched, cudaStream_t s);
 // Tracking (vrf_track.cu).
 int pose_fused_blocks(int n);
-void launch_pose_fused(bool fp64_sh, const DevGrid& g, const DevParams& p, const DevCam& cam,
+// kParityFp64: k_pose_group<double> (FP64 SH + Jacobian partials; pose_gradient,
+// track_frame). kGnUniform: k_pose_group_u (fp32 partials; the Gauss-Newton
+// tracker). kGroupFp32: k_pose_group<float>, the GN kernel's checker (tests).
+enum class PoseKernel : int { kParityFp64 = 0, kGnUniform = 1, kGroupFp32 = 2 };
+void launch_pose_fused(PoseKernel which, const DevGrid& g, const DevParams& p, const DevCam& cam,
                        const double4* rgbd_base, const int* frame_idx, long long npix,
                        const DevPose* pose, const int* pixels, const uint32_t* order, int n,
                        double lambda_p, double lambda_d, PosePartial* partials, int* err,
@@ -131,23 +135,12 @@ void launch_draw_strat(const double4* rgbd_base, const int* frame_idx, long long
 void launch_gn_step(const PosePartial* ne, DevPose* pose, double damping, double* hist,
                     int iteration, cudaStream_t s);
 
-// Warp-per-ray fast path (vrf_warp.cu).
-int warp_kernel_blocks();
+// Coherent ray order (vrf_order.cu).
 size_t ray_order_tmp_bytes(int n);
 void launch_ray_order(const int* batch, int n, uint32_t* keys, uint32_t* ids, uint32_t* keys2,
                       uint32_t* order, void* tmp, size_t tmp_bytes, cudaStream_t s);
 void launch_pixel_order(const int* pixels, int n, uint32_t* keys, uint32_t* ids, uint32_t* keys2,
                         uint32_t* order, void* tmp, size_t tmp_bytes, cudaStream_t s);
-void launch_map_forward_w(const DevGrid& g, const DevParams& p, const DevCam& cam,
-                          const double4* rgbd, const DevPose* poses, int n_frames,
-                          const int* batch, const uint32_t* order, int n, double4* ray_cd,
-                          uint8_t* flags, MapPartial* partials, int* queue, int* err,
-                          cudaStream_t s);
-void launch_map_backward_w(const DevGrid& g, const DevParams& p, const DevCam& cam,
-                           const double4* rgbd, const DevPose* poses, const int* batch,
-                           const uint32_t* order, int n, const double4* ray_cd,
-                           const uint8_t* flags, const MapStats* stats, const int* global_counts,
-                           float* grad, double lambda_d, int* queue, cudaStream_t s);
 
 // Utilities.
 void launch_fill_payload(float* payload, long long n_vertices, float sigma, cudaStream_t s);

@@ -604,19 +604,113 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
   }
 }
 
-// Scatter sinks: where an aggregated corner (4 factors x SH basis = 28 slots)
-// goes. RedSink issues 7 red.global.add.v4.f32 from registers (default).
-// BulkSink writes the 112-B vertex gradient into a per-thread shared-memory ring
-// and issues ONE cp.reduce.async.bulk (.add.f32, SASS UBLKRED) per corner, so
-// the L2 sees one 112-B reduction instead of seven 16-B ones. Microbenchmark
-// (tools/microbench/bulk_red.cu, 1M threads x 64 coherent flushes, all lanes
-// active): 29 G vertex-flushes/s with red.v4 against 50 G/s bulk. Inside the
-// divergent backward it loses (UBLKRED is uniform-datapath: serialised over the
-// active lanes), so it stays an A/B option (VRF_SCATTER=bulk).
+// ---- per-ray corner aggregation (all K2 variants)
+// The 28-slot upstream of a sample is [dL/dsigma, dcol_ch * basis_m], and the SH
+// basis is constant along a ray, so the contribution to corner k over any run of
+// samples factorises into a[0][k] = sum w_k up_sigma and a[1+ch][k] = sum w_k
+// dcol_ch (clamp-gated): 32 registers instead of 224. A corner is flushed
+// (expanded to 28 slots and reduced into the gradient) only when the ray leaves
+// it. The corners a move to a neighbouring cell (face, edge or vertex adjacent)
+// keeps are carried, and carried by RELABELLING rather than by moving registers:
+// logical corner k of the current cell lives in register slot k ^ X. A shared
+// vertex's corner labels in the two cells differ exactly in the bits of the
+// moved axes, so a move along the axis mask M flushes the departing slots and
+// sets X ^= M; the trilinear weights follow by swapping each axis' (1 - f, f)
+// pair where X has the bit. Every move direction runs the same straight-line
+// code. (r01 moved the registers with one shift routine per direction; a warp
+// ran those variants one after another: ~35 warp instructions per sample at 15
+// active lanes, ncu v23.)
+struct CornerAgg {
+  float a[4][8];  // slot s: logical corner s ^ X of the current cell
+  uint32_t X;
+  uint32_t base;  // vertex_index of the current cell; kNoCell before the first
+  int cx, cy, cz;
+};
+constexpr uint32_t kNoCell = 0xffffffffu;
+
+__device__ __forceinline__ void agg_init(CornerAgg& A) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) A.a[c][k] = 0.f;
+  A.X = 0;
+  A.base = kNoCell;
+  A.cx = A.cy = A.cz = 0;
+}
+
+// Vertex offset of logical corner k from the cell's base vertex (corner_index).
+__device__ __forceinline__ uint32_t corner_off(const DevGrid& g, uint32_t k) {
+  return (k & 1u) + ((k >> 1) & 1u) * (uint32_t)g.rx + (k >> 2) * g.rxy;
+}
+
+// Flushes the slots in `slots` (bit s = slot s) to the sink and zeroes them.
+template <typename Sink>
+__device__ __forceinline__ void agg_flush(CornerAgg& A, Sink& sink, const DevGrid& g,
+                                          uint32_t slots) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (slots & (1u << s)) {
+      // all-zero corners (samples in free space with sigma_raw <= 0 carry w = 0
+      // and a gated dL/dsigma) add nothing: not flushed
+      if (A.a[0][s] != 0.f || A.a[1][s] != 0.f || A.a[2][s] != 0.f || A.a[3][s] != 0.f)
+        sink(A.base + corner_off(g, (uint32_t)s ^ A.X), A.a[0][s], A.a[1][s], A.a[2][s],
+             A.a[3][s]);
+      A.a[0][s] = A.a[1][s] = A.a[2][s] = A.a[3][s] = 0.f;
+    }
+  }
+}
+
+// The ray's next sample is in cell s: flush what it leaves, relabel what it keeps.
+// Returns true when the cell changed.
+template <typename Sink>
+__device__ __forceinline__ bool agg_enter(CornerAgg& A, Sink& sink, const DevGrid& g,
+                                          const Sample& s) {
+  if (s.base == A.base) return false;
+  if (A.base != kNoCell) {
+    const int dx = s.cx - A.cx, dy = s.cy - A.cy, dz = s.cz - A.cz;
+    uint32_t dep = 0xffu, M = 0;
+    if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) {
+      // departing logical corners: bit = 0 on an axis moved up, 1 on one moved
+      // down; in slot terms the per-axis half-masks swap where X has the bit
+      dep = 0;
+      if (dx != 0) dep |= ((A.X & 1u) ^ (uint32_t)(dx < 0)) ? 0xAAu : 0x55u;
+      if (dy != 0) dep |= (((A.X >> 1) & 1u) ^ (uint32_t)(dy < 0)) ? 0xCCu : 0x33u;
+      if (dz != 0) dep |= (((A.X >> 2) & 1u) ^ (uint32_t)(dz < 0)) ? 0xF0u : 0x0Fu;
+      M = (uint32_t)(dx != 0) | ((uint32_t)(dy != 0) << 1) | ((uint32_t)(dz != 0) << 2);
+    }
+    agg_flush(A, sink, g, dep);
+    A.X ^= M;
+  }
+  A.base = s.base;
+  A.cx = s.cx;
+  A.cy = s.cy;
+  A.cz = s.cz;
+  return true;
+}
+
+// Adds a sample's (u_sigma, u_r, u_g, u_b) with trilinear weights (fx, fy, fz).
+__device__ __forceinline__ void agg_add(CornerAgg& A, float fx, float fy, float fz, float u0,
+                                        float u1, float u2, float u3) {
+  const bool sx = A.X & 1u, sy = (A.X >> 1) & 1u, sz = (A.X >> 2) & 1u;
+  const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
+  const float wx[2] = {sx ? fx : gx, sx ? gx : fx};
+  const float wy[2] = {sy ? fy : gy, sy ? gy : fy};
+  const float wz[2] = {sz ? fz : gz, sz ? gz : fz};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
+    A.a[0][k] = fmaf(wk, u0, A.a[0][k]);
+    A.a[1][k] = fmaf(wk, u1, A.a[1][k]);
+    A.a[2][k] = fmaf(wk, u2, A.a[2][k]);
+    A.a[3][k] = fmaf(wk, u3, A.a[3][k]);
+  }
+}
+
+// Direct scatter of a flushed corner: basis expansion + 7 red.global.add.v4.f32.
 struct RedSink {
   float4* __restrict__ grad;
-  __device__ __forceinline__ void operator()(uint32_t v, float s, float r, float gg, float b,
-                                             const float (&bf)[9]) {
+  const float* bf;  // the ray's SH basis (9)
+  __device__ __forceinline__ void operator()(uint32_t v, float s, float r, float gg, float b) {
     float4* dst = grad + (size_t)v * kVec4PerVertex;
     float x[28];
     x[0] = s;
@@ -630,121 +724,17 @@ struct RedSink {
     for (int j = 0; j < kVec4PerVertex; ++j)
       atomicAdd(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
   }
-  __device__ __forceinline__ void finish() {}
 };
 
-constexpr int kBulkSlots = 2;  // per-thread ring of 112-B staging slots
-struct BulkSink {
-  float4* __restrict__ grad;
-  float4* ring;  // this thread's kBulkSlots x 7 float4 in shared memory
-  int slot;
-  __device__ __forceinline__ void operator()(uint32_t v, float s, float r, float gg, float b,
-                                             const float (&bf)[9]) {
-    float4* my = ring + slot * kVec4PerVertex;
-    slot = (slot + 1) % kBulkSlots;
-    // the bulk op that last used this slot must have finished reading it
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kBulkSlots - 1) : "memory");
-    float x[28];
-    x[0] = s;
-#pragma unroll
-    for (int mm = 0; mm < 9; ++mm) {
-      x[1 + mm] = r * bf[mm];
-      x[10 + mm] = gg * bf[mm];
-      x[19 + mm] = b * bf[mm];
-    }
-#pragma unroll
-    for (int j = 0; j < kVec4PerVertex; ++j)
-      my[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(my);
-    asm volatile(
-        "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
-            grad + (size_t)v * kVec4PerVertex),
-        "r"(sa), "n"(kVec4PerVertex * 16)
-        : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  }
-  // all reductions complete (and the ring no longer read) before the thread exits
-  __device__ __forceinline__ void finish() {
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  }
-};
-
-// Scatter corner k of the aggregated cell (slots: sigma, a_ch * basis_m).
-template <typename Sink>
-__device__ __forceinline__ void flush_corner(Sink& sink, const DevGrid& g, uint32_t base,
-                                             float (&a)[4][8], const float (&bf)[9], int k) {
-  const float s = a[0][k], r = a[1][k], gg = a[2][k], b = a[3][k];
-  a[0][k] = a[1][k] = a[2][k] = a[3][k] = 0.f;
-  if (s == 0.f && r == 0.f && gg == 0.f && b == 0.f) return;
-  sink(corner_index(g, base, k), s, r, gg, b, bf);
-}
-
-// Face-adjacent move along the axis of corner bit BIT (+1 if POS): flush the 4
-// departing corners, carry the 4 shared ones to their new corner slots.
-template <int BIT, bool POS, typename Sink>
-__device__ __forceinline__ void shift_cell(Sink& sink, const DevGrid& g, uint32_t old_base,
-                                           float (&a)[4][8], const float (&bf)[9]) {
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if (((k & BIT) != 0) != POS) flush_corner(sink, g, old_base, a, bf, k);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    if (k & BIT) continue;
-    const int hi = k | BIT;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (POS) {
-        a[c][k] = a[c][hi];
-        a[c][hi] = 0.f;
-      } else {
-        a[c][hi] = a[c][k];
-        a[c][k] = 0.f;
-      }
-    }
-  }
-}
-
-// Move of the aggregated cell by (dx, dy, dz): a neighbouring cell (face, edge
-// or vertex adjacent) is reached as up to three unit face shifts, so every
-// corner shared with the new cell is carried and only the corners the ray
-// leaves are flushed (an edge move flushes 6, not 8; corners that are zero —
-// fresh slots of an intermediate cell — are skipped by flush_corner). Anything
-// farther (a block jump) flushes all 8.
-template <typename Sink>
-__device__ __forceinline__ void move_cell(Sink& sink, const DevGrid& g, uint32_t old_base,
-                                          int dx, int dy, int dz, float (&a)[4][8],
-                                          const float (&bf)[9]) {
-  if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) flush_corner(sink, g, old_base, a, bf, k);
-    return;
-  }
-  uint32_t b = old_base;
-  if (dx > 0) shift_cell<1, true>(sink, g, b, a, bf);
-  if (dx < 0) shift_cell<1, false>(sink, g, b, a, bf);
-  b += dx;
-  if (dy > 0) shift_cell<2, true>(sink, g, b, a, bf);
-  if (dy < 0) shift_cell<2, false>(sink, g, b, a, bf);
-  b += dy * g.rx;
-  if (dz > 0) shift_cell<4, true>(sink, g, b, a, bf);
-  if (dz < 0) shift_cell<4, false>(sink, g, b, a, bf);
-}
-
-// Fast-path backward of one ray (fp32 SH, fp32 gradient accumulation). Same
-// schedule, sigma_raw replay, T and termination as the forward pass (all FP64,
-// reference order), so exactly the forward's samples are visited. The colour /
-// depth terms of dL/dsigma_i use the running form
+// Fast-path backward of one ray (fp32 SH, fp32 gradient accumulation) by
+// re-marching it: the rays the record buffer could not hold (kOverflow) and the
+// record-free configuration (vrf_set_record_limits(max_k = 0)). Same schedule,
+// sigma_raw replay, T and termination as the forward pass (all FP64, reference
+// order), so exactly the forward's samples are visited. The colour / depth terms
+// of dL/dsigma_i use the running form
 //   sum_ch upc_ch (c_ch T_{i+1} - C_ch + prefix_ch) = uc_i T_{i+1} + Q_i,
 //   Q_i = sum_ch upc_ch (prefix_ch,i - C_ch),  uc_i = sum_ch upc_ch c_ch,i
 // (gradients.cpp:69-97 regrouped), which keeps 3 FP64 scalars live instead of 11.
-// Per-ray scatter aggregation: the 28-slot upstream of a sample is
-// [dL/dsigma, dcol_ch * basis_m] and basis is constant along the ray, so the
-// contribution to corner k over any run of samples factorises into
-// a[0][k] = sum w_k up_sigma and a[1+ch][k] = sum w_k dcol_ch (clamp-gated):
-// 32 registers instead of 224. Corners are flushed (red.global.add.v4.f32)
-// only when the ray leaves them; corners shared with a face-adjacent next cell
-// are carried over.
 template <bool SKIP>
 __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevParams& p, March& m,
                                                   const MapUp& u, float4* __restrict__ grad) {
@@ -762,15 +752,10 @@ __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevPar
   double T = 1.0;
   double Q = -(upc0 * u.C[0] + upc1 * u.C[1] + upc2 * u.C[2]);
   double Qd = -upd * u.D;
-  float a[4][8];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
-  uint32_t cur = 0xffffffffu;
-  int pcx = 0, pcy = 0, pcz = 0;
+  CornerAgg A;
+  agg_init(A);
   int last_tb = -1;
-  RedSink sink{grad};
+  RedSink sink{grad, bf};
   Sample s;
   while (march_next<SKIP>(g, m, s)) {
     Shade sh;
@@ -791,41 +776,19 @@ __device__ __forceinline__ void map_backward_fast(const DevGrid& g, const DevPar
       ds += upd * (s.t * T_next) + Qd;
     }
     ds *= s.delta;
-    if (s.base != cur) {
-      if (cur != 0xffffffffu)
-        move_cell(sink, g, cur, s.cx - pcx, s.cy - pcy, s.cz - pcz, a, bf);
-      cur = s.base;
-      pcx = s.cx;
-      pcy = s.cy;
-      pcz = s.cz;
-      mark_touched(g, s.cx, s.cy, s.cz, last_tb);
-    }
+    if (agg_enter(A, sink, g, s)) mark_touched(g, s.cx, s.cy, s.cz, last_tb);
     const float wf = (float)wgt;
-    const float u0 = sh.sigma_raw > 0.0 ? (float)ds : 0.f;
-    const float u1 = sh.clamped[0] ? 0.f : (float)upc0 * wf;
-    const float u2 = sh.clamped[1] ? 0.f : (float)upc1 * wf;
-    const float u3 = sh.clamped[2] ? 0.f : (float)upc2 * wf;
-    const float fx = (float)s.fx, fy = (float)s.fy, fz = (float)s.fz;
-    const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
-      a[0][k] = fmaf(wk, u0, a[0][k]);
-      a[1][k] = fmaf(wk, u1, a[1][k]);
-      a[2][k] = fmaf(wk, u2, a[2][k]);
-      a[3][k] = fmaf(wk, u3, a[3][k]);
-    }
+    agg_add(A, (float)s.fx, (float)s.fy, (float)s.fz, sh.sigma_raw > 0.0 ? (float)ds : 0.f,
+            sh.clamped[0] ? 0.f : (float)upc0 * wf, sh.clamped[1] ? 0.f : (float)upc1 * wf,
+            sh.clamped[2] ? 0.f : (float)upc2 * wf);
     T = T_next;
     if (T < p.eps) break;
   }
-  if (cur != 0xffffffffu) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) flush_corner(sink, g, cur, a, bf, k);
-  }
+  if (A.base != kNoCell) agg_flush(A, sink, g, 0xffu);
 }
 
-template <int MINB, bool SKIP>
-__global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
+template <bool SKIP>
+__global__ void __launch_bounds__(kThreads, 4) k_map_backward(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
     const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
@@ -839,7 +802,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
   if (st.bad != INT_MAX) return;  // non-finite loss: the reference throws before updating
   const uint8_t fl = flags[i];
   if (!(fl & kHit)) return;
-  if (overflow_only && !(fl & kOverflow)) return;  // recorded rays: k_map_backward_rec
+  if (overflow_only && !(fl & kOverflow)) return;  // recorded rays: K2q / K2g
   const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
   const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
   MapUp u;
@@ -849,138 +812,50 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward(
   map_backward_fast<SKIP>(g, p, m, u, grad);
 }
 
-// Backward over the forward's SampleRec (fast path): no payload gathers.
-// Walking each ray's samples last to first turns the prefix form of
-// gradients.cpp:69-97 into a suffix form without cancellation,
-// -C + prefix_i = -sum_{j>i} c_j w_j:
-//   dL/dsigma_i = delta_i [sum_ch upc_ch (c_ch,i T_{i+1} - Sc_ch) + upd (t_i T_{i+1} - Sd)],
-// Sc / Sd the running suffix sums. Sample positions (t_i, delta_i, cell,
-// trilinear weights) are re-derived exactly from the stored segment index
-// (renderer.cpp:66-73: s0 = lo + k step). The reverse walk also staggers the
-// lanes of a warp along their rays, so neighbouring rays do not hit the same
-// vertices with atomics at the same time (forward order measured 10% slower, r01).
-// Measured alternative (r01): queueing departing corners per warp and draining
-// them with all lanes cut divergence but not time — the scatter is bound by L2
-// atomic throughput (~2 corner flushes per sample; 38% distinct within a warp's
-// 176-entry window), so fewer instructions do not help without merging.
-template <int MINB, bool BULK>
-__global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
-    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
-    const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
-    const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
-    const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
-    float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
-    const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
-  __shared__ __align__(16) float4 s_ring[BULK ? kThreads : 1][kBulkSlots][kVec4PerVertex];
-  __shared__ __align__(16) float4 s_stage[BULK ? 1 : kThreads][kVec4PerVertex];  // per-warp merge
-  float4 (*stage)[kVec4PerVertex] = &s_stage[BULK ? 0 : (threadIdx.x & ~31)];
-  using Sink = typename std::conditional<BULK, BulkSink, RedSink>::type;
-  Sink sink;
-  if constexpr (BULK)
-    sink = BulkSink{grad, &s_ring[threadIdx.x][0][0], 0};
-  else
-    sink = RedSink{grad};
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const int i = order ? (int)order[t] : t;
-  const MapStats st = *stats;
-  if (st.bad != INT_MAX) return;  // non-finite loss: the reference throws before updating
-  const uint8_t fl = flags[i];
-  if (!(fl & kHit) || (fl & kOverflow)) return;
-  const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
-  const double4 tg = rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
-  MapUp u;
-  if (!map_upstream(st, global_counts, ray_cd[i], tg, fl, lambda_d, u)) return;
-  March m;
-  ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
-  float bf[9];
-  {
-    double basis[9];
-    if (!sh_basis(m.d, basis)) return;
-#pragma unroll
-    for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
-  }
-  if (!march_begin(g, p, m)) return;
-  const double upc0 = u.upc[0], upc1 = u.upc[1], upc2 = u.upc[2];
-  const bool use_depth = u.use_depth;
-  const double upd = use_depth ? u.upd : 0.0;
-  double Sc0 = 0.0, Sc1 = 0.0, Sc2 = 0.0, Sd = 0.0;
-  float a[4][8];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[c][k] = 0.f;
-  uint32_t cur = 0xffffffffu;
-  int pcx = 0, pcy = 0, pcz = 0;
-  int last_tb = -1;
-  // records are prefetched one iteration ahead: the dependent load of the next
-  // (uncoalesced, mostly L2/DRAM) record overlaps this sample's math and scatter
-  int c = rec_count[t] - 1;
-  float2 n0 = make_float2(0.f, 0.f), n1 = n0, n2 = n0;
-  if (c >= 0) {
-    const float2* q = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
-    n0 = __ldg(q);
-    n1 = __ldg(q + 1);
-    n2 = __ldg(q + 2);
-  }
-  for (; c >= 0; --c) {
-    const float2 q0 = n0, q1 = n1, q2 = n2;
-    if (c > 0) {
-      const float2* q = reinterpret_cast<const float2*>(rec + rec_index(t, c - 1, K));
-      n0 = __ldg(q);
-      n1 = __ldg(q + 1);
-      n2 = __ldg(q + 2);
-    }
-    const uint32_t kf = __float_as_uint(q2.y);
-    const double kseg = (double)(kf >> 4);
-    const double s0 = dadd(m.lo, dmul(kseg, m.step));
-    const double s0s = dadd(s0, m.step);
-    const double s1 = (m.hi < s0s) ? m.hi : s0s;
-    const double delta = dsub(s1, s0);
-    const double tm = dmul(0.5, dadd(s0, s1));
-    const double pp[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
-                          dadd(m.o[2], dmul(tm, m.d[2]))};
-    Sample s;
-    locate(g, pp, s);
-    const double w = (double)q0.x, Tn = (double)q0.y;
-    const double c0 = (double)q1.x, c1 = (double)q1.y, c2 = (double)q2.x;
-    double ds = upc0 * (c0 * Tn - Sc0) + upc1 * (c1 * Tn - Sc1) + upc2 * (c2 * Tn - Sc2);
-    if (use_depth) ds += upd * (tm * Tn - Sd);
-    ds *= delta;
-    Sc0 += c0 * w;
-    Sc1 += c1 * w;
-    Sc2 += c2 * w;
-    Sd += tm * w;
-    if (s.base != cur) {
-      if (cur != 0xffffffffu)
-        move_cell(sink, g, cur, s.cx - pcx, s.cy - pcy, s.cz - pcz, a, bf);
-      cur = s.base;
-      pcx = s.cx;
-      pcy = s.cy;
-      pcz = s.cz;
-      mark_touched(g, s.cx, s.cy, s.cz, last_tb);
-    }
-    const float wf = q0.x;
-    const float u0 = (kf & kRecSigmaPos) ? (float)ds : 0.f;
-    const float u1 = (kf & 1u) ? 0.f : (float)upc0 * wf;
-    const float u2 = (kf & 2u) ? 0.f : (float)upc1 * wf;
-    const float u3 = (kf & 4u) ? 0.f : (float)upc2 * wf;
-    const float fx = (float)s.fx, fy = (float)s.fy, fz = (float)s.fz;
-    const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
-      a[0][k] = fmaf(wk, u0, a[0][k]);
-      a[1][k] = fmaf(wk, u1, a[1][k]);
-      a[2][k] = fmaf(wk, u2, a[2][k]);
-      a[3][k] = fmaf(wk, u3, a[3][k]);
-    }
-  }
-  if (cur != 0xffffffffu) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) flush_corner(sink, g, cur, a, bf, k);
-  }
-  sink.finish();
+// One record of the reverse walk, decoded: the sample's position is re-derived
+// exactly from the stored segment index (renderer.cpp:66-73: s0 = lo + k step,
+// midpoint, locate — FP64, the forward's arithmetic), so the cell and trilinear
+// weights are the forward's.
+struct RecSample {
+  Sample s;
+  double tm, delta, w, Tn, c0, c1, c2;
+  uint32_t kf;
+};
+__device__ __forceinline__ void decode_record(const DevGrid& g, const March& m, float2 q0,
+                                              float2 q1, float2 q2, RecSample& r) {
+  r.kf = __float_as_uint(q2.y);
+  const double kseg = (double)(r.kf >> 4);
+  const double s0 = dadd(m.lo, dmul(kseg, m.step));
+  const double s0s = dadd(s0, m.step);
+  const double s1 = (m.hi < s0s) ? m.hi : s0s;
+  r.delta = dsub(s1, s0);
+  r.tm = dmul(0.5, dadd(s0, s1));
+  const double pp[3] = {dadd(m.o[0], dmul(r.tm, m.d[0])), dadd(m.o[1], dmul(r.tm, m.d[1])),
+                        dadd(m.o[2], dmul(r.tm, m.d[2]))};
+  locate(g, pp, r.s);
+  r.w = (double)q0.x;
+  r.Tn = (double)q0.y;
+  r.c0 = (double)q1.x;
+  r.c1 = (double)q1.y;
+  r.c2 = (double)q2.x;
+}
+
+// Suffix-form sample upstream of the reverse walk (see K2q) and the aggregate
+// update; Sc / Sd advance past the sample.
+__device__ __forceinline__ void walk_sample(CornerAgg& A, const RecSample& r, double upc0,
+                                            double upc1, double upc2, bool use_depth, double upd,
+                                            double& Sc0, double& Sc1, double& Sc2, double& Sd) {
+  double ds = upc0 * (r.c0 * r.Tn - Sc0) + upc1 * (r.c1 * r.Tn - Sc1) + upc2 * (r.c2 * r.Tn - Sc2);
+  if (use_depth) ds += upd * (r.tm * r.Tn - Sd);
+  ds *= r.delta;
+  Sc0 += r.c0 * r.w;
+  Sc1 += r.c1 * r.w;
+  Sc2 += r.c2 * r.w;
+  Sd += r.tm * r.w;
+  const float wf = (float)r.w;
+  agg_add(A, (float)r.s.fx, (float)r.s.fy, (float)r.s.fz,
+          (r.kf & kRecSigmaPos) ? (float)ds : 0.f, (r.kf & 1u) ? 0.f : (float)upc0 * wf,
+          (r.kf & 2u) ? 0.f : (float)upc1 * wf, (r.kf & 4u) ? 0.f : (float)upc2 * wf);
 }
 
 // K2g: the record walk for small batches, 8 lanes per ray. Below ~40K rays the
@@ -989,8 +864,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_rec(
 // contiguous chunks. Pass 1: every lane sums its chunk's c_ch w and t w. A
 // shuffle suffix-scan gives each lane the sums of the records after its chunk
 // (the starting Sc / Sd of the reverse walk). Pass 2: every lane walks its chunk
-// backwards exactly as K2 does (suffix-form dL/dsigma, per-lane corner
-// aggregation, face-shift carries, red.v4 flushes; chunk ends flush their
+// backwards exactly as K2q does (suffix-form dL/dsigma, per-lane corner
+// aggregation, relabelled carries, red.v4 flushes; chunk ends flush their
 // cell). Same gradient up to fp32 summation order.
 __global__ void __launch_bounds__(kThreads) k_map_backward_g(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
@@ -1055,81 +930,40 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
       Sd += ad;
     }
   }
-  const double upc0 = u.upc[0], upc1 = u.upc[1], upc2 = u.upc[2];
-  const bool use_depth = u.use_depth;
-  const double upd = use_depth ? u.upd : 0.0;
-  float a[4][8];
-#pragma unroll
-  for (int cc = 0; cc < 4; ++cc)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[cc][k] = 0.f;
-  uint32_t cur = 0xffffffffu;
-  int pcx = 0, pcy = 0, pcz = 0;
+  const double upd = u.use_depth ? u.upd : 0.0;
+  CornerAgg A;
+  agg_init(A);
   int last_tb = -1;
-  RedSink sink{grad};
+  RedSink sink{grad, bf};
   for (int c = c1 - 1; c >= c0; --c) {
     const float2* q = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
-    const float2 q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
-    const uint32_t kf = __float_as_uint(q2.y);
-    const double kseg = (double)(kf >> 4);
-    const double s0 = dadd(m.lo, dmul(kseg, m.step));
-    const double s0s = dadd(s0, m.step);
-    const double s1 = (m.hi < s0s) ? m.hi : s0s;
-    const double delta = dsub(s1, s0);
-    const double tm = dmul(0.5, dadd(s0, s1));
-    const double pp[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
-                          dadd(m.o[2], dmul(tm, m.d[2]))};
-    Sample s;
-    locate(g, pp, s);
-    const double w = (double)q0.x, Tn = (double)q0.y;
-    const double cr = (double)q1.x, cg = (double)q1.y, cb = (double)q2.x;
-    double ds = upc0 * (cr * Tn - Sc0) + upc1 * (cg * Tn - Sc1) + upc2 * (cb * Tn - Sc2);
-    if (use_depth) ds += upd * (tm * Tn - Sd);
-    ds *= delta;
-    Sc0 += cr * w;
-    Sc1 += cg * w;
-    Sc2 += cb * w;
-    Sd += tm * w;
-    if (s.base != cur) {
-      if (cur != 0xffffffffu) move_cell(sink, g, cur, s.cx - pcx, s.cy - pcy, s.cz - pcz, a, bf);
-      cur = s.base;
-      pcx = s.cx;
-      pcy = s.cy;
-      pcz = s.cz;
-      mark_touched(g, s.cx, s.cy, s.cz, last_tb);
-    }
-    const float wf = q0.x;
-    const float u0 = (kf & kRecSigmaPos) ? (float)ds : 0.f;
-    const float u1 = (kf & 1u) ? 0.f : (float)upc0 * wf;
-    const float u2 = (kf & 2u) ? 0.f : (float)upc1 * wf;
-    const float u3 = (kf & 4u) ? 0.f : (float)upc2 * wf;
-    const float fx = (float)s.fx, fy = (float)s.fy, fz = (float)s.fz;
-    const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
-      a[0][k] = fmaf(wk, u0, a[0][k]);
-      a[1][k] = fmaf(wk, u1, a[1][k]);
-      a[2][k] = fmaf(wk, u2, a[2][k]);
-      a[3][k] = fmaf(wk, u3, a[3][k]);
-    }
+    RecSample r;
+    decode_record(g, m, __ldg(q), __ldg(q + 1), __ldg(q + 2), r);
+    if (agg_enter(A, sink, g, r.s)) mark_touched(g, r.s.cx, r.s.cy, r.s.cz, last_tb);
+    walk_sample(A, r, u.upc[0], u.upc[1], u.upc[2], u.use_depth, upd, Sc0, Sc1, Sc2, Sd);
   }
-  if (cur != 0xffffffffu) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) flush_corner(sink, g, cur, a, bf, k);
-  }
+  if (A.base != kNoCell) agg_flush(A, sink, g, 0xffu);
 }
 
-// K2q: the same reverse walk with a DEFERRED, convergent scatter. The flush of a
-// departing corner is the divergent part of K2 (a lane moves cell every ~2
-// samples, at a different iteration from its neighbours: ncu r01 v19 shows ~70%
-// of K2's warp instructions in the flush code at 7.7 active lanes). Here a move
-// only appends (vertex, a_sigma, a_r, a_g, a_b) to the lane's ring in shared
-// memory (2 stores per corner); every iteration each lane then pops up to POPS
-// entries and scatters them (basis expansion + 7 red.v4). Pops run after the
-// warp reconverges, so they execute with every lane that has queued work. The
-// loop runs until every lane of the warp has finished its ray AND drained its
-// ring (warp-uniform exit; lanes without a ray just help drain).
+// K2q (default): the reverse record walk with a DEFERRED, convergent scatter.
+// Walking each ray's samples last to first turns the prefix form of
+// gradients.cpp:69-97 into a suffix form without cancellation,
+// -C + prefix_i = -sum_{j>i} c_j w_j:
+//   dL/dsigma_i = delta_i [sum_ch upc_ch (c_ch,i T_{i+1} - Sc_ch) + upd (t_i T_{i+1} - Sd)],
+// Sc / Sd the running suffix sums; no payload is gathered. The reverse walk also
+// staggers the lanes of a warp along their rays, so neighbouring rays do not hit
+// the same vertices with atomics at the same time (forward order measured 10%
+// slower, r01). A flushed corner is only appended (vertex, a_sigma, a_r, a_g,
+// a_b) to the lane's ring in shared memory; every iteration each lane then pops
+// up to POPS entries and scatters them after the warp reconverges. The loop runs
+// until every lane of the warp has finished its ray AND drained its ring
+// (warp-uniform exit; lanes without a ray help drain).
+#ifndef VRF_K2_MERGE
+#define VRF_K2_MERGE 1  // same-round duplicate merging: 0 off, 1 leader sums, 2 column-parallel
+#endif
+#ifndef VRF_K2_MINB
+#define VRF_K2_MINB 3
+#endif
 constexpr int kQ = 16;  // ring entries per thread (power of 2); a step enqueues <= 8
 constexpr int kQSmemBytes = kQ * kThreads * (16 + 4);
 constexpr int kQMergeSmemBytes = kQSmemBytes + kThreads * kVec4PerVertex * 16;
@@ -1138,8 +972,7 @@ struct QueueSink {
   float4* qa;    // [kQ][kThreads] (a_sigma, a_r, a_g, a_b)
   int tid;
   uint32_t tail;
-  __device__ __forceinline__ void operator()(uint32_t v, float s, float r, float gg, float b,
-                                             const float (&)[9]) {
+  __device__ __forceinline__ void operator()(uint32_t v, float s, float r, float gg, float b) {
     const int slot = (int)(tail & (kQ - 1)) * kThreads + tid;
     qv[slot] = v;
     qa[slot] = make_float4(s, r, gg, b);
@@ -1147,19 +980,13 @@ struct QueueSink {
   }
 };
 
-#ifdef VRF_QSTATS
-__device__ unsigned long long g_qstats[4];  // pops, merged-away pops, rounds, active lanes
-#endif
-// One pop round: the lane's oldest queued corner -> basis expansion + 7 red.v4
-// (VRF_K2_MERGE=0). The default pops through queue_pop_merge: the ~28 lanes
-// popping together often hold the same vertex (33% of pops duplicate another
-// lane's vertex in the same round, VRF_QSTATS counters), so merging them cuts
-// the L2 reductions by a third (L2 busy 69% -> 50%). At config 3 that only
-// moves the limit to issue (14.7 ms either way); at config 4, where the 15 GB
-// gradient misses L2, it saves DRAM read-modify-writes (29.3 -> 25.7 ms).
-// MERGE variant: lanes popping the same vertex in a round are grouped
-// (__match_any_sync); members stage their expanded 28-vector in the warp's
-// shared buffer, the leader sums the group and issues the only 7 red.v4.
+// One pop round: the lane's oldest queued corner. The ~28 lanes popping together
+// often hold the same vertex (33% of pops duplicate another lane's vertex in the
+// same round, r01 counters): lanes popping the same vertex are grouped
+// (__match_any_sync), members stage their expanded 28-vector in the warp's shared
+// buffer, and the leader sums the group and issues the only 7 red.v4. This cuts
+// the L2 reductions by a third; at config 4, where the 15 GB gradient misses L2,
+// it saves DRAM read-modify-writes (K2 29.3 -> 25.7 ms, r01).
 __device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& head,
                                                 float4* __restrict__ grad, const float (&bf)[9],
                                                 float4 (*stage)[kVec4PerVertex]) {
@@ -1180,7 +1007,38 @@ __device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& he
       x[10 + mm] = e.z * bf[mm];
       x[19 + mm] = e.w * bf[mm];
     }
+#if VRF_K2_MERGE == 2
+    // column-parallel: every member stages; member r of g sums columns r, r+g, ...
     if (grp != (1u << lane)) {
+#pragma unroll
+      for (int j = 0; j < kVec4PerVertex; ++j)
+        stage[lane][j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+      __syncwarp(grp);
+      const int g = __popc(grp), r = __popc(grp & ((1u << lane) - 1u));
+      float4* dst = grad + (size_t)v * kVec4PerVertex;
+      for (int j = r; j < kVec4PerVertex; j += g) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        unsigned rest = grp;
+        while (rest) {
+          const int o = __ffs(rest) - 1;
+          rest &= rest - 1;
+          const float4 y = stage[o][j];
+          acc.x += y.x;
+          acc.y += y.y;
+          acc.z += y.z;
+          acc.w += y.w;
+        }
+        atomicAdd(dst + j, acc);
+      }
+      __syncwarp(grp);
+      return;
+    }
+    if (true) {
+#elif VRF_K2_MERGE == 0
+    if (false) {
+#else
+    if (grp != (1u << lane)) {
+#endif
       if (lane != leader) {
 #pragma unroll
         for (int j = 0; j < kVec4PerVertex; ++j)
@@ -1204,7 +1062,7 @@ __device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& he
       }
       __syncwarp(grp);
     }
-    if (lane == leader) {
+    if (lane == leader || VRF_K2_MERGE == 0) {
       float4* dst = grad + (size_t)v * kVec4PerVertex;
 #pragma unroll
       for (int j = 0; j < kVec4PerVertex; ++j)
@@ -1213,44 +1071,7 @@ __device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& he
   }
 }
 
-__device__ __forceinline__ void queue_pop(const QueueSink& q, uint32_t& head,
-                                          float4* __restrict__ grad, const float (&bf)[9]) {
-  if (head != q.tail) {
-    const int slot = (int)(head & (kQ - 1)) * kThreads + q.tid;
-    const uint32_t v = q.qv[slot];
-    const float4 e = q.qa[slot];
-    ++head;
-#ifdef VRF_QSTATS
-    const unsigned act = __activemask();
-    const unsigned grp = __match_any_sync(act, v);
-    const int lane = threadIdx.x & 31;
-    if (lane == __ffs(act) - 1) {
-      atomicAdd(&g_qstats[2], 1ull);
-      atomicAdd(&g_qstats[3], (unsigned long long)__popc(act));
-    }
-    atomicAdd(&g_qstats[0], 1ull);
-    if (lane != __ffs(grp) - 1) atomicAdd(&g_qstats[1], 1ull);
-#endif
-    RedSink{grad}(v, e.x, e.y, e.z, e.w, bf);
-  }
-}
-
-// Pop through the bulk reduce: one cp.reduce.async.bulk (UBLKRED, 112 B) per
-// vertex instead of 7 red.v4. Convergent pops avoid what made BulkSink lose
-// inside the divergent K2.
-__device__ __forceinline__ void queue_pop_bulk(const QueueSink& q, uint32_t& head,
-                                               float4* __restrict__ grad, const float (&bf)[9],
-                                               BulkSink& bs) {
-  if (head != q.tail) {
-    const int slot = (int)(head & (kQ - 1)) * kThreads + q.tid;
-    const uint32_t v = q.qv[slot];
-    const float4 e = q.qa[slot];
-    ++head;
-    bs(v, e.x, e.y, e.z, e.w, bf);
-  }
-}
-
-template <int MINB, int POPS, bool BULK, bool MERGE = false>
+template <int MINB, int POPS>
 __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, const int* __restrict__ batch, int n,
@@ -1258,15 +1079,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
     float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
     const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
-  // dynamic shared memory (kQSmemBytes): the rings, [kQ][kThreads] float4 + u32
+  // dynamic shared memory (kQMergeSmemBytes): the rings, [kQ][kThreads] float4 +
+  // u32, then the per-warp merge staging [32][7] float4
   extern __shared__ __align__(16) float4 s_dyn[];
   float4* s_qa = s_dyn;
   uint32_t* s_qv = reinterpret_cast<uint32_t*>(s_dyn + kQ * kThreads);
-  // MERGE: per-warp staging [32][7] float4 after the rings
   float4 (*stage)[kVec4PerVertex] = reinterpret_cast<float4 (*)[kVec4PerVertex]>(
       s_dyn + kQ * kThreads + kQ * kThreads / 4) + (threadIdx.x & ~31);
-  __shared__ __align__(16) float4 s_ring[BULK ? kThreads : 1][kBulkSlots][kVec4PerVertex];
-  BulkSink bs{grad, &s_ring[BULK ? threadIdx.x : 0][0][0], 0};
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   // ---- per-ray setup; a lane with nothing to scatter keeps c = -1 but stays in
   // the loop (the loop's exit vote is warp-wide)
@@ -1299,17 +1118,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
   const bool use_depth = c >= 0 && u.use_depth;
   const double upd = use_depth ? u.upd : 0.0;
   double Sc0 = 0.0, Sc1 = 0.0, Sc2 = 0.0, Sd = 0.0;
-  float a[4][8];
-#pragma unroll
-  for (int cc = 0; cc < 4; ++cc)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[cc][k] = 0.f;
-  uint32_t cur = 0xffffffffu;
-  int pcx = 0, pcy = 0, pcz = 0;
+  CornerAgg A;
+  agg_init(A);
   int last_tb = -1;
   QueueSink q{s_qv, s_qa, (int)threadIdx.x, 0u};
   uint32_t head = 0;
   bool final_pending = c >= 0;  // the last cell's 8 corners, flushed after the walk
+  // records are prefetched one iteration ahead: the dependent load of the next
+  // record overlaps this sample's math and scatter
   float2 n0 = make_float2(0.f, 0.f), n1 = n0, n2 = n0;
   if (c >= 0) {
     const float2* qq = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
@@ -1327,75 +1143,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
         n2 = __ldg(qq + 2);
       }
       --c;
-      const uint32_t kf = __float_as_uint(q2.y);
-      const double kseg = (double)(kf >> 4);
-      const double s0 = dadd(m.lo, dmul(kseg, m.step));
-      const double s0s = dadd(s0, m.step);
-      const double s1 = (m.hi < s0s) ? m.hi : s0s;
-      const double delta = dsub(s1, s0);
-      const double tm = dmul(0.5, dadd(s0, s1));
-      const double pp[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
-                            dadd(m.o[2], dmul(tm, m.d[2]))};
-      Sample s;
-      locate(g, pp, s);
-      const double w = (double)q0.x, Tn = (double)q0.y;
-      const double c0 = (double)q1.x, c1 = (double)q1.y, c2 = (double)q2.x;
-      double ds = upc0 * (c0 * Tn - Sc0) + upc1 * (c1 * Tn - Sc1) + upc2 * (c2 * Tn - Sc2);
-      if (use_depth) ds += upd * (tm * Tn - Sd);
-      ds *= delta;
-      Sc0 += c0 * w;
-      Sc1 += c1 * w;
-      Sc2 += c2 * w;
-      Sd += tm * w;
-      if (s.base != cur) {
-        if (cur != 0xffffffffu)
-          move_cell(q, g, cur, s.cx - pcx, s.cy - pcy, s.cz - pcz, a, bf);
-        cur = s.base;
-        pcx = s.cx;
-        pcy = s.cy;
-        pcz = s.cz;
-        mark_touched(g, s.cx, s.cy, s.cz, last_tb);
-      }
-      const float wf = q0.x;
-      const float u0 = (kf & kRecSigmaPos) ? (float)ds : 0.f;
-      const float u1 = (kf & 1u) ? 0.f : (float)upc0 * wf;
-      const float u2 = (kf & 2u) ? 0.f : (float)upc1 * wf;
-      const float u3 = (kf & 4u) ? 0.f : (float)upc2 * wf;
-      const float fx = (float)s.fx, fy = (float)s.fy, fz = (float)s.fz;
-      const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
-        a[0][k] = fmaf(wk, u0, a[0][k]);
-        a[1][k] = fmaf(wk, u1, a[1][k]);
-        a[2][k] = fmaf(wk, u2, a[2][k]);
-        a[3][k] = fmaf(wk, u3, a[3][k]);
-      }
+      RecSample r;
+      decode_record(g, m, q0, q1, q2, r);
+      if (agg_enter(A, q, g, r.s)) mark_touched(g, r.s.cx, r.s.cy, r.s.cz, last_tb);
+      walk_sample(A, r, upc0, upc1, upc2, use_depth, upd, Sc0, Sc1, Sc2, Sd);
     } else if (final_pending && q.tail - head <= (uint32_t)(kQ - 8)) {
       final_pending = false;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) flush_corner(q, g, cur, a, bf, k);
+      agg_flush(A, q, g, 0xffu);
     }
     // convergent scatter: every lane with queued corners pops up to POPS, then
     // more until every ring has room for the next step's <= 8 entries
-    if constexpr (BULK) {
 #pragma unroll
-      for (int r = 0; r < POPS; ++r) queue_pop_bulk(q, head, grad, bf, bs);
-      while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
-        queue_pop_bulk(q, head, grad, bf, bs);
-    } else if constexpr (MERGE) {
-#pragma unroll
-      for (int r = 0; r < POPS; ++r) queue_pop_merge(q, head, grad, bf, stage);
-      while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
-        queue_pop_merge(q, head, grad, bf, stage);
-    } else {
-#pragma unroll
-      for (int r = 0; r < POPS; ++r) queue_pop(q, head, grad, bf);
-      while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
-        queue_pop(q, head, grad, bf);
-    }
+    for (int r = 0; r < POPS; ++r) queue_pop_merge(q, head, grad, bf, stage);
+    while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
+      queue_pop_merge(q, head, grad, bf, stage);
   }
-  if constexpr (BULK) bs.finish();
 }
 
 // ------------------------------------------------------------------ K3 deterministic records
@@ -1998,89 +1760,22 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
                              const int* global_counts, float4* grad, double lambda_d,
                              const uint32_t* order, const SampleRec* rec, int K,
                              const int* rec_count, cudaStream_t s) {
-  // CTAs per SM: the direct K2 needs 154 registers (3); the queued one fits 4
-  // (127 registers, 40 KB ring) — measured 15.0 vs 14.7 ms per 1M-ray backward (r01)
-  static const int minb_env = [] {
-    const char* e = std::getenv("VRF_REC_MINB");
-    return e ? std::atoi(e) : 0;
-  }();
-  // scatter: the queued convergent K2 (default), or the direct divergent K2 with
-  // per-float4 red (VRF_K2=direct) or the bulk reduce (VRF_SCATTER=bulk). r01,
-  // per 1M-ray backward: queued 14.7 ms, direct red 15.0 ms, direct bulk 21.5 ms,
-  // queued with bulk pops 16.2 ms (UBLKRED does not beat red.v4 on this address
-  // pattern even with every lane active; 1, 2 or 3 pops per step: same time).
-  static const bool bulk = [] {
-    const char* e = std::getenv("VRF_SCATTER");
-    return e && std::string(e) == "bulk";
-  }();
-  static const bool direct = [] {
-    const char* e = std::getenv("VRF_K2");
-    return bulk || (e && std::string(e) == "direct");
-  }();
-  const int blocks = (n + kThreads - 1) / kThreads;
-  const int minb = minb_env ? minb_env : (direct ? 3 : 4);
   if (n <= bwd_group_max()) {  // small batch: 8 lanes per ray (K2g)
     k_map_backward_g<<<(n + kThreads / 8 - 1) / (kThreads / 8), kThreads, 0, s>>>(
         g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
         order, rec, K, rec_count);
     return;
   }
-  if (!direct) {
-#define VRF_Q_LAUNCH(MB)                                                                        \
-  do {                                                                                          \
-    static const bool attr = [] {                                                               \
-      return cudaFuncSetAttribute(k_map_backward_q<MB, 2, false>,                               \
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
-                                  kQSmemBytes) == cudaSuccess;                                  \
-    }();                                                                                        \
-    (void)attr;                                                                                 \
-    k_map_backward_q<MB, 2, false><<<blocks, kThreads, kQSmemBytes, s>>>(                       \
-        g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d, \
-        order, rec, K, rec_count);                                                              \
-  } while (0)
-    // same-round duplicate merging (default; VRF_K2_MERGE=0 for the plain pops).
-    // r01 v23: config 3 K2 14.63 vs 14.68 ms, config 4 (sparse 513^3, 8M rays)
-    // 25.7 vs 29.3 ms: the merged reductions save DRAM read-modify-writes when
-    // the gradient does not fit in L2.
-    static const bool merge = [] {
-      const char* e = std::getenv("VRF_K2_MERGE");
-      return !(e && std::string(e) == "0");
-    }();
-    if (merge && minb_env == 0) {  // 3 CTAs/SM (168 registers)
-      static const bool attr = cudaFuncSetAttribute(k_map_backward_q<3, 2, false, true>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    kQMergeSmemBytes) == cudaSuccess;
-      (void)attr;
-      k_map_backward_q<3, 2, false, true><<<blocks, kThreads, kQMergeSmemBytes, s>>>(
-          g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
-          order, rec, K, rec_count);
-    } else if (minb == 3) {
-      VRF_Q_LAUNCH(3);
-    } else {
-      VRF_Q_LAUNCH(4);
-    }
-#undef VRF_Q_LAUNCH
-#ifdef VRF_QSTATS
-    unsigned long long qs[4];
-    cudaStreamSynchronize(s);
-    cudaMemcpyFromSymbol(qs, g_qstats, sizeof(qs));
-    std::fprintf(stderr, "qstats pops %llu dup %llu rounds %llu lanes/round %.2f\n", qs[0], qs[1],
-                 qs[2], qs[2] ? (double)qs[3] / qs[2] : 0.0);
-    std::memset(qs, 0, sizeof(qs));
-    cudaMemcpyToSymbol(g_qstats, qs, sizeof(qs));
-#endif
-    return;
-  }
-#define VRF_REC_LAUNCH(MB, BK)                                                                  \
-  k_map_backward_rec<MB, BK><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd, \
-                                                         flags, stats, global_counts, grad,       \
-                                                         lambda_d, order, rec, K, rec_count)
-  if (minb == 4) {
-    if (bulk) VRF_REC_LAUNCH(4, true); else VRF_REC_LAUNCH(4, false);
-  } else {
-    if (bulk) VRF_REC_LAUNCH(3, true); else VRF_REC_LAUNCH(3, false);
-  }
-#undef VRF_REC_LAUNCH
+  // K2q: 3 CTAs/SM, 2 pops per step. r01 (config 3 / config 4, ms): 1, 2 or 3
+  // pops 14.54 / 14.63 / 15.02 and 25.82 / 25.71 / 25.78.
+  constexpr int kMinB = VRF_K2_MINB, kPops = 2;
+  static const bool attr = cudaFuncSetAttribute(k_map_backward_q<kMinB, kPops>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                kQMergeSmemBytes) == cudaSuccess;
+  (void)attr;
+  k_map_backward_q<kMinB, kPops><<<(n + kThreads - 1) / kThreads, kThreads, kQMergeSmemBytes, s>>>(
+      g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
+      order, rec, K, rec_count);
 }
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s) {
   k_map_reduce<<<1, 1024, 0, s>>>(partials, nparts, out);
@@ -2090,30 +1785,17 @@ void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam
                          const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
                          const int* global_counts, float4* grad, double lambda_d,
                          bool overflow_only, const uint32_t* order, cudaStream_t s) {
-  // 4 CTAs x 128 threads per SM: 128 registers (measured best of 2/3/4, r01);
-  // VRF_BWD_MINB=3 selects the 168-register build for A/B runs.
-  // The empty-block jump is compiled in only when the grid has empty blocks.
-  static const int minb = [] {
-    const char* e = std::getenv("VRF_BWD_MINB");
-    return (e && std::atoi(e) == 3) ? 3 : 4;
-  }();
+  // 4 CTAs x 128 threads per SM (measured best of 2/3/4, r01). The empty-block
+  // jump is compiled in only when the grid has empty blocks.
   const int blocks = (n + kThreads - 1) / kThreads;
-#define VRF_BWD_LAUNCH(MB, SK)                                                                 \
-  k_map_backward<MB, SK><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd, \
-                                                     flags, stats, global_counts, grad,        \
-                                                     lambda_d, order, overflow_only)
-  if (minb == 3) {
-    if (g.all_blocks_active)
-      VRF_BWD_LAUNCH(3, false);
-    else
-      VRF_BWD_LAUNCH(3, true);
-  } else {
-    if (g.all_blocks_active)
-      VRF_BWD_LAUNCH(4, false);
-    else
-      VRF_BWD_LAUNCH(4, true);
-  }
-#undef VRF_BWD_LAUNCH
+  if (g.all_blocks_active)
+    k_map_backward<false><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
+                                                      flags, stats, global_counts, grad,
+                                                      lambda_d, order, overflow_only);
+  else
+    k_map_backward<true><<<blocks, kThreads, 0, s>>>(g, p, cam, rgbd, poses, batch, n, ray_cd,
+                                                     flags, stats, global_counts, grad, lambda_d,
+                                                     order, overflow_only);
 }
 void launch_map_backward_records(const DevGrid& g, const DevParams& p, const DevCam& cam,
                                  const double4* rgbd, const DevPose* poses, const int* batch,

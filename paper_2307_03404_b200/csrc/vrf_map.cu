@@ -151,13 +151,7 @@ int grad_deterministic(vrf_context* ctx, const vrf_mapping_config* cfg, const in
 void launch_backward_fast(vrf_context* ctx, const vrf_mapping_config* cfg, const DevParams& p,
                           const int* batch_dev, int n, const int* global_counts) {
   cudaEvent_t pb = prof_begin(ctx);
-  if (ctx->map_kernel == 1)
-    launch_map_backward_w(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
-                          batch_dev, (const uint32_t*)ctx->s_order.ptr, n,
-                          (const double4*)ctx->s_raycd.ptr, (const uint8_t*)ctx->s_flags.ptr,
-                          ctx->d_stats, global_counts, ctx->grad, cfg->lambda_d,
-                          ctx->d_queue + 1, ctx->stream);
-  else {
+  {
     if (ctx->rec_K > 0) {
       launch_map_backward_rec(dev_grid(ctx), p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses,
                               batch_dev, n, (const double4*)ctx->s_raycd.ptr,
@@ -211,8 +205,8 @@ int map_gradient(vrf_context* ctx, const vrf_mapping_config* cfg, const int* bat
   DevParams p;
   if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
   if (n > 0) launch_backward_fast(ctx, cfg, p, batch_dev, n, nullptr);
-  // the thread-per-ray scatter kernels mark the touched blocks; the warp variant does not
-  ctx->touched_valid = ctx->map_kernel == 0;
+  // the scatter kernels mark every touched 8^3-vertex block (K4 runs block-sparse)
+  ctx->touched_valid = true;
   CU(cudaGetLastError());
   if (need_host_stats && (rc = read_stats(ctx, st_out))) return rc;
   return VRF_OK;

@@ -1,0 +1,63 @@
+// Coherent ray order for the per-ray kernels: rays sorted by (keyframe, Morton
+// order of 4x4-pixel tiles), so the 32 rays of a warp march nearly the same
+// cells and the grid / gradient lines of the rays in flight stay in L2 (r01:
+// 1.18e9 -> 3.41e9 mapping samples/s over draw order).
+#include <cub/cub.cuh>
+
+#include "vrf_internal.h"
+
+namespace vrf {
+
+namespace {
+
+// ------------------------------------------------------------------ ray ordering
+__device__ __forceinline__ uint32_t spread_bits(uint32_t x) {  // 10 bits -> 20 (every other)
+  x &= 0x3ff;
+  x = (x | (x << 8)) & 0x00ff00ff;
+  x = (x | (x << 4)) & 0x0f0f0f0f;
+  x = (x | (x << 2)) & 0x33333333;
+  x = (x | (x << 1)) & 0x55555555;
+  return x;
+}
+
+__global__ void k_ray_keys(const int* __restrict__ batch, int n, uint32_t* keys, uint32_t* ids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t f = (uint32_t)batch[3 * i], x = (uint32_t)batch[3 * i + 1] >> 2,
+                 y = (uint32_t)batch[3 * i + 2] >> 2;
+  // keyframe in the high bits, Morton order of 4x4-pixel tiles below
+  keys[i] = (f << 20) | spread_bits(x) | (spread_bits(y) << 1);
+  ids[i] = (uint32_t)i;
+}
+
+// Tracking pixels (px, py): Morton order of 4x4-pixel tiles.
+__global__ void k_pixel_keys(const int* __restrict__ px, int n, uint32_t* keys, uint32_t* ids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t x = (uint32_t)px[2 * i] >> 2, y = (uint32_t)px[2 * i + 1] >> 2;
+  keys[i] = spread_bits(x) | (spread_bits(y) << 1);
+  ids[i] = (uint32_t)i;
+}
+
+}  // namespace
+
+void launch_pixel_order(const int* pixels, int n, uint32_t* keys, uint32_t* ids, uint32_t* keys2,
+                        uint32_t* order, void* tmp, size_t tmp_bytes, cudaStream_t s) {
+  k_pixel_keys<<<(n + 255) / 256, 256, 0, s>>>(pixels, n, keys, ids);
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, ids, order, n, 0, 32, s);
+}
+
+void launch_ray_order(const int* batch, int n, uint32_t* keys, uint32_t* ids, uint32_t* keys2,
+                      uint32_t* order, void* tmp, size_t tmp_bytes, cudaStream_t s) {
+  k_ray_keys<<<(n + 255) / 256, 256, 0, s>>>(batch, n, keys, ids);
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, ids, order, n, 0, 32, s);
+}
+
+size_t ray_order_tmp_bytes(int n) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, n, 0, 32);
+  return b;
+}
+
+}  // namespace vrf

@@ -67,7 +67,8 @@ struct PoseResult {
 };
 
 int pose_pass(vrf_context* ctx, int frame, const vrf_intrinsics* intr, const vrf_pose* pose,
-              const int32_t* pixels, int n, const vrf_tracking_loss* cfg, PoseResult* res) {
+              const int32_t* pixels, int n, const vrf_tracking_loss* cfg, PoseResult* res,
+              PoseKernel which = PoseKernel::kParityFp64) {
   int rc = need_grid(ctx);
   if (rc) return rc;
   if (frame < 0 || frame >= ctx->n_frames)
@@ -111,9 +112,9 @@ int pose_pass(vrf_context* ctx, int frame, const vrf_intrinsics* intr, const vrf
   launch_pixel_order((const int*)ctx->s_batch.ptr, n, (uint32_t*)ctx->s_okeys.ptr,
                      (uint32_t*)ctx->s_oids.ptr, (uint32_t*)ctx->s_okeys2.ptr,
                      (uint32_t*)ctx->s_order.ptr, ctx->s_otmp.ptr, tmp, ctx->stream);
-  // K5: forward + Jacobian in one pass per ray, FP64 SH (the reference-parity path)
+  // K5: forward + Jacobian in one pass per ray (FP64 SH on the reference-parity path)
   cudaEvent_t pb = prof_begin(ctx);
-  launch_pose_fused(/*fp64_sh=*/true, g, p, cam, ctx->rgbd, ctx->d_frame, npix, ctx->d_pose,
+  launch_pose_fused(which, g, p, cam, ctx->rgbd, ctx->d_frame, npix, ctx->d_pose,
                     (const int*)ctx->s_batch.ptr, order, n, cfg->lambda_p, cfg->lambda_d,
                     (PosePartial*)ctx->s_partials.ptr, ctx->d_err, ctx->stream);
   prof_end(ctx, kProfPoseBackward, pb);
@@ -200,39 +201,6 @@ void apply_perturbation(const double om[3], const double ta[3], vrf_pose* pose) 
   for (int a = 0; a < 3; ++a) pose->t[a] = pose->t[a] + ta[a];
 }
 
-// (A + lambda diag(A) + 1e-12 I) x = -b, Cholesky on the 6x6 upper-packed A.
-bool solve_lm(const double jtj[21], const double jtr[6], double damping, double x[6]) {
-  double A[6][6];
-  int idx = 0;
-  for (int a = 0; a < 6; ++a)
-    for (int b = a; b < 6; ++b) A[a][b] = A[b][a] = jtj[idx++];
-  for (int a = 0; a < 6; ++a) A[a][a] += damping * A[a][a] + 1e-12;
-  double L[6][6] = {};
-  for (int i = 0; i < 6; ++i)
-    for (int j = 0; j <= i; ++j) {
-      double s = A[i][j];
-      for (int k = 0; k < j; ++k) s -= L[i][k] * L[j][k];
-      if (i == j) {
-        if (!(s > 0.0)) return false;
-        L[i][i] = std::sqrt(s);
-      } else {
-        L[i][j] = s / L[j][j];
-      }
-    }
-  double y[6];
-  for (int i = 0; i < 6; ++i) {
-    double s = -jtr[i];
-    for (int k = 0; k < i; ++k) s -= L[i][k] * y[k];
-    y[i] = s / L[i][i];
-  }
-  for (int i = 5; i >= 0; --i) {
-    double s = y[i];
-    for (int k = i + 1; k < 6; ++k) s -= L[k][i] * x[k];
-    x[i] = s / L[i][i];
-  }
-  return true;
-}
-
 }  // namespace
 
 extern "C" {
@@ -298,9 +266,24 @@ int vrf_pose_gradient(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
 int vrf_pose_normal_equations(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
                               const vrf_pose* pose, const int32_t* pixels, int n,
                               const vrf_tracking_loss* cfg, vrf_normal_equations* out) {
+  return vrf_pose_normal_equations_ex(ctx, frame, intr, pose, pixels, n, cfg,
+                                      VRF_POSE_KERNEL_PARITY, out);
+}
+
+int vrf_pose_normal_equations_ex(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
+                                 const vrf_pose* pose, const int32_t* pixels, int n,
+                                 const vrf_tracking_loss* cfg, int kernel,
+                                 vrf_normal_equations* out) {
   cudaSetDevice(ctx->device);
+  PoseKernel which;
+  switch (kernel) {
+    case VRF_POSE_KERNEL_PARITY: which = PoseKernel::kParityFp64; break;
+    case VRF_POSE_KERNEL_GN: which = PoseKernel::kGnUniform; break;
+    case VRF_POSE_KERNEL_GN_CHECK: which = PoseKernel::kGroupFp32; break;
+    default: return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "pose_normal_equations: unknown kernel");
+  }
   PoseResult r;
-  int rc = pose_pass(ctx, frame, intr, pose, pixels, n, cfg, &r);
+  int rc = pose_pass(ctx, frame, intr, pose, pixels, n, cfg, &r, which);
   if (rc) return rc;
   std::memcpy(out->jtj, r.jtj, sizeof(r.jtj));
   std::memcpy(out->jtr, r.jtr, sizeof(r.jtr));
@@ -430,10 +413,18 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
   if ((rc = check_frames(ctx, intr))) return rc;
   DevParams p;
   if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
-  // stratified draws over a 2^L x 2^L tile grid: n = 4^L rays per iteration
+  // n = rays_per_iteration stratified draws over a 2^L x 2^L tile grid, 4^L <= n
+  const int n = cfg->rays_per_iteration;
+  if (n <= 0)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "track_frame_gn: rays_per_iteration must be > 0");
   int L = 0;
-  while ((4LL << (2 * L)) <= (long long)std::max(cfg->rays_per_iteration, 1)) ++L;
-  const int n = 1 << (2 * L);
+  while ((4LL << (2 * L)) <= (long long)n) ++L;
+  PoseKernel which;
+  switch (cfg->kernel) {
+    case VRF_POSE_KERNEL_GN: which = PoseKernel::kGnUniform; break;
+    case VRF_POSE_KERNEL_GN_CHECK: which = PoseKernel::kGroupFp32; break;
+    default: return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "track_frame_gn: unknown kernel");
+  }
   const int iters = cfg->iterations;
   const int nb = pose_fused_blocks(n);
   if ((rc = ensure(ctx, ctx->s_batch, sizeof(int32_t) * 2 * (size_t)n))) return rc;
@@ -461,6 +452,7 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
   put(&p, sizeof(p));
   put(&cam, sizeof(cam));
   put(&n, sizeof(n));
+  put(&which, sizeof(which));
   put(&iters, sizeof(iters));
   put(&cfg->lambda_p, sizeof(double));
   put(&cfg->lambda_d, sizeof(double));
@@ -483,7 +475,7 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
     for (int it = 0; it < iters; ++it) {
       launch_draw_strat(ctx->rgbd, ctx->d_frame, npix, intr->width, intr->height, L,
                         cfg->max_redraws, ctx->d_gn_seed, it, (int*)ctx->s_batch.ptr, n, cs);
-      launch_pose_fused(/*fp64_sh=*/false, g, p, cam, ctx->rgbd, ctx->d_frame, npix,
+      launch_pose_fused(which, g, p, cam, ctx->rgbd, ctx->d_frame, npix,
                         ctx->d_gn_pose, (const int*)ctx->s_batch.ptr, nullptr, n, cfg->lambda_p,
                         cfg->lambda_d, (PosePartial*)ctx->s_partials.ptr, ctx->d_err, cs);
       launch_pose_reduce2((const PosePartial*)ctx->s_partials.ptr, nb, ctx->d_pose_out, cs);
@@ -519,6 +511,7 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
                      ctx->stream));
   if ((rc = check_err_flag(ctx))) return rc;  // syncs the stream
   prof_collect(ctx);
+  ctx->gn_last_hist.assign(hist, hist + 3 * iters);
   if (hist[1] == 0.0)
     return set_err(ctx, VRF_ERR_RUNTIME, "untrackable frame: all sampled rays miss the grid");
   for (int a = 0; a < 4; ++a) res.pose.q[a] = fin.q[a];
@@ -529,6 +522,12 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
     for (int it = 0; it < iters; ++it) ctx->prof_track_samples += (long long)hist[3 * it + 2];
   *out = res;
   return VRF_OK;
+}
+
+int vrf_track_frame_gn_history(vrf_context* ctx, double* hist, int cap) {
+  const int n = (int)ctx->gn_last_hist.size();
+  if (hist && cap > 0) std::memcpy(hist, ctx->gn_last_hist.data(), sizeof(double) * std::min(n, cap));
+  return n / 3;
 }
 
 }  // extern "C"

@@ -1,14 +1,17 @@
 // Tracking kernels.
 //
-//   k_pose_group   (default) one march per ray, 8 lanes per ray (one trilinear
-//                  corner each): composites Ĉ, D̂ and builds the ray's 4x6
-//                  Jacobian of [C; D] w.r.t. the pose chart [omega; tau]
-//                  (gradients.cpp:116-143 with unit upstreams, chart as
-//                  tracking.cpp:125-128) -> per-CTA partial J^T J (21) + J^T r (6)
-//                  + loss + hit count. The reference's 1/m normalisation
-//                  (tracking.cpp:118-120) is a host-side scale, so no global
-//                  sync is needed inside the pass.
-//   k_pose_fused   the same pass, one thread per ray (A/B).
+//   k_pose_group   one march per ray, 8 lanes per ray (one trilinear corner
+//                  each): composites Ĉ, D̂ and builds the ray's 4x6 Jacobian of
+//                  [C; D] w.r.t. the pose chart [omega; tau] (gradients.cpp:116-143
+//                  with unit upstreams, chart as tracking.cpp:125-128) -> per-CTA
+//                  partial J^T J (21) + J^T r (6) + loss + hit count. The
+//                  reference's 1/m normalisation (tracking.cpp:118-120) is a
+//                  host-side scale, so no global sync is needed inside the pass.
+//                  <double>: FP64 SH and Jacobian partials — the reference-parity
+//                  path (pose_gradient, track_frame). <float>: the checker of the
+//                  GN kernel below (same arithmetic, group-independent control).
+//   k_pose_group_u the Gauss-Newton path's pose kernel: the same per-ray
+//                  arithmetic as k_pose_group<float>, warp-synchronous control.
 //   k_draw_strat   device pixel draws for the Gauss-Newton tracker: stratified
 //                  over a tile grid in Morton order (coherent warps by
 //                  construction), redraws inside the tile on invalid depth
@@ -32,222 +35,6 @@ namespace {
 
 constexpr int kT = 128;
 
-template <typename ShT>
-__global__ void __launch_bounds__(kT) k_pose_fused(
-    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd_base,
-    const int* __restrict__ frame_idx, long long npix, const DevPose* __restrict__ pose_ptr,
-    const int* __restrict__ pixels, const uint32_t* __restrict__ order, int n, double lambda_p,
-    double lambda_d, PosePartial* __restrict__ partials, int* err) {
-  __shared__ double s_d[kT / 32][32];
-  __shared__ long long s_l[kT / 32];
-  __shared__ int s_i[kT / 32];
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = (order && t < n) ? (int)order[t] : t;
-  const double4* rgbd = rgbd_base + npix * (long long)(*frame_idx);
-  double jtj[21], jtr[6], loss = 0.0;
-#pragma unroll
-  for (int k = 0; k < 21; ++k) jtj[k] = 0.0;
-#pragma unroll
-  for (int k = 0; k < 6; ++k) jtr[k] = 0.0;
-  int hit = 0;
-  long long samples = 0;
-  const int px = t < n ? pixels[2 * i] : -1, py = t < n ? pixels[2 * i + 1] : -1;
-  if (t < n && px >= 0) {
-    if (px >= cam.width || py < 0 || py >= cam.height) {
-      atomicOr(err, 2);
-    } else {
-      const DevPose pose = *pose_ptr;
-      March m;
-      ray_from_pixel(cam, pose, (double)px, (double)py, m);
-      double basis[9];
-      // One march: compositing and the Jacobian together. dC/dsigma_i =
-      // delta_i (c_i T_{i+1} - C + prefix_i) (gradients.cpp:69-97) is linear in
-      // the not-yet-known totals C, D, so the per-axis sums split into
-      //   J = sum_i [delta_i (c_i T_{i+1} + prefix_i) g_i + w_i Gc_i] - C sum_i delta_i g_i
-      // (g_i = gated spatial gradient of sigma) and C is applied after the ray.
-      double Jo[4][3], Jd[4][3], Bo[3] = {0, 0, 0}, Bd[3] = {0, 0, 0};
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = 0.0;
-      double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
-      int count = 0;
-      if (!sh_basis(m.d, basis)) {
-        atomicOr(err, 1);
-      } else if (march_begin(g, p, m)) {
-        const double sgn[2] = {-1.0, 1.0};
-        ShT bs[9];
-#pragma unroll
-        for (int mm = 0; mm < 9; ++mm) bs[mm] = ShT(basis[mm]);
-        Sample s;
-        while (march_next(g, m, s)) {
-          // trilerp + SH colour (renderer.cpp:98-112) and the spatial gradients
-          // of sigma and the basis-contracted SH channels (voxel_grid.cpp:130-151)
-          // from the same 8 corner loads
-          const double wx[2] = {dsub(1.0, s.fx), s.fx}, wy[2] = {dsub(1.0, s.fy), s.fy},
-                       wz[2] = {dsub(1.0, s.fz), s.fz};
-          double sraw = 0.0;
-          ShT csh[3] = {ShT(0), ShT(0), ShT(0)};
-          double Gs[3] = {0, 0, 0}, Gc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-#pragma unroll 1
-          for (int k = 0; k < 8; ++k) {
-            const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
-            const double wk = dmul(dmul(wx[dx], wy[dy]), wz[dz]);
-            const double dw[3] = {sgn[dx] * wy[dy] * wz[dz] * g.inv_voxel,
-                                  wx[dx] * sgn[dy] * wz[dz] * g.inv_voxel,
-                                  wx[dx] * wy[dy] * sgn[dz] * g.inv_voxel};
-            const float4* vp4 = g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
-            float v[28];
-#pragma unroll
-            for (int j = 0; j < kVec4PerVertex; ++j) {
-              const float4 a = __ldg(vp4 + j);
-              v[4 * j] = a.x;
-              v[4 * j + 1] = a.y;
-              v[4 * j + 2] = a.z;
-              v[4 * j + 3] = a.w;
-            }
-            sraw = dadd(sraw, dmul(wk, (double)v[0]));
-            double shd[3];
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-              ShT acc = ShT(0);
-#pragma unroll
-              for (int mm = 0; mm < 9; ++mm) acc = fma(bs[mm], (ShT)v[1 + ch * 9 + mm], acc);
-              shd[ch] = (double)acc;
-              csh[ch] = fma(ShT(wk), acc, csh[ch]);
-            }
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              Gs[a] = fma(dw[a], (double)v[0], Gs[a]);
-#pragma unroll
-              for (int ch = 0; ch < 3; ++ch) Gc[ch][a] = fma(dw[a], shd[ch], Gc[ch][a]);
-            }
-          }
-          double c[3];
-          bool clamped[3];
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            const double v = 0.5 + (double)csh[ch];
-            clamped[ch] = (v <= 0.0 || v >= 1.0);
-            c[ch] = (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);
-          }
-          const double sigma = (sraw < 0.0) ? 0.0 : sraw;
-          const double decay = exp(dmul(-sigma, s.delta));
-          const double wgt = dmul(T, dsub(1.0, decay));
-          const double T_next = dmul(T, decay);
-          ++count;
-          double dsig[4];
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            prefix[ch] = dadd(prefix[ch], dmul(c[ch], wgt));
-            dsig[ch] = s.delta * (c[ch] * T_next + prefix[ch]);
-          }
-          prefix_d = dadd(prefix_d, dmul(s.t, wgt));
-          dsig[3] = s.delta * (s.t * T_next + prefix_d);
-          const bool sgate = sraw > 0.0;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const double gs = sgate ? s.delta * Gs[a] : 0.0;
-            Bo[a] += gs;
-            Bd[a] = fma(s.t, gs, Bd[a]);
-          }
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              double gv = sgate ? dsig[r] * Gs[a] : 0.0;
-              if (r < 3 && !clamped[r]) gv += wgt * Gc[r][a];
-              Jo[r][a] += gv;
-              Jd[r][a] = fma(s.t, gv, Jd[r][a]);
-            }
-          }
-          T = T_next;
-          if (T < p.eps) break;
-        }
-      }
-      if (count > 0) {
-        hit = 1;
-        samples = count;
-        const double4 tg = rgbd[(long long)py * cam.width + px];
-        // Ĉ = prefix, D̂ = prefix_d (renderer.cpp:120-126, same accumulation order)
-        const double C[4] = {prefix[0], prefix[1], prefix[2], prefix_d};
-        const double res[4] = {dsub(C[0], tg.x), dsub(C[1], tg.y), dsub(C[2], tg.z),
-                               dsub(C[3], tg.w)};
-        // tracking.cpp:117: lambda_p |cres|^2 + lambda_d dres^2
-        loss = dadd(dmul(lambda_p, dadd(dadd(dmul(res[0], res[0]), dmul(res[1], res[1])),
-                                        dmul(res[2], res[2]))),
-                    dmul(dmul(lambda_d, res[3]), res[3]));
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            Jo[r][a] -= C[r] * Bo[a];
-            Jd[r][a] -= C[r] * Bd[a];
-          }
-        // chart (tracking.cpp:125-128): tau <- dL/do, omega <- d x (dL/dd - d (d.dL/dd))
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const double dd = dot3(m.d, Jd[r]);
-          double gp[3], om[3];
-          for (int a = 0; a < 3; ++a) gp[a] = Jd[r][a] - m.d[a] * dd;
-          cross3(m.d, gp, om);
-          const double J[6] = {om[0], om[1], om[2], Jo[r][0], Jo[r][1], Jo[r][2]};
-          const double lam = r < 3 ? lambda_p : lambda_d;
-          int idx = 0;
-#pragma unroll
-          for (int a = 0; a < 6; ++a) {
-#pragma unroll
-            for (int b = a; b < 6; ++b) jtj[idx++] += lam * J[a] * J[b];
-            jtr[a] += lam * J[a] * res[r];
-          }
-        }
-      }
-    }
-  }
-  // CTA reduction in a fixed order (warp butterflies, then warps in order)
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double vals[28];
-#pragma unroll
-  for (int k = 0; k < 21; ++k) vals[k] = jtj[k];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) vals[21 + k] = jtr[k];
-  vals[27] = loss;
-#pragma unroll
-  for (int k = 0; k < 28; ++k) {
-    double v = warp_sum(vals[k]);
-    if (lane == 0) s_d[wid][k] = v;
-  }
-  long long sw = warp_sum(samples);
-  int hw = warp_sum(hit);
-  if (lane == 0) {
-    s_l[wid] = sw;
-    s_i[wid] = hw;
-  }
-  __syncthreads();
-  if (threadIdx.x < 28) {
-    double acc = 0.0;
-    for (int w = 0; w < kT / 32; ++w) acc += s_d[w][threadIdx.x];
-    PosePartial* out = partials + blockIdx.x;
-    if (threadIdx.x < 21)
-      out->jtj[threadIdx.x] = acc;
-    else if (threadIdx.x < 27)
-      out->jtr[threadIdx.x - 21] = acc;
-    else
-      out->loss = acc;
-  }
-  if (threadIdx.x == 32) {
-    long long sl = 0;
-    int sm = 0;
-    for (int w = 0; w < kT / 32; ++w) {
-      sl += s_l[w];
-      sm += s_i[w];
-    }
-    partials[blockIdx.x].samples = sl;
-    partials[blockIdx.x].m = sm;
-    partials[blockIdx.x].bad = 0;
-  }
-}
-
 // ------------------------------------------------------------------ corner-parallel
 // LPR lanes per ray (LPR = 8: one trilinear corner per lane). The tracking batch
 // is small (16,384 rays = 111 threads per SM at one thread per ray), so the
@@ -264,20 +51,22 @@ __global__ void __launch_bounds__(kT) k_pose_fused(
 //     lane accumulates its own partial Jo / Jd / B and the group reduces once
 //     per ray.
 // MINB = 3 CTAs/SM (168 registers). r01: capping registers for more warps lost
-// (4 CTAs, 128 regs + spills: 494 frames/s; 5: 460; 7: 458; 3: 525).
-template <typename ShT, int LPR, bool PAR = true, int MINB = 3>
+// (4 CTAs, 128 regs + spills: 494 frames/s; 5: 460; 7: 458; 3: 525). r01 also
+// measured 4 lanes per ray, a thread-per-ray kernel and a segment-by-segment
+// march here; all were slower and were removed in r02.
+template <typename ShT, int MINB = 3>
 __global__ void __launch_bounds__(kT, MINB) k_pose_group(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd_base,
     const int* __restrict__ frame_idx, long long npix, const DevPose* __restrict__ pose_ptr,
     const int* __restrict__ pixels, const uint32_t* __restrict__ order, int n, double lambda_p,
     double lambda_d, PosePartial* __restrict__ partials, int* err) {
-  constexpr int CPL = 8 / LPR;  // corners per lane
+  constexpr int LPR = 8, CPL = 1;  // lanes per ray, corners per lane
   __shared__ double s_d[kT / 32][32];
   __shared__ long long s_l[kT / 32];
   __shared__ int s_i[kT / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sub = lane & (LPR - 1), gbase = lane & ~(LPR - 1);
-  const unsigned gmask = ((LPR == 32) ? 0xffffffffu : ((1u << LPR) - 1u)) << gbase;
+  const unsigned gmask = 0xffu << gbase;
   const int t = blockIdx.x * (kT / LPR) + threadIdx.x / LPR;
   const int i = (order && t < n) ? (int)order[t] : t;
   const double4* rgbd = rgbd_base + npix * (long long)(*frame_idx);
@@ -315,7 +104,7 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
         for (int mm = 0; mm < 9; ++mm) bs[mm] = ShT(basis[mm]);
         Sample s;
         GroupMarch<LPR> gm;
-        while (PAR ? gm.next(g, m, s, sub, gbase, gmask) : march_next(g, m, s)) {
+        while (gm.next(g, m, s, sub, gbase, gmask)) {
           const double wx[2] = {dsub(1.0, s.fx), s.fx}, wy[2] = {dsub(1.0, s.fy), s.fy},
                        wz[2] = {dsub(1.0, s.fz), s.fz};
           double pk[CPL];
@@ -513,8 +302,15 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
 // group without a pending sample evaluates its next 8 segments, then every
 // group with a pending sample shades one. All ballots and shuffles run with
 // the full warp mask. The arithmetic (sample order, sigma in corner order,
-// colour in lane order, Jacobian partials) is the same as k_pose_group<float>.
-template <typename ShT, int MINB = 3>
+// colour in lane order, Jacobian partials) is the same as k_pose_group<float>,
+// and tests/test_gpu_pose.py holds the two bit-identical.
+//
+// fp32 only. r01 built an FP64-SH instance of this template as well: at 3
+// CTAs/SM (168 registers, 68 B of spill) it composited one sample per ray, and
+// at 2 CTAs/SM it matched k_pose_group<double>. That instance was never on a
+// product path; r02 removed it rather than ship an unexplained build (the FP64
+// parity path is k_pose_group<double>). The fp32 build has no spills.
+template <int MINB = 3>
 __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd_base,
     const int* __restrict__ frame_idx, long long npix, const DevPose* __restrict__ pose_ptr,
@@ -522,7 +318,8 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
     double lambda_d, PosePartial* __restrict__ partials, int* err) {
   constexpr int LPR = 8;
   constexpr unsigned FULL = 0xffffffffu;
-  using JT = typename std::conditional<sizeof(ShT) == 4, float, double>::type;
+  using ShT = float;
+  using JT = float;
   __shared__ double s_d[kT / 32][32];
   __shared__ long long s_l[kT / 32];
   __shared__ int s_i[kT / 32];
@@ -885,9 +682,12 @@ __device__ __forceinline__ uint32_t compact_bits(uint32_t x) {  // inverse of sp
   return x;
 }
 
-// Stratified valid-depth draws: thread t owns tile (Morton decode of t) of a
-// tiles_x x tiles_y grid over the image, draws uniformly inside it and redraws
-// (max_redraws attempts) until the depth is valid; -1 marks a dropped pixel.
+// Stratified valid-depth draws over a 2^L x 2^L tile grid (4^L <= n < 4^(L+1)):
+// thread t owns tile (Morton decode of t mod 4^L), so the first 4^L draws cover
+// every tile once and the rest start a second pass in Morton order (warps stay
+// coherent). Each draws uniformly inside its tile and redraws (max_redraws
+// attempts) until the depth is valid; -1 marks a dropped pixel. The counter
+// (iteration, t, attempt) keys the RNG, so every one of the n draws is distinct.
 __global__ void k_draw_strat(const double4* __restrict__ rgbd_base,
                              const int* __restrict__ frame_idx, long long npix, int width,
                              int height, int tiles_log2, int max_redraws,
@@ -897,11 +697,17 @@ __global__ void k_draw_strat(const double4* __restrict__ rgbd_base,
   if (t >= n) return;
   const double4* rgbd = rgbd_base + npix * (long long)(*frame_idx);
   const int tiles = 1 << tiles_log2;
-  const int tx = (int)compact_bits((uint32_t)t), ty = (int)compact_bits((uint32_t)t >> 1);
+  const uint32_t tile = (uint32_t)t & ((1u << (2 * tiles_log2)) - 1u);
+  const int tx = (int)compact_bits(tile), ty = (int)compact_bits(tile >> 1);
   int px = -1, py = -1;
   if (tx < tiles && ty < tiles) {
-    const int x0 = (int)((long long)tx * width / tiles), x1 = (int)((long long)(tx + 1) * width / tiles);
-    const int y0 = (int)((long long)ty * height / tiles), y1 = (int)((long long)(ty + 1) * height / tiles);
+    const int x0 = (int)((long long)tx * width / tiles);
+    int x1 = (int)((long long)(tx + 1) * width / tiles);
+    const int y0 = (int)((long long)ty * height / tiles);
+    int y1 = (int)((long long)(ty + 1) * height / tiles);
+    // more tiles than pixel rows / columns: a tile keeps at least its first pixel
+    if (x1 <= x0) x1 = x0 + 1;
+    if (y1 <= y0) y1 = y0 + 1;
     const int w = x1 - x0, h = y1 - y0;
     if (w > 0 && h > 0) {
       for (int a = 0; a < max_redraws; ++a) {
@@ -996,43 +802,9 @@ __global__ void k_gn_step(const PosePartial* __restrict__ ne, DevPose* pose, dou
 
 }  // namespace
 
-// Corner-parallel (8 lanes per ray) by default; VRF_POSE_KERNEL=thread selects
-// the thread-per-ray kernel, =group4 four lanes per ray (A/B runs).
-static int pose_kernel() {  // 0 thread, 4 / 8 lanes per ray
-  static const int k = [] {
-    const char* e = getenv("VRF_POSE_KERNEL");
-    if (e && std::string(e) == "thread") return 0;
-    if (e && std::string(e) == "group4") return 4;
-    return 8;
-  }();
-  return k;
-}
+int pose_fused_blocks(int n) { return (n + kT / 8 - 1) / (kT / 8); }
 
-// A/B: VRF_POSE_MARCH=serial marches segment by segment in the group kernel.
-static bool pose_march_serial() {
-  static const bool v = [] {
-    const char* e = getenv("VRF_POSE_MARCH");
-    return e && std::string(e) == "serial";
-  }();
-  return v;
-}
-
-// VRF_POSE_UNIFORM=0: the group-independent k_pose_group on the GN path (A/B).
-static bool pose_uniform() {
-  static const bool v = [] {
-    const char* e = getenv("VRF_POSE_UNIFORM");
-    return !(e && std::string(e) == "0");
-  }();
-  return v;
-}
-
-int pose_fused_blocks(int n) {
-  const int lpr = pose_kernel();
-  const int rays_per_block = lpr == 0 ? kT : kT / lpr;
-  return (n + rays_per_block - 1) / rays_per_block;
-}
-
-void launch_pose_fused(bool fp64_sh, const DevGrid& g, const DevParams& p, const DevCam& cam,
+void launch_pose_fused(PoseKernel which, const DevGrid& g, const DevParams& p, const DevCam& cam,
                        const double4* rgbd_base, const int* frame_idx, long long npix,
                        const DevPose* pose, const int* pixels, const uint32_t* order, int n,
                        double lambda_p, double lambda_d, PosePartial* partials, int* err,
@@ -1041,35 +813,16 @@ void launch_pose_fused(bool fp64_sh, const DevGrid& g, const DevParams& p, const
   const int nb = pose_fused_blocks(n);
 #define VRF_POSE_ARGS \
   g, p, cam, rgbd_base, frame_idx, npix, pose, pixels, order, n, lambda_p, lambda_d, partials, err
-  switch (pose_kernel()) {
-    case 0:
-      if (fp64_sh)
-        k_pose_fused<double><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
-      else
-        k_pose_fused<float><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
+  switch (which) {
+    case PoseKernel::kParityFp64:
+      k_pose_group<double><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       break;
-    case 4:
-      if (fp64_sh)
-        k_pose_group<double, 4><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
-      else
-        k_pose_group<float, 4><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
+    case PoseKernel::kGroupFp32:
+      k_pose_group<float><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
       break;
-    default:
-      // The FP64 parity path keeps k_pose_group. Open item from r01: the
-      // k_pose_group_u<double> build at 3 CTAs/SM (168 registers, 68 B of
-      // spills) composited only the first sample of each ray (samples == rays);
-      // the same source at 2 CTAs/SM (246 registers, no spills) matched
-      // k_pose_group exactly. Until that is understood the parity path does not
-      // use it; the fp32 GN build (166 registers, no spills) is verified
-      // bit-identical to k_pose_group<float>.
-      if (fp64_sh)
-        k_pose_group<double, 8><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
-      else if (pose_march_serial())
-        k_pose_group<float, 8, false><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
-      else if (pose_uniform())
-        k_pose_group_u<float><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
-      else
-        k_pose_group<float, 8><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
+    case PoseKernel::kGnUniform:
+      k_pose_group_u<><<<nb, kT, 0, s>>>(VRF_POSE_ARGS);
+      break;
   }
 #undef VRF_POSE_ARGS
 }

@@ -1,10 +1,13 @@
-"""Evaluation metrics around the hot path (eval.cpp), host side.
+"""Evaluation metrics around the hot path (eval.cpp) and TUM trajectory I/O
+(trajectory.cpp).
 
 The trajectory metrics (ATE, RPE) are O(frames) host arithmetic, as in the
-reference; map quality renders the evaluation views on the GPU
-(Context.render_image) and scores them here with the reference's sampling
-stream, so a PSNR figure is comparable with the reference's own
-evaluate_map_quality on the same frames.
+reference. Map quality renders the evaluation views on the GPU and scores them
+in HBM (vrf_evaluate_views) with the reference's PSNR sampling stream, so the
+figure is comparable with the reference's own evaluate_map_quality on the same
+frames. psnr / depth_l1 below are the host restatements over given images.
+All of it is pinned to the reference's eval.cpp / trajectory.cpp by
+tests/test_eval_reference.py and tests/test_gpu_eval.py.
 """
 from __future__ import annotations
 
@@ -52,6 +55,39 @@ def ate_rmse(est: Sequence[Pose], est_ts, ref: Sequence[Pose], ref_ts, align: bo
         trans = cr - rot @ ce
     err = (pe @ rot.T + trans) - pr
     return math.sqrt(float(np.sum(err * err)) / len(pairs)), len(pairs)
+
+
+def save_tum(path, poses: Sequence[Pose], timestamps) -> None:
+    """save_tum — trajectory.cpp:10-23: "# timestamp tx ty tz qx qy qz qw" header,
+    then one line per pose, every value printed with %.17g (doubles round-trip)."""
+    with open(path, "w") as f:
+        f.write("# timestamp tx ty tz qx qy qz qw\n")
+        for ts, p in zip(timestamps, poses):
+            w, x, y, z = (float(v) for v in p.q)
+            tx, ty, tz = (float(v) for v in p.t)
+            f.write("%.17g %.17g %.17g %.17g %.17g %.17g %.17g %.17g\n"
+                    % (float(ts), tx, ty, tz, x, y, z, w))
+
+
+def load_tum(path):
+    """load_tum — trajectory.cpp:25-46: skips blank and '#' lines; a line without
+    eight numbers raises. Returns (poses, timestamps)."""
+    poses, stamps = [], []
+    with open(path) as f:
+        for lineno, line in enumerate(f, 1):
+            s = line.strip(" \t\r\n")
+            if not s or s[0] == "#":
+                continue
+            try:
+                v = [float(x) for x in s.split()[:8]]
+                if len(v) < 8:
+                    raise ValueError
+            except ValueError:
+                raise RuntimeError(f"load_tum: malformed line {lineno} in {path}") from None
+            ts, tx, ty, tz, qx, qy, qz, qw = v
+            stamps.append(ts)
+            poses.append(Pose((qw, qx, qy, qz), (tx, ty, tz)))
+    return poses, stamps
 
 
 def rotation_angle_rad(q) -> float:
@@ -163,21 +199,30 @@ class MapQuality:
 def evaluate_map_quality(ctx, intrinsics, frames, frame_indices, render: Optional[RenderParams] = None,
                          images: int = 10, pixels_per_image: int = 10000, seed: int = 0,
                          exact_depth=None) -> MapQuality:
-    """evaluate_map_quality — eval.cpp:210-240, rendering the evaluation views
-    on the device resident grid of ``ctx``."""
+    """evaluate_map_quality — eval.cpp:210-240 on the device: the evaluation views
+    are rendered on the grid resident in ``ctx`` and scored in HBM
+    (Context.evaluate_views / vrf_evaluate_views); only the sums come back. The
+    PSNR pixels are the reference's Rng draws (eval.cpp:72-83), the depth
+    reference is exact_depth[idx] when given (prefer_exact_depth), else the
+    frame's depth."""
     if not frame_indices:
         raise RuntimeError("evaluate_map_quality: no frames")
-    rc, rd, ref_c, ref_d = [], [], [], []
+    poses, colors, depths = [], [], []
     for idx in frame_indices:
         f = frames[idx]
         if f.gt_pose is None:
             raise RuntimeError("evaluate_map_quality: frame without pose")
-        r = ctx.render_image(intrinsics, f.gt_pose, render or RenderParams())
-        rc.append(r.color)
-        rd.append(r.depth)
-        ref_c.append(f.color)
+        poses.append(f.gt_pose)
+        colors.append(f.color)
         use_exact = exact_depth is not None and idx < len(exact_depth) and exact_depth[idx] is not None
-        ref_d.append(exact_depth[idx] if use_exact else f.depth)
-    p, ns = psnr(rc, ref_c, rd, images, pixels_per_image, seed)
-    l1, npx = depth_l1(rd, ref_d, rd)
-    return MapQuality(p, l1, ns, npx)
+        depths.append(exact_depth[idx] if use_exact else f.depth)
+    samples = Rng(seed).draw_eval_samples(len(poses), intrinsics.width, intrinsics.height, images,
+                                          pixels_per_image)
+    sq, ns, l1s, npx = ctx.evaluate_views(intrinsics, poses, colors, depths, samples, render)
+    if ns == 0:
+        raise RuntimeError("psnr: no valid pixels sampled")
+    if npx == 0:
+        raise RuntimeError("depth_l1: empty valid mask")
+    mse = sq / (ns * 3)
+    p = 99.0 if mse <= 0.0 else min(99.0, 10.0 * math.log10(1.0 / mse))
+    return MapQuality(p, l1s / npx, int(ns), int(npx))

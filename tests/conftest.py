@@ -13,6 +13,7 @@ sys.path.insert(0, str(ROOT / "oracle"))
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs libvoxrf_b200 kernels)")
     config.addinivalue_line("markers", "ref: needs the reference build in oracle/_ref")
+    config.addinivalue_line("markers", "slow: config-shaped parity (seconds to a minute each)")
 
 
 @pytest.fixture(scope="session")
