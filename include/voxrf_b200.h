@@ -232,6 +232,20 @@ int vrf_grid_load(vrf_context* ctx, const char* path);
 /* VoxelGrid::prune(tau) — voxel_grid.cpp:169-188. */
 int vrf_grid_prune(vrf_context* ctx, double tau, int64_t* deactivated);
 
+/* ---- drop-in residency (integration/voxrf_gpu_backend.cpp keeps the device grid in
+ * step with a caller's VoxelGrid without whole-grid copies per call):
+ * partial writes of host-modified vertex ranges, an occupancy refresh, and the log
+ * of the float4 groups the last RMSProp pass updated (mapping.cpp:218-231's
+ * touched set) for a sparse write-back of the in-place result. */
+int vrf_grid_write_vertices(vrf_context* ctx, int64_t first, int64_t count, const double* data);
+int vrf_rmsprop_write_vertices(vrf_context* ctx, int64_t first, int64_t count, const double* v);
+int vrf_grid_set_occupancy(vrf_context* ctx, const uint8_t* occupancy);
+/* on: every later mapping step logs its updated groups (ids = vertex * 7 + group,
+ * new theta and v as 4 floats each); the log holds the last step only. */
+int vrf_track_updates(vrf_context* ctx, int on);
+int vrf_updates_count(vrf_context* ctx, int64_t* n);
+int vrf_updates_read(vrf_context* ctx, int64_t n, uint32_t* ids, float* theta, float* v);
+
 /* ---- frames: Frame (frame.hpp:10-19); colour H*W*3, depth H*W along-ray metres */
 int vrf_frames_upload(vrf_context* ctx, const vrf_intrinsics* intr, int n,
                       const double* const* colors, const double* const* depths,

@@ -12,6 +12,8 @@
 
 using namespace voxrf;
 
+extern "C" void voxrf_b200_dropin_traffic(std::uint64_t* uploaded, std::uint64_t* written_back);
+
 extern "C" {
 Frame voxrf_ref_render_image(const VoxelGrid&, const CameraIntrinsics&, const Pose&,
                              const RenderParams&, int, int);
@@ -125,6 +127,78 @@ TEST_CASE("drop-in mapping_step matches the reference mapping_step") {
   }
   std::vector<const Frame*> none;
   CHECK_THROWS_AS(mapping_step(ga, none, s.intr, cfg, ra, rnga), std::runtime_error);
+}
+
+TEST_CASE("drop-in residency: repeat calls re-send nothing, caller writes reach the device") {
+  Scene s = make_scene();
+  const Pose& pose = *s.frames[2].gt_pose;
+  std::uint64_t up0 = 0, back0 = 0, up1 = 0, back1 = 0;
+  auto same_as_ref = [&](const VoxelGrid& g) {
+    const Frame a = render_image(g, s.intr, pose, RenderParams{}, 1);
+    const Frame b = voxrf_ref_render_image(g, s.intr, pose, RenderParams{}, 1, 1);
+    return max_rel(a.color.data, b.color.data, 1e-6) < 1e-10 &&
+           max_rel(a.depth.data, b.depth.data, 1e-6) < 1e-10;
+  };
+  VoxelGrid g = blob_grid(17, 0.1);
+  CHECK(same_as_ref(g));
+  voxrf_b200_dropin_traffic(&up0, &back0);
+  CHECK(same_as_ref(g));  // unchanged grid: no re-upload beyond the unprotectable end pages
+  voxrf_b200_dropin_traffic(&up1, &back1);
+  CHECK(up1 - up0 < 64 * 1024);
+  // payload writes (a dense shell of sigma through the middle of the view)
+  for (std::uint32_t v = 0; v < std::uint32_t(g.geometry().num_vertices()); v += 3)
+    g.vertex(v)[0] = float(g.vertex(v)[0] + 15.0);  // (fp32-exact: the device stores fp32)
+  CHECK(same_as_ref(g));
+  // occupancy writes (prune-like deactivation)
+  for (int cz = 4; cz < 12; ++cz)
+    for (int cy = 0; cy < 16; ++cy)
+      for (int cx = 0; cx < 16; ++cx) g.set_cell_active(cx, cy, cz, false);
+  CHECK(same_as_ref(g));
+  // a new grid object (possibly at the same address) with other content
+  g = VoxelGrid();
+  g = blob_grid(17, 0.1);
+  for (std::uint32_t v = 0; v < std::uint32_t(g.geometry().num_vertices()); ++v) g.vertex(v)[0] *= 0.5;
+  CHECK(same_as_ref(g));
+}
+
+TEST_CASE("drop-in mapping_step chains in place with sparse write-back") {
+  Scene s = make_scene();
+  std::vector<const Frame*> kf;
+  for (const Frame& f : s.frames) kf.push_back(&f);
+  VoxelGrid ga(s.grid.geometry(), 0.1), gb(s.grid.geometry(), 0.1);
+  MappingConfig cfg;
+  cfg.rays_per_batch = 64;
+  cfg.deterministic = true;
+  RmspropState ra, rb;
+  Rng rnga(11), rngb(11);
+  std::uint64_t up0 = 0, back0 = 0, up1 = 0, back1 = 0;
+  mapping_step(ga, kf, s.intr, cfg, ra, rnga);
+  voxrf_ref_mapping_step(gb, kf, s.intr, cfg, rb, rngb);
+  voxrf_b200_dropin_traffic(&up0, &back0);
+  for (int step = 1; step < 4; ++step) {
+    const MapStepStats a = mapping_step(ga, kf, s.intr, cfg, ra, rnga);
+    const MapStepStats b = voxrf_ref_mapping_step(gb, kf, s.intr, cfg, rb, rngb);
+    CHECK(a.rays_color == b.rays_color);
+    CHECK(a.loss_total == doctest::Approx(b.loss_total).epsilon(1e-4));
+  }
+  voxrf_b200_dropin_traffic(&up1, &back1);
+  const std::uint64_t grid_bytes = ga.data().size() * sizeof(double);
+  // chained steps: grid, RMSProp state and keyframes stay resident ...
+  CHECK(up1 - up0 < 3 * 64 * 1024);
+  // ... and only the updated float4 groups come back (64 rays touch a fraction)
+  CHECK(back1 - back0 < 3 * grid_bytes / 4);
+  // untouched vertices keep the caller's exact fp64 values (the reference's
+  // in-place semantics); touched ones agree with the reference's fp64 update
+  double worst = 0.0, scale = 0.0;
+  std::size_t exact = 0;
+  for (std::size_t i = 0; i < ga.data().size(); ++i) {
+    worst = std::max(worst, std::abs(ga.data()[i] - gb.data()[i]));
+    scale = std::max(scale, std::abs(gb.data()[i]));
+    exact += ga.data()[i] == gb.data()[i];
+  }
+  CHECK(worst <= 1e-4 * scale);
+  CHECK(exact > ga.data().size() / 4);
+  CHECK(ra.v.size() == rb.v.size());
 }
 
 TEST_CASE("drop-in pose_gradient and track_frame match the reference") {

@@ -13,9 +13,17 @@
 // (proj/include/voxrf) and links it in place of those six definitions
 // (INTEGRATION.md); everything else (VoxelGrid, per-ray CPU functions used by
 // tests and gradcheck, dataset/eval/CLI) is unchanged.
+//
+// Device residency: the caller's grid, RMSProp state and keyframes stay in HBM
+// between calls. Each host buffer the device mirrors is write-tracked
+// (host_mirror.hpp), so a repeat call uploads only what the caller changed, and
+// mapping_step writes back only the float4 groups its RMSProp pass updated (the
+// reference's touched set, mapping.cpp:218-231) — untouched vertices keep their
+// host fp64 values, as in the reference's in-place update.
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -23,10 +31,13 @@
 #include "voxrf/mapping.hpp"
 #include "voxrf/renderer.hpp"
 #include "voxrf/tracking.hpp"
+#include "host_mirror.hpp"
 #include "voxrf_b200.h"
 
 namespace voxrf {
 namespace {
+
+using voxrf_b200::HostMirror;
 
 vrf_context* ctx() {
   static vrf_context* c = [] {
@@ -36,6 +47,7 @@ vrf_context* ctx() {
     if (rc != VRF_OK)
       throw std::runtime_error("voxrf_b200: no usable CUDA device (status " +
                                std::to_string(rc) + "); there is no CPU fallback");
+    vrf_track_updates(h, 1);  // mapping_step's sparse write-back
     return h;
   }();
   return c;
@@ -74,9 +86,170 @@ vrf_render_params to_c(const RenderParams& r) {
   return vrf_render_params{r.step, r.t_near, r.t_far, r.termination_eps};
 }
 
-void upload_grid(const VoxelGrid& grid) {
-  const vrf_grid_geometry g = to_c(grid.geometry());
-  check(vrf_grid_upload(ctx(), &g, grid.data().data(), grid.occupancy().data()));
+// ---- device residency
+struct Residency {
+  bool grid_valid = false;
+  const double* data = nullptr;
+  std::size_t data_n = 0;
+  const std::uint8_t* occ = nullptr;
+  std::size_t occ_n = 0;
+  GridGeometry geom;
+  const double* rms = nullptr;  // host RMSProp buffer the device state matches
+  std::size_t rms_n = 0;
+  struct Slot {
+    const double* c = nullptr;
+    const double* d = nullptr;
+    std::size_t cn = 0, dn = 0;
+    vrf_pose pose{};
+  };
+  std::vector<Slot> slots;
+  vrf_intrinsics intr{};
+  // statistics for tests / the bench: bytes uploaded and written back
+  std::uint64_t up_bytes = 0, back_bytes = 0;
+  std::int64_t last_samples = 0;  // composited samples of the last mapping_step
+};
+Residency g_res;
+
+bool same_geom(const GridGeometry& a, const GridGeometry& b) {
+  return a.res == b.res && a.origin == b.origin && a.voxel_size == b.voxel_size;
+}
+
+constexpr std::size_t kVertexBytes = sizeof(double) * kPayloadSize;
+
+// Vertex ranges covering dirty byte ranges of a [V][28] fp64 buffer.
+template <typename F>
+void for_dirty_vertices(const double* buf, F&& f) {
+  for (const auto& r : HostMirror::dirty(buf)) {
+    const std::size_t v0 = r.first / kVertexBytes;
+    const std::size_t v1 = (r.second + kVertexBytes - 1) / kVertexBytes;
+    f(v0, v1 - v0);
+  }
+}
+
+void sync_grid(const VoxelGrid& grid) {
+  HostMirror::refresh();
+  const double* d = grid.data().data();
+  const std::size_t n = grid.data().size();
+  const std::uint8_t* o = grid.occupancy().data();
+  const std::size_t on = grid.occupancy().size();
+  const bool same = g_res.grid_valid && d == g_res.data && n == g_res.data_n &&
+                    o == g_res.occ && on == g_res.occ_n &&
+                    same_geom(grid.geometry(), g_res.geom) &&
+                    HostMirror::tracked(d, n * sizeof(double)) && HostMirror::tracked(o, on);
+  if (!same) {
+    const vrf_grid_geometry g = to_c(grid.geometry());
+    check(vrf_grid_upload(ctx(), &g, d, o));  // (re-allocates: RMSProp state restarts)
+    g_res.up_bytes += n * sizeof(double) + on;
+    HostMirror::track(d, n * sizeof(double));
+    HostMirror::track(o, on);
+    g_res.grid_valid = true;
+    g_res.data = d;
+    g_res.data_n = n;
+    g_res.occ = o;
+    g_res.occ_n = on;
+    g_res.geom = grid.geometry();
+    g_res.rms = nullptr;
+    return;
+  }
+  if (!HostMirror::dirty(o).empty()) {  // set_cell_active / prune since the last call
+    check(vrf_grid_set_occupancy(ctx(), o));
+    g_res.up_bytes += on;
+    HostMirror::clean(o);
+  }
+  for_dirty_vertices(d, [&](std::size_t v0, std::size_t nv) {
+    check(vrf_grid_write_vertices(ctx(), std::int64_t(v0), std::int64_t(nv), d + v0 * kPayloadSize));
+    g_res.up_bytes += nv * kVertexBytes;
+  });
+  HostMirror::clean(d);
+}
+
+// mapping.cpp:219: a state of the wrong size restarts at zero.
+void sync_rmsprop(RmspropState& st, std::size_t n) {
+  if (st.v.size() != n) st.reset(n);
+  double* v = st.v.data();
+  if (v == g_res.rms && n == g_res.rms_n && HostMirror::tracked(v, n * sizeof(double))) {
+    for_dirty_vertices(v, [&](std::size_t v0, std::size_t nv) {
+      check(vrf_rmsprop_write_vertices(ctx(), std::int64_t(v0), std::int64_t(nv),
+                                       v + v0 * kPayloadSize));
+      g_res.up_bytes += nv * kVertexBytes;
+    });
+  } else {
+    check(vrf_rmsprop_upload(ctx(), v));
+    g_res.up_bytes += n * sizeof(double);
+    HostMirror::track(v, n * sizeof(double));
+    g_res.rms = v;
+    g_res.rms_n = n;
+  }
+  HostMirror::clean(v);
+}
+
+// The frames of the call in slots 0..n-1; a slot is rewritten only when its
+// buffers changed (new buffers, or writes since they were uploaded).
+void sync_frames(const CameraIntrinsics& intr, const std::vector<const Frame*>& frames) {
+  const vrf_intrinsics ic = to_c(intr);
+  const bool same_intr = std::memcmp(&ic, &g_res.intr, sizeof(ic)) == 0;
+  if (!same_intr || g_res.slots.size() < frames.size()) {
+    const std::size_t cap = std::max(frames.size(), same_intr ? 2 * g_res.slots.size() : 0);
+    check(vrf_frames_reserve(ctx(), &ic, int(cap)));
+    g_res.slots.assign(cap, {});
+    g_res.intr = ic;
+  }
+  for (std::size_t i = 0; i < frames.size(); ++i) {
+    const Frame& f = *frames[i];
+    Residency::Slot want{f.color.data.data(), f.depth.data.data(), f.color.data.size(),
+                         f.depth.data.size(), to_c(f.gt_pose ? *f.gt_pose : Pose{})};
+    Residency::Slot& have = g_res.slots[i];
+    const bool same_buffers = have.c == want.c && have.d == want.d && have.cn == want.cn &&
+                              have.dn == want.dn &&
+                              HostMirror::tracked(want.c, want.cn * sizeof(double)) &&
+                              HostMirror::tracked(want.d, want.dn * sizeof(double)) &&
+                              HostMirror::dirty(want.c).empty() &&
+                              HostMirror::dirty(want.d).empty();
+    if (!same_buffers) {
+      check(vrf_frame_set(ctx(), int(i), want.c, want.d, &want.pose));
+      g_res.up_bytes += (want.cn + want.dn) * sizeof(double);
+      HostMirror::track(want.c, want.cn * sizeof(double));
+      HostMirror::track(want.d, want.dn * sizeof(double));
+      have = want;
+    } else if (std::memcmp(&have.pose, &want.pose, sizeof(vrf_pose)) != 0) {
+      check(vrf_frame_set_pose(ctx(), int(i), &want.pose));
+      have.pose = want.pose;
+    }
+  }
+}
+
+// Writes mapping_step's result back into the caller's grid and RMSProp state:
+// the updated float4 groups only, or everything when most groups changed.
+void write_back(VoxelGrid& grid, RmspropState& st) {
+  double* d = grid.data().data();
+  double* v = st.v.data();
+  const std::size_t groups = grid.data().size() / 4;
+  std::int64_t n = 0;
+  check(vrf_updates_count(ctx(), &n));
+  HostMirror::unprotect(d);
+  HostMirror::unprotect(v);
+  if (std::size_t(n) * 3 > groups) {  // dense: cheaper than the indexed form
+    check(vrf_grid_download(ctx(), d, nullptr));
+    check(vrf_rmsprop_download(ctx(), v));
+    g_res.back_bytes += 2 * groups * 4 * sizeof(float);
+  } else if (n > 0) {
+    static std::vector<std::uint32_t> ids;
+    static std::vector<float> th, vv;
+    ids.resize(std::size_t(n));
+    th.resize(4 * std::size_t(n));
+    vv.resize(4 * std::size_t(n));
+    check(vrf_updates_read(ctx(), n, ids.data(), th.data(), vv.data()));
+    for (std::int64_t i = 0; i < n; ++i) {
+      const std::size_t o = 4 * std::size_t(ids[std::size_t(i)]);  // == vertex * 28 + 4 group
+      for (int e = 0; e < 4; ++e) {
+        d[o + e] = th[4 * std::size_t(i) + e];
+        v[o + e] = vv[4 * std::size_t(i) + e];
+      }
+    }
+    g_res.back_bytes += std::size_t(n) * (4 + 32);
+  }
+  HostMirror::clean(d);
+  HostMirror::clean(v);
 }
 
 void upload_frames(const CameraIntrinsics& intr, const std::vector<const Frame*>& frames) {
@@ -90,6 +263,8 @@ void upload_frames(const CameraIntrinsics& intr, const std::vector<const Frame*>
   const vrf_intrinsics ic = to_c(intr);
   check(vrf_frames_upload(ctx(), &ic, int(frames.size()), colors.data(), depths.data(),
                           poses.data()));
+  g_res.slots.clear();  // the slot store was replaced
+  g_res.intr = vrf_intrinsics{};
 }
 
 vrf_mapping_config to_c(const MappingConfig& c) {
@@ -173,7 +348,7 @@ Frame render_image(const VoxelGrid& grid, const CameraIntrinsics& intr, const Po
   frame.color = ImageF(out_w, out_h, 3);
   frame.depth = ImageF(out_w, out_h, 1);
   frame.gt_pose = pose;
-  upload_grid(grid);
+  sync_grid(grid);
   const vrf_intrinsics ic = to_c(intr);
   const vrf_pose pc = to_c(pose);
   const vrf_render_params rp = to_c(params);
@@ -188,19 +363,19 @@ MapStepStats mapping_step(VoxelGrid& grid, const std::vector<const Frame*>& keyf
   if (keyframes.empty()) throw std::runtime_error("mapping_step: no keyframes");
   const std::vector<int32_t> batch =
       draw_batch(rng, int(keyframes.size()), intrinsics, config.rays_per_batch);
-  upload_grid(grid);
-  upload_frames(intrinsics, keyframes);
-  if (rmsprop.v.size() == grid.data().size())
-    check(vrf_rmsprop_upload(ctx(), rmsprop.v.data()));
-  else
-    check(vrf_rmsprop_reset(ctx()));
+  sync_grid(grid);
+  sync_rmsprop(rmsprop, grid.data().size());
+  sync_frames(intrinsics, keyframes);
   const vrf_mapping_config cc = to_c(config);
   vrf_map_step_stats st{};
-  check(vrf_mapping_step(ctx(), &cc, batch.data(), config.rays_per_batch, &st));
+  const int rc = vrf_mapping_step(ctx(), &cc, batch.data(), config.rays_per_batch, &st);
+  if (rc != VRF_OK) {
+    g_res.grid_valid = false;  // (no update happened; re-sync next call)
+    check(rc);
+  }
+  g_res.last_samples = st.samples;
   // In-place contract (mapping.hpp:80): grid and RMSProp state are updated.
-  check(vrf_grid_download(ctx(), grid.data().data(), nullptr));
-  rmsprop.v.resize(grid.data().size());
-  check(vrf_rmsprop_download(ctx(), rmsprop.v.data()));
+  write_back(grid, rmsprop);
   return to_stats(st);
 }
 
@@ -216,6 +391,7 @@ MapResult map_scene(const Dataset& dataset, const MappingConfig& config,
   const GridGeometry geom = geometry ? *geometry : fit_grid_geometry(dataset, keyframes, config);
   MapResult result{VoxelGrid(geom, config.sigma_init), {}};
   upload_frames(dataset.intrinsics, keyframes);
+  g_res.grid_valid = false;  // the device grid becomes map_scene's own
   const vrf_mapping_config cc = to_c(config);
   const auto t0 = std::chrono::steady_clock::now();
   int iteration = 0;
@@ -223,7 +399,10 @@ MapResult map_scene(const Dataset& dataset, const MappingConfig& config,
   // schedule: stages refine on the device (vrf_grid_upsample ==
   // VoxelGrid::upsampled + RMSProp reset, mapping.cpp:297-300) and the host
   // grid is written back once at the end.
-  upload_grid(result.grid);
+  {
+    const vrf_grid_geometry g0 = to_c(result.grid.geometry());
+    check(vrf_grid_upload(ctx(), &g0, result.grid.data().data(), result.grid.occupancy().data()));
+  }
   check(vrf_rmsprop_reset(ctx()));
   uint64_t rs[4];
   vrf_rng_seed(config.seed, rs);  // == Rng(config.seed), mapping.cpp:292
@@ -276,8 +455,8 @@ PoseGradient pose_gradient(const VoxelGrid& grid, const Frame& frame,
                            const CameraIntrinsics& intrinsics, const Pose& pose,
                            const std::vector<PixelSample>& pixels, const TrackingConfig& config) {
   if (pixels.empty()) throw std::runtime_error("pose_gradient: empty pixel set");
-  upload_grid(grid);
-  upload_frames(intrinsics, {&frame});
+  sync_grid(grid);
+  sync_frames(intrinsics, {&frame});
   std::vector<int32_t> px(2 * pixels.size());
   for (std::size_t i = 0; i < pixels.size(); ++i) {
     px[2 * i] = pixels[i].px;
@@ -304,8 +483,8 @@ TrackFrameResult track_frame(const VoxelGrid& grid, const Frame& frame,
     r.pose = init;
     return r;
   }
-  upload_grid(grid);
-  upload_frames(intrinsics, {&frame});
+  sync_grid(grid);
+  sync_frames(intrinsics, {&frame});
   return track_uploaded(0, intrinsics, init, config);
 }
 
@@ -314,10 +493,10 @@ TrackSequenceResult track_sequence(const VoxelGrid& grid, const Dataset& dataset
   if (dataset.frames.empty()) throw std::runtime_error("track_sequence: empty dataset");
   if (!dataset.frames.front().gt_pose)
     throw std::runtime_error("track_sequence: first frame needs a pose");
-  upload_grid(grid);
+  sync_grid(grid);
   std::vector<const Frame*> all;
   for (const Frame& f : dataset.frames) all.push_back(&f);
-  upload_frames(dataset.intrinsics, all);
+  sync_frames(dataset.intrinsics, all);
 
   TrackSequenceResult result;
   const Pose first = *dataset.frames.front().gt_pose;
@@ -350,3 +529,13 @@ TrackSequenceResult track_sequence(const VoxelGrid& grid, const Dataset& dataset
 }
 
 }  // namespace voxrf
+
+// Residency counters of the drop-in (tests, bench): bytes uploaded to the device
+// and written back to the caller's buffers since the process started.
+extern "C" void voxrf_b200_dropin_traffic(std::uint64_t* uploaded, std::uint64_t* written_back) {
+  *uploaded = voxrf::g_res.up_bytes;
+  *written_back = voxrf::g_res.back_bytes;
+}
+// Composited samples of the last drop-in mapping_step (MapStepStats has no such
+// field; the bench's samples/s needs it).
+extern "C" std::int64_t voxrf_b200_dropin_last_samples() { return voxrf::g_res.last_samples; }

@@ -127,6 +127,12 @@ _SIGS = {
     "vrf_set_shard_multiple": (C.c_int, [vp, C.c_int]),
     "vrf_set_stream": (C.c_int, [vp, vp]),
     "vrf_set_record_limits": (C.c_int, [vp, C.c_double, C.c_int]),
+    "vrf_grid_write_vertices": (C.c_int, [vp, C.c_int64, C.c_int64, vp]),
+    "vrf_rmsprop_write_vertices": (C.c_int, [vp, C.c_int64, C.c_int64, vp]),
+    "vrf_grid_set_occupancy": (C.c_int, [vp, vp]),
+    "vrf_track_updates": (C.c_int, [vp, C.c_int]),
+    "vrf_updates_count": (C.c_int, [vp, P(C.c_int64)]),
+    "vrf_updates_read": (C.c_int, [vp, C.c_int64, vp, vp, vp]),
     "vrf_get_device_buffers": (C.c_int, [vp, P(DeviceBuffers_c)]),
     "vrf_kernel_launch_count": (C.c_int64, [vp]),
     "vrf_profile_enable": (C.c_int, [vp, C.c_int]),

@@ -46,6 +46,8 @@ void vrf_context_destroy(vrf_context* ctx) {
   cudaFree(ctx->d_pose_out);
   cudaFree(ctx->d_pose);
   cudaFree(ctx->d_touched);
+  cudaFree(ctx->d_upd_count);
+  cudaFree(ctx->payload_soa);
   cudaFree(ctx->d_nblocks);
   cudaFree(ctx->d_frame);
   cudaFree(ctx->d_gn_pose);
@@ -58,6 +60,7 @@ void vrf_context_destroy(vrf_context* ctx) {
                            &ctx->s_count, &ctx->s_offsets, &ctx->s_keys, &ctx->s_keys2,
                            &ctx->s_ids, &ctx->s_ids2, &ctx->s_values, &ctx->s_grad64, &ctx->s_cub,
                            &ctx->s_stage, &ctx->s_out, &ctx->s_batch2, &ctx->s_rec,
+                           &ctx->s_upd_ids, &ctx->s_upd_theta, &ctx->s_upd_v,
                            &ctx->s_reccount})
     cudaFree(s->ptr);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
@@ -196,6 +199,16 @@ int vrf_grid_upload(vrf_context* ctx, const vrf_grid_geometry* geom, const doubl
     launch_f64_to_f32((const double*)ctx->s_out.ptr, ctx->payload + off, n, ctx->stream);
     LAUNCHED(1);
   }
+  if ((rc = upload_occupancy_u8(ctx, occupancy))) return rc;
+  update_blocks(ctx);
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_grid_set_occupancy(vrf_context* ctx, const uint8_t* occupancy) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
   if ((rc = upload_occupancy_u8(ctx, occupancy))) return rc;
   update_blocks(ctx);
   CU(cudaStreamSynchronize(ctx->stream));

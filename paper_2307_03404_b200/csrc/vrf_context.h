@@ -39,6 +39,7 @@ struct vrf_context {
   vrf_grid_geometry geom{};
   long long V = 0, Vpad = 0, C = 0;
   float* payload = nullptr;
+  float4* payload_soa = nullptr;  // A/B only (VRF_GATHER_SOA): [7][V] copy for K0's gathers
   float* grad = nullptr;
   float* rms = nullptr;
   uint32_t* occ = nullptr;
@@ -84,6 +85,10 @@ struct vrf_context {
   int rec_K = 0;
   int max_ray_samples = 0;  // longest ray seen by a mapping forward (sizes rec_K)
   long long rec_need_tried = 0;  // last record depth the budget was evaluated for
+  // RMSProp update log for the drop-in's sparse write-back (vrf_track_updates)
+  bool log_updates = false;
+  vrf_host::DeviceScratch s_upd_ids, s_upd_theta, s_upd_v;
+  unsigned long long* d_upd_count = nullptr;
   double rec_budget_gb = -1.0;   // vrf_set_record_limits: <= 0 automatic (30 % of free HBM)
   int rec_max_k = -1;            // vrf_set_record_limits: < 0 automatic, 0 no records
 
@@ -281,6 +286,8 @@ inline DevGrid dev_grid(const vrf_context* ctx) {
   g.inv_voxel = 1.0 / q.voxel_size;
   g.rcp_voxel = 1.0 / q.voxel_size;
   g.payload = reinterpret_cast<const float4*>(ctx->payload);
+  g.soa = ctx->payload_soa;
+  g.soa_stride = (long long)ctx->V;
   g.occ = ctx->occ;
   g.bocc = ctx->bocc;
   g.bx = ctx->bdim[0];
@@ -421,6 +428,14 @@ inline double psnr_from_lp(double lp) {  // mapping.cpp:107-110
 // Forward + fixed-order reduce for a device batch; leaves ray_cd/flags/stats on device.
 inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_dev,
                            int n, bool fast, int* ray_count = nullptr) {
+#ifdef VRF_GATHER_SOA
+  if (fast) {  // A/B: refresh the planar copy K0 gathers from (misc slot, not K0)
+    if (!ctx->payload_soa) CU(cudaMalloc(&ctx->payload_soa, sizeof(float4) * 7 * ctx->V));
+    cudaEvent_t pt = prof_begin(ctx);
+    launch_aos_to_soa((const float4*)ctx->payload, ctx->payload_soa, ctx->V, ctx->stream);
+    prof_end(ctx, kProfMapMisc, pt);
+  }
+#endif
   const DevGrid g = dev_grid(ctx);
   DevParams p;
   int rc = resolve_params(ctx, &cfg->render, &p);

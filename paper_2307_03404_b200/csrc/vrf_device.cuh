@@ -44,6 +44,10 @@ struct DevGrid {
   double inv_voxel;       // 1 / voxel (spatial gradient scale, voxel_grid.cpp:136)
   double rcp_voxel;       // RN(1 / voxel), host IEEE division (div_voxel)
   const float4* __restrict__ payload;  // [V][7]
+  // A/B only (-DVRF_GATHER_SOA): a channel-group-planar copy [7][soa_stride] of the
+  // payload that K0's gathers read instead (tools/ab/soa.sh)
+  const float4* __restrict__ soa;
+  long long soa_stride;
   const uint32_t* __restrict__ occ;    // 1 bit per cell, cell_index order
   // Coarse occupancy: 1 bit per block of kBlock^3 cells (any active cell -> 1);
   // lets the march jump over empty blocks without changing the sample set.
@@ -420,11 +424,17 @@ __device__ __forceinline__ void shade_fast(const DevGrid& g, const Sample& s, co
   float cr = 0.f, cg = 0.f, cb = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
+#ifdef VRF_GATHER_SOA
+    const float4* vp = g.soa + corner_index(g, s.base, k);
+    const long long js = g.soa_stride;
+#else
     const float4* vp = g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
+    constexpr long long js = 1;
+#endif
     float v[28];
 #pragma unroll
     for (int j = 0; j < kVec4PerVertex; ++j) {
-      const float4 a = __ldg(vp + j);
+      const float4 a = __ldg(vp + j * js);
       v[4 * j] = a.x;
       v[4 * j + 1] = a.y;
       v[4 * j + 2] = a.z;

@@ -86,11 +86,21 @@ void launch_map_backward_records(const DevGrid& g, const DevParams& p, const Dev
 void launch_segmented_reduce(const uint32_t* sorted_keys, const uint32_t* perm,
                              const double* values, long long nrec, double* grad_out_f64,
                              cudaStream_t s);
+// Log of the float4 groups an RMSProp pass updated (index, new theta, new v): the
+// drop-in's sparse write-back (vrf_updates_read). count == nullptr: off.
+struct UpdateLog {
+  uint32_t* ids = nullptr;
+  float4* theta = nullptr;
+  float4* v = nullptr;
+  unsigned long long* count = nullptr;
+  long long cap = 0;
+};
 // Block-sparse RMSProp over the touched 8^3-vertex blocks; clears the bitmap.
 void launch_rmsprop_blocks(float4* theta, float4* grad, float4* v, uint32_t* tb, int rx, int ry,
                            int rz, int tbx, int tby, int tbz, double rho, double lr_sigma,
                            double lr_sh, double eps, const MapStats* stats,
-                           unsigned long long* touched, cudaStream_t s);
+                           unsigned long long* touched, cudaStream_t s,
+                           const UpdateLog& log = UpdateLog{});
 // Block-sparse multi-GPU exchange (8^3-vertex blocks, packed [n][512][28] fp32; id < 0 = pad).
 void launch_touched_flags(const uint32_t* tb, int nb, uint8_t* flags, cudaStream_t s);
 void launch_blocks_pack(const float4* src, const int* ids, int n, int rx, int ry, int rz, int tbx,
@@ -114,7 +124,8 @@ void launch_blocks_apply(float4* theta, float4* v, const int* ids, int n, int rx
                          double lr_sh, double eps, cudaStream_t s);
 void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, long long v_end,
                     double rho, double lr_sigma, double lr_sh, double eps,
-                    const MapStats* stats, unsigned long long* touched, cudaStream_t s);
+                    const MapStats* stats, unsigned long long* touched, cudaStream_t s,
+                    const UpdateLog& log = UpdateLog{});
 // Tracking (vrf_track.cu).
 int pose_fused_blocks(int n);
 // kParityFp64: k_pose_group<double> (FP64 SH + Jacobian partials; pose_gradient,
@@ -144,6 +155,8 @@ void launch_pixel_order(const int* pixels, int n, uint32_t* keys, uint32_t* ids,
 
 // Utilities.
 void launch_fill_payload(float* payload, long long n_vertices, float sigma, cudaStream_t s);
+// A/B only: payload [V][7] float4 -> [7][V] (tools/ab/soa.sh)
+void launch_aos_to_soa(const float4* aos, float4* soa, long long nv, cudaStream_t s);
 void launch_f64_to_f32(const double* in, float* out, long long n, cudaStream_t s);
 void launch_f32_to_f64(const float* in, double* out, long long n, cudaStream_t s);
 void launch_pack_occupancy(const uint8_t* occ_u8, uint32_t* bits, long long n_cells,

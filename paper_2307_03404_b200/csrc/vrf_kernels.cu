@@ -213,7 +213,8 @@ __device__ __forceinline__ size_t rec_index(int t, int c, int K) {
 // gathers the 896 B of corner payload again. Records are warp-tiled
 // sample-major (rec_index): the lanes of a warp composite their c-th samples in
 // the same loop iteration, so each record store is one coalesced 768 B access.
-__global__ void __launch_bounds__(kThreads) k_map_forward_rec(
+// 4 CTAs/SM (128 registers): r01 measured 3 / 4 / 5 CTAs at 8.83 / 8.21 / 8.75 ms.
+__global__ void __launch_bounds__(kThreads, 4) k_map_forward_rec(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
     double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
@@ -1229,13 +1230,31 @@ __global__ void __launch_bounds__(kThreads) k_segmented_reduce(
 }
 
 // ------------------------------------------------------------------ K4 RMSProp
+// Appends an updated float4 group (its index and new theta / v) to the update
+// log the drop-in write-back reads (vrf_updates_read); warp-aggregated slot.
+__device__ __forceinline__ void log_update(const UpdateLog& log, long long f, float4 th,
+                                           float4 v4) {
+  const unsigned m = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(log.count, (unsigned long long)__popc(m));
+  base = __shfl_sync(m, base, leader);
+  const unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
+  if (pos < (unsigned long long)log.cap) {
+    log.ids[pos] = (uint32_t)f;
+    log.theta[pos] = th;
+    log.v[pos] = v4;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_rmsprop(float4* __restrict__ theta,
                                                  float4* __restrict__ grad,
                                                  float4* __restrict__ vstate, long long f_begin,
                                                  long long f_end, double rho, double lr_sigma,
                                                  double lr_sh, double eps,
                                                  const MapStats* __restrict__ stats,
-                                                 unsigned long long* __restrict__ touched) {
+                                                 unsigned long long* __restrict__ touched,
+                                                 UpdateLog log) {
   if (stats) {
     const MapStats st = *stats;
     if (st.bad != INT_MAX || st.m_c == 0) return;
@@ -1264,6 +1283,7 @@ __global__ void __launch_bounds__(256) k_rmsprop(float4* __restrict__ theta,
     theta[f] = th;
     vstate[f] = v4;
     grad[f] = zero;
+    if (log.count) log_update(log, f, th, v4);
   }
   if (touched) {  // float4 groups updated (algorithmic optimizer bytes: 96 B each)
     n_touched = warp_sum(n_touched);
@@ -1279,7 +1299,7 @@ __global__ void __launch_bounds__(256) k_rmsprop_blocks(
     float4* __restrict__ theta, float4* __restrict__ grad, float4* __restrict__ vstate,
     const uint32_t* __restrict__ tb, int rx, int ry, int rz, int tbx, int tby, double rho,
     double lr_sigma, double lr_sh, double eps, const MapStats* __restrict__ stats,
-    unsigned long long* __restrict__ touched) {
+    unsigned long long* __restrict__ touched, UpdateLog log) {
   const int b = blockIdx.x;
   if (!((tb[b >> 5] >> (b & 31)) & 1u)) return;
   if (stats) {
@@ -1314,6 +1334,7 @@ __global__ void __launch_bounds__(256) k_rmsprop_blocks(
     theta[f] = th;
     vstate[f] = v4;
     grad[f] = zero;
+    if (log.count) log_update(log, f, th, v4);
   }
   if (touched) {
     n_touched = warp_sum(n_touched);
@@ -1817,19 +1838,20 @@ void launch_segmented_reduce(const uint32_t* keys, const uint32_t* perm, const d
 }
 void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, long long v_end,
                     double rho, double lr_sigma, double lr_sh, double eps,
-                    const MapStats* stats, unsigned long long* touched, cudaStream_t s) {
+                    const MapStats* stats, unsigned long long* touched, cudaStream_t s,
+                    const UpdateLog& log) {
   const long long f0 = v_begin * kVec4PerVertex, f1 = v_end * kVec4PerVertex;
   if (f1 <= f0) return;
   k_rmsprop<<<grid_blocks(f1 - f0, 256), 256, 0, s>>>(theta, grad, v, f0, f1, rho, lr_sigma,
-                                                      lr_sh, eps, stats, touched);
+                                                      lr_sh, eps, stats, touched, log);
 }
 void launch_rmsprop_blocks(float4* theta, float4* grad, float4* v, uint32_t* tb, int rx, int ry,
                            int rz, int tbx, int tby, int tbz, double rho, double lr_sigma,
                            double lr_sh, double eps, const MapStats* stats,
-                           unsigned long long* touched, cudaStream_t s) {
+                           unsigned long long* touched, cudaStream_t s, const UpdateLog& log) {
   const int nb = tbx * tby * tbz;
   k_rmsprop_blocks<<<nb, 256, 0, s>>>(theta, grad, v, tb, rx, ry, rz, tbx, tby, rho, lr_sigma,
-                                      lr_sh, eps, stats, touched);
+                                      lr_sh, eps, stats, touched, log);
   cudaMemsetAsync(tb, 0, sizeof(uint32_t) * ((nb + 31) / 32 + 1), s);
 }
 void launch_touched_flags(const uint32_t* tb, int nb, uint8_t* flags, cudaStream_t s) {
@@ -1862,6 +1884,16 @@ void launch_exchange_p2p(const PeerTable& pt, float4* v, int nb, int rx, int ry,
   if (grid > 0)
     k_exchange_p2p<<<grid, 256, 0, s>>>(pt, v, nb, rx, ry, rz, tbx, tby, rho, lr_sigma, lr_sh, eps,
                                         stats);
+}
+__global__ void k_aos_to_soa(const float4* __restrict__ aos, float4* __restrict__ soa,
+                             long long nv) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv * kVec4PerVertex) return;
+  const long long v = i / kVec4PerVertex, j = i % kVec4PerVertex;
+  soa[j * nv + v] = aos[i];
+}
+void launch_aos_to_soa(const float4* aos, float4* soa, long long nv, cudaStream_t s) {
+  k_aos_to_soa<<<grid_blocks(nv * kVec4PerVertex, 256), 256, 0, s>>>(aos, soa, nv);
 }
 void launch_fill_payload(float* payload, long long nv, float sigma, cudaStream_t s) {
   k_fill_payload<<<grid_blocks(nv * kPayload, 256), 256, 0, s>>>(payload, nv, sigma);

@@ -175,7 +175,29 @@ void launch_backward_fast(vrf_context* ctx, const vrf_mapping_config* cfg, const
 
 // K4 over the whole grid, or block-sparse when the fast scatter marked every
 // touched block of this gradient (ctx->touched_valid).
-void launch_rmsprop_step(vrf_context* ctx, const vrf_mapping_config* cfg) {
+// The update log (drop-in write-back): one slot per float4 group of the grid.
+int update_log(vrf_context* ctx, UpdateLog* log) {
+  *log = UpdateLog{};
+  if (!ctx->log_updates) return VRF_OK;
+  const size_t groups = (size_t)ctx->V * kVec4PerVertex;
+  int rc;
+  if ((rc = ensure(ctx, ctx->s_upd_ids, sizeof(uint32_t) * groups))) return rc;
+  if ((rc = ensure(ctx, ctx->s_upd_theta, sizeof(float4) * groups))) return rc;
+  if ((rc = ensure(ctx, ctx->s_upd_v, sizeof(float4) * groups))) return rc;
+  if (!ctx->d_upd_count) CU(cudaMalloc(&ctx->d_upd_count, sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(ctx->d_upd_count, 0, sizeof(unsigned long long), ctx->stream));
+  log->ids = (uint32_t*)ctx->s_upd_ids.ptr;
+  log->theta = (float4*)ctx->s_upd_theta.ptr;
+  log->v = (float4*)ctx->s_upd_v.ptr;
+  log->count = ctx->d_upd_count;
+  log->cap = (long long)groups;
+  return VRF_OK;
+}
+
+int launch_rmsprop_step(vrf_context* ctx, const vrf_mapping_config* cfg) {
+  UpdateLog log;
+  int rc = update_log(ctx, &log);
+  if (rc) return rc;
   cudaEvent_t pr = prof_begin(ctx);
   static const bool force_full = std::getenv("VRF_RMSPROP_FULL") != nullptr;  // A/B, tests
   if (ctx->touched_valid && !force_full) {
@@ -183,17 +205,18 @@ void launch_rmsprop_step(vrf_context* ctx, const vrf_mapping_config* cfg) {
                           ctx->geom.res[0], ctx->geom.res[1], ctx->geom.res[2], ctx->tdim[0],
                           ctx->tdim[1], ctx->tdim[2], cfg->rmsprop_decay, cfg->lr_sigma,
                           cfg->lr_sh, cfg->rmsprop_eps, ctx->d_stats,
-                          ctx->profiling ? ctx->d_touched : nullptr, ctx->stream);
+                          ctx->profiling ? ctx->d_touched : nullptr, ctx->stream, log);
   } else {
     launch_rmsprop((float4*)ctx->payload, (float4*)ctx->grad, (float4*)ctx->rms, 0, ctx->V,
                    cfg->rmsprop_decay, cfg->lr_sigma, cfg->lr_sh, cfg->rmsprop_eps, ctx->d_stats,
-                   ctx->profiling ? ctx->d_touched : nullptr, ctx->stream);
+                   ctx->profiling ? ctx->d_touched : nullptr, ctx->stream, log);
     const long long ntb = (long long)ctx->tdim[0] * ctx->tdim[1] * ctx->tdim[2];
     cudaMemsetAsync(ctx->tb, 0, sizeof(uint32_t) * ((ntb + 31) / 32 + 1), ctx->stream);
   }
   ctx->touched_valid = false;
   prof_end(ctx, kProfRmsprop, pr);
   LAUNCHED(1);
+  return VRF_OK;
 }
 
 // Fills ctx->grad (fp32) with this batch's gradient. Deterministic mode goes
@@ -246,7 +269,7 @@ int step_impl(vrf_context* ctx, const vrf_mapping_config* cfg, const int* batch_
     if ((rc = map_gradient(ctx, cfg, batch_dev, n, &st, false))) return rc;
   }
   // K4: RMSProp over the touched groups (g != 0 == the reference's touched set).
-  launch_rmsprop_step(ctx, cfg);
+  if ((rc = launch_rmsprop_step(ctx, cfg))) return rc;
   CU(cudaGetLastError());
   if ((rc = check_err_flag(ctx))) return rc;
   if ((rc = read_stats(ctx, &st))) return rc;
@@ -321,7 +344,7 @@ int vrf_mapping_steps(vrf_context* ctx, const vrf_mapping_config* cfg, uint64_t 
     const int c = i & 1;
     CU(cudaMemcpyAsync((void*)db[c], hb[c], bbytes, cudaMemcpyHostToDevice, ctx->stream));
     if ((rc = map_gradient(ctx, cfg, db[c], n_rays, nullptr, false))) return rc;
-    launch_rmsprop_step(ctx, cfg);
+    if ((rc = launch_rmsprop_step(ctx, cfg))) return rc;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(h_st, ctx->d_stats, sizeof(MapStats), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(h_err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -543,6 +566,68 @@ int vrf_map_apply(vrf_context* ctx, const vrf_mapping_config* cfg, int64_t verte
   LAUNCHED(1);
   CU(cudaGetLastError());
   return VRF_OK;
+}
+
+// ---- drop-in residency: partial uploads and the update log (integration/)
+int vrf_track_updates(vrf_context* ctx, int on) {
+  ctx->log_updates = on != 0;
+  return VRF_OK;
+}
+
+int vrf_updates_count(vrf_context* ctx, int64_t* n) {
+  cudaSetDevice(ctx->device);
+  unsigned long long c = 0;
+  if (ctx->log_updates && ctx->d_upd_count) {
+    CU(cudaMemcpyAsync(&c, ctx->d_upd_count, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  *n = (int64_t)c;
+  return VRF_OK;
+}
+
+int vrf_updates_read(vrf_context* ctx, int64_t n, uint32_t* ids, float* theta, float* v) {
+  cudaSetDevice(ctx->device);
+  if (!ctx->log_updates || n <= 0) return VRF_OK;
+  if (n > (int64_t)(ctx->V * kVec4PerVertex))
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_updates_read: count exceeds the grid");
+  CU(cudaMemcpyAsync(ids, ctx->s_upd_ids.ptr, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(theta, ctx->s_upd_theta.ptr, sizeof(float4) * n, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(v, ctx->s_upd_v.ptr, sizeof(float4) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+namespace {
+int write_vertices(vrf_context* ctx, float* dst, int64_t first, int64_t count, const double* src,
+                   const char* what) {
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if (first < 0 || count < 0 || first + count > ctx->V)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, std::string(what) + ": vertex range");
+  const long long total = count * 28, chunk = 4LL << 20;
+  if ((rc = ensure(ctx, ctx->s_out, sizeof(double) * chunk))) return rc;
+  for (long long off = 0; off < total; off += chunk) {
+    const long long n = std::min(chunk, total - off);
+    CU(cudaMemcpyAsync(ctx->s_out.ptr, src + off, sizeof(double) * n, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    launch_f64_to_f32((const double*)ctx->s_out.ptr, dst + first * 28 + off, n, ctx->stream);
+    LAUNCHED(1);
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+}  // namespace
+
+int vrf_grid_write_vertices(vrf_context* ctx, int64_t first, int64_t count, const double* data) {
+  cudaSetDevice(ctx->device);
+  return write_vertices(ctx, ctx->payload, first, count, data, "vrf_grid_write_vertices");
+}
+
+int vrf_rmsprop_write_vertices(vrf_context* ctx, int64_t first, int64_t count, const double* v) {
+  cudaSetDevice(ctx->device);
+  return write_vertices(ctx, ctx->rms, first, count, v, "vrf_rmsprop_write_vertices");
 }
 
 }  // extern "C"

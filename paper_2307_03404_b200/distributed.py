@@ -60,6 +60,10 @@ class GpuEngine:
         self.num_vertices = int(b.num_vertices)
         self.padded = int(b.padded_vertices)
         dev = torch.device("cuda", ctx.device)
+        # the NCCL collectives run on torch's current stream: the context's kernels
+        # must run on that same stream, or a reduce-scatter could read the gradient
+        # before map_backward has finished writing it
+        ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
         self.grad = torch.as_tensor(_CudaArray(b.grad, self.padded * 28), device=dev)
         self.payload = torch.as_tensor(_CudaArray(b.payload, self.padded * 28), device=dev)
 

@@ -20,8 +20,8 @@ def test_dropin_binary_against_reference():
     assert BIN.exists(), "integration/_build/voxrf_dropin_tests missing: run __graft_entry__.build()"
     r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
-    # 45 reference cases + 4 drop-in cases; the single expected failure is the
+    # 45 reference cases + 7 drop-in cases; the single expected failure is the
     # reference's own float-vs-double check at test_renderer.cpp:295-296.
-    assert "test cases: 50 | 49 passed | 1 failed" in r.stdout, out[-4000:]
+    assert "test cases: 52 | 51 passed | 1 failed" in r.stdout, out[-4000:]
     bad = [ln for ln in r.stderr.splitlines() if "ERROR:" in ln]
     assert all("test_renderer.cpp:295" in ln or "test_renderer.cpp:296" in ln for ln in bad), out[-4000:]
