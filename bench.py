@@ -577,7 +577,7 @@ def run_ours(args):
                                              "warp_instructions", "registers")}
                     if nk else None),
         "launches": k_n, "kernel_ms": {k: v[0] for k, v in kern.items()},
-        "other_ms": {k: prof[k][0] for k in ("map_misc",) if k in prof},
+        "other_ms": {k: prof[k][0] for k in ("misc",) if k in prof},
         "step_algorithmic_GBps": step_bytes / (ms / 1e3) / 1e9,
         "step_algorithmic_frac": step_bytes / (ms / 1e3) / 1e9 / peak,
     }

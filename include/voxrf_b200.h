@@ -231,6 +231,12 @@ int vrf_grid_save(vrf_context* ctx, const char* path);
 int vrf_grid_load(vrf_context* ctx, const char* path);
 /* VoxelGrid::prune(tau) — voxel_grid.cpp:169-188. */
 int vrf_grid_prune(vrf_context* ctx, double tau, int64_t* deactivated);
+/* Device-side integrity digest of the grid (geometry, fp32 payload, occupancy
+ * bits): an order-independent 64-bit hash computed in one pass over HBM. Used to
+ * check that tracking and rendering never mutate the grid without
+ * a download; VoxelGrid::checksum (voxel_grid.cpp:280-292, FNV-1a over the fp64
+ * bytes) stays a host computation on a downloaded grid. */
+int vrf_grid_digest(vrf_context* ctx, uint64_t* out);
 
 /* ---- drop-in residency (integration/voxrf_gpu_backend.cpp keeps the device grid in
  * step with a caller's VoxelGrid without whole-grid copies per call):

@@ -26,6 +26,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "voxrf/mapping.hpp"
@@ -239,13 +240,23 @@ void write_back(VoxelGrid& grid, RmspropState& st) {
     th.resize(4 * std::size_t(n));
     vv.resize(4 * std::size_t(n));
     check(vrf_updates_read(ctx(), n, ids.data(), th.data(), vv.data()));
-    for (std::int64_t i = 0; i < n; ++i) {
-      const std::size_t o = 4 * std::size_t(ids[std::size_t(i)]);  // == vertex * 28 + 4 group
-      for (int e = 0; e < 4; ++e) {
-        d[o + e] = th[4 * std::size_t(i) + e];
-        v[o + e] = vv[4 * std::size_t(i) + e];
+    // scatter into the caller's fp64 buffers (random access: split over threads;
+    // the logged groups are distinct, so the chunks never write the same element)
+    auto scatter = [&](std::int64_t i0, std::int64_t i1) {
+      for (std::int64_t i = i0; i < i1; ++i) {
+        const std::size_t o = 4 * std::size_t(ids[std::size_t(i)]);  // == vertex * 28 + 4 group
+        for (int e = 0; e < 4; ++e) {
+          d[o + e] = th[4 * std::size_t(i) + e];
+          v[o + e] = vv[4 * std::size_t(i) + e];
+        }
       }
-    }
+    };
+    const int nt = n < (1 << 16) ? 1 : int(std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency())));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t)
+      pool.emplace_back(scatter, n * t / nt, n * (t + 1) / nt);
+    scatter(0, n / nt);
+    for (auto& th_ : pool) th_.join();
     g_res.back_bytes += std::size_t(n) * (4 + 32);
   }
   HostMirror::clean(d);

@@ -147,6 +147,7 @@ _SIGS = {
     "vrf_grid_download_f32": (C.c_int, [vp, vp]),
     "vrf_grid_get_geometry": (C.c_int, [vp, P(GridGeometry_c)]),
     "vrf_grid_prune": (C.c_int, [vp, C.c_double, P(C.c_int64)]),
+    "vrf_grid_digest": (C.c_int, [vp, P(C.c_uint64)]),
     "vrf_grid_upsample": (C.c_int, [vp, C.c_int]),
     "vrf_grid_save": (C.c_int, [vp, C.c_char_p]),
     "vrf_grid_load": (C.c_int, [vp, C.c_char_p]),

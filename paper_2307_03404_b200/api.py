@@ -486,6 +486,12 @@ class Context:
         self._check(self._lib.vrf_grid_download(self._h, _ptr(grid.data), _ptr(grid.active)))
         return grid
 
+    def grid_digest(self) -> int:
+        """Device-side integrity digest of the resident grid (vrf_grid_digest)."""
+        out = C.c_uint64()
+        self._check(self._lib.vrf_grid_digest(self._h, C.byref(out)))
+        return int(out.value)
+
     def download_payload_f32(self) -> np.ndarray:
         out = np.empty((self.geom.num_vertices, PAYLOAD), dtype=np.float32)
         self._check(self._lib.vrf_grid_download_f32(self._h, _ptr(out)))

@@ -47,6 +47,7 @@ void vrf_context_destroy(vrf_context* ctx) {
   cudaFree(ctx->d_pose);
   cudaFree(ctx->d_touched);
   cudaFree(ctx->d_upd_count);
+  cudaFree(ctx->d_digest);
   cudaFree(ctx->payload_soa);
   cudaFree(ctx->d_nblocks);
   cudaFree(ctx->d_frame);
@@ -202,6 +203,32 @@ int vrf_grid_upload(vrf_context* ctx, const vrf_grid_geometry* geom, const doubl
   if ((rc = upload_occupancy_u8(ctx, occupancy))) return rc;
   update_blocks(ctx);
   CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+// A cheap device-side grid-integrity check (tracking never mutates
+// the grid; voxel_grid.cpp:280-292's FNV-1a checksum is sequential over the fp64
+// bytes and stays host-side). Covers the geometry, the fp32 payload and the
+// occupancy bits.
+int vrf_grid_digest(vrf_context* ctx, uint64_t* out) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  if (!ctx->d_digest) CU(cudaMalloc(&ctx->d_digest, sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(ctx->d_digest, 0, sizeof(unsigned long long), ctx->stream));
+  launch_digest((const uint32_t*)ctx->payload, ctx->V * 28, 0x5041594c4f4144ULL, ctx->d_digest,
+                ctx->stream);
+  launch_digest(ctx->occ, (ctx->C + 31) / 32, 0x4f43435550ULL, ctx->d_digest, ctx->stream);
+  LAUNCHED(2);
+  unsigned long long h = 0;
+  CU(cudaMemcpyAsync(&h, ctx->d_digest, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  // fold in the geometry
+  const vrf_grid_geometry& gm = ctx->geom;
+  uint64_t x = h;
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(&gm);
+  for (size_t k = 0; k < sizeof(gm); ++k) x = (x ^ p[k]) * 0x100000001b3ULL;
+  *out = x;
   return VRF_OK;
 }
 

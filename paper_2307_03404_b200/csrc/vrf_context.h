@@ -48,6 +48,7 @@ struct vrf_context {
   uint32_t* socc = nullptr;  // 64^3-cell superblock occupancy
   int sdim[3] = {0, 0, 0};
   uint32_t* tb = nullptr;    // touched 8^3-vertex blocks of the pending gradient
+  uint32_t* tc = nullptr;    // touched 8^3-cell blocks marked by the scatter (-> tb)
   // fused peer-memory exchange (vrf_peers_set / vrf_peers_open_ipc / vrf_exchange_p2p)
   vrf::PeerTable peers{};
   bool peers_set = false;
@@ -89,6 +90,7 @@ struct vrf_context {
   bool log_updates = false;
   vrf_host::DeviceScratch s_upd_ids, s_upd_theta, s_upd_v;
   unsigned long long* d_upd_count = nullptr;
+  unsigned long long* d_digest = nullptr;
   double rec_budget_gb = -1.0;   // vrf_set_record_limits: <= 0 automatic (30 % of free HBM)
   int rec_max_k = -1;            // vrf_set_record_limits: < 0 automatic, 0 no records
 
@@ -208,6 +210,8 @@ inline void free_grid(vrf_context* ctx) {
   cudaFree(ctx->bocc);
   cudaFree(ctx->socc);
   cudaFree(ctx->tb);
+  cudaFree(ctx->tc);
+  ctx->tc = nullptr;
   ctx->payload = ctx->grad = ctx->rms = nullptr;
   ctx->occ = nullptr;
   ctx->bocc = nullptr;
@@ -248,6 +252,8 @@ inline int alloc_grid(vrf_context* ctx, const vrf_grid_geometry* g) {
     ctx->bdim[a] = (g->res[a] - 1 + (1 << kBlockLog2) - 1) >> kBlockLog2;
   const long long nblk = (long long)ctx->bdim[0] * ctx->bdim[1] * ctx->bdim[2];
   CU(cudaMalloc(&ctx->bocc, sizeof(uint32_t) * ((nblk + 31) / 32 + 1)));
+  CU(cudaMalloc(&ctx->tc, sizeof(uint32_t) * ((nblk + 31) / 32 + 1)));
+  CU(cudaMemsetAsync(ctx->tc, 0, sizeof(uint32_t) * ((nblk + 31) / 32 + 1), ctx->stream));
   constexpr int kS = kSuperLog2 - kBlockLog2;
   for (int a = 0; a < 3; ++a) ctx->sdim[a] = (ctx->bdim[a] + (1 << kS) - 1) >> kS;
   const long long nsup = (long long)ctx->sdim[0] * ctx->sdim[1] * ctx->sdim[2];
@@ -298,6 +304,7 @@ inline DevGrid dev_grid(const vrf_context* ctx) {
   g.sy = ctx->sdim[1];
   g.sz = ctx->sdim[2];
   g.tb = ctx->tb;
+  g.tc = ctx->tc;
   g.tbx = ctx->tdim[0];
   g.tby = ctx->tdim[1];
   g.tbz = ctx->tdim[2];
@@ -469,7 +476,12 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
     // at least doubles K, so steps do not reallocate. Longer rays overflow to
     // the recompute-march backward.
     ctx->rec_K = 0;
-    if (ctx->rec_max_k != 0) {
+    // records carry 10-bit cell coordinates: larger grids take the recompute-march
+    // backward (no records)
+    const bool rec_fits = ctx->geom.res[0] - 1 <= kRecMaxCells &&
+                          ctx->geom.res[1] - 1 <= kRecMaxCells &&
+                          ctx->geom.res[2] - 1 <= kRecMaxCells;
+    if (ctx->rec_max_k != 0 && rec_fits) {
       const double env_gb = ctx->rec_budget_gb > 0.0 ? ctx->rec_budget_gb : -1.0;
       long long need = 1024;
       if (ctx->max_ray_samples > 0) {

@@ -57,40 +57,31 @@ struct DevGrid {
   // Second level: 1 bit per superblock of 8^3 blocks (64^3 cells).
   const uint32_t* __restrict__ socc;
   int sx, sy, sz;
-  // Touched vertex blocks (8^3 vertices): set by the fast scatter, consumed
-  // (and cleared) by the block-sparse RMSProp.
+  // Touched vertex blocks (8^3 vertices), consumed (and cleared) by the
+  // block-sparse RMSProp and the multi-GPU exchanges; derived after each scatter
+  // from the touched CELL blocks (8^3 cells, the bocc grid) the scatter marks.
   uint32_t* tb;
   int tbx, tby, tbz;
+  uint32_t* tc;
 };
 
 constexpr int kBlockLog2 = 3;  // 8^3-cell blocks
 constexpr int kSuperLog2 = 6;  // 64^3-cell superblocks
 constexpr int kTouchLog2 = 3;  // 8^3-vertex touched blocks
 
-// Marks the touched blocks of every corner vertex of cell (cx, cy, cz): the
-// cell's own block, plus the +1 neighbours when a corner sits on the block's
-// upper face. `last` caches the last interior block id to skip repeats; the
-// atomic is skipped when the bit is already set.
+// Marks the 8^3-cell block of cell (cx, cy, cz) as touched by the scatter (the
+// vertex blocks its corners fall in are derived after the pass, k_touched_dilate:
+// a cell block's vertices span its own vertex block and the +x/+y/+z neighbours).
+// `last` caches the last block id to skip repeats; the atomic is skipped when the
+// bit is already set.
 __device__ __forceinline__ void mark_touched(const DevGrid& g, int cx, int cy, int cz, int& last) {
-  constexpr int M = (1 << kTouchLog2) - 1;
-  const int bx = cx >> kTouchLog2, by = cy >> kTouchLog2, bz = cz >> kTouchLog2;
-  const int ex = (cx & M) == M, ey = (cy & M) == M, ez = (cz & M) == M;
-  const int id = bx + g.tbx * (by + g.tby * bz);
-  // a cell on the +x/+y/+z face layer of its block also owns vertices of the
-  // next block(s): the key carries the edge flags, so runs of cells in the same
-  // (block, face layer) are marked once
-  const int key = (id << 3) | ex | (ey << 1) | (ez << 2);
-  if (key == last) return;
-  last = key;
-  for (int dz = 0; dz <= ez; ++dz)
-    for (int dy = 0; dy <= ey; ++dy)
-      for (int dx = 0; dx <= ex; ++dx) {
-        const int b = (bx + dx) + g.tbx * ((by + dy) + g.tby * (bz + dz));
-        const uint32_t bit = 1u << (b & 31);
-        // L1-cached check: bits are only ever set during the pass, so a stale
-        // word can only cost a redundant atomicOr, never a missed mark
-        if (!(__ldca(g.tb + (b >> 5)) & bit)) atomicOr(g.tb + (b >> 5), bit);
-      }
+  const int b = (cx >> kBlockLog2) + g.bx * ((cy >> kBlockLog2) + g.by * (cz >> kBlockLog2));
+  if (b == last) return;
+  last = b;
+  const uint32_t bit = 1u << (b & 31);
+  // L1-cached check: bits are only ever set during the pass, so a stale word can
+  // only cost a redundant atomicOr, never a missed mark
+  if (!(__ldca(g.tc + (b >> 5)) & bit)) atomicOr(g.tc + (b >> 5), bit);
 }
 
 // RenderParams after effective_step / effective_t_far (renderer.hpp:18-24).
@@ -386,6 +377,11 @@ struct GroupMarch {
     s.fy = __shfl_sync(gmask, mine.fy, src);
     s.fz = __shfl_sync(gmask, mine.fz, src);
     s.base = __shfl_sync(gmask, mine.base, src);
+    const uint32_t cpk = __shfl_sync(gmask, (uint32_t)mine.cx | ((uint32_t)mine.cy << 10) |
+                                                ((uint32_t)mine.cz << 20), src);
+    s.cx = (int)(cpk & 1023u);
+    s.cy = (int)((cpk >> 10) & 1023u);
+    s.cz = (int)(cpk >> 20);
     seg = __shfl_sync(gmask, mine_k, src);
     return true;
   }
@@ -425,8 +421,10 @@ __device__ __forceinline__ void shade_fast(const DevGrid& g, const Sample& s, co
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
 #ifdef VRF_GATHER_SOA
-    const float4* vp = g.soa + corner_index(g, s.base, k);
-    const long long js = g.soa_stride;
+    // (contexts that never ran a mapping forward have no planar copy: AoS)
+    const float4* vp = g.soa ? g.soa + corner_index(g, s.base, k)
+                             : g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
+    const long long js = g.soa ? g.soa_stride : 1;
 #else
     const float4* vp = g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
     constexpr long long js = 1;

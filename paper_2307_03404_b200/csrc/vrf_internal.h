@@ -29,15 +29,24 @@ struct PosePartial {
 
 enum FlagBits : uint8_t { kHit = 1, kDepthValid = 2, kOverflow = 4 };
 
-// Per-sample record of the fast mapping forward (24 B), consumed by the
-// reverse-order backward: weight w_i, T_{i+1}, clamped colour, and
-// kf = (segment index << 4) | clamp bits (0-2) | sigma_raw > 0 (bit 3).
+// Per-sample record of the fast mapping forward (32 B, two float4), consumed by
+// the reverse-order backward: weight w_i, T_{i+1}, clamped colour,
+// kf = (segment index << 4) | clamp bits (0-2) | sigma_raw > 0 (bit 3), the
+// sample's cell (cx | cy << 10 | cz << 20, located in FP64 by the forward) and
+// its segment midpoint t (fp32). The backward re-derives only the trilinear
+// weights, in fp32 (r02; r01's 24 B record re-located the cell in FP64).
 struct SampleRec {
-  float w, tn, c0, c1, c2;
-  uint32_t kf;
+  float w, tn, c0, c1;
+  float c2;
+  uint32_t kf, cell;
+  float tm;
 };
-static_assert(sizeof(SampleRec) == 24, "SampleRec layout");
+static_assert(sizeof(SampleRec) == 32, "SampleRec layout");
 constexpr uint32_t kRecSigmaPos = 8;
+constexpr int kRecMaxCells = 1024;  // per axis (10-bit cell coordinates in the record)
+__host__ __device__ __forceinline__ uint32_t pack_cell(int cx, int cy, int cz) {
+  return (uint32_t)cx | ((uint32_t)cy << 10) | ((uint32_t)cz << 20);
+}
 
 // Launchers (vrf_kernels.cu). All take the context stream.
 void launch_render_image(const DevGrid& g, const DevParams& p, const DevCam& cam,
@@ -103,6 +112,10 @@ void launch_rmsprop_blocks(float4* theta, float4* grad, float4* v, uint32_t* tb,
                            const UpdateLog& log = UpdateLog{});
 // Block-sparse multi-GPU exchange (8^3-vertex blocks, packed [n][512][28] fp32; id < 0 = pad).
 void launch_touched_flags(const uint32_t* tb, int nb, uint8_t* flags, cudaStream_t s);
+// Touched cell blocks (marked by the scatter) -> touched vertex blocks (ORed into
+// tb); clears tc.
+void launch_touched_dilate(uint32_t* tc, int bx, int by, int bz, uint32_t* tb, int tbx, int tby,
+                           int tbz, cudaStream_t s);
 void launch_blocks_pack(const float4* src, const int* ids, int n, int rx, int ry, int rz, int tbx,
                         int tby, float4* out, cudaStream_t s);
 void launch_blocks_unpack(float4* dst, const int* ids, int n, int rx, int ry, int rz, int tbx,
@@ -155,6 +168,9 @@ void launch_pixel_order(const int* pixels, int n, uint32_t* keys, uint32_t* ids,
 
 // Utilities.
 void launch_fill_payload(float* payload, long long n_vertices, float sigma, cudaStream_t s);
+// Order-independent 64-bit digest of n 32-bit words, added into *out.
+void launch_digest(const uint32_t* words, long long n, uint64_t salt, unsigned long long* out,
+                   cudaStream_t s);
 // A/B only: payload [V][7] float4 -> [7][V] (tools/ab/soa.sh)
 void launch_aos_to_soa(const float4* aos, float4* soa, long long nv, cudaStream_t s);
 void launch_f64_to_f32(const double* in, float* out, long long n, cudaStream_t s);

@@ -268,10 +268,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_map_forward_rec(
             const uint32_t kf = ((uint32_t)(m.k - 1) << 4) | (sh.clamped[0] ? 1u : 0u) |
                                 (sh.clamped[1] ? 2u : 0u) | (sh.clamped[2] ? 4u : 0u) |
                                 (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
-            float2* d = reinterpret_cast<float2*>(rec + rec_index(t, st.count - 1, K));
-            d[0] = make_float2((float)wgt, (float)st.T);
-            d[1] = make_float2((float)sh.c[0], (float)sh.c[1]);
-            d[2] = make_float2((float)sh.c[2], __uint_as_float(kf));
+            float4* d = reinterpret_cast<float4*>(rec + rec_index(t, st.count - 1, K));
+            d[0] = make_float4((float)wgt, (float)st.T, (float)sh.c[0], (float)sh.c[1]);
+            d[1] = make_float4((float)sh.c[2], __uint_as_float(kf),
+                               __uint_as_float(pack_cell(s.cx, s.cy, s.cz)), (float)s.t);
           }
           if (st.terminated) break;
         }
@@ -539,10 +539,10 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
             const uint32_t kf = ((uint32_t)gm.seg << 4) | (sh.clamped[0] ? 1u : 0u) |
                                 (sh.clamped[1] ? 2u : 0u) | (sh.clamped[2] ? 4u : 0u) |
                                 (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
-            float2* d = reinterpret_cast<float2*>(rec + rec_index(t, st.count - 1, K));
-            d[0] = make_float2((float)wgt, (float)st.T);
-            d[1] = make_float2((float)sh.c[0], (float)sh.c[1]);
-            d[2] = make_float2((float)sh.c[2], __uint_as_float(kf));
+            float4* d = reinterpret_cast<float4*>(rec + rec_index(t, st.count - 1, K));
+            d[0] = make_float4((float)wgt, (float)st.T, (float)sh.c[0], (float)sh.c[1]);
+            d[1] = make_float4((float)sh.c[2], __uint_as_float(kf),
+                               __uint_as_float(pack_cell(s.cx, s.cy, s.cz)), (float)s.t);
           }
           if (st.terminated) break;
         }
@@ -623,6 +623,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
 // active lanes, ncu v23.)
 struct CornerAgg {
   float a[4][8];  // slot s: logical corner s ^ X of the current cell
+  uint32_t nz;    // slots that may hold a nonzero sum (free-space samples add zeros)
   uint32_t X;
   uint32_t base;  // vertex_index of the current cell; kNoCell before the first
   int cx, cy, cz;
@@ -634,6 +635,7 @@ __device__ __forceinline__ void agg_init(CornerAgg& A) {
   for (int c = 0; c < 4; ++c)
 #pragma unroll
     for (int k = 0; k < 8; ++k) A.a[c][k] = 0.f;
+  A.nz = 0;
   A.X = 0;
   A.base = kNoCell;
   A.cx = A.cy = A.cz = 0;
@@ -648,14 +650,16 @@ __device__ __forceinline__ uint32_t corner_off(const DevGrid& g, uint32_t k) {
 template <typename Sink>
 __device__ __forceinline__ void agg_flush(CornerAgg& A, Sink& sink, const DevGrid& g,
                                           uint32_t slots) {
+  // all-zero corners add nothing and are not flushed: a slot is nonzero only if a
+  // sample with a nonzero upstream reached it since it was last flushed (free-
+  // space samples with sigma_raw <= 0 carry w = 0 and a gated dL/dsigma)
+  const uint32_t live = slots & A.nz;
+  A.nz &= ~slots;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    if (slots & (1u << s)) {
-      // all-zero corners (samples in free space with sigma_raw <= 0 carry w = 0
-      // and a gated dL/dsigma) add nothing: not flushed
-      if (A.a[0][s] != 0.f || A.a[1][s] != 0.f || A.a[2][s] != 0.f || A.a[3][s] != 0.f)
-        sink(A.base + corner_off(g, (uint32_t)s ^ A.X), A.a[0][s], A.a[1][s], A.a[2][s],
-             A.a[3][s]);
+    if (live & (1u << s)) {
+      sink(A.base + corner_off(g, (uint32_t)s ^ A.X), A.a[0][s], A.a[1][s], A.a[2][s],
+           A.a[3][s]);
       A.a[0][s] = A.a[1][s] = A.a[2][s] = A.a[3][s] = 0.f;
     }
   }
@@ -692,6 +696,7 @@ __device__ __forceinline__ bool agg_enter(CornerAgg& A, Sink& sink, const DevGri
 // Adds a sample's (u_sigma, u_r, u_g, u_b) with trilinear weights (fx, fy, fz).
 __device__ __forceinline__ void agg_add(CornerAgg& A, float fx, float fy, float fz, float u0,
                                         float u1, float u2, float u3) {
+  if (u0 != 0.f || u1 != 0.f || u2 != 0.f || u3 != 0.f) A.nz = 0xffu;
   const bool sx = A.X & 1u, sy = (A.X >> 1) & 1u, sz = (A.X >> 2) & 1u;
   const float gx = 1.f - fx, gy = 1.f - fy, gz = 1.f - fz;
   const float wx[2] = {sx ? fx : gx, sx ? gx : fx};
@@ -813,50 +818,93 @@ __global__ void __launch_bounds__(kThreads, 4) k_map_backward(
   map_backward_fast<SKIP>(g, p, m, u, grad);
 }
 
-// One record of the reverse walk, decoded: the sample's position is re-derived
-// exactly from the stored segment index (renderer.cpp:66-73: s0 = lo + k step,
-// midpoint, locate — FP64, the forward's arithmetic), so the cell and trilinear
-// weights are the forward's.
+// The ray as the record walk needs it (fp32): origin, direction, segment end
+// and step, and the grid origin / inverse voxel for the trilinear weights.
+struct WalkRay {
+  float o[3], d[3];
+  float hi, step;
+};
+__device__ __forceinline__ WalkRay walk_ray(const March& m) {
+  WalkRay w;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    w.o[a] = (float)m.o[a];
+    w.d[a] = (float)m.d[a];
+  }
+  w.hi = (float)m.hi;
+  w.step = (float)m.step;
+  return w;
+}
+
+// One record of the reverse walk, decoded. The cell comes from the record (the
+// forward located it in FP64 with the reference's arithmetic), so the scatter
+// targets exactly the forward's corners; the trilinear weights are re-derived in
+// fp32 from the stored segment midpoint (weight error ~1e-5, far inside the fast
+// path's 1e-3 gradient bar), and delta is the step except on the segment
+// clipped at t_far, where s1 = hi gives delta = 2 (hi - t_mid).
 struct RecSample {
-  Sample s;
-  double tm, delta, w, Tn, c0, c1, c2;
+  int cx, cy, cz;
+  uint32_t base;
+  float fx, fy, fz;
+  float tm, delta, w, Tn, c0, c1, c2;
   uint32_t kf;
 };
-__device__ __forceinline__ void decode_record(const DevGrid& g, const March& m, float2 q0,
-                                              float2 q1, float2 q2, RecSample& r) {
-  r.kf = __float_as_uint(q2.y);
-  const double kseg = (double)(r.kf >> 4);
-  const double s0 = dadd(m.lo, dmul(kseg, m.step));
-  const double s0s = dadd(s0, m.step);
-  const double s1 = (m.hi < s0s) ? m.hi : s0s;
-  r.delta = dsub(s1, s0);
-  r.tm = dmul(0.5, dadd(s0, s1));
-  const double pp[3] = {dadd(m.o[0], dmul(r.tm, m.d[0])), dadd(m.o[1], dmul(r.tm, m.d[1])),
-                        dadd(m.o[2], dmul(r.tm, m.d[2]))};
-  locate(g, pp, r.s);
-  r.w = (double)q0.x;
-  r.Tn = (double)q0.y;
-  r.c0 = (double)q1.x;
-  r.c1 = (double)q1.y;
-  r.c2 = (double)q2.x;
+__device__ __forceinline__ void decode_record(const DevGrid& g, const WalkRay& m, float4 q0,
+                                              float4 q1, RecSample& r) {
+  r.w = q0.x;
+  r.Tn = q0.y;
+  r.c0 = q0.z;
+  r.c1 = q0.w;
+  r.c2 = q1.x;
+  r.kf = __float_as_uint(q1.y);
+  const uint32_t cell = __float_as_uint(q1.z);
+  r.tm = q1.w;
+  r.cx = (int)(cell & 1023u);
+  r.cy = (int)((cell >> 10) & 1023u);
+  r.cz = (int)(cell >> 20);
+  r.base = (uint32_t)r.cx + (uint32_t)g.rx * ((uint32_t)r.cy + (uint32_t)g.ry * (uint32_t)r.cz);
+  r.delta = fminf(m.step, 2.f * (m.hi - r.tm));
+  const float iv = (float)g.rcp_voxel;
+  const float gx = (fmaf(r.tm, m.d[0], m.o[0]) - (float)g.ox) * iv;
+  const float gy = (fmaf(r.tm, m.d[1], m.o[1]) - (float)g.oy) * iv;
+  const float gz = (fmaf(r.tm, m.d[2], m.o[2]) - (float)g.oz) * iv;
+  r.fx = fminf(fmaxf(gx - (float)r.cx, 0.f), 1.f);
+  r.fy = fminf(fmaxf(gy - (float)r.cy, 0.f), 1.f);
+  r.fz = fminf(fmaxf(gz - (float)r.cz, 0.f), 1.f);
+}
+
+__device__ __forceinline__ void load_record(const SampleRec* rec, int t, int c, int K, float4& q0,
+                                            float4& q1) {
+  const float4* q = reinterpret_cast<const float4*>(rec + rec_index(t, c, K));
+  q0 = __ldg(q);
+  q1 = __ldg(q + 1);
+}
+
+// The walk's cell as the corner aggregation sees it.
+__device__ __forceinline__ Sample rec_cell(const RecSample& r) {
+  Sample s{};
+  s.base = r.base;
+  s.cx = r.cx;
+  s.cy = r.cy;
+  s.cz = r.cz;
+  return s;
 }
 
 // Suffix-form sample upstream of the reverse walk (see K2q) and the aggregate
-// update; Sc / Sd advance past the sample.
-__device__ __forceinline__ void walk_sample(CornerAgg& A, const RecSample& r, double upc0,
-                                            double upc1, double upc2, bool use_depth, double upd,
-                                            double& Sc0, double& Sc1, double& Sc2, double& Sd) {
-  double ds = upc0 * (r.c0 * r.Tn - Sc0) + upc1 * (r.c1 * r.Tn - Sc1) + upc2 * (r.c2 * r.Tn - Sc2);
-  if (use_depth) ds += upd * (r.tm * r.Tn - Sd);
+// update; Sc / Sd advance past the sample (fp32: the fast path's precision).
+__device__ __forceinline__ void walk_sample(CornerAgg& A, const RecSample& r, float upc0,
+                                            float upc1, float upc2, float upd, float& Sc0,
+                                            float& Sc1, float& Sc2, float& Sd) {
+  float ds = upc0 * (r.c0 * r.Tn - Sc0) + upc1 * (r.c1 * r.Tn - Sc1) + upc2 * (r.c2 * r.Tn - Sc2);
+  ds = fmaf(upd, r.tm * r.Tn - Sd, ds);
   ds *= r.delta;
-  Sc0 += r.c0 * r.w;
-  Sc1 += r.c1 * r.w;
-  Sc2 += r.c2 * r.w;
-  Sd += r.tm * r.w;
-  const float wf = (float)r.w;
-  agg_add(A, (float)r.s.fx, (float)r.s.fy, (float)r.s.fz,
-          (r.kf & kRecSigmaPos) ? (float)ds : 0.f, (r.kf & 1u) ? 0.f : (float)upc0 * wf,
-          (r.kf & 2u) ? 0.f : (float)upc1 * wf, (r.kf & 4u) ? 0.f : (float)upc2 * wf);
+  Sc0 = fmaf(r.c0, r.w, Sc0);
+  Sc1 = fmaf(r.c1, r.w, Sc1);
+  Sc2 = fmaf(r.c2, r.w, Sc2);
+  Sd = fmaf(r.tm, r.w, Sd);
+  agg_add(A, r.fx, r.fy, r.fz, (r.kf & kRecSigmaPos) ? ds : 0.f,
+          (r.kf & 1u) ? 0.f : upc0 * r.w, (r.kf & 2u) ? 0.f : upc1 * r.w,
+          (r.kf & 4u) ? 0.f : upc2 * r.w);
 }
 
 // K2g: the record walk for small batches, 8 lanes per ray. Below ~40K rays the
@@ -899,31 +947,26 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
     for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
   }
   if (!march_begin(g, p, m)) return;
+  const WalkRay wr = walk_ray(m);
   const int cnt = rec_count[t];
   const int L = (cnt + LPR - 1) / LPR;
   const int c0 = sub * L, c1 = min(cnt, c0 + L);  // this lane's records [c0, c1)
   // pass 1: chunk sums of c_ch w and t w
-  double P0 = 0.0, P1 = 0.0, P2 = 0.0, Pd = 0.0;
+  float P0 = 0.f, P1 = 0.f, P2 = 0.f, Pd = 0.f;
   for (int c = c0; c < c1; ++c) {
-    const float2* q = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
-    const float2 q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
-    const double kseg = (double)(__float_as_uint(q2.y) >> 4);
-    const double s0 = dadd(m.lo, dmul(kseg, m.step));
-    const double s0s = dadd(s0, m.step);
-    const double s1 = (m.hi < s0s) ? m.hi : s0s;
-    const double tm = dmul(0.5, dadd(s0, s1));
-    const double w = (double)q0.x;
-    P0 += (double)q1.x * w;
-    P1 += (double)q1.y * w;
-    P2 += (double)q2.x * w;
-    Pd += tm * w;
+    float4 q0, q1;
+    load_record(rec, t, c, K, q0, q1);
+    P0 = fmaf(q0.z, q0.x, P0);
+    P1 = fmaf(q0.w, q0.x, P1);
+    P2 = fmaf(q1.x, q0.x, P2);
+    Pd = fmaf(q1.w, q0.x, Pd);
   }
   // suffix sums of the later chunks (lanes sub+1 .. 7)
-  double Sc0 = 0.0, Sc1 = 0.0, Sc2 = 0.0, Sd = 0.0;
+  float Sc0 = 0.f, Sc1 = 0.f, Sc2 = 0.f, Sd = 0.f;
 #pragma unroll
   for (int j = LPR - 1; j > 0; --j) {
-    const double a0 = __shfl_sync(gmask, P0, gbase + j), a1 = __shfl_sync(gmask, P1, gbase + j);
-    const double a2 = __shfl_sync(gmask, P2, gbase + j), ad = __shfl_sync(gmask, Pd, gbase + j);
+    const float a0 = __shfl_sync(gmask, P0, gbase + j), a1 = __shfl_sync(gmask, P1, gbase + j);
+    const float a2 = __shfl_sync(gmask, P2, gbase + j), ad = __shfl_sync(gmask, Pd, gbase + j);
     if (j > sub) {
       Sc0 += a0;
       Sc1 += a1;
@@ -931,17 +974,18 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
       Sd += ad;
     }
   }
-  const double upd = u.use_depth ? u.upd : 0.0;
+  const float upd = u.use_depth ? (float)u.upd : 0.f;
   CornerAgg A;
   agg_init(A);
   int last_tb = -1;
   RedSink sink{grad, bf};
   for (int c = c1 - 1; c >= c0; --c) {
-    const float2* q = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
+    float4 q0, q1;
+    load_record(rec, t, c, K, q0, q1);
     RecSample r;
-    decode_record(g, m, __ldg(q), __ldg(q + 1), __ldg(q + 2), r);
-    if (agg_enter(A, sink, g, r.s)) mark_touched(g, r.s.cx, r.s.cy, r.s.cz, last_tb);
-    walk_sample(A, r, u.upc[0], u.upc[1], u.upc[2], u.use_depth, upd, Sc0, Sc1, Sc2, Sd);
+    decode_record(g, wr, q0, q1, r);
+    if (agg_enter(A, sink, g, rec_cell(r))) mark_touched(g, r.cx, r.cy, r.cz, last_tb);
+    walk_sample(A, r, (float)u.upc[0], (float)u.upc[1], (float)u.upc[2], upd, Sc0, Sc1, Sc2, Sd);
   }
   if (A.base != kNoCell) agg_flush(A, sink, g, 0xffu);
 }
@@ -960,10 +1004,10 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 // until every lane of the warp has finished its ray AND drained its ring
 // (warp-uniform exit; lanes without a ray help drain).
 #ifndef VRF_K2_MERGE
-#define VRF_K2_MERGE 1  // same-round duplicate merging: 0 off, 1 leader sums, 2 column-parallel
+#define VRF_K2_MERGE 3  // same-round duplicate merging: 0 off, 1 leader sums, 2 column-parallel, 3 factor-domain
 #endif
 #ifndef VRF_K2_MINB
-#define VRF_K2_MINB 3
+#define VRF_K2_MINB 4  // CTAs per SM: 128 registers (r02: 11.8 vs 12.5 ms at 3)
 #endif
 constexpr int kQ = 16;  // ring entries per thread (power of 2); a step enqueues <= 8
 constexpr int kQSmemBytes = kQ * kThreads * (16 + 4);
@@ -1000,6 +1044,50 @@ __device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& he
     const unsigned grp = __match_any_sync(act, v);
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(grp) - 1;
+#if VRF_K2_MERGE == 3
+    // factor-domain merge: members stage only their 4 factors; the leader expands
+    // each member's factors with that member's SH basis (s_bf) into its own sums
+    if (grp != (1u << lane)) {
+      float4* stage_e = reinterpret_cast<float4*>(stage);  // [32] of the warp
+      if (lane != leader) stage_e[lane] = e;
+      __syncwarp(grp);
+      if (lane == leader) {
+        float x[28];
+        x[0] = e.x;
+#pragma unroll
+        for (int mm = 0; mm < 9; ++mm) {
+          x[1 + mm] = e.y * bf[mm];
+          x[10 + mm] = e.z * bf[mm];
+          x[19 + mm] = e.w * bf[mm];
+        }
+        const float(*sbf)[12] = reinterpret_cast<const float(*)[12]>(
+            reinterpret_cast<const float4*>(stage) + 32 * kVec4PerVertex - 32 * 3);
+        unsigned rest = grp & ~(1u << lane);
+        while (rest) {
+          const int o = __ffs(rest) - 1;
+          rest &= rest - 1;
+          const float4 eo = stage_e[o];
+          float b2[12];
+          *reinterpret_cast<float4*>(b2) = *reinterpret_cast<const float4*>(&sbf[o][0]);
+          *reinterpret_cast<float4*>(b2 + 4) = *reinterpret_cast<const float4*>(&sbf[o][4]);
+          *reinterpret_cast<float4*>(b2 + 8) = *reinterpret_cast<const float4*>(&sbf[o][8]);
+          x[0] += eo.x;
+#pragma unroll
+          for (int mm = 0; mm < 9; ++mm) {
+            x[1 + mm] = fmaf(eo.y, b2[mm], x[1 + mm]);
+            x[10 + mm] = fmaf(eo.z, b2[mm], x[10 + mm]);
+            x[19 + mm] = fmaf(eo.w, b2[mm], x[19 + mm]);
+          }
+        }
+        float4* dst = grad + (size_t)v * kVec4PerVertex;
+#pragma unroll
+        for (int j = 0; j < kVec4PerVertex; ++j)
+          atomicAdd(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
+      }
+      __syncwarp(grp);
+      return;
+    }
+#endif
     float x[28];
     x[0] = e.x;
 #pragma unroll
@@ -1091,8 +1179,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
   // ---- per-ray setup; a lane with nothing to scatter keeps c = -1 but stays in
   // the loop (the loop's exit vote is warp-wide)
   int c = -1;
-  March m;
-  MapUp u{};
+  WalkRay wr{};
+  float upc0 = 0.f, upc1 = 0.f, upc2 = 0.f, upd = 0.f;
   float bf[9];
   for (int mm = 0; mm < 9; ++mm) bf[mm] = 0.f;
   if (t < n) {
@@ -1104,21 +1192,36 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
       const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
       const double4 tg =
           rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+      MapUp u;
       if (map_upstream(st, global_counts, ray_cd[i], tg, fl, lambda_d, u)) {
+        March m;
         ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
         double basis[9];
         if (sh_basis(m.d, basis)) {
 #pragma unroll
           for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
-          if (march_begin(g, p, m)) c = rec_count[t] - 1;
+          if (march_begin(g, p, m)) {
+            c = rec_count[t] - 1;
+            wr = walk_ray(m);
+            upc0 = (float)u.upc[0];
+            upc1 = (float)u.upc[1];
+            upc2 = (float)u.upc[2];
+            upd = u.use_depth ? (float)u.upd : 0.f;
+          }
         }
       }
     }
   }
-  const double upc0 = u.upc[0], upc1 = u.upc[1], upc2 = u.upc[2];
-  const bool use_depth = c >= 0 && u.use_depth;
-  const double upd = use_depth ? u.upd : 0.0;
-  double Sc0 = 0.0, Sc1 = 0.0, Sc2 = 0.0, Sd = 0.0;
+#if VRF_K2_MERGE == 3
+  {  // the lane's SH basis, read by the group leaders of the factor-domain merge
+    float* sbf = reinterpret_cast<float*>(reinterpret_cast<float4*>(stage) + 32 * kVec4PerVertex -
+                                          32 * 3) + 12 * (threadIdx.x & 31);
+#pragma unroll
+    for (int mm = 0; mm < 9; ++mm) sbf[mm] = bf[mm];
+    __syncwarp();
+  }
+#endif
+  float Sc0 = 0.f, Sc1 = 0.f, Sc2 = 0.f, Sd = 0.f;
   CornerAgg A;
   agg_init(A);
   int last_tb = -1;
@@ -1127,27 +1230,17 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
   bool final_pending = c >= 0;  // the last cell's 8 corners, flushed after the walk
   // records are prefetched one iteration ahead: the dependent load of the next
   // record overlaps this sample's math and scatter
-  float2 n0 = make_float2(0.f, 0.f), n1 = n0, n2 = n0;
-  if (c >= 0) {
-    const float2* qq = reinterpret_cast<const float2*>(rec + rec_index(t, c, K));
-    n0 = __ldg(qq);
-    n1 = __ldg(qq + 1);
-    n2 = __ldg(qq + 2);
-  }
+  float4 n0 = make_float4(0.f, 0.f, 0.f, 0.f), n1 = n0;
+  if (c >= 0) load_record(rec, t, c, K, n0, n1);
   while (__any_sync(0xffffffffu, c >= 0 || final_pending || head != q.tail)) {
     if (c >= 0) {
-      const float2 q0 = n0, q1 = n1, q2 = n2;
-      if (c > 0) {
-        const float2* qq = reinterpret_cast<const float2*>(rec + rec_index(t, c - 1, K));
-        n0 = __ldg(qq);
-        n1 = __ldg(qq + 1);
-        n2 = __ldg(qq + 2);
-      }
+      const float4 q0 = n0, q1 = n1;
+      if (c > 0) load_record(rec, t, c - 1, K, n0, n1);
       --c;
       RecSample r;
-      decode_record(g, m, q0, q1, q2, r);
-      if (agg_enter(A, q, g, r.s)) mark_touched(g, r.s.cx, r.s.cy, r.s.cz, last_tb);
-      walk_sample(A, r, upc0, upc1, upc2, use_depth, upd, Sc0, Sc1, Sc2, Sd);
+      decode_record(g, wr, q0, q1, r);
+      if (agg_enter(A, q, g, rec_cell(r))) mark_touched(g, r.cx, r.cy, r.cz, last_tb);
+      walk_sample(A, r, upc0, upc1, upc2, upd, Sc0, Sc1, Sc2, Sd);
     } else if (final_pending && q.tail - head <= (uint32_t)(kQ - 8)) {
       final_pending = false;
       agg_flush(A, q, g, 0xffu);
@@ -1348,6 +1441,27 @@ __global__ void __launch_bounds__(256) k_rmsprop_blocks(
 // vertices outside the grid zero), reduced across ranks block-wise, applied by
 // the owning rank and the updated payload blocks gathered back. id < 0 = padding.
 constexpr int kBlockVerts = 1 << (3 * kTouchLog2);
+
+// Touched vertex blocks from the touched cell blocks: vertex block v (vertices
+// [8 v, 8 v + 7] per axis) holds a corner of cell block c (cells [8 c, 8 c + 7],
+// vertices [8 c, 8 c + 8]) iff c == v or c == v - 1 on every axis.
+__global__ void k_touched_dilate(const uint32_t* __restrict__ tc, int bx, int by, int bz,
+                                 uint32_t* __restrict__ tb, int tbx, int tby, int tbz) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= tbx * tby * tbz) return;
+  const int vx = v % tbx, vy = (v / tbx) % tby, vz = v / (tbx * tby);
+  bool on = false;
+#pragma unroll
+  for (int d = 0; d < 8; ++d) {
+    const int cx = vx - (d & 1), cy = vy - ((d >> 1) & 1), cz = vz - (d >> 2);
+    if (cx < 0 || cy < 0 || cz < 0 || cx >= bx || cy >= by || cz >= bz) continue;
+    const int c = cx + bx * (cy + by * cz);
+    on |= (tc[c >> 5] >> (c & 31)) & 1u;
+  }
+  const unsigned m = __ballot_sync(__activemask(), on);
+  // one word per 32 consecutive vertex blocks: the warp's lane 0 writes it
+  if ((threadIdx.x & 31) == 0) atomicOr(tb + (v >> 5), m);
+}
 
 __global__ void k_touched_flags(const uint32_t* __restrict__ tb, int nb, uint8_t* __restrict__ f) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1787,7 +1901,7 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
         order, rec, K, rec_count);
     return;
   }
-  // K2q: 3 CTAs/SM, 2 pops per step. r01 (config 3 / config 4, ms): 1, 2 or 3
+  // K2q: 4 CTAs/SM (VRF_K2_MINB), 2 pops per step. r01 (config 3 / config 4, ms): 1, 2 or 3
   // pops 14.54 / 14.63 / 15.02 and 25.82 / 25.71 / 25.78.
   constexpr int kMinB = VRF_K2_MINB, kPops = 2;
   static const bool attr = cudaFuncSetAttribute(k_map_backward_q<kMinB, kPops>,
@@ -1854,6 +1968,12 @@ void launch_rmsprop_blocks(float4* theta, float4* grad, float4* v, uint32_t* tb,
                                       lr_sh, eps, stats, touched, log);
   cudaMemsetAsync(tb, 0, sizeof(uint32_t) * ((nb + 31) / 32 + 1), s);
 }
+void launch_touched_dilate(uint32_t* tc, int bx, int by, int bz, uint32_t* tb, int tbx, int tby,
+                           int tbz, cudaStream_t s) {
+  const int nv = tbx * tby * tbz;
+  k_touched_dilate<<<(nv + 255) / 256, 256, 0, s>>>(tc, bx, by, bz, tb, tbx, tby, tbz);
+  cudaMemsetAsync(tc, 0, sizeof(uint32_t) * (((long long)bx * by * bz + 31) / 32 + 1), s);
+}
 void launch_touched_flags(const uint32_t* tb, int nb, uint8_t* flags, cudaStream_t s) {
   k_touched_flags<<<(nb + 255) / 256, 256, 0, s>>>(tb, nb, flags);
 }
@@ -1887,13 +2007,44 @@ void launch_exchange_p2p(const PeerTable& pt, float4* v, int nb, int rx, int ry,
 }
 __global__ void k_aos_to_soa(const float4* __restrict__ aos, float4* __restrict__ soa,
                              long long nv) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nv * kVec4PerVertex) return;
-  const long long v = i / kVec4PerVertex, j = i % kVec4PerVertex;
-  soa[j * nv + v] = aos[i];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv * kVec4PerVertex;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long v = i / kVec4PerVertex, j = i % kVec4PerVertex;
+    soa[j * nv + v] = aos[i];
+  }
 }
 void launch_aos_to_soa(const float4* aos, float4* soa, long long nv, cudaStream_t s) {
   k_aos_to_soa<<<grid_blocks(nv * kVec4PerVertex, 256), 256, 0, s>>>(aos, soa, nv);
+}
+// Order-independent 64-bit digest of a word array: sum over i of mix(i, w_i)
+// (splitmix64 finaliser of the index-salted word), so any changed word, moved word
+// or changed length changes it w.h.p.; per-block sums, one atomic add per block.
+__device__ __forceinline__ uint64_t digest_mix(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__global__ void __launch_bounds__(256) k_digest(const uint32_t* __restrict__ w, long long n,
+                                                uint64_t salt, unsigned long long* out) {
+  uint64_t acc = 0;
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < n;
+       i += (long long)gridDim.x * 256)
+    acc += digest_mix(salt ^ ((uint64_t)i << 32) ^ (uint64_t)__ldg(w + i));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  __shared__ uint64_t s[8];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int k = 0; k < 8; ++k) t += s[k];
+    atomicAdd(out, (unsigned long long)t);
+  }
+}
+void launch_digest(const uint32_t* words, long long n, uint64_t salt, unsigned long long* out,
+                   cudaStream_t s) {
+  if (n > 0) k_digest<<<148 * 8, 256, 0, s>>>(words, n, salt, out);
 }
 void launch_fill_payload(float* payload, long long nv, float sigma, cudaStream_t s) {
   k_fill_payload<<<grid_blocks(nv * kPayload, 256), 256, 0, s>>>(payload, nv, sigma);

@@ -169,6 +169,9 @@ void launch_backward_fast(vrf_context* ctx, const vrf_mapping_config* cfg, const
                         (float4*)ctx->grad, cfg->lambda_d, /*overflow_only=*/ctx->rec_K > 0,
                         (const uint32_t*)ctx->s_order.ptr, ctx->stream);
   }
+  launch_touched_dilate(ctx->tc, ctx->bdim[0], ctx->bdim[1], ctx->bdim[2], ctx->tb, ctx->tdim[0],
+                        ctx->tdim[1], ctx->tdim[2], ctx->stream);
+  LAUNCHED(1);
   prof_end(ctx, kProfMapBackward, pb);
   LAUNCHED(1);
 }

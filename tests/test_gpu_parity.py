@@ -544,3 +544,38 @@ def test_synth_from_grid_matches_oracle_renders(ctx, oracle):
         cq, dq = synth.quantize_frame(c, d, intr.depth_scale)
         assert np.mean(f.color != cq) < 1e-3 and np.mean(f.depth != dq) < 1e-3
         assert f.gt_pose is p
+
+
+def test_grid_digest_tracks_mutation_only(ctx, oracle):
+    """vrf_grid_digest (device-side integrity check): unchanged by rendering and
+    tracking (tracking never mutates the grid), changed by a mapping
+    step, an occupancy change or a single payload float."""
+    grid, intr, frames = room_scene()
+    ctx.load_grid(grid)
+    ctx.load_frames(intr, frames)
+    d0 = ctx.grid_digest()
+    assert d0 == ctx.grid_digest()
+    ctx.render_image(intr, frames[1].gt_pose)
+    rng = np.random.default_rng(1)
+    px = np.stack([rng.integers(0, intr.width, 64), rng.integers(0, intr.height, 64)], 1)
+    ctx.pose_gradient(1, intr, frames[1].gt_pose, px, TrackingConfig())
+    ctx.track_frame(1, intr, frames[1].gt_pose, TrackingConfig(rays_per_iteration=128,
+                                                               iterations=3))
+    ctx.track_frame_gn(1, intr, frames[1].gt_pose, GNConfig(rays_per_iteration=256,
+                                                            iterations=2))
+    assert ctx.grid_digest() == d0
+    g = grid.copy()
+    g.data[17, 5] = np.float32(g.data[17, 5] + 0.5)
+    ctx.load_grid(g)
+    assert ctx.grid_digest() != d0
+    g2 = grid.copy()
+    g2.active[3] = not g2.active[3]
+    ctx.load_grid(g2)
+    assert ctx.grid_digest() != d0
+    ctx.load_grid(grid)
+    assert ctx.grid_digest() == d0
+    ctx.load_grid(fresh_grid(grid))
+    d1 = ctx.grid_digest()
+    ctx.mapping_step(MappingConfig(), oracle.draw_batch(3, len(frames), intr.width,
+                                                        intr.height, 256))
+    assert ctx.grid_digest() != d1

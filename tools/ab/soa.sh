@@ -9,7 +9,7 @@ for v in default soa; do
   python bench.py --no-cpu --no-tracking --no-dropin --steps 10 > gpurun_out/soa_$v.json 2>/dev/null
   python -c "
 import json; d=json.load(open('gpurun_out/soa_$v.json')); k=d['roofline']['kernel_ms']; n=d['steps']; o=d['roofline']['other_ms']
-print('$v', round(d['value']/1e9,3), 'fwd', round(k['map_forward']/n,3), 'bwd', round(k['map_backward']/n,3), 'misc', round(o.get('map_misc',0)/n,3))"
+print('$v', round(d['value']/1e9,3), 'fwd', round(k['map_forward']/n,3), 'bwd', round(k['map_backward']/n,3), 'misc', round(o.get('misc',0)/n,3))"
   if [ $rep = 1 ]; then
     ncu --metrics $M --clock-control none -k regex:k_map_forward_rec -s 3 -c 1 --csv \
       python bench.py --no-cpu --no-tracking --no-dropin --steps 1 --warmup 3 2>/dev/null \
