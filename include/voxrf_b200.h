@@ -251,6 +251,10 @@ int vrf_grid_set_occupancy(vrf_context* ctx, const uint8_t* occupancy);
 int vrf_track_updates(vrf_context* ctx, int on);
 int vrf_updates_count(vrf_context* ctx, int64_t* n);
 int vrf_updates_read(vrf_context* ctx, int64_t n, uint32_t* ids, float* theta, float* v);
+/* Page-locked host memory for staging buffers (cudaMallocHost; NULL on failure):
+ * device <-> host copies into it run at full PCIe / C2C speed. */
+void* vrf_host_alloc(size_t bytes);
+void vrf_host_free(void* p);
 
 /* ---- frames: Frame (frame.hpp:10-19); colour H*W*3, depth H*W along-ray metres */
 int vrf_frames_upload(vrf_context* ctx, const vrf_intrinsics* intr, int n,

@@ -234,12 +234,20 @@ void write_back(VoxelGrid& grid, RmspropState& st) {
     check(vrf_rmsprop_download(ctx(), v));
     g_res.back_bytes += 2 * groups * 4 * sizeof(float);
   } else if (n > 0) {
-    static std::vector<std::uint32_t> ids;
-    static std::vector<float> th, vv;
-    ids.resize(std::size_t(n));
-    th.resize(4 * std::size_t(n));
-    vv.resize(4 * std::size_t(n));
-    check(vrf_updates_read(ctx(), n, ids.data(), th.data(), vv.data()));
+    // page-locked staging (grown on demand, kept): the D2H runs at link speed
+    static void* stage = nullptr;
+    static std::size_t stage_bytes = 0;
+    const std::size_t need = std::size_t(n) * (sizeof(std::uint32_t) + 8 * sizeof(float));
+    if (stage_bytes < need) {
+      vrf_host_free(stage);
+      stage_bytes = need + need / 4;
+      stage = vrf_host_alloc(stage_bytes);
+      if (!stage) throw std::runtime_error("voxrf_b200: page-locked staging allocation failed");
+    }
+    float* th = static_cast<float*>(stage);
+    float* vv = th + 4 * std::size_t(n);
+    std::uint32_t* ids = reinterpret_cast<std::uint32_t*>(vv + 4 * std::size_t(n));
+    check(vrf_updates_read(ctx(), n, ids, th, vv));
     // scatter into the caller's fp64 buffers (random access: split over threads;
     // the logged groups are distinct, so the chunks never write the same element)
     auto scatter = [&](std::int64_t i0, std::int64_t i1) {

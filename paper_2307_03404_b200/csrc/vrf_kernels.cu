@@ -214,7 +214,10 @@ __device__ __forceinline__ size_t rec_index(int t, int c, int K) {
 // sample-major (rec_index): the lanes of a warp composite their c-th samples in
 // the same loop iteration, so each record store is one coalesced 768 B access.
 // 4 CTAs/SM (128 registers): r01 measured 3 / 4 / 5 CTAs at 8.83 / 8.21 / 8.75 ms.
-__global__ void __launch_bounds__(kThreads, 4) k_map_forward_rec(
+#ifndef VRF_K0_MINB
+#define VRF_K0_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
     double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
@@ -1004,7 +1007,10 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 // until every lane of the warp has finished its ray AND drained its ring
 // (warp-uniform exit; lanes without a ray help drain).
 #ifndef VRF_K2_MERGE
-#define VRF_K2_MERGE 3  // same-round duplicate merging: 0 off, 1 leader sums, 2 column-parallel, 3 factor-domain
+#define VRF_K2_MERGE 3  // same-round duplicate merging: 1 leader sums expanded vectors, 3 factor-domain
+#endif
+#ifndef VRF_K2_POP2
+#define VRF_K2_POP2 0  // A/B: load both pops' queue entries up front
 #endif
 #ifndef VRF_K2_MINB
 #define VRF_K2_MINB 4  // CTAs per SM: 128 registers (r02: 11.8 vs 12.5 ms at 3)
@@ -1032,62 +1038,15 @@ struct QueueSink {
 // buffer, and the leader sums the group and issues the only 7 red.v4. This cuts
 // the L2 reductions by a third; at config 4, where the 15 GB gradient misses L2,
 // it saves DRAM read-modify-writes (K2 29.3 -> 25.7 ms, r01).
-__device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& head,
-                                                float4* __restrict__ grad, const float (&bf)[9],
-                                                float4 (*stage)[kVec4PerVertex]) {
-  if (head != q.tail) {
-    const int slot = (int)(head & (kQ - 1)) * kThreads + q.tid;
-    const uint32_t v = q.qv[slot];
-    const float4 e = q.qa[slot];
-    ++head;
+// One merged pop of the entry (v, e) the caller loaded (has: the lane popped).
+__device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
+                                          float4* __restrict__ grad, const float (&bf)[9],
+                                          float4 (*stage)[kVec4PerVertex]) {
+  if (has) {
     const unsigned act = __activemask();
     const unsigned grp = __match_any_sync(act, v);
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(grp) - 1;
-#if VRF_K2_MERGE == 3
-    // factor-domain merge: members stage only their 4 factors; the leader expands
-    // each member's factors with that member's SH basis (s_bf) into its own sums
-    if (grp != (1u << lane)) {
-      float4* stage_e = reinterpret_cast<float4*>(stage);  // [32] of the warp
-      if (lane != leader) stage_e[lane] = e;
-      __syncwarp(grp);
-      if (lane == leader) {
-        float x[28];
-        x[0] = e.x;
-#pragma unroll
-        for (int mm = 0; mm < 9; ++mm) {
-          x[1 + mm] = e.y * bf[mm];
-          x[10 + mm] = e.z * bf[mm];
-          x[19 + mm] = e.w * bf[mm];
-        }
-        const float(*sbf)[12] = reinterpret_cast<const float(*)[12]>(
-            reinterpret_cast<const float4*>(stage) + 32 * kVec4PerVertex - 32 * 3);
-        unsigned rest = grp & ~(1u << lane);
-        while (rest) {
-          const int o = __ffs(rest) - 1;
-          rest &= rest - 1;
-          const float4 eo = stage_e[o];
-          float b2[12];
-          *reinterpret_cast<float4*>(b2) = *reinterpret_cast<const float4*>(&sbf[o][0]);
-          *reinterpret_cast<float4*>(b2 + 4) = *reinterpret_cast<const float4*>(&sbf[o][4]);
-          *reinterpret_cast<float4*>(b2 + 8) = *reinterpret_cast<const float4*>(&sbf[o][8]);
-          x[0] += eo.x;
-#pragma unroll
-          for (int mm = 0; mm < 9; ++mm) {
-            x[1 + mm] = fmaf(eo.y, b2[mm], x[1 + mm]);
-            x[10 + mm] = fmaf(eo.z, b2[mm], x[10 + mm]);
-            x[19 + mm] = fmaf(eo.w, b2[mm], x[19 + mm]);
-          }
-        }
-        float4* dst = grad + (size_t)v * kVec4PerVertex;
-#pragma unroll
-        for (int j = 0; j < kVec4PerVertex; ++j)
-          atomicAdd(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
-      }
-      __syncwarp(grp);
-      return;
-    }
-#endif
     float x[28];
     x[0] = e.x;
 #pragma unroll
@@ -1096,38 +1055,34 @@ __device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& he
       x[10 + mm] = e.z * bf[mm];
       x[19 + mm] = e.w * bf[mm];
     }
-#if VRF_K2_MERGE == 2
-    // column-parallel: every member stages; member r of g sums columns r, r+g, ...
     if (grp != (1u << lane)) {
-#pragma unroll
-      for (int j = 0; j < kVec4PerVertex; ++j)
-        stage[lane][j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+#if VRF_K2_MERGE == 3
+      // factor-domain merge: members stage only their 4 factors; the leader
+      // expands each member's factors with that member's SH basis (the warp's
+      // s_bf rows) into its own sums
+      float4* stage_e = reinterpret_cast<float4*>(stage);  // [32] of the warp
+      if (lane != leader) stage_e[lane] = e;
       __syncwarp(grp);
-      const int g = __popc(grp), r = __popc(grp & ((1u << lane) - 1u));
-      float4* dst = grad + (size_t)v * kVec4PerVertex;
-      for (int j = r; j < kVec4PerVertex; j += g) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        unsigned rest = grp;
+      if (lane == leader) {
+        const float4* sbf = reinterpret_cast<const float4*>(stage) + 32 * kVec4PerVertex - 32 * 3;
+        unsigned rest = grp & ~(1u << lane);
         while (rest) {
           const int o = __ffs(rest) - 1;
           rest &= rest - 1;
-          const float4 y = stage[o][j];
-          acc.x += y.x;
-          acc.y += y.y;
-          acc.z += y.z;
-          acc.w += y.w;
+          const float4 eo = stage_e[o], b0 = sbf[3 * o], b1 = sbf[3 * o + 1], b2 = sbf[3 * o + 2];
+          const float bb[9] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x};
+          x[0] += eo.x;
+#pragma unroll
+          for (int mm = 0; mm < 9; ++mm) {
+            x[1 + mm] = fmaf(eo.y, bb[mm], x[1 + mm]);
+            x[10 + mm] = fmaf(eo.z, bb[mm], x[10 + mm]);
+            x[19 + mm] = fmaf(eo.w, bb[mm], x[19 + mm]);
+          }
         }
-        atomicAdd(dst + j, acc);
       }
-      __syncwarp(grp);
-      return;
-    }
-    if (true) {
-#elif VRF_K2_MERGE == 0
-    if (false) {
 #else
-    if (grp != (1u << lane)) {
-#endif
+      // leader merge of expanded vectors: members stage their 28-vector, the
+      // leader sums the group
       if (lane != leader) {
 #pragma unroll
         for (int j = 0; j < kVec4PerVertex; ++j)
@@ -1149,15 +1104,56 @@ __device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& he
           }
         }
       }
+#endif
       __syncwarp(grp);
     }
-    if (lane == leader || VRF_K2_MERGE == 0) {
+    if (lane == leader) {  // (a lone lane is its own leader)
       float4* dst = grad + (size_t)v * kVec4PerVertex;
 #pragma unroll
       for (int j = 0; j < kVec4PerVertex; ++j)
         atomicAdd(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
     }
   }
+}
+
+__device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& head,
+                                                float4* __restrict__ grad, const float (&bf)[9],
+                                                float4 (*stage)[kVec4PerVertex]) {
+  const bool has = head != q.tail;
+  uint32_t v = 0;
+  float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (has) {
+    const int slot = (int)(head & (kQ - 1)) * kThreads + q.tid;
+    v = q.qv[slot];
+    e = q.qa[slot];
+    ++head;
+  }
+  pop_entry(has, v, e, grad, bf, stage);
+}
+
+// Two pops with both entries loaded up front: the second entry's shared-memory
+// latency hides behind the first pop (ncu r02: short-scoreboard stalls on the
+// popped vertex led K2's stall reasons).
+__device__ __forceinline__ void queue_pop_merge2(const QueueSink& q, uint32_t& head,
+                                                 float4* __restrict__ grad, const float (&bf)[9],
+                                                 float4 (*stage)[kVec4PerVertex]) {
+  const uint32_t n = q.tail - head;
+  const bool h0 = n > 0, h1 = n > 1;
+  uint32_t v0 = 0, v1 = 0;
+  float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f), e1 = e0;
+  if (h0) {
+    const int s0 = (int)(head & (kQ - 1)) * kThreads + q.tid;
+    v0 = q.qv[s0];
+    e0 = q.qa[s0];
+  }
+  if (h1) {
+    const int s1 = (int)((head + 1) & (kQ - 1)) * kThreads + q.tid;
+    v1 = q.qv[s1];
+    e1 = q.qa[s1];
+  }
+  head += (uint32_t)h0 + (uint32_t)h1;
+  pop_entry(h0, v0, e0, grad, bf, stage);
+  pop_entry(h1, v1, e1, grad, bf, stage);
 }
 
 template <int MINB, int POPS>
@@ -1247,8 +1243,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     }
     // convergent scatter: every lane with queued corners pops up to POPS, then
     // more until every ring has room for the next step's <= 8 entries
+#if VRF_K2_POP2
+    static_assert(POPS == 2, "paired pops");
+    queue_pop_merge2(q, head, grad, bf, stage);
+#else
 #pragma unroll
     for (int r = 0; r < POPS; ++r) queue_pop_merge(q, head, grad, bf, stage);
+#endif
     while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
       queue_pop_merge(q, head, grad, bf, stage);
   }

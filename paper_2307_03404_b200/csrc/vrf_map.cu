@@ -572,6 +572,15 @@ int vrf_map_apply(vrf_context* ctx, const vrf_mapping_config* cfg, int64_t verte
 }
 
 // ---- drop-in residency: partial uploads and the update log (integration/)
+void* vrf_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  return cudaMallocHost(&p, bytes) == cudaSuccess ? p : nullptr;
+}
+
+void vrf_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int vrf_track_updates(vrf_context* ctx, int on) {
   ctx->log_updates = on != 0;
   return VRF_OK;
