@@ -217,6 +217,9 @@ __device__ __forceinline__ size_t rec_index(int t, int c, int K) {
 #ifndef VRF_K0_MINB
 #define VRF_K0_MINB 4
 #endif
+#ifndef VRF_K0_COOP
+#define VRF_K0_COOP 0  // A/B: warp-cooperative corner staging in shared memory
+#endif
 __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
@@ -328,6 +331,209 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
     partials[blockIdx.x] = q;
   }
 }
+
+#if VRF_K0_COOP
+// K0 with warp-cooperative corner staging (A/B, -DVRF_K0_COOP=1). The 32 rays of
+// a warp are coherent, so at one march step they sit in a handful of distinct
+// cells; the thread-per-ray gather reads every corner through L1 once per lane
+// (56 LDG.128 per sample, ~5.6 L1 wavefronts each: K0 is bound by the L1 data
+// pipe). Here each step groups the lanes by cell (__match_any_sync), the warp
+// loads each distinct cell's 8 corners once with coalesced 112-B runs into shared
+// memory, and every lane shades from there. Same values, same FP64 arithmetic:
+// bit-identical to k_map_forward_rec.
+constexpr int kCoopSlots = 8;    // distinct cells staged per round
+constexpr int kCoopStride = 57;  // float4 per staged cell: 8 corners x 7 + 1 (bank spread)
+
+__device__ __forceinline__ void shade_staged(const float4* cell, const double w[8],
+                                             const float bf[9], Shade& out) {
+  double sraw = 0.0;
+  float cr = 0.f, cg = 0.f, cb = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float v[28];
+#pragma unroll
+    for (int j = 0; j < kVec4PerVertex; ++j) {
+      const float4 a = cell[k * kVec4PerVertex + j];
+      v[4 * j] = a.x;
+      v[4 * j + 1] = a.y;
+      v[4 * j + 2] = a.z;
+      v[4 * j + 3] = a.w;
+    }
+    sraw = dadd(sraw, dmul(w[k], (double)v[0]));
+    float dr = 0.f, dg = 0.f, db = 0.f;
+#pragma unroll
+    for (int m = 0; m < 9; ++m) {
+      dr = fmaf(bf[m], v[1 + m], dr);
+      dg = fmaf(bf[m], v[10 + m], dg);
+      db = fmaf(bf[m], v[19 + m], db);
+    }
+    const float wk = (float)w[k];
+    cr = fmaf(wk, dr, cr);
+    cg = fmaf(wk, dg, cg);
+    cb = fmaf(wk, db, cb);
+  }
+  out.sigma_raw = sraw;
+  const float cc[3] = {cr, cg, cb};
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const double v = 0.5 + (double)cc[ch];
+    out.clamped[ch] = (v <= 0.0 || v >= 1.0);
+    out.c[ch] = (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_coop(
+    DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
+    const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
+    double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
+    const uint32_t* __restrict__ order, SampleRec* __restrict__ rec, int K,
+    int* __restrict__ rec_count) {
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ double s_d[32];
+  __shared__ long long s_l[32];
+  __shared__ int s_i[32];
+  __shared__ __align__(16) float4 s_cells[kThreads / 32][kCoopSlots * kCoopStride];
+  __shared__ uint32_t s_base[kThreads / 32][kCoopSlots];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (order && t < n) ? (int)order[t] : t;
+  double lp = 0.0, lg = 0.0;
+  long long samples = 0;
+  int mc = 0, md = 0, bad = INT_MAX;
+  int f = 0, px = 0, py = 0;
+  bool valid = false, alive = false;
+  March m;
+  Composite st;
+  st.T = 1.0;
+  st.C[0] = st.C[1] = st.C[2] = 0.0;
+  st.D = 0.0;
+  st.count = 0;
+  st.terminated = false;
+  float bf[9];
+  for (int mm = 0; mm < 9; ++mm) bf[mm] = 0.f;
+  if (t < n) {
+    f = batch[3 * i];
+    px = batch[3 * i + 1];
+    py = batch[3 * i + 2];
+    if (f < 0 || f >= n_frames || px < 0 || px >= cam.width || py < 0 || py >= cam.height) {
+      atomicOr(err, 2);  // generate_ray: pixel outside image
+    } else {
+      valid = true;
+      ray_from_pixel(cam, poses[f], (double)px, (double)py, m);
+      double basis[9];
+      const bool basis_ok = sh_basis(m.d, basis);
+#pragma unroll
+      for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
+      if (!basis_ok)
+        atomicOr(err, 1);
+      else
+        alive = march_begin(g, p, m);
+    }
+  }
+  float4* cells = s_cells[wid];
+  uint32_t* bases = s_base[wid];
+  while (__any_sync(FULL, alive)) {
+    Sample s;
+    bool has = false;
+    if (alive) {
+      has = march_next(g, m, s);
+      if (!has) alive = false;
+    }
+    const unsigned grp = __match_any_sync(FULL, has ? s.base : 0xffffffffu);
+    const int leader = __ffs(grp) - 1;
+    const unsigned lm = __ballot_sync(FULL, has && lane == leader);  // one bit per distinct cell
+    const int D = __popc(lm);
+    const int slot = __popc(lm & ((1u << leader) - 1u));
+    for (int r0 = 0; r0 < D; r0 += kCoopSlots) {
+      const int nd = min(kCoopSlots, D - r0);
+      if (has && lane == leader && slot >= r0 && slot < r0 + kCoopSlots) bases[slot - r0] = s.base;
+      __syncwarp();
+      // the staged cells' 8 corners, 7 float4 each, as contiguous 112-B runs
+      for (int it = lane; it < nd * 8 * kVec4PerVertex; it += 32) {
+        const int vs = it / kVec4PerVertex, j = it - vs * kVec4PerVertex;
+        const int c = vs >> 3, k = vs & 7;
+        const float4* src = g.payload + (size_t)corner_index(g, bases[c], k) * kVec4PerVertex;
+        cells[c * kCoopStride + k * kVec4PerVertex + j] = __ldg(src + j);
+      }
+      __syncwarp();
+      if (has && slot >= r0 && slot < r0 + kCoopSlots) {
+        Shade sh;
+        {
+          double w[8];
+          corner_weights(s, w);
+          shade_staged(cells + (slot - r0) * kCoopStride, w, bf, sh);
+        }
+        double decay;
+        const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
+        if (st.count <= K) {
+          const uint32_t kf = ((uint32_t)(m.k - 1) << 4) | (sh.clamped[0] ? 1u : 0u) |
+                              (sh.clamped[1] ? 2u : 0u) | (sh.clamped[2] ? 4u : 0u) |
+                              (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
+          float4* d = reinterpret_cast<float4*>(rec + rec_index(t, st.count - 1, K));
+          d[0] = make_float4((float)wgt, (float)st.T, (float)sh.c[0], (float)sh.c[1]);
+          d[1] = make_float4((float)sh.c[2], __uint_as_float(kf),
+                             __uint_as_float(pack_cell(s.cx, s.cy, s.cz)), (float)s.t);
+        }
+        if (st.terminated) alive = false;
+      }
+      __syncwarp();
+    }
+  }
+  if (t < n) {
+    uint8_t fl = 0;
+    int stored = 0;
+    if (valid) {
+      if (st.count == 0) {
+        st.C[0] = st.C[1] = st.C[2] = 0.0;
+        st.D = 0.0;
+      }
+      const double4 tg =
+          rgbd[(long long)f * cam.width * cam.height + (long long)py * cam.width + px];
+      if (st.count > 0) {
+        fl |= kHit;
+        if (st.count > K) fl |= kOverflow;
+        stored = st.count > K ? 0 : st.count;
+        mc = 1;
+        samples = st.count;
+        const double r0 = dsub(st.C[0], tg.x), r1 = dsub(st.C[1], tg.y), r2 = dsub(st.C[2], tg.z);
+        const double sq = dadd(dadd(dmul(r0, r0), dmul(r1, r1)), dmul(r2, r2));
+        if (!isfinite(sq) || !isfinite(st.D)) {
+          bad = i;
+        } else {
+          lp = sq;
+          if (tg.w > 0.0) {
+            fl |= kDepthValid;
+            md = 1;
+            const double dr = dsub(st.D, tg.w);
+            lg = dmul(dr, dr);
+          }
+        }
+      }
+      ray_cd[i] = make_double4(st.C[0], st.C[1], st.C[2], st.D);
+    }
+    flags[i] = fl;
+    rec_count[t] = stored;
+  }
+  const double blp = block_sum(lp, s_d);
+  const double blg = block_sum(lg, s_d);
+  const long long bs = block_sum(samples, s_l);
+  const int bmc = block_sum(mc, s_i);
+  const int bmd = block_sum(md, s_i);
+  const int bbad = block_min(bad, s_i);
+  const int bmax = -block_min(-(int)samples, s_i);
+  if (threadIdx.x == 0) {
+    MapPartial q;
+    q.lp = blp;
+    q.lg = blg;
+    q.samples = bs;
+    q.m_c = bmc;
+    q.m_d = bmd;
+    q.bad = bbad;
+    q.max_count = bmax;
+    partials[blockIdx.x] = q;
+  }
+}
+#endif
 
 // Fixed-order reduction of the per-block partials (deterministic).
 __global__ void __launch_bounds__(1024) k_map_reduce(const MapPartial* __restrict__ parts,
@@ -1875,9 +2081,15 @@ void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& 
         rec_count);
     return;
   }
+#if VRF_K0_COOP
+  k_map_forward_coop<<<map_forward_blocks(n), kThreads, 0, s>>>(g, p, cam, rgbd, poses, n_frames,
+                                                                batch, n, ray_cd, flags, partials,
+                                                                err, order, rec, K, rec_count);
+#else
   k_map_forward_rec<<<map_forward_blocks(n), kThreads, 0, s>>>(g, p, cam, rgbd, poses, n_frames,
                                                                batch, n, ray_cd, flags, partials,
                                                                err, order, rec, K, rec_count);
+#endif
 }
 // Rays up to which K2 runs 8 lanes per ray (K2g); VRF_BWD_GROUP_MAX overrides.
 // r01 (config-3 scene, backward ms, K2g vs K2q): 4K rays 0.19 vs 1.07, 16K 0.41
