@@ -84,6 +84,7 @@ struct vrf_context {
       s_ids, s_ids2, s_values, s_grad64, s_cub, s_stage, s_out, s_batch2, s_rec, s_reccount;
   // fast-path sample records of the last forward (0 = recompute-march backward)
   int rec_K = 0;
+  size_t rec_slots = 0;  // records per plane of s_rec (nn32 * rec_K; rec_planes)
   int max_ray_samples = 0;  // longest ray seen by a mapping forward (sizes rec_K)
   long long rec_need_tried = 0;  // last record depth the budget was evaluated for
   // RMSProp update log for the drop-in's sparse write-back (vrf_track_updates)
@@ -489,7 +490,7 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
         while (need < ctx->max_ray_samples * 5LL / 4 && need < 1024) need *= 2;
       }
       const size_t nn32 = (nn + 31) & ~(size_t)31;  // warp-tiled record layout
-      const double per_level = (double)nn32 * (double)sizeof(SampleRec);
+      const double per_level = (double)nn32 * (double)kRecBytes;
       // K the held buffer already covers; regrow only for a real shortfall
       // (2x), so a budget-limited cap does not reallocate every step
       const long long held_K = (long long)((double)ctx->s_rec.bytes / per_level);
@@ -514,11 +515,12 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
       // other allocators (e.g. torch's caching allocator in the multi-GPU
       // driver) may hold memory the budget counted: halve on out-of-memory
       while (K >= kmin &&
-             !try_ensure(ctx->stream, ctx->s_rec, sizeof(SampleRec) * nn32 * (size_t)K))
+             !try_ensure(ctx->stream, ctx->s_rec, kRecBytes * nn32 * (size_t)K))
         K /= 2;
       if (K >= kmin) {
         if ((rc = ensure(ctx, ctx->s_reccount, sizeof(int) * nn))) return rc;
         ctx->rec_K = (int)(K & ~3LL);
+        ctx->rec_slots = nn32 * (size_t)ctx->rec_K;
       }
     }
     cudaEvent_t pb = prof_begin(ctx);
@@ -526,7 +528,8 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
       launch_map_forward_rec(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
                              batch_dev, n, (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,
                              (MapPartial*)ctx->s_partials.ptr, ctx->d_err,
-                             (const uint32_t*)ctx->s_order.ptr, (SampleRec*)ctx->s_rec.ptr,
+                             (const uint32_t*)ctx->s_order.ptr,
+                             rec_planes(ctx->s_rec.ptr, ctx->rec_slots),
                              ctx->rec_K, (int*)ctx->s_reccount.ptr, ctx->stream);
     else
       launch_map_forward(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,

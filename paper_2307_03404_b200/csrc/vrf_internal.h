@@ -29,19 +29,24 @@ struct PosePartial {
 
 enum FlagBits : uint8_t { kHit = 1, kDepthValid = 2, kOverflow = 4 };
 
-// Per-sample record of the fast mapping forward (32 B, two float4), consumed by
-// the reverse-order backward: weight w_i, T_{i+1}, clamped colour,
-// kf = (segment index << 4) | clamp bits (0-2) | sigma_raw > 0 (bit 3), the
-// sample's cell (cx | cy << 10 | cz << 20, located in FP64 by the forward) and
-// its segment midpoint t (fp32). The backward re-derives only the trilinear
-// weights, in fp32 (r02; r01's 24 B record re-located the cell in FP64).
-struct SampleRec {
-  float w, tn, c0, c1;
-  float c2;
-  uint32_t kf, cell;
-  float tm;
+// Per-sample record of the fast mapping forward (24 B in two planes), consumed by
+// the reverse-order backward. Plane a (float4): w_i, T_{i+1}, the clamped colour
+// as 16-bit fixed point in [0, 1] (c0 | c1 << 16, c2 | flags << 16; flags = clamp
+// bits 0-2 and sigma_raw > 0 in bit 3). Plane b (uint2): the sample's cell
+// (cx | cy << 10 | cz << 20, located in FP64 by the forward) and its segment
+// midpoint t (fp32). The backward re-derives only the trilinear weights, in fp32
+// (r01's 24 B record re-located the cell in FP64; r02's first 32 B record kept
+// fp32 colour). Both planes share the slot index rec_index(t, c, K).
+struct RecBuf {
+  float4* a;
+  uint2* b;
 };
-static_assert(sizeof(SampleRec) == 32, "SampleRec layout");
+constexpr size_t kRecBytes = sizeof(float4) + sizeof(uint2);
+// The two planes of a record buffer of `slots` records at `base`.
+inline RecBuf rec_planes(void* base, size_t slots) {
+  return RecBuf{(float4*)base, (uint2*)((char*)base + slots * sizeof(float4))};
+}
+constexpr float kRecColorScale = 65535.f;
 constexpr uint32_t kRecSigmaPos = 8;
 constexpr int kRecMaxCells = 1024;  // per axis (10-bit cell coordinates in the record)
 __host__ __device__ __forceinline__ uint32_t pack_cell(int cx, int cy, int cz) {
@@ -62,7 +67,7 @@ void launch_map_forward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                         const uint32_t* order, cudaStream_t s);
 int map_forward_blocks(int n);
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s);
-// Fast forward that also stores up to K SampleRec per ray, warp-tiled sample-major
+// Fast forward that also stores up to K sample records per ray, warp-tiled sample-major
 // (rec_index(slot, c, K), slot = coherent order index); rays with more samples get
 // kOverflow. rec_count[slot] = samples stored.
 // CTAs of the K0 launch for n rays (the small-batch K0g has 16 rays per CTA).
@@ -70,7 +75,7 @@ int map_forward_rec_blocks(int n);
 void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
                             const double4* rgbd, const DevPose* poses, int n_frames,
                             const int* batch, int n, double4* ray_cd, uint8_t* flags,
-                            MapPartial* partials, int* err, const uint32_t* order, SampleRec* rec,
+                            MapPartial* partials, int* err, const uint32_t* order, RecBuf rec,
                             int K, int* rec_count, cudaStream_t s);
 // Backward over the records (no payload gathers); kOverflow rays are
 // left to launch_map_backward(..., overflow_only = true).
@@ -78,7 +83,7 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
                              const double4* rgbd, const DevPose* poses, const int* batch, int n,
                              const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
                              const int* global_counts, float4* grad, double lambda_d,
-                             const uint32_t* order, const SampleRec* rec, int K,
+                             const uint32_t* order, const RecBuf rec, int K,
                              const int* rec_count, cudaStream_t s);
 void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                          const double4* rgbd, const DevPose* poses, const int* batch, int n,

@@ -198,21 +198,37 @@ __global__ void __launch_bounds__(kThreads) k_map_forward(
 }
 
 // Record slot of sample c of the ray in slot t: warp-tiled sample-major
-// ("AoSoA"): the 32 rays of a warp own one contiguous K x 32 x 24 B region, and
-// within it sample c of all 32 lanes is contiguous. A warp's c-th stores are one
-// coalesced 768 B access, and each warp walks its own region (few TLB pages;
-// the plain c * n + t layout strode n x 24 B between a ray's samples).
+// ("AoSoA"): the 32 rays of a warp own one contiguous K x 32-record region of
+// each plane, and within it sample c of all 32 lanes is contiguous. The rays of
+// a warp are coherent (Morton tiles), so its lanes mostly composite (and walk
+// back) their c-th samples together: those stores and loads coalesce. (A
+// ray-major layout measured 10.7 / 13.9 ms for K0 / K2 against 8.7 / 11.8, r02.)
 __device__ __forceinline__ size_t rec_index(int t, int c, int K) {
   return ((size_t)(t >> 5) * (size_t)K + (size_t)c) * 32 + (size_t)(t & 31);
 }
 
+// Stores one sample record (vrf_internal.h: RecBuf): two coalesced stores per
+// warp (16 B + 8 B per lane), colour as 16-bit fixed point.
+__device__ __forceinline__ void store_record(RecBuf rec, size_t idx, double wgt, double T,
+                                             const Shade& sh, int cx, int cy, int cz,
+                                             double tm) {
+  const uint32_t fl = (sh.clamped[0] ? 1u : 0u) | (sh.clamped[1] ? 2u : 0u) |
+                      (sh.clamped[2] ? 4u : 0u) | (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
+  const uint32_t q0 = __float2uint_rn((float)sh.c[0] * kRecColorScale);
+  const uint32_t q1 = __float2uint_rn((float)sh.c[1] * kRecColorScale);
+  const uint32_t q2 = __float2uint_rn((float)sh.c[2] * kRecColorScale);
+  rec.a[idx] = make_float4((float)wgt, (float)T, __uint_as_float(q0 | (q1 << 16)),
+                           __uint_as_float(q2 | (fl << 16)));
+  rec.b[idx] = make_uint2(pack_cell(cx, cy, cz), __float_as_uint((float)tm));
+}
+
 // Fast forward (fp32 SH) that records every composited sample for the
 // backward: identical march, sigma_raw replay, compositing and termination as
-// k_map_forward<float>; per sample it stores w_i, T_{i+1}, the clamped colour
-// and (segment index, clamp / sigma gates) — 24 B — so the backward never
+// k_map_forward<float>; per sample it stores w_i, T_{i+1}, the clamped colour,
+// clamp / sigma gates, cell and midpoint — 24 B — so the backward never
 // gathers the 896 B of corner payload again. Records are warp-tiled
 // sample-major (rec_index): the lanes of a warp composite their c-th samples in
-// the same loop iteration, so each record store is one coalesced 768 B access.
+// the same loop iteration, so each record store is coalesced.
 // 4 CTAs/SM (128 registers): r01 measured 3 / 4 / 5 CTAs at 8.83 / 8.21 / 8.75 ms.
 #ifndef VRF_K0_MINB
 #define VRF_K0_MINB 4
@@ -224,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
     double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
-    const uint32_t* __restrict__ order, SampleRec* __restrict__ rec, int K,
+    const uint32_t* __restrict__ order, RecBuf rec, int K,
     int* __restrict__ rec_count) {
   __shared__ double s_d[32];
   __shared__ long long s_l[32];
@@ -271,13 +287,8 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
           double decay;
           const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
           if (st.count <= K) {
-            const uint32_t kf = ((uint32_t)(m.k - 1) << 4) | (sh.clamped[0] ? 1u : 0u) |
-                                (sh.clamped[1] ? 2u : 0u) | (sh.clamped[2] ? 4u : 0u) |
-                                (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
-            float4* d = reinterpret_cast<float4*>(rec + rec_index(t, st.count - 1, K));
-            d[0] = make_float4((float)wgt, (float)st.T, (float)sh.c[0], (float)sh.c[1]);
-            d[1] = make_float4((float)sh.c[2], __uint_as_float(kf),
-                               __uint_as_float(pack_cell(s.cx, s.cy, s.cz)), (float)s.t);
+            store_record(rec, rec_index(t, st.count - 1, K), wgt, st.T, sh, s.cx, s.cy, s.cz,
+                         s.t);
           }
           if (st.terminated) break;
         }
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_coop(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
     double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
-    const uint32_t* __restrict__ order, SampleRec* __restrict__ rec, int K,
+    const uint32_t* __restrict__ order, RecBuf rec, int K,
     int* __restrict__ rec_count) {
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double s_d[32];
@@ -466,13 +477,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_coop(
         double decay;
         const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
         if (st.count <= K) {
-          const uint32_t kf = ((uint32_t)(m.k - 1) << 4) | (sh.clamped[0] ? 1u : 0u) |
-                              (sh.clamped[1] ? 2u : 0u) | (sh.clamped[2] ? 4u : 0u) |
-                              (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
-          float4* d = reinterpret_cast<float4*>(rec + rec_index(t, st.count - 1, K));
-          d[0] = make_float4((float)wgt, (float)st.T, (float)sh.c[0], (float)sh.c[1]);
-          d[1] = make_float4((float)sh.c[2], __uint_as_float(kf),
-                             __uint_as_float(pack_cell(s.cx, s.cy, s.cz)), (float)s.t);
+          store_record(rec, rec_index(t, st.count - 1, K), wgt, st.T, sh, s.cx, s.cy, s.cz, s.t);
         }
         if (st.terminated) alive = false;
       }
@@ -655,7 +660,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
     double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
-    const uint32_t* __restrict__ order, SampleRec* __restrict__ rec, int K,
+    const uint32_t* __restrict__ order, RecBuf rec, int K,
     int* __restrict__ rec_count) {
   constexpr int LPR = kFwdLanes;
   __shared__ double s_d[32];
@@ -745,13 +750,8 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
           double decay;
           const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
           if (lead && st.count <= K) {
-            const uint32_t kf = ((uint32_t)gm.seg << 4) | (sh.clamped[0] ? 1u : 0u) |
-                                (sh.clamped[1] ? 2u : 0u) | (sh.clamped[2] ? 4u : 0u) |
-                                (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
-            float4* d = reinterpret_cast<float4*>(rec + rec_index(t, st.count - 1, K));
-            d[0] = make_float4((float)wgt, (float)st.T, (float)sh.c[0], (float)sh.c[1]);
-            d[1] = make_float4((float)sh.c[2], __uint_as_float(kf),
-                               __uint_as_float(pack_cell(s.cx, s.cy, s.cz)), (float)s.t);
+            store_record(rec, rec_index(t, st.count - 1, K), wgt, st.T, sh, s.cx, s.cy, s.cz,
+                         s.t);
           }
           if (st.terminated) break;
         }
@@ -1058,16 +1058,20 @@ struct RecSample {
   float tm, delta, w, Tn, c0, c1, c2;
   uint32_t kf;
 };
+__device__ __forceinline__ float rec_color(uint32_t q) {
+  return (float)(q & 0xffffu) * (1.f / kRecColorScale);
+}
 __device__ __forceinline__ void decode_record(const DevGrid& g, const WalkRay& m, float4 q0,
-                                              float4 q1, RecSample& r) {
+                                              uint2 q1, RecSample& r) {
   r.w = q0.x;
   r.Tn = q0.y;
-  r.c0 = q0.z;
-  r.c1 = q0.w;
-  r.c2 = q1.x;
-  r.kf = __float_as_uint(q1.y);
-  const uint32_t cell = __float_as_uint(q1.z);
-  r.tm = q1.w;
+  const uint32_t c01 = __float_as_uint(q0.z), c2f = __float_as_uint(q0.w);
+  r.c0 = rec_color(c01);
+  r.c1 = rec_color(c01 >> 16);
+  r.c2 = rec_color(c2f);
+  r.kf = c2f >> 16;
+  const uint32_t cell = q1.x;
+  r.tm = __uint_as_float(q1.y);
   r.cx = (int)(cell & 1023u);
   r.cy = (int)((cell >> 10) & 1023u);
   r.cz = (int)(cell >> 20);
@@ -1082,11 +1086,11 @@ __device__ __forceinline__ void decode_record(const DevGrid& g, const WalkRay& m
   r.fz = fminf(fmaxf(gz - (float)r.cz, 0.f), 1.f);
 }
 
-__device__ __forceinline__ void load_record(const SampleRec* rec, int t, int c, int K, float4& q0,
-                                            float4& q1) {
-  const float4* q = reinterpret_cast<const float4*>(rec + rec_index(t, c, K));
-  q0 = __ldg(q);
-  q1 = __ldg(q + 1);
+__device__ __forceinline__ void load_record(RecBuf rec, int t, int c, int K, float4& q0,
+                                            uint2& q1) {
+  const size_t i = rec_index(t, c, K);
+  q0 = __ldg(rec.a + i);
+  q1 = __ldg(rec.b + i);
 }
 
 // The walk's cell as the corner aggregation sees it.
@@ -1131,7 +1135,7 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
     const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
     const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
     float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
-    const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
+    RecBuf rec, int K, const int* __restrict__ rec_count) {
   constexpr int LPR = 8;
   const int lane = threadIdx.x & 31, sub = lane & (LPR - 1), gbase = lane & ~(LPR - 1);
   const unsigned gmask = ((1u << LPR) - 1u) << gbase;
@@ -1163,12 +1167,14 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
   // pass 1: chunk sums of c_ch w and t w
   float P0 = 0.f, P1 = 0.f, P2 = 0.f, Pd = 0.f;
   for (int c = c0; c < c1; ++c) {
-    float4 q0, q1;
+    float4 q0;
+    uint2 q1;
     load_record(rec, t, c, K, q0, q1);
-    P0 = fmaf(q0.z, q0.x, P0);
-    P1 = fmaf(q0.w, q0.x, P1);
-    P2 = fmaf(q1.x, q0.x, P2);
-    Pd = fmaf(q1.w, q0.x, Pd);
+    const uint32_t c01 = __float_as_uint(q0.z);
+    P0 = fmaf(rec_color(c01), q0.x, P0);
+    P1 = fmaf(rec_color(c01 >> 16), q0.x, P1);
+    P2 = fmaf(rec_color(__float_as_uint(q0.w)), q0.x, P2);
+    Pd = fmaf(__uint_as_float(q1.y), q0.x, Pd);
   }
   // suffix sums of the later chunks (lanes sub+1 .. 7)
   float Sc0 = 0.f, Sc1 = 0.f, Sc2 = 0.f, Sd = 0.f;
@@ -1189,7 +1195,8 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
   int last_tb = -1;
   RedSink sink{grad, bf};
   for (int c = c1 - 1; c >= c0; --c) {
-    float4 q0, q1;
+    float4 q0;
+    uint2 q1;
     load_record(rec, t, c, K, q0, q1);
     RecSample r;
     decode_record(g, wr, q0, q1, r);
@@ -1362,6 +1369,105 @@ __device__ __forceinline__ void queue_pop_merge2(const QueueSink& q, uint32_t& h
   pop_entry(h1, v1, e1, grad, bf, stage);
 }
 
+// ---- K2q cell-record ring (VRF_K2_RING=1). A move stores the departing
+// cell's whole aggregate (8 slots x 4 factors, unconditionally: 8 STS.128 at
+// full warp) plus a header (base vertex, X, live-slot mask) as one record; pops
+// pick the live slots of the oldest record in slot order and derive each
+// vertex from the header. The entry ring (QueueSink) instead branches per live
+// slot at enqueue (corner offset, ring position, two stores), which ran at ~10
+// active lanes and took ~20 % of K2's warp instructions (ncu v11 SASS profile).
+// Two records per thread: before every step a lane holds at most one pending
+// record, as the entry ring held at most 8 pending entries.
+#ifndef VRF_K2_RING
+#define VRF_K2_RING 1
+#endif
+constexpr int kRingRecs = 2;
+constexpr int kRingSmemBytes =
+    kRingRecs * 8 * kThreads * 16 + kRingRecs * kThreads * 8 + kThreads * kVec4PerVertex * 16;
+struct RingQueue {
+  float4* rec;   // [kRingRecs][8][kThreads] slot factors
+  uint2* hdr;    // [kRingRecs][kThreads] (base vertex, X | live << 8)
+  int tid;
+  uint32_t st;   // bits 0-7: unpopped live slots of the head record; bit 8: head
+                 // record; bits 9+: records pending
+  __device__ __forceinline__ uint32_t pending() const { return st >> 9; }
+};
+
+// Stores the aggregate's slots `live` (nonzero) as the lane's next record.
+__device__ __forceinline__ void ring_push(RingQueue& q, const CornerAgg& A, uint32_t live) {
+  const uint32_t hr = (q.st >> 8) & 1u, np = q.pending();
+  const uint32_t r = hr ^ np;  // np <= 1 here
+  float4* d = q.rec + (size_t)r * 8 * kThreads + q.tid;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) d[s * kThreads] = make_float4(A.a[0][s], A.a[1][s], A.a[2][s], A.a[3][s]);
+  q.hdr[r * kThreads + q.tid] = make_uint2(A.base, A.X | (live << 8));
+  q.st = (np == 0 ? (live | (hr << 8)) : (q.st & 0x1ffu)) | ((np + 1) << 9);
+}
+
+// Zeroes the slots in `dep` (branch-free selects).
+__device__ __forceinline__ void agg_zero(CornerAgg& A, uint32_t dep) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const bool z = (dep >> s) & 1u;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) A.a[c][s] = z ? 0.f : A.a[c][s];
+  }
+  A.nz &= ~dep;
+}
+
+// agg_enter for the record ring.
+__device__ __forceinline__ bool ring_enter(CornerAgg& A, RingQueue& q, const DevGrid& g,
+                                           const Sample& s) {
+  if (s.base == A.base) return false;
+  if (A.base != kNoCell) {
+    const int dx = s.cx - A.cx, dy = s.cy - A.cy, dz = s.cz - A.cz;
+    uint32_t dep = 0xffu, M = 0;
+    if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) {
+      dep = 0;
+      if (dx != 0) dep |= ((A.X & 1u) ^ (uint32_t)(dx < 0)) ? 0xAAu : 0x55u;
+      if (dy != 0) dep |= (((A.X >> 1) & 1u) ^ (uint32_t)(dy < 0)) ? 0xCCu : 0x33u;
+      if (dz != 0) dep |= (((A.X >> 2) & 1u) ^ (uint32_t)(dz < 0)) ? 0xF0u : 0x0Fu;
+      M = (uint32_t)(dx != 0) | ((uint32_t)(dy != 0) << 1) | ((uint32_t)(dz != 0) << 2);
+    }
+    const uint32_t live = dep & A.nz;
+    if (live) {
+      ring_push(q, A, live);
+      agg_zero(A, dep);
+    }
+    A.X ^= M;
+  }
+  A.base = s.base;
+  A.cx = s.cx;
+  A.cy = s.cy;
+  A.cz = s.cz;
+  return true;
+}
+
+// One merged pop round over the rings.
+__device__ __forceinline__ void ring_pop_merge(RingQueue& q, const DevGrid& g,
+                                               float4* __restrict__ grad, const float (&bf)[9],
+                                               float4 (*stage)[kVec4PerVertex]) {
+  const bool has = q.pending() != 0;
+  uint32_t v = 0;
+  float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (has) {
+    const uint32_t pm = q.st & 0xffu, hr = (q.st >> 8) & 1u;
+    const int sl = __ffs(pm) - 1;
+    const uint2 h = q.hdr[hr * kThreads + q.tid];
+    v = h.x + corner_off(g, (uint32_t)sl ^ (h.y & 7u));
+    e = q.rec[(size_t)(hr * 8 + sl) * kThreads + q.tid];
+    const uint32_t rest = pm & (pm - 1);
+    if (rest) {
+      q.st = (q.st & ~0xffu) | rest;
+    } else {
+      const uint32_t np = q.pending() - 1, nh = hr ^ 1u;
+      const uint32_t npm = np ? (q.hdr[nh * kThreads + q.tid].y >> 8) : 0u;
+      q.st = npm | (nh << 8) | (np << 9);
+    }
+  }
+  pop_entry(has, v, e, grad, bf, stage);
+}
+
 template <int MINB, int POPS>
 __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd,
@@ -1369,14 +1475,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
     const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
     float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
-    const SampleRec* __restrict__ rec, int K, const int* __restrict__ rec_count) {
+    RecBuf rec, int K, const int* __restrict__ rec_count) {
   // dynamic shared memory (kQMergeSmemBytes): the rings, [kQ][kThreads] float4 +
   // u32, then the per-warp merge staging [32][7] float4
   extern __shared__ __align__(16) float4 s_dyn[];
+#if VRF_K2_RING
+  // (kRingSmemBytes): the record rings [2][8][kThreads] float4, their headers
+  // [2][kThreads] uint2, then the per-warp merge staging
+  float4* s_rr = s_dyn;
+  uint2* s_rh = reinterpret_cast<uint2*>(s_dyn + kRingRecs * 8 * kThreads);
+  float4 (*stage)[kVec4PerVertex] = reinterpret_cast<float4 (*)[kVec4PerVertex]>(
+      s_dyn + kRingRecs * 8 * kThreads + kRingRecs * kThreads / 2) + (threadIdx.x & ~31);
+#else
   float4* s_qa = s_dyn;
   uint32_t* s_qv = reinterpret_cast<uint32_t*>(s_dyn + kQ * kThreads);
   float4 (*stage)[kVec4PerVertex] = reinterpret_cast<float4 (*)[kVec4PerVertex]>(
       s_dyn + kQ * kThreads + kQ * kThreads / 4) + (threadIdx.x & ~31);
+#endif
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   // ---- per-ray setup; a lane with nothing to scatter keeps c = -1 but stays in
   // the loop (the loop's exit vote is warp-wide)
@@ -1427,16 +1542,43 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
   CornerAgg A;
   agg_init(A);
   int last_tb = -1;
+#if VRF_K2_RING
+  RingQueue q{s_rr, s_rh, (int)threadIdx.x, 0u};
+#else
   QueueSink q{s_qv, s_qa, (int)threadIdx.x, 0u};
   uint32_t head = 0;
+#endif
   bool final_pending = c >= 0;  // the last cell's 8 corners, flushed after the walk
   // records are prefetched one iteration ahead: the dependent load of the next
   // record overlaps this sample's math and scatter
-  float4 n0 = make_float4(0.f, 0.f, 0.f, 0.f), n1 = n0;
+  float4 n0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint2 n1 = make_uint2(0u, 0u);
   if (c >= 0) load_record(rec, t, c, K, n0, n1);
+#if VRF_K2_RING
+  while (__any_sync(0xffffffffu, c >= 0 || final_pending || q.pending() != 0)) {
+    if (c >= 0) {
+      const float4 q0 = n0;
+      const uint2 q1 = n1;
+      if (c > 0) load_record(rec, t, c - 1, K, n0, n1);
+      --c;
+      RecSample r;
+      decode_record(g, wr, q0, q1, r);
+      if (ring_enter(A, q, g, rec_cell(r))) mark_touched(g, r.cx, r.cy, r.cz, last_tb);
+      walk_sample(A, r, upc0, upc1, upc2, upd, Sc0, Sc1, Sc2, Sd);
+    } else if (final_pending && q.pending() < (uint32_t)kRingRecs) {
+      final_pending = false;
+      if (A.nz) ring_push(q, A, A.nz);
+    }
+#pragma unroll
+    for (int r = 0; r < POPS; ++r) ring_pop_merge(q, g, grad, bf, stage);
+    while (__any_sync(0xffffffffu, q.pending() >= (uint32_t)kRingRecs))
+      ring_pop_merge(q, g, grad, bf, stage);
+  }
+#else
   while (__any_sync(0xffffffffu, c >= 0 || final_pending || head != q.tail)) {
     if (c >= 0) {
-      const float4 q0 = n0, q1 = n1;
+      const float4 q0 = n0;
+      const uint2 q1 = n1;
       if (c > 0) load_record(rec, t, c - 1, K, n0, n1);
       --c;
       RecSample r;
@@ -1459,6 +1601,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     while (__any_sync(0xffffffffu, q.tail - head > (uint32_t)(kQ - 8)))
       queue_pop_merge(q, head, grad, bf, stage);
   }
+#endif
 }
 
 // ------------------------------------------------------------------ K3 deterministic records
@@ -2073,7 +2216,7 @@ int map_forward_rec_blocks(int n) {
 void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
                             const double4* rgbd, const DevPose* poses, int n_frames,
                             const int* batch, int n, double4* ray_cd, uint8_t* flags,
-                            MapPartial* partials, int* err, const uint32_t* order, SampleRec* rec,
+                            MapPartial* partials, int* err, const uint32_t* order, RecBuf rec,
                             int K, int* rec_count, cudaStream_t s) {
   if (n <= fwd_group_max()) {
     k_map_forward_rec_g<<<map_forward_rec_blocks(n), kThreads, 0, s>>>(
@@ -2106,7 +2249,7 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
                              const double4* rgbd, const DevPose* poses, const int* batch, int n,
                              const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
                              const int* global_counts, float4* grad, double lambda_d,
-                             const uint32_t* order, const SampleRec* rec, int K,
+                             const uint32_t* order, RecBuf rec, int K,
                              const int* rec_count, cudaStream_t s) {
   if (n <= bwd_group_max()) {  // small batch: 8 lanes per ray (K2g)
     k_map_backward_g<<<(n + kThreads / 8 - 1) / (kThreads / 8), kThreads, 0, s>>>(
@@ -2117,11 +2260,12 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
   // K2q: 4 CTAs/SM (VRF_K2_MINB), 2 pops per step. r01 (config 3 / config 4, ms): 1, 2 or 3
   // pops 14.54 / 14.63 / 15.02 and 25.82 / 25.71 / 25.78.
   constexpr int kMinB = VRF_K2_MINB, kPops = 2;
+  constexpr int kSmem = VRF_K2_RING ? kRingSmemBytes : kQMergeSmemBytes;
   static const bool attr = cudaFuncSetAttribute(k_map_backward_q<kMinB, kPops>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                kQMergeSmemBytes) == cudaSuccess;
+                                                kSmem) == cudaSuccess;
   (void)attr;
-  k_map_backward_q<kMinB, kPops><<<(n + kThreads - 1) / kThreads, kThreads, kQMergeSmemBytes, s>>>(
+  k_map_backward_q<kMinB, kPops><<<(n + kThreads - 1) / kThreads, kThreads, kSmem, s>>>(
       g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
       order, rec, K, rec_count);
 }

@@ -158,7 +158,7 @@ void launch_backward_fast(vrf_context* ctx, const vrf_mapping_config* cfg, const
                               (const uint8_t*)ctx->s_flags.ptr, ctx->d_stats, global_counts,
                               (float4*)ctx->grad, cfg->lambda_d,
                               (const uint32_t*)ctx->s_order.ptr,
-                              (const SampleRec*)ctx->s_rec.ptr, ctx->rec_K,
+                              rec_planes(ctx->s_rec.ptr, ctx->rec_slots), ctx->rec_K,
                               (const int*)ctx->s_reccount.ptr, ctx->stream);
       LAUNCHED(1);
     }
