@@ -518,7 +518,7 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
              !try_ensure(ctx->stream, ctx->s_rec, kRecBytes * nn32 * (size_t)K))
         K /= 2;
       if (K >= kmin) {
-        if ((rc = ensure(ctx, ctx->s_reccount, sizeof(int) * nn))) return rc;
+        if ((rc = ensure(ctx, ctx->s_reccount, sizeof(int2) * nn))) return rc;
         ctx->rec_K = (int)(K & ~3LL);
         ctx->rec_slots = nn32 * (size_t)ctx->rec_K;
       }
@@ -530,7 +530,7 @@ inline int map_forward_dev(vrf_context* ctx, const vrf_mapping_config* cfg, cons
                              (MapPartial*)ctx->s_partials.ptr, ctx->d_err,
                              (const uint32_t*)ctx->s_order.ptr,
                              rec_planes(ctx->s_rec.ptr, ctx->rec_slots),
-                             ctx->rec_K, (int*)ctx->s_reccount.ptr, ctx->stream);
+                             ctx->rec_K, (int2*)ctx->s_reccount.ptr, ctx->stream);
     else
       launch_map_forward(g, p, dev_cam(&ctx->fintr), ctx->rgbd, ctx->poses, ctx->n_frames,
                          batch_dev, n, (double4*)ctx->s_raycd.ptr, (uint8_t*)ctx->s_flags.ptr,

@@ -30,13 +30,15 @@ struct PosePartial {
 enum FlagBits : uint8_t { kHit = 1, kDepthValid = 2, kOverflow = 4 };
 
 // Per-sample record of the fast mapping forward (24 B in two planes), consumed by
-// the reverse-order backward. Plane a (float4): w_i, T_{i+1}, the clamped colour
-// as 16-bit fixed point in [0, 1] (c0 | c1 << 16, c2 | flags << 16; flags = clamp
-// bits 0-2 and sigma_raw > 0 in bit 3). Plane b (uint2): the sample's cell
-// (cx | cy << 10 | cz << 20, located in FP64 by the forward) and its segment
-// midpoint t (fp32). The backward re-derives only the trilinear weights, in fp32
-// (r01's 24 B record re-located the cell in FP64; r02's first 32 B record kept
-// fp32 colour). Both planes share the slot index rec_index(t, c, K).
+// the reverse-order backward. Plane a (float4): w_i and the clamped colour, each
+// channel negated when its clamp fired (sign bit = clamp flag). Plane b (uint2):
+// the sample's cell (cx | cy << 10 | cz << 20, located in FP64 by the forward)
+// with sigma_raw > 0 in bit 30, and its segment midpoint t (fp32). T_{i+1} is not
+// stored: the walk rebuilds it from the ray's final T (rec_count[t].y) as
+// T_i = T_{i+1} + w_i. The backward re-derives only the trilinear weights, in
+// fp32. Both planes share the slot index rec_index(t, c, K). (r01 stored 24 B
+// and re-located the cell in FP64; r02's first record was 32 B with T and the
+// flags in separate words: K0 9.15 ms against 8.70 here.)
 struct RecBuf {
   float4* a;
   uint2* b;
@@ -46,8 +48,7 @@ constexpr size_t kRecBytes = sizeof(float4) + sizeof(uint2);
 inline RecBuf rec_planes(void* base, size_t slots) {
   return RecBuf{(float4*)base, (uint2*)((char*)base + slots * sizeof(float4))};
 }
-constexpr float kRecColorScale = 65535.f;
-constexpr uint32_t kRecSigmaPos = 8;
+constexpr uint32_t kRecSigmaPos = 1u << 30;  // in the cell word
 constexpr int kRecMaxCells = 1024;  // per axis (10-bit cell coordinates in the record)
 __host__ __device__ __forceinline__ uint32_t pack_cell(int cx, int cy, int cz) {
   return (uint32_t)cx | ((uint32_t)cy << 10) | ((uint32_t)cz << 20);
@@ -69,14 +70,14 @@ int map_forward_blocks(int n);
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s);
 // Fast forward that also stores up to K sample records per ray, warp-tiled sample-major
 // (rec_index(slot, c, K), slot = coherent order index); rays with more samples get
-// kOverflow. rec_count[slot] = samples stored.
+// kOverflow. rec_count[slot] = (samples stored, final T as float bits).
 // CTAs of the K0 launch for n rays (the small-batch K0g has 16 rays per CTA).
 int map_forward_rec_blocks(int n);
 void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
                             const double4* rgbd, const DevPose* poses, int n_frames,
                             const int* batch, int n, double4* ray_cd, uint8_t* flags,
                             MapPartial* partials, int* err, const uint32_t* order, RecBuf rec,
-                            int K, int* rec_count, cudaStream_t s);
+                            int K, int2* rec_count, cudaStream_t s);
 // Backward over the records (no payload gathers); kOverflow rays are
 // left to launch_map_backward(..., overflow_only = true).
 void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
@@ -84,7 +85,7 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
                              const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
                              const int* global_counts, float4* grad, double lambda_d,
                              const uint32_t* order, const RecBuf rec, int K,
-                             const int* rec_count, cudaStream_t s);
+                             const int2* rec_count, cudaStream_t s);
 void launch_map_backward(const DevGrid& g, const DevParams& p, const DevCam& cam,
                          const double4* rgbd, const DevPose* poses, const int* batch, int n,
                          const double4* ray_cd, const uint8_t* flags, const MapStats* stats,

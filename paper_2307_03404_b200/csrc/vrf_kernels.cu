@@ -207,19 +207,17 @@ __device__ __forceinline__ size_t rec_index(int t, int c, int K) {
   return ((size_t)(t >> 5) * (size_t)K + (size_t)c) * 32 + (size_t)(t & 31);
 }
 
-// Stores one sample record (vrf_internal.h: RecBuf): two coalesced stores per
-// warp (16 B + 8 B per lane), colour as 16-bit fixed point.
-__device__ __forceinline__ void store_record(RecBuf rec, size_t idx, double wgt, double T,
-                                             const Shade& sh, int cx, int cy, int cz,
-                                             double tm) {
-  const uint32_t fl = (sh.clamped[0] ? 1u : 0u) | (sh.clamped[1] ? 2u : 0u) |
-                      (sh.clamped[2] ? 4u : 0u) | (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
-  const uint32_t q0 = __float2uint_rn((float)sh.c[0] * kRecColorScale);
-  const uint32_t q1 = __float2uint_rn((float)sh.c[1] * kRecColorScale);
-  const uint32_t q2 = __float2uint_rn((float)sh.c[2] * kRecColorScale);
-  rec.a[idx] = make_float4((float)wgt, (float)T, __uint_as_float(q0 | (q1 << 16)),
-                           __uint_as_float(q2 | (fl << 16)));
-  rec.b[idx] = make_uint2(pack_cell(cx, cy, cz), __float_as_uint((float)tm));
+// Stores one sample record (vrf_internal.h: RecBuf): a 16 B and an 8 B store.
+// A clamped channel's colour is stored negated (its sign bit is the clamp
+// flag; the clamped value is 0 or 1, and -0.f keeps the bit).
+__device__ __forceinline__ void store_record(RecBuf rec, size_t idx, double wgt, const Shade& sh,
+                                             int cx, int cy, int cz, double tm) {
+  float c[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) c[ch] = sh.clamped[ch] ? -(float)sh.c[ch] : (float)sh.c[ch];
+  rec.a[idx] = make_float4((float)wgt, c[0], c[1], c[2]);
+  rec.b[idx] = make_uint2(pack_cell(cx, cy, cz) | (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u),
+                          __float_as_uint((float)tm));
 }
 
 // Fast forward (fp32 SH) that records every composited sample for the
@@ -241,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
     double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
     const uint32_t* __restrict__ order, RecBuf rec, int K,
-    int* __restrict__ rec_count) {
+    int2* __restrict__ rec_count) {
   __shared__ double s_d[32];
   __shared__ long long s_l[32];
   __shared__ int s_i[32];
@@ -254,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
     const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
     uint8_t fl = 0;
     int stored = 0;
+    float tfin = 1.f;  // T after the ray's last composited sample
     if (f < 0 || f >= n_frames || px < 0 || px >= cam.width || py < 0 || py >= cam.height) {
       atomicOr(err, 2);  // generate_ray: pixel outside image
     } else {
@@ -287,8 +286,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
           double decay;
           const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
           if (st.count <= K) {
-            store_record(rec, rec_index(t, st.count - 1, K), wgt, st.T, sh, s.cx, s.cy, s.cz,
-                         s.t);
+            store_record(rec, rec_index(t, st.count - 1, K), wgt, sh, s.cx, s.cy, s.cz, s.t);
           }
           if (st.terminated) break;
         }
@@ -302,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
         fl |= kHit;
         if (st.count > K) fl |= kOverflow;
         stored = st.count > K ? 0 : st.count;
+        tfin = (float)st.T;
         mc = 1;
         samples = st.count;
         const double r0 = dsub(st.C[0], tg.x), r1 = dsub(st.C[1], tg.y), r2 = dsub(st.C[2], tg.z);
@@ -321,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
       ray_cd[i] = make_double4(st.C[0], st.C[1], st.C[2], st.D);
     }
     flags[i] = fl;
-    rec_count[t] = stored;
+    rec_count[t] = make_int2(stored, __float_as_int(tfin));
   }
   const double blp = block_sum(lp, s_d);
   const double blg = block_sum(lg, s_d);
@@ -398,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_coop(
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
     double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
     const uint32_t* __restrict__ order, RecBuf rec, int K,
-    int* __restrict__ rec_count) {
+    int2* __restrict__ rec_count) {
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ double s_d[32];
   __shared__ long long s_l[32];
@@ -477,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_coop(
         double decay;
         const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
         if (st.count <= K) {
-          store_record(rec, rec_index(t, st.count - 1, K), wgt, st.T, sh, s.cx, s.cy, s.cz, s.t);
+          store_record(rec, rec_index(t, st.count - 1, K), wgt, sh, s.cx, s.cy, s.cz, s.t);
         }
         if (st.terminated) alive = false;
       }
@@ -487,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_coop(
   if (t < n) {
     uint8_t fl = 0;
     int stored = 0;
+    float tfin = 1.f;  // T after the ray's last composited sample
     if (valid) {
       if (st.count == 0) {
         st.C[0] = st.C[1] = st.C[2] = 0.0;
@@ -498,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_coop(
         fl |= kHit;
         if (st.count > K) fl |= kOverflow;
         stored = st.count > K ? 0 : st.count;
+        tfin = (float)st.T;
         mc = 1;
         samples = st.count;
         const double r0 = dsub(st.C[0], tg.x), r1 = dsub(st.C[1], tg.y), r2 = dsub(st.C[2], tg.z);
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_coop(
       ray_cd[i] = make_double4(st.C[0], st.C[1], st.C[2], st.D);
     }
     flags[i] = fl;
-    rec_count[t] = stored;
+    rec_count[t] = make_int2(stored, __float_as_int(tfin));
   }
   const double blp = block_sum(lp, s_d);
   const double blg = block_sum(lg, s_d);
@@ -661,7 +662,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
     const DevPose* __restrict__ poses, int n_frames, const int* __restrict__ batch, int n,
     double4* __restrict__ ray_cd, uint8_t* __restrict__ flags, MapPartial* partials, int* err,
     const uint32_t* __restrict__ order, RecBuf rec, int K,
-    int* __restrict__ rec_count) {
+    int2* __restrict__ rec_count) {
   constexpr int LPR = kFwdLanes;
   __shared__ double s_d[32];
   __shared__ long long s_l[32];
@@ -678,6 +679,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
     const int f = batch[3 * i], px = batch[3 * i + 1], py = batch[3 * i + 2];
     uint8_t fl = 0;
     int stored = 0;
+    float tfin = 1.f;  // T after the ray's last composited sample
     if (f < 0 || f >= n_frames || px < 0 || px >= cam.width || py < 0 || py >= cam.height) {
       if (lead) atomicOr(err, 2);  // generate_ray: pixel outside image
     } else {
@@ -750,8 +752,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
           double decay;
           const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
           if (lead && st.count <= K) {
-            store_record(rec, rec_index(t, st.count - 1, K), wgt, st.T, sh, s.cx, s.cy, s.cz,
-                         s.t);
+            store_record(rec, rec_index(t, st.count - 1, K), wgt, sh, s.cx, s.cy, s.cz, s.t);
           }
           if (st.terminated) break;
         }
@@ -765,6 +766,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
         fl |= kHit;
         if (st.count > K) fl |= kOverflow;
         stored = st.count > K ? 0 : st.count;
+        tfin = (float)st.T;
         mc = 1;
         samples = st.count;
         const double r0 = dsub(st.C[0], tg.x), r1 = dsub(st.C[1], tg.y), r2 = dsub(st.C[2], tg.z);
@@ -785,7 +787,7 @@ __global__ void __launch_bounds__(kThreads) k_map_forward_rec_g(
     }
     if (lead) {
       flags[i] = fl;
-      rec_count[t] = stored;
+      rec_count[t] = make_int2(stored, __float_as_int(tfin));
     }
   }
   if (!lead) {  // one contribution per ray
@@ -1055,26 +1057,22 @@ struct RecSample {
   int cx, cy, cz;
   uint32_t base;
   float fx, fy, fz;
-  float tm, delta, w, Tn, c0, c1, c2;
+  float tm, delta, w, c0, c1, c2;
   uint32_t kf;
 };
-__device__ __forceinline__ float rec_color(uint32_t q) {
-  return (float)(q & 0xffffu) * (1.f / kRecColorScale);
-}
 __device__ __forceinline__ void decode_record(const DevGrid& g, const WalkRay& m, float4 q0,
                                               uint2 q1, RecSample& r) {
   r.w = q0.x;
-  r.Tn = q0.y;
-  const uint32_t c01 = __float_as_uint(q0.z), c2f = __float_as_uint(q0.w);
-  r.c0 = rec_color(c01);
-  r.c1 = rec_color(c01 >> 16);
-  r.c2 = rec_color(c2f);
-  r.kf = c2f >> 16;
+  r.c0 = fabsf(q0.y);
+  r.c1 = fabsf(q0.z);
+  r.c2 = fabsf(q0.w);
+  r.kf = (q1.x & kRecSigmaPos) | (__float_as_uint(q0.y) >> 31) |
+         ((__float_as_uint(q0.z) >> 31) << 1) | ((__float_as_uint(q0.w) >> 31) << 2);
   const uint32_t cell = q1.x;
   r.tm = __uint_as_float(q1.y);
   r.cx = (int)(cell & 1023u);
   r.cy = (int)((cell >> 10) & 1023u);
-  r.cz = (int)(cell >> 20);
+  r.cz = (int)((cell >> 20) & 1023u);
   r.base = (uint32_t)r.cx + (uint32_t)g.rx * ((uint32_t)r.cy + (uint32_t)g.ry * (uint32_t)r.cz);
   r.delta = fminf(m.step, 2.f * (m.hi - r.tm));
   const float iv = (float)g.rcp_voxel;
@@ -1105,16 +1103,20 @@ __device__ __forceinline__ Sample rec_cell(const RecSample& r) {
 
 // Suffix-form sample upstream of the reverse walk (see K2q) and the aggregate
 // update; Sc / Sd advance past the sample (fp32: the fast path's precision).
+// Tn = T_{i+1} of this sample on entry (the walk starts from the ray's final T)
+// and T_i on exit: T_i = T_{i+1} + w_i (renderer.cpp's w_i = T_i alpha_i,
+// T_{i+1} = T_i (1 - alpha_i)).
 __device__ __forceinline__ void walk_sample(CornerAgg& A, const RecSample& r, float upc0,
                                             float upc1, float upc2, float upd, float& Sc0,
-                                            float& Sc1, float& Sc2, float& Sd) {
-  float ds = upc0 * (r.c0 * r.Tn - Sc0) + upc1 * (r.c1 * r.Tn - Sc1) + upc2 * (r.c2 * r.Tn - Sc2);
-  ds = fmaf(upd, r.tm * r.Tn - Sd, ds);
+                                            float& Sc1, float& Sc2, float& Sd, float& Tn) {
+  float ds = upc0 * (r.c0 * Tn - Sc0) + upc1 * (r.c1 * Tn - Sc1) + upc2 * (r.c2 * Tn - Sc2);
+  ds = fmaf(upd, r.tm * Tn - Sd, ds);
   ds *= r.delta;
   Sc0 = fmaf(r.c0, r.w, Sc0);
   Sc1 = fmaf(r.c1, r.w, Sc1);
   Sc2 = fmaf(r.c2, r.w, Sc2);
   Sd = fmaf(r.tm, r.w, Sd);
+  Tn += r.w;
   agg_add(A, r.fx, r.fy, r.fz, (r.kf & kRecSigmaPos) ? ds : 0.f,
           (r.kf & 1u) ? 0.f : upc0 * r.w, (r.kf & 2u) ? 0.f : upc1 * r.w,
           (r.kf & 4u) ? 0.f : upc2 * r.w);
@@ -1135,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
     const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
     const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
     float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
-    RecBuf rec, int K, const int* __restrict__ rec_count) {
+    RecBuf rec, int K, const int2* __restrict__ rec_count) {
   constexpr int LPR = 8;
   const int lane = threadIdx.x & 31, sub = lane & (LPR - 1), gbase = lane & ~(LPR - 1);
   const unsigned gmask = ((1u << LPR) - 1u) << gbase;
@@ -1161,32 +1163,37 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
   }
   if (!march_begin(g, p, m)) return;
   const WalkRay wr = walk_ray(m);
-  const int cnt = rec_count[t];
+  const int2 rc = rec_count[t];
+  const int cnt = rc.x;
   const int L = (cnt + LPR - 1) / LPR;
   const int c0 = sub * L, c1 = min(cnt, c0 + L);  // this lane's records [c0, c1)
   // pass 1: chunk sums of c_ch w and t w
-  float P0 = 0.f, P1 = 0.f, P2 = 0.f, Pd = 0.f;
+  float P0 = 0.f, P1 = 0.f, P2 = 0.f, Pd = 0.f, Pw = 0.f;
   for (int c = c0; c < c1; ++c) {
     float4 q0;
     uint2 q1;
     load_record(rec, t, c, K, q0, q1);
-    const uint32_t c01 = __float_as_uint(q0.z);
-    P0 = fmaf(rec_color(c01), q0.x, P0);
-    P1 = fmaf(rec_color(c01 >> 16), q0.x, P1);
-    P2 = fmaf(rec_color(__float_as_uint(q0.w)), q0.x, P2);
+    P0 = fmaf(fabsf(q0.y), q0.x, P0);
+    P1 = fmaf(fabsf(q0.z), q0.x, P1);
+    P2 = fmaf(fabsf(q0.w), q0.x, P2);
     Pd = fmaf(__uint_as_float(q1.y), q0.x, Pd);
+    Pw += q0.x;
   }
   // suffix sums of the later chunks (lanes sub+1 .. 7)
-  float Sc0 = 0.f, Sc1 = 0.f, Sc2 = 0.f, Sd = 0.f;
+  // (and T_{i+1} of the chunk's last record: the ray's final T plus the
+  // weights of the later chunks)
+  float Sc0 = 0.f, Sc1 = 0.f, Sc2 = 0.f, Sd = 0.f, Tn = __int_as_float(rc.y);
 #pragma unroll
   for (int j = LPR - 1; j > 0; --j) {
     const float a0 = __shfl_sync(gmask, P0, gbase + j), a1 = __shfl_sync(gmask, P1, gbase + j);
     const float a2 = __shfl_sync(gmask, P2, gbase + j), ad = __shfl_sync(gmask, Pd, gbase + j);
+    const float aw = __shfl_sync(gmask, Pw, gbase + j);
     if (j > sub) {
       Sc0 += a0;
       Sc1 += a1;
       Sc2 += a2;
       Sd += ad;
+      Tn += aw;
     }
   }
   const float upd = u.use_depth ? (float)u.upd : 0.f;
@@ -1201,7 +1208,8 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
     RecSample r;
     decode_record(g, wr, q0, q1, r);
     if (agg_enter(A, sink, g, rec_cell(r))) mark_touched(g, r.cx, r.cy, r.cz, last_tb);
-    walk_sample(A, r, (float)u.upc[0], (float)u.upc[1], (float)u.upc[2], upd, Sc0, Sc1, Sc2, Sd);
+    walk_sample(A, r, (float)u.upc[0], (float)u.upc[1], (float)u.upc[2], upd, Sc0, Sc1, Sc2, Sd,
+                Tn);
   }
   if (A.base != kNoCell) agg_flush(A, sink, g, 0xffu);
 }
@@ -1475,7 +1483,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     const double4* __restrict__ ray_cd, const uint8_t* __restrict__ flags,
     const MapStats* __restrict__ stats, const int* __restrict__ global_counts,
     float4* __restrict__ grad, double lambda_d, const uint32_t* __restrict__ order,
-    RecBuf rec, int K, const int* __restrict__ rec_count) {
+    RecBuf rec, int K, const int2* __restrict__ rec_count) {
   // dynamic shared memory (kQMergeSmemBytes): the rings, [kQ][kThreads] float4 +
   // u32, then the per-warp merge staging [32][7] float4
   extern __shared__ __align__(16) float4 s_dyn[];
@@ -1497,7 +1505,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
   // the loop (the loop's exit vote is warp-wide)
   int c = -1;
   WalkRay wr{};
-  float upc0 = 0.f, upc1 = 0.f, upc2 = 0.f, upd = 0.f;
+  float upc0 = 0.f, upc1 = 0.f, upc2 = 0.f, upd = 0.f, Tn = 1.f;
   float bf[9];
   for (int mm = 0; mm < 9; ++mm) bf[mm] = 0.f;
   if (t < n) {
@@ -1518,7 +1526,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
 #pragma unroll
           for (int mm = 0; mm < 9; ++mm) bf[mm] = (float)basis[mm];
           if (march_begin(g, p, m)) {
-            c = rec_count[t] - 1;
+            const int2 rc = rec_count[t];
+            c = rc.x - 1;
+            Tn = __int_as_float(rc.y);
             wr = walk_ray(m);
             upc0 = (float)u.upc[0];
             upc1 = (float)u.upc[1];
@@ -1564,7 +1574,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
       RecSample r;
       decode_record(g, wr, q0, q1, r);
       if (ring_enter(A, q, g, rec_cell(r))) mark_touched(g, r.cx, r.cy, r.cz, last_tb);
-      walk_sample(A, r, upc0, upc1, upc2, upd, Sc0, Sc1, Sc2, Sd);
+      walk_sample(A, r, upc0, upc1, upc2, upd, Sc0, Sc1, Sc2, Sd, Tn);
     } else if (final_pending && q.pending() < (uint32_t)kRingRecs) {
       final_pending = false;
       if (A.nz) ring_push(q, A, A.nz);
@@ -1584,7 +1594,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
       RecSample r;
       decode_record(g, wr, q0, q1, r);
       if (agg_enter(A, q, g, rec_cell(r))) mark_touched(g, r.cx, r.cy, r.cz, last_tb);
-      walk_sample(A, r, upc0, upc1, upc2, upd, Sc0, Sc1, Sc2, Sd);
+      walk_sample(A, r, upc0, upc1, upc2, upd, Sc0, Sc1, Sc2, Sd, Tn);
     } else if (final_pending && q.tail - head <= (uint32_t)(kQ - 8)) {
       final_pending = false;
       agg_flush(A, q, g, 0xffu);
@@ -2217,7 +2227,7 @@ void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& 
                             const double4* rgbd, const DevPose* poses, int n_frames,
                             const int* batch, int n, double4* ray_cd, uint8_t* flags,
                             MapPartial* partials, int* err, const uint32_t* order, RecBuf rec,
-                            int K, int* rec_count, cudaStream_t s) {
+                            int K, int2* rec_count, cudaStream_t s) {
   if (n <= fwd_group_max()) {
     k_map_forward_rec_g<<<map_forward_rec_blocks(n), kThreads, 0, s>>>(
         g, p, cam, rgbd, poses, n_frames, batch, n, ray_cd, flags, partials, err, order, rec, K,
@@ -2250,7 +2260,7 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
                              const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
                              const int* global_counts, float4* grad, double lambda_d,
                              const uint32_t* order, RecBuf rec, int K,
-                             const int* rec_count, cudaStream_t s) {
+                             const int2* rec_count, cudaStream_t s) {
   if (n <= bwd_group_max()) {  // small batch: 8 lanes per ray (K2g)
     k_map_backward_g<<<(n + kThreads / 8 - 1) / (kThreads / 8), kThreads, 0, s>>>(
         g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,

@@ -159,7 +159,7 @@ void launch_backward_fast(vrf_context* ctx, const vrf_mapping_config* cfg, const
                               (float4*)ctx->grad, cfg->lambda_d,
                               (const uint32_t*)ctx->s_order.ptr,
                               rec_planes(ctx->s_rec.ptr, ctx->rec_slots), ctx->rec_K,
-                              (const int*)ctx->s_reccount.ptr, ctx->stream);
+                              (const int2*)ctx->s_reccount.ptr, ctx->stream);
       LAUNCHED(1);
     }
     // without records: every ray; with records: only the rays that overflowed K
