@@ -461,6 +461,100 @@ __device__ __forceinline__ void shade_fast(const DevGrid& g, const Sample& s, co
   }
 }
 
+// Per-ray corner cache of the fast forward (K0). A corner's contribution to
+// shade_fast depends only on the ray (its basis) and the corner: (sigma_k,
+// sum_m basis_m v_k[ch,m]). Consecutive samples share corners: all 8 within a
+// cell, 4 across a face. The lane keeps the 8 corner contributions of its
+// current cell in shared memory, relabelled as K2's CornerAgg does (logical
+// corner k in slot k ^ X; a move along axes M refills the departing slots with
+// the entering corners and sets X ^= M), and gathers only the corners it has
+// not seen: ~3 of 8 per sample instead of 8. Same operations in the same order
+// as shade_fast, so the results are bit-identical.
+// VRF_K0_CACHE=1 (A/B build, tools/ab/k0_cache.sh): K0 shades through the
+// corner cache. It cuts K0's L1 data-pipe wavefronts by 28 % and its global
+// sectors by half, but the per-corner branch diverges (+14 % warp instructions)
+// and K0 turns latency-bound: config 3 9.07 ms against 8.68, config 4 27.8
+// against 28.7 (r02). A predicated, branch-free form spilled and took 11.2 ms.
+#ifndef VRF_K0_CACHE
+#define VRF_K0_CACHE 0
+#endif
+constexpr int kCacheStride = 128;  // threads per CTA of the kernels that use it
+struct CornerCache {
+  float4* slot0;  // this lane's slot 0; slot s at slot0[s * kCacheStride]
+  uint32_t X;
+  uint32_t cell;  // pack_cell of the cached cell; 0xffffffff: empty
+};
+__device__ __forceinline__ uint32_t cache_pack(int cx, int cy, int cz) {
+  return (uint32_t)cx | ((uint32_t)cy << 10) | ((uint32_t)cz << 20);
+}
+// Slots (bit s = slot s) to refill for the sample's cell, updating X / cell.
+__device__ __forceinline__ uint32_t cache_enter(CornerCache& cc, const Sample& s) {
+  const uint32_t key = cache_pack(s.cx, s.cy, s.cz);
+  if (key == cc.cell) return 0u;
+  uint32_t dep = 0xffu;
+  if (cc.cell != 0xffffffffu) {
+    const int dx = s.cx - (int)(cc.cell & 1023u), dy = s.cy - (int)((cc.cell >> 10) & 1023u),
+              dz = s.cz - (int)(cc.cell >> 20);
+    if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) {
+      dep = 0;
+      if (dx != 0) dep |= ((cc.X & 1u) ^ (uint32_t)(dx < 0)) ? 0xAAu : 0x55u;
+      if (dy != 0) dep |= (((cc.X >> 1) & 1u) ^ (uint32_t)(dy < 0)) ? 0xCCu : 0x33u;
+      if (dz != 0) dep |= (((cc.X >> 2) & 1u) ^ (uint32_t)(dz < 0)) ? 0xF0u : 0x0Fu;
+      cc.X ^= (uint32_t)(dx != 0) | ((uint32_t)(dy != 0) << 1) | ((uint32_t)(dz != 0) << 2);
+    }
+  }
+  cc.cell = key;
+  return dep;
+}
+__device__ __forceinline__ void shade_cached(const DevGrid& g, const Sample& s, const double w[8],
+                                             const float bf[9], CornerCache& cc, Shade& out) {
+  const uint32_t refill = cache_enter(cc, s);
+  double sraw = 0.0;
+  float cr = 0.f, cg = 0.f, cb = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t sl = (uint32_t)k ^ cc.X;
+    float4* cp = cc.slot0 + sl * kCacheStride;
+    float4 cv;
+    if ((refill >> sl) & 1u) {
+      const float4* vp = g.payload + (size_t)corner_index(g, s.base, k) * kVec4PerVertex;
+      float v[28];
+#pragma unroll
+      for (int j = 0; j < kVec4PerVertex; ++j) {
+        const float4 a = __ldg(vp + j);
+        v[4 * j] = a.x;
+        v[4 * j + 1] = a.y;
+        v[4 * j + 2] = a.z;
+        v[4 * j + 3] = a.w;
+      }
+      float dr = 0.f, dg = 0.f, db = 0.f;
+#pragma unroll
+      for (int m = 0; m < 9; ++m) {
+        dr = fmaf(bf[m], v[1 + m], dr);
+        dg = fmaf(bf[m], v[10 + m], dg);
+        db = fmaf(bf[m], v[19 + m], db);
+      }
+      cv = make_float4(v[0], dr, dg, db);
+      *cp = cv;
+    } else {
+      cv = *cp;
+    }
+    sraw = dadd(sraw, dmul(w[k], (double)cv.x));
+    const float wk = (float)w[k];
+    cr = fmaf(wk, cv.y, cr);
+    cg = fmaf(wk, cv.z, cg);
+    cb = fmaf(wk, cv.w, cb);
+  }
+  out.sigma_raw = sraw;
+  const float c3[3] = {cr, cg, cb};
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const double v = 0.5 + (double)c3[ch];
+    out.clamped[ch] = (v <= 0.0 || v >= 1.0);
+    out.c[ch] = (v < 0.0) ? 0.0 : ((1.0 < v) ? 1.0 : v);
+  }
+}
+
 template <typename ShT>
 __device__ __forceinline__ void shade(const DevGrid& g, const Sample& s, const double w[8],
                                       const double basis[9], Shade& out) {

@@ -243,6 +243,10 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
   __shared__ double s_d[32];
   __shared__ long long s_l[32];
   __shared__ int s_i[32];
+#if VRF_K0_CACHE
+  static_assert(kThreads == kCacheStride, "corner cache layout");
+  __shared__ float4 s_cache[8 * kThreads];
+#endif
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = (order && t < n) ? (int)order[t] : t;
   double lp = 0.0, lg = 0.0;
@@ -276,12 +280,19 @@ __global__ void __launch_bounds__(kThreads, VRF_K0_MINB) k_map_forward_rec(
         atomicOr(err, 1);
       } else if (march_begin(g, p, m)) {
         Sample s;
+#if VRF_K0_CACHE
+        CornerCache cc{s_cache + threadIdx.x, 0u, 0xffffffffu};
+#endif
         while (march_next(g, m, s)) {
           Shade sh;
           {
             double w[8];
             corner_weights(s, w);
+#if VRF_K0_CACHE
+            shade_cached(g, s, w, bf, cc, sh);
+#else
             shade_fast(g, s, w, bf, sh);
+#endif
           }
           double decay;
           const double wgt = composite_step(st, sh, s.t, s.delta, p.eps, decay);
