@@ -1244,6 +1244,9 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 #ifndef VRF_K2_POP2
 #define VRF_K2_POP2 0  // A/B: load both pops' queue entries up front
 #endif
+#ifndef VRF_K2_MERGE_MIN
+#define VRF_K2_MERGE_MIN 2  // smallest duplicate group merged before the reduction
+#endif
 #ifndef VRF_K2_MINB
 #define VRF_K2_MINB 4  // CTAs per SM: 128 registers (r02: 11.8 vs 12.5 ms at 3)
 #endif
@@ -1276,7 +1279,13 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
                                           float4 (*stage)[kVec4PerVertex]) {
   if (has) {
     const unsigned act = __activemask();
+#if VRF_K2_MERGE_MIN > 2
+    // A/B: groups smaller than VRF_K2_MERGE_MIN reduce lane by lane
+    unsigned grp = __match_any_sync(act, v);
+    if (__popc(grp) < VRF_K2_MERGE_MIN) grp = 1u << (threadIdx.x & 31);
+#else
     const unsigned grp = __match_any_sync(act, v);
+#endif
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(grp) - 1;
     float x[28];
@@ -1412,8 +1421,25 @@ struct RingQueue {
   __device__ __forceinline__ uint32_t pending() const { return st >> 9; }
 };
 
-// Stores the aggregate's slots `live` (nonzero) as the lane's next record.
+#ifndef VRF_K2_POP_LOGICAL
+#define VRF_K2_POP_LOGICAL 1
+#endif
+// Slot mask -> logical-corner mask (bit k = slot k ^ X).
+__device__ __forceinline__ uint32_t slots_to_corners(uint32_t m, uint32_t X) {
+  if (X & 1u) m = ((m & 0x55u) << 1) | ((m & 0xAAu) >> 1);
+  if (X & 2u) m = ((m & 0x33u) << 2) | ((m & 0xCCu) >> 2);
+  if (X & 4u) m = ((m & 0x0Fu) << 4) | ((m & 0xF0u) >> 4);
+  return m;
+}
+
+// Stores the aggregate's slots `live` (nonzero) as the lane's next record. The
+// record's pop mask is kept in logical-corner order (VRF_K2_POP_LOGICAL), so
+// neighbouring rays that leave the same cell pop its corners in the same order
+// and meet in the same pop round, where the merge catches them.
 __device__ __forceinline__ void ring_push(RingQueue& q, const CornerAgg& A, uint32_t live) {
+#if VRF_K2_POP_LOGICAL
+  live = slots_to_corners(live, A.X);
+#endif
   const uint32_t hr = (q.st >> 8) & 1u, np = q.pending();
   const uint32_t r = hr ^ np;  // np <= 1 here
   float4* d = q.rec + (size_t)r * 8 * kThreads + q.tid;
@@ -1471,9 +1497,14 @@ __device__ __forceinline__ void ring_pop_merge(RingQueue& q, const DevGrid& g,
   float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
   if (has) {
     const uint32_t pm = q.st & 0xffu, hr = (q.st >> 8) & 1u;
-    const int sl = __ffs(pm) - 1;
     const uint2 h = q.hdr[hr * kThreads + q.tid];
-    v = h.x + corner_off(g, (uint32_t)sl ^ (h.y & 7u));
+#if VRF_K2_POP_LOGICAL
+    const uint32_t k = (uint32_t)__ffs(pm) - 1u, sl = k ^ (h.y & 7u);
+    v = h.x + corner_off(g, k);
+#else
+    const uint32_t sl = (uint32_t)__ffs(pm) - 1u;
+    v = h.x + corner_off(g, sl ^ (h.y & 7u));
+#endif
     e = q.rec[(size_t)(hr * 8 + sl) * kThreads + q.tid];
     const uint32_t rest = pm & (pm - 1);
     if (rest) {
