@@ -141,6 +141,38 @@ def test_mapping_gradient_matches_oracle(ctx, oracle, deterministic):
         assert rel_err(grad, grad_o, 1e-4 * scale) < RTOL_GRAD
 
 
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_mapping_gradient_with_clamped_colour_and_free_space(ctx, oracle, deterministic):
+    """Colours that clamp (SH coefficients up to +-1.5) and samples with sigma_raw
+    <= 0 (sigma in [-0.3, 0.6]): the reference gates dL/dc per clamped channel and
+    dL/dsigma on sigma_raw > 0 (gradients.cpp:69-97). The fast path carries both
+    gates through its sample records (clamp flags in the colour sign bits, the
+    sigma gate in the cell word, vrf_internal.h)."""
+    grid, intr, frames = room_scene()
+    g0 = fresh_grid(grid, seed=8, sh_noise=1.5)
+    rng = np.random.default_rng(9)
+    g0.data[:, 0] = rng.uniform(-0.3, 0.6, g0.data.shape[0]).astype(np.float32)
+    cfg = MappingConfig(deterministic=deterministic)
+    batch = oracle.draw_batch(22, len(frames), intr.width, intr.height, 512)
+    ctx.load_grid(g0)
+    ctx.load_frames(intr, frames)
+    grad, st = ctx.mapping_gradient(cfg, batch)
+    _, _, grad_o, st_o = oracle.mapping_step(g0, frames, intr, cfg, batch, apply=False,
+                                             want_grad=True)
+    assert st.rays_color == st_o.rays_color and st.samples == st_o.samples
+    assert abs(st.loss_photometric - st_o.loss_photometric) <= 1e-9 * st_o.loss_photometric
+    # the gates fire: some colour rows of touched vertices are exactly zero in the
+    # reference (every contributing sample clamped), and some sigma entries too
+    touched_o = np.abs(grad_o).sum(1) > 0
+    assert np.any((grad_o[touched_o, 1:10] == 0).all(1))
+    assert np.any(grad_o[touched_o, 0] == 0)
+    assert np.array_equal(np.abs(grad).sum(1) > 0, touched_o)
+    assert np.array_equal(grad == 0, grad_o == 0)
+    scale = np.abs(grad_o).max()
+    tol = 1e-9 if deterministic else RTOL_GRAD
+    assert rel_err(grad, grad_o, (1e-9 if deterministic else 1e-4) * scale) < tol
+
+
 def test_deterministic_gradient_is_bit_reproducible(ctx, oracle):
     grid, intr, frames = room_scene()
     g0 = fresh_grid(grid, seed=4)
