@@ -1412,13 +1412,19 @@ __device__ __forceinline__ void queue_pop_merge2(const QueueSink& q, uint32_t& h
 constexpr int kRingRecs = 2;
 constexpr int kRingSmemBytes =
     kRingRecs * 8 * kThreads * 16 + kRingRecs * kThreads * 8 + kThreads * kVec4PerVertex * 16;
+#ifndef VRF_K2_HDR_REG
+#define VRF_K2_HDR_REG 1  // the head record's base and X in registers
+#endif
 struct RingQueue {
   float4* rec;   // [kRingRecs][8][kThreads] slot factors
   uint2* hdr;    // [kRingRecs][kThreads] (base vertex, X | live << 8)
   int tid;
   uint32_t st;   // bits 0-7: unpopped live slots of the head record; bit 8: head
-                 // record; bits 9+: records pending
-  __device__ __forceinline__ uint32_t pending() const { return st >> 9; }
+                 // record; bits 9-10: records pending; bits 16-18: the head's X
+#if VRF_K2_HDR_REG
+  uint32_t hbase;  // the head record's base vertex
+#endif
+  __device__ __forceinline__ uint32_t pending() const { return (st >> 9) & 3u; }
 };
 
 #ifndef VRF_K2_POP_LOGICAL
@@ -1446,7 +1452,16 @@ __device__ __forceinline__ void ring_push(RingQueue& q, const CornerAgg& A, uint
 #pragma unroll
   for (int s = 0; s < 8; ++s) d[s * kThreads] = make_float4(A.a[0][s], A.a[1][s], A.a[2][s], A.a[3][s]);
   q.hdr[r * kThreads + q.tid] = make_uint2(A.base, A.X | (live << 8));
+#if VRF_K2_HDR_REG
+  if (np == 0) {
+    q.st = live | (hr << 8) | (1u << 9) | (A.X << 16);
+    q.hbase = A.base;
+  } else {
+    q.st += 1u << 9;
+  }
+#else
   q.st = (np == 0 ? (live | (hr << 8)) : (q.st & 0x1ffu)) | ((np + 1) << 9);
+#endif
 }
 
 // Zeroes the slots in `dep` (branch-free selects).
@@ -1497,7 +1512,11 @@ __device__ __forceinline__ void ring_pop_merge(RingQueue& q, const DevGrid& g,
   float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
   if (has) {
     const uint32_t pm = q.st & 0xffu, hr = (q.st >> 8) & 1u;
+#if VRF_K2_HDR_REG
+    const uint2 h = make_uint2(q.hbase, (q.st >> 16) & 7u);
+#else
     const uint2 h = q.hdr[hr * kThreads + q.tid];
+#endif
 #if VRF_K2_POP_LOGICAL
     const uint32_t k = (uint32_t)__ffs(pm) - 1u, sl = k ^ (h.y & 7u);
     v = h.x + corner_off(g, k);
@@ -1511,8 +1530,15 @@ __device__ __forceinline__ void ring_pop_merge(RingQueue& q, const DevGrid& g,
       q.st = (q.st & ~0xffu) | rest;
     } else {
       const uint32_t np = q.pending() - 1, nh = hr ^ 1u;
+#if VRF_K2_HDR_REG
+      uint2 nx = make_uint2(0u, 0u);
+      if (np) nx = q.hdr[nh * kThreads + q.tid];
+      q.st = (nx.y >> 8) | (nh << 8) | (np << 9) | ((nx.y & 7u) << 16);
+      q.hbase = nx.x;
+#else
       const uint32_t npm = np ? (q.hdr[nh * kThreads + q.tid].y >> 8) : 0u;
       q.st = npm | (nh << 8) | (np << 9);
+#endif
     }
   }
   pop_entry(has, v, e, grad, bf, stage);
@@ -1595,7 +1621,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
   agg_init(A);
   int last_tb = -1;
 #if VRF_K2_RING
+#if VRF_K2_HDR_REG
+  RingQueue q{s_rr, s_rh, (int)threadIdx.x, 0u, 0u};
+#else
   RingQueue q{s_rr, s_rh, (int)threadIdx.x, 0u};
+#endif
 #else
   QueueSink q{s_qv, s_qa, (int)threadIdx.x, 0u};
   uint32_t head = 0;

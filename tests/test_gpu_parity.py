@@ -160,12 +160,16 @@ def test_mapping_gradient_with_clamped_colour_and_free_space(ctx, oracle, determ
     _, _, grad_o, st_o = oracle.mapping_step(g0, frames, intr, cfg, batch, apply=False,
                                              want_grad=True)
     assert st.rays_color == st_o.rays_color and st.samples == st_o.samples
-    assert abs(st.loss_photometric - st_o.loss_photometric) <= 1e-9 * st_o.loss_photometric
-    # the gates fire: some colour rows of touched vertices are exactly zero in the
-    # reference (every contributing sample clamped), and some sigma entries too
+    # (the fast forward contracts SH in fp32: ~1e-7 per channel at these coefficients)
+    ltol = 1e-9 if deterministic else 1e-6
+    assert abs(st.loss_photometric - st_o.loss_photometric) <= ltol * st_o.loss_photometric
+    # the clamp gate fires: some colour rows of touched vertices are exactly zero in
+    # the reference (every contributing sample clamped that channel). Samples with
+    # sigma_raw <= 0 have w = 0 and a gated dL/dsigma, so the vertices only they
+    # reach stay untouched: the zero patterns below must agree exactly.
     touched_o = np.abs(grad_o).sum(1) > 0
     assert np.any((grad_o[touched_o, 1:10] == 0).all(1))
-    assert np.any(grad_o[touched_o, 0] == 0)
+    assert np.mean(g0.data[:, 0] < 0) > 0.25
     assert np.array_equal(np.abs(grad).sum(1) > 0, touched_o)
     assert np.array_equal(grad == 0, grad_o == 0)
     scale = np.abs(grad_o).max()
