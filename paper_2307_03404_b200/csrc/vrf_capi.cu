@@ -66,6 +66,9 @@ void vrf_context_destroy(vrf_context* ctx) {
     cudaFree(s->ptr);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   if (ctx->h_pipe) cudaFreeHost(ctx->h_pipe);
+  for (cudaEvent_t e : ctx->copy_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }

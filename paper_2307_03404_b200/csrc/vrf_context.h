@@ -78,6 +78,10 @@ struct vrf_context {
   // pinned double buffer of the pipelined mapping loop (vrf_mapping_steps)
   void* h_pipe = nullptr;
   size_t h_pipe_bytes = 0;
+  // vrf_mapping_steps: the next batch's H2D runs on its own stream during the
+  // current step (created on first use)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_ev[2] = {nullptr, nullptr};
 
   // grow-only scratch
   vrf_host::DeviceScratch s_batch, s_raycd, s_flags, s_partials, s_count, s_offsets, s_keys, s_keys2,

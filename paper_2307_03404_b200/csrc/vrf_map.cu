@@ -342,17 +342,31 @@ int vrf_mapping_steps(vrf_context* ctx, const vrf_mapping_config* cfg, uint64_t 
   const int* db[2] = {(const int*)ctx->s_batch.ptr, (const int*)ctx->s_batch2.ptr};
   DevParams p;
   if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
+  if (!ctx->copy_stream) {
+    CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : ctx->copy_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // batch i+1 is drawn on the host and copied to the device (copy stream) while
+  // the device runs step i; step i+1 waits on the copy's event
   vrf_rng_draw_batch(rng_state, n_keyframes, W, H, n_rays, hb[0]);
+  CU(cudaMemcpyAsync((void*)db[0], hb[0], bbytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+  CU(cudaEventRecord(ctx->copy_ev[0], ctx->copy_stream));
   for (int i = 0; i < n_steps; ++i) {
     const int c = i & 1;
-    CU(cudaMemcpyAsync((void*)db[c], hb[c], bbytes, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->copy_ev[c], 0));
     if ((rc = map_gradient(ctx, cfg, db[c], n_rays, nullptr, false))) return rc;
     if ((rc = launch_rmsprop_step(ctx, cfg))) return rc;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(h_st, ctx->d_stats, sizeof(MapStats), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(h_err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    if (i + 1 < n_steps)  // overlaps the device work of step i
+    if (i + 1 < n_steps) {  // overlaps the device work of step i
+      // (db[c ^ 1] was last read by step i - 1, which the previous iteration's
+      // synchronize retired)
       vrf_rng_draw_batch(rng_state, n_keyframes, W, H, n_rays, hb[c ^ 1]);
+      CU(cudaMemcpyAsync((void*)db[c ^ 1], hb[c ^ 1], bbytes, cudaMemcpyHostToDevice,
+                         ctx->copy_stream));
+      CU(cudaEventRecord(ctx->copy_ev[c ^ 1], ctx->copy_stream));
+    }
     CU(cudaStreamSynchronize(ctx->stream));
     prof_collect(ctx);
     if (*h_err & 2) return set_err(ctx, VRF_ERR_OUT_OF_RANGE, "generate_ray: pixel outside image");
