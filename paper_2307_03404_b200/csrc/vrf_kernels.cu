@@ -1244,6 +1244,9 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 #ifndef VRF_K2_POP2
 #define VRF_K2_POP2 0  // A/B: load both pops' queue entries up front
 #endif
+#ifndef VRF_K2_PROBE_NORED
+#define VRF_K2_PROBE_NORED 0  // timing probe builds only (tools/ab/k2_probe.sh)
+#endif
 #ifndef VRF_K2_MERGE_MIN
 #define VRF_K2_MERGE_MIN 2  // smallest duplicate group merged before the reduction
 #endif
@@ -1253,6 +1256,26 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 constexpr int kQ = 16;  // ring entries per thread (power of 2); a step enqueues <= 8
 constexpr int kQSmemBytes = kQ * kThreads * (16 + 4);
 constexpr int kQMergeSmemBytes = kQSmemBytes + kThreads * kVec4PerVertex * 16;
+// Per-warp vertex cache of K2q (VRF_K2_VCACHE=1). The 32 coherent rays of a
+// warp span one or two voxels at room depths, so each vertex is flushed by many
+// of its lanes over a few iterations, mostly in different pop rounds (where the
+// same-round merge cannot see them). The warp keeps kVCache recently flushed
+// vertices' 28 sums in shared memory (hashed slots, one owner per slot and
+// round) and reduces an entry into the gradient only when its slot is taken
+// by another vertex, and at the end of the kernel.
+#ifndef VRF_K2_VCACHE
+#define VRF_K2_VCACHE 0
+#endif
+constexpr int kVCache = 28;
+// the warp's staging region (float4 units): [0, 32) member factors, then the
+// lanes' SH bases (12 floats each, 96 float4); with the cache, its entries
+// (kVCache x 7 float4) and tags (kVCache u32) follow
+constexpr int kSbfOff = VRF_K2_VCACHE ? 32 : 32 * kVec4PerVertex - 32 * 3;
+constexpr int kVCacheOff = 128;
+constexpr int kWarpStage =
+    VRF_K2_VCACHE ? kVCacheOff + kVCache * kVec4PerVertex + kVCache / 4 : 32 * kVec4PerVertex;
+static_assert(kVCache % 4 == 0, "tags fill whole float4");
+static_assert(!VRF_K2_VCACHE || VRF_K2_MERGE == 3, "the vertex cache sits in the factor-merge layout");
 struct QueueSink {
   uint32_t* qv;  // [kQ][kThreads] vertex ids
   float4* qa;    // [kQ][kThreads] (a_sigma, a_r, a_g, a_b)
@@ -1276,7 +1299,7 @@ struct QueueSink {
 // One merged pop of the entry (v, e) the caller loaded (has: the lane popped).
 __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
                                           float4* __restrict__ grad, const float (&bf)[9],
-                                          float4 (*stage)[kVec4PerVertex]) {
+                                          float4* stage) {
   if (has) {
     const unsigned act = __activemask();
 #if VRF_K2_MERGE_MIN > 2
@@ -1301,11 +1324,11 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
       // factor-domain merge: members stage only their 4 factors; the leader
       // expands each member's factors with that member's SH basis (the warp's
       // s_bf rows) into its own sums
-      float4* stage_e = reinterpret_cast<float4*>(stage);  // [32] of the warp
+      float4* stage_e = stage;  // [32] of the warp
       if (lane != leader) stage_e[lane] = e;
       __syncwarp(grp);
       if (lane == leader) {
-        const float4* sbf = reinterpret_cast<const float4*>(stage) + 32 * kVec4PerVertex - 32 * 3;
+        const float4* sbf = stage + kSbfOff;
         unsigned rest = grp & ~(1u << lane);
         while (rest) {
           const int o = __ffs(rest) - 1;
@@ -1327,7 +1350,8 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
       if (lane != leader) {
 #pragma unroll
         for (int j = 0; j < kVec4PerVertex; ++j)
-          stage[lane][j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+          stage[lane * kVec4PerVertex + j] =
+              make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
       }
       __syncwarp(grp);
       if (lane == leader) {
@@ -1337,7 +1361,7 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
           rest &= rest - 1;
 #pragma unroll
           for (int j = 0; j < kVec4PerVertex; ++j) {
-            const float4 y = stage[o][j];
+            const float4 y = stage[o * kVec4PerVertex + j];
             x[4 * j] += y.x;
             x[4 * j + 1] += y.y;
             x[4 * j + 2] += y.z;
@@ -1348,18 +1372,71 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
 #endif
       __syncwarp(grp);
     }
+#if VRF_K2_VCACHE
+    // the warp's vertex cache (see kVCache): each leader adds its group's sums
+    // into the cached entry for v; a different vertex in that slot is evicted
+    // (reduced to the gradient) first. Leaders whose slots collide in this round
+    // beyond the first reduce directly.
+    const unsigned leaders = __ballot_sync(act, lane == leader);
+    if (lane == leader) {
+      const uint32_t slot = __umulhi(v * 0x9E3779B1u, (uint32_t)kVCache);
+      const unsigned sg = __match_any_sync(leaders, slot);
+      float4* ent = stage + kVCacheOff + slot * kVec4PerVertex;
+      uint32_t* tag = reinterpret_cast<uint32_t*>(stage + kVCacheOff + kVCache * kVec4PerVertex);
+      const bool own = __ffs(sg) - 1 == lane;
+      const uint32_t old = own ? tag[slot] : v;
+      const bool hit = old == v;
+      if (own && !hit) {
+        if (old != kNoCell) {
+          float4* od = grad + (size_t)old * kVec4PerVertex;
+#pragma unroll
+          for (int j = 0; j < kVec4PerVertex; ++j) atomicAdd(od + j, ent[j]);
+        }
+        tag[slot] = v;
+      }
+      if (own) {
+#pragma unroll
+        for (int j = 0; j < kVec4PerVertex; ++j) {
+          float4 a = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+          if (hit) {
+            const float4 c = ent[j];
+            a.x += c.x;
+            a.y += c.y;
+            a.z += c.z;
+            a.w += c.w;
+          }
+          ent[j] = a;
+        }
+      } else {
+        float4* dst = grad + (size_t)v * kVec4PerVertex;
+#pragma unroll
+        for (int j = 0; j < kVec4PerVertex; ++j)
+          atomicAdd(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
+      }
+    }
+#else
     if (lane == leader) {  // (a lone lane is its own leader)
       float4* dst = grad + (size_t)v * kVec4PerVertex;
+#if VRF_K2_PROBE_NORED
+      // timing probe only (wrong gradient): the reductions replaced by a
+      // data-dependent branch that keeps the expansion alive
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 28; ++j) acc += x[j];
+      if (acc == 1234.5f) dst[0] = make_float4(acc, 0.f, 0.f, 0.f);
+#else
 #pragma unroll
       for (int j = 0; j < kVec4PerVertex; ++j)
         atomicAdd(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
+#endif
     }
+#endif
   }
 }
 
 __device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& head,
                                                 float4* __restrict__ grad, const float (&bf)[9],
-                                                float4 (*stage)[kVec4PerVertex]) {
+                                                float4* stage) {
   const bool has = head != q.tail;
   uint32_t v = 0;
   float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1377,7 +1454,7 @@ __device__ __forceinline__ void queue_pop_merge(const QueueSink& q, uint32_t& he
 // popped vertex led K2's stall reasons).
 __device__ __forceinline__ void queue_pop_merge2(const QueueSink& q, uint32_t& head,
                                                  float4* __restrict__ grad, const float (&bf)[9],
-                                                 float4 (*stage)[kVec4PerVertex]) {
+                                                 float4* stage) {
   const uint32_t n = q.tail - head;
   const bool h0 = n > 0, h1 = n > 1;
   uint32_t v0 = 0, v1 = 0;
@@ -1411,7 +1488,7 @@ __device__ __forceinline__ void queue_pop_merge2(const QueueSink& q, uint32_t& h
 #endif
 constexpr int kRingRecs = 2;
 constexpr int kRingSmemBytes =
-    kRingRecs * 8 * kThreads * 16 + kRingRecs * kThreads * 8 + kThreads * kVec4PerVertex * 16;
+    kRingRecs * 8 * kThreads * 16 + kRingRecs * kThreads * 8 + (kThreads / 32) * kWarpStage * 16;
 #ifndef VRF_K2_HDR_REG
 #define VRF_K2_HDR_REG 1  // the head record's base and X in registers
 #endif
@@ -1506,7 +1583,7 @@ __device__ __forceinline__ bool ring_enter(CornerAgg& A, RingQueue& q, const Dev
 // One merged pop round over the rings.
 __device__ __forceinline__ void ring_pop_merge(RingQueue& q, const DevGrid& g,
                                                float4* __restrict__ grad, const float (&bf)[9],
-                                               float4 (*stage)[kVec4PerVertex]) {
+                                               float4* stage) {
   const bool has = q.pending() != 0;
   uint32_t v = 0;
   float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1560,13 +1637,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
   // [2][kThreads] uint2, then the per-warp merge staging
   float4* s_rr = s_dyn;
   uint2* s_rh = reinterpret_cast<uint2*>(s_dyn + kRingRecs * 8 * kThreads);
-  float4 (*stage)[kVec4PerVertex] = reinterpret_cast<float4 (*)[kVec4PerVertex]>(
-      s_dyn + kRingRecs * 8 * kThreads + kRingRecs * kThreads / 2) + (threadIdx.x & ~31);
+  float4* stage = s_dyn + kRingRecs * 8 * kThreads + kRingRecs * kThreads / 2 +
+                  (threadIdx.x >> 5) * kWarpStage;
 #else
   float4* s_qa = s_dyn;
   uint32_t* s_qv = reinterpret_cast<uint32_t*>(s_dyn + kQ * kThreads);
-  float4 (*stage)[kVec4PerVertex] = reinterpret_cast<float4 (*)[kVec4PerVertex]>(
-      s_dyn + kQ * kThreads + kQ * kThreads / 4) + (threadIdx.x & ~31);
+  static_assert(!VRF_K2_VCACHE, "the vertex cache needs the record ring");
+  float4* stage = s_dyn + kQ * kThreads + kQ * kThreads / 4 + (threadIdx.x >> 5) * kWarpStage;
 #endif
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   // ---- per-ray setup; a lane with nothing to scatter keeps c = -1 but stays in
@@ -1609,10 +1686,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
   }
 #if VRF_K2_MERGE == 3
   {  // the lane's SH basis, read by the group leaders of the factor-domain merge
-    float* sbf = reinterpret_cast<float*>(reinterpret_cast<float4*>(stage) + 32 * kVec4PerVertex -
-                                          32 * 3) + 12 * (threadIdx.x & 31);
+    float* sbf = reinterpret_cast<float*>(stage + kSbfOff) + 12 * (threadIdx.x & 31);
 #pragma unroll
     for (int mm = 0; mm < 9; ++mm) sbf[mm] = bf[mm];
+#if VRF_K2_VCACHE
+    uint32_t* tag = reinterpret_cast<uint32_t*>(stage + kVCacheOff + kVCache * kVec4PerVertex);
+    if ((threadIdx.x & 31) < kVCache) tag[threadIdx.x & 31] = kNoCell;
+#endif
     __syncwarp();
   }
 #endif
@@ -1656,6 +1736,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
     while (__any_sync(0xffffffffu, q.pending() >= (uint32_t)kRingRecs))
       ring_pop_merge(q, g, grad, bf, stage);
   }
+#if VRF_K2_VCACHE
+  // the cached vertices still owed to the gradient, 7 float4 each, by all lanes
+  __syncwarp();
+  {
+    const uint32_t* tag =
+        reinterpret_cast<const uint32_t*>(stage + kVCacheOff + kVCache * kVec4PerVertex);
+    for (int i = threadIdx.x & 31; i < kVCache * kVec4PerVertex; i += 32) {
+      const uint32_t vv = tag[i / kVec4PerVertex];
+      if (vv != kNoCell)
+        atomicAdd(grad + (size_t)vv * kVec4PerVertex + i % kVec4PerVertex, stage[kVCacheOff + i]);
+    }
+  }
+#endif
 #else
   while (__any_sync(0xffffffffu, c >= 0 || final_pending || head != q.tail)) {
     if (c >= 0) {
