@@ -1244,6 +1244,9 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 #ifndef VRF_K2_POP2
 #define VRF_K2_POP2 0  // A/B: load both pops' queue entries up front
 #endif
+#ifndef VRF_K2_GROUP_MAX
+#define VRF_K2_GROUP_MAX 32  // largest merged duplicate group (A/B knob)
+#endif
 #ifndef VRF_K2_PROBE_NORED
 #define VRF_K2_PROBE_NORED 0  // timing probe builds only (tools/ab/k2_probe.sh)
 #endif
@@ -1306,6 +1309,16 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
     // A/B: groups smaller than VRF_K2_MERGE_MIN reduce lane by lane
     unsigned grp = __match_any_sync(act, v);
     if (__popc(grp) < VRF_K2_MERGE_MIN) grp = 1u << (threadIdx.x & 31);
+#elif VRF_K2_GROUP_MAX < 32
+    // A/B: duplicate groups split into sub-groups of at most VRF_K2_GROUP_MAX
+    // lanes (bounds the serial leader loop; each sub-group reduces separately)
+    unsigned grp = __match_any_sync(act, v);
+    if (__popc(grp) > VRF_K2_GROUP_MAX) {
+      const unsigned below = grp & ((1u << (threadIdx.x & 31)) - 1u);
+      const unsigned long long key =
+          ((unsigned long long)v << 8) | (unsigned)(__popc(below) / VRF_K2_GROUP_MAX);
+      grp = __match_any_sync(grp, key);
+    }
 #else
     const unsigned grp = __match_any_sync(act, v);
 #endif
