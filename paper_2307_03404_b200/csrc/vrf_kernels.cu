@@ -1244,6 +1244,9 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 #ifndef VRF_K2_POP2
 #define VRF_K2_POP2 0  // A/B: load both pops' queue entries up front
 #endif
+#ifndef VRF_K2_POPS
+#define VRF_K2_POPS 2  // pop rounds per walk step
+#endif
 #ifndef VRF_K2_GROUP_MAX
 #define VRF_K2_GROUP_MAX 32  // largest merged duplicate group (A/B knob)
 #endif
@@ -2447,7 +2450,7 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
   }
   // K2q: 4 CTAs/SM (VRF_K2_MINB), 2 pops per step. r01 (config 3 / config 4, ms): 1, 2 or 3
   // pops 14.54 / 14.63 / 15.02 and 25.82 / 25.71 / 25.78.
-  constexpr int kMinB = VRF_K2_MINB, kPops = 2;
+  constexpr int kMinB = VRF_K2_MINB, kPops = VRF_K2_POPS;
   constexpr int kSmem = VRF_K2_RING ? kRingSmemBytes : kQMergeSmemBytes;
   static const bool attr = cudaFuncSetAttribute(k_map_backward_q<kMinB, kPops>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
