@@ -242,6 +242,14 @@ def test_mapping_errors_follow_the_reference(ctx, oracle):
     with pytest.raises(RuntimeError, match="no ray hit the grid"):
         ctx.mapping_step(MappingConfig(), np.array([[0, 1, 1], [1, 2, 2]]))
     assert np.array_equal(ctx.download_grid().data, g.data)
+    # an empty batch (rays_per_batch = 0) has no hits either (mapping.cpp:151),
+    # in the fast and the deterministic mode, and leaves the grid as it was
+    ctx.load_grid(fresh_grid(grid))
+    before = ctx.download_grid().data.copy()
+    for det in (False, True):
+        with pytest.raises(RuntimeError, match="no ray hit the grid"):
+            ctx.mapping_step(MappingConfig(deterministic=det), np.zeros((0, 3), np.int32))
+    assert np.array_equal(ctx.download_grid().data, before)
 
 
 def test_pose_gradient_matches_oracle(ctx, oracle):
