@@ -207,6 +207,19 @@ __device__ __forceinline__ size_t rec_index(int t, int c, int K) {
   return ((size_t)(t >> 5) * (size_t)K + (size_t)c) * 32 + (size_t)(t & 31);
 }
 
+// VRF_REC_HINT: the records stream through L2 at evict-first priority (written
+// once by K0, read once by K2) to keep the payload and gradient lines resident.
+// Bit 0: K0's record stores; bit 1: K2's record loads (also no L1 allocation).
+#ifndef VRF_REC_HINT
+#define VRF_REC_HINT 1
+#endif
+#if VRF_REC_HINT
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+#endif
 // Stores one sample record (vrf_internal.h: RecBuf): a 16 B and an 8 B store.
 // A clamped channel's colour is stored negated (its sign bit is the clamp
 // flag; the clamped value is 0 or 1, and -0.f keeps the bit).
@@ -215,9 +228,20 @@ __device__ __forceinline__ void store_record(RecBuf rec, size_t idx, double wgt,
   float c[3];
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) c[ch] = sh.clamped[ch] ? -(float)sh.c[ch] : (float)sh.c[ch];
+#if VRF_REC_HINT & 1
+  const unsigned long long pol = evict_first_policy();
+  const uint32_t cw = pack_cell(cx, cy, cz) | (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u);
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+               :: "l"(rec.a + idx), "f"((float)wgt), "f"(c[0]), "f"(c[1]), "f"(c[2]), "l"(pol)
+               : "memory");
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;"
+               :: "l"(rec.b + idx), "r"(cw), "r"(__float_as_uint((float)tm)), "l"(pol)
+               : "memory");
+#else
   rec.a[idx] = make_float4((float)wgt, c[0], c[1], c[2]);
   rec.b[idx] = make_uint2(pack_cell(cx, cy, cz) | (sh.sigma_raw > 0.0 ? kRecSigmaPos : 0u),
                           __float_as_uint((float)tm));
+#endif
 }
 
 // Fast forward (fp32 SH) that records every composited sample for the
@@ -1098,8 +1122,16 @@ __device__ __forceinline__ void decode_record(const DevGrid& g, const WalkRay& m
 __device__ __forceinline__ void load_record(RecBuf rec, int t, int c, int K, float4& q0,
                                             uint2& q1) {
   const size_t i = rec_index(t, c, K);
+#if VRF_REC_HINT & 2
+  const unsigned long long pol = evict_first_policy();
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(q0.x), "=f"(q0.y), "=f"(q0.z), "=f"(q0.w) : "l"(rec.a + i), "l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+      : "=r"(q1.x), "=r"(q1.y) : "l"(rec.b + i), "l"(pol));
+#else
   q0 = __ldg(rec.a + i);
   q1 = __ldg(rec.b + i);
+#endif
 }
 
 // The walk's cell as the corner aggregation sees it.
