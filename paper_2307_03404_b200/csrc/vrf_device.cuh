@@ -409,6 +409,32 @@ struct Shade {
   bool clamped[3];
 };
 
+// VRF_GATHER_HINT=1 (A/B): the fast forward's corner gathers at L2 evict-last
+// priority (the payload stays resident against the streaming records).
+#ifndef VRF_GATHER_HINT
+#define VRF_GATHER_HINT 0
+#endif
+__device__ __forceinline__ float4 ldg_payload(const float4* p, unsigned long long pol) {
+#if VRF_GATHER_HINT
+  float4 r;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
+  return r;
+#else
+  (void)pol;
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ unsigned long long payload_policy() {
+#if VRF_GATHER_HINT
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+#else
+  return 0ull;
+#endif
+}
+
 // Fast path (fp32 SH): the colour is contracted with the basis per corner,
 // c_ch = 0.5 + sum_k w_k (sum_m basis_m v_k[ch,m]), so only 3 accumulators are
 // live instead of 27. sigma_raw stays the FP64 reference-order replay, so T and
@@ -418,6 +444,7 @@ __device__ __forceinline__ void shade_fast(const DevGrid& g, const Sample& s, co
                                            const float bf[9], Shade& out) {
   double sraw = 0.0;
   float cr = 0.f, cg = 0.f, cb = 0.f;
+  const unsigned long long pol = payload_policy();
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
 #ifdef VRF_GATHER_SOA
@@ -432,7 +459,7 @@ __device__ __forceinline__ void shade_fast(const DevGrid& g, const Sample& s, co
     float v[28];
 #pragma unroll
     for (int j = 0; j < kVec4PerVertex; ++j) {
-      const float4 a = __ldg(vp + j * js);
+      const float4 a = ldg_payload(vp + j * js, pol);
       v[4 * j] = a.x;
       v[4 * j + 1] = a.y;
       v[4 * j + 2] = a.z;
