@@ -255,6 +255,9 @@ __device__ __forceinline__ void store_record(RecBuf rec, size_t idx, double wgt,
 #ifndef VRF_K0_MINB
 #define VRF_K0_MINB 4
 #endif
+#ifndef VRF_K0_CARVEOUT
+#define VRF_K0_CARVEOUT -1  // driver default
+#endif
 #ifndef VRF_K0_COOP
 #define VRF_K0_COOP 0  // A/B: warp-cooperative corner staging in shared memory
 #endif
@@ -1297,6 +1300,9 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 #ifndef VRF_K2_POP2
 #define VRF_K2_POP2 0  // A/B: load both pops' queue entries up front
 #endif
+#ifndef VRF_K2_SYNC_ACT
+#define VRF_K2_SYNC_ACT 1  // merge synchronised over all popping lanes (r02: 10.80 -> 10.39 ms)
+#endif
 #ifndef VRF_K2_POPS
 #define VRF_K2_POPS 2  // pop rounds per walk step
 #endif
@@ -1388,7 +1394,37 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
       x[10 + mm] = e.z * bf[mm];
       x[19 + mm] = e.w * bf[mm];
     }
+#if VRF_K2_MERGE == 3 && VRF_K2_SYNC_ACT
+    // (the same merge as below, synchronised over all popping lanes: one
+    // warp-uniform mask, so WARPSYNC needs no per-group collective emulation)
+    {
+      const bool multi = grp != (1u << lane);
+      float4* stage_e = stage;
+      if (multi && lane != leader) stage_e[lane] = e;
+      __syncwarp(act);
+      if (multi && lane == leader) {
+        const float4* sbf = stage + kSbfOff;
+        unsigned rest = grp & ~(1u << lane);
+        while (rest) {
+          const int o = __ffs(rest) - 1;
+          rest &= rest - 1;
+          const float4 eo = stage_e[o], b0 = sbf[3 * o], b1 = sbf[3 * o + 1], b2 = sbf[3 * o + 2];
+          const float bb[9] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x};
+          x[0] += eo.x;
+#pragma unroll
+          for (int mm = 0; mm < 9; ++mm) {
+            x[1 + mm] = fmaf(eo.y, bb[mm], x[1 + mm]);
+            x[10 + mm] = fmaf(eo.z, bb[mm], x[10 + mm]);
+            x[19 + mm] = fmaf(eo.w, bb[mm], x[19 + mm]);
+          }
+        }
+      }
+      __syncwarp(act);
+    }
+    if (false) {
+#else
     if (grp != (1u << lane)) {
+#endif
 #if VRF_K2_MERGE == 3
       // factor-domain merge: members stage only their 4 factors; the leader
       // expands each member's factors with that member's SH basis (the warp's
@@ -2471,6 +2507,13 @@ void launch_map_forward_rec(const DevGrid& g, const DevParams& p, const DevCam& 
                                                                 batch, n, ray_cd, flags, partials,
                                                                 err, order, rec, K, rec_count);
 #else
+#if VRF_K0_CARVEOUT >= 0
+  // A/B: the L1 / shared-memory split of the SMs running K0 (percent shared)
+  static const bool carve = cudaFuncSetAttribute(k_map_forward_rec,
+                                                 cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                 VRF_K0_CARVEOUT) == cudaSuccess;
+  (void)carve;
+#endif
   k_map_forward_rec<<<map_forward_blocks(n), kThreads, 0, s>>>(g, p, cam, rgbd, poses, n_frames,
                                                                batch, n, ray_cd, flags, partials,
                                                                err, order, rec, K, rec_count);
