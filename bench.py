@@ -131,24 +131,72 @@ def ncu_kernel(kernel: str, config: int = 3):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and clock-event-reason sampling during the timed region
+    (B200_PROFILING.md clocks line). In-process NVML polling every ~2 ms, so a
+    timed region of ~100 ms still gets dozens of samples; nvidia-smi -lms (whose
+    first sample can arrive after such a region ends) is the fallback when NVML
+    is unavailable."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index=0):
         self.index = index
         self.proc = None
         self.rows = []
+        self.stop = threading.Event()
+        self.t = None
+        self.source = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        # NVML enumerates all GPUs; map the CUDA ordinal through CUDA_VISIBLE_DEVICES
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = self.index
+        if vis:
+            ids = [x.strip() for x in vis.split(",") if x.strip()]
+            if idx < len(ids) and ids[idx].isdigit():
+                idx = int(ids[idx])
+            elif idx < len(ids):
+                return pynvml, pynvml.nvmlDeviceGetHandleByUUID(ids[idx])
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
+
+    def _poll(self, nv, h):
+        bits = [(n, getattr(nv, c)) for n, c in self.REASONS]
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                break
+            self.rows.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active"
+                                                   for _, b in bits])
+            self.stop.wait(0.002)
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+        try:
+            nv, h = self._nvml_handle()
+            self.t = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self.t.start()
+            self.source = "nvml"
+            return self
+        except Exception:
+            pass
+        q = ("clocks.sm,clocks.max.sm,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            self.source = "nvidia-smi"
         except FileNotFoundError:
             self.proc = None
         return self
@@ -158,27 +206,29 @@ class Clocks:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        elif self.t:
+            self.t.join(timeout=5)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in self.rows:
-            for n, v in zip(names, r[3:7]):
+            for (n, _), v in zip(self.REASONS, r[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "source": self.source}
 
 
 def snapshot_state(ctx, torch, device):
