@@ -1303,6 +1303,9 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 #ifndef VRF_K2_SYNC_ACT
 #define VRF_K2_SYNC_ACT 1  // merge synchronised over all popping lanes (r02: 10.80 -> 10.39 ms)
 #endif
+#ifndef VRF_K2_MERGE_PIPE
+#define VRF_K2_MERGE_PIPE 0
+#endif
 #ifndef VRF_K2_POPS
 #define VRF_K2_POPS 2  // pop rounds per walk step
 #endif
@@ -1405,6 +1408,34 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
       if (multi && lane == leader) {
         const float4* sbf = stage + kSbfOff;
         unsigned rest = grp & ~(1u << lane);
+#if VRF_K2_MERGE_PIPE
+        // software-pipelined: the next member's operands load while this one's
+        // 27 FMAs run (A/B; needs the registers of a second member)
+        int o = __ffs(rest) - 1;
+        rest &= rest - 1;
+        float4 eo = stage_e[o], b0 = sbf[3 * o], b1 = sbf[3 * o + 1];
+        float b8 = sbf[3 * o + 2].x;
+        while (true) {
+          const bool more = rest != 0;
+          const int on = more ? __ffs(rest) - 1 : o;
+          rest &= rest - 1;
+          const float4 en = stage_e[on], c0 = sbf[3 * on], c1 = sbf[3 * on + 1];
+          const float c8 = sbf[3 * on + 2].x;
+          const float bb[9] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b8};
+          x[0] += eo.x;
+#pragma unroll
+          for (int mm = 0; mm < 9; ++mm) {
+            x[1 + mm] = fmaf(eo.y, bb[mm], x[1 + mm]);
+            x[10 + mm] = fmaf(eo.z, bb[mm], x[10 + mm]);
+            x[19 + mm] = fmaf(eo.w, bb[mm], x[19 + mm]);
+          }
+          if (!more) break;
+          eo = en;
+          b0 = c0;
+          b1 = c1;
+          b8 = c8;
+        }
+#else
         while (rest) {
           const int o = __ffs(rest) - 1;
           rest &= rest - 1;
@@ -1418,6 +1449,7 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
             x[19 + mm] = fmaf(eo.w, bb[mm], x[19 + mm]);
           }
         }
+#endif
       }
       __syncwarp(act);
     }
