@@ -1289,11 +1289,14 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 // Sc / Sd the running suffix sums; no payload is gathered. The reverse walk also
 // staggers the lanes of a warp along their rays, so neighbouring rays do not hit
 // the same vertices with atomics at the same time (forward order measured 10%
-// slower, r01). A flushed corner is only appended (vertex, a_sigma, a_r, a_g,
-// a_b) to the lane's ring in shared memory; every iteration each lane then pops
-// up to POPS entries and scatters them after the warp reconverges. The loop runs
-// until every lane of the warp has finished its ray AND drained its ring
-// (warp-uniform exit; lanes without a ray help drain).
+// slower, r01). A cell the ray leaves is only stored, as one record of its 8
+// aggregated corner slots, in the lane's ring in shared memory (the cell-record
+// ring below, default since r02; VRF_K2_RING=0 is r01's per-corner entry ring);
+// every iteration each lane then pops up to POPS corners and scatters them after
+// the warp reconverges, merging same-round duplicates (pop_entry). The
+// reductions carry an L2 evict-last policy (red_vertex). The loop runs until
+// every lane of the warp has finished its ray AND drained its ring (warp-uniform
+// exit; lanes without a ray help drain).
 #ifndef VRF_K2_MERGE
 #define VRF_K2_MERGE 3  // same-round duplicate merging: 1 leader sums expanded vectors, 3 factor-domain
 #endif
@@ -1304,7 +1307,7 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 #define VRF_K2_SYNC_ACT 1  // merge synchronised over all popping lanes (r02: 10.80 -> 10.39 ms)
 #endif
 #ifndef VRF_K2_MERGE_PIPE
-#define VRF_K2_MERGE_PIPE 0
+#define VRF_K2_MERGE_PIPE 0  // A/B: software-pipelined merge loop (slower, r02)
 #endif
 #ifndef VRF_K2_POPS
 #define VRF_K2_POPS 2  // pop rounds per walk step
@@ -1319,7 +1322,7 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 #define VRF_K2_MERGE_MIN 2  // smallest duplicate group merged before the reduction
 #endif
 #ifndef VRF_K2_MINB
-#define VRF_K2_MINB 4  // CTAs per SM: 128 registers (r02: 11.8 vs 12.5 ms at 3)
+#define VRF_K2_MINB 4  // CTAs per SM: 128 registers (config 3, r02: 10.39 vs 10.87 ms at 3)
 #endif
 constexpr int kQ = 16;  // ring entries per thread (power of 2); a step enqueues <= 8
 constexpr int kQSmemBytes = kQ * kThreads * (16 + 4);
@@ -1609,7 +1612,7 @@ __device__ __forceinline__ void queue_pop_merge2(const QueueSink& q, uint32_t& h
   pop_entry(h1, v1, e1, grad, bf, stage);
 }
 
-// ---- K2q cell-record ring (VRF_K2_RING=1). A move stores the departing
+// ---- K2q cell-record ring (VRF_K2_RING=1, the default). A move stores the departing
 // cell's whole aggregate (8 slots x 4 factors, unconditionally: 8 STS.128 at
 // full warp) plus a header (base vertex, X, live-slot mask) as one record; pops
 // pick the live slots of the oldest record in slot order and derive each
