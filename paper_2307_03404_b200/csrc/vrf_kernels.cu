@@ -1306,6 +1306,9 @@ __global__ void __launch_bounds__(kThreads) k_map_backward_g(
 #ifndef VRF_K2_SYNC_ACT
 #define VRF_K2_SYNC_ACT 1  // merge synchronised over all popping lanes (r02: 10.80 -> 10.39 ms)
 #endif
+#ifndef VRF_K2_STAGE2
+#define VRF_K2_STAGE2 0  // A/B: double-buffered merge staging, one barrier per round (no gain, r02)
+#endif
 #ifndef VRF_K2_MERGE_PIPE
 #define VRF_K2_MERGE_PIPE 0  // A/B: software-pipelined merge loop (slower, r02)
 #endif
@@ -1346,6 +1349,8 @@ constexpr int kVCacheOff = 128;
 constexpr int kWarpStage =
     VRF_K2_VCACHE ? kVCacheOff + kVCache * kVec4PerVertex + kVCache / 4 : 32 * kVec4PerVertex;
 static_assert(kVCache % 4 == 0, "tags fill whole float4");
+static_assert(!VRF_K2_STAGE2 || (!VRF_K2_VCACHE && VRF_K2_MERGE == 3 && VRF_K2_SYNC_ACT),
+              "the second staging buffer uses the factor-merge layout's free rows [32, 64)");
 static_assert(!VRF_K2_VCACHE || VRF_K2_MERGE == 3, "the vertex cache sits in the factor-merge layout");
 struct QueueSink {
   uint32_t* qv;  // [kQ][kThreads] vertex ids
@@ -1370,7 +1375,7 @@ struct QueueSink {
 // One merged pop of the entry (v, e) the caller loaded (has: the lane popped).
 __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
                                           float4* __restrict__ grad, const float (&bf)[9],
-                                          float4* stage) {
+                                          float4* stage, int buf = 0) {
   if (has) {
     const unsigned act = __activemask();
 #if VRF_K2_MERGE_MIN > 2
@@ -1405,7 +1410,10 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
     // warp-uniform mask, so WARPSYNC needs no per-group collective emulation)
     {
       const bool multi = grp != (1u << lane);
-      float4* stage_e = stage;
+      // VRF_K2_STAGE2: consecutive pop rounds alternate between two staging
+      // buffers, and the loop's full-warp votes separate a buffer's reuse, so
+      // the barrier after the leaders' reads is not needed
+      float4* stage_e = stage + (VRF_K2_STAGE2 ? 32 * buf : 0);
       if (multi && lane != leader) stage_e[lane] = e;
       __syncwarp(act);
       if (multi && lane == leader) {
@@ -1454,7 +1462,9 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
         }
 #endif
       }
+#if !VRF_K2_STAGE2
       __syncwarp(act);
+#endif
     }
     if (false) {
 #else
@@ -1635,7 +1645,8 @@ struct RingQueue {
   uint2* hdr;    // [kRingRecs][kThreads] (base vertex, X | live << 8)
   int tid;
   uint32_t st;   // bits 0-7: unpopped live slots of the head record; bit 8: head
-                 // record; bits 9-10: records pending; bits 16-18: the head's X
+                 // record; bits 9-10: records pending; bit 12: pop-round parity;
+                 // bits 16-18: the head's X
 #if VRF_K2_HDR_REG
   uint32_t hbase;  // the head record's base vertex
 #endif
@@ -1669,13 +1680,13 @@ __device__ __forceinline__ void ring_push(RingQueue& q, const CornerAgg& A, uint
   q.hdr[r * kThreads + q.tid] = make_uint2(A.base, A.X | (live << 8));
 #if VRF_K2_HDR_REG
   if (np == 0) {
-    q.st = live | (hr << 8) | (1u << 9) | (A.X << 16);
+    q.st = live | (hr << 8) | (1u << 9) | (A.X << 16) | (q.st & (1u << 12));
     q.hbase = A.base;
   } else {
     q.st += 1u << 9;
   }
 #else
-  q.st = (np == 0 ? (live | (hr << 8)) : (q.st & 0x1ffu)) | ((np + 1) << 9);
+  q.st = (np == 0 ? (live | (hr << 8)) : (q.st & 0x1ffu)) | ((np + 1) << 9) | (q.st & (1u << 12));
 #endif
 }
 
@@ -1725,6 +1736,9 @@ __device__ __forceinline__ void ring_pop_merge(RingQueue& q, const DevGrid& g,
   const bool has = q.pending() != 0;
   uint32_t v = 0;
   float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+#if VRF_K2_STAGE2
+  q.st ^= 1u << 12;  // round parity (warp-uniform: every lane runs every round)
+#endif
   if (has) {
     const uint32_t pm = q.st & 0xffu, hr = (q.st >> 8) & 1u;
 #if VRF_K2_HDR_REG
@@ -1748,15 +1762,15 @@ __device__ __forceinline__ void ring_pop_merge(RingQueue& q, const DevGrid& g,
 #if VRF_K2_HDR_REG
       uint2 nx = make_uint2(0u, 0u);
       if (np) nx = q.hdr[nh * kThreads + q.tid];
-      q.st = (nx.y >> 8) | (nh << 8) | (np << 9) | ((nx.y & 7u) << 16);
+      q.st = (nx.y >> 8) | (nh << 8) | (np << 9) | ((nx.y & 7u) << 16) | (q.st & (1u << 12));
       q.hbase = nx.x;
 #else
       const uint32_t npm = np ? (q.hdr[nh * kThreads + q.tid].y >> 8) : 0u;
-      q.st = npm | (nh << 8) | (np << 9);
+      q.st = npm | (nh << 8) | (np << 9) | (q.st & (1u << 12));
 #endif
     }
   }
-  pop_entry(has, v, e, grad, bf, stage);
+  pop_entry(has, v, e, grad, bf, stage, (int)((q.st >> 12) & 1u));
 }
 
 template <int MINB, int POPS>
