@@ -251,6 +251,13 @@ int vrf_grid_set_occupancy(vrf_context* ctx, const uint8_t* occupancy);
 int vrf_track_updates(vrf_context* ctx, int on);
 int vrf_updates_count(vrf_context* ctx, int64_t* n);
 int vrf_updates_read(vrf_context* ctx, int64_t n, uint32_t* ids, float* theta, float* v);
+/* Entries [first, first + count) of the log; sorted != 0: in ascending id order
+ * (the first such call after a logged step sorts the log on the device). */
+int vrf_updates_read_range(vrf_context* ctx, int64_t first, int64_t count, int sorted,
+                           uint32_t* ids, float* theta, float* v);
+/* fp32 device state to host, floats [first, first + count) of which = 0 the payload
+ * [V][28], 1 the RMSProp v [V][28] (the drop-in's chunked dense write-back). */
+int vrf_state_read_f32(vrf_context* ctx, int which, int64_t first, int64_t count, float* dst);
 /* Page-locked host memory for staging buffers (cudaMallocHost; NULL on failure):
  * device <-> host copies into it run at full PCIe / C2C speed. */
 void* vrf_host_alloc(size_t bytes);

@@ -20,6 +20,7 @@
 #include "voxrf/renderer.hpp"
 
 extern "C" void voxrf_b200_dropin_traffic(std::uint64_t* uploaded, std::uint64_t* written_back);
+extern "C" void voxrf_b200_dropin_phase_ms(double* out);
 extern "C" std::int64_t voxrf_b200_dropin_last_samples();
 
 using namespace voxrf;
@@ -64,6 +65,8 @@ int main(int argc, char** argv) {
   for (int i = 0; i < warmup; ++i) mapping_step(grid, kf, intr, cfg, rms, rng);
   std::uint64_t up0, back0, up1, back1;
   voxrf_b200_dropin_traffic(&up0, &back0);
+  double ph0[6], ph1[6];
+  voxrf_b200_dropin_phase_ms(ph0);
   long long samples = 0;
   const auto t0 = std::chrono::steady_clock::now();
   for (int i = 0; i < steps; ++i) {
@@ -72,12 +75,17 @@ int main(int argc, char** argv) {
   }
   const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   voxrf_b200_dropin_traffic(&up1, &back1);
+  voxrf_b200_dropin_phase_ms(ph1);
   std::printf("{\"api\": \"voxrf::mapping_step (reference C++ signature, drop-in)\", "
               "\"rays_per_step\": %d, \"steps\": %d, \"samples_per_s\": %.6e, "
               "\"rays_per_s\": %.6e, \"ms_per_step\": %.4f, \"upload_bytes_per_step\": %.0f, "
-              "\"writeback_bytes_per_step\": %.0f, \"grid_bytes_fp64\": %zu}\n",
+              "\"writeback_bytes_per_step\": %.0f, \"grid_bytes_fp64\": %zu, "
+              "\"phase_ms_per_step\": {\"draw\": %.3f, \"sync\": %.3f, \"device_step\": %.3f, "
+              "\"write_back\": %.3f, \"write_back_d2h\": %.3f, \"write_back_scatter\": %.3f}}\n",
               rays, steps, samples / s, double(rays) * steps / s, 1e3 * s / steps,
               double(up1 - up0) / steps, double(back1 - back0) / steps,
-              grid.data().size() * sizeof(double));
+              grid.data().size() * sizeof(double), (ph1[0] - ph0[0]) / steps,
+              (ph1[1] - ph0[1]) / steps, (ph1[2] - ph0[2]) / steps, (ph1[3] - ph0[3]) / steps,
+              (ph1[4] - ph0[4]) / steps, (ph1[5] - ph0[5]) / steps);
   return 0;
 }

@@ -20,6 +20,8 @@
 // mapping_step writes back only the float4 groups its RMSProp pass updated (the
 // reference's touched set, mapping.cpp:218-231) — untouched vertices keep their
 // host fp64 values, as in the reference's in-place update.
+#include <immintrin.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
@@ -89,6 +91,10 @@ vrf_render_params to_c(const RenderParams& r) {
 
 // ---- device residency
 struct Residency {
+  // drop-in mapping_step wall time by phase (ms, cumulative): batch draw,
+  // residency sync, device step, write-back (voxrf_b200_dropin_phase_ms)
+  double phase_ms[4] = {0.0, 0.0, 0.0, 0.0};
+  double wb_ms[2] = {0.0, 0.0};  // write-back: blocked in the D2H reads, the rest (host work not overlapped)
   bool grid_valid = false;
   const double* data = nullptr;
   std::size_t data_n = 0;
@@ -221,6 +227,47 @@ void sync_frames(const CameraIntrinsics& intr, const std::vector<const Frame*>& 
 
 // Writes mapping_step's result back into the caller's grid and RMSProp state:
 // the updated float4 groups only, or everything when most groups changed.
+// Host worker pool for the write-back: splits [0, n) over up to `threads` threads.
+template <typename F>
+void parallel_for(std::int64_t n, int threads, F&& f) {
+  const int nt = n < (1 << 15) ? 1 : threads;
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(f, n * t / nt, n * (t + 1) / nt);
+  f(0, n / nt);
+  for (auto& th : pool) th.join();
+}
+
+// dst[i] = double(src[i]) for a contiguous run. The dense write-back widens
+// 2 x 1.9 GB of fp32 into 2 x 3.8 GB of the caller's fp64 buffers; with
+// non-temporal stores the host does not read the destination lines first.
+__attribute__((target("avx2"))) void widen_stream_avx2(double* dst, const float* src,
+                                                       std::int64_t n) {
+  std::int64_t i = 0;
+  for (; i < n && (reinterpret_cast<std::uintptr_t>(dst + i) & 31); ++i) dst[i] = double(src[i]);
+  for (; i + 4 <= n; i += 4)
+    _mm256_stream_pd(dst + i, _mm256_cvtps_pd(_mm_loadu_ps(src + i)));
+  for (; i < n; ++i) dst[i] = double(src[i]);
+  _mm_sfence();
+}
+void widen(double* dst, const float* src, std::int64_t n) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2) return widen_stream_avx2(dst, src, n);
+  for (std::int64_t i = 0; i < n; ++i) dst[i] = double(src[i]);
+}
+
+int writeback_threads() {
+  static const int n = int(std::min<unsigned>(32, std::max(1u, std::thread::hardware_concurrency())));
+  return n;
+}
+
+// In-place contract of mapping_step (mapping.hpp:80): the device's updated theta
+// and RMSProp v reach the caller's fp64 buffers. Chunked through two page-locked
+// staging buffers, so the D2H of chunk i+1 runs while host threads convert /
+// scatter chunk i.
+//  * sparse (the RMSProp update log, sorted by group id on the device, so the
+//    scatter walks the caller's arrays forward): 36 B per updated float4 group;
+//  * dense (when over a third of the groups changed): both fp32 arrays, widened
+//    on the host.
 void write_back(VoxelGrid& grid, RmspropState& st) {
   double* d = grid.data().data();
   double* v = st.v.data();
@@ -229,44 +276,70 @@ void write_back(VoxelGrid& grid, RmspropState& st) {
   check(vrf_updates_count(ctx(), &n));
   HostMirror::unprotect(d);
   HostMirror::unprotect(v);
+  constexpr std::int64_t kChunk = std::int64_t(1) << 21;  // entries (sparse) / 4-float groups (dense)
+  static void* stage[2] = {nullptr, nullptr};
+  constexpr std::size_t kStageBytes = std::size_t(kChunk) * (sizeof(std::uint32_t) + 8 * sizeof(float));
+  for (void*& b : stage)
+    if (!b && !(b = vrf_host_alloc(kStageBytes)))
+      throw std::runtime_error("voxrf_b200: page-locked staging allocation failed");
+  const int nt = writeback_threads();
+  const auto w0 = std::chrono::steady_clock::now();
+  double d2h_ms = 0.0;
+  std::thread worker;  // host work on the previous chunk
+  auto timed_read = [&](auto&& read) {
+    const auto a = std::chrono::steady_clock::now();
+    read();
+    d2h_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  };
   if (std::size_t(n) * 3 > groups) {  // dense: cheaper than the indexed form
-    check(vrf_grid_download(ctx(), d, nullptr));
-    check(vrf_rmsprop_download(ctx(), v));
+    const std::int64_t total = std::int64_t(grid.data().size());  // floats per array
+    const std::int64_t step = 4 * kChunk;
+    int k = 0;
+    for (int which = 0; which < 2; ++which) {
+      double* dst = which == 0 ? d : v;
+      for (std::int64_t off = 0; off < total; off += step, k ^= 1) {
+        const std::int64_t cnt = std::min(step, total - off);
+        float* buf = static_cast<float*>(stage[k]);
+        timed_read([&] { check(vrf_state_read_f32(ctx(), which, off, cnt, buf)); });
+        if (worker.joinable()) worker.join();
+        worker = std::thread([=] {
+          parallel_for(cnt, nt, [=](std::int64_t i0, std::int64_t i1) {
+            widen(dst + off + i0, buf + i0, i1 - i0);
+          });
+        });
+      }
+    }
+    if (worker.joinable()) worker.join();
     g_res.back_bytes += 2 * groups * 4 * sizeof(float);
   } else if (n > 0) {
-    // page-locked staging (grown on demand, kept): the D2H runs at link speed
-    static void* stage = nullptr;
-    static std::size_t stage_bytes = 0;
-    const std::size_t need = std::size_t(n) * (sizeof(std::uint32_t) + 8 * sizeof(float));
-    if (stage_bytes < need) {
-      vrf_host_free(stage);
-      stage_bytes = need + need / 4;
-      stage = vrf_host_alloc(stage_bytes);
-      if (!stage) throw std::runtime_error("voxrf_b200: page-locked staging allocation failed");
+    int k = 0;
+    for (std::int64_t off = 0; off < n; off += kChunk, k ^= 1) {
+      const std::int64_t cnt = std::min(kChunk, n - off);
+      float* th = static_cast<float*>(stage[k]);
+      float* vv = th + 4 * kChunk;
+      std::uint32_t* ids = reinterpret_cast<std::uint32_t*>(vv + 4 * kChunk);
+      timed_read([&] { check(vrf_updates_read_range(ctx(), off, cnt, 1, ids, th, vv)); });
+      if (worker.joinable()) worker.join();
+      // the logged groups are distinct, so the threads never write the same element
+      worker = std::thread([=] {
+        parallel_for(cnt, nt, [=](std::int64_t i0, std::int64_t i1) {
+          for (std::int64_t i = i0; i < i1; ++i) {
+            const std::size_t o = 4 * std::size_t(ids[std::size_t(i)]);  // == vertex * 28 + 4 group
+            for (int e = 0; e < 4; ++e) {
+              d[o + e] = th[4 * std::size_t(i) + e];
+              v[o + e] = vv[4 * std::size_t(i) + e];
+            }
+          }
+        });
+      });
     }
-    float* th = static_cast<float*>(stage);
-    float* vv = th + 4 * std::size_t(n);
-    std::uint32_t* ids = reinterpret_cast<std::uint32_t*>(vv + 4 * std::size_t(n));
-    check(vrf_updates_read(ctx(), n, ids, th, vv));
-    // scatter into the caller's fp64 buffers (random access: split over threads;
-    // the logged groups are distinct, so the chunks never write the same element)
-    auto scatter = [&](std::int64_t i0, std::int64_t i1) {
-      for (std::int64_t i = i0; i < i1; ++i) {
-        const std::size_t o = 4 * std::size_t(ids[std::size_t(i)]);  // == vertex * 28 + 4 group
-        for (int e = 0; e < 4; ++e) {
-          d[o + e] = th[4 * std::size_t(i) + e];
-          v[o + e] = vv[4 * std::size_t(i) + e];
-        }
-      }
-    };
-    const int nt = n < (1 << 16) ? 1 : int(std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency())));
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t)
-      pool.emplace_back(scatter, n * t / nt, n * (t + 1) / nt);
-    scatter(0, n / nt);
-    for (auto& th_ : pool) th_.join();
+    if (worker.joinable()) worker.join();
     g_res.back_bytes += std::size_t(n) * (4 + 32);
   }
+  const double total_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+  g_res.wb_ms[0] += d2h_ms;
+  g_res.wb_ms[1] += total_ms - d2h_ms;
   HostMirror::clean(d);
   HostMirror::clean(v);
 }
@@ -380,11 +453,15 @@ MapStepStats mapping_step(VoxelGrid& grid, const std::vector<const Frame*>& keyf
                           const CameraIntrinsics& intrinsics, const MappingConfig& config,
                           RmspropState& rmsprop, Rng& rng) {
   if (keyframes.empty()) throw std::runtime_error("mapping_step: no keyframes");
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
   const std::vector<int32_t> batch =
       draw_batch(rng, int(keyframes.size()), intrinsics, config.rays_per_batch);
+  const auto t1 = clock::now();
   sync_grid(grid);
   sync_rmsprop(rmsprop, grid.data().size());
   sync_frames(intrinsics, keyframes);
+  const auto t2 = clock::now();
   const vrf_mapping_config cc = to_c(config);
   vrf_map_step_stats st{};
   const int rc = vrf_mapping_step(ctx(), &cc, batch.data(), config.rays_per_batch, &st);
@@ -393,8 +470,17 @@ MapStepStats mapping_step(VoxelGrid& grid, const std::vector<const Frame*>& keyf
     check(rc);
   }
   g_res.last_samples = st.samples;
+  const auto t3 = clock::now();
   // In-place contract (mapping.hpp:80): grid and RMSProp state are updated.
   write_back(grid, rmsprop);
+  const auto t4 = clock::now();
+  const auto ms = [](clock::time_point a, clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  g_res.phase_ms[0] += ms(t0, t1);
+  g_res.phase_ms[1] += ms(t1, t2);
+  g_res.phase_ms[2] += ms(t2, t3);
+  g_res.phase_ms[3] += ms(t3, t4);
   return to_stats(st);
 }
 
@@ -551,6 +637,14 @@ TrackSequenceResult track_sequence(const VoxelGrid& grid, const Dataset& dataset
 
 // Residency counters of the drop-in (tests, bench): bytes uploaded to the device
 // and written back to the caller's buffers since the process started.
+// Cumulative drop-in mapping_step wall time by phase (ms): [0] batch draw, [1]
+// residency sync, [2] device step, [3] write-back, [4] of which the update-log
+// D2H, [5] of which the host scatter.
+extern "C" void voxrf_b200_dropin_phase_ms(double* out) {
+  for (int i = 0; i < 4; ++i) out[i] = voxrf::g_res.phase_ms[i];
+  out[4] = voxrf::g_res.wb_ms[0];
+  out[5] = voxrf::g_res.wb_ms[1];
+}
 extern "C" void voxrf_b200_dropin_traffic(std::uint64_t* uploaded, std::uint64_t* written_back) {
   *uploaded = voxrf::g_res.up_bytes;
   *written_back = voxrf::g_res.back_bytes;

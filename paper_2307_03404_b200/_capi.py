@@ -133,6 +133,8 @@ _SIGS = {
     "vrf_track_updates": (C.c_int, [vp, C.c_int]),
     "vrf_updates_count": (C.c_int, [vp, P(C.c_int64)]),
     "vrf_updates_read": (C.c_int, [vp, C.c_int64, vp, vp, vp]),
+    "vrf_updates_read_range": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int, vp, vp, vp]),
+    "vrf_state_read_f32": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, vp]),
     "vrf_host_alloc": (vp, [C.c_size_t]),
     "vrf_host_free": (None, [vp]),
     "vrf_get_device_buffers": (C.c_int, [vp, P(DeviceBuffers_c)]),

@@ -62,6 +62,8 @@ void vrf_context_destroy(vrf_context* ctx) {
                            &ctx->s_ids, &ctx->s_ids2, &ctx->s_values, &ctx->s_grad64, &ctx->s_cub,
                            &ctx->s_stage, &ctx->s_out, &ctx->s_batch2, &ctx->s_rec,
                            &ctx->s_upd_ids, &ctx->s_upd_theta, &ctx->s_upd_v,
+                           &ctx->s_upd_sids, &ctx->s_upd_perm, &ctx->s_upd_iota,
+                           &ctx->s_upd_tmp, &ctx->s_upd_gth, &ctx->s_upd_gv,
                            &ctx->s_reccount})
     cudaFree(s->ptr);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);

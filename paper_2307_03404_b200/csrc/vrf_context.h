@@ -95,6 +95,9 @@ struct vrf_context {
   bool log_updates = false;
   vrf_host::DeviceScratch s_upd_ids, s_upd_theta, s_upd_v;
   unsigned long long* d_upd_count = nullptr;
+  // sorted view of the log (vrf_updates_read_range): ids, log positions, scratch
+  vrf_host::DeviceScratch s_upd_sids, s_upd_perm, s_upd_iota, s_upd_tmp, s_upd_gth, s_upd_gv;
+  bool upd_sorted = false;  // the sorted view matches the current log
   unsigned long long* d_digest = nullptr;
   double rec_budget_gb = -1.0;   // vrf_set_record_limits: <= 0 automatic (30 % of free HBM)
   int rec_max_k = -1;            // vrf_set_record_limits: < 0 automatic, 0 no records

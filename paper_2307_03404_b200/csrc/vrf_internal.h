@@ -101,6 +101,14 @@ void launch_map_backward_records(const DevGrid& g, const DevParams& p, const Dev
 void launch_segmented_reduce(const uint32_t* sorted_keys, const uint32_t* perm,
                              const double* values, long long nrec, double* grad_out_f64,
                              cudaStream_t s);
+// The update log sorted by group id (perm: log position of each sorted entry),
+// and a contiguous gather of a range of it (vrf_order.cu).
+void launch_update_sort(const uint32_t* ids, long long n, uint32_t* ids_sorted, uint32_t* iota,
+                        uint32_t* perm, void* tmp, size_t tmp_bytes, cudaStream_t s);
+size_t update_sort_tmp_bytes(long long n);
+void launch_update_gather(const uint32_t* perm, long long first, long long count,
+                          const float4* theta, const float4* v, float4* theta_out, float4* v_out,
+                          cudaStream_t s);
 // Log of the float4 groups an RMSProp pass updated (index, new theta, new v): the
 // drop-in's sparse write-back (vrf_updates_read). count == nullptr: off.
 struct UpdateLog {

@@ -189,6 +189,7 @@ int update_log(vrf_context* ctx, UpdateLog* log) {
   if ((rc = ensure(ctx, ctx->s_upd_v, sizeof(float4) * groups))) return rc;
   if (!ctx->d_upd_count) CU(cudaMalloc(&ctx->d_upd_count, sizeof(unsigned long long)));
   CU(cudaMemsetAsync(ctx->d_upd_count, 0, sizeof(unsigned long long), ctx->stream));
+  ctx->upd_sorted = false;
   log->ids = (uint32_t*)ctx->s_upd_ids.ptr;
   log->theta = (float4*)ctx->s_upd_theta.ptr;
   log->v = (float4*)ctx->s_upd_v.ptr;
@@ -621,6 +622,67 @@ int vrf_updates_read(vrf_context* ctx, int64_t n, uint32_t* ids, float* theta, f
   CU(cudaMemcpyAsync(theta, ctx->s_upd_theta.ptr, sizeof(float4) * n, cudaMemcpyDeviceToHost,
                      ctx->stream));
   CU(cudaMemcpyAsync(v, ctx->s_upd_v.ptr, sizeof(float4) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_updates_read_range(vrf_context* ctx, int64_t first, int64_t count, int sorted,
+                           uint32_t* ids, float* theta, float* v) {
+  cudaSetDevice(ctx->device);
+  if (!ctx->log_updates || count <= 0) return VRF_OK;
+  int64_t n = 0;
+  int rc = vrf_updates_count(ctx, &n);
+  if (rc) return rc;
+  if (first < 0 || first + count > n)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_updates_read_range: range exceeds the log");
+  if (!sorted) {
+    CU(cudaMemcpyAsync(ids, (const uint32_t*)ctx->s_upd_ids.ptr + first, sizeof(uint32_t) * count,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(theta, (const float4*)ctx->s_upd_theta.ptr + first, sizeof(float4) * count,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(v, (const float4*)ctx->s_upd_v.ptr + first, sizeof(float4) * count,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return VRF_OK;
+  }
+  if (!ctx->upd_sorted) {  // once per logged step: sort the whole log by id
+    const size_t tb = update_sort_tmp_bytes(n);
+    if ((rc = ensure(ctx, ctx->s_upd_sids, sizeof(uint32_t) * n))) return rc;
+    if ((rc = ensure(ctx, ctx->s_upd_perm, sizeof(uint32_t) * n))) return rc;
+    if ((rc = ensure(ctx, ctx->s_upd_iota, sizeof(uint32_t) * n))) return rc;
+    if ((rc = ensure(ctx, ctx->s_upd_tmp, tb))) return rc;
+    launch_update_sort((const uint32_t*)ctx->s_upd_ids.ptr, n, (uint32_t*)ctx->s_upd_sids.ptr,
+                       (uint32_t*)ctx->s_upd_iota.ptr, (uint32_t*)ctx->s_upd_perm.ptr,
+                       ctx->s_upd_tmp.ptr, tb, ctx->stream);
+    CU(cudaGetLastError());
+    ctx->upd_sorted = true;
+  }
+  if ((rc = ensure(ctx, ctx->s_upd_gth, sizeof(float4) * count))) return rc;
+  if ((rc = ensure(ctx, ctx->s_upd_gv, sizeof(float4) * count))) return rc;
+  launch_update_gather((const uint32_t*)ctx->s_upd_perm.ptr, first, count,
+                       (const float4*)ctx->s_upd_theta.ptr, (const float4*)ctx->s_upd_v.ptr,
+                       (float4*)ctx->s_upd_gth.ptr, (float4*)ctx->s_upd_gv.ptr, ctx->stream);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(ids, (const uint32_t*)ctx->s_upd_sids.ptr + first, sizeof(uint32_t) * count,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(theta, ctx->s_upd_gth.ptr, sizeof(float4) * count, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(v, ctx->s_upd_gv.ptr, sizeof(float4) * count, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return VRF_OK;
+}
+
+int vrf_state_read_f32(vrf_context* ctx, int which, int64_t first, int64_t count, float* dst) {
+  cudaSetDevice(ctx->device);
+  int rc = need_grid(ctx);
+  if (rc) return rc;
+  const float* src = which == 0 ? ctx->payload : which == 1 ? ctx->rms : nullptr;
+  if (!src) return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_state_read_f32: which");
+  if (first < 0 || count < 0 || first + count > (int64_t)ctx->V * 28)
+    return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "vrf_state_read_f32: range");
+  CU(cudaMemcpyAsync(dst, src + first, sizeof(float) * count, cudaMemcpyDeviceToHost,
+                     ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return VRF_OK;
 }

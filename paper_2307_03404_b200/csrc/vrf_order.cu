@@ -2,6 +2,8 @@
 // order of 4x4-pixel tiles), so the 32 rays of a warp march nearly the same
 // cells and the grid / gradient lines of the rays in flight stay in L2 (r01:
 // 1.18e9 -> 3.41e9 mapping samples/s over draw order).
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "vrf_internal.h"
@@ -39,6 +41,11 @@ __global__ void k_pixel_keys(const int* __restrict__ px, int n, uint32_t* keys, 
   ids[i] = (uint32_t)i;
 }
 
+__global__ void k_iota(uint32_t* out, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint32_t)i;
+}
+
 }  // namespace
 
 void launch_pixel_order(const int* pixels, int n, uint32_t* keys, uint32_t* ids, uint32_t* keys2,
@@ -51,6 +58,38 @@ void launch_ray_order(const int* batch, int n, uint32_t* keys, uint32_t* ids, ui
                       uint32_t* order, void* tmp, size_t tmp_bytes, cudaStream_t s) {
   k_ray_keys<<<(n + 255) / 256, 256, 0, s>>>(batch, n, keys, ids);
   cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, ids, order, n, 0, 32, s);
+}
+
+// The RMSProp update log in vertex order (the drop-in's host scatter then walks
+// the caller's fp64 arrays forward): sort (id, position) pairs by id.
+void launch_update_sort(const uint32_t* ids, long long n, uint32_t* ids_sorted, uint32_t* iota,
+                        uint32_t* perm, void* tmp, size_t tmp_bytes, cudaStream_t s) {
+  k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(iota, n);
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ids, ids_sorted, iota, perm, (int)n, 0, 32, s);
+}
+size_t update_sort_tmp_bytes(long long n) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 32);
+  return b;
+}
+// Entries [first, first + count) of the sorted log, gathered contiguously.
+__global__ void k_update_gather(const uint32_t* __restrict__ perm, long long first, long long count,
+                                const float4* __restrict__ theta, const float4* __restrict__ v,
+                                float4* __restrict__ theta_out, float4* __restrict__ v_out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t p = perm[first + i];
+    theta_out[i] = theta[p];
+    v_out[i] = v[p];
+  }
+}
+void launch_update_gather(const uint32_t* perm, long long first, long long count,
+                          const float4* theta, const float4* v, float4* theta_out, float4* v_out,
+                          cudaStream_t s) {
+  const long long blocks = std::min<long long>((count + 255) / 256, 148LL * 16);
+  k_update_gather<<<(unsigned)std::max(1LL, blocks), 256, 0, s>>>(perm, first, count, theta, v,
+                                                                  theta_out, v_out);
 }
 
 size_t ray_order_tmp_bytes(int n) {

@@ -195,9 +195,38 @@ def test_update_log_and_partial_writes(ctx, oracle):
         vv = np.zeros((n.value, 4), np.float32)
         assert lib.vrf_updates_read(h, n.value, ids.ctypes.data, th.ctypes.data,
                                     vv.ctypes.data) == 0
+        # the sorted, ranged read (the drop-in's chunked write-back): the same
+        # entries in ascending id order, in two ranges
+        k = n.value // 3
+        sid = np.zeros(n.value, np.uint32)
+        sth = np.zeros((n.value, 4), np.float32)
+        svv = np.zeros((n.value, 4), np.float32)
+        for a, b in ((0, k), (k, n.value)):
+            assert lib.vrf_updates_read_range(h, a, b - a, 1, sid[a:].ctypes.data,
+                                              sth[a:].ctypes.data, svv[a:].ctypes.data) == 0
+        order = np.argsort(ids)
+        assert np.array_equal(sid, ids[order])
+        assert np.array_equal(sth, th[order]) and np.array_equal(svv, vv[order])
+        part = np.zeros((5, 4), np.float32)
+        assert lib.vrf_updates_read_range(h, 1, 5, 0, sid.ctypes.data, part.ctypes.data,
+                                          svv.ctypes.data) == 0
+        assert np.array_equal(part, th[1:6])
+        assert lib.vrf_updates_read_range(h, n.value - 1, 2, 1, sid.ctypes.data,
+                                          part.ctypes.data, svv.ctypes.data) != 0
     finally:
         lib.vrf_track_updates(h, 0)
     after = ctx.download_payload_f32().reshape(-1, 7, 4)
+    # chunked fp32 state reads (payload and RMSProp v)
+    nf = after.size
+    got = np.zeros(nf, np.float32)
+    for a in range(0, nf, 1000):
+        c = min(1000, nf - a)
+        assert lib.vrf_state_read_f32(h, 0, a, c, got[a:].ctypes.data) == 0
+    assert np.array_equal(got, after.reshape(-1))
+    assert lib.vrf_state_read_f32(h, 1, 0, nf, got.ctypes.data) == 0
+    np.testing.assert_array_equal(got, ctx.rmsprop_v().reshape(-1).astype(np.float32))
+    assert lib.vrf_state_read_f32(h, 2, 0, 1, got.ctypes.data) != 0
+    assert lib.vrf_state_read_f32(h, 0, nf - 1, 2, got.ctypes.data) != 0
     flat_b, flat_a = before.reshape(-1, 4), after.reshape(-1, 4)
     assert len(np.unique(ids)) == len(ids)
     np.testing.assert_array_equal(flat_a[ids], th)
