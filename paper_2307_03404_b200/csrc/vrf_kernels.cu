@@ -2579,6 +2579,29 @@ static int bwd_group_max() {
   }();
   return v;
 }
+// Batch size (rays) from which K2q runs at 3 CTAs/SM; VRF_K2_MINB3_RAYS overrides.
+static int k2_minb3_rays() {
+  static const int v = [] {
+    const char* e = std::getenv("VRF_K2_MINB3_RAYS");
+    return e ? std::atoi(e) : (4 << 20);
+  }();
+  return v;
+}
+template <int MINB, int POPS, int SMEM>
+static void launch_k2q(const DevGrid& g, const DevParams& p, const DevCam& cam,
+                       const double4* rgbd, const DevPose* poses, const int* batch, int n,
+                       const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
+                       const int* global_counts, float4* grad, double lambda_d,
+                       const uint32_t* order, RecBuf rec, int K, const int2* rec_count,
+                       cudaStream_t s) {
+  static const bool attr = cudaFuncSetAttribute(k_map_backward_q<MINB, POPS>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                SMEM) == cudaSuccess;
+  (void)attr;
+  k_map_backward_q<MINB, POPS><<<(n + kThreads - 1) / kThreads, kThreads, SMEM, s>>>(
+      g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
+      order, rec, K, rec_count);
+}
 void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam& cam,
                              const double4* rgbd, const DevPose* poses, const int* batch, int n,
                              const double4* ray_cd, const uint8_t* flags, const MapStats* stats,
@@ -2592,16 +2615,20 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
     return;
   }
   // K2q: 4 CTAs/SM (VRF_K2_MINB), 2 pops per step. r01 (config 3 / config 4, ms): 1, 2 or 3
-  // pops 14.54 / 14.63 / 15.02 and 25.82 / 25.71 / 25.78.
-  constexpr int kMinB = VRF_K2_MINB, kPops = VRF_K2_POPS;
+  // pops 14.54 / 14.63 / 15.02 and 25.82 / 25.71 / 25.78. Batches of >= k2_minb3_rays()
+  // rays run the 3-CTA/SM build (168-register cap): r02, config 4 (8M rays, 513^3
+  // sparse, reductions missing L2) 26.3-26.5 ms against 28.1 at 4 CTAs/SM; config 3
+  // (1M rays) prefers 4 (10.39 against 10.87 ms).
+  constexpr int kPops = VRF_K2_POPS;
   constexpr int kSmem = VRF_K2_RING ? kRingSmemBytes : kQMergeSmemBytes;
-  static const bool attr = cudaFuncSetAttribute(k_map_backward_q<kMinB, kPops>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                kSmem) == cudaSuccess;
-  (void)attr;
-  k_map_backward_q<kMinB, kPops><<<(n + kThreads - 1) / kThreads, kThreads, kSmem, s>>>(
-      g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats, global_counts, grad, lambda_d,
-      order, rec, K, rec_count);
+  if (VRF_K2_MINB != 3 && n >= k2_minb3_rays()) {
+    launch_k2q<3, kPops, kSmem>(g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats,
+                                global_counts, grad, lambda_d, order, rec, K, rec_count, s);
+    return;
+  }
+  launch_k2q<VRF_K2_MINB, kPops, kSmem>(g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats,
+                                        global_counts, grad, lambda_d, order, rec, K,
+                                        rec_count, s);
 }
 void launch_map_reduce(const MapPartial* partials, int nparts, MapStats* out, cudaStream_t s) {
   k_map_reduce<<<1, 1024, 0, s>>>(partials, nparts, out);

@@ -37,6 +37,8 @@ def test_bench_line_has_the_contract_keys():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    # achieved counts compulsory HBM bytes, so it is a real fraction of the peak
+    assert 0 < r["frac"] <= 1.2
     assert d["tracking"]["frames_per_s"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
 

@@ -576,6 +576,37 @@ def test_fast_gradient_matches_deterministic_at_larger_batches(ctx, oracle, n_ra
     assert np.array_equal(fast != 0, det != 0)
 
 
+def test_k2q_three_ctas_per_sm_matches_deterministic(tmp_path):
+    """The 3-CTA/SM K2q build that batches of >= 4M rays run (config 4), forced
+    at 200K rays with VRF_K2_MINB3_RAYS=0: the fast gradient against the
+    deterministic FP64 one at the same 1e-3 tolerance, same touched set."""
+    import subprocess
+    import sys as _sys
+    script = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, "."); sys.path.insert(0, "oracle")
+from scenes import room_scene, fresh_grid
+from paper_2307_03404_b200 import Context, MappingConfig
+import oracle as orc
+grid, intr, frames = room_scene(res=33, width=64, height=48)
+ctx = Context(0)
+ctx.load_grid(fresh_grid(grid, seed=9)); ctx.load_frames(intr, frames)
+batch = orc.Oracle().draw_batch(21, len(frames), intr.width, intr.height, 200000)
+fast, sf = ctx.mapping_gradient(MappingConfig(), batch)
+det, sd = ctx.mapping_gradient(MappingConfig(deterministic=True), batch)
+np.savez(sys.argv[1], fast=fast, det=det, s=np.array([sf.samples, sd.samples]))
+'''
+    f = tmp_path / "k2q3.npz"
+    env = dict(os.environ, VRF_K2_MINB3_RAYS="0")
+    subprocess.run([_sys.executable, "-c", script, str(f)], check=True, env=env,
+                   cwd=str(Path(__file__).resolve().parent.parent))
+    d = np.load(f)
+    assert d["s"][0] == d["s"][1]
+    scale = np.abs(d["det"]).max()
+    assert np.max(np.abs(d["fast"] - d["det"])) <= 1e-3 * scale
+    assert np.array_equal(d["fast"] != 0, d["det"] != 0)
+
+
 def test_synth_from_grid_matches_oracle_renders(ctx, oracle):
     """synth_from_grid (dataset.cpp:443-462) on the device: the quantised frames
     equal the oracle's render_image quantised the same way (renders agree to
