@@ -2723,6 +2723,7 @@ void launch_exchange_p2p(const PeerTable& pt, float4* v, int nb, int rx, int ry,
     k_exchange_p2p<<<grid, 256, 0, s>>>(pt, v, nb, rx, ry, rz, tbx, tby, rho, lr_sigma, lr_sh, eps,
                                         stats);
 }
+#ifdef VRF_GATHER_SOA  // A/B build only (the planar gather layout)
 __global__ void k_aos_to_soa(const float4* __restrict__ aos, float4* __restrict__ soa,
                              long long nv) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv * kVec4PerVertex;
@@ -2734,6 +2735,7 @@ __global__ void k_aos_to_soa(const float4* __restrict__ aos, float4* __restrict_
 void launch_aos_to_soa(const float4* aos, float4* soa, long long nv, cudaStream_t s) {
   k_aos_to_soa<<<grid_blocks(nv * kVec4PerVertex, 256), 256, 0, s>>>(aos, soa, nv);
 }
+#endif
 // Order-independent 64-bit digest of a word array: sum over i of mix(i, w_i)
 // (splitmix64 finaliser of the index-salted word), so any changed word, moved word
 // or changed length changes it w.h.p.; per-block sums, one atomic add per block.
