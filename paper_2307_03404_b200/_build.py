@@ -7,8 +7,10 @@ from __future__ import annotations
 
 import hashlib
 import os
+import re
 import shutil
 import subprocess
+import tempfile
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -46,6 +48,58 @@ def _digest() -> str:
     return h.hexdigest()
 
 
+_WIDTH = {".64": 8, ".128": 16, ".U8": 1, ".S8": 1, ".U16": 2, ".S16": 2}
+
+
+def unwritten_local_loads(lib: Path) -> dict:
+    """Kernels whose SASS loads a stack slot ([R1 + off]) that no store of the
+    kernel writes. r02 found ptxas (CUDA 12.9, sm_100a) spilling
+    k_pose_group_u under a 128-register cap with LDL.LU from two slots and no
+    STL to either (the ray origin was read back as garbage). Kernels that store
+    through computed addresses (local arrays) are skipped: their slots cannot be
+    matched statically. {} when clean or when cuobjdump / nvdisasm are absent."""
+    cuobjdump, nvdisasm = shutil.which("cuobjdump"), shutil.which("nvdisasm")
+    if not cuobjdump or not nvdisasm:
+        return {}
+    bad = {}
+    with tempfile.TemporaryDirectory() as d:
+        r = subprocess.run([cuobjdump, "-xelf", "all", str(Path(lib).resolve())], cwd=d,
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            return {}
+        for cub in sorted(Path(d).glob("*.cubin")):
+            sass = subprocess.run([nvdisasm, "-c", str(cub)], capture_output=True,
+                                  text=True).stdout.split("\n")
+            kern, st, ld, computed = None, {}, {}, set()
+            for raw in sass:
+                m = re.match(r"\s*\.text\.(\S+):", raw)
+                if m:
+                    kern = m.group(1)
+                    continue
+                m = re.search(r"\b(STL|LDL)((?:\.[A-Z0-9]+)*)\s+(.*?);", raw)
+                if not (m and kern):
+                    continue
+                w = next((v for k, v in _WIDTH.items() if k in m.group(2).split(".") or
+                          m.group(2).endswith(k)), 4)
+                a = re.search(r"\[R1(?:\+0x([0-9a-f]+))?\]", m.group(3))
+                if not a:
+                    if m.group(1) == "STL":
+                        computed.add(kern)
+                    continue
+                o = int(a.group(1) or "0", 16)
+                (st if m.group(1) == "STL" else ld).setdefault(kern, []).append((o, w))
+            for k, loads in ld.items():
+                if k in computed:
+                    continue
+                cov = set()
+                for o, w in st.get(k, []):
+                    cov.update(range(o, o + w))
+                miss = sorted({o for o, w in loads if not set(range(o, o + w)) <= cov})
+                if miss:
+                    bad[k] = miss
+    return bad
+
+
 def build(force: bool = False, verbose: bool = False, libdir: Path = LIBDIR,
           defines=()) -> Path:
     """Compile every CUDA source for sm_100a and link the C-ABI library. libdir /
@@ -81,6 +135,12 @@ def build(force: bool = False, verbose: bool = False, libdir: Path = LIBDIR,
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")
     (libdir / "ptxas.log").write_text("\n".join(log))
+    bad = unwritten_local_loads(lib)
+    if bad:
+        lib.unlink()
+        raise RuntimeError(
+            "ptxas emitted local-memory loads from stack slots the kernel never stores "
+            f"(the spill miscompile of DESIGN.md §5): {bad}")
     stamp.write_text(digest)
     if verbose:
         print("\n".join(log))

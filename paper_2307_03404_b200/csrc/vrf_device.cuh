@@ -258,8 +258,15 @@ __device__ __forceinline__ bool super_active(const DevGrid& g, int cx, int cy, i
 // would be dropped by the occupancy test, so skipping them leaves the schedule
 // unchanged. A 1e-6 m margin keeps the jump clear of the exit face and absorbs
 // the rounding of the reciprocal-based exit time.
+// RECIP = true recomputes the reciprocals (m.inv_d, m.inv_step) instead of
+// reading them, and a non-null `origin` (the ray origin in global memory, e.g.
+// the pose translation every ray of a tracking batch starts from) replaces m.o:
+// the same values, so the same jump, and callers short of registers need not
+// keep them live (k_pose_group_u).
+template <bool RECIP = false>
 __device__ __forceinline__ long long skip_empty_box(const DevGrid& g, const March& m,
-                                                    const Sample& s, int L) {
+                                                    const Sample& s, int L,
+                                                    const double* __restrict__ origin = nullptr) {
   const double ext = (double)(1 << L) * g.voxel;
   const int b[3] = {s.cx >> L, s.cy >> L, s.cz >> L};
   const double org[3] = {g.ox, g.oy, g.oz};
@@ -267,11 +274,12 @@ __device__ __forceinline__ long long skip_empty_box(const DevGrid& g, const Marc
   for (int a = 0; a < 3; ++a) {
     if (m.d[a] == 0.0) continue;
     const double face = org[a] + (m.d[a] > 0.0 ? (b[a] + 1) : b[a]) * ext;
-    const double t = (face - m.o[a]) * m.inv_d[a];
+    const double oa = (RECIP && origin) ? __ldg(origin + a) : m.o[a];
+    const double t = (face - oa) * (RECIP ? 1.0 / m.d[a] : m.inv_d[a]);
     t_out = t < t_out ? t : t_out;
   }
   // midpoint of segment k is ~ lo + (k + 0.5) step; stay below t_out - margin
-  const double kf = floor((t_out - 1e-6 - m.lo) * m.inv_step - 0.5);
+  const double kf = floor((t_out - 1e-6 - m.lo) * (RECIP ? 1.0 / m.step : m.inv_step) - 0.5);
   const long long k_new = kf > (double)m.nseg ? m.nseg : (long long)kf;
   return k_new > m.k ? k_new : m.k;
 }

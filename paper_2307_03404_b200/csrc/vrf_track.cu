@@ -310,7 +310,10 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
 // at 2 CTAs/SM it matched k_pose_group<double>. That instance was never on a
 // product path; r02 removed it rather than ship an unexplained build (the FP64
 // parity path is k_pose_group<double>). The fp32 build has no spills.
-template <int MINB = 3>
+#ifndef VRF_POSE_U_MINB
+#define VRF_POSE_U_MINB 3  // CTAs per SM of k_pose_group_u (A/B knob)
+#endif
+template <int MINB = VRF_POSE_U_MINB>
 __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd_base,
     const int* __restrict__ frame_idx, long long npix, const DevPose* __restrict__ pose_ptr,
@@ -363,7 +366,8 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
   double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
   int count = 0;
   const int kc = sub, dx = kc & 1, dy = (kc >> 1) & 1, dz = (kc >> 2) & 1;
-  const double sgn[2] = {-1.0, 1.0};
+  // this lane's corner signs (sgn[d] of k_pose_group: -1 for d = 0, +1 for d = 1)
+  const JT sx = dx ? JT(1) : JT(-1), sy = dy ? JT(1) : JT(-1), sz = dz ? JT(1) : JT(-1);
   Sample mine{};  // value-initialised: lanes read it only after a located segment
   unsigned act = 0;
   while (__any_sync(FULL, alive)) {
@@ -379,8 +383,12 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
         const double len = dsub(s1, s0);
         if (len >= 1e-12) {
           const double tm = dmul(0.5, dadd(s0, s1));
-          const double pp[3] = {dadd(m.o[0], dmul(tm, m.d[0])), dadd(m.o[1], dmul(tm, m.d[1])),
-                                dadd(m.o[2], dmul(tm, m.d[2]))};
+          // the origin is the pose translation, shared by every ray: read it
+          // (uniform address, L1 broadcast) instead of keeping m.o live
+          const double* po = pose_ptr->t;
+          const double pp[3] = {dadd(__ldg(po), dmul(tm, m.d[0])),
+                                dadd(__ldg(po + 1), dmul(tm, m.d[1])),
+                                dadd(__ldg(po + 2), dmul(tm, m.d[2]))};
           if (locate(g, pp, mine)) {
             if (cell_active(g, mine.cell)) {
               a = true;
@@ -403,8 +411,9 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
     }
     long long kn = 0;
     if (jskip >= 0 && sub == jskip)
-      kn = skip_empty_box(g, m, mine,
-                          super_active(g, mine.cx, mine.cy, mine.cz) ? kBlockLog2 : kSuperLog2);
+      kn = skip_empty_box<true>(g, m, mine,
+                                super_active(g, mine.cx, mine.cy, mine.cz) ? kBlockLog2 : kSuperLog2,
+                                pose_ptr->t);
     kn = __shfl_sync(FULL, kn, gbase + (jskip >= 0 ? jskip : 0));
     if (jskip >= 0 && kn > m.k) m.k = kn;
     if (need && act == 0 && m.k >= m.nseg) alive = false;  // ray exhausted
@@ -423,20 +432,16 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
     double pk = 0.0;
     ShT cp[3] = {ShT(0), ShT(0), ShT(0)};
     JT Gs[3] = {0, 0, 0}, Gc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    double wx[2] = {0, 0}, wy[2] = {0, 0}, wz[2] = {0, 0};
     if (has) {
-      wx[0] = dsub(1.0, s.fx);
-      wx[1] = s.fx;
-      wy[0] = dsub(1.0, s.fy);
-      wy[1] = s.fy;
-      wz[0] = dsub(1.0, s.fz);
-      wz[1] = s.fz;
-      const JT wxj[2] = {JT(wx[0]), JT(wx[1])}, wyj[2] = {JT(wy[0]), JT(wy[1])},
-               wzj[2] = {JT(wz[0]), JT(wz[1])};
+      // the lane's own corner weights, selected rather than indexed (the [2]
+      // arrays of k_pose_group live in local memory here): the same values, so
+      // the same arithmetic bit for bit
+      const double wxl = dx ? s.fx : dsub(1.0, s.fx), wyl = dy ? s.fy : dsub(1.0, s.fy),
+                   wzl = dz ? s.fz : dsub(1.0, s.fz);
+      const JT wxj = JT(wxl), wyj = JT(wyl), wzj = JT(wzl);
       const JT iv = JT(g.inv_voxel);
-      const double wk = dmul(dmul(wx[dx], wy[dy]), wz[dz]);
-      const JT dw[3] = {JT(sgn[dx]) * wyj[dy] * wzj[dz] * iv, wxj[dx] * JT(sgn[dy]) * wzj[dz] * iv,
-                        wxj[dx] * wyj[dy] * JT(sgn[dz]) * iv};
+      const double wk = dmul(dmul(wxl, wyl), wzl);
+      const JT dw[3] = {sx * wyj * wzj * iv, wxj * sy * wzj * iv, wxj * wyj * sz * iv};
       const float4* vp4 = g.payload + (size_t)corner_index(g, s.base, kc) * kVec4PerVertex;
       float v[28];
 #pragma unroll
@@ -512,6 +517,11 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
           Jd[r][q] = fma(JT(s.t), gv, Jd[r][q]);
         }
       }
+#if VRF_POSE_DEBUG
+      if (blockIdx.x == 0 && threadIdx.x < 16)
+        printf("dbg t%d cnt%d sraw %.6g delta %.6g st %.6g decay %.6g T %.6g->%.6g act %x k %lld nseg %lld\n",
+               threadIdx.x, count, sraw, s.delta, s.t, decay, T, T_next, act, m.k, m.nseg);
+#endif
       T = T_next;
       if (T < p.eps) alive = false;
     }
