@@ -305,11 +305,12 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
 // colour in lane order, Jacobian partials) is the same as k_pose_group<float>,
 // and tests/test_gpu_pose.py holds the two bit-identical.
 //
-// fp32 only. r01 built an FP64-SH instance of this template as well: at 3
-// CTAs/SM (168 registers, 68 B of spill) it composited one sample per ray, and
-// at 2 CTAs/SM it matched k_pose_group<double>. That instance was never on a
-// product path; r02 removed it rather than ship an unexplained build (the FP64
-// parity path is k_pose_group<double>). The fp32 build has no spills.
+// fp32 only (the FP64 parity path is k_pose_group<double>). r01's FP64-SH
+// instance and r02's 4-CTA/SM build composited one sample per ray: ptxas
+// (CUDA 12.9) spilled the ray origin to stack slots it never stored
+// (profiles/r02_pose_spill_bug.md). The march therefore reads the origin from
+// the pose, and the kernel builds without spills at 3 or 4 CTAs/SM; every build
+// rejects never-stored stack loads (_build.unwritten_local_loads).
 #ifndef VRF_POSE_U_MINB
 #define VRF_POSE_U_MINB 3  // CTAs per SM of k_pose_group_u (A/B knob)
 #endif
