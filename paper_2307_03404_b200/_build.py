@@ -51,6 +51,39 @@ def _digest() -> str:
 _WIDTH = {".64": 8, ".128": 16, ".U8": 1, ".S8": 1, ".U16": 2, ".S16": 2}
 
 
+def scan_local_slots(sass_lines) -> dict:
+    """{kernel: [stack offsets loaded but never stored]} for one `nvdisasm -c`
+    listing (see unwritten_local_loads)."""
+    bad = {}
+    kern, st, ld, computed = None, {}, {}, set()
+    for raw in sass_lines:
+        m = re.match(r"\s*\.text\.(\S+):", raw)
+        if m:
+            kern = m.group(1)
+            continue
+        m = re.search(r"\b(STL|LDL)((?:\.[A-Z0-9]+)*)\s+(.*?);", raw)
+        if not (m and kern):
+            continue
+        w = next((v for k, v in _WIDTH.items() if m.group(2).endswith(k)), 4)
+        a = re.search(r"\[R1(?:\+0x([0-9a-f]+))?\]", m.group(3))
+        if not a:
+            if m.group(1) == "STL":
+                computed.add(kern)
+            continue
+        o = int(a.group(1) or "0", 16)
+        (st if m.group(1) == "STL" else ld).setdefault(kern, []).append((o, w))
+    for k, loads in ld.items():
+        if k in computed:
+            continue
+        cov = set()
+        for o, w in st.get(k, []):
+            cov.update(range(o, o + w))
+        miss = sorted({o for o, w in loads if not set(range(o, o + w)) <= cov})
+        if miss:
+            bad[k] = miss
+    return bad
+
+
 def unwritten_local_loads(lib: Path) -> dict:
     """Kernels whose SASS loads a stack slot ([R1 + off]) that no store of the
     kernel writes. r02 found ptxas (CUDA 12.9, sm_100a) spilling
@@ -70,33 +103,7 @@ def unwritten_local_loads(lib: Path) -> dict:
         for cub in sorted(Path(d).glob("*.cubin")):
             sass = subprocess.run([nvdisasm, "-c", str(cub)], capture_output=True,
                                   text=True).stdout.split("\n")
-            kern, st, ld, computed = None, {}, {}, set()
-            for raw in sass:
-                m = re.match(r"\s*\.text\.(\S+):", raw)
-                if m:
-                    kern = m.group(1)
-                    continue
-                m = re.search(r"\b(STL|LDL)((?:\.[A-Z0-9]+)*)\s+(.*?);", raw)
-                if not (m and kern):
-                    continue
-                w = next((v for k, v in _WIDTH.items() if k in m.group(2).split(".") or
-                          m.group(2).endswith(k)), 4)
-                a = re.search(r"\[R1(?:\+0x([0-9a-f]+))?\]", m.group(3))
-                if not a:
-                    if m.group(1) == "STL":
-                        computed.add(kern)
-                    continue
-                o = int(a.group(1) or "0", 16)
-                (st if m.group(1) == "STL" else ld).setdefault(kern, []).append((o, w))
-            for k, loads in ld.items():
-                if k in computed:
-                    continue
-                cov = set()
-                for o, w in st.get(k, []):
-                    cov.update(range(o, o + w))
-                miss = sorted({o for o, w in loads if not set(range(o, o + w)) <= cov})
-                if miss:
-                    bad[k] = miss
+            bad.update(scan_local_slots(sass))
     return bad
 
 

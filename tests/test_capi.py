@@ -54,3 +54,38 @@ def test_bench_and_entry_compile():
     root = Path(__file__).resolve().parent.parent
     for name in ("bench.py", "__graft_entry__.py"):
         py_compile.compile(str(root / name), doraise=True)
+
+
+def test_spill_slot_scanner_flags_never_stored_loads():
+    """_build.scan_local_slots (the build-time guard against the ptxas spill
+    miscompile, profiles/r02_pose_spill_bug.md) on fabricated listings: a load
+    from a slot no store writes is flagged; covered loads, and kernels that store
+    through computed addresses, are not."""
+    from paper_2307_03404_b200 import _build
+    sass = """
+        .text._Z3badv:
+        /*0000*/  STL [R1+0x70], R0 ;
+        /*0010*/  STL.128 [R1], R4 ;
+        /*0020*/  LDL.LU.64 R16, [R1+0x68] ;
+        /*0030*/  LDL.64 R18, [R1+0x8] ;
+        /*0040*/  LDL R2, [R1+0x70] ;
+        .text._Z4goodv:
+        /*0000*/  STL.64 [R1+0x8], R2 ;
+        /*0010*/  LDL.LU.64 R4, [R1+0x8] ;
+        .text._Z8computedv:
+        /*0000*/  STL [R7], R2 ;
+        /*0010*/  LDL R4, [R1+0x20] ;
+    """.split("\n")
+    assert _build.scan_local_slots(sass) == {"_Z3badv": [0x68]}
+
+
+def test_built_library_has_no_never_stored_stack_loads():
+    """The product library as built: no kernel reads a stack slot it never
+    writes (skipped when cuobjdump / nvdisasm are absent)."""
+    import shutil
+    from paper_2307_03404_b200 import _build
+    lib = Path(_capi._LIB_PATH)
+    if not lib.exists() or not shutil.which("nvdisasm"):
+        import pytest
+        pytest.skip("library or nvdisasm absent")
+    assert _build.unwritten_local_loads(lib) == {}
