@@ -579,23 +579,25 @@ int vrf_frame_set_u8u16(vrf_context* ctx, int slot, const uint8_t* rgb, const ui
   if (slot < 0 || slot >= ctx->frame_capacity)
     return set_err(ctx, VRF_ERR_OUT_OF_RANGE, "frames: slot out of range");
   const long long npix = (long long)ctx->fintr.width * ctx->fintr.height;
-  const size_t bytes = (size_t)npix * 3 + (size_t)npix * 2;
+  const size_t doff = ((size_t)npix * 3 + 15) & ~(size_t)15;  // aligned depth block
+  const size_t poff = (doff + (size_t)npix * 2 + 15) & ~(size_t)15;  // the pose after it
+  const size_t bytes = doff + (size_t)npix * 2;
   int rc = ensure(ctx, ctx->s_stage, bytes + 16);
   if (rc) return rc;
-  if ((rc = ensure_pinned(ctx, std::max(bytes + 16, sizeof(DevPose))))) return rc;
+  if ((rc = ensure_pinned(ctx, poff + sizeof(DevPose)))) return rc;
   char* h = (char*)ctx->h_pinned;
-  const size_t doff = ((size_t)npix * 3 + 15) & ~(size_t)15;  // aligned depth block
   std::memcpy(h, rgb, (size_t)npix * 3);
   std::memcpy(h + doff, depth, (size_t)npix * 2);
+  const DevPose dp = dev_pose(pose);
+  std::memcpy(h + poff, &dp, sizeof(dp));
   char* st = (char*)ctx->s_stage.ptr;
-  CU(cudaMemcpyAsync(st, h, doff + (size_t)npix * 2, cudaMemcpyHostToDevice, ctx->stream));
+  // one sensor copy, the decode, the pose copy, one synchronize (the pinned
+  // stage is reused by the next call)
+  CU(cudaMemcpyAsync(st, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
   launch_pack_frames_u8((const uint8_t*)st, (const uint16_t*)(st + doff), ctx->fintr.depth_scale,
                         ctx->rgbd + npix * slot, npix, ctx->stream);
   LAUNCHED(1);
-  CU(cudaStreamSynchronize(ctx->stream));  // the pinned stage is reused below
-  const DevPose dp = dev_pose(pose);
-  std::memcpy(ctx->h_pinned, &dp, sizeof(dp));
-  CU(cudaMemcpyAsync(ctx->poses + slot, ctx->h_pinned, sizeof(DevPose), cudaMemcpyHostToDevice,
+  CU(cudaMemcpyAsync(ctx->poses + slot, h + poff, sizeof(DevPose), cudaMemcpyHostToDevice,
                      ctx->stream));
   ctx->host_depth[slot].clear();  // rebuilt from the device on demand (Adam tracking)
   ctx->n_frames = std::max(ctx->n_frames, slot + 1);
