@@ -29,6 +29,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "voxrf/mapping.hpp"
@@ -371,14 +372,19 @@ vrf_mapping_config to_c(const MappingConfig& c) {
   return o;
 }
 
-// mapping.cpp:121-128: the batch is drawn single-threaded from the caller's Rng.
+// mapping.cpp:121-128: the batch is drawn from the caller's Rng. The library's
+// vrf_rng_draw_batch produces the same stream (one raw draw per index, so large
+// batches are drawn in parallel from jumped-ahead states) and leaves the Rng
+// where the reference's loop would. Rng is xoshiro256**'s four words and nothing
+// else (rng.hpp:13-81), so its state is copied bytewise.
+static_assert(std::is_trivially_copyable_v<Rng> && sizeof(Rng) == 4 * sizeof(std::uint64_t),
+              "voxrf::Rng is expected to hold exactly the xoshiro256** state");
 std::vector<int32_t> draw_batch(Rng& rng, int n_frames, const CameraIntrinsics& intr, int n) {
   std::vector<int32_t> b(3 * std::size_t(n));
-  for (int i = 0; i < n; ++i) {
-    b[3 * i] = int32_t(rng.uniform_index(std::uint64_t(n_frames)));
-    b[3 * i + 1] = int32_t(rng.uniform_index(std::uint64_t(intr.width)));
-    b[3 * i + 2] = int32_t(rng.uniform_index(std::uint64_t(intr.height)));
-  }
+  std::uint64_t st[4];
+  std::memcpy(st, &rng, sizeof(st));
+  vrf_rng_draw_batch(st, n_frames, intr.width, intr.height, n, b.data());
+  std::memcpy(static_cast<void*>(&rng), st, sizeof(st));
   return b;
 }
 

@@ -1,6 +1,9 @@
 // Tracking entry points of the C-ABI: pose_gradient (tracking.cpp:76-143), the
 // Gauss-Newton normal equations, track_frame with the reference's Adam loop
 // (tracking.cpp:170-252) and a Gauss-Newton/LM tracker.
+#include <thread>
+#include <vector>
+
 #include "vrf_context.h"
 
 using namespace vrf;
@@ -37,6 +40,55 @@ struct Xoshiro {
   }
   uint64_t index(uint64_t n) { return (uint64_t)(((unsigned __int128)next() * n) >> 64); }
 };
+
+// Jump-ahead of the xoshiro256** state by k steps. The state transition is
+// linear over GF(2)^256, so T^k = product of the cached powers T^(2^j) for the
+// set bits of k; each power is kept as its 256 column images (the state bit b
+// maps to column b), and applying one is 256 conditional 4-word XORs.
+struct XoshiroPowers {
+  static constexpr int kMax = 34;  // k < 2^34 draws (3 per ray, n < 2^31)
+  uint64_t col[kMax][256][4];
+  static void step(uint64_t s[4]) {
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = (s[3] << 45) | (s[3] >> 19);
+  }
+  static void apply(const uint64_t (&m)[256][4], uint64_t s[4]) {
+    uint64_t o[4] = {0, 0, 0, 0};
+    for (int b = 0; b < 256; ++b)
+      if ((s[b >> 6] >> (b & 63)) & 1u)
+        for (int w = 0; w < 4; ++w) o[w] ^= m[b][w];
+    for (int w = 0; w < 4; ++w) s[w] = o[w];
+  }
+  XoshiroPowers() {
+    for (int b = 0; b < 256; ++b) {
+      uint64_t e[4] = {0, 0, 0, 0};
+      e[b >> 6] = 1ull << (b & 63);
+      step(e);
+      for (int w = 0; w < 4; ++w) col[0][b][w] = e[w];
+    }
+    for (int j = 1; j < kMax; ++j)
+      for (int b = 0; b < 256; ++b) {
+        uint64_t e[4];
+        for (int w = 0; w < 4; ++w) e[w] = col[j - 1][b][w];
+        apply(col[j - 1], e);
+        for (int w = 0; w < 4; ++w) col[j][b][w] = e[w];
+      }
+  }
+};
+void xoshiro_jump(uint64_t s[4], uint64_t k) {
+  if (k == 0) return;
+  static const XoshiroPowers* P = new XoshiroPowers();  // built once, 272 KB
+  for (int j = 0; k; ++j, k >>= 1)
+    if (k & 1u) {
+      if (j >= XoshiroPowers::kMax) abort();
+      XoshiroPowers::apply(P->col[j], s);
+    }
+}
 
 // tracking.cpp:147-166
 void draw_valid_pixels(const std::vector<double>& depth, int w, int h, int count, int max_redraws,
@@ -218,13 +270,41 @@ uint64_t vrf_rng_next(uint64_t state[4]) {
 }
 void vrf_rng_draw_batch(uint64_t state[4], int n_frames, int width, int height, int n,
                         int32_t* batch) {
+  // mapping.cpp:121-128: three draws per ray, one raw output each (index(n) =
+  // (next * n) >> 64), so ray i starts at stream position 3 i and chunks of a
+  // large batch can be drawn in parallel from jumped-ahead states (bit-identical
+  // to the sequential stream; the final state is the one after 3 n draws).
+  auto draw = [=](Xoshiro r, int i0, int i1) {
+    for (int i = i0; i < i1; ++i) {
+      batch[3 * i] = (int32_t)r.index((uint64_t)n_frames);
+      batch[3 * i + 1] = (int32_t)r.index((uint64_t)width);
+      batch[3 * i + 2] = (int32_t)r.index((uint64_t)height);
+    }
+  };
   Xoshiro r(0);
   for (int i = 0; i < 4; ++i) r.s[i] = state[i];
-  for (int i = 0; i < n; ++i) {
-    batch[3 * i] = (int32_t)r.index((uint64_t)n_frames);
-    batch[3 * i + 1] = (int32_t)r.index((uint64_t)width);
-    batch[3 * i + 2] = (int32_t)r.index((uint64_t)height);
+  const int hw = (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+  const int parts = n >= (1 << 16) ? std::min(hw, n >> 15) : 1;
+  if (parts <= 1) {
+    for (int i = 0; i < n; ++i) {
+      batch[3 * i] = (int32_t)r.index((uint64_t)n_frames);
+      batch[3 * i + 1] = (int32_t)r.index((uint64_t)width);
+      batch[3 * i + 2] = (int32_t)r.index((uint64_t)height);
+    }
+    for (int i = 0; i < 4; ++i) state[i] = r.s[i];
+    return;
+  } else {
+    std::vector<std::thread> pool;
+    for (int c = 1; c < parts; ++c) {
+      const int i0 = (int)((long long)n * c / parts), i1 = (int)((long long)n * (c + 1) / parts);
+      Xoshiro rc = r;
+      xoshiro_jump(rc.s, 3ull * (uint64_t)i0);
+      pool.emplace_back(draw, rc, i0, i1);
+    }
+    draw(r, 0, (int)((long long)n / parts));
+    for (auto& t : pool) t.join();
   }
+  xoshiro_jump(r.s, 3ull * (uint64_t)n);
   for (int i = 0; i < 4; ++i) state[i] = r.s[i];
 }
 int vrf_rng_draw_valid_pixels(uint64_t state[4], const double* depth, int width, int height,

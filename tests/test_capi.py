@@ -89,3 +89,31 @@ def test_built_library_has_no_never_stored_stack_loads():
         import pytest
         pytest.skip("library or nvdisasm absent")
     assert _build.unwritten_local_loads(lib) == {}
+
+
+def test_parallel_batch_draw_equals_the_sequential_stream():
+    """vrf_rng_draw_batch draws batches of >= 65,536 rays in parallel chunks from
+    jumped-ahead xoshiro256** states (GF(2) powers of the transition). The rays
+    and the final state equal the sequential stream's (rng.hpp:20-41: one raw
+    draw per uniform_index), here checked against the same stream drawn in
+    sub-threshold pieces, which run sequentially."""
+    from paper_2307_03404_b200 import Rng
+    for n in (65536, 100003, 1 << 20):
+        a = Rng(11)
+        b = Rng(11)
+        got = a.draw_batch(10, 1200, 680, n)
+        parts, left = [], n
+        while left:
+            m = min(left, 40000)
+            parts.append(b.draw_batch(10, 1200, 680, m))
+            left -= m
+        assert np.array_equal(got, np.concatenate(parts))
+        assert list(a.state) == list(b.state)
+
+
+def test_host_rng_matches_oracle_across_the_parallel_threshold(oracle):
+    """The same, against the C oracle's sequential Rng (the reference stream)."""
+    from paper_2307_03404_b200 import Rng
+    n = 70000
+    got = Rng(5).draw_batch(3, 64, 48, n)
+    assert np.array_equal(got, oracle.draw_batch(5, 3, 64, 48, n))
