@@ -1345,6 +1345,8 @@ constexpr int kVCache = 28;
 // lanes' SH bases (12 floats each, 96 float4); with the cache, its entries
 // (kVCache x 7 float4) and tags (kVCache u32) follow
 constexpr int kSbfOff = VRF_K2_VCACHE ? 32 : 32 * kVec4PerVertex - 32 * 3;
+// (MERGE 4 stages up to 15 holder rows of 7 float4 below kSbfOff = 128)
+static_assert(VRF_K2_MERGE != 4 || 16 * kVec4PerVertex <= kSbfOff, "merge-4 rows overlap the bases");
 constexpr int kVCacheOff = 128;
 constexpr int kWarpStage =
     VRF_K2_VCACHE ? kVCacheOff + kVCache * kVec4PerVertex + kVCache / 4 : 32 * kVec4PerVertex;
@@ -1365,6 +1367,12 @@ struct QueueSink {
   }
 };
 
+#ifndef VRF_K2_GSTATS
+#define VRF_K2_GSTATS 0
+#endif
+#if VRF_K2_GSTATS
+__device__ unsigned long long g_k2_gsize[33], g_k2_rmax[33];
+#endif
 // One pop round: the lane's oldest queued corner. The ~28 lanes popping together
 // often hold the same vertex (33% of pops duplicate another lane's vertex in the
 // same round, r01 counters): lanes popping the same vertex are grouped
@@ -1397,6 +1405,15 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
 #endif
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(grp) - 1;
+#if VRF_K2_GSTATS
+    // diagnostic build: histogram of duplicate-group sizes (one count per group)
+    // and of each pop round's largest group (the merge loop's trip count + 1)
+    {
+      if (lane == leader) atomicAdd(&g_k2_gsize[__popc(grp)], 1ull);
+      const unsigned mx = __reduce_max_sync(act, (unsigned)__popc(grp));
+      if (lane == __ffs(act) - 1) atomicAdd(&g_k2_rmax[mx], 1ull);
+    }
+#endif
     float x[28];
     x[0] = e.x;
 #pragma unroll
@@ -1405,7 +1422,72 @@ __device__ __forceinline__ void pop_entry(bool has, uint32_t v, float4 e,
       x[10 + mm] = e.z * bf[mm];
       x[19 + mm] = e.w * bf[mm];
     }
-#if VRF_K2_MERGE == 3 && VRF_K2_SYNC_ACT
+#if VRF_K2_MERGE == 4
+    // Pairwise-first merge (A/B). r02 counters (tools/k2_groups.py, config 3):
+    // 58 % of pops sit in duplicate groups, a pop round's largest group has
+    // 3-4 lanes at the median, and the leader loop below ran 3.2 trips per
+    // round on 3 active lanes. Here level 1 runs every pair of a group at once
+    // in the factor domain (rank 2j absorbs rank 2j+1), and the leader then sums
+    // the surviving even-ranked partial sums as expanded vectors: a group of k
+    // costs 1 + ceil(k/2) - 1 serial steps instead of k - 1.
+    {
+      const unsigned below = grp & ((1u << lane) - 1u);
+      const int rank = __popc(below);
+      const bool multi = grp != (1u << lane);
+      float4* stage_e = stage;  // [32] member factors
+      if (multi && (rank & 1)) stage_e[lane] = e;
+      __syncwarp(act);
+      if (multi && !(rank & 1)) {
+        const unsigned above = grp & ~((2u << lane) - 1u);
+        if (above) {  // the next lane of the group is this lane's odd partner
+          const int o = __ffs(above) - 1;
+          const float* sb = reinterpret_cast<const float*>(stage + kSbfOff) + 12 * o;
+          const float4 eo = stage_e[o], b0 = reinterpret_cast<const float4*>(sb)[0],
+                       b1 = reinterpret_cast<const float4*>(sb)[1];
+          const float bb[9] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, sb[8]};
+          x[0] += eo.x;
+#pragma unroll
+          for (int mm = 0; mm < 9; ++mm) {
+            x[1 + mm] = fmaf(eo.y, bb[mm], x[1 + mm]);
+            x[10 + mm] = fmaf(eo.z, bb[mm], x[10 + mm]);
+            x[19 + mm] = fmaf(eo.w, bb[mm], x[19 + mm]);
+          }
+        }
+      }
+      // level 2: even ranks >= 2 hold partial sums for their group's leader
+      const bool holder = multi && !(rank & 1) && rank >= 2;
+      const unsigned hm = __ballot_sync(act, holder);
+      const bool any2 = hm != 0u;  // warp-uniform
+      if (any2) {
+        __syncwarp(act);  // the factor rows are read; their space is reused
+        if (holder) {
+          float4* row = stage + __popc(hm & ((1u << lane) - 1u)) * kVec4PerVertex;
+#pragma unroll
+          for (int j = 0; j < kVec4PerVertex; ++j)
+            row[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+        }
+        __syncwarp(act);
+        if (lane == leader) {
+          unsigned rest = grp & hm;
+          while (rest) {
+            const int o = __ffs(rest) - 1;
+            rest &= rest - 1;
+            const float4* row = stage + __popc(hm & ((1u << o) - 1u)) * kVec4PerVertex;
+#pragma unroll
+            for (int j = 0; j < kVec4PerVertex; ++j) {
+              const float4 y = row[j];
+              x[4 * j] += y.x;
+              x[4 * j + 1] += y.y;
+              x[4 * j + 2] += y.z;
+              x[4 * j + 3] += y.w;
+            }
+          }
+        }
+      }
+      __syncwarp(act);
+    }
+    if (false) {
+#elif VRF_K2_MERGE == 3 && VRF_K2_SYNC_ACT
     // (the same merge as below, synchronised over all popping lanes: one
     // warp-uniform mask, so WARPSYNC needs no per-group collective emulation)
     {
@@ -1836,7 +1918,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_map_backward_q(
       }
     }
   }
-#if VRF_K2_MERGE == 3
+#if VRF_K2_MERGE >= 3
   {  // the lane's SH basis, read by the group leaders of the factor-domain merge
     float* sbf = reinterpret_cast<float*>(stage + kSbfOff) + 12 * (threadIdx.x & 31);
 #pragma unroll
@@ -2824,3 +2906,17 @@ void launch_prune(const DevGrid& g, uint32_t* bits, double tau, unsigned long lo
 }
 
 }  // namespace vrf
+
+#if VRF_K2_GSTATS
+// diagnostic build only: read and clear the K2 duplicate-group histograms
+// (out[0..32] group sizes, out[33..65] largest group per pop round)
+extern "C" int vrf_debug_k2_hist(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, vrf::g_k2_gsize, sizeof(unsigned long long) * 33);
+  cudaMemcpyFromSymbol(out + 33, vrf::g_k2_rmax, sizeof(unsigned long long) * 33);
+  static const unsigned long long z[33] = {};
+  cudaMemcpyToSymbol(vrf::g_k2_gsize, z, sizeof(z));
+  cudaMemcpyToSymbol(vrf::g_k2_rmax, z, sizeof(z));
+  return (int)cudaGetLastError();
+}
+#endif
+
