@@ -33,7 +33,11 @@ namespace vrf {
 
 namespace {
 
-constexpr int kT = 128;
+#ifndef VRF_POSE_KT
+#define VRF_POSE_KT 128  // threads per CTA of the pose kernels (A/B knob)
+#endif
+constexpr int kT = VRF_POSE_KT;
+static_assert(kT >= 64 && kT % 32 == 0, "the CTA reduction uses threads 0-32");
 
 // ------------------------------------------------------------------ corner-parallel
 // LPR lanes per ray (LPR = 8: one trilinear corner per lane). The tracking batch
