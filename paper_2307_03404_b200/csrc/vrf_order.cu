@@ -1,5 +1,5 @@
 // Coherent ray order for the per-ray kernels: rays sorted by (keyframe, Morton
-// order of 4x4-pixel tiles), so the 32 rays of a warp march nearly the same
+// order of the pixel), so the 32 rays of a warp march nearly the same
 // cells and the grid / gradient lines of the rays in flight stay in L2 (r01:
 // 1.18e9 -> 3.41e9 mapping samples/s over draw order).
 #include <algorithm>
@@ -22,13 +22,31 @@ __device__ __forceinline__ uint32_t spread_bits(uint32_t x) {  // 10 bits -> 20 
   return x;
 }
 
+#ifndef VRF_RAY_TILE_LOG2
+#define VRF_RAY_TILE_LOG2 0  // Morton tile edge 2^T pixels: single pixels (r02 A/B,
+                             // tools/ab/tile.sh: 1.118e10 vs 1.114e10 samples/s for 4x4)
+#endif
+__device__ __forceinline__ uint32_t spread_bits11(uint32_t x) {  // 11 bits -> 22
+  x &= 0x7ff;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
 __global__ void k_ray_keys(const int* __restrict__ batch, int n, uint32_t* keys, uint32_t* ids) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+#if VRF_RAY_TILE_LOG2 == 2
   const uint32_t f = (uint32_t)batch[3 * i], x = (uint32_t)batch[3 * i + 1] >> 2,
                  y = (uint32_t)batch[3 * i + 2] >> 2;
   // keyframe in the high bits, Morton order of 4x4-pixel tiles below
   keys[i] = (f << 20) | spread_bits(x) | (spread_bits(y) << 1);
+#else
+  const uint32_t f = (uint32_t)batch[3 * i], x = (uint32_t)batch[3 * i + 1] >> VRF_RAY_TILE_LOG2,
+                 y = (uint32_t)batch[3 * i + 2] >> VRF_RAY_TILE_LOG2;
+  keys[i] = (f << 22) | spread_bits11(x) | (spread_bits11(y) << 1);
+#endif
   ids[i] = (uint32_t)i;
 }
 
