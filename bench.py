@@ -656,25 +656,34 @@ def run_ours(args):
         gt_ctx.track_frame_gn(1, intr, tposes[0], gn)  # warm-up (allocations)
         torch.cuda.synchronize()
         gt_ctx.profile_enable(True)
-        errs = []
-        t0 = time.perf_counter()
-        prev = tposes[0]
-        for i in range(1, len(tframes)):
-            r = gt_ctx.track_frame_gn(i, intr, prev, gn)
-            prev = r.pose
-            errs.append(np.linalg.norm(np.asarray(r.pose.t) - np.asarray(tposes[i].t)))
-        dt = time.perf_counter() - t0
+        # PASSES identical passes over the frames (each from tposes[0]); the
+        # median pass is reported, so one host hiccup in a ~10 ms region does
+        # not decide the number
+        PASSES = 3
+        dts = []
+        for _ in range(PASSES):
+            errs = []
+            t0 = time.perf_counter()
+            prev = tposes[0]
+            for i in range(1, len(tframes)):
+                r = gt_ctx.track_frame_gn(i, intr, prev, gn)
+                prev = r.pose
+                errs.append(np.linalg.norm(np.asarray(r.pose.t) - np.asarray(tposes[i].t)))
+            dts.append(time.perf_counter() - t0)
+        dt = sorted(dts)[PASSES // 2]
         tp = gt_ctx.profile_read()
         gt_ctx.profile_enable(False)
         nf = len(tframes) - 1
-        g_ms = tp["pose_backward"][0]  # the GN CUDA graphs, CUDA events
-        t_samples = tp.get("track_samples", 0)
+        g_ms = tp["pose_backward"][0] / PASSES  # the GN CUDA graphs, CUDA events
+        t_samples = tp.get("track_samples", 0) / PASSES
         t_rays = nf * gn.iterations * gn.rays_per_iteration
         # SURVEY.md 8d tracking bytes: 896 B per composited sample + 32 B per ray
         t_bytes = 896.0 * t_samples + 32.0 * t_rays
         t_gbps = t_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else 0.0
         tracking = {"config": "config2: 1200x680, 257^3 map, GN/LM 16384 rays x 10 it",
                     "frames_per_s": nf / dt, "ms_per_frame": 1e3 * dt / nf,
+                    "timing": f"median of {PASSES} passes over {nf} frames (each pass from the "
+                              "same initial pose)",
                     "kernel_ms_per_frame": g_ms / nf,
                     "rays_per_s": t_rays / (g_ms / 1e3) if g_ms > 0 else None,
                     "samples_per_s": t_samples / (g_ms / 1e3) if g_ms > 0 else None,
@@ -693,12 +702,15 @@ def run_ours(args):
         gt_ctx.set_frame_u8u16(0, sens[0].color_u8, sens[0].depth_u16, tposes[0])
         gt_ctx.track_frame_gn(0, intr, tposes[0], gn)  # warm-up (slot, graph)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        prev = tposes[0]
-        for i in range(1, len(sens)):
-            gt_ctx.set_frame_u8u16(0, sens[i].color_u8, sens[i].depth_u16, prev)
-            prev = gt_ctx.track_frame_gn(0, intr, prev, gn).pose
-        e_dt = time.perf_counter() - t0
+        e_dts = []
+        for _ in range(PASSES):
+            t0 = time.perf_counter()
+            prev = tposes[0]
+            for i in range(1, len(sens)):
+                gt_ctx.set_frame_u8u16(0, sens[i].color_u8, sens[i].depth_u16, prev)
+                prev = gt_ctx.track_frame_gn(0, intr, prev, gn).pose
+            e_dts.append(time.perf_counter() - t0)
+        e_dt = sorted(e_dts)[PASSES // 2]
         tracking["e2e"] = {
             "frames_per_s": nf / e_dt, "ms_per_frame": 1e3 * e_dt / nf,
             "h2d_bytes_per_frame": intr.width * intr.height * 5, "d2h_bytes_per_frame": 56,
