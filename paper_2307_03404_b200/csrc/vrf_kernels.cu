@@ -2661,11 +2661,15 @@ static int bwd_group_max() {
   }();
   return v;
 }
-// Batch size (rays) from which K2q runs at 3 CTAs/SM; VRF_K2_MINB3_RAYS overrides.
-static int k2_minb3_rays() {
-  static const int v = [] {
-    const char* e = std::getenv("VRF_K2_MINB3_RAYS");
-    return e ? std::atoi(e) : (4 << 20);
+// Grid size (vertices) from which K2q runs at 3 CTAs/SM; VRF_K2_MINB3_VERTS
+// overrides (0: always). r02: config 4 (513^3 sparse) prefers 3 CTAs/SM at 8M rays
+// per batch (26.4 against 27.8 ms) and at 1M (5.64 against 5.94 ms, the per-rank
+// batch of an 8-GPU run), config 3 (257^3) prefers 4 (10.39 against 10.87 ms):
+// the choice follows the grid, not the batch.
+static long long k2_minb3_verts() {
+  static const long long v = [] {
+    const char* e = std::getenv("VRF_K2_MINB3_VERTS");
+    return e ? std::atoll(e) : (64LL << 20);
   }();
   return v;
 }
@@ -2697,13 +2701,11 @@ void launch_map_backward_rec(const DevGrid& g, const DevParams& p, const DevCam&
     return;
   }
   // K2q: 4 CTAs/SM (VRF_K2_MINB), 2 pops per step. r01 (config 3 / config 4, ms): 1, 2 or 3
-  // pops 14.54 / 14.63 / 15.02 and 25.82 / 25.71 / 25.78. Batches of >= k2_minb3_rays()
-  // rays run the 3-CTA/SM build (168-register cap): r02, config 4 (8M rays, 513^3
-  // sparse, reductions missing L2) 26.3-26.5 ms against 28.1 at 4 CTAs/SM; config 3
-  // (1M rays) prefers 4 (10.39 against 10.87 ms).
+  // pops 14.54 / 14.63 / 15.02 and 25.82 / 25.71 / 25.78. Grids of >= k2_minb3_verts()
+  // vertices run the 3-CTA/SM build (168-register cap).
   constexpr int kPops = VRF_K2_POPS;
   constexpr int kSmem = VRF_K2_RING ? kRingSmemBytes : kQMergeSmemBytes;
-  if (VRF_K2_MINB != 3 && n >= k2_minb3_rays()) {
+  if (VRF_K2_MINB != 3 && (long long)g.rx * g.ry * g.rz >= k2_minb3_verts()) {
     launch_k2q<3, kPops, kSmem>(g, p, cam, rgbd, poses, batch, n, ray_cd, flags, stats,
                                 global_counts, grad, lambda_d, order, rec, K, rec_count, s);
     return;

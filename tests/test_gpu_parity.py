@@ -577,8 +577,8 @@ def test_fast_gradient_matches_deterministic_at_larger_batches(ctx, oracle, n_ra
 
 
 def test_k2q_three_ctas_per_sm_matches_deterministic(tmp_path):
-    """The 3-CTA/SM K2q build that batches of >= 4M rays run (config 4), forced
-    at 200K rays with VRF_K2_MINB3_RAYS=0: the fast gradient against the
+    """The 3-CTA/SM K2q build that grids of >= 64M vertices run (config 4), forced
+    at 200K rays with VRF_K2_MINB3_VERTS=0: the fast gradient against the
     deterministic FP64 one at the same 1e-3 tolerance, same touched set."""
     import subprocess
     import sys as _sys
@@ -597,7 +597,7 @@ det, sd = ctx.mapping_gradient(MappingConfig(deterministic=True), batch)
 np.savez(sys.argv[1], fast=fast, det=det, s=np.array([sf.samples, sd.samples]))
 '''
     f = tmp_path / "k2q3.npz"
-    env = dict(os.environ, VRF_K2_MINB3_RAYS="0")
+    env = dict(os.environ, VRF_K2_MINB3_VERTS="0")
     subprocess.run([_sys.executable, "-c", script, str(f)], check=True, env=env,
                    cwd=str(Path(__file__).resolve().parent.parent))
     d = np.load(f)
