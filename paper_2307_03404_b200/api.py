@@ -337,9 +337,14 @@ class Rng:
     def uniform(self) -> float:
         return (self.next_u64() >> 11) * 2.0 ** -53
 
-    def draw_batch(self, n_frames: int, width: int, height: int, n: int) -> np.ndarray:
-        """mapping.cpp:121-128 — n (frame, px, py) triples."""
-        out = np.empty((n, 3), dtype=np.int32)
+    def draw_batch(self, n_frames: int, width: int, height: int, n: int,
+                   out: np.ndarray = None) -> np.ndarray:
+        """mapping.cpp:121-128 — n (frame, px, py) triples; into `out` (a C-contiguous
+        int32 (n, 3) array, e.g. a pinned host buffer) when given."""
+        if out is None:
+            out = np.empty((n, 3), dtype=np.int32)
+        elif out.dtype != np.int32 or out.shape != (n, 3) or not out.flags.c_contiguous:
+            raise ValueError("draw_batch: out must be a C-contiguous int32 array of shape (n, 3)")
         capi.load().vrf_rng_draw_batch(self.state, n_frames, width, height, n,
                                        out.ctypes.data_as(C.c_void_p))
         return out
