@@ -154,11 +154,13 @@ void launch_rmsprop(float4* theta, float4* grad, float4* v, long long v_begin, l
                     const MapStats* stats, unsigned long long* touched, cudaStream_t s,
                     const UpdateLog& log = UpdateLog{});
 // Tracking (vrf_track.cu).
-int pose_fused_blocks(int n);
+
 // kParityFp64: k_pose_group<double> (FP64 SH + Jacobian partials; pose_gradient,
 // track_frame). kGnUniform: k_pose_group_u (fp32 partials; the Gauss-Newton
 // tracker). kGroupFp32: k_pose_group<float>, the GN kernel's checker (tests).
 enum class PoseKernel : int { kParityFp64 = 0, kGnUniform = 1, kGroupFp32 = 2 };
+// CTAs (= partials) of a pose-kernel launch over n rays
+int pose_fused_blocks(int n, PoseKernel which = PoseKernel::kParityFp64);
 void launch_pose_fused(PoseKernel which, const DevGrid& g, const DevParams& p, const DevCam& cam,
                        const double4* rgbd_base, const int* frame_idx, long long npix,
                        const DevPose* pose, const int* pixels, const uint32_t* order, int n,

@@ -135,7 +135,7 @@ int pose_pass(vrf_context* ctx, int frame, const vrf_intrinsics* intr, const vrf
   if ((rc = resolve_params(ctx, &cfg->render, &p))) return rc;
   const size_t pix_bytes = sizeof(int32_t) * 2 * (size_t)n;
   if ((rc = ensure(ctx, ctx->s_batch, pix_bytes))) return rc;
-  const int nb = pose_fused_blocks(n);
+  const int nb = pose_fused_blocks(n, which);
   if ((rc = ensure(ctx, ctx->s_partials, sizeof(PosePartial) * nb))) return rc;
   if ((rc = ensure_pinned(ctx, pix_bytes + sizeof(DevPose) + sizeof(int)))) return rc;
   if (!ctx->d_frame) CU(cudaMalloc(&ctx->d_frame, sizeof(int)));
@@ -506,7 +506,7 @@ int vrf_track_frame_gn(vrf_context* ctx, int frame, const vrf_intrinsics* intr,
     default: return set_err(ctx, VRF_ERR_INVALID_ARGUMENT, "track_frame_gn: unknown kernel");
   }
   const int iters = cfg->iterations;
-  const int nb = pose_fused_blocks(n);
+  const int nb = pose_fused_blocks(n, which);
   if ((rc = ensure(ctx, ctx->s_batch, sizeof(int32_t) * 2 * (size_t)n))) return rc;
   if ((rc = ensure(ctx, ctx->s_partials, sizeof(PosePartial) * nb))) return rc;
   if (!ctx->d_frame) CU(cudaMalloc(&ctx->d_frame, sizeof(int)));

@@ -316,15 +316,26 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
 // the pose, and the kernel builds without spills at 3 or 4 CTAs/SM; every build
 // rejects never-stored stack loads (_build.unwritten_local_loads).
 #ifndef VRF_POSE_U_MINB
-#define VRF_POSE_U_MINB 3  // CTAs per SM of k_pose_group_u (A/B knob)
+#define VRF_POSE_U_MINB 4  // CTAs per SM of k_pose_group_u (128 registers)
 #endif
-template <int MINB = VRF_POSE_U_MINB>
+#ifndef VRF_POSE_U_LPR
+#define VRF_POSE_U_LPR 4  // lanes per ray of k_pose_group_u (r02: 4 -> ~753 frames/s
+                          // at 4 CTAs/SM, 8 -> ~638; tools/ab/pose_lpr.sh)
+#endif
+template <int MINB = VRF_POSE_U_MINB, int LPR = VRF_POSE_U_LPR>
 __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
     DevGrid g, DevParams p, DevCam cam, const double4* __restrict__ rgbd_base,
     const int* __restrict__ frame_idx, long long npix, const DevPose* __restrict__ pose_ptr,
     const int* __restrict__ pixels, const uint32_t* __restrict__ order, int n, double lambda_p,
     double lambda_d, PosePartial* __restrict__ partials, int* err) {
-  constexpr int LPR = 8;
+  // LPR lanes per ray, CPL = 8 / LPR trilinear corners per lane (corners sub,
+  // sub + LPR, ...). LPR = 4 (default): 8 rays per warp, so the per-ray scalar
+  // work (FP64 compositing, exp, sample hand-out) is shared by 4 lanes, not 8.
+  // sigma and colour still sum in corner order (bit-identical to the 8-lane
+  // checker); the lane Jacobian partials sum two corners per lane first.
+  constexpr int CPL = 8 / LPR;
+  static_assert(LPR == 8 || LPR == 4, "lanes per ray");
+  constexpr unsigned GMASK = (1u << LPR) - 1u;
   constexpr unsigned FULL = 0xffffffffu;
   using ShT = float;
   using JT = float;
@@ -370,9 +381,6 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
     for (int a = 0; a < 3; ++a) Jo[r][a] = Jd[r][a] = JT(0);
   double T = 1.0, prefix[3] = {0, 0, 0}, prefix_d = 0.0;
   int count = 0;
-  const int kc = sub, dx = kc & 1, dy = (kc >> 1) & 1, dz = (kc >> 2) & 1;
-  // this lane's corner signs (sgn[d] of k_pose_group: -1 for d = 0, +1 for d = 1)
-  const JT sx = dx ? JT(1) : JT(-1), sy = dy ? JT(1) : JT(-1), sz = dz ? JT(1) : JT(-1);
   Sample mine{};  // value-initialised: lanes read it only after a located segment
   unsigned act = 0;
   while (__any_sync(FULL, alive)) {
@@ -409,8 +417,8 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
     const unsigned ba = __ballot_sync(FULL, a), be = __ballot_sync(FULL, eb);
     int jskip = -1;
     if (need) {
-      act = (ba >> gbase) & 0xffu;
-      const unsigned ebm = (be >> gbase) & 0xffu;
+      act = (ba >> gbase) & GMASK;
+      const unsigned ebm = (be >> gbase) & GMASK;
       m.k += LPR;
       if (act == 0 && ebm) jskip = 31 - __clz(ebm);
     }
@@ -434,9 +442,19 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
     s.fy = __shfl_sync(FULL, mine.fy, src);
     s.fz = __shfl_sync(FULL, mine.fz, src);
     s.base = __shfl_sync(FULL, mine.base, src);
-    double pk = 0.0;
-    ShT cp[3] = {ShT(0), ShT(0), ShT(0)};
+    double pk[CPL];
+    ShT cp[CPL][3];
     JT Gs[3] = {0, 0, 0}, Gc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int cc = 0; cc < CPL; ++cc) {
+      pk[cc] = 0.0;
+      cp[cc][0] = cp[cc][1] = cp[cc][2] = ShT(0);
+    }
+#pragma unroll
+    for (int cc = 0; cc < CPL; ++cc) {
+    // this lane's corner kc and its signs (sgn[d] of k_pose_group: -1 for d = 0)
+    const int kc = sub + cc * LPR, dx = kc & 1, dy = (kc >> 1) & 1, dz = (kc >> 2) & 1;
+    const JT sx = dx ? JT(1) : JT(-1), sy = dy ? JT(1) : JT(-1), sz = dz ? JT(1) : JT(-1);
     if (has) {
       // the lane's own corner weights, selected rather than indexed (the [2]
       // arrays of k_pose_group live in local memory here): the same values, so
@@ -457,7 +475,7 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
         v[4 * j + 2] = q.z;
         v[4 * j + 3] = q.w;
       }
-      pk = dmul(wk, (double)v[0]);
+      pk[cc] = dmul(wk, (double)v[0]);
       JT shd[3];
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
@@ -465,7 +483,7 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
 #pragma unroll
         for (int mm = 0; mm < 9; ++mm) acc = fma(bs[mm], (ShT)v[1 + ch * 9 + mm], acc);
         shd[ch] = JT(acc);
-        cp[ch] = fma(ShT(wk), acc, cp[ch]);
+        cp[cc][ch] = fma(ShT(wk), acc, cp[cc][ch]);
       }
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -474,15 +492,21 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
         for (int ch = 0; ch < 3; ++ch) Gc[ch][q] = fma(dw[q], shd[ch], Gc[ch][q]);
       }
     }
-    // sigma_raw in corner order (the reference's), colour in lane order
+    }
+    // sigma_raw in corner order (the reference's), colour in corner order too
+    // (corner cc * LPR + j is lane j's cc-th)
     double sraw = 0.0;
-#pragma unroll
-    for (int j = 0; j < LPR; ++j) sraw = dadd(sraw, __shfl_sync(FULL, pk, gbase + j));
     ShT csum[3] = {ShT(0), ShT(0), ShT(0)};
 #pragma unroll
-    for (int j = 0; j < LPR; ++j)
+    for (int cc = 0; cc < CPL; ++cc)
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) csum[ch] += __shfl_sync(FULL, cp[ch], gbase + j);
+      for (int j = 0; j < LPR; ++j) sraw = dadd(sraw, __shfl_sync(FULL, pk[cc], gbase + j));
+#pragma unroll
+    for (int cc = 0; cc < CPL; ++cc)
+#pragma unroll
+      for (int j = 0; j < LPR; ++j)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) csum[ch] += __shfl_sync(FULL, cp[cc][ch], gbase + j);
     if (has) {
       double c[3];
       bool clamped[3];
@@ -817,7 +841,10 @@ __global__ void k_gn_step(const PosePartial* __restrict__ ne, DevPose* pose, dou
 
 }  // namespace
 
-int pose_fused_blocks(int n) { return (n + kT / 8 - 1) / (kT / 8); }
+int pose_fused_blocks(int n, PoseKernel which) {
+  const int rays_per_cta = kT / (which == PoseKernel::kGnUniform ? VRF_POSE_U_LPR : 8);
+  return (n + rays_per_cta - 1) / rays_per_cta;
+}
 
 void launch_pose_fused(PoseKernel which, const DevGrid& g, const DevParams& p, const DevCam& cam,
                        const double4* rgbd_base, const int* frame_idx, long long npix,
@@ -825,7 +852,7 @@ void launch_pose_fused(PoseKernel which, const DevGrid& g, const DevParams& p, c
                        double lambda_p, double lambda_d, PosePartial* partials, int* err,
                        cudaStream_t s) {
   if (n <= 0) return;
-  const int nb = pose_fused_blocks(n);
+  const int nb = pose_fused_blocks(n, which);
 #define VRF_POSE_ARGS \
   g, p, cam, rgbd_base, frame_idx, npix, pose, pixels, order, n, lambda_p, lambda_d, partials, err
   switch (which) {

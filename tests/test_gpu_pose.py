@@ -107,7 +107,11 @@ def test_gn_kernel_gauss_newton_step_matches_oracle_step(ctx, oracle):
 
 
 @pytest.mark.parametrize("res,w,h,n", SCENES + [(33, 64, 48, 37)])
-def test_gn_kernel_bit_identical_to_checker(ctx, res, w, h, n):
+def test_gn_kernel_matches_checker(ctx, res, w, h, n):
+    """The production GN kernel (4 lanes per ray, two corners per lane) against
+    the independent 8-lane checker: the same samples and rays (sigma and colour
+    sum in corner order in both), the loss to FP64 block-sum order, and JᵀJ / Jᵀr
+    to the fp32 lane-partial order (two corners summed per lane first)."""
     grid, intr, frames = room_scene(res=res, width=w, height=h)
     ctx.load_grid(grid)
     ctx.load_frames(intr, frames)
@@ -119,15 +123,17 @@ def test_gn_kernel_bit_identical_to_checker(ctx, res, w, h, n):
         b = ctx.pose_normal_equations(f, intr, pose, px, TrackingConfig(),
                                       kernel=capi.POSE_KERNEL_GN_CHECK)
         assert a.samples == b.samples and a.rays_used == b.rays_used
-        assert a.loss == b.loss
-        assert np.array_equal(a.jtj, b.jtj) and np.array_equal(a.jtr, b.jtr)
+        assert abs(a.loss - b.loss) <= 1e-12 * abs(b.loss)
+        assert np.max(np.abs(a.jtj - b.jtj)) <= 1e-5 * np.max(np.abs(b.jtj))
+        assert np.max(np.abs(a.jtr - b.jtr)) <= 1e-5 * np.max(np.abs(b.jtr))
 
 
 @pytest.mark.parametrize("rays", [4096, 2048, 3000])
-def test_track_frame_gn_kernels_identical_per_iteration(ctx, rays):
+def test_track_frame_gn_kernels_agree_per_iteration(ctx, rays):
     """Whole GN frames (device draws, pose kernel, reduce, LM step; one CUDA
-    graph) through the production kernel and the checker: identical poses and
-    identical per-iteration (loss, m, samples). Non-power-of-4 ray counts draw
+    graph) through the production kernel and the checker: the same draws and
+    hits per iteration, losses and sample counts that agree to the fp32
+    Jacobian-order noise, and poses within 1e-6. Non-power-of-4 ray counts draw
     exactly rays_per_iteration pixels."""
     grid, intr, frames = room_scene(res=33, width=64, height=48)
     frame = frames[1]
@@ -141,8 +147,12 @@ def test_track_frame_gn_kernels_identical_per_iteration(ctx, rays):
         out[k] = (r, ctx.track_frame_gn_history())
     (ra, ha), (rb, hb) = out[capi.POSE_KERNEL_GN], out[capi.POSE_KERNEL_GN_CHECK]
     assert ha.shape == (6, 3)
-    assert np.array_equal(ha, hb)
-    assert np.array_equal(ra.pose.q, rb.pose.q) and np.array_equal(ra.pose.t, rb.pose.t)
+    assert np.array_equal(ha[:, 1], hb[:, 1])
+    assert ha[0, 2] == hb[0, 2] and ha[0, 0] == pytest.approx(hb[0, 0], rel=1e-12)
+    np.testing.assert_allclose(ha[:, 0], hb[:, 0], rtol=1e-4)
+    np.testing.assert_allclose(ha[:, 2], hb[:, 2], rtol=1e-3)
+    np.testing.assert_allclose(ra.pose.t, rb.pose.t, atol=1e-6)
+    np.testing.assert_allclose(ra.pose.q, rb.pose.q, atol=1e-6)
     # every pixel of this frame has valid depth and the room encloses the camera:
     # all rays_per_iteration draws hit, and each composites more than one sample
     assert np.all(ha[:, 1] == rays)
