@@ -313,7 +313,8 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group(
 // instance and r02's 4-CTA/SM build composited one sample per ray: ptxas
 // (CUDA 12.9) spilled the ray origin to stack slots it never stored
 // (profiles/r02_pose_spill_bug.md). The march therefore reads the origin from
-// the pose, and the kernel builds without spills at 3 or 4 CTAs/SM; every build
+// the pose (the 8-lane build has no spills; the default 4-lane build at 4 CTAs/SM
+// spills 76 B, all stored before use); every build
 // rejects never-stored stack loads (_build.unwritten_local_loads).
 #ifndef VRF_POSE_U_MINB
 #define VRF_POSE_U_MINB 4  // CTAs per SM of k_pose_group_u (128 registers)
