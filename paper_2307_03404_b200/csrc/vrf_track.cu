@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kT, MINB) k_pose_group_u(
   // sigma and colour still sum in corner order (bit-identical to the 8-lane
   // checker); the lane Jacobian partials sum two corners per lane first.
   constexpr int CPL = 8 / LPR;
-  static_assert(LPR == 8 || LPR == 4, "lanes per ray");
+  static_assert(LPR == 8 || LPR == 4 || LPR == 2, "lanes per ray");
   constexpr unsigned GMASK = (1u << LPR) - 1u;
   constexpr unsigned FULL = 0xffffffffu;
   using ShT = float;
